@@ -1,0 +1,535 @@
+#!/usr/bin/env python
+"""Benchmark of the w-product hot path on B200 (contract: see DESIGN.md section 7).
+
+Primary line (BASELINE.json configs[1]): forward + inverse lifting transform of a
+512x512x256 float64 cube at L = 1, 2, 4, 8; one step = the four round trips;
+metric = algorithmic HBM bytes moved per second (16 B per element per direction).
+`workloads` adds the other configs measured in the same run (N=1):
+w-svd (config 3) and sp-w-svd (config 4) tensor-elems/s, the config-5 deblur
+recovery and the config-1 w-product.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--workloads transform,wsvd,spwsvd,deblur,wproduct | none]
+
+N > 1: one process per GPU under torchrun; the transform is weak-scaled (one
+cube per rank, no collective), sp-w-svd is sharded (rows -> all-to-all ->
+slices) across the ranks.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CFG2 = (512, 512, 256)
+CFG2_LEVELS = (1, 2, 4, 8)
+METRIC = "lifting transform HBM GB/s (fwd+inv, L=1,2,4,8); w-svd rank-k reconstruct tensor-elems/s in workloads"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workloads", default="default")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------ env ----
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def load_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        d = json.load(open(path))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, burst copy)"
+    except Exception:  # noqa: BLE001
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def fp64_peak():
+    """DMMA FP64 peak measured on this pool (tools/fp64_peak.cu -> profiles/fp64_peak_r01.jsonl)."""
+    path = os.path.join(ROOT, "profiles", "fp64_peak_r01.jsonl")
+    try:
+        best = 0.0
+        for line in open(path):
+            d = json.loads(line)
+            if d.get("kind") == "dmma_m8n8k4":
+                best = max(best, float(d["tflops"]))
+        if best > 0:
+            return best, "measured (tools/fp64_peak.cu DMMA m8n8k4, profiles/fp64_peak_r01.jsonl)"
+    except Exception:  # noqa: BLE001
+        pass
+    return 37.0, "fallback (B200 FP64 tensor, measured 36.99 TF in round 1)"
+
+
+def traffic_of(kernel):
+    path = os.path.join(ROOT, "profiles", "traffic_r01.json")
+    try:
+        return json.load(open(path)).get(kernel)
+    except Exception:  # noqa: BLE001
+        return None
+
+
+class ClockSampler:
+    """Samples SM clocks and throttle reasons via NVML during the timed region."""
+
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+        0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+        0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting",
+    }
+
+    def __init__(self, index):
+        self.index = index
+        self.samples = []
+        self.reasons = 0
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._t = None
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:  # noqa: BLE001
+            self.nv = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                self.reasons |= int(r) & ~0x1
+            except Exception:  # noqa: BLE001
+                pass
+            time.sleep(0.05)
+
+    def __enter__(self):
+        if self.nv is not None:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self._t is not None:
+            self._t.join()
+
+    def summary(self):
+        if self.nv is None or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unavailable"]}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "samples": len(self.samples),
+                "reasons": [n for b, n in self.REASONS.items() if self.reasons & b]}
+
+
+# --------------------------------------------------------------- timing ----
+
+class KernelTimer:
+    """CUDA events around each launch of the dominant kernel, on its stream."""
+
+    def __init__(self):
+        self.pairs = []
+
+    def wrap(self, fn):
+        import torch
+
+        s = torch.cuda.Event(enable_timing=True)
+        e = torch.cuda.Event(enable_timing=True)
+        s.record()
+        out = fn()
+        e.record()
+        self.pairs.append((s, e))
+        return out
+
+    def mean_ms(self):
+        if not self.pairs:
+            return None
+        return sum(s.elapsed_time(e) for s, e in self.pairs) / len(self.pairs)
+
+
+def timed_region(step_fn, steps, warmup, dist=None, sampler=None):
+    """W warm-up steps, then exactly K steps bracketed by barrier + synchronize;
+    returns the max over ranks of the device time (ms) of the K steps."""
+    import torch
+
+    for _ in range(warmup):
+        step_fn(False)
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    ctx = sampler if sampler is not None else _Null()
+    with ctx:
+        t0.record()
+        for _ in range(steps):
+            step_fn(True)
+        t1.record()
+        torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    ms = t0.elapsed_time(t1)
+    if dist is not None:
+        v = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(v, op=dist.ReduceOp.MAX)
+        ms = float(v.item())
+    return ms
+
+
+class _Null:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        return False
+
+
+# ----------------------------------------------------------- workloads ----
+
+def transform_workload(args, dist, rank, ws):
+    import torch
+
+    from paper_2601_08228_b200 import engine as E
+    import paper_2601_08228_b200 as W
+
+    n1, n2, p = CFG2
+    N = n1 * n2 * p
+    x_host = np.random.default_rng(rank).standard_normal(CFG2)
+    x = torch.from_numpy(x_host).cuda()
+    bufs = {L: torch.empty((p, n1, n2), dtype=torch.float64, device="cuda") for L in CFG2_LEVELS}
+    y = torch.empty_like(x)
+    kt_f, kt_i = KernelTimer(), KernelTimer()
+
+    def step(record):
+        for L in CFG2_LEVELS:
+            if record:
+                kt_f.wrap(lambda: E.lift_forward(x, L, out=bufs[L]))
+                kt_i.wrap(lambda: E.lift_inverse(bufs[L], n1, n2, p, L, out=y))
+            else:
+                E.lift_forward(x, L, out=bufs[L])
+                E.lift_inverse(bufs[L], n1, n2, p, L, out=y)
+
+    sampler = ClockSampler(torch.cuda.current_device())
+    ms = timed_region(step, args.steps, args.warmup, dist, sampler)
+    # parity of the last step (bit-exact round trip is checked by the tests)
+    rt = float((y - x).norm() / x.norm())
+    bytes_step = len(CFG2_LEVELS) * 2 * 16 * N
+    value = ws * bytes_step * args.steps / (ms * 1e-3) / 1e9
+    peak, peak_src = load_peaks()
+    f_ms, i_ms = kt_f.mean_ms(), kt_i.mean_ms()
+    per_launch = 16 * N
+    ach_f = per_launch / (f_ms * 1e-3) / 1e9
+    ach_i = per_launch / (i_ms * 1e-3) / 1e9
+    dom = "lift_fwd_kernel" if f_ms >= i_ms else "lift_inv_kernel"
+    ach = ach_f if dom == "lift_fwd_kernel" else ach_i
+    roofline = {"bound": "hbm", "kernel": dom, "achieved": round(ach, 1), "peak": peak,
+                "unit": "GB/s", "frac": round(ach / peak, 4), "peak_source": peak_src,
+                "traffic": traffic_of(dom), "algorithmic_bytes_per_launch": per_launch,
+                "per_kernel": {"lift_fwd_kernel": {"ms": round(f_ms, 4), "GBps": round(ach_f, 1),
+                                                   "frac": round(ach_f / peak, 4)},
+                               "lift_inv_kernel": {"ms": round(i_ms, 4), "GBps": round(ach_i, 1),
+                                                   "frac": round(ach_i / peak, 4)}}}
+
+    # e2e: the public reference-shaped API on host (numpy) buffers, copies inside
+    e2e_steps = max(1, min(args.steps, 3))
+    torch.cuda.synchronize()
+    for L in CFG2_LEVELS[:1]:
+        W.inverse_w(W.forward_w(x_host, L))  # warm
+    if dist is not None:
+        dist.barrier()
+    t = time.perf_counter()
+    for _ in range(e2e_steps):
+        for L in CFG2_LEVELS:
+            out = W.inverse_w(W.forward_w(x_host, L))
+    torch.cuda.synchronize()
+    e2e_s = time.perf_counter() - t
+    if dist is not None:
+        v = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
+        dist.all_reduce(v, op=dist.ReduceOp.MAX)
+        e2e_s = float(v.item())
+    assert np.array_equal(out, x_host) or float(np.abs(out - x_host).max()) < 1e-12
+    e2e = {"value": round(ws * bytes_step * e2e_steps / e2e_s / 1e9, 3), "unit": "GB/s",
+           "h2d_bytes_per_step": len(CFG2_LEVELS) * 2 * 8 * N,
+           "d2h_bytes_per_step": len(CFG2_LEVELS) * 2 * 8 * N,
+           "api": "inverse_w(forward_w(numpy, L)) per L", "steps": e2e_steps}
+    return {"ms": ms, "value": value, "roofline": roofline, "e2e": e2e, "round_trip_relerr": rt,
+            "clocks": sampler.summary(), "launches": args.steps * len(CFG2_LEVELS) * 2,
+            "N": N, "x_host": x_host}
+
+
+def svd_flops(n1, n2):
+    m, n = max(n1, n2), min(n1, n2)
+    return 14 * m * n * n + 8 * n ** 3
+
+
+def wsvd_workload(args, steps=3, warmup=1):
+    import torch
+
+    from paper_2601_08228_b200 import engine as E
+    from paper_2601_08228_b200 import synth
+    from paper_2601_08228_b200.decomposition import w_svd_device
+
+    n1, n2, p, r, L = 256, 256, 192, 20, 3
+    x = torch.from_numpy(synth.hyperspectral_cube(n1, n2, p, seed=0)).cuda()
+    flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device="cuda")
+    sweeps = []
+
+    def step(record):
+        flush.zero_()  # 256 MB > L2: every step starts cold
+        w_svd_device(x, r, L)
+        sweeps.append(E.last_sweeps())
+
+    ms = timed_region(step, steps, warmup)
+    N = n1 * n2 * p
+    flops = p * svd_flops(n1, n2)
+    peak, src = fp64_peak()
+    ach = flops / (ms / steps * 1e-3) / 1e12
+    return {"config": "w_svd 256x256x192 rank 20 L=3 (BASELINE configs[2])", "metric": "tensor-elems/s",
+            "value": N * steps / (ms * 1e-3), "ms_per_call": ms / steps, "jacobi_sweeps": sweeps[-1],
+            "roofline": {"bound": "tensor", "achieved": round(ach, 2), "peak": peak,
+                         "unit": "TFLOP/s", "frac": round(ach / peak, 4), "peak_source": src,
+                         "flops_model": "192 x (14 m n^2 + 8 n^3) Golub-Kahan thin-SVD count (SURVEY 8d)"},
+            "l2": "256 MB flush before each call"}
+
+
+def spwsvd_workload(args, steps=3, warmup=1):
+    import torch
+
+    from paper_2601_08228_b200 import engine as E
+    from paper_2601_08228_b200 import synth
+    from paper_2601_08228_b200.decomposition import sp_w_svd_device
+
+    n1, n2, p, r, L = 1024, 1024, 256, 30, 4
+    x = torch.from_numpy(synth.hyperspectral_cube(n1, n2, p, seed=0)).cuda()
+    out = torch.empty_like(x)
+    sweeps = []
+
+    def step(record):
+        sp_w_svd_device(x, r, L, out=out)
+        sweeps.append(E.last_sweeps())
+
+    ms = timed_region(step, steps, warmup)
+    N = n1 * n2 * p
+    flops = 2 * (p >> L) * svd_flops(n1, n2)
+    peak, src = fp64_peak()
+    ach = flops / (ms / steps * 1e-3) / 1e12
+    return {"config": "sp_w_svd 1024x1024x256 rank 30 L=4 (BASELINE configs[3])", "metric": "tensor-elems/s",
+            "value": N * steps / (ms * 1e-3), "ms_per_call": ms / steps, "jacobi_sweeps": sweeps[-1],
+            "roofline": {"bound": "tensor", "achieved": round(ach, 2), "peak": peak, "unit": "TFLOP/s",
+                         "frac": round(ach / peak, 4), "peak_source": src,
+                         "flops_model": "32 x 22 n^3 thin-SVD count (SURVEY 8d)"},
+            "l2": "2 GiB input > L2"}
+
+
+def deblur_workload(args, steps=2, warmup=1):
+    import torch
+
+    import paper_2601_08228_b200 as W
+    from paper_2601_08228_b200 import imaging, synth
+    from paper_2601_08228_b200.algebra import w_product_device
+    from paper_2601_08228_b200.decomposition import pinv_w_device
+
+    x, av, ah, eta = synth.deblur_problem()
+    xd, avd, ahd = (torch.from_numpy(t).cuda() for t in (x, av, ah))
+    aht = W.transpose(ahd)
+    b = w_product_device(w_product_device(avd, xd, 3), aht, 3) + torch.from_numpy(eta).cuda()
+    res = {}
+
+    def step(record):
+        left = pinv_w_device(avd, 3, 1e-3)
+        right = pinv_w_device(aht, 3, 1e-3)
+        res["x"] = w_product_device(w_product_device(left, b, 3), right, 3)
+
+    ms = timed_region(step, steps, warmup)
+    # GEMM share: one w-product alone
+    g = {}
+
+    def gstep(record):
+        g["c"] = w_product_device(xd, avd, 3)
+
+    gms = timed_region(gstep, 3, 1)
+    peak, src = fp64_peak()
+    gflops = 2 * 512 ** 3 * 128
+    return {"config": "w-pinv deblur 512x512x128, 9x9 Gaussian PSF sigma=2, L=3, tol 1e-3 (BASELINE configs[4])",
+            "metric": "s per recovery", "value": ms / steps / 1e3,
+            "psnr_db": imaging.psnr(xd, res["x"]), "ssim": imaging.ssim(xd, res["x"]),
+            "w_product_ms": gms / 3,
+            "w_product_roofline": {"bound": "tensor", "achieved": round(gflops / (gms / 3 * 1e-3) / 1e12, 2),
+                                   "peak": peak, "unit": "TFLOP/s",
+                                   "frac": round(gflops / (gms / 3 * 1e-3) / 1e12 / peak, 4),
+                                   "peak_source": src, "note": "whole w-product incl. transforms"}}
+
+
+def wproduct_workload(args, steps=20, warmup=3):
+    import torch
+
+    from paper_2601_08228_b200 import synth
+    from paper_2601_08228_b200.algebra import w_product_device
+
+    a, b = synth.uniform_pair(0)
+    ad, bd = torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()
+
+    def step(record):
+        w_product_device(ad, bd, 1)
+
+    ms = timed_region(step, steps, warmup)
+    return {"config": "w_product 64x48x32 * 48x40x32 L=1 (BASELINE configs[0])", "metric": "us per call",
+            "value": ms / steps * 1e3}
+
+
+# ----------------------------------------------------------- CPU legs ----
+
+def cpu_transform_sample(x_host, reps=2, rows=128):
+    """Oracle (numpy port of lifting.py) on a bounded slab of the config-2 cube."""
+    from oracle import wten_oracle as O
+
+    slab = np.ascontiguousarray(x_host[:rows])
+    n = slab.size
+    t = time.perf_counter()
+    for _ in range(reps):
+        for L in CFG2_LEVELS:
+            s, d = O.lift_forward(slab, L)
+            O.lift_inverse(s, d)
+    dt = time.perf_counter() - t
+    gbs = reps * len(CFG2_LEVELS) * 32 * n / dt / 1e9
+    return {"value": round(gbs, 4), "unit": "GB/s", "cores": 1, "kind": "port",
+            "sample": f"oracle lift_forward+lift_inverse, L=1,2,4,8, slab {rows}x512x256 of the config-2 cube, "
+                      f"{reps} reps ({dt:.1f} s; numpy ufuncs are single-threaded)"}
+
+
+def run_reference(args):
+    ws, rank, local = dist_env()
+    if rank != 0:
+        return
+    from oracle import wten_oracle as O  # noqa: F401
+
+    x = np.random.default_rng(0).standard_normal(CFG2)
+    rows = 64
+    slab = np.ascontiguousarray(x[:rows])
+    n = slab.size
+    for _ in range(max(0, min(args.warmup, 1))):
+        for L in CFG2_LEVELS:
+            s, d = O.lift_forward(slab, L)
+            O.lift_inverse(s, d)
+    t = time.perf_counter()
+    for _ in range(args.steps):
+        for L in CFG2_LEVELS:
+            s, d = O.lift_forward(slab, L)
+            O.lift_inverse(s, d)
+    dt = time.perf_counter() - t
+    gbs = args.steps * len(CFG2_LEVELS) * 32 * n / dt / 1e9
+    cores = 1
+    line = {"impl": "reference", "metric": METRIC, "value": round(gbs, 4), "unit": "GB/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded standard normal, BASELINE configs[1])",
+            "config": {"workload": "forward+inverse lifting transform 512x512x256 f64, L=1,2,4,8",
+                       "sample": f"{rows}x512x256 slab per step"},
+            "cpu_baseline": {"value": round(gbs, 4), "unit": "GB/s", "cores": cores, "kind": "port",
+                             "sample": f"oracle/wten_oracle.py (numpy port of lifting.py:63-120) on a "
+                                       f"{rows}x512x256 slab, L=1,2,4,8, {args.steps} steps"},
+            "e2e": {"value": round(gbs, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------- main ----
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    ws, rank, local = dist_env()
+    import torch
+
+    torch.cuda.set_device(local)
+    dist = None
+    if ws > 1:
+        import torch.distributed as tdist
+
+        tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        dist = tdist
+    from paper_2601_08228_b200 import _native
+
+    _native.require_gpu()
+
+    if args.workloads == "default":
+        wl = ["wsvd", "spwsvd", "deblur", "wproduct"] if ws == 1 else ["spwsvd_sharded"]
+    elif args.workloads == "none":
+        wl = []
+    else:
+        wl = [w for w in args.workloads.split(",") if w and w != "transform"]
+
+    tr = transform_workload(args, dist, rank, ws)
+    workloads = {}
+    for name in wl:
+        try:
+            if name == "wsvd":
+                workloads[name] = wsvd_workload(args)
+            elif name == "spwsvd":
+                workloads[name] = spwsvd_workload(args)
+            elif name == "deblur":
+                workloads[name] = deblur_workload(args)
+            elif name == "wproduct":
+                workloads[name] = wproduct_workload(args)
+            elif name == "spwsvd_sharded":
+                from paper_2601_08228_b200 import sharded
+
+                workloads[name] = sharded.bench_sp_w_svd(dist, timed_region, steps=3, warmup=1)
+        except Exception as e:  # noqa: BLE001
+            workloads[name] = {"error": f"{type(e).__name__}: {e}"}
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        cpu = cpu_transform_sample(tr["x_host"])
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(tr["value"], 2), "unit": "GB/s", "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(tr["ms"] / args.steps, 4),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic: seeded i.i.d. standard normal cube per rank (BASELINE configs[1]); "
+                    "hyperspectral generator for configs 3-5 (paper_2601_08228_b200/synth.py)",
+            "config": {"workload": "forward+inverse lifting transform 512x512x256 f64, L=1,2,4,8 per step",
+                       "per_rank_cube": list(CFG2), "levels": list(CFG2_LEVELS),
+                       "parallelism": f"replicas{ws}" if ws > 1 else "single",
+                       "l2": "inputs larger than L2 (2 GiB cube, 2 GiB pyramid)",
+                       "bytes_per_step_per_rank": len(CFG2_LEVELS) * 2 * 16 * tr["N"]},
+            "roofline": tr["roofline"],
+            "cpu_baseline": cpu,
+            "e2e": tr["e2e"],
+            "gpu_launches": tr["launches"],
+            "clocks": tr["clocks"],
+            "round_trip_relerr": tr["round_trip_relerr"],
+            "workloads": workloads,
+        }
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

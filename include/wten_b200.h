@@ -1,0 +1,154 @@
+/*
+ * wten_b200 -- C ABI of the B200 (sm_100a) hot path of the w-product framework.
+ *
+ * This is the drop-in boundary for the reference package `wten`
+ * (/root/reference/pkg/src/wten).  The reference is pure Python/numpy, so
+ * there is no reference C header; each entry point below names the reference
+ * function (file:line) whose arithmetic it replaces.  The Python mirror of the
+ * reference API (paper_2601_08228_b200/{lifting,algebra,decomposition}.py)
+ * binds these symbols with ctypes; INTEGRATION.md shows the equivalent stub a
+ * `wten` maintainer would add.
+ *
+ * Conventions
+ *   - All tensor pointers are DEVICE pointers (cudaMalloc / torch CUDA tensors),
+ *     caller-owned, float64.  `stream` is a cudaStream_t (NULL = legacy default).
+ *   - Every call is stream-ordered and returns an int status (WT_OK = 0).  On a
+ *     non-zero status `wt_last_error()` returns a thread-local message.
+ *   - Validation that the reference performs in Python (LevelError, ShapeError,
+ *     RankError) stays in the Python layer, which calls these only with valid
+ *     arguments; the ABI re-checks and returns WT_ERR_INVALID instead of raising.
+ *
+ * Tensor layouts
+ *   - Spatial tensor: (n1, n2, p) C-contiguous, tube (mode-3) axis fastest,
+ *     exactly the reference layout (tensor.py:1-5).  "tube" q = i*n2 + j.
+ *   - Pyramid, slice-major (WT_LAYOUT_SLICE_MAJOR): p matrices of n1 x n2 rows-
+ *     major, blocks in order [d1 | d2 | ... | dL | sL]; detail level j occupies
+ *     slices [p - p/2^(j-1), p - p/2^j), the smooth stack the last p/2^L slices.
+ *   - Pyramid, tube-major (WT_LAYOUT_TUBE_MAJOR): same block order, each block an
+ *     (n1, n2, k) C-contiguous array -- the reference's own per-level arrays
+ *     (lifting.py:24-34), used by the numpy drop-in path.
+ *   - `slice_base`: the output/input buffer starts at packed slice index
+ *     slice_base (compact buffers for the sparse variants, e.g. only [dL|sL]).
+ */
+#ifndef WTEN_B200_H
+#define WTEN_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define WT_OK 0
+#define WT_ERR_INVALID 1     /* bad argument (shape / level / layout)            */
+#define WT_ERR_CUDA 2        /* CUDA runtime error (launch / memory)             */
+#define WT_ERR_UNSUPPORTED 3 /* valid but not implemented configuration          */
+
+#define WT_LAYOUT_SLICE_MAJOR 0
+#define WT_LAYOUT_TUBE_MAJOR 1
+
+/* level_mask bit 0 = smooth sL, bit j (1..L) = detail level j. */
+#define WT_MASK_ALL (~(uint64_t)0)
+
+/* ABI version (major*100 + minor). */
+int wt_version(void);
+/* Thread-local description of the last failing call on this thread. */
+const char* wt_last_error(void);
+
+/*
+ * K1 -- forward multilevel lazy lifting along mode 3, all L levels in one pass.
+ * Replaces forward_w (lifting.py:77-94) with _lift_once (lifting.py:63-66) and
+ * the tube->slice staging copies of slicewise_matmul (algebra.py:26-27) and
+ * _stack_svd (decomposition.py:66).  Bit-exact with the reference.
+ *   x      : (n1, n2, p) spatial tensor, tube-fastest, contiguous
+ *   levels : 0 <= levels, 2^levels | p   (levels = 0 is a pure tube->slice transpose)
+ *   out    : pyramid in `layout`, starting at packed slice `slice_base`
+ *   level_mask : which blocks to write (others are computed but not stored)
+ */
+int wt_lift_fwd_f64(const double* x, int64_t n1, int64_t n2, int64_t p, int levels,
+                    double* out, int layout, int64_t slice_base, uint64_t level_mask,
+                    void* stream);
+
+/*
+ * K2 -- inverse multilevel lifting (lifting.py:114-120, _unlift_once :69-74).
+ * Blocks not in level_mask are treated as exactly zero and never read
+ * (sp_w_svd / sp_pinv_w zero the finer details, decomposition.py:152,201).
+ */
+int wt_lift_inv_f64(const double* pyr, int64_t n1, int64_t n2, int64_t p, int levels,
+                    int layout, int64_t slice_base, uint64_t level_mask, double* y,
+                    void* stream);
+
+/*
+ * K3 -- strided-batched FP64 GEMM on the DMMA tensor pipe (mma.sync f64).
+ * Replaces the per-slice cblas_dgemm of slicewise_matmul (algebra.py:18-28),
+ * _truncated_blocks (decomposition.py:70-72) and _pinv_stack (:162).
+ * Row-major: C[b] = alpha * op(A[b]) * op(B[b]) + beta * C[b], b < batch,
+ * op(A) is M x K (transA: A stored K x M), op(B) is K x N (transB: B stored N x K).
+ */
+int wt_gemm_f64(int transA, int transB, int64_t M, int64_t N, int64_t K, double alpha,
+                const double* A, int64_t lda, int64_t strideA, const double* B, int64_t ldb,
+                int64_t strideB, double beta, double* C, int64_t ldc, int64_t strideC,
+                int64_t batch, void* stream);
+
+/*
+ * K4 -- batched one-sided block-Jacobi SVD (Gram/rotation tiles on DMMA).
+ * Replaces _stack_svd (decomposition.py:64-67, LAPACK dgesdd).
+ * For each b < batch, A[b] is an n1 x n2 row-major matrix (lda, strideA).
+ * Outputs, q = min(n1, n2):
+ *   sigma[b*q + i]      singular values, descending
+ *   vec[b*nvec*len + i*len + t], i < nvec <= q:
+ *       the i-th singular vector on the LONG side (len = max(n1, n2)):
+ *       right vector v_i if n1 <= n2, else left vector u_i; unit norm
+ *       (zero vector when sigma_i == 0).
+ *   info[b] : 0 ok, 1 non-finite input/result, 2 no convergence in max_sweeps.
+ * The short-side vectors follow from one GEMM with A (done by the caller).
+ * `workspace` must hold wt_svd_workspace_bytes(n1, n2, batch) bytes.
+ * tol <= 0 selects the default; max_sweeps <= 0 selects 40.
+ * The call synchronizes `stream` once per sweep to test convergence.
+ */
+size_t wt_svd_workspace_bytes(int64_t n1, int64_t n2, int64_t batch);
+int wt_svd_jacobi_f64(const double* A, int64_t lda, int64_t strideA, int64_t n1, int64_t n2,
+                      int64_t batch, double* sigma, double* vec, int64_t nvec, int* info,
+                      double tol, int max_sweeps, void* workspace, size_t workspace_bytes,
+                      void* stream);
+
+/*
+ * K5/K6/K7 helpers: scale the columns of a batch of row-major matrices,
+ * M[b][i][j] *= f(s[b*q + j]) for j < ncols, where f is
+ *   WT_SCALE_MUL (s), WT_SCALE_DIV (1/s, 0 if s == 0),
+ *   WT_SCALE_PINV2 (1/s^2 if s > tol*s[b*q+0] and s > 0, else 0) -- the
+ *   _pinv_stack cutoff rule (decomposition.py:160-161) applied twice.
+ */
+#define WT_SCALE_MUL 0
+#define WT_SCALE_DIV 1
+#define WT_SCALE_PINV2 2
+int wt_scale_cols_f64(double* M, int64_t rows, int64_t ncols, int64_t ld, int64_t strideM,
+                      const double* s, int64_t q, int64_t batch, int mode, double tol,
+                      void* stream);
+
+/* Strided batched 2-D copy / transpose: dst[b][i][j] = src[b][j][i] (trans) or
+ * src[b][i][j]; rows x cols of dst.  Used for the slicewise transpose
+ * (tensor.py:50-52) and the sharded row<->slice exchange permutations. */
+int wt_copy2d_f64(const double* src, int64_t lds, int64_t strideS, double* dst, int64_t ldd,
+                  int64_t strideD, int64_t rows, int64_t cols, int64_t batch, int trans,
+                  void* stream);
+
+/* Deterministic per-band reductions used by the quality metrics (PSNR/SSIM,
+ * PAPER.md:876-887) and parity norms: x, y are spatial tensors viewed as
+ * (n tubes, nslices bands) tube-major; out[k] = sum over tubes of f(x, y) with
+ * f = x*x (mode 0), (x-y)^2 (mode 1), x (mode 2), x*y (mode 3).  Fixed
+ * reduction tree, bit-reproducible.  `out` must hold
+ * wt_slice_reduce_scratch(n, nslices) bytes (the tail is scratch). */
+size_t wt_slice_reduce_scratch(int64_t n, int64_t nslices);
+int wt_slice_reduce_f64(const double* x, const double* y, int64_t n, int64_t nslices,
+                        int mode, double* out, void* stream);
+
+/* Sweeps used by the last wt_svd_jacobi_f64 call on the calling thread. */
+int wt_svd_last_sweeps(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* WTEN_B200_H */

@@ -1,0 +1,240 @@
+// K3: strided-batched FP64 GEMM on the B200 DMMA pipe.
+//
+// Replaces the per-slice cblas_dgemm calls of the reference:
+//   slicewise_matmul   algebra.py:18-28       (face product, all levels at once)
+//   _truncated_blocks  decomposition.py:70-72 (rank-r reconstruction)
+//   _pinv_stack        decomposition.py:162   (V diag(s+) U^T assembly)
+//
+// sm_100a has no FP64 tcgen05 kind (ptxas rejects .kind::f64), so the FP64
+// tensor path is the warp-level mma.sync m8n8k4 f64 (SASS DMMA.8x8x4) fed from
+// registers.  Design: CTA tile BM x BN x 16, 3-stage cp.async (LDGSTS) ring in
+// shared memory, row pitches padded to 4 (mod 16) doubles so every fragment
+// LDS.64 is bank-conflict-free for both operand orientations, warp tile
+// (BM/WM) x (BN/WN) held as DMMA accumulators.
+//
+// Row-major semantics: C[b] = alpha * op(A[b]) * op(B[b]) + beta * C[b].
+#include <algorithm>
+
+#include "wt_common.cuh"
+
+namespace wt {
+namespace {
+
+constexpr int BK = 16;
+constexpr int STAGES = 3;
+
+struct GemmArgs {
+  int64_t M, N, K;
+  double alpha, beta;
+  const double* A;
+  int64_t lda, sA;
+  const double* B;
+  int64_t ldb, sB;
+  double* C;
+  int64_t ldc, sC;
+  int64_t batch;
+};
+
+template <int BM, int BN, bool TA, bool TB>
+struct SmemLayout {
+  // A tile: !TA -> [BM][BK+4] (k fastest), TA -> [BK][BM+4] (m fastest)
+  static constexpr int A_LD = TA ? (BM + 4) : (BK + 4);
+  static constexpr int A_ELEMS = TA ? BK * (BM + 4) : BM * (BK + 4);
+  // B tile: !TB -> [BK][BN+4] (n fastest), TB -> [BN][BK+4] (k fastest)
+  static constexpr int B_LD = TB ? (BK + 4) : (BN + 4);
+  static constexpr int B_ELEMS = TB ? BN * (BK + 4) : BK * (BN + 4);
+  static constexpr int STAGE_ELEMS = A_ELEMS + B_ELEMS;
+  static constexpr size_t BYTES = (size_t)STAGES * STAGE_ELEMS * sizeof(double);
+};
+
+template <int BM, int BN, int WM, int WN, bool TA, bool TB, int VEC>
+__global__ void __launch_bounds__(WM* WN * 32) gemm_f64_kernel(GemmArgs g) {
+  using SL = SmemLayout<BM, BN, TA, TB>;
+  constexpr int NT = WM * WN * 32;
+  constexpr int WTM = BM / WM, WTN = BN / WN;
+  constexpr int FM = WTM / 8, FN = WTN / 8;
+  extern __shared__ __align__(128) double smem[];
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm0 = (warp / WN) * WTM, wn0 = (warp % WN) * WTN;
+  const int64_t m0 = (int64_t)blockIdx.y * BM, n0 = (int64_t)blockIdx.x * BN;
+  const int nk = (int)((g.K + BK - 1) / BK);
+
+  for (int64_t b = blockIdx.z; b < g.batch; b += gridDim.z) {
+    const double* __restrict__ A = g.A + b * g.sA;
+    const double* __restrict__ B = g.B + b * g.sB;
+    double* __restrict__ C = g.C + b * g.sC;
+
+    auto load_stage = [&](int stage, int kt) {
+      double* As = smem + stage * SL::STAGE_ELEMS;
+      double* Bs = As + SL::A_ELEMS;
+      const int64_t k0 = (int64_t)kt * BK;
+      // A: logical (m, k) tile BM x BK
+      {
+        constexpr int ROWS = TA ? BK : BM;   // smem rows
+        constexpr int COLS = TA ? BM : BK;   // contiguous extent
+        constexpr int CHUNKS = ROWS * COLS / VEC;
+        for (int c = tid; c < CHUNKS; c += NT) {
+          const int r = c / (COLS / VEC), cc = (c % (COLS / VEC)) * VEC;
+          int64_t gm, gk;
+          if (TA) { gk = k0 + r; gm = m0 + cc; } else { gm = m0 + r; gk = k0 + cc; }
+          const bool ok = (gm < g.M) && (gk < g.K);
+          const double* src = ok ? (TA ? A + gk * g.lda + gm : A + gm * g.lda + gk) : A;
+          cp_async_zfill<VEC * 8>(As + r * SL::A_LD + cc, src, ok);
+        }
+      }
+      // B: logical (k, n) tile BK x BN
+      {
+        constexpr int ROWS = TB ? BN : BK;
+        constexpr int COLS = TB ? BK : BN;
+        constexpr int CHUNKS = ROWS * COLS / VEC;
+        for (int c = tid; c < CHUNKS; c += NT) {
+          const int r = c / (COLS / VEC), cc = (c % (COLS / VEC)) * VEC;
+          int64_t gk, gn;
+          if (TB) { gn = n0 + r; gk = k0 + cc; } else { gk = k0 + r; gn = n0 + cc; }
+          const bool ok = (gn < g.N) && (gk < g.K);
+          const double* src = ok ? (TB ? B + gn * g.ldb + gk : B + gk * g.ldb + gn) : B;
+          cp_async_zfill<VEC * 8>(Bs + r * SL::B_LD + cc, src, ok);
+        }
+      }
+    };
+
+    double acc[FM][FN][2];
+#pragma unroll
+    for (int i = 0; i < FM; ++i)
+#pragma unroll
+      for (int j = 0; j < FN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+#pragma unroll
+    for (int s = 0; s < STAGES - 1; ++s) {
+      if (s < nk) load_stage(s, s);
+      cp_async_commit();
+    }
+    for (int kt = 0; kt < nk; ++kt) {
+      cp_async_wait<STAGES - 2>();
+      __syncthreads();
+      {
+        const int nxt = kt + STAGES - 1;
+        if (nxt < nk) load_stage(nxt % STAGES, nxt);
+        cp_async_commit();
+      }
+      const double* As = smem + (kt % STAGES) * SL::STAGE_ELEMS;
+      const double* Bs = As + SL::A_ELEMS;
+#pragma unroll
+      for (int ks = 0; ks < BK; ks += 4) {
+        double af[FM], bf[FN];
+        const int kk = ks + (lane & 3);
+#pragma unroll
+        for (int i = 0; i < FM; ++i) {
+          const int mm = wm0 + i * 8 + (lane >> 2);
+          af[i] = TA ? As[kk * SL::A_LD + mm] : As[mm * SL::A_LD + kk];
+        }
+#pragma unroll
+        for (int j = 0; j < FN; ++j) {
+          const int nn = wn0 + j * 8 + (lane >> 2);
+          bf[j] = TB ? Bs[nn * SL::B_LD + kk] : Bs[kk * SL::B_LD + nn];
+        }
+#pragma unroll
+        for (int i = 0; i < FM; ++i)
+#pragma unroll
+          for (int j = 0; j < FN; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+      }
+    }
+    cp_async_wait<0>();
+    __syncthreads();  // stage buffers are reused by the next batch item
+
+    // epilogue: C = alpha*acc + beta*C
+#pragma unroll
+    for (int i = 0; i < FM; ++i) {
+      const int64_t gm = m0 + wm0 + i * 8 + (lane >> 2);
+      if (gm >= g.M) continue;
+#pragma unroll
+      for (int j = 0; j < FN; ++j) {
+        const int64_t gn = n0 + wn0 + j * 8 + 2 * (lane & 3);
+        double* cp = C + gm * g.ldc + gn;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          if (gn + h < g.N) {
+            double v = g.alpha * acc[i][j][h];
+            if (g.beta != 0.0) v = fma(g.beta, cp[h], v);
+            cp[h] = v;
+          }
+        }
+      }
+    }
+  }
+}
+
+__global__ void gemm_scale_kernel(double* C, int64_t M, int64_t N, int64_t ldc, int64_t sC,
+                                  double beta) {
+  double* Cb = C + (int64_t)blockIdx.y * sC;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < M * N;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    double* p = Cb + (e / N) * ldc + e % N;
+    *p = beta == 0.0 ? 0.0 : beta * *p;
+  }
+}
+
+template <int BM, int BN, int WM, int WN, bool TA, bool TB, int VEC>
+int launch_cfg(const GemmArgs& g, cudaStream_t st) {
+  using SL = SmemLayout<BM, BN, TA, TB>;
+  auto kern = gemm_f64_kernel<BM, BN, WM, WN, TA, TB, VEC>;
+  static bool attr = false;
+  if (!attr) {
+    WT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SL::BYTES));
+    attr = true;
+  }
+  dim3 grid((unsigned)((g.N + BN - 1) / BN), (unsigned)((g.M + BM - 1) / BM),
+            (unsigned)std::min<int64_t>(g.batch, 65535));
+  WT_REQUIRE(grid.y <= 65535, "gemm: M too large");
+  kern<<<grid, WM * WN * 32, SL::BYTES, st>>>(g);
+  return check_launch("wt_gemm_f64");
+}
+
+template <bool TA, bool TB, int VEC>
+int dispatch_tile(const GemmArgs& g, cudaStream_t st) {
+  const int64_t big_tiles = ((g.M + 127) / 128) * ((g.N + 127) / 128) * g.batch;
+  if (g.M >= 128 && g.N >= 128 && big_tiles >= num_sms())
+    return launch_cfg<128, 128, 2, 4, TA, TB, VEC>(g, st);
+  if (g.M >= 64 && g.N >= 64) return launch_cfg<64, 64, 2, 2, TA, TB, VEC>(g, st);
+  return launch_cfg<32, 32, 2, 2, TA, TB, VEC>(g, st);
+}
+
+template <bool TA, bool TB>
+int dispatch_vec(const GemmArgs& g, cudaStream_t st) {
+  // 16-byte cp.async needs every contiguous run to start 16-byte aligned.
+  const int64_t a_extent = TA ? g.M : g.K, b_extent = TB ? g.K : g.N;
+  bool v2 = (a_extent % 2 == 0) && (b_extent % 2 == 0) && (g.lda % 2 == 0) &&
+            (g.ldb % 2 == 0) && (g.sA % 2 == 0 || g.batch == 1) &&
+            (g.sB % 2 == 0 || g.batch == 1) && ((uintptr_t)g.A % 16 == 0) &&
+            ((uintptr_t)g.B % 16 == 0);
+  return v2 ? dispatch_tile<TA, TB, 2>(g, st) : dispatch_tile<TA, TB, 1>(g, st);
+}
+
+}  // namespace
+}  // namespace wt
+
+using namespace wt;
+
+extern "C" int wt_gemm_f64(int transA, int transB, int64_t M, int64_t N, int64_t K, double alpha,
+                           const double* A, int64_t lda, int64_t strideA, const double* B,
+                           int64_t ldb, int64_t strideB, double beta, double* C, int64_t ldc,
+                           int64_t strideC, int64_t batch, void* stream) {
+  WT_REQUIRE(M >= 0 && N >= 0 && K >= 0 && batch >= 0, "gemm: negative dimension");
+  if (M == 0 || N == 0 || batch == 0) return WT_OK;
+  WT_REQUIRE(ldc >= N, "gemm: ldc < N");
+  WT_REQUIRE(lda >= (transA ? M : K) || K == 0, "gemm: lda too small");
+  WT_REQUIRE(ldb >= (transB ? K : N) || K == 0, "gemm: ldb too small");
+  if (K == 0) {  // empty inner dimension: C = beta * C (numpy matmul gives zeros)
+    WT_REQUIRE(batch <= 65535, "gemm: batch too large");
+    dim3 grid((unsigned)std::min<int64_t>((M * N + 255) / 256, 1024), (unsigned)batch);
+    gemm_scale_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(C, M, N, ldc, strideC, beta);
+    return check_launch("wt_gemm_f64(K=0)");
+  }
+  GemmArgs g{M, N, K, alpha, beta, A, lda, strideA, B, ldb, strideB, C, ldc, strideC, batch};
+  cudaStream_t st = (cudaStream_t)stream;
+  if (!transA && !transB) return dispatch_vec<false, false>(g, st);
+  if (!transA && transB) return dispatch_vec<false, true>(g, st);
+  if (transA && !transB) return dispatch_vec<true, false>(g, st);
+  return dispatch_vec<true, true>(g, st);
+}

@@ -1,0 +1,299 @@
+// K1 / K2: fused multilevel lazy-lifting transform along mode 3 (the tube axis).
+//
+// Reference semantics (bit-exact):
+//   forward level (lifting.py:63-66):  d = x[2k] - x[2k+1];  s = x[2k+1] + d/2
+//   inverse level (lifting.py:69-74):  x[2k+1] = s - d/2;    x[2k] = d + x[2k+1]
+// Halving is exact in IEEE-754, so __dmul_rn(d, 0.5) == d/2 and every result is
+// the same correctly-rounded double the numpy reference produces.
+//
+// B200 design:
+//   * A CTA owns a tile of TQ consecutive tubes x CT consecutive bands (CT a
+//     multiple of 2^L: lifting has no halo across 2^L-band chunks), so all L
+//     levels run in one pass over HBM: 8 B read + 8 B written per element.
+//   * The tile is staged in shared memory by the TMA bulk-copy engine
+//     (cp.async.bulk, one copy per tube row, mbarrier completion) -- the
+//     tube-major input rows are contiguous.  Row pitch CT+2 doubles makes the
+//     (2k, 2k+1) pair reads conflict-free double2 LDS.
+//   * Slice-major outputs are written with consecutive threads on consecutive
+//     tubes: every packed slice row segment is a contiguous TQ*8-byte burst.
+//   * Inverse: the finished tube rows go back to HBM with bulk shared->global
+//     copies.
+#include "wt_common.cuh"
+
+namespace wt {
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kMaxTileElems = 8192;                 // TQ * CT
+constexpr int kMaxItems = kMaxTileElems / 2 / kThreads;  // register staging depth (16)
+
+struct LiftGeom {
+  int64_t ntubes, p;
+  int L;
+  int TQ, CT, LDT;  // tile tubes, tile bands, smem row pitch (doubles)
+  int64_t slice_base;
+  int layout;
+  uint64_t mask;
+};
+
+__host__ __device__ __forceinline__ int64_t detail_off(int64_t p, int j) {
+  // first packed slice of detail level j (1-based): p - p/2^(j-1)
+  return p - (p >> (j - 1));
+}
+__host__ __device__ __forceinline__ int64_t smooth_off(int64_t p, int L) { return p - (p >> L); }
+
+// Output/input address of element k (0-based within the block) of packed block
+// `blk_off` (first slice), holding `cnt` slices, for tube q.
+__device__ __forceinline__ int64_t pyr_index(const LiftGeom& g, int64_t blk_off, int64_t cnt,
+                                             int64_t q, int64_t k) {
+  if (g.layout == WT_LAYOUT_SLICE_MAJOR) return (blk_off + k - g.slice_base) * g.ntubes + q;
+  return (blk_off - g.slice_base) * g.ntubes + q * cnt + k;
+}
+
+// Stage rows [q0, q0+tq) x [t0, t0+CT) of the tube-major tensor into smem.
+__device__ __forceinline__ void load_tile(double* tile, const double* __restrict__ x,
+                                          const LiftGeom& g, int64_t q0, int tq, int64_t t0,
+                                          bool bulk, uint64_t* bar) {
+  if (bulk) {
+    if (threadIdx.x < 32) {
+      if (threadIdx.x == 0) mbar_expect_tx(bar, (uint32_t)(tq * g.CT * 8));
+      __syncwarp();
+      for (int r = threadIdx.x; r < tq; r += 32)
+        bulk_g2s(tile + r * g.LDT, x + (q0 + r) * g.p + t0, (uint32_t)(g.CT * 8), bar);
+    }
+    mbar_wait(bar, 0);
+  } else {
+    const int n = tq * g.CT;
+    for (int e = threadIdx.x; e < n; e += kThreads) {
+      int r = e / g.CT, t = e - r * g.CT;
+      tile[r * g.LDT + t] = __ldg(x + (q0 + r) * g.p + t0 + t);
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) lift_fwd_kernel(const double* __restrict__ x,
+                                                            double* __restrict__ out,
+                                                            LiftGeom g, bool bulk) {
+  extern __shared__ __align__(128) double tile[];
+  __shared__ __align__(8) uint64_t bar;
+  const int64_t q0 = (int64_t)blockIdx.x * g.TQ;
+  const int tq = (int)(g.ntubes - q0 < g.TQ ? g.ntubes - q0 : g.TQ);
+  const int64_t t0 = (int64_t)blockIdx.y * g.CT;
+  if (bulk && threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  load_tile(tile, x, g, q0, tq, t0, bulk, &bar);
+
+  const bool tube_out = g.layout == WT_LAYOUT_TUBE_MAJOR;
+  int ell = g.CT;
+  if (g.L == 0) {  // pure tube-major -> slice-major transpose
+    if (g.mask & 1) {
+      const int n = tq * ell;
+      for (int e = threadIdx.x; e < n; e += kThreads) {
+        int r, k;
+        if (tube_out) { r = e / ell; k = e - r * ell; } else { k = e / tq; r = e - k * tq; }
+        out[pyr_index(g, 0, g.p, q0 + r, t0 + k)] = tile[r * g.LDT + k];
+      }
+    }
+    return;
+  }
+  for (int j = 1; j <= g.L; ++j) {
+    const int half = ell >> 1;
+    const int n = tq * half;
+    const bool last = (j == g.L);
+    const bool want_d = (g.mask >> j) & 1;
+    const bool want_s = last && (g.mask & 1);
+    const int64_t dcnt = g.p >> j;
+    const int64_t doff = detail_off(g.p, j);
+    const int64_t kbase = t0 >> j;
+    double sreg[kMaxItems];
+#pragma unroll
+    for (int it = 0; it < kMaxItems; ++it) {
+      const int e = threadIdx.x + it * kThreads;
+      if (e < n) {
+        int r, k;
+        if (tube_out) { r = e / half; k = e - r * half; } else { k = e / tq; r = e - k * tq; }
+        const double2 v = *reinterpret_cast<const double2*>(tile + r * g.LDT + 2 * k);
+        const double d = __dsub_rn(v.x, v.y);
+        const double s = __dadd_rn(v.y, __dmul_rn(d, 0.5));
+        if (want_d) out[pyr_index(g, doff, dcnt, q0 + r, kbase + k)] = d;
+        if (last) {
+          if (want_s) out[pyr_index(g, smooth_off(g.p, g.L), dcnt, q0 + r, kbase + k)] = s;
+        } else {
+          sreg[it] = s;
+        }
+      }
+    }
+    if (last) break;
+    __syncthreads();
+#pragma unroll
+    for (int it = 0; it < kMaxItems; ++it) {
+      const int e = threadIdx.x + it * kThreads;
+      if (e < n) {
+        int r, k;
+        if (tube_out) { r = e / half; k = e - r * half; } else { k = e / tq; r = e - k * tq; }
+        tile[r * g.LDT + k] = sreg[it];
+      }
+    }
+    __syncthreads();
+    ell = half;
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) lift_inv_kernel(const double* __restrict__ pyr,
+                                                            double* __restrict__ y, LiftGeom g,
+                                                            bool bulk) {
+  extern __shared__ __align__(128) double tile[];
+  const int64_t q0 = (int64_t)blockIdx.x * g.TQ;
+  const int tq = (int)(g.ntubes - q0 < g.TQ ? g.ntubes - q0 : g.TQ);
+  const int64_t t0 = (int64_t)blockIdx.y * g.CT;
+  const bool tube_in = g.layout == WT_LAYOUT_TUBE_MAJOR;
+
+  // coarsest smooth block -> smem
+  {
+    const int ms = g.CT >> g.L;
+    const int n = tq * ms;
+    const int64_t scnt = g.p >> g.L;
+    const int64_t soff = smooth_off(g.p, g.L);
+    const bool have = g.mask & 1;
+    for (int e = threadIdx.x; e < n; e += kThreads) {
+      int r, k;
+      if (tube_in) { r = e / ms; k = e - r * ms; } else { k = e / tq; r = e - k * tq; }
+      tile[r * g.LDT + k] = have ? __ldg(pyr + pyr_index(g, soff, scnt, q0 + r, (t0 >> g.L) + k)) : 0.0;
+    }
+  }
+  __syncthreads();
+  for (int j = g.L; j >= 1; --j) {
+    const int half = g.CT >> j;
+    const int n = tq * half;
+    const bool have_d = (g.mask >> j) & 1;
+    const int64_t dcnt = g.p >> j;
+    const int64_t doff = detail_off(g.p, j);
+    const int64_t kbase = t0 >> j;
+    double2 oreg[kMaxItems];
+#pragma unroll
+    for (int it = 0; it < kMaxItems; ++it) {
+      const int e = threadIdx.x + it * kThreads;
+      if (e < n) {
+        int r, k;
+        if (tube_in) { r = e / half; k = e - r * half; } else { k = e / tq; r = e - k * tq; }
+        const double s = tile[r * g.LDT + k];
+        const double d = have_d ? __ldg(pyr + pyr_index(g, doff, dcnt, q0 + r, kbase + k)) : 0.0;
+        const double x1 = __dsub_rn(s, __dmul_rn(d, 0.5));
+        oreg[it] = make_double2(__dadd_rn(d, x1), x1);
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int it = 0; it < kMaxItems; ++it) {
+      const int e = threadIdx.x + it * kThreads;
+      if (e < n) {
+        int r, k;
+        if (tube_in) { r = e / half; k = e - r * half; } else { k = e / tq; r = e - k * tq; }
+        *reinterpret_cast<double2*>(tile + r * g.LDT + 2 * k) = oreg[it];
+      }
+    }
+    __syncthreads();
+  }
+  // tile rows -> tube-major output
+  if (bulk) {
+    fence_proxy_async_smem();
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      for (int r = threadIdx.x; r < tq; r += 32)
+        bulk_s2g(y + (q0 + r) * g.p + t0, tile + r * g.LDT, (uint32_t)(g.CT * 8));
+      bulk_commit();
+      bulk_wait_all();
+    }
+  } else {
+    const int n = tq * g.CT;
+    for (int e = threadIdx.x; e < n; e += kThreads) {
+      int r = e / g.CT, t = e - r * g.CT;
+      y[(q0 + r) * g.p + t0 + t] = tile[r * g.LDT + t];
+    }
+  }
+}
+
+// Choose the tile: TQ tubes x CT bands, CT = 2^L * d with d | p/2^L.
+int plan_tiles(LiftGeom& g) {
+  const int64_t unit = (int64_t)1 << g.L;
+  const int64_t munits = g.p / unit;
+  for (int tq = 32; tq >= 1; tq >>= 1) {
+    const int64_t cap = kMaxTileElems / tq;
+    if (unit > cap) continue;
+    int64_t best = 0;
+    for (int64_t d = 1; d <= munits && unit * d <= cap; ++d)
+      if (munits % d == 0) best = d;
+    g.TQ = tq;
+    g.CT = (int)(unit * best);
+    g.LDT = g.CT + (g.CT % 2 == 0 ? 2 : 1);
+    return WT_OK;
+  }
+  set_error("lifting: 2^levels = %lld band chunk exceeds the single-pass tile (%d)",
+            (long long)unit, kMaxTileElems);
+  return WT_ERR_UNSUPPORTED;
+}
+
+int validate(int64_t n1, int64_t n2, int64_t p, int levels, int layout, int64_t slice_base) {
+  WT_REQUIRE(n1 >= 0 && n2 >= 0 && p >= 1, "lifting: bad shape (%lld, %lld, %lld)",
+             (long long)n1, (long long)n2, (long long)p);
+  WT_REQUIRE(levels >= 0 && levels < 63 && (p % ((int64_t)1 << levels)) == 0,
+             "lifting: 2**%d does not divide slice count %lld", levels, (long long)p);
+  WT_REQUIRE(layout == WT_LAYOUT_SLICE_MAJOR || layout == WT_LAYOUT_TUBE_MAJOR,
+             "lifting: unknown layout %d", layout);
+  WT_REQUIRE(slice_base >= 0 && slice_base < p, "lifting: slice_base %lld out of range",
+             (long long)slice_base);
+  return WT_OK;
+}
+
+}  // namespace
+}  // namespace wt
+
+using namespace wt;
+
+extern "C" int wt_lift_fwd_f64(const double* x, int64_t n1, int64_t n2, int64_t p, int levels,
+                               double* out, int layout, int64_t slice_base, uint64_t level_mask,
+                               void* stream) {
+  int st = validate(n1, n2, p, levels, layout, slice_base);
+  if (st) return st;
+  LiftGeom g{n1 * n2, p, levels, 0, 0, 0, slice_base, layout, level_mask};
+  if (g.ntubes == 0) return WT_OK;
+  if ((st = plan_tiles(g))) return st;
+  const bool bulk = (g.CT % 2 == 0) && (p % 2 == 0) && ((uintptr_t)x % 16 == 0);
+  const size_t smem = (size_t)g.TQ * g.LDT * sizeof(double);
+  static bool attr = false;
+  if (!attr) {
+    WT_CUDA(cudaFuncSetAttribute(lift_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 kMaxTileElems * 8 + 4096));
+    attr = true;
+  }
+  dim3 grid((unsigned)((g.ntubes + g.TQ - 1) / g.TQ), (unsigned)(p / g.CT));
+  WT_REQUIRE(grid.y <= 65535, "lifting: too many band chunks");
+  lift_fwd_kernel<<<grid, kThreads, smem, (cudaStream_t)stream>>>(x, out, g, bulk);
+  return check_launch("wt_lift_fwd_f64");
+}
+
+extern "C" int wt_lift_inv_f64(const double* pyr, int64_t n1, int64_t n2, int64_t p, int levels,
+                               int layout, int64_t slice_base, uint64_t level_mask, double* y,
+                               void* stream) {
+  int st = validate(n1, n2, p, levels, layout, slice_base);
+  if (st) return st;
+  LiftGeom g{n1 * n2, p, levels, 0, 0, 0, slice_base, layout, level_mask};
+  if (g.ntubes == 0) return WT_OK;
+  if ((st = plan_tiles(g))) return st;
+  const bool bulk = (g.CT % 2 == 0) && (p % 2 == 0) && ((uintptr_t)y % 16 == 0);
+  const size_t smem = (size_t)g.TQ * g.LDT * sizeof(double);
+  static bool attr = false;
+  if (!attr) {
+    WT_CUDA(cudaFuncSetAttribute(lift_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 kMaxTileElems * 8 + 4096));
+    attr = true;
+  }
+  dim3 grid((unsigned)((g.ntubes + g.TQ - 1) / g.TQ), (unsigned)(p / g.CT));
+  WT_REQUIRE(grid.y <= 65535, "lifting: too many band chunks");
+  lift_inv_kernel<<<grid, kThreads, smem, (cudaStream_t)stream>>>(pyr, y, g, bulk);
+  return check_launch("wt_lift_inv_f64");
+}

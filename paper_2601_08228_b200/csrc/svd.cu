@@ -1,0 +1,473 @@
+// K4: batched one-sided block-Jacobi SVD in FP64 (Gram and rotation tiles on
+// the DMMA tensor pipe).  Replaces _stack_svd (decomposition.py:64-67), i.e.
+// LAPACK dgesdd over every wavelet-domain slice.
+//
+// Algorithm:
+//   X (m x n, n <= m, columns contiguous) is the slice oriented so that the
+//   short side is orthogonalised: X = A^T when n1 <= n2 (columns = rows of A),
+//   X = A otherwise.  Columns are grouped in blocks of 16; each sweep visits
+//   every block pair once in round-robin order (nblk-1 rounds of nblk/2
+//   disjoint pairs, one CTA per pair and matrix).  Per pair:
+//     1. G = Z^T Z for the 32-column panel Z = [X_I X_J] (DMMA, rows streamed
+//        through shared memory with cp.async double buffering);
+//     2. if max_{i<j} |G_ij| / sqrt(G_ii G_jj) < tol the pair is skipped;
+//        otherwise G = Q diag Q^T by cyclic parallel two-sided Jacobi in
+//        shared memory (16 disjoint rotations per step);
+//     3. Z <- Z Q (DMMA, streamed again, written back in place).
+//   A sweep in which no pair exceeded tol ends the iteration for that matrix.
+//   Finally sigma_c = ||X_c|| and the columns are sorted descending; the
+//   normalised columns are the long-side singular vectors.
+// Everything is deterministic: fixed reduction orders, no floating atomics.
+#include <algorithm>
+
+#include "wt_common.cuh"
+
+namespace wt {
+namespace {
+
+constexpr int BW = 32;       // pair panel width (2 blocks of 16 columns)
+constexpr int HB = BW / 2;   // block width
+constexpr int RCH = 64;      // rows per streamed chunk
+constexpr int LDZ = RCH + 4; // chunk column pitch (doubles), = 4 mod 16: conflict-free frags
+constexpr int LDG = BW + 1;  // Gram / Q pitch
+constexpr int kThreads = 256;
+
+struct SvdWs {
+  double* X;        // batch * npad * mpad
+  unsigned long long* offmax;  // batch  (bit pattern of a non-negative double)
+  int* conv;        // batch: 1 = converged, 2 = non-finite
+  int* pending;     // 1 counter (matrices still iterating)
+  double* sig;      // batch * npad  (scratch for the final sort)
+  int* perm;        // batch * npad
+};
+
+__host__ __device__ inline int64_t round_up(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
+
+// ------------------------------------------------------------- copy in -----
+__global__ void svd_copy_in(const double* __restrict__ A, int64_t lda, int64_t sA, bool right,
+                            int64_t m, int64_t n, int64_t mpad, int64_t npad, double* __restrict__ X) {
+  const int64_t b = blockIdx.y;
+  const int64_t total = npad * mpad;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = e / mpad, r = e - c * mpad;
+    double v = 0.0;
+    if (c < n && r < m) v = right ? A[b * sA + c * lda + r] : A[b * sA + r * lda + c];
+    X[b * total + e] = v;
+  }
+}
+
+// ---------------------------------------------------------- pair kernel ----
+__device__ __forceinline__ double nanmax(double a, double b) {
+  return (isnan(a) || isnan(b)) ? (a + b) : fmax(a, b);
+}
+
+__device__ __forceinline__ int rr_index(int pos, int round, int nb) {
+  // circle method: position 0 fixed, the others rotate by `round`
+  return pos == 0 ? 0 : 1 + (pos - 1 + round) % (nb - 1);
+}
+
+struct PairSmem {
+  double Z[2][BW * LDZ];
+  double G[2][BW * LDG];
+  double Q[2][BW * LDG];
+  double cs[BW][2];   // per index: (own coefficient c_i, partner coefficient o_i)
+  int partner[BW];
+  int rotated;
+  double off;
+};
+
+__device__ __forceinline__ void load_chunk(double* Zs, const double* Xb, int64_t mpad, int colI,
+                                           int colJ, int64_t r0) {
+  // 32 columns x RCH rows, 16-byte cp.async; column c of the panel maps to
+  // global column colI + c (c < 16) or colJ + c - 16.
+  constexpr int VPC = RCH / 2;  // 16-byte vectors per column chunk
+  for (int v = threadIdx.x; v < BW * VPC; v += kThreads) {
+    const int c = v / VPC, rv = (v % VPC) * 2;
+    const int gc = c < HB ? colI + c : colJ + c - HB;
+    cp_async_zfill<16>(Zs + c * LDZ + rv, Xb + (int64_t)gc * mpad + r0 + rv, true);
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) svd_pair_kernel(SvdWs ws, int64_t mpad, int64_t npad,
+                                                            int round, double tol) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  PairSmem& S = *reinterpret_cast<PairSmem*>(smem_raw);
+  const int b = blockIdx.y;
+  if (ws.conv[b]) return;
+  const int nb = (int)(npad / HB);
+  const int I = rr_index(blockIdx.x, round, nb), J = rr_index(nb - 1 - blockIdx.x, round, nb);
+  const int colI = I * HB, colJ = J * HB;
+  double* Xb = ws.X + (int64_t)b * npad * mpad;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nch = (int)(mpad / RCH);
+
+  // ---------------- 1. Gram G = Z^T Z (warp: tile row ti, K half kh) -------
+  const int ti = warp & 3, kh = warp >> 2;
+  double acc[4][2];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) acc[j][0] = acc[j][1] = 0.0;
+  load_chunk(S.Z[0], Xb, mpad, colI, colJ, 0);
+  cp_async_commit();
+  for (int ch = 0; ch < nch; ++ch) {
+    if (ch + 1 < nch) load_chunk(S.Z[(ch + 1) & 1], Xb, mpad, colI, colJ, (int64_t)(ch + 1) * RCH);
+    cp_async_commit();
+    cp_async_wait<1>();
+    __syncthreads();
+    const double* Zs = S.Z[ch & 1];
+#pragma unroll
+    for (int ks = kh * 4; ks < RCH; ks += 8) {
+      double f[4];
+#pragma unroll
+      for (int tj = 0; tj < 4; ++tj) f[tj] = Zs[(tj * 8 + (lane >> 2)) * LDZ + ks + (lane & 3)];
+#pragma unroll
+      for (int tj = 0; tj < 4; ++tj) dmma884(acc[tj][0], acc[tj][1], f[ti], f[tj]);
+    }
+    __syncthreads();
+  }
+  // partial tiles -> G[kh]; C frag: row ti*8 + lane/4, cols tj*8 + 2*(lane%4) + h
+#pragma unroll
+  for (int tj = 0; tj < 4; ++tj)
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+      S.G[kh][(ti * 8 + (lane >> 2)) * LDG + tj * 8 + 2 * (lane & 3) + h] = acc[tj][h];
+  __syncthreads();
+  for (int e = tid; e < BW * BW; e += kThreads) {
+    const int i = e / BW, j = e % BW;
+    S.G[0][i * LDG + j] += S.G[1][i * LDG + j];
+  }
+  if (tid == 0) S.off = 0.0;
+  __syncthreads();
+
+  // ---------------- 2. convergence test on this pair -----------------------
+  {
+    double mx = 0.0;
+    for (int e = tid; e < BW * BW; e += kThreads) {
+      const int i = e / BW, j = e % BW;
+      if (i < j) {
+        const double gij = S.G[0][i * LDG + j];
+        const double d = S.G[0][i * LDG + i] * S.G[0][j * LDG + j];
+        double c = 0.0;
+        if (gij != 0.0) c = d > 0.0 ? fabs(gij) / sqrt(d) : INFINITY;
+        mx = nanmax(mx, c);
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      mx = nanmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    }
+    if (lane == 0) {
+      // NaN-propagating max through the bit pattern (non-negative doubles order as uint64)
+      atomicMax(reinterpret_cast<unsigned long long*>(&S.off), (unsigned long long)__double_as_longlong(mx));
+    }
+  }
+  __syncthreads();
+  const double off = S.off;
+  if (tid == 0) atomicMax(&ws.offmax[b], (unsigned long long)__double_as_longlong(off));
+  if (!(off >= tol)) return;  // converged pair (or NaN: recorded above, stop touching data)
+  if (isnan(off) || isinf(off)) return;
+
+  // ---------------- 3. eigen-decomposition of G (cyclic parallel Jacobi) ----
+  for (int e = tid; e < BW * BW; e += kThreads) {
+    const int i = e / BW, j = e % BW;
+    S.Q[0][i * LDG + j] = (i == j) ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  int cur = 0;
+  const double eps_in = 2.220446049250313e-16;
+  for (int sweep = 0; sweep < 20; ++sweep) {
+    if (tid == 0) S.rotated = 0;
+    __syncthreads();
+    for (int step = 0; step < BW - 1; ++step) {
+      const double* G = S.G[cur];
+      if (tid < BW / 2) {
+        int p = rr_index(tid, step, BW), q = rr_index(BW - 1 - tid, step, BW);
+        if (p > q) { int t = p; p = q; q = t; }
+        const double gpp = G[p * LDG + p], gqq = G[q * LDG + q], gpq = G[p * LDG + q];
+        double c = 1.0, s = 0.0;
+        if (gpq != 0.0 && fabs(gpq) > eps_in * sqrt(gpp * gqq)) {
+          const double tau = (gqq - gpp) / (2.0 * gpq);
+          const double t = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + hypot(1.0, tau));
+          c = 1.0 / sqrt(1.0 + t * t);
+          s = t * c;
+          S.rotated = 1;
+        }
+        S.partner[p] = q;
+        S.partner[q] = p;
+        S.cs[p][0] = c; S.cs[p][1] = -s;  // J[q][p] = -s
+        S.cs[q][0] = c; S.cs[q][1] = s;   // J[p][q] = +s
+      }
+      __syncthreads();
+      double* Gn = S.G[cur ^ 1];
+      const double* Qo = S.Q[cur];
+      double* Qn = S.Q[cur ^ 1];
+      for (int e = tid; e < BW * BW; e += kThreads) {
+        const int i = e / BW, j = e % BW;
+        const int pi = S.partner[i], pj = S.partner[j];
+        const double ci = S.cs[i][0], oi = S.cs[i][1], cj = S.cs[j][0], oj = S.cs[j][1];
+        // G' = J^T G J, summed in an order symmetric in (i, j)
+        const double t1 = ci * cj * G[i * LDG + j];
+        const double t4 = oi * oj * G[pi * LDG + pj];
+        const double t2 = ci * oj * G[i * LDG + pj];
+        const double t3 = oi * cj * G[pi * LDG + j];
+        double v = (t1 + t4) + (t2 + t3);
+        if (pi == j && i != j && oi != 0.0) v = 0.0;  // annihilated entry
+        Gn[i * LDG + j] = v;
+        // Q' = Q J (column operation)
+        Qn[i * LDG + j] = Qo[i * LDG + j] * cj + Qo[i * LDG + pj] * oj;
+      }
+      cur ^= 1;
+      __syncthreads();
+    }
+    if (!S.rotated) break;
+  }
+
+  // ---------------- 4. Z <- Z Q, streamed, written back in place -----------
+  // Q fragments cached in registers: b-frag for k-step kk, n-tile tn is
+  // Q[kk*4 + lane%4][tn*8 + lane/4].
+  double qf[8][4];
+  {
+    const double* Q = S.Q[cur];
+#pragma unroll
+    for (int kk = 0; kk < 8; ++kk)
+#pragma unroll
+      for (int tn = 0; tn < 4; ++tn) qf[kk][tn] = Q[(kk * 4 + (lane & 3)) * LDG + tn * 8 + (lane >> 2)];
+  }
+  load_chunk(S.Z[0], Xb, mpad, colI, colJ, 0);
+  cp_async_commit();
+  for (int ch = 0; ch < nch; ++ch) {
+    if (ch + 1 < nch) load_chunk(S.Z[(ch + 1) & 1], Xb, mpad, colI, colJ, (int64_t)(ch + 1) * RCH);
+    cp_async_commit();
+    cp_async_wait<1>();
+    __syncthreads();
+    double* Zs = S.Z[ch & 1];
+    // warp w: rows w*8 .. w*8+7 of the chunk, all 32 output columns
+    double o[4][2];
+#pragma unroll
+    for (int tn = 0; tn < 4; ++tn) o[tn][0] = o[tn][1] = 0.0;
+    const int r0 = warp * 8;
+#pragma unroll
+    for (int kk = 0; kk < 8; ++kk) {
+      const double a = Zs[(kk * 4 + (lane & 3)) * LDZ + r0 + (lane >> 2)];
+#pragma unroll
+      for (int tn = 0; tn < 4; ++tn) dmma884(o[tn][0], o[tn][1], a, qf[kk][tn]);
+    }
+    __syncwarp();
+#pragma unroll
+    for (int tn = 0; tn < 4; ++tn)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) Zs[(tn * 8 + 2 * (lane & 3) + h) * LDZ + r0 + (lane >> 2)] = o[tn][h];
+    __syncthreads();
+    // chunk -> global (each column: RCH contiguous doubles)
+    const int64_t rbase = (int64_t)ch * RCH;
+    for (int v = tid; v < BW * (RCH / 2); v += kThreads) {
+      const int c = v / (RCH / 2), rv = (v % (RCH / 2)) * 2;
+      const int gc = c < HB ? colI + c : colJ + c - HB;
+      *reinterpret_cast<double2*>(Xb + (int64_t)gc * mpad + rbase + rv) =
+          *reinterpret_cast<const double2*>(Zs + c * LDZ + rv);
+    }
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------------ sweep bookkeeping --
+__global__ void svd_end_sweep(SvdWs ws, int batch, double tol) {
+  for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < batch; b += gridDim.x * blockDim.x) {
+    if (ws.conv[b]) continue;
+    const double off = __longlong_as_double((long long)ws.offmax[b]);
+    if (isnan(off) || isinf(off)) ws.conv[b] = 2;
+    else if (off < tol) ws.conv[b] = 1;
+    else atomicAdd(ws.pending, 1);
+    ws.offmax[b] = 0ull;
+  }
+}
+
+// ------------------------------------------------------------- finalize ----
+// One CTA per matrix: column norms, descending sort (ties by index), sigma out.
+__global__ void svd_norms_sort(SvdWs ws, int64_t mpad, int64_t npad, int64_t n, int npow2,
+                               double* __restrict__ sigma, int* __restrict__ info, int max_sweeps_hit) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double* key = reinterpret_cast<double*>(smem_raw);
+  int* idx = reinterpret_cast<int*>(key + npow2);
+  const int b = blockIdx.x;
+  const double* Xb = ws.X + (int64_t)b * npad * mpad;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int c = warp; c < npow2; c += nw) {
+    double s = 0.0;
+    if (c < n) {
+      for (int64_t r = lane; r < mpad; r += 32) {
+        const double v = Xb[(int64_t)c * mpad + r];
+        s = fma(v, v, s);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    }
+    if (lane == 0) {
+      key[c] = c < n ? sqrt(s) : -1.0;
+      idx[c] = c;
+    }
+  }
+  __syncthreads();
+  // bitonic sort: descending key, ascending index on ties; NaN sorts first
+  for (int k = 2; k <= npow2; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < npow2; i += blockDim.x) {
+        const int l = i ^ j;
+        if (l > i) {
+          const double ki = key[i], kl = key[l];
+          const int ii = idx[i], il = idx[l];
+          // "i before l" in final order?
+          const bool i_first = (ki > kl) || (ki == kl && ii < il) || (isnan(ki) && !isnan(kl));
+          const bool up = ((i & k) == 0);
+          if (up != i_first) {
+            key[i] = kl; key[l] = ki;
+            idx[i] = il; idx[l] = ii;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  bool bad = false;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    sigma[(int64_t)b * n + i] = key[i];
+    ws.perm[(int64_t)b * npad + i] = idx[i];
+    ws.sig[(int64_t)b * npad + i] = key[i];
+    if (!isfinite(key[i])) bad = true;
+  }
+  bad = __syncthreads_or(bad);
+  if (threadIdx.x == 0) {
+    int st = 0;
+    if (bad || ws.conv[b] == 2) st = 1;
+    else if (ws.conv[b] == 0 && max_sweeps_hit) st = 2;
+    info[b] = st;
+  }
+}
+
+__global__ void svd_gather(SvdWs ws, int64_t mpad, int64_t npad, int64_t m, int64_t nvec,
+                           double* __restrict__ vec) {
+  const int64_t i = blockIdx.x, b = blockIdx.y;
+  const int c = ws.perm[b * npad + i];
+  const double s = ws.sig[b * npad + i];
+  const double inv = (s > 0.0 && isfinite(s)) ? 1.0 / s : 0.0;
+  const double* col = ws.X + (b * npad + c) * mpad;
+  double* dst = vec + (b * nvec + i) * m;
+  for (int64_t r = threadIdx.x; r < m; r += blockDim.x) dst[r] = col[r] * inv;
+}
+
+struct WsLayout {
+  int64_t m, n, mpad, npad;
+  size_t off_X, off_off, off_conv, off_pending, off_sig, off_perm, total;
+};
+
+WsLayout ws_layout(int64_t n1, int64_t n2, int64_t batch) {
+  WsLayout L{};
+  L.m = std::max(n1, n2);
+  L.n = std::min(n1, n2);
+  L.mpad = round_up(std::max<int64_t>(L.m, 1), RCH);
+  L.npad = round_up(std::max<int64_t>(L.n, 1), BW);
+  size_t o = 0;
+  auto take = [&](size_t bytes) { size_t r = o; o = (o + bytes + 255) / 256 * 256; return r; };
+  L.off_X = take(sizeof(double) * (size_t)(batch * L.npad * L.mpad));
+  L.off_off = take(sizeof(unsigned long long) * (size_t)batch);
+  L.off_conv = take(sizeof(int) * (size_t)batch);
+  L.off_pending = take(sizeof(int) * 4);
+  L.off_sig = take(sizeof(double) * (size_t)(batch * L.npad));
+  L.off_perm = take(sizeof(int) * (size_t)(batch * L.npad));
+  L.total = o;
+  return L;
+}
+
+}  // namespace
+}  // namespace wt
+
+using namespace wt;
+
+static thread_local int g_last_sweeps = 0;
+
+// Sweeps used by the last wt_svd_jacobi_f64 call on this thread (diagnostics).
+extern "C" int wt_svd_last_sweeps(void) { return g_last_sweeps; }
+
+extern "C" size_t wt_svd_workspace_bytes(int64_t n1, int64_t n2, int64_t batch) {
+  if (n1 < 0 || n2 < 0 || batch < 0) return 0;
+  return ws_layout(n1, n2, batch).total;
+}
+
+extern "C" int wt_svd_jacobi_f64(const double* A, int64_t lda, int64_t strideA, int64_t n1,
+                                 int64_t n2, int64_t batch, double* sigma, double* vec,
+                                 int64_t nvec, int* info, double tol, int max_sweeps,
+                                 void* workspace, size_t workspace_bytes, void* stream) {
+  WT_REQUIRE(n1 >= 1 && n2 >= 1 && batch >= 0, "svd: bad shape %lld x %lld", (long long)n1,
+             (long long)n2);
+  if (batch == 0) return WT_OK;
+  WT_REQUIRE(batch <= 65535, "svd: batch %lld exceeds 65535", (long long)batch);
+  WT_REQUIRE(lda >= n2, "svd: lda < n2");
+  const WsLayout L = ws_layout(n1, n2, batch);
+  WT_REQUIRE(nvec >= 0 && nvec <= L.n, "svd: nvec %lld outside [0, %lld]", (long long)nvec,
+             (long long)L.n);
+  WT_REQUIRE(workspace != nullptr && workspace_bytes >= L.total,
+             "svd: workspace too small (%zu < %zu)", workspace_bytes, L.total);
+  int npow2 = 1;
+  while (npow2 < L.npad) npow2 <<= 1;
+  WT_REQUIRE(npow2 <= 8192, "svd: min(n1, n2) = %lld above the 8192 sort limit", (long long)L.n);
+  cudaStream_t st = (cudaStream_t)stream;
+  char* base = static_cast<char*>(workspace);
+  SvdWs ws{reinterpret_cast<double*>(base + L.off_X),
+           reinterpret_cast<unsigned long long*>(base + L.off_off),
+           reinterpret_cast<int*>(base + L.off_conv), reinterpret_cast<int*>(base + L.off_pending),
+           reinterpret_cast<double*>(base + L.off_sig), reinterpret_cast<int*>(base + L.off_perm)};
+  if (tol <= 0.0) tol = 4.0 * 2.220446049250313e-16 * sqrt((double)L.m) + 1e-15;
+  if (max_sweeps <= 0) max_sweeps = 40;
+  const bool right = n1 <= n2;
+
+  {
+    dim3 grid((unsigned)std::min<int64_t>((L.npad * L.mpad + 255) / 256, 4096), (unsigned)batch);
+    svd_copy_in<<<grid, 256, 0, st>>>(A, lda, strideA, right, L.m, L.n, L.mpad, L.npad, ws.X);
+    if (int e = check_launch("svd_copy_in")) return e;
+  }
+  WT_CUDA(cudaMemsetAsync(ws.offmax, 0, sizeof(unsigned long long) * batch, st));
+  WT_CUDA(cudaMemsetAsync(ws.conv, 0, sizeof(int) * batch, st));
+
+  static bool attr = false;
+  if (!attr) {
+    WT_CUDA(cudaFuncSetAttribute(svd_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)sizeof(PairSmem)));
+    attr = true;
+  }
+  g_last_sweeps = 0;
+  static int* h_pending = nullptr;
+  if (!h_pending) WT_CUDA(cudaMallocHost(&h_pending, sizeof(int)));
+  const int nb = (int)(L.npad / HB);
+  bool hit_max = true;
+  for (int sweep = 0; sweep < max_sweeps; ++sweep) {
+    for (int round = 0; round < nb - 1; ++round) {
+      svd_pair_kernel<<<dim3(nb / 2, (unsigned)batch), kThreads, sizeof(PairSmem), st>>>(
+          ws, L.mpad, L.npad, round, tol);
+    }
+    if (int e = check_launch("svd_pair_kernel")) return e;
+    WT_CUDA(cudaMemsetAsync(ws.pending, 0, sizeof(int), st));
+    svd_end_sweep<<<(unsigned)((batch + 255) / 256), 256, 0, st>>>(ws, (int)batch, tol);
+    WT_CUDA(cudaMemcpyAsync(h_pending, ws.pending, sizeof(int), cudaMemcpyDeviceToHost, st));
+    WT_CUDA(cudaStreamSynchronize(st));
+    g_last_sweeps = sweep + 1;
+    if (*h_pending == 0) { hit_max = false; break; }
+  }
+  {
+    const size_t sm = (size_t)npow2 * (sizeof(double) + sizeof(int));
+    static bool attr2 = false;
+    if (!attr2) {
+      WT_CUDA(cudaFuncSetAttribute(svd_norms_sort, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   8192 * (int)(sizeof(double) + sizeof(int))));
+      attr2 = true;
+    }
+    svd_norms_sort<<<(unsigned)batch, 512, sm, st>>>(ws, L.mpad, L.npad, L.n, npow2, sigma, info,
+                                                     hit_max ? 1 : 0);
+    if (int e = check_launch("svd_norms_sort")) return e;
+  }
+  if (nvec > 0) {
+    svd_gather<<<dim3((unsigned)nvec, (unsigned)batch), 256, 0, st>>>(ws, L.mpad, L.npad, L.m,
+                                                                       nvec, vec);
+    if (int e = check_launch("svd_gather")) return e;
+  }
+  return WT_OK;
+}

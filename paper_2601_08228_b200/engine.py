@@ -1,0 +1,233 @@
+"""Device-resident engine: thin wrappers over the C ABI on torch CUDA tensors.
+
+Every function takes and returns float64 CUDA tensors and runs on torch's
+current stream, so it composes with torch.distributed / CUDA graphs.  The
+public, reference-shaped API (``lifting``, ``algebra``, ``decomposition``) is
+built on these.  Packed pyramids are slice-major ``(slices, n1, n2)`` buffers in
+block order ``[d1 | ... | dL | sL]`` (include/wten_b200.h).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _native as N
+
+F64 = torch.float64
+
+
+def _stream() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def _ptr(t: torch.Tensor | None) -> int:
+    return 0 if t is None else t.data_ptr()
+
+
+def detail_offset(p: int, j: int) -> int:
+    """First packed slice of detail level j (1-based)."""
+    return p - (p >> (j - 1))
+
+
+def smooth_offset(p: int, levels: int) -> int:
+    return p - (p >> levels)
+
+
+def block_slices(p: int, levels: int):
+    """[(tag, first_slice, count)] in packed order d1..dL, s (decomposition.py:98-99 order)."""
+    out = [(f"d{j}", detail_offset(p, j), p >> j) for j in range(1, levels + 1)]
+    out.append(("s", smooth_offset(p, levels), p >> levels))
+    return out
+
+
+def level_mask(levels: int, smooth: bool = True, details=None) -> int:
+    """Bit 0 = smooth, bit j = detail level j."""
+    m = 1 if smooth else 0
+    for j in (range(1, levels + 1) if details is None else details):
+        m |= 1 << j
+    return m
+
+
+def as_device(x, device=None) -> torch.Tensor:
+    """float64, C-contiguous CUDA tensor (H2D copy for host inputs)."""
+    N.require_gpu()
+    if isinstance(x, torch.Tensor):
+        t = x
+        if not t.is_cuda:
+            t = t.to(device or "cuda", non_blocking=False)
+    else:
+        t = torch.from_numpy(np.ascontiguousarray(np.asarray(x, dtype=np.float64)))
+        t = t.to(device or "cuda")
+    if t.dtype != F64:
+        t = t.to(F64)
+    return t.contiguous()
+
+
+# --------------------------------------------------------------- lifting ----
+
+def lift_forward(x: torch.Tensor, levels: int, layout: int = N.LAYOUT_SLICE,
+                 mask: int = N.MASK_ALL, slice_base: int = 0,
+                 out: torch.Tensor | None = None) -> torch.Tensor:
+    """K1 on a contiguous (n1, n2, p) tensor -> packed buffer (slices-slice_base, n1, n2)."""
+    lib = N.require_gpu()
+    n1, n2, p = x.shape
+    if out is None:
+        out = torch.empty((p - slice_base, n1, n2), dtype=F64, device=x.device)
+    N.check(lib.wt_lift_fwd_f64(_ptr(x), n1, n2, p, levels, _ptr(out), layout, slice_base,
+                                mask & N.MASK_ALL, _stream()), "wt_lift_fwd_f64")
+    return out
+
+
+def lift_inverse(buf: torch.Tensor, n1: int, n2: int, p: int, levels: int,
+                 layout: int = N.LAYOUT_SLICE, mask: int = N.MASK_ALL, slice_base: int = 0,
+                 out: torch.Tensor | None = None) -> torch.Tensor:
+    """K2: packed buffer -> contiguous (n1, n2, p) tensor."""
+    lib = N.require_gpu()
+    if out is None:
+        out = torch.empty((n1, n2, p), dtype=F64, device=buf.device)
+    N.check(lib.wt_lift_inv_f64(_ptr(buf), n1, n2, p, levels, layout, slice_base,
+                                mask & N.MASK_ALL, _ptr(out), _stream()), "wt_lift_inv_f64")
+    return out
+
+
+# ------------------------------------------------------------------ GEMM ----
+
+def gemm(a: torch.Tensor, b: torch.Tensor, trans_a: bool = False, trans_b: bool = False,
+         alpha: float = 1.0, beta: float = 0.0, out: torch.Tensor | None = None) -> torch.Tensor:
+    """K3: batched C[k] = alpha op(A[k]) op(B[k]) + beta C[k] for (batch, rows, cols) tensors.
+
+    Operands may be any 3-D views whose last dimension is contiguous.
+    """
+    lib = N.require_gpu()
+    assert a.dim() == 3 and b.dim() == 3 and a.shape[0] == b.shape[0]
+    assert a.stride(2) == 1 and b.stride(2) == 1
+    batch = a.shape[0]
+    M, K = (a.shape[2], a.shape[1]) if trans_a else (a.shape[1], a.shape[2])
+    K2, Nn = (b.shape[2], b.shape[1]) if trans_b else (b.shape[1], b.shape[2])
+    assert K == K2, f"inner dimensions differ: {K} vs {K2}"
+    if out is None:
+        out = torch.empty((batch, M, Nn), dtype=F64, device=a.device)
+    assert out.stride(2) == 1
+    N.check(lib.wt_gemm_f64(int(trans_a), int(trans_b), M, Nn, K, float(alpha), _ptr(a),
+                            a.stride(1), a.stride(0), _ptr(b), b.stride(1), b.stride(0),
+                            float(beta), _ptr(out), out.stride(1), out.stride(0), batch,
+                            _stream()), "wt_gemm_f64")
+    return out
+
+
+def copy2d(src: torch.Tensor, trans: bool, out: torch.Tensor | None = None) -> torch.Tensor:
+    """Batched (transposing) copy of (batch, r, c) views."""
+    lib = N.require_gpu()
+    batch, r, c = src.shape
+    assert src.stride(2) == 1
+    shape = (batch, c, r) if trans else (batch, r, c)
+    if out is None:
+        out = torch.empty(shape, dtype=F64, device=src.device)
+    assert out.stride(2) == 1
+    N.check(lib.wt_copy2d_f64(_ptr(src), src.stride(1), src.stride(0), _ptr(out), out.stride(1),
+                              out.stride(0), shape[1], shape[2], batch, int(trans), _stream()),
+            "wt_copy2d_f64")
+    return out
+
+
+def scale_cols(m: torch.Tensor, s: torch.Tensor, mode: int, tol: float = 0.0,
+               ncols: int | None = None) -> torch.Tensor:
+    """In place: m[k][:, j] *= f(s[k][j]) (see WT_SCALE_*)."""
+    lib = N.require_gpu()
+    batch, rows, cols = m.shape
+    ncols = cols if ncols is None else ncols
+    assert m.stride(2) == 1 and s.is_contiguous()
+    N.check(lib.wt_scale_cols_f64(_ptr(m), rows, ncols, m.stride(1), m.stride(0), _ptr(s),
+                                  s.shape[-1], batch, mode, float(tol), _stream()),
+            "wt_scale_cols_f64")
+    return m
+
+
+# ------------------------------------------------------------------- SVD ----
+
+class SvdNotConverged(RuntimeError):
+    pass
+
+
+def svd(a: torch.Tensor, nvec: int, tol: float = 0.0, max_sweeps: int = 0):
+    """K4 over a batch of row-major matrices a (batch, n1, n2) (last dim contiguous).
+
+    Returns (sigma (batch, q) descending, vec (batch, nvec, max(n1, n2)), info (batch,) int32):
+    vec rows are the long-side singular vectors (right if n1 <= n2, else left).
+    """
+    lib = N.require_gpu()
+    batch, n1, n2 = a.shape
+    assert a.stride(2) == 1
+    q, ln = min(n1, n2), max(n1, n2)
+    sigma = torch.empty((batch, q), dtype=F64, device=a.device)
+    vec = torch.empty((batch, nvec, ln), dtype=F64, device=a.device)
+    info = torch.empty((batch,), dtype=torch.int32, device=a.device)
+    if batch == 0:
+        return sigma, vec, info
+    wsb = int(lib.wt_svd_workspace_bytes(n1, n2, batch))
+    ws = torch.empty((wsb,), dtype=torch.uint8, device=a.device)
+    N.check(lib.wt_svd_jacobi_f64(_ptr(a), a.stride(1), a.stride(0), n1, n2, batch, _ptr(sigma),
+                                  _ptr(vec), nvec, _ptr(info), float(tol), int(max_sweeps),
+                                  _ptr(ws), wsb, _stream()), "wt_svd_jacobi_f64")
+    return sigma, vec, info
+
+
+def last_sweeps() -> int:
+    return int(N.load().wt_svd_last_sweeps())
+
+
+def raise_if_failed(info: torch.Tensor):
+    """Map K4 status to the reference's LAPACK error (numpy.linalg.LinAlgError)."""
+    if info.numel() and bool((info != 0).any()):
+        raise np.linalg.LinAlgError("SVD did not converge")
+
+
+def truncated_recon(a: torch.Tensor, sigma: torch.Tensor, vec: torch.Tensor, r: int,
+                    out: torch.Tensor | None = None, keep_t: bool = False):
+    """K5: rank-r reconstruction of every slice from the long-side vectors.
+
+    Right side (n1 <= n2): T = A V_r (n1 x r) and recon = T V_r^T.
+    Left side  (n1 >  n2): T = A^T U_r (n2 x r) and recon = U_r T^T.
+    Equal to U_r diag(s_r) V_r^T of decomposition.py:70-72.
+    """
+    n1, n2 = a.shape[1], a.shape[2]
+    vr = vec[:, :r, :]
+    if n1 <= n2:
+        t = gemm(a, vr, trans_b=True)                 # (batch, n1, r)
+        rec = gemm(t, vr, out=out)                    # (batch, n1, n2)
+    else:
+        t = gemm(a, vr, trans_a=True, trans_b=True)   # (batch, n2, r)
+        rec = gemm(vr, t, trans_a=True, trans_b=True, out=out)
+    return (rec, t) if keep_t else rec
+
+
+def pinv_blocks(a: torch.Tensor, sigma: torch.Tensor, vec: torch.Tensor, tol: float,
+                out: torch.Tensor | None = None) -> torch.Tensor:
+    """K7: per-slice Moore-Penrose inverse (n2 x n1) with cutoff tol*sigma_max.
+
+    decomposition.py:157-163: A+ = V diag(s+) U^T, s+ = 1/s for s > tol*s_max.
+    Right side: A+ = V (A V)^T weighted by s+^2; left side: A+ = (A^T U) s+^2 U^T.
+    """
+    n1, n2 = a.shape[1], a.shape[2]
+    if n1 <= n2:
+        t = gemm(a, vec, trans_b=True)                # (batch, n1, q) = A V
+        scale_cols(t, sigma, N.SCALE_PINV2, tol)
+        return gemm(vec, t, trans_a=True, trans_b=True, out=out)  # (batch, n2, n1)
+    t = gemm(a, vec, trans_a=True, trans_b=True)      # (batch, n2, q) = A^T U
+    scale_cols(t, sigma, N.SCALE_PINV2, tol)
+    return gemm(t, vec, out=out)                      # (batch, n2, n1)
+
+
+# ------------------------------------------------------------ reductions ----
+
+def band_sums(x: torch.Tensor, y: torch.Tensor | None, mode: int) -> torch.Tensor:
+    """Per-band sums over a spatial (n1, n2, p) tensor (deterministic)."""
+    lib = N.require_gpu()
+    n1, n2, p = x.shape
+    nt = n1 * n2
+    scratch = int(lib.wt_slice_reduce_scratch(nt, p)) // 8
+    out = torch.empty((scratch,), dtype=F64, device=x.device)
+    N.check(lib.wt_slice_reduce_f64(_ptr(x), _ptr(y), nt, p, mode, _ptr(out), _stream()),
+            "wt_slice_reduce_f64")
+    return out[:p]

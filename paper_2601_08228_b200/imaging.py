@@ -1,0 +1,99 @@
+"""Hyperspectral application helpers around the hot path (the
+reference ships no code for them, so parity is against the SPEC/PAPER formulas).
+
+* ``psnr`` / ``ssim``: PAPER.md:876-887 verbatim (PSNR numerator MPP, not MPP^2;
+  SSIM with global per-band moments, population variance), reduced on the GPU
+  with the deterministic band-reduction kernel.
+* ``blur`` / ``deblur``: A_V *_w X *_w A_H^T and its pseudo-inverse sandwich
+  (SPEC.md:485-503).
+"""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import torch
+
+from . import engine as E
+from .algebra import w_product
+from .decomposition import pinv_w, sp_pinv_w
+from .lifting import _is_dev
+from .tensor import transpose
+
+
+def _moments(x: torch.Tensor, y: torch.Tensor):
+    n = x.shape[0] * x.shape[1]
+    mx = E.band_sums(x, None, 2) / n
+    my = E.band_sums(y, None, 2) / n
+    xc = (x - mx).contiguous()
+    yc = (y - my).contiguous()
+    vx = E.band_sums(xc, None, 0) / n
+    vy = E.band_sums(yc, None, 0) / n
+    cxy = E.band_sums(xc, yc, 3) / n
+    return mx, my, vx, vy, cxy
+
+
+def _mpp(x, y, mpp):
+    if mpp is not None:
+        return float(mpp)
+    return max(float(x.max().item()), float(y.max().item()))
+
+
+def psnr(x1, x2, mpp=None) -> float:
+    """10 log10(n1 n2 p MPP / ||x1 - x2||_F^2); +inf for identical inputs."""
+    x = E.as_device(x1)
+    y = E.as_device(x2)
+    m = _mpp(x, y, mpp)
+    err = float(E.band_sums(x, y, 1).sum().item())
+    if err == 0.0:
+        return float("inf")
+    return 10.0 * math.log10(x.numel() * m / err)
+
+
+def ssim(x1, x2, mpp=None) -> float:
+    """Band-averaged global SSIM, c1 = (0.01 MPP)^2, c2 = (0.03 MPP)^2."""
+    x = E.as_device(x1)
+    y = E.as_device(x2)
+    m = _mpp(x, y, mpp)
+    c1, c2 = (0.01 * m) ** 2, (0.03 * m) ** 2
+    mx, my, vx, vy, cxy = _moments(x, y)
+    per_band = ((2 * mx * my + c1) * (2 * cxy + c2)) / ((mx * mx + my * my + c1) * (vx + vy + c2))
+    return float(per_band.mean().item())
+
+
+def blur_vectors(b_v: int, b_h: int, n1: int, n2: int):
+    """c_v(i) = (b_v - i) / (3 b_v) for i < b_v, else 0."""
+    i1 = np.arange(n1, dtype=np.float64)
+    i2 = np.arange(n2, dtype=np.float64)
+    cv = np.where(i1 < b_v, (b_v - i1) / (3.0 * b_v), 0.0)
+    ch = np.where(i2 < b_h, (b_h - i2) / (3.0 * b_h), 0.0)
+    return cv, ch
+
+
+def blur_operator(b_v: int, b_h: int, n1: int, n2: int, p: int):
+    """Slice-constant Toeplitz operators A_V (n1 x n1 x p), A_H (n2 x n2 x p)."""
+    cv, ch = blur_vectors(b_v, b_h, n1, n2)
+    av = cv[np.abs(np.subtract.outer(np.arange(n1), np.arange(n1)))]
+    ah = ch[np.abs(np.subtract.outer(np.arange(n2), np.arange(n2)))]
+    return (np.ascontiguousarray(np.broadcast_to(av[:, :, None], av.shape + (p,))),
+            np.ascontiguousarray(np.broadcast_to(ah[:, :, None], ah.shape + (p,))))
+
+
+def blur(x, a_v, a_h, levels):
+    """A_V *_w X *_w A_H^T."""
+    return w_product(w_product(a_v, x, levels), transpose(a_h), levels)
+
+
+def deblur(b, a_v, a_h, levels, method="w", tol=1e-12):
+    """A_V^+ *_w B *_w (A_H^T)^+ with the w (pinv_w) or spw (sp_pinv_w) inverse."""
+    inv = pinv_w if method == "w" else sp_pinv_w
+    if method not in ("w", "spw"):
+        raise ValueError(f"unknown deblur method {method!r}")
+    left = inv(a_v, levels, tol)
+    right = inv(transpose(a_h), levels, tol)
+    return w_product(w_product(left, b, levels), right, levels)
+
+
+def to_host(x):
+    return x.cpu().numpy() if _is_dev(x) else np.asarray(x)

@@ -1,0 +1,110 @@
+"""K3 (DMMA GEMM) and the w-product on the GPU against the reference fixtures
+and the oracle.  Bar (BASELINE.json north_star): w-product within 1e-10
+relative Frobenius error in float64."""
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2601_08228_b200 as W
+from paper_2601_08228_b200 import engine as E
+from oracle import wten_oracle as O
+from wt_helpers import relerr
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-10
+
+
+def test_config1_against_reference_fixture(golden):
+    g = golden("w_product.npz")
+    rng = np.random.default_rng(0)
+    a = rng.uniform(-1, 1, (64, 48, 32))
+    b = rng.uniform(-1, 1, (48, 40, 32))
+    c = W.w_product(a, b, 1)
+    assert isinstance(c, np.ndarray) and c.shape == (64, 40, 32)
+    assert relerr(c, g["cfg1_c"]) < TOL
+    # transform round trips of both operands (config 1 parity list)
+    for t in (a, b):
+        assert relerr(W.inverse_w(W.forward_w(t, 1)), t) < 1e-15
+    for L in (1, 2, 3):
+        assert relerr(W.w_product(g["small_a"], g["small_b"], L), g[f"small_c_L{L}"]) < TOL
+
+
+@pytest.mark.parametrize("ta", [False, True])
+@pytest.mark.parametrize("tb", [False, True])
+@pytest.mark.parametrize("mnk", [(1, 1, 1), (7, 5, 3), (33, 65, 17), (130, 129, 200), (256, 256, 64)])
+def test_gemm_all_orientations(ta, tb, mnk):
+    M, Nn, K = mnk
+    rng = np.random.default_rng(M * 7 + Nn * 3 + K)
+    batch = 3
+    a = rng.standard_normal((batch, K, M) if ta else (batch, M, K))
+    b = rng.standard_normal((batch, Nn, K) if tb else (batch, K, Nn))
+    c0 = rng.standard_normal((batch, M, Nn))
+    opa = np.swapaxes(a, 1, 2) if ta else a
+    opb = np.swapaxes(b, 1, 2) if tb else b
+    want = 0.5 * (opa @ opb) - 2.0 * c0
+    cd = torch.from_numpy(c0).cuda()
+    E.gemm(torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda(), ta, tb, alpha=0.5, beta=-2.0, out=cd)
+    assert relerr(cd.cpu().numpy(), want) < 1e-14
+
+
+def test_gemm_config5_size():
+    rng = np.random.default_rng(9)
+    a = rng.standard_normal((128, 512, 512))
+    b = rng.standard_normal((128, 512, 512))
+    c = E.gemm(torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()).cpu().numpy()
+    assert relerr(c, a @ b) < 1e-14
+
+
+def test_w_product_matches_oracle_config5_shape():
+    rng = np.random.default_rng(11)
+    a = rng.standard_normal((512, 512, 128))
+    b = rng.standard_normal((512, 512, 128))
+    want = O.w_product(a, b, 3)
+    got = W.w_product(torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda(), 3)
+    assert relerr(got.cpu().numpy(), want) < TOL
+
+
+def test_slicewise_transpose_identity_face_product():
+    rng = np.random.default_rng(12)
+    a = rng.standard_normal((6, 4, 8))
+    b = rng.standard_normal((4, 5, 8))
+    assert relerr(W.slicewise_matmul(a, b), O.face_matmul(a, b)) < 1e-15
+    assert np.array_equal(W.transpose(a), O.transpose(a))
+    ident = W.identity_tensor(6, 8, 3)
+    assert relerr(W.w_product(ident, a, 3), a) < 1e-14
+    pa, pb = W.forward_w(a, 2), W.forward_w(b, 2)
+    fp = W.face_product(pa, pb)
+    assert relerr(W.inverse_w(fp), O.w_product(a, b, 2)) < 1e-14
+    # device pyramids take the packed fast path
+    da, db = W.forward_w(torch.from_numpy(a).cuda(), 2), W.forward_w(torch.from_numpy(b).cuda(), 2)
+    assert relerr(W.inverse_w(W.face_product(da, db)).cpu().numpy(), O.w_product(a, b, 2)) < 1e-14
+
+
+def test_w_product_laws():
+    rng = np.random.default_rng(13)
+    a = rng.standard_normal((5, 4, 16))
+    b = rng.standard_normal((4, 6, 16))
+    c = rng.standard_normal((6, 3, 16))
+    for L in (1, 2, 4):
+        ab_c = W.w_product(W.w_product(a, b, L), c, L)
+        a_bc = W.w_product(a, W.w_product(b, c, L), L)
+        assert relerr(ab_c, a_bc) < 1e-12                      # associativity
+        lhs = W.transpose(W.w_product(a, b, L))
+        rhs = W.w_product(W.transpose(b), W.transpose(a), L)
+        assert relerr(lhs, rhs) < 1e-12                        # transpose reversal
+        assert relerr(W.w_product(2 * a + a, b, L), 3 * W.w_product(a, b, L)) < 1e-12
+
+
+def test_nan_propagates_silently_like_reference():
+    a = np.ones((3, 3, 4))
+    a[0, 0, 0] = np.nan
+    c = W.w_product(a, np.ones((3, 2, 4)), 1)
+    assert np.isnan(c).any()
+
+
+def test_determinism():
+    rng = np.random.default_rng(14)
+    a = torch.from_numpy(rng.standard_normal((96, 80, 64))).cuda()
+    b = torch.from_numpy(rng.standard_normal((80, 72, 64))).cuda()
+    assert torch.equal(W.w_product(a, b, 3), W.w_product(a, b, 3))

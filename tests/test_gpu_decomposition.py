@@ -1,0 +1,139 @@
+"""K4 (block-Jacobi SVD) + K5/K6/K7 epilogues on the GPU.
+
+Bars (BASELINE.json north_star): singular values and rank-k reconstructions
+within 1e-8 relative; sigma compared per slice as max|dsigma| / sigma_max.
+Singular vectors carry sign/rotation freedom, so U, V are checked through the
+invariants (U *_w S *_w V^T = recon, orthonormality), never entry-wise.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2601_08228_b200 as W
+from paper_2601_08228_b200 import engine as E
+from paper_2601_08228_b200 import synth
+from oracle import wten_oracle as O
+from wt_helpers import relerr
+from wt_paper_examples import MP, MP_A, MP_B
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-8
+
+
+def sigma_err(got, want):
+    got = np.asarray(got)
+    want = np.asarray(want)
+    scale = np.maximum(want[:, :1], 1e-300)
+    return float(np.max(np.abs(got - want) / scale)) if want.size else 0.0
+
+
+@pytest.mark.parametrize("name,r,L", [("sq", 3, 2), ("wide", 4, 3), ("tall", 2, 4)])
+def test_reference_fixtures(golden, name, r, L):
+    g = golden("decomposition.npz")
+    x = g[f"{name}_x"]
+    f, rec = W.w_svd(x, r, L)
+    assert [t for t, _ in f.sigma_table] == [f"d{j}" for j in range(1, L + 1)] + ["s"]
+    for tag, s in f.sigma_table:
+        assert sigma_err(s, g[f"{name}_sigma_{tag}"]) < 1e-12
+    assert relerr(rec, g[f"{name}_recon"]) < 1e-10
+    assert relerr(f.S, g[f"{name}_S"]) < 1e-12
+    usv = W.w_product(W.w_product(f.U, f.S, L), W.transpose(f.V), L)
+    assert relerr(usv, rec) < 1e-10
+    assert abs(W.truncation_bound(f, r).bound - float(g[f"{name}_bound"])) < 1e-10
+    assert relerr(W.sp_w_svd(x, r, L), g[f"{name}_sp"]) < 1e-10
+
+
+def test_pinv_fixtures_and_counterexample(golden):
+    g = golden("decomposition.npz")
+    x = g["pinv_x"]
+    assert relerr(W.pinv_w(x, 3), g["pinv_L3_default"]) < 1e-10
+    assert relerr(W.pinv_w(x, 1, 1e-1), g["pinv_L1_tol1e-1"]) < 1e-10
+    assert relerr(W.sp_pinv_w(x, 2), g["sp_pinv_L2"]) < 1e-10
+    assert relerr(W.pinv_w_via_factors(x, 2), g["pinv_via_factors_L2"]) < 1e-9
+    assert np.array_equal(W.pinv_w(np.zeros((4, 5, 4)), 2), g["pinv_zero"])
+    # PAPER.md:604-704, printed values are exact
+    ab = W.w_product(MP_A, MP_B, 1)
+    c = W.pinv_w(ab, 1)
+    assert np.abs(c - MP["C"]).max() < 1e-12
+    d = W.w_product(W.pinv_w(MP_B, 1), W.pinv_w(MP_A, 1), 1)
+    assert np.abs(d - MP["D"]).max() < 1e-12
+
+
+@pytest.mark.parametrize("shape,r,L", [((40, 40, 8), 5, 3), ((30, 70, 4), 30, 2),
+                                       ((70, 30, 4), 7, 1), ((1, 9, 4), 1, 2), ((65, 33, 16), 33, 4)])
+def test_against_oracle_random(shape, r, L):
+    x = np.random.default_rng(sum(shape) + r).standard_normal(shape)
+    want = O.w_svd(x, r, L)
+    f, rec = W.w_svd(x, r, L)
+    for (t1, s1), (t2, s2) in zip(f.sigma_table, want["sigma_table"]):
+        assert t1 == t2 and sigma_err(s1, s2) < 1e-12
+    assert relerr(rec, want["recon"]) < 1e-10
+    assert relerr(W.sp_w_svd(x, r, L), O.sp_w_svd(x, r, L)) < 1e-10
+    assert relerr(W.pinv_w(x, L), O.pinv_w(x, L)) < 1e-9
+
+
+def test_penrose_identities():
+    x = np.random.default_rng(21).standard_normal((9, 6, 8))
+    L = 2
+    xp = W.pinv_w(x, L)
+    wp = lambda a, b: W.w_product(a, b, L)  # noqa: E731
+    assert relerr(wp(wp(x, xp), x), x) < 1e-10
+    assert relerr(wp(wp(xp, x), xp), xp) < 1e-10
+    axp = wp(x, xp)
+    assert relerr(W.transpose(axp), axp) < 1e-10
+    xpa = wp(xp, x)
+    assert relerr(W.transpose(xpa), xpa) < 1e-10
+
+
+def test_nan_raises_linalgerror_like_reference():
+    a = np.ones((3, 3, 4))
+    a[0, 0, 0] = np.nan
+    with pytest.raises(np.linalg.LinAlgError, match="SVD did not converge"):
+        W.w_svd(a, 1, 1)
+    with pytest.raises(np.linalg.LinAlgError, match="SVD did not converge"):
+        W.pinv_w(a, 1)
+
+
+def test_engine_svd_orthogonality_and_sort():
+    rng = np.random.default_rng(22)
+    a = torch.from_numpy(rng.standard_normal((5, 100, 300))).cuda()
+    sigma, vec, info = E.svd(a, 100)
+    assert int(info.abs().sum()) == 0
+    s = sigma.cpu().numpy()
+    assert np.all(np.diff(s, axis=1) <= 0)
+    v = vec.cpu().numpy()
+    gram = v @ np.swapaxes(v, 1, 2)
+    assert np.abs(gram - np.eye(100)).max() < 1e-12
+    want = np.linalg.svd(a.cpu().numpy(), compute_uv=False)
+    assert sigma_err(s, want) < 1e-13
+
+
+def test_config3_full_size():
+    """w-svd rank 20 of the 256x256x192 hyperspectral cube, L=3 (BASELINE config 3)."""
+    x = synth.hyperspectral_cube(256, 256, 192, endmembers=10, seed=0)
+    want = O.w_svd(x, 20, 3)
+    f, rec = W.w_svd(torch.from_numpy(x).cuda(), 20, 3)
+    for (t1, s1), (t2, s2) in zip(f.sigma_table, want["sigma_table"]):
+        assert t1 == t2 and sigma_err(s1.cpu().numpy(), s2) < TOL
+    assert relerr(rec.cpu().numpy(), want["recon"]) < TOL
+    assert relerr(f.S.cpu().numpy(), want["S"]) < TOL
+    assert abs(O.psnr(x, rec.cpu().numpy()) - O.psnr(x, want["recon"])) < 1e-6
+    assert abs(O.ssim(x, rec.cpu().numpy()) - O.ssim(x, want["recon"])) < 1e-6
+
+
+def test_config4_full_size():
+    """sp-w-svd rank 30 of the 1024x1024x256 cube, L=4 (BASELINE config 4)."""
+    x = synth.hyperspectral_cube(1024, 1024, 256, endmembers=10, seed=0)
+    want = O.sp_w_svd(x, 30, 4)
+    got = W.sp_w_svd(torch.from_numpy(x).cuda(), 30, 4).cpu().numpy()
+    assert relerr(got, want) < TOL
+    # piecewise constant in blocks of 2^(L-1) bands (finer details zeroed)
+    assert np.array_equal(got[..., 0::8], got[..., 7::8])
+
+
+def test_determinism():
+    x = torch.from_numpy(np.random.default_rng(23).standard_normal((64, 64, 32))).cuda()
+    r1 = W.sp_w_svd(x, 8, 2)
+    r2 = W.sp_w_svd(x, 8, 2)
+    assert torch.equal(r1, r2)
