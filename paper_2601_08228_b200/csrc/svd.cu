@@ -31,6 +31,8 @@ constexpr int RCH = 64;      // rows per streamed chunk
 constexpr int LDZ = RCH + 4; // chunk column pitch (doubles), = 4 mod 16: conflict-free frags
 constexpr int LDG = BW + 1;  // Gram / Q pitch
 constexpr int kThreads = 256;
+constexpr double kFloor = 8.0;   // rounding-floor multiple (see the convergence test)
+constexpr int kInnerSweeps = 16;
 
 struct SvdWs {
   double* X;        // batch * npad * mpad
@@ -71,10 +73,7 @@ struct PairSmem {
   double Z[2][BW * LDZ];
   double G[2][BW * LDG];
   double Q[2][BW * LDG];
-  double cs[BW][2];   // per index: (own coefficient c_i, partner coefficient o_i)
-  int partner[BW];
-  int rotated;
-  double off;
+  double warp_off[kThreads / 32];
 };
 
 __device__ __forceinline__ void load_chunk(double* Zs, const double* Xb, int64_t mpad, int colI,
@@ -136,91 +135,104 @@ __global__ void __launch_bounds__(kThreads) svd_pair_kernel(SvdWs ws, int64_t mp
     const int i = e / BW, j = e % BW;
     S.G[0][i * LDG + j] += S.G[1][i * LDG + j];
   }
-  if (tid == 0) S.off = 0.0;
   __syncthreads();
 
   // ---------------- 2. convergence test on this pair -----------------------
+  // Pair (i, j) is orthogonal enough when
+  //   |g_ij| <= tol * sqrt(g_ii g_jj) + kFloor * eps * sqrt(gmax * max(g_ii, g_jj)),
+  // the second term being the rounding floor of forming Z Q in FP64 (a small
+  // column cannot be made more orthogonal to a large one than eps * |z_max|).
+  // `off` is the largest |g_ij| / (that bound) * tol, so off < tol <=> converged.
+  double gmax = 0.0;
+#pragma unroll 4
+  for (int i = 0; i < BW; ++i) gmax = fmax(gmax, S.G[0][i * LDG + i]);
+  const double floor_c = kFloor * 2.220446049250313e-16 / tol;
   {
     double mx = 0.0;
     for (int e = tid; e < BW * BW; e += kThreads) {
       const int i = e / BW, j = e % BW;
       if (i < j) {
+        const double gii = S.G[0][i * LDG + i], gjj = S.G[0][j * LDG + j];
         const double gij = S.G[0][i * LDG + j];
-        const double d = S.G[0][i * LDG + i] * S.G[0][j * LDG + j];
+        const double den = sqrt(gii * gjj) + floor_c * sqrt(gmax * fmax(gii, gjj));
         double c = 0.0;
-        if (gij != 0.0) c = d > 0.0 ? fabs(gij) / sqrt(d) : INFINITY;
+        if (gij != 0.0) c = den > 0.0 ? fabs(gij) / den : INFINITY;
+        if (isnan(gii) || isnan(gjj)) c = gii + gjj;
         mx = nanmax(mx, c);
       }
     }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      mx = nanmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    }
-    if (lane == 0) {
-      // NaN-propagating max through the bit pattern (non-negative doubles order as uint64)
-      atomicMax(reinterpret_cast<unsigned long long*>(&S.off), (unsigned long long)__double_as_longlong(mx));
-    }
+    for (int o = 16; o > 0; o >>= 1) mx = nanmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if (lane == 0) S.warp_off[warp] = mx;
   }
   __syncthreads();
-  const double off = S.off;
+  double off = 0.0;
+#pragma unroll
+  for (int w = 0; w < kThreads / 32; ++w) off = nanmax(off, S.warp_off[w]);
+  // NaN-propagating max through the bit pattern (non-negative doubles order as uint64)
   if (tid == 0) atomicMax(&ws.offmax[b], (unsigned long long)__double_as_longlong(off));
   if (!(off >= tol)) return;  // converged pair (or NaN: recorded above, stop touching data)
-  if (isnan(off) || isinf(off)) return;
+  if (isinf(off)) return;
 
   // ---------------- 3. eigen-decomposition of G (cyclic parallel Jacobi) ----
+  // 16 groups of 16 threads; group g owns rotation pair g of every step, computes
+  // its (c, s) redundantly (no shared round trip), then applies G <- G J,
+  // Q <- Q J (columns p, q) and, after a barrier, G <- J^T G (rows p, q).
   for (int e = tid; e < BW * BW; e += kThreads) {
     const int i = e / BW, j = e % BW;
     S.Q[0][i * LDG + j] = (i == j) ? 1.0 : 0.0;
   }
   __syncthreads();
-  int cur = 0;
-  const double eps_in = 2.220446049250313e-16;
-  for (int sweep = 0; sweep < 20; ++sweep) {
-    if (tid == 0) S.rotated = 0;
-    __syncthreads();
-    for (int step = 0; step < BW - 1; ++step) {
-      const double* G = S.G[cur];
-      if (tid < BW / 2) {
-        int p = rr_index(tid, step, BW), q = rr_index(BW - 1 - tid, step, BW);
-        if (p > q) { int t = p; p = q; q = t; }
+  {
+    double* G = S.G[0];
+    double* Q = S.Q[0];
+    const int grp = tid >> 4, sub = tid & 15;
+    for (int sweep = 0; sweep < kInnerSweeps; ++sweep) {
+      int my_rot = 0;
+      for (int step = 0; step < BW - 1; ++step) {
+        int p = rr_index(grp, step, BW), q = rr_index(BW - 1 - grp, step, BW);
+        if (p > q) { const int t = p; p = q; q = t; }
         const double gpp = G[p * LDG + p], gqq = G[q * LDG + q], gpq = G[p * LDG + q];
+        const double den = sqrt(gpp * gqq) + floor_c * sqrt(gmax * fmax(gpp, gqq));
+        const bool rot = gpq != 0.0 && fabs(gpq) > tol * den;
+        __syncwarp();
         double c = 1.0, s = 0.0;
-        if (gpq != 0.0 && fabs(gpq) > eps_in * sqrt(gpp * gqq)) {
+        if (rot) {
           const double tau = (gqq - gpp) / (2.0 * gpq);
           const double t = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + hypot(1.0, tau));
           c = 1.0 / sqrt(1.0 + t * t);
           s = t * c;
-          S.rotated = 1;
+          my_rot = 1;
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {  // columns: G <- G J, Q <- Q J
+            const int i = sub + 16 * h;
+            const double a = G[i * LDG + p], bq = G[i * LDG + q];
+            G[i * LDG + p] = c * a - s * bq;
+            G[i * LDG + q] = s * a + c * bq;
+            const double qa = Q[i * LDG + p], qb = Q[i * LDG + q];
+            Q[i * LDG + p] = c * qa - s * qb;
+            Q[i * LDG + q] = s * qa + c * qb;
+          }
         }
-        S.partner[p] = q;
-        S.partner[q] = p;
-        S.cs[p][0] = c; S.cs[p][1] = -s;  // J[q][p] = -s
-        S.cs[q][0] = c; S.cs[q][1] = s;   // J[p][q] = +s
+        __syncthreads();
+        if (rot) {
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {  // rows: G <- J^T G
+            const int j = sub + 16 * h;
+            const double a = G[p * LDG + j], bq = G[q * LDG + j];
+            double np = c * a - s * bq, nq = s * a + c * bq;
+            if (j == q) np = 0.0;  // annihilated pair
+            if (j == p) nq = 0.0;
+            G[p * LDG + j] = np;
+            G[q * LDG + j] = nq;
+          }
+        }
+        __syncthreads();
       }
-      __syncthreads();
-      double* Gn = S.G[cur ^ 1];
-      const double* Qo = S.Q[cur];
-      double* Qn = S.Q[cur ^ 1];
-      for (int e = tid; e < BW * BW; e += kThreads) {
-        const int i = e / BW, j = e % BW;
-        const int pi = S.partner[i], pj = S.partner[j];
-        const double ci = S.cs[i][0], oi = S.cs[i][1], cj = S.cs[j][0], oj = S.cs[j][1];
-        // G' = J^T G J, summed in an order symmetric in (i, j)
-        const double t1 = ci * cj * G[i * LDG + j];
-        const double t4 = oi * oj * G[pi * LDG + pj];
-        const double t2 = ci * oj * G[i * LDG + pj];
-        const double t3 = oi * cj * G[pi * LDG + j];
-        double v = (t1 + t4) + (t2 + t3);
-        if (pi == j && i != j && oi != 0.0) v = 0.0;  // annihilated entry
-        Gn[i * LDG + j] = v;
-        // Q' = Q J (column operation)
-        Qn[i * LDG + j] = Qo[i * LDG + j] * cj + Qo[i * LDG + pj] * oj;
-      }
-      cur ^= 1;
-      __syncthreads();
+      if (!__syncthreads_or(my_rot)) break;
     }
-    if (!S.rotated) break;
   }
+  const int cur = 0;
 
   // ---------------- 4. Z <- Z Q, streamed, written back in place -----------
   // Q fragments cached in registers: b-frag for k-step kk, n-tile tn is
