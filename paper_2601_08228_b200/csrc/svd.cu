@@ -18,6 +18,8 @@
 //   Finally sigma_c = ||X_c|| and the columns are sorted descending; the
 //   normalised columns are the long-side singular vectors.
 // Everything is deterministic: fixed reduction orders, no floating atomics.
+#include <stdlib.h>
+
 #include <algorithm>
 
 #include "wt_common.cuh"
@@ -31,8 +33,8 @@ constexpr int RCH = 64;      // rows per streamed chunk
 constexpr int LDZ = RCH + 4; // chunk column pitch (doubles), = 4 mod 16: conflict-free frags
 constexpr int LDG = BW + 1;  // Gram / Q pitch
 constexpr int kThreads = 256;
-constexpr double kFloor = 8.0;   // rounding-floor multiple (see the convergence test)
-constexpr int kInnerSweeps = 16;
+constexpr double kFloorEps = 1e3 * 2.220446049250313e-16;  // null-column floor (see the test)
+constexpr int kMaxInnerSweeps = 16;
 
 struct SvdWs {
   double* X;        // batch * npad * mpad
@@ -74,6 +76,7 @@ struct PairSmem {
   double G[2][BW * LDG];
   double Q[2][BW * LDG];
   double warp_off[kThreads / 32];
+  int perm[BW];
 };
 
 __device__ __forceinline__ void load_chunk(double* Zs, const double* Xb, int64_t mpad, int colI,
@@ -88,8 +91,8 @@ __device__ __forceinline__ void load_chunk(double* Zs, const double* Xb, int64_t
   }
 }
 
-__global__ void __launch_bounds__(kThreads) svd_pair_kernel(SvdWs ws, int64_t mpad, int64_t npad,
-                                                            int round, double tol) {
+__global__ void __launch_bounds__(kThreads, 2) svd_pair_kernel(SvdWs ws, int64_t mpad, int64_t npad,
+                                                               int round, double tol, int inner_sweeps) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   PairSmem& S = *reinterpret_cast<PairSmem*>(smem_raw);
   const int b = blockIdx.y;
@@ -139,14 +142,15 @@ __global__ void __launch_bounds__(kThreads) svd_pair_kernel(SvdWs ws, int64_t mp
 
   // ---------------- 2. convergence test on this pair -----------------------
   // Pair (i, j) is orthogonal enough when
-  //   |g_ij| <= tol * sqrt(g_ii g_jj) + kFloor * eps * sqrt(gmax * max(g_ii, g_jj)),
-  // the second term being the rounding floor of forming Z Q in FP64 (a small
-  // column cannot be made more orthogonal to a large one than eps * |z_max|).
+  //   |g_ij| <= tol * sqrt(g_ii g_jj) + (1e3 eps)^2 * gmax,
+  // the second term only matters for numerically-null columns (norm below
+  // ~1e-13 |z_max|), whose directions are rounding noise and must not keep
+  // the iteration alive; real columns are held to the relative tolerance.
   // `off` is the largest |g_ij| / (that bound) * tol, so off < tol <=> converged.
   double gmax = 0.0;
 #pragma unroll 4
   for (int i = 0; i < BW; ++i) gmax = fmax(gmax, S.G[0][i * LDG + i]);
-  const double floor_c = kFloor * 2.220446049250313e-16 / tol;
+  const double floor_c = kFloorEps * kFloorEps / tol;
   {
     double mx = 0.0;
     for (int e = tid; e < BW * BW; e += kThreads) {
@@ -154,7 +158,7 @@ __global__ void __launch_bounds__(kThreads) svd_pair_kernel(SvdWs ws, int64_t mp
       if (i < j) {
         const double gii = S.G[0][i * LDG + i], gjj = S.G[0][j * LDG + j];
         const double gij = S.G[0][i * LDG + j];
-        const double den = sqrt(gii * gjj) + floor_c * sqrt(gmax * fmax(gii, gjj));
+        const double den = sqrt(gii * gjj) + floor_c * gmax;
         double c = 0.0;
         if (gij != 0.0) c = den > 0.0 ? fabs(gij) / den : INFINITY;
         if (isnan(gii) || isnan(gjj)) c = gii + gjj;
@@ -187,13 +191,13 @@ __global__ void __launch_bounds__(kThreads) svd_pair_kernel(SvdWs ws, int64_t mp
     double* G = S.G[0];
     double* Q = S.Q[0];
     const int grp = tid >> 4, sub = tid & 15;
-    for (int sweep = 0; sweep < kInnerSweeps; ++sweep) {
+    for (int sweep = 0; sweep < inner_sweeps; ++sweep) {
       int my_rot = 0;
       for (int step = 0; step < BW - 1; ++step) {
         int p = rr_index(grp, step, BW), q = rr_index(BW - 1 - grp, step, BW);
         if (p > q) { const int t = p; p = q; q = t; }
         const double gpp = G[p * LDG + p], gqq = G[q * LDG + q], gpq = G[p * LDG + q];
-        const double den = sqrt(gpp * gqq) + floor_c * sqrt(gmax * fmax(gpp, gqq));
+        const double den = sqrt(gpp * gqq) + floor_c * gmax;
         const bool rot = gpq != 0.0 && fabs(gpq) > tol * den;
         __syncwarp();
         double c = 1.0, s = 0.0;
@@ -232,6 +236,18 @@ __global__ void __launch_bounds__(kThreads) svd_pair_kernel(SvdWs ws, int64_t mp
       if (!__syncthreads_or(my_rot)) break;
     }
   }
+  // order the pair's columns by descending norm (block I gets the largest):
+  // keeps the cyclic sweeps close to sorted, which speeds outer convergence
+  if (tid < BW) {
+    const double di = S.G[0][tid * LDG + tid];
+    int rank = 0;
+    for (int j = 0; j < BW; ++j) {
+      const double dj = S.G[0][j * LDG + j];
+      rank += (dj > di) || (dj == di && j < tid);
+    }
+    S.perm[rank] = tid;
+  }
+  __syncthreads();
   const int cur = 0;
 
   // ---------------- 4. Z <- Z Q, streamed, written back in place -----------
@@ -243,7 +259,7 @@ __global__ void __launch_bounds__(kThreads) svd_pair_kernel(SvdWs ws, int64_t mp
 #pragma unroll
     for (int kk = 0; kk < 8; ++kk)
 #pragma unroll
-      for (int tn = 0; tn < 4; ++tn) qf[kk][tn] = Q[(kk * 4 + (lane & 3)) * LDG + tn * 8 + (lane >> 2)];
+      for (int tn = 0; tn < 4; ++tn) qf[kk][tn] = Q[(kk * 4 + (lane & 3)) * LDG + S.perm[tn * 8 + (lane >> 2)]];
   }
   load_chunk(S.Z[0], Xb, mpad, colI, colJ, 0);
   cp_async_commit();
@@ -450,11 +466,13 @@ extern "C" int wt_svd_jacobi_f64(const double* A, int64_t lda, int64_t strideA, 
   static int* h_pending = nullptr;
   if (!h_pending) WT_CUDA(cudaMallocHost(&h_pending, sizeof(int)));
   const int nb = (int)(L.npad / HB);
+  int inner = kMaxInnerSweeps;
+  if (const char* e = getenv("WT_SVD_INNER_SWEEPS")) inner = std::max(1, std::min(kMaxInnerSweeps, atoi(e)));
   bool hit_max = true;
   for (int sweep = 0; sweep < max_sweeps; ++sweep) {
     for (int round = 0; round < nb - 1; ++round) {
       svd_pair_kernel<<<dim3(nb / 2, (unsigned)batch), kThreads, sizeof(PairSmem), st>>>(
-          ws, L.mpad, L.npad, round, tol);
+          ws, L.mpad, L.npad, round, tol, inner);
     }
     if (int e = check_launch("svd_pair_kernel")) return e;
     WT_CUDA(cudaMemsetAsync(ws.pending, 0, sizeof(int), st));
