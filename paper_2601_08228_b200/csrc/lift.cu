@@ -18,6 +18,8 @@
 //     tubes: every packed slice row segment is a contiguous TQ*8-byte burst.
 //   * Inverse: the finished tube rows go back to HBM with bulk shared->global
 //     copies.
+#include <algorithm>
+
 #include "wt_common.cuh"
 
 namespace wt {
@@ -250,6 +252,11 @@ int validate(int64_t n1, int64_t n2, int64_t p, int levels, int layout, int64_t 
 }
 
 }  // namespace
+
+int lift_fwd_fast(const double* x, int64_t ntubes, int64_t p, int L, double* out,
+                  int64_t slice_base, uint64_t mask, cudaStream_t st);
+int lift_inv_fast(const double* pyr, int64_t ntubes, int64_t p, int L, double* y,
+                  int64_t slice_base, uint64_t mask, cudaStream_t st);
 }  // namespace wt
 
 using namespace wt;
@@ -261,6 +268,10 @@ extern "C" int wt_lift_fwd_f64(const double* x, int64_t n1, int64_t n2, int64_t 
   if (st) return st;
   LiftGeom g{n1 * n2, p, levels, 0, 0, 0, slice_base, layout, level_mask};
   if (g.ntubes == 0) return WT_OK;
+  if (layout == WT_LAYOUT_SLICE_MAJOR) {
+    st = lift_fwd_fast(x, g.ntubes, p, levels, out, slice_base, level_mask, (cudaStream_t)stream);
+    if (st != WT_ERR_UNSUPPORTED) return st;
+  }
   if ((st = plan_tiles(g))) return st;
   const bool bulk = (g.CT % 2 == 0) && (p % 2 == 0) && ((uintptr_t)x % 16 == 0);
   const size_t smem = (size_t)g.TQ * g.LDT * sizeof(double);
@@ -283,6 +294,10 @@ extern "C" int wt_lift_inv_f64(const double* pyr, int64_t n1, int64_t n2, int64_
   if (st) return st;
   LiftGeom g{n1 * n2, p, levels, 0, 0, 0, slice_base, layout, level_mask};
   if (g.ntubes == 0) return WT_OK;
+  if (layout == WT_LAYOUT_SLICE_MAJOR) {
+    st = lift_inv_fast(pyr, g.ntubes, p, levels, y, slice_base, level_mask, (cudaStream_t)stream);
+    if (st != WT_ERR_UNSUPPORTED) return st;
+  }
   if ((st = plan_tiles(g))) return st;
   const bool bulk = (g.CT % 2 == 0) && (p % 2 == 0) && ((uintptr_t)y % 16 == 0);
   const size_t smem = (size_t)g.TQ * g.LDT * sizeof(double);

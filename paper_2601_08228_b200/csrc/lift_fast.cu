@@ -1,0 +1,332 @@
+// K1 / K2 hot path: persistent, double-buffered lifting kernels for the
+// slice-major pyramid (the layout the face GEMM and the SVD consume).
+//
+// Same arithmetic as lift.cu (bit-exact with lifting.py:63-74); the difference
+// is the schedule:
+//   * persistent CTAs (grid = SMs x resident CTAs) walk the tiles; the next
+//     tile's input is in flight while the current one is lifted;
+//   * forward input tiles arrive by TMA bulk copies (one per tube row, mbarrier
+//     completion), inverse input rows by 16-byte cp.async;
+//   * levels are processed in register-blocked stages of up to 3 levels: a
+//     thread takes 2^W consecutive values of one tube, runs W levels in
+//     registers and emits every detail directly -- one barrier per stage
+//     instead of two per level (ncu: the per-level version was index-math and
+//     barrier bound at L = 8);
+//   * the tile height TQ (tubes) is a compile-time constant, so every index
+//     split is a shift/mask; consecutive threads own consecutive tubes, so each
+//     packed slice row is written / read as TQ*8-byte bursts.
+#include <algorithm>
+
+#include "wt_common.cuh"
+
+namespace wt {
+namespace fast {
+
+constexpr int kT = 256;
+constexpr int kMaxElems = 4096;  // TQ * CT per tile (32 KB)
+
+struct FGeom {
+  int64_t ntubes, p;
+  int L, CT;
+  int LDT;         // forward: tube-major tile pitch (CT + 2)
+  int LDA0, LDA1;  // stage buffers: CT/8 + 2, CT/64 + 2
+  int64_t slice_base;
+  uint64_t mask;
+  uint32_t nqt, ntiles;
+};
+
+__device__ __forceinline__ int64_t doff(int64_t p, int j) { return p - (p >> (j - 1)); }
+__device__ __forceinline__ int64_t soff(int64_t p, int L) { return p - (p >> L); }
+
+template <int TQ>
+__device__ __forceinline__ void tile_at(const FGeom& g, uint32_t t, int64_t& q0, int& tq, int64_t& t0) {
+  const uint32_t qt = t % g.nqt, ct = t / g.nqt;
+  q0 = (int64_t)qt * TQ;
+  tq = (int)(g.ntubes - q0 < TQ ? g.ntubes - q0 : TQ);
+  t0 = (int64_t)ct * g.CT;
+}
+
+// ------------------------------------------------------------- forward ----
+// W levels after level l0 on `len` smooth values per tube held in src (pitch ps).
+template <int TQ, int W>
+__device__ __forceinline__ void fwd_stage(const double* src, int ps, double* dst, int pd, int l0,
+                                          int len, const FGeom& g, double* __restrict__ out,
+                                          int64_t q0, int tq, int64_t t0) {
+  constexpr int V = 1 << W;
+  const int items = TQ * (len >> W);
+  const bool last = (l0 + W == g.L);
+  for (int e = threadIdx.x; e < items; e += kT) {
+    const int r = e & (TQ - 1), c = e / TQ;
+    if (r >= tq) continue;
+    double v[V];
+#pragma unroll
+    for (int i = 0; i < V; i += 2) {
+      const double2 t2 = *reinterpret_cast<const double2*>(src + r * ps + c * V + i);
+      v[i] = t2.x;
+      v[i + 1] = t2.y;
+    }
+#pragma unroll
+    for (int w = 0; w < W; ++w) {
+      const int lev = l0 + w + 1;
+      const int n = V >> (w + 1);
+      const bool want = (g.mask >> lev) & 1;
+      double* o = out + (doff(g.p, lev) + (t0 >> lev) + (int64_t)c * n - g.slice_base) * g.ntubes + q0 + r;
+#pragma unroll
+      for (int i = 0; i < (V >> 1); ++i) {
+        if (i < n) {
+          const double d = __dsub_rn(v[2 * i], v[2 * i + 1]);
+          const double s = __dadd_rn(v[2 * i + 1], __dmul_rn(d, 0.5));
+          if (want) o[(int64_t)i * g.ntubes] = d;
+          v[i] = s;
+        }
+      }
+    }
+    if (last) {
+      if (g.mask & 1) out[(soff(g.p, g.L) + (t0 >> g.L) + c - g.slice_base) * g.ntubes + q0 + r] = v[0];
+    } else {
+      dst[r * pd + c] = v[0];
+    }
+  }
+}
+
+template <int TQ>
+__global__ void __launch_bounds__(kT) fwd_persistent(const double* __restrict__ x,
+                                                     double* __restrict__ out, FGeom g) {
+  extern __shared__ __align__(128) double sm[];
+  __shared__ __align__(8) uint64_t bar[2];
+  double* tiles[2] = {sm, sm + TQ * g.LDT};
+  double* aux[2] = {sm + 2 * TQ * g.LDT, sm + 2 * TQ * g.LDT + TQ * g.LDA0};
+  const int lda[2] = {g.LDA0, g.LDA1};
+  if (threadIdx.x == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  auto issue = [&](uint32_t t, int buf) {
+    if (threadIdx.x < 32) {
+      int64_t q0, t0;
+      int tq;
+      tile_at<TQ>(g, t, q0, tq, t0);
+      if (threadIdx.x == 0) mbar_expect_tx(&bar[buf], (uint32_t)(tq * g.CT * 8));
+      __syncwarp();
+      for (int r = threadIdx.x; r < tq; r += 32)
+        bulk_g2s(tiles[buf] + r * g.LDT, x + (q0 + r) * g.p + t0, (uint32_t)(g.CT * 8), &bar[buf]);
+    }
+  };
+  uint32_t t = blockIdx.x;
+  if (t < g.ntiles) issue(t, 0);
+  for (int i = 0; t < g.ntiles; ++i, t += gridDim.x) {
+    const int buf = i & 1;
+    if (t + gridDim.x < g.ntiles) issue(t + gridDim.x, buf ^ 1);
+    mbar_wait(&bar[buf], (i >> 1) & 1);
+    int64_t q0, t0;
+    int tq;
+    tile_at<TQ>(g, t, q0, tq, t0);
+    const double* src = tiles[buf];
+    int ps = g.LDT, len = g.CT, l0 = 0, stage = 0;
+    while (l0 < g.L) {
+      const int W = min(3, g.L - l0);
+      double* dst = aux[stage & 1];
+      const int pd = lda[stage & 1];
+      if (W == 3) fwd_stage<TQ, 3>(src, ps, dst, pd, l0, len, g, out, q0, tq, t0);
+      else if (W == 2) fwd_stage<TQ, 2>(src, ps, dst, pd, l0, len, g, out, q0, tq, t0);
+      else fwd_stage<TQ, 1>(src, ps, dst, pd, l0, len, g, out, q0, tq, t0);
+      l0 += W;
+      len >>= W;
+      if (l0 < g.L) {
+        __syncthreads();
+        src = dst;
+        ps = pd;
+        ++stage;
+      }
+    }
+    __syncthreads();  // tile buffer `buf` is refilled two iterations later
+  }
+}
+
+// ------------------------------------------------------------- inverse ----
+// Tile-local rows of the prefetched slice-major input follow the packed order
+// [d1 | ... | dL | sL] with the tile's CT bands in place of p.
+__device__ __forceinline__ int drow(int CT, int j) { return CT - (CT >> (j - 1)); }
+
+// Levels hi .. hi-W+1: each thread expands one s_hi value into 2^W values of
+// s_{hi-W} using the prefetched details; the final stage (down to level 1)
+// stores the 2^W consecutive bands straight to y.
+template <int TQ, int W>
+__device__ __forceinline__ void inv_stage(const double* I, const double* ssrc, int pss, bool s_in,
+                                          double* dst, int pd, int hi, const FGeom& g,
+                                          double* __restrict__ y, int64_t q0, int tq, int64_t t0) {
+  constexpr int V = 1 << W;
+  const int CT = g.CT;
+  const int nval = CT >> hi;
+  const int items = TQ * nval;
+  const bool final_stage = (hi - W == 0);
+  const bool have_s = g.mask & 1;
+  const int srow = CT - (CT >> g.L);
+  for (int e = threadIdx.x; e < items; e += kT) {
+    const int r = e & (TQ - 1), c = e / TQ;
+    if (r >= tq) continue;
+    double v[V];
+    v[0] = s_in ? (have_s ? I[(srow + c) * TQ + r] : 0.0) : ssrc[r * pss + c];
+#pragma unroll
+    for (int w = 0; w < W; ++w) {
+      const int lev = hi - w;
+      const int n = 1 << w;
+      const bool have_d = (g.mask >> lev) & 1;
+      const double* dr = I + (drow(CT, lev) + c * n) * TQ + r;
+#pragma unroll
+      for (int i = (V >> 1) - 1; i >= 0; --i) {
+        if (i < n) {
+          const double d = have_d ? dr[i * TQ] : 0.0;
+          const double x1 = __dsub_rn(v[i], __dmul_rn(d, 0.5));
+          v[2 * i] = __dadd_rn(d, x1);
+          v[2 * i + 1] = x1;
+        }
+      }
+    }
+    double* o = final_stage ? y + (q0 + r) * g.p + t0 + (int64_t)c * V : dst + r * pd + c * V;
+#pragma unroll
+    for (int i = 0; i < V; i += 2) *reinterpret_cast<double2*>(o + i) = make_double2(v[i], v[i + 1]);
+  }
+}
+
+template <int TQ>
+__global__ void __launch_bounds__(kT) inv_persistent(const double* __restrict__ pyr,
+                                                     double* __restrict__ y, FGeom g) {
+  extern __shared__ __align__(128) double sm[];
+  const int CT = g.CT;
+  double* in[2] = {sm, sm + CT * TQ};
+  double* aux[2] = {sm + 2 * CT * TQ, sm + 2 * CT * TQ + TQ * g.LDA0};
+  constexpr int CPR = TQ / 2;  // 16-byte chunks per row
+  auto issue = [&](uint32_t t, int buf) {
+    int64_t q0, t0;
+    int tq;
+    tile_at<TQ>(g, t, q0, tq, t0);
+    double* dstb = in[buf];
+    for (int j = 1; j <= g.L + 1; ++j) {
+      const bool smooth = j > g.L;
+      if (!((g.mask >> (smooth ? 0 : j)) & 1)) continue;
+      const int rows = smooth ? (CT >> g.L) : (CT >> j);
+      const int row0 = smooth ? CT - (CT >> g.L) : drow(CT, j);
+      const int64_t s0 = smooth ? soff(g.p, g.L) + (t0 >> g.L) : doff(g.p, j) + (t0 >> j);
+      const double* base = pyr + (s0 - g.slice_base) * g.ntubes + q0;
+      for (int e = threadIdx.x; e < rows * CPR; e += kT) {
+        const int rr = e / CPR, v = (e % CPR) * 2;
+        const bool ok = v < tq;
+        cp_async_zfill<16>(dstb + (row0 + rr) * TQ + v, base + (int64_t)rr * g.ntubes + (ok ? v : 0), ok);
+      }
+    }
+    cp_async_commit();
+  };
+  uint32_t t = blockIdx.x;
+  if (t < g.ntiles) issue(t, 0);
+  else cp_async_commit();
+  for (int i = 0; t < g.ntiles; ++i, t += gridDim.x) {
+    const int buf = i & 1;
+    if (t + gridDim.x < g.ntiles) issue(t + gridDim.x, buf ^ 1);
+    else cp_async_commit();
+    cp_async_wait<1>();
+    __syncthreads();
+    int64_t q0, t0;
+    int tq;
+    tile_at<TQ>(g, t, q0, tq, t0);
+    const double* I = in[buf];
+    int hi = g.L, stage = 0;
+    const double* ssrc = nullptr;
+    int pss = 0;
+    while (hi > 0) {
+      const int W = (hi - 1) % 3 + 1;  // top stage absorbs the remainder: final stage is 3 wide
+      double* dst = aux[stage & 1];
+      const int pd = g.LDA0;
+      const bool s_in = (hi == g.L);
+      if (W == 3) inv_stage<TQ, 3>(I, ssrc, pss, s_in, dst, pd, hi, g, y, q0, tq, t0);
+      else if (W == 2) inv_stage<TQ, 2>(I, ssrc, pss, s_in, dst, pd, hi, g, y, q0, tq, t0);
+      else inv_stage<TQ, 1>(I, ssrc, pss, s_in, dst, pd, hi, g, y, q0, tq, t0);
+      hi -= W;
+      if (hi > 0) {
+        __syncthreads();
+        ssrc = dst;
+        pss = pd;
+        ++stage;
+      }
+    }
+    __syncthreads();  // input buffer / stage buffers are reused by later tiles
+  }
+  cp_async_wait<0>();
+}
+
+bool plan(FGeom& g, int& TQ) {
+  const int64_t unit = (int64_t)1 << g.L;
+  const int64_t munits = g.p / unit;
+  for (int tq = 16; tq >= 2; tq >>= 1) {
+    const int64_t cap = kMaxElems / tq;
+    if (unit > cap) continue;
+    int64_t best = 0;
+    for (int64_t d = 1; d <= munits && unit * d <= cap; ++d)
+      if (munits % d == 0) best = d;
+    TQ = tq;
+    g.CT = (int)(unit * best);
+    g.LDT = g.CT + 2;
+    g.LDA0 = std::max(2, g.CT / 8) + 2;
+    g.LDA1 = std::max(2, g.CT / 64) + 2;
+    const int64_t nqt = (g.ntubes + tq - 1) / tq;
+    const int64_t ntiles = nqt * (g.p / g.CT);
+    if (ntiles >= (1LL << 31)) return false;
+    g.nqt = (uint32_t)nqt;
+    g.ntiles = (uint32_t)ntiles;
+    return true;
+  }
+  return false;
+}
+
+template <typename K>
+int launch(K kern, size_t smem, uint32_t ntiles, cudaStream_t st, const double* a, double* b,
+           const FGeom& g, const char* what) {
+  WT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kT, smem) != cudaSuccess || per_sm < 1)
+    per_sm = 1;
+  const int grid = (int)std::min<int64_t>(ntiles, (int64_t)num_sms() * per_sm);
+  kern<<<grid, kT, smem, st>>>(a, b, g);
+  return check_launch(what);
+}
+
+}  // namespace fast
+
+// Returns WT_ERR_UNSUPPORTED when the fast path does not apply (caller falls back).
+int lift_fwd_fast(const double* x, int64_t ntubes, int64_t p, int L, double* out,
+                  int64_t slice_base, uint64_t mask, cudaStream_t st) {
+  using namespace fast;
+  if (L < 1 || p % 2 || (uintptr_t)x % 16) return WT_ERR_UNSUPPORTED;
+  FGeom g{ntubes, p, L, 0, 0, 0, 0, slice_base, mask, 0, 0};
+  int TQ = 0;
+  if (!plan(g, TQ)) return WT_ERR_UNSUPPORTED;
+  const size_t smem = ((size_t)2 * TQ * g.LDT + (size_t)TQ * (g.LDA0 + g.LDA1)) * sizeof(double);
+  switch (TQ) {
+    case 16: return launch(fwd_persistent<16>, smem, g.ntiles, st, x, out, g, "wt_lift_fwd_f64");
+    case 8: return launch(fwd_persistent<8>, smem, g.ntiles, st, x, out, g, "wt_lift_fwd_f64");
+    case 4: return launch(fwd_persistent<4>, smem, g.ntiles, st, x, out, g, "wt_lift_fwd_f64");
+    default: return launch(fwd_persistent<2>, smem, g.ntiles, st, x, out, g, "wt_lift_fwd_f64");
+  }
+}
+
+int lift_inv_fast(const double* pyr, int64_t ntubes, int64_t p, int L, double* y,
+                  int64_t slice_base, uint64_t mask, cudaStream_t st) {
+  using namespace fast;
+  if (L < 1 || p % 2 || ntubes % 2 || (uintptr_t)y % 16 || (uintptr_t)pyr % 16)
+    return WT_ERR_UNSUPPORTED;
+  FGeom g{ntubes, p, L, 0, 0, 0, 0, slice_base, mask, 0, 0};
+  int TQ = 0;
+  if (!plan(g, TQ)) return WT_ERR_UNSUPPORTED;
+  const size_t smem = ((size_t)2 * g.CT * TQ + (size_t)2 * TQ * g.LDA0) * sizeof(double);
+  if (smem > 200 * 1024) return WT_ERR_UNSUPPORTED;
+  switch (TQ) {
+    case 16: return launch(inv_persistent<16>, smem, g.ntiles, st, pyr, y, g, "wt_lift_inv_f64");
+    case 8: return launch(inv_persistent<8>, smem, g.ntiles, st, pyr, y, g, "wt_lift_inv_f64");
+    case 4: return launch(inv_persistent<4>, smem, g.ntiles, st, pyr, y, g, "wt_lift_inv_f64");
+    default: return launch(inv_persistent<2>, smem, g.ntiles, st, pyr, y, g, "wt_lift_inv_f64");
+  }
+}
+
+}  // namespace wt
