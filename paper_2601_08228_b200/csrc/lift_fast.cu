@@ -39,7 +39,7 @@ __device__ __forceinline__ int64_t doff(int64_t p, int j) { return p - (p >> (j 
 __device__ __forceinline__ int64_t soff(int64_t p, int L) { return p - (p >> L); }
 
 template <int TQ>
-__device__ __forceinline__ void tile_at(const FGeom& g, uint32_t t, int64_t& q0, int& tq, int64_t& t0) {
+__device__ __forceinline__ void tile_at(const FGeom g, uint32_t t, int64_t& q0, int& tq, int64_t& t0) {
   const uint32_t qt = t % g.nqt, ct = t / g.nqt;
   q0 = (int64_t)qt * TQ;
   tq = (int)(g.ntubes - q0 < TQ ? g.ntubes - q0 : TQ);
@@ -50,7 +50,7 @@ __device__ __forceinline__ void tile_at(const FGeom& g, uint32_t t, int64_t& q0,
 // W levels after level l0 on `len` smooth values per tube held in src (pitch ps).
 template <int TQ, int W>
 __device__ __forceinline__ void fwd_stage(const double* src, int ps, double* dst, int pd, int l0,
-                                          int len, const FGeom& g, double* __restrict__ out,
+                                          int len, const FGeom g, double* __restrict__ out,
                                           int64_t q0, int tq, int64_t t0) {
   constexpr int V = 1 << W;
   const int items = TQ * (len >> W);
@@ -94,9 +94,10 @@ __global__ void __launch_bounds__(kT) fwd_persistent(const double* __restrict__ 
                                                      double* __restrict__ out, FGeom g) {
   extern __shared__ __align__(128) double sm[];
   __shared__ __align__(8) uint64_t bar[2];
-  double* tiles[2] = {sm, sm + TQ * g.LDT};
-  double* aux[2] = {sm + 2 * TQ * g.LDT, sm + 2 * TQ * g.LDT + TQ * g.LDA0};
-  const int lda[2] = {g.LDA0, g.LDA1};
+  // pointer arithmetic on `sm` (not arrays of pointers) keeps every access LDS/STS
+  const int tile_sz = TQ * g.LDT;
+  double* const aux0 = sm + 2 * tile_sz;
+  double* const aux1 = aux0 + TQ * g.LDA0;
   if (threadIdx.x == 0) {
     mbar_init(&bar[0], 1);
     mbar_init(&bar[1], 1);
@@ -111,7 +112,7 @@ __global__ void __launch_bounds__(kT) fwd_persistent(const double* __restrict__ 
       if (threadIdx.x == 0) mbar_expect_tx(&bar[buf], (uint32_t)(tq * g.CT * 8));
       __syncwarp();
       for (int r = threadIdx.x; r < tq; r += 32)
-        bulk_g2s(tiles[buf] + r * g.LDT, x + (q0 + r) * g.p + t0, (uint32_t)(g.CT * 8), &bar[buf]);
+        bulk_g2s(sm + buf * tile_sz + r * g.LDT, x + (q0 + r) * g.p + t0, (uint32_t)(g.CT * 8), &bar[buf]);
     }
   };
   uint32_t t = blockIdx.x;
@@ -123,12 +124,12 @@ __global__ void __launch_bounds__(kT) fwd_persistent(const double* __restrict__ 
     int64_t q0, t0;
     int tq;
     tile_at<TQ>(g, t, q0, tq, t0);
-    const double* src = tiles[buf];
+    const double* src = sm + buf * tile_sz;
     int ps = g.LDT, len = g.CT, l0 = 0, stage = 0;
     while (l0 < g.L) {
       const int W = min(3, g.L - l0);
-      double* dst = aux[stage & 1];
-      const int pd = lda[stage & 1];
+      double* dst = (stage & 1) ? aux1 : aux0;
+      const int pd = (stage & 1) ? g.LDA1 : g.LDA0;
       if (W == 3) fwd_stage<TQ, 3>(src, ps, dst, pd, l0, len, g, out, q0, tq, t0);
       else if (W == 2) fwd_stage<TQ, 2>(src, ps, dst, pd, l0, len, g, out, q0, tq, t0);
       else fwd_stage<TQ, 1>(src, ps, dst, pd, l0, len, g, out, q0, tq, t0);
@@ -155,7 +156,7 @@ __device__ __forceinline__ int drow(int CT, int j) { return CT - (CT >> (j - 1))
 // stores the 2^W consecutive bands straight to y.
 template <int TQ, int W>
 __device__ __forceinline__ void inv_stage(const double* I, const double* ssrc, int pss, bool s_in,
-                                          double* dst, int pd, int hi, const FGeom& g,
+                                          double* dst, int pd, int hi, const FGeom g,
                                           double* __restrict__ y, int64_t q0, int tq, int64_t t0) {
   constexpr int V = 1 << W;
   const int CT = g.CT;
@@ -185,9 +186,15 @@ __device__ __forceinline__ void inv_stage(const double* I, const double* ssrc, i
         }
       }
     }
-    double* o = final_stage ? y + (q0 + r) * g.p + t0 + (int64_t)c * V : dst + r * pd + c * V;
+    if (final_stage) {
+      double* o = y + (q0 + r) * g.p + t0 + (int64_t)c * V;
 #pragma unroll
-    for (int i = 0; i < V; i += 2) *reinterpret_cast<double2*>(o + i) = make_double2(v[i], v[i + 1]);
+      for (int i = 0; i < V; i += 2) *reinterpret_cast<double2*>(o + i) = make_double2(v[i], v[i + 1]);
+    } else {
+      double* o = dst + r * pd + c * V;
+#pragma unroll
+      for (int i = 0; i < V; i += 2) *reinterpret_cast<double2*>(o + i) = make_double2(v[i], v[i + 1]);
+    }
   }
 }
 
@@ -196,14 +203,15 @@ __global__ void __launch_bounds__(kT) inv_persistent(const double* __restrict__ 
                                                      double* __restrict__ y, FGeom g) {
   extern __shared__ __align__(128) double sm[];
   const int CT = g.CT;
-  double* in[2] = {sm, sm + CT * TQ};
-  double* aux[2] = {sm + 2 * CT * TQ, sm + 2 * CT * TQ + TQ * g.LDA0};
+  // pointer arithmetic on `sm` (not arrays of pointers) keeps every access LDS/STS
+  double* const aux0 = sm + 2 * CT * TQ;
+  double* const aux1 = aux0 + TQ * g.LDA0;
   constexpr int CPR = TQ / 2;  // 16-byte chunks per row
   auto issue = [&](uint32_t t, int buf) {
     int64_t q0, t0;
     int tq;
     tile_at<TQ>(g, t, q0, tq, t0);
-    double* dstb = in[buf];
+    double* dstb = sm + buf * (CT * TQ);
     for (int j = 1; j <= g.L + 1; ++j) {
       const bool smooth = j > g.L;
       if (!((g.mask >> (smooth ? 0 : j)) & 1)) continue;
@@ -231,13 +239,13 @@ __global__ void __launch_bounds__(kT) inv_persistent(const double* __restrict__ 
     int64_t q0, t0;
     int tq;
     tile_at<TQ>(g, t, q0, tq, t0);
-    const double* I = in[buf];
+    const double* I = sm + buf * (CT * TQ);
     int hi = g.L, stage = 0;
     const double* ssrc = nullptr;
     int pss = 0;
     while (hi > 0) {
       const int W = (hi - 1) % 3 + 1;  // top stage absorbs the remainder: final stage is 3 wide
-      double* dst = aux[stage & 1];
+      double* dst = (stage & 1) ? aux1 : aux0;
       const int pd = g.LDA0;
       const bool s_in = (hi == g.L);
       if (W == 3) inv_stage<TQ, 3>(I, ssrc, pss, s_in, dst, pd, hi, g, y, q0, tq, t0);
