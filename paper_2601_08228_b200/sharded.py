@@ -1,0 +1,210 @@
+"""Multi-GPU w-svd / sp-w-svd / w-pinv: rows -> wavelet slices -> rows.
+
+One process per GPU (torch.distributed, NCCL over NVLink/NVSwitch).  The cube
+is sharded by spatial rows i (complete tubes), so the lifting transform needs
+no communication (every 2^L-band chunk of a tube is independent, SURVEY.md
+finding 3).  The facewise SVD is independent per wavelet slice, so one
+all-to-all redistributes the packed slices from row shards to slice shards, the
+slices are decomposed locally, and a second all-to-all brings the results back
+to row shards for the inverse transform.  sp-w-svd
+only exchanges the 2m coarsest slices [dL | sL] (1/2^(L-1) of the data).
+
+The compute behind the exchange is pluggable (``ops``): :class:`CudaOps` is the
+product (K1/K2/K4/K5 kernels + NCCL); the CPU tests drive the same exchange
+logic over gloo with an oracle-backed ops object.
+"""
+
+from __future__ import annotations
+
+import torch
+import torch.distributed as dist
+
+from . import _native as N
+from . import engine as E
+from .decomposition import _check_levels, _check_rank
+
+
+def splits(n: int, parts: int):
+    """Balanced contiguous split sizes (first n % parts parts get one extra)."""
+    base, extra = divmod(n, parts)
+    return [base + (1 if g < extra else 0) for g in range(parts)]
+
+
+def offsets(sizes):
+    out, acc = [], 0
+    for s in sizes:
+        out.append(acc)
+        acc += s
+    return out
+
+
+class CudaOps:
+    """Product compute for the sharded pipelines (hand-written sm_100a kernels)."""
+
+    def __init__(self, device=None):
+        self.device = device or torch.device("cuda", torch.cuda.current_device())
+
+    def empty(self, shape):
+        return torch.empty(shape, dtype=torch.float64, device=self.device)
+
+    def forward(self, x, levels, mask, slice_base):
+        return E.lift_forward(x, levels, mask=mask, slice_base=slice_base)
+
+    def inverse(self, buf, n1, n2, p, levels, mask, slice_base):
+        return E.lift_inverse(buf, n1, n2, p, levels, mask=mask, slice_base=slice_base)
+
+    def copy_rows(self, src, dst):
+        E.copy2d(src, trans=False, out=dst)
+
+    def truncated(self, slices, r):
+        if slices.shape[0] == 0:
+            return self.empty(slices.shape)
+        sigma, vec, info = E.svd(slices, r)
+        E.raise_if_failed(info)
+        return E.truncated_recon(slices, sigma, vec, r)
+
+    def pinv(self, slices, tol):
+        k, n1, n2 = slices.shape
+        if k == 0:
+            return self.empty((0, n2, n1))
+        sigma, vec, info = E.svd(slices, min(n1, n2))
+        E.raise_if_failed(info)
+        return E.pinv_blocks(slices, sigma, vec, tol)
+
+
+def _a2a(out, inp, out_splits, in_splits, group):
+    dist.all_to_all_single(out, inp, out_splits, in_splits, group=group)
+
+
+def rows_to_slices(ops, local, rows, group):
+    """(K, R_me, c) packed slices of my rows -> (K_me, n, c) full slices I own.
+
+    ``rows`` = row split sizes of every rank (sum n); slices are split with
+    :func:`splits` (K_me for rank me).
+    """
+    G = dist.get_world_size(group)
+    me = dist.get_rank(group)
+    K, R_me, c = local.shape
+    ks = splits(K, G)
+    n = sum(rows)
+    in_splits = [ks[h] * R_me * c for h in range(G)]
+    out_splits = [ks[me] * rows[g] * c for g in range(G)]
+    recv = ops.empty((sum(out_splits),))
+    _a2a(recv, local.reshape(-1), out_splits, in_splits, group)
+    full = ops.empty((ks[me], n, c))
+    off, r0 = 0, 0
+    for g in range(G):
+        cnt = out_splits[g]
+        if cnt:
+            ops.copy_rows(recv[off:off + cnt].view(ks[me], rows[g], c), full[:, r0:r0 + rows[g], :])
+        off += cnt
+        r0 += rows[g]
+    return full, ks
+
+
+def slices_to_rows(ops, full, ks, rows, group):
+    """Inverse of :func:`rows_to_slices` for (K_me, n, c) results with output row splits ``rows``."""
+    G = dist.get_world_size(group)
+    me = dist.get_rank(group)
+    k_me, n, c = full.shape
+    K = sum(ks)
+    in_splits = [k_me * rows[g] * c for g in range(G)]
+    send = ops.empty((sum(in_splits),))
+    off, r0 = 0, 0
+    for g in range(G):
+        cnt = in_splits[g]
+        if cnt:
+            ops.copy_rows(full[:, r0:r0 + rows[g], :], send[off:off + cnt].view(k_me, rows[g], c))
+        off += cnt
+        r0 += rows[g]
+    out_splits = [ks[h] * rows[me] * c for h in range(G)]
+    recv = ops.empty((sum(out_splits),))
+    _a2a(recv, send, out_splits, in_splits, group)
+    return recv.view(K, rows[me], c)  # rank-major order == slice order
+
+
+def sp_w_svd_sharded(x_local, r, levels, n1, group=None, ops=None):
+    """sp-w-svd of an (n1, n2, p) cube whose rows are sharded over the group.
+
+    ``x_local`` holds this rank's rows (split by :func:`splits`); returns this
+    rank's rows of the reconstruction.  Equal (up to the per-slice SVD) to
+    ``decomposition.sp_w_svd`` on the gathered cube.
+    """
+    ops = ops or CudaOps()
+    G = dist.get_world_size(group)
+    me = dist.get_rank(group)
+    R, n2, p = x_local.shape
+    rows = splits(n1, G)
+    assert R == rows[me], f"rank {me} holds {R} rows, expected {rows[me]}"
+    _check_rank(r, n1, n2)
+    _check_levels(p, levels)
+    m = p >> levels
+    base = p - 2 * m
+    mask = E.level_mask(levels, smooth=True, details=[levels])
+    coarse = ops.forward(x_local, levels, mask, base)          # (2m, R, n2)
+    full, ks = rows_to_slices(ops, coarse, rows, group)         # (k_me, n1, n2)
+    rec = ops.truncated(full, r)
+    back = slices_to_rows(ops, rec, ks, rows, group)            # (2m, R, n2)
+    return ops.inverse(back, R, n2, p, levels, mask, base)
+
+
+def w_svd_recon_sharded(x_local, r, levels, n1, group=None, ops=None):
+    """Rank-r w-svd reconstruction (all p wavelet slices) of a row-sharded cube."""
+    ops = ops or CudaOps()
+    G = dist.get_world_size(group)
+    me = dist.get_rank(group)
+    R, n2, p = x_local.shape
+    rows = splits(n1, G)
+    assert R == rows[me]
+    _check_rank(r, n1, n2)
+    _check_levels(p, levels)
+    pyr = ops.forward(x_local, levels, N.MASK_ALL, 0)           # (p, R, n2)
+    full, ks = rows_to_slices(ops, pyr, rows, group)
+    rec = ops.truncated(full, r)
+    back = slices_to_rows(ops, rec, ks, rows, group)
+    return ops.inverse(back, R, n2, p, levels, N.MASK_ALL, 0)
+
+
+def pinv_w_sharded(x_local, levels, n1, tol=1e-12, group=None, ops=None):
+    """w-pinv of a row-sharded (n1, n2, p) cube; returns this rank's rows of the
+    (n2, n1, p) pseudo-inverse (its rows split over n2 with :func:`splits`)."""
+    ops = ops or CudaOps()
+    G = dist.get_world_size(group)
+    me = dist.get_rank(group)
+    R, n2, p = x_local.shape
+    rows = splits(n1, G)
+    assert R == rows[me]
+    _check_levels(p, levels)
+    pyr = ops.forward(x_local, levels, N.MASK_ALL, 0)
+    full, ks = rows_to_slices(ops, pyr, rows, group)            # (k_me, n1, n2)
+    inv = ops.pinv(full, tol)                                   # (k_me, n2, n1)
+    out_rows = splits(n2, G)
+    back = slices_to_rows(ops, inv, ks, out_rows, group)        # (p, n2_me, n1)
+    return ops.inverse(back, out_rows[me], n1, p, levels, N.MASK_ALL, 0)
+
+
+def bench_sp_w_svd(dist_mod, timed_region, steps=3, warmup=1, shape=(1024, 1024, 256), r=30,
+                   levels=4):
+    """Config 4 strong-scaled over the group (rows sharded; see bench.py)."""
+    from . import synth
+
+    G = dist_mod.get_world_size()
+    me = dist_mod.get_rank()
+    n1, n2, p = shape
+    rows = splits(n1, G)
+    r0 = sum(rows[:me])
+    cube = synth.hyperspectral_cube(n1, n2, p, seed=0)
+    x = torch.from_numpy(cube[r0:r0 + rows[me]].copy()).cuda()
+    del cube
+    out = {}
+
+    def step(record):
+        out["y"] = sp_w_svd_sharded(x, r, levels, n1)
+
+    ms = timed_region(step, steps, warmup, dist_mod)
+    total = n1 * n2 * p
+    k = 2 * (p >> levels)
+    return {"config": f"sp_w_svd {n1}x{n2}x{p} rank {r} L={levels}, rows sharded over {G} GPUs, "
+                      f"{k} coarse slices exchanged by NCCL all-to-all",
+            "metric": "tensor-elems/s", "value": total * steps / (ms * 1e-3), "ms_per_call": ms / steps,
+            "scaling": "strong", "exchange_bytes_per_rank": 2 * 8 * k * rows[me] * n2}

@@ -1,0 +1,43 @@
+"""The sharded pipelines with the product ops (CUDA kernels + NCCL) on one GPU
+(world size 1: the all-to-alls are local copies).  The multi-rank exchange is
+covered by tests/test_sharded_cpu.py over gloo."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+
+import paper_2601_08228_b200 as W
+from paper_2601_08228_b200 import sharded
+from oracle import wten_oracle as O
+from wt_helpers import relerr
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def nccl1():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    yield
+    dist.destroy_process_group()
+
+
+def test_sharded_equals_single_gpu(nccl1):
+    x = np.random.default_rng(31).standard_normal((64, 48, 32))
+    xd = torch.from_numpy(x).cuda()
+    sp = sharded.sp_w_svd_sharded(xd, 6, 3, 64)
+    assert torch.equal(sp, W.sp_w_svd(xd, 6, 3))
+    assert relerr(sp.cpu().numpy(), O.sp_w_svd(x, 6, 3)) < 1e-10
+    ws = sharded.w_svd_recon_sharded(xd, 6, 2, 64)
+    assert relerr(ws.cpu().numpy(), O.w_svd(x, 6, 2)["recon"]) < 1e-10
+    pv = sharded.pinv_w_sharded(xd, 2, 64)
+    assert relerr(pv.cpu().numpy(), O.pinv_w(x, 2)) < 1e-9

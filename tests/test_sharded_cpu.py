@@ -1,0 +1,110 @@
+"""Multi-process (gloo, CPU) tests of the sharded rows -> slices -> rows pipelines.
+
+The exchange logic of paper_2601_08228_b200/sharded.py (all-to-all split
+sizes, row/slice permutations, uneven splits) runs exactly as on the GPUs; the
+per-shard compute is the CPU oracle, so each sharded result must equal the
+oracle applied to the gathered cube.
+"""
+
+import os
+import socket
+import tempfile
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from oracle import wten_oracle as O
+
+
+class OracleOps:
+    """CPU stand-in for sharded.CudaOps (test infrastructure only)."""
+
+    def empty(self, shape):
+        return torch.empty(shape, dtype=torch.float64)
+
+    def forward(self, x, levels, mask, base):
+        s, d = O.lift_forward(x.numpy(), levels)
+        return torch.from_numpy(O.packed_slices(s, d)[base:].copy())
+
+    def inverse(self, buf, n1, n2, p, levels, mask, base):
+        full = np.zeros((p, n1, n2))
+        full[base:] = buf.numpy()
+        blocks, off = [], 0
+        for j in range(1, levels + 1):
+            cnt = p >> j
+            blocks.append(np.moveaxis(full[off:off + cnt], 0, 2))
+            off += cnt
+        smooth = np.moveaxis(full[off:], 0, 2)
+        return torch.from_numpy(O.lift_inverse(smooth, blocks))
+
+    def copy_rows(self, src, dst):
+        dst.copy_(src)
+
+    def truncated(self, slices, r):
+        if slices.shape[0] == 0:
+            return slices.clone()
+        st = np.moveaxis(slices.numpy(), 0, 2)
+        return torch.from_numpy(np.ascontiguousarray(np.moveaxis(O.truncated(*O.stack_svd(st), r), 2, 0)))
+
+    def pinv(self, slices, tol):
+        k, n1, n2 = slices.shape
+        if k == 0:
+            return torch.empty((0, n2, n1), dtype=torch.float64)
+        st = np.moveaxis(slices.numpy(), 0, 2)
+        return torch.from_numpy(np.ascontiguousarray(np.moveaxis(O.pinv_stack(st, tol), 2, 0)))
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _worker(rank, ws, port, outdir, case):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=ws)
+    from paper_2601_08228_b200 import sharded
+
+    n1, n2, p, r, L = case
+    x = np.random.default_rng(7).standard_normal((n1, n2, p))
+    rows = sharded.splits(n1, ws)
+    r0 = sum(rows[:rank])
+    xl = torch.from_numpy(x[r0:r0 + rows[rank]].copy())
+    ops = OracleOps()
+    sp = sharded.sp_w_svd_sharded(xl, r, L, n1, ops=ops)
+    ws_rec = sharded.w_svd_recon_sharded(xl, r, L, n1, ops=ops)
+    pv = sharded.pinv_w_sharded(xl, L, n1, tol=1e-12, ops=ops)
+    np.savez(os.path.join(outdir, f"r{rank}.npz"), sp=sp.numpy(), ws=ws_rec.numpy(), pv=pv.numpy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("ws,case", [(2, (12, 10, 16, 3, 3)), (3, (10, 7, 8, 2, 2)),
+                                     (4, (9, 9, 8, 4, 3))])
+def test_sharded_pipelines_match_oracle(ws, case):
+    n1, n2, p, r, L = case
+    with tempfile.TemporaryDirectory() as d:
+        mp.spawn(_worker, args=(ws, _free_port(), d, case), nprocs=ws, join=True)
+        parts = [np.load(os.path.join(d, f"r{g}.npz")) for g in range(ws)]
+        sp = np.concatenate([q["sp"] for q in parts], axis=0)
+        wsr = np.concatenate([q["ws"] for q in parts], axis=0)
+        pv = np.concatenate([q["pv"] for q in parts], axis=0)
+    x = np.random.default_rng(7).standard_normal((n1, n2, p))
+    np.testing.assert_allclose(sp, O.sp_w_svd(x, r, L), rtol=0, atol=1e-12)
+    np.testing.assert_allclose(wsr, O.w_svd(x, r, L)["recon"], rtol=0, atol=1e-12)
+    np.testing.assert_allclose(pv, O.pinv_w(x, L), rtol=0, atol=1e-10)
+
+
+def test_splits():
+    from paper_2601_08228_b200 import sharded
+
+    assert sharded.splits(10, 3) == [4, 3, 3]
+    assert sharded.splits(32, 8) == [4] * 8
+    assert sharded.splits(2, 4) == [1, 1, 0, 0]
+    assert sharded.offsets([4, 3, 3]) == [0, 4, 7]
