@@ -38,7 +38,7 @@ def slicewise_matmul(a, b):
     sb = _stack_to_slices(E.as_device(b))
     sc = E.gemm(sa, sb)
     out = E.lift_inverse(sc, n1, n3, k, 0)  # (k, n1, n3) -> (n1, n3, k)
-    return out if dev else out.cpu().numpy()
+    return out if dev else E.to_host(out)
 
 
 def face_product(a, b):
@@ -98,7 +98,7 @@ def w_product(a, b, levels):
         z = np.zeros((n1, n3, p))
         return torch.from_numpy(z).cuda() if dev else z
     c = w_product_device(E.as_device(a), E.as_device(b), levels)
-    return c if dev else c.cpu().numpy()
+    return c if dev else E.to_host(c)
 
 
 def identity_tensor(n, p, levels):

@@ -73,7 +73,7 @@ def _prep(a):
 
 
 def _out(t: torch.Tensor, dev: bool):
-    return t if dev else t.cpu().numpy()
+    return t if dev else E.to_host(t)
 
 
 # ----------------------------------------------------------------- w-svd ----

@@ -64,6 +64,14 @@ def as_device(x, device=None) -> torch.Tensor:
     return t.contiguous()
 
 
+def to_host(t: torch.Tensor) -> np.ndarray:
+    """D2H into pinned host memory (full-bandwidth DMA); the returned numpy array
+    owns a reference to the pinned buffer."""
+    h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+    h.copy_(t)
+    return h.numpy()
+
+
 # --------------------------------------------------------------- lifting ----
 
 def lift_forward(x: torch.Tensor, levels: int, layout: int = N.LAYOUT_SLICE,

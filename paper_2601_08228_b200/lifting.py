@@ -45,6 +45,7 @@ class WaveletPyramid:
         self._smooth = smooth
         self._details = list(details) if details is not None else []
         self._packed = None  # (buf, levels, (n1, n2, p), ids of the views handed out)
+        self._host_flat = None  # (pinned flat host buffer, ids of its block views)
 
     # dataclass-like field access -------------------------------------------
     @property
@@ -105,12 +106,17 @@ class WaveletPyramid:
         return self.m + sum(d.shape[2] for d in self._details)
 
     # packed-buffer bookkeeping ------------------------------------------------
+    def _views(self):
+        return (self._smooth,) + tuple(self._details)
+
+    def _same_views(self, handed_out) -> bool:
+        # identity (not id()) of the block objects handed out: the tuple keeps
+        # them alive, so a replaced block can never alias a recycled id
+        cur = self._views()
+        return len(cur) == len(handed_out) and all(a is b for a, b in zip(cur, handed_out))
+
     def _packed_intact(self) -> bool:
-        if self._packed is None:
-            return False
-        ids = self._packed[3]
-        cur = (id(self._smooth),) + tuple(id(d) for d in self._details)
-        return ids == cur
+        return self._packed is not None and self._same_views(self._packed[3])
 
     def packed(self):
         """The slice-major device buffer ``(p, n1, n2)`` if this pyramid still owns one."""
@@ -123,7 +129,7 @@ def _pyramid_from_packed(buf: torch.Tensor, levels: int, n1: int, n2: int, p: in
         views[tag] = buf[off:off + cnt].permute(1, 2, 0)
     details = [views[f"d{j}"] for j in range(1, levels + 1)]
     pyr = WaveletPyramid(views["s"], details)
-    pyr._packed = (buf, levels, (n1, n2, p), (id(pyr._smooth),) + tuple(id(d) for d in details))
+    pyr._packed = (buf, levels, (n1, n2, p), pyr._views())
     return pyr
 
 
@@ -158,12 +164,15 @@ def forward_w(t, levels):
     x = E.as_device(t)
     if dev:
         return _pyramid_from_packed(E.lift_forward(x, levels), levels, n1, n2, p)
-    # host mode: tube-major blocks = the reference's own per-level arrays
-    host = E.lift_forward(x, levels, layout=N.LAYOUT_TUBE).cpu().numpy().reshape(-1)
+    # host mode: tube-major blocks = the reference's own per-level arrays, all
+    # views of one pinned host buffer (inverse_w re-uploads it without packing)
+    host = E.to_host(E.lift_forward(x, levels, layout=N.LAYOUT_TUBE)).reshape(-1)
     nt = n1 * n2
     blocks = {tag: host[off * nt:(off + cnt) * nt].reshape(n1, n2, cnt)
               for tag, off, cnt in E.block_slices(p, levels)}
-    return WaveletPyramid(blocks["s"], [blocks[f"d{j}"] for j in range(1, levels + 1)])
+    pyr = WaveletPyramid(blocks["s"], [blocks[f"d{j}"] for j in range(1, levels + 1)])
+    pyr._host_flat = (host, pyr._views())
+    return pyr
 
 
 def check_consistent(pyr):
@@ -204,9 +213,13 @@ def inverse_w(pyr):
         if _is_dev(z):
             return torch.zeros((n1, n2, p), dtype=torch.float64, device=z.device)
         return np.zeros((n1, n2, p), dtype=np.float64)
-    flat, dev = _pack_blocks(pyr)
+    hf = getattr(pyr, "_host_flat", None)
+    if hf is not None and pyr._same_views(hf[1]):
+        flat, dev = E.as_device(hf[0]), False   # blocks are still views of the pinned buffer
+    else:
+        flat, dev = _pack_blocks(pyr)
     y = E.lift_inverse(flat, n1, n2, p, levels, layout=N.LAYOUT_TUBE)
-    return y if dev else y.cpu().numpy()
+    return y if dev else E.to_host(y)
 
 
 def constant_pyramid(block, p, levels):

@@ -62,7 +62,7 @@ def transpose(t):
     sl = E.lift_forward(x, 0)                 # (p, n1, n2)
     st = E.copy2d(sl, trans=True)             # (p, n2, n1)
     y = E.lift_inverse(st, n2, n1, p, 0)      # (n2, n1, p)
-    return y if dev else y.cpu().numpy()
+    return y if dev else E.to_host(y)
 
 
 def trace(t):
