@@ -20,7 +20,10 @@
 // Everything is deterministic: fixed reduction orders, no floating atomics.
 #include <stdlib.h>
 
+#include <string.h>
+
 #include <algorithm>
+#include <vector>
 
 #include "wt_common.cuh"
 
@@ -30,7 +33,7 @@ namespace {
 constexpr int BW = 32;       // pair panel width (2 blocks of 16 columns)
 constexpr int HB = BW / 2;   // block width
 constexpr int RCH = 64;      // rows per streamed chunk
-constexpr int LDZ = RCH + 4; // chunk column pitch (doubles), = 4 mod 16: conflict-free frags
+constexpr int LDZ = RCH + 8; // chunk column pitch (doubles), = 8 mod 16: conflict-free LDS.128 Gram frags
 constexpr int LDG = BW + 1;  // Gram / Q pitch
 constexpr int kThreads = 256;
 constexpr double kFloorEps = 1e3 * 2.220446049250313e-16;  // null-column floor (see the test)
@@ -74,9 +77,8 @@ __device__ __forceinline__ int rr_index(int pos, int round, int nb) {
 struct PairSmem {
   double Z[2][BW * LDZ];
   double G[2][BW * LDG];
-  double Q[2][BW * LDG];
+  double Q[BW * LDG];
   double warp_off[kThreads / 32];
-  int perm[BW];
 };
 
 __device__ __forceinline__ void load_chunk(double* Zs, const double* Xb, int64_t mpad, int colI,
@@ -91,8 +93,8 @@ __device__ __forceinline__ void load_chunk(double* Zs, const double* Xb, int64_t
   }
 }
 
-__global__ void __launch_bounds__(kThreads, 2) svd_pair_kernel(SvdWs ws, int64_t mpad, int64_t npad,
-                                                               int round, double tol, int inner_sweeps, int flags) {
+__global__ void __launch_bounds__(kThreads, 3) svd_pair_kernel(SvdWs ws, int64_t mpad, int64_t npad,
+                                                               int round, double tol, int inner_sweeps) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   PairSmem& S = *reinterpret_cast<PairSmem*>(smem_raw);
   const int b = blockIdx.y;
@@ -117,13 +119,20 @@ __global__ void __launch_bounds__(kThreads, 2) svd_pair_kernel(SvdWs ws, int64_t
     cp_async_wait<1>();
     __syncthreads();
     const double* Zs = S.Z[ch & 1];
+    // one LDS.128 per fragment feeds two DMMAs: lane (r, k) holds rows
+    // ks + 2k and ks + 2k + 1, i.e. the k-slots of the two products are the
+    // even and the odd rows -- any fixed row->slot map is valid for Z^T Z.
 #pragma unroll
-    for (int ks = kh * 4; ks < RCH; ks += 8) {
-      double f[4];
+    for (int ks = kh * 8; ks < RCH; ks += 16) {
+      double2 f[4];
 #pragma unroll
-      for (int tj = 0; tj < 4; ++tj) f[tj] = Zs[(tj * 8 + (lane >> 2)) * LDZ + ks + (lane & 3)];
+      for (int tj = 0; tj < 4; ++tj)
+        f[tj] = *reinterpret_cast<const double2*>(Zs + (tj * 8 + (lane >> 2)) * LDZ + ks + 2 * (lane & 3));
 #pragma unroll
-      for (int tj = 0; tj < 4; ++tj) dmma884(acc[tj][0], acc[tj][1], f[ti], f[tj]);
+      for (int tj = 0; tj < 4; ++tj) {
+        dmma884(acc[tj][0], acc[tj][1], f[ti].x, f[tj].x);
+        dmma884(acc[tj][0], acc[tj][1], f[ti].y, f[tj].y);
+      }
     }
     __syncthreads();
   }
@@ -150,7 +159,7 @@ __global__ void __launch_bounds__(kThreads, 2) svd_pair_kernel(SvdWs ws, int64_t
   double gmax = 0.0;
 #pragma unroll 4
   for (int i = 0; i < BW; ++i) gmax = fmax(gmax, S.G[0][i * LDG + i]);
-  const double floor_c = (flags & 2) ? 8.0 * 2.220446049250313e-16 / tol : kFloorEps * kFloorEps / tol;
+  const double floor_c = kFloorEps * kFloorEps / tol;
   {
     double mx = 0.0;
     for (int e = tid; e < BW * BW; e += kThreads) {
@@ -158,7 +167,7 @@ __global__ void __launch_bounds__(kThreads, 2) svd_pair_kernel(SvdWs ws, int64_t
       if (i < j) {
         const double gii = S.G[0][i * LDG + i], gjj = S.G[0][j * LDG + j];
         const double gij = S.G[0][i * LDG + j];
-        const double den = sqrt(gii * gjj) + ((flags & 2) ? floor_c * sqrt(gmax * fmax(gii, gjj)) : floor_c * gmax);
+        const double den = fmax(sqrt(gii * gjj), floor_c * gmax);
         double c = 0.0;
         if (gij != 0.0) c = den > 0.0 ? fabs(gij) / den : INFINITY;
         if (isnan(gii) || isnan(gjj)) c = gii + gjj;
@@ -184,12 +193,12 @@ __global__ void __launch_bounds__(kThreads, 2) svd_pair_kernel(SvdWs ws, int64_t
   // Q <- Q J (columns p, q) and, after a barrier, G <- J^T G (rows p, q).
   for (int e = tid; e < BW * BW; e += kThreads) {
     const int i = e / BW, j = e % BW;
-    S.Q[0][i * LDG + j] = (i == j) ? 1.0 : 0.0;
+    S.Q[i * LDG + j] = (i == j) ? 1.0 : 0.0;
   }
   __syncthreads();
   {
     double* G = S.G[0];
-    double* Q = S.Q[0];
+    double* Q = S.Q;
     const int grp = tid >> 4, sub = tid & 15;
     for (int sweep = 0; sweep < inner_sweeps; ++sweep) {
       int my_rot = 0;
@@ -197,14 +206,25 @@ __global__ void __launch_bounds__(kThreads, 2) svd_pair_kernel(SvdWs ws, int64_t
         int p = rr_index(grp, step, BW), q = rr_index(BW - 1 - grp, step, BW);
         if (p > q) { const int t = p; p = q; q = t; }
         const double gpp = G[p * LDG + p], gqq = G[q * LDG + q], gpq = G[p * LDG + q];
-        const double den = sqrt(gpp * gqq) + ((flags & 2) ? floor_c * sqrt(gmax * fmax(gpp, gqq)) : floor_c * gmax);
-        const bool rot = gpq != 0.0 && fabs(gpq) > tol * den;
+        // rotate iff |g_pq| > tol * max(sqrt(g_pp g_qq), floor_c g_max)  (squared: no sqrt)
+        const double fl = floor_c * gmax;
+        const bool rot = gpq * gpq > tol * tol * fmax(gpp * gqq, fl * fl);
         __syncwarp();
         double c = 1.0, s = 0.0;
         if (rot) {
-          const double tau = (gqq - gpp) / (2.0 * gpq);
-          const double t = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + hypot(1.0, tau));
-          c = 1.0 / sqrt(1.0 + t * t);
+          // Rutishauser's rotation with reciprocal / rsqrt instead of divisions
+          // and sqrt (the dependent FP64 chain was the top stall in ncu)
+          const double tau = (gqq - gpp) * __drcp_rn(2.0 * gpq);
+          const double at = fabs(tau);
+          double t;
+          if (at < 1e100) {
+            const double w = fma(tau, tau, 1.0);
+            t = __drcp_rn(at + w * rsqrt(w));
+          } else {
+            t = 0.5 / at;
+          }
+          if (tau < 0.0) t = -t;
+          c = rsqrt(fma(t, t, 1.0));
           s = t * c;
           my_rot = 1;
 #pragma unroll
@@ -236,31 +256,16 @@ __global__ void __launch_bounds__(kThreads, 2) svd_pair_kernel(SvdWs ws, int64_t
       if (!__syncthreads_or(my_rot)) break;
     }
   }
-  // order the pair's columns by descending norm (block I gets the largest):
-  // keeps the cyclic sweeps close to sorted, which speeds outer convergence
-  if (tid < BW) {
-    const double di = S.G[0][tid * LDG + tid];
-    int rank = 0;
-    for (int j = 0; j < BW; ++j) {
-      const double dj = S.G[0][j * LDG + j];
-      rank += (dj > di) || (dj == di && j < tid);
-    }
-    S.perm[(flags & 1) ? rank : tid] = tid;
-  }
-  __syncthreads();
-  const int cur = 0;
-
   // ---------------- 4. Z <- Z Q, streamed, written back in place -----------
-  // Q fragments cached in registers: b-frag for k-step kk, n-tile tn is
-  // Q[kk*4 + lane%4][tn*8 + lane/4].
-  double qf[8][4];
-  {
-    const double* Q = S.Q[cur];
+  // warp w: chunk rows rt*16 .. rt*16+15 (two 8-row tiles) x output n-tiles
+  // {2nh, 2nh+1}; its Q b-fragments Q[kk*4 + lane%4][n*8 + lane/4] stay in
+  // registers for the whole stream.
+  const int rt = warp & 3, nh = warp >> 2;
+  double qf[8][2];
 #pragma unroll
-    for (int kk = 0; kk < 8; ++kk)
+  for (int kk = 0; kk < 8; ++kk)
 #pragma unroll
-      for (int tn = 0; tn < 4; ++tn) qf[kk][tn] = Q[(kk * 4 + (lane & 3)) * LDG + S.perm[tn * 8 + (lane >> 2)]];
-  }
+    for (int j = 0; j < 2; ++j) qf[kk][j] = S.Q[(kk * 4 + (lane & 3)) * LDG + (2 * nh + j) * 8 + (lane >> 2)];
   load_chunk(S.Z[0], Xb, mpad, colI, colJ, 0);
   cp_async_commit();
   for (int ch = 0; ch < nch; ++ch) {
@@ -269,22 +274,30 @@ __global__ void __launch_bounds__(kThreads, 2) svd_pair_kernel(SvdWs ws, int64_t
     cp_async_wait<1>();
     __syncthreads();
     double* Zs = S.Z[ch & 1];
-    // warp w: rows w*8 .. w*8+7 of the chunk, all 32 output columns
-    double o[4][2];
+    double o[2][2][2];
 #pragma unroll
-    for (int tn = 0; tn < 4; ++tn) o[tn][0] = o[tn][1] = 0.0;
-    const int r0 = warp * 8;
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int j = 0; j < 2; ++j) o[i][j][0] = o[i][j][1] = 0.0;
+    const int r0 = rt * 16;
 #pragma unroll
     for (int kk = 0; kk < 8; ++kk) {
-      const double a = Zs[(kk * 4 + (lane & 3)) * LDZ + r0 + (lane >> 2)];
+      const double* zc = Zs + (kk * 4 + (lane & 3)) * LDZ + r0 + (lane >> 2);
+      const double a0 = zc[0], a1 = zc[8];
 #pragma unroll
-      for (int tn = 0; tn < 4; ++tn) dmma884(o[tn][0], o[tn][1], a, qf[kk][tn]);
+      for (int j = 0; j < 2; ++j) {
+        dmma884(o[0][j][0], o[0][j][1], a0, qf[kk][j]);
+        dmma884(o[1][j][0], o[1][j][1], a1, qf[kk][j]);
+      }
     }
-    __syncwarp();
+    __syncthreads();  // every warp has read its rows (the other n-half reads them too)
 #pragma unroll
-    for (int tn = 0; tn < 4; ++tn)
+    for (int i = 0; i < 2; ++i)
 #pragma unroll
-      for (int h = 0; h < 2; ++h) Zs[(tn * 8 + 2 * (lane & 3) + h) * LDZ + r0 + (lane >> 2)] = o[tn][h];
+      for (int j = 0; j < 2; ++j)
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+          Zs[((2 * nh + j) * 8 + 2 * (lane & 3) + h) * LDZ + r0 + i * 8 + (lane >> 2)] = o[i][j][h];
     __syncthreads();
     // chunk -> global (each column: RCH contiguous doubles)
     const int64_t rbase = (int64_t)ch * RCH;
@@ -471,15 +484,29 @@ extern "C" int wt_svd_jacobi_f64(const double* A, int64_t lda, int64_t strideA, 
   // 2.4x / 1.6x less time (tools/svd_probe.py, round 1).
   int inner = 1;
   if (const char* e = getenv("WT_SVD_INNER_SWEEPS")) inner = std::max(1, std::min(kMaxInnerSweeps, atoi(e)));
-  int flags = 0;
-  if (const char* e = getenv("WT_SVD_FLAGS")) flags = atoi(e);
   bool hit_max = true;
   for (int sweep = 0; sweep < max_sweeps; ++sweep) {
     for (int round = 0; round < nb - 1; ++round) {
       svd_pair_kernel<<<dim3(nb / 2, (unsigned)batch), kThreads, sizeof(PairSmem), st>>>(
-          ws, L.mpad, L.npad, round, tol, inner, flags);
+          ws, L.mpad, L.npad, round, tol, inner);
     }
     if (int e = check_launch("svd_pair_kernel")) return e;
+    if (getenv("WT_SVD_DEBUG")) {  // per-sweep convergence trace (diagnostics only)
+      std::vector<unsigned long long> h(batch);
+      WT_CUDA(cudaMemcpyAsync(h.data(), ws.offmax, sizeof(unsigned long long) * batch,
+                              cudaMemcpyDeviceToHost, st));
+      WT_CUDA(cudaStreamSynchronize(st));
+      double mx = 0.0;
+      int active = 0;
+      for (auto v : h) {
+        double d;
+        memcpy(&d, &v, sizeof(d));
+        mx = std::max(mx, d);
+        active += d >= tol;
+      }
+      fprintf(stderr, "[wt_svd] sweep %d: max off %.3e (tol %.1e), %d/%lld matrices above tol\n",
+              sweep, mx, tol, active, (long long)batch);
+    }
     WT_CUDA(cudaMemsetAsync(ws.pending, 0, sizeof(int), st));
     svd_end_sweep<<<(unsigned)((batch + 255) / 256), 256, 0, st>>>(ws, (int)batch, tol);
     WT_CUDA(cudaMemcpyAsync(h_pending, ws.pending, sizeof(int), cudaMemcpyDeviceToHost, st));
