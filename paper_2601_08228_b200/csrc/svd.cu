@@ -185,6 +185,7 @@ __global__ void __launch_bounds__(kThreads, 3) svd_pair_kernel(SvdWs ws, int64_t
   // NaN-propagating max through the bit pattern (non-negative doubles order as uint64)
   if (tid == 0) atomicMax(&ws.offmax[b], (unsigned long long)__double_as_longlong(off));
   if (!(off >= tol)) return;  // converged pair (or NaN: recorded above, stop touching data)
+  if (tid == 0) atomicAdd(ws.pending + 1, 1);  // rotated-pair counter (diagnostics)
   if (isinf(off)) return;
 
   // ---------------- 3. eigen-decomposition of G (cyclic parallel Jacobi) ----
@@ -468,6 +469,7 @@ extern "C" int wt_svd_jacobi_f64(const double* A, int64_t lda, int64_t strideA, 
   }
   WT_CUDA(cudaMemsetAsync(ws.offmax, 0, sizeof(unsigned long long) * batch, st));
   WT_CUDA(cudaMemsetAsync(ws.conv, 0, sizeof(int) * batch, st));
+  WT_CUDA(cudaMemsetAsync(ws.pending, 0, sizeof(int) * 2, st));
 
   static bool attr = false;
   if (!attr) {
@@ -504,8 +506,12 @@ extern "C" int wt_svd_jacobi_f64(const double* A, int64_t lda, int64_t strideA, 
         mx = std::max(mx, d);
         active += d >= tol;
       }
-      fprintf(stderr, "[wt_svd] sweep %d: max off %.3e (tol %.1e), %d/%lld matrices above tol\n",
-              sweep, mx, tol, active, (long long)batch);
+      int rotated = 0;
+      WT_CUDA(cudaMemcpy(&rotated, ws.pending + 1, sizeof(int), cudaMemcpyDeviceToHost));
+      WT_CUDA(cudaMemset(ws.pending + 1, 0, sizeof(int)));
+      fprintf(stderr, "[wt_svd] sweep %d: max off %.3e (tol %.1e), %d/%lld matrices above tol, "
+              "%d/%lld pair visits rotated\n", sweep, mx, tol, active, (long long)batch, rotated,
+              (long long)(nb / 2) * (nb - 1) * batch);
     }
     WT_CUDA(cudaMemsetAsync(ws.pending, 0, sizeof(int), st));
     svd_end_sweep<<<(unsigned)((batch + 255) / 256), 256, 0, st>>>(ws, (int)batch, tol);
