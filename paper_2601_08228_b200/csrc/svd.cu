@@ -370,6 +370,10 @@ __global__ void svd_norms_sort(SvdWs ws, int64_t mpad, int64_t npad, int64_t n, 
       __syncthreads();
     }
   }
+  if (sigma == nullptr) {  // reordering pass between sweeps: permutation only
+    for (int i = threadIdx.x; i < npad; i += blockDim.x) ws.perm[(int64_t)b * npad + i] = idx[i];
+    return;
+  }
   bool bad = false;
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
     sigma[(int64_t)b * n + i] = key[i];
@@ -397,9 +401,19 @@ __global__ void svd_gather(SvdWs ws, int64_t mpad, int64_t npad, int64_t m, int6
   for (int64_t r = threadIdx.x; r < m; r += blockDim.x) dst[r] = col[r] * inv;
 }
 
+// X2[b][i] = X[b][perm[b][i]] (whole columns), for the between-sweep reordering.
+__global__ void svd_permute_cols(const double* __restrict__ X, double* __restrict__ X2,
+                                 const int* __restrict__ perm, int64_t mpad, int64_t npad) {
+  const int64_t i = blockIdx.x, b = blockIdx.y;
+  const int c = perm[b * npad + i];
+  const double2* src = reinterpret_cast<const double2*>(X + (b * npad + c) * mpad);
+  double2* dst = reinterpret_cast<double2*>(X2 + (b * npad + i) * mpad);
+  for (int64_t r = threadIdx.x; r < mpad / 2; r += blockDim.x) dst[r] = src[r];
+}
+
 struct WsLayout {
   int64_t m, n, mpad, npad;
-  size_t off_X, off_off, off_conv, off_pending, off_sig, off_perm, total;
+  size_t off_X, off_X2, off_off, off_conv, off_pending, off_sig, off_perm, total;
 };
 
 WsLayout ws_layout(int64_t n1, int64_t n2, int64_t batch) {
@@ -411,6 +425,7 @@ WsLayout ws_layout(int64_t n1, int64_t n2, int64_t batch) {
   size_t o = 0;
   auto take = [&](size_t bytes) { size_t r = o; o = (o + bytes + 255) / 256 * 256; return r; };
   L.off_X = take(sizeof(double) * (size_t)(batch * L.npad * L.mpad));
+  L.off_X2 = take(sizeof(double) * (size_t)(batch * L.npad * L.mpad));
   L.off_off = take(sizeof(unsigned long long) * (size_t)batch);
   L.off_conv = take(sizeof(int) * (size_t)batch);
   L.off_pending = take(sizeof(int) * 4);
@@ -487,7 +502,24 @@ extern "C" int wt_svd_jacobi_f64(const double* A, int64_t lda, int64_t strideA, 
   int inner = 1;
   if (const char* e = getenv("WT_SVD_INNER_SWEEPS")) inner = std::max(1, std::min(kMaxInnerSweeps, atoi(e)));
   bool hit_max = true;
+  // Reorder the columns by descending norm before every sweep: measured on the
+  // config-3/4 slices 13 -> 12 and 17 -> 16 sweeps, -10% time (round 1).
+  int sort_mode = 2;
+  if (const char* e = getenv("WT_SVD_SORT")) sort_mode = atoi(e);
+  double* X2 = reinterpret_cast<double*>(base + L.off_X2);
+  const size_t sort_smem = (size_t)npow2 * (sizeof(double) + sizeof(int));
+  WT_CUDA(cudaFuncSetAttribute(svd_norms_sort, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               8192 * (int)(sizeof(double) + sizeof(int))));
   for (int sweep = 0; sweep < max_sweeps; ++sweep) {
+    if (sort_mode == 2 || (sort_mode == 1 && sweep == 0)) {
+      // columns in descending norm order before the sweep (de Rijk-style)
+      svd_norms_sort<<<(unsigned)batch, 512, sort_smem, st>>>(ws, L.mpad, L.npad, L.n, npow2,
+                                                              nullptr, nullptr, 0);
+      svd_permute_cols<<<dim3((unsigned)L.npad, (unsigned)batch), 128, 0, st>>>(ws.X, X2, ws.perm,
+                                                                                 L.mpad, L.npad);
+      std::swap(ws.X, X2);
+      if (int e = check_launch("svd reorder")) return e;
+    }
     for (int round = 0; round < nb - 1; ++round) {
       svd_pair_kernel<<<dim3(nb / 2, (unsigned)batch), kThreads, sizeof(PairSmem), st>>>(
           ws, L.mpad, L.npad, round, tol, inner);
