@@ -106,11 +106,15 @@ __global__ void __launch_bounds__(kThreads, 3) svd_pair_kernel(SvdWs ws, int64_t
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nch = (int)(mpad / RCH);
 
-  // ---------------- 1. Gram G = Z^T Z (warp: tile row ti, K half kh) -------
-  const int ti = warp & 3, kh = warp >> 2;
-  double acc[4][2];
+  // ---------------- 1. Gram G = Z^T Z: upper 10 of the 16 8x8 tiles --------
+  // Rows are split over the 8 warps (warp w owns rows w*8 .. w*8+7 of every
+  // chunk).  One LDS.128 per column group feeds two DMMAs: lane (r, k) holds
+  // rows 2k and 2k+1, so the two products' k-slots are the even and the odd
+  // rows -- any fixed row->slot map is valid for Z^T Z.  4 LDS.128 feed 20
+  // DMMAs per warp per chunk; the 8 partial Grams are summed by a fixed tree.
+  double acc[10][2];
 #pragma unroll
-  for (int j = 0; j < 4; ++j) acc[j][0] = acc[j][1] = 0.0;
+  for (int t = 0; t < 10; ++t) acc[t][0] = acc[t][1] = 0.0;
   load_chunk(S.Z[0], Xb, mpad, colI, colJ, 0);
   cp_async_commit();
   for (int ch = 0; ch < nch; ++ch) {
@@ -119,35 +123,59 @@ __global__ void __launch_bounds__(kThreads, 3) svd_pair_kernel(SvdWs ws, int64_t
     cp_async_wait<1>();
     __syncthreads();
     const double* Zs = S.Z[ch & 1];
-    // one LDS.128 per fragment feeds two DMMAs: lane (r, k) holds rows
-    // ks + 2k and ks + 2k + 1, i.e. the k-slots of the two products are the
-    // even and the odd rows -- any fixed row->slot map is valid for Z^T Z.
+    double2 f[4];
 #pragma unroll
-    for (int ks = kh * 8; ks < RCH; ks += 16) {
-      double2 f[4];
+    for (int tj = 0; tj < 4; ++tj)
+      f[tj] = *reinterpret_cast<const double2*>(Zs + (tj * 8 + (lane >> 2)) * LDZ + warp * 8 + 2 * (lane & 3));
+    int t = 0;
 #pragma unroll
-      for (int tj = 0; tj < 4; ++tj)
-        f[tj] = *reinterpret_cast<const double2*>(Zs + (tj * 8 + (lane >> 2)) * LDZ + ks + 2 * (lane & 3));
+    for (int ta = 0; ta < 4; ++ta)
 #pragma unroll
-      for (int tj = 0; tj < 4; ++tj) {
-        dmma884(acc[tj][0], acc[tj][1], f[ti].x, f[tj].x);
-        dmma884(acc[tj][0], acc[tj][1], f[ti].y, f[tj].y);
+      for (int tb = ta; tb < 4; ++tb, ++t) {
+        dmma884(acc[t][0], acc[t][1], f[ta].x, f[tb].x);
+        dmma884(acc[t][0], acc[t][1], f[ta].y, f[tb].y);
       }
+    __syncthreads();
+  }
+  {
+    // deterministic tree over the 8 warps through the (now free) chunk buffers
+    double* red = S.Z[0];  // 4 x 10 x 64 doubles
+#pragma unroll
+    for (int half = 4; half >= 1; half >>= 1) {
+      if (warp >= half && warp < 2 * half) {
+#pragma unroll
+        for (int t = 0; t < 10; ++t) {
+          red[((warp - half) * 10 + t) * 64 + 2 * lane] = acc[t][0];
+          red[((warp - half) * 10 + t) * 64 + 2 * lane + 1] = acc[t][1];
+        }
+      }
+      __syncthreads();
+      if (warp < half) {
+#pragma unroll
+        for (int t = 0; t < 10; ++t) {
+          acc[t][0] += red[(warp * 10 + t) * 64 + 2 * lane];
+          acc[t][1] += red[(warp * 10 + t) * 64 + 2 * lane + 1];
+        }
+      }
+      __syncthreads();
+    }
+    if (warp == 0) {  // C frag: row ta*8 + lane/4, col tb*8 + 2*(lane%4) + h; mirror below
+      int t = 0;
+#pragma unroll
+      for (int ta = 0; ta < 4; ++ta)
+#pragma unroll
+        for (int tb = ta; tb < 4; ++tb, ++t)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int r = ta * 8 + (lane >> 2), c = tb * 8 + 2 * (lane & 3) + h;
+            if (ta < tb || r <= c) {
+              S.G[0][r * LDG + c] = acc[t][h];
+              S.G[0][c * LDG + r] = acc[t][h];
+            }
+          }
     }
     __syncthreads();
   }
-  // partial tiles -> G[kh]; C frag: row ti*8 + lane/4, cols tj*8 + 2*(lane%4) + h
-#pragma unroll
-  for (int tj = 0; tj < 4; ++tj)
-#pragma unroll
-    for (int h = 0; h < 2; ++h)
-      S.G[kh][(ti * 8 + (lane >> 2)) * LDG + tj * 8 + 2 * (lane & 3) + h] = acc[tj][h];
-  __syncthreads();
-  for (int e = tid; e < BW * BW; e += kThreads) {
-    const int i = e / BW, j = e % BW;
-    S.G[0][i * LDG + j] += S.G[1][i * LDG + j];
-  }
-  __syncthreads();
 
   // ---------------- 2. convergence test on this pair -----------------------
   // Pair (i, j) is orthogonal enough when
@@ -280,25 +308,25 @@ __global__ void __launch_bounds__(kThreads, 3) svd_pair_kernel(SvdWs ws, int64_t
     for (int i = 0; i < 2; ++i)
 #pragma unroll
       for (int j = 0; j < 2; ++j) o[i][j][0] = o[i][j][1] = 0.0;
-    const int r0 = rt * 16;
+    // one LDS.128 per k-step: rows r0 + 2(lane/4) and +1 feed the "even" and
+    // "odd" 8-row tiles; results go back as STS.128 row pairs
+    const int r0 = rt * 16 + 2 * (lane >> 2);
 #pragma unroll
     for (int kk = 0; kk < 8; ++kk) {
-      const double* zc = Zs + (kk * 4 + (lane & 3)) * LDZ + r0 + (lane >> 2);
-      const double a0 = zc[0], a1 = zc[8];
+      const double2 a = *reinterpret_cast<const double2*>(Zs + (kk * 4 + (lane & 3)) * LDZ + r0);
 #pragma unroll
       for (int j = 0; j < 2; ++j) {
-        dmma884(o[0][j][0], o[0][j][1], a0, qf[kk][j]);
-        dmma884(o[1][j][0], o[1][j][1], a1, qf[kk][j]);
+        dmma884(o[0][j][0], o[0][j][1], a.x, qf[kk][j]);
+        dmma884(o[1][j][0], o[1][j][1], a.y, qf[kk][j]);
       }
     }
     __syncthreads();  // every warp has read its rows (the other n-half reads them too)
 #pragma unroll
-    for (int i = 0; i < 2; ++i)
+    for (int j = 0; j < 2; ++j)
 #pragma unroll
-      for (int j = 0; j < 2; ++j)
-#pragma unroll
-        for (int h = 0; h < 2; ++h)
-          Zs[((2 * nh + j) * 8 + 2 * (lane & 3) + h) * LDZ + r0 + i * 8 + (lane >> 2)] = o[i][j][h];
+      for (int h = 0; h < 2; ++h)
+        *reinterpret_cast<double2*>(Zs + ((2 * nh + j) * 8 + 2 * (lane & 3) + h) * LDZ + r0) =
+            make_double2(o[0][j][h], o[1][j][h]);
     __syncthreads();
     // chunk -> global (each column: RCH contiguous doubles)
     const int64_t rbase = (int64_t)ch * RCH;
