@@ -266,7 +266,8 @@ def transform_workload(args, dist, rank, ws):
 
     e2e_steps = max(1, min(args.steps, 5))
     e2e_ms = timed_region(e2e_step, e2e_steps, 1, dist)
-    assert torch.equal(y_pin, x_pin)
+    # a lifting round trip reproduces x to rounding (not bit-exactly): SPEC.md:124
+    assert float((y_pin - x_pin).norm() / x_pin.norm()) < 1e-12
     e2e = {"value": round(ws * bytes_step * e2e_steps / (e2e_ms * 1e-3) / 1e9, 3), "unit": "GB/s",
            "h2d_bytes_per_step": len(CFG2_LEVELS) * 8 * N,
            "d2h_bytes_per_step": len(CFG2_LEVELS) * 8 * N,
@@ -279,7 +280,7 @@ def transform_workload(args, dist, rank, ws):
         for L in CFG2_LEVELS:
             out = W.inverse_w(W.forward_w(x_host, L))
     np_s = time.perf_counter() - t
-    assert np.array_equal(out, x_host)
+    assert float(np.linalg.norm((out - x_host).ravel()) / np.linalg.norm(x_host.ravel())) < 1e-12
     e2e["numpy_dropin"] = {"value": round(bytes_step * n_np / np_s / 1e9, 3), "unit": "GB/s",
                            "api": "inverse_w(forward_w(numpy, L)) per L (pyramid returned to host)",
                            "h2d_bytes_per_step": len(CFG2_LEVELS) * 16 * N,
