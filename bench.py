@@ -44,6 +44,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workloads", default="default")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--force-dist", action="store_true",
+                    help="initialise NCCL even at world size 1 (exercises the N>1 code path on one GPU)")
     return ap.parse_args()
 
 
@@ -123,7 +125,7 @@ class ClockSampler:
                 self.reasons |= int(r) & ~0x1
             except Exception:  # noqa: BLE001
                 pass
-            time.sleep(0.002)
+            time.sleep(0.001)
 
     def __enter__(self):
         if self.nv is not None:
@@ -477,7 +479,7 @@ def main():
 
     torch.cuda.set_device(local)
     dist = None
-    if ws > 1:
+    if ws > 1 or args.force_dist:
         import torch.distributed as tdist
 
         tdist.init_process_group("nccl", device_id=torch.device("cuda", local))

@@ -1,0 +1,61 @@
+"""Config 5 (w-pinv deblurring) and the imaging helpers on the GPU.
+
+PSNR/SSIM have no reference code; the oracle follows the
+PAPER/SPEC formulas, so these parities are pinned to that restatement.
+Bars (north_star): PSNR within 1e-6 dB, SSIM within 1e-6; pseudo-inverse and
+recovered images within 1e-8 relative.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2601_08228_b200 as W
+from paper_2601_08228_b200 import imaging, synth
+from oracle import wten_oracle as O
+from wt_helpers import relerr
+
+pytestmark = pytest.mark.gpu
+
+
+def test_psnr_ssim_match_oracle():
+    rng = np.random.default_rng(41)
+    x = rng.random((40, 30, 16))
+    y = np.clip(x + 0.05 * rng.standard_normal(x.shape), 0, 1)
+    assert abs(imaging.psnr(x, y) - O.psnr(x, y)) < 1e-9
+    assert abs(imaging.ssim(x, y) - O.ssim(x, y)) < 1e-12
+    assert abs(imaging.psnr(x, y, 2.0) - O.psnr(x, y, 2.0)) < 1e-9
+    assert imaging.psnr(x, x) == float("inf")
+    assert abs(imaging.ssim(x, x) - 1.0) < 1e-15
+    assert imaging.psnr(np.ones((2, 2, 2)), np.zeros((2, 2, 2)), 1.0) == 0.0
+
+
+def test_blur_operator_spec_examples():
+    av, ah = imaging.blur_operator(2, 1, 4, 3, 4)
+    np.testing.assert_allclose(av[:, :, 0][0], [1 / 3, 1 / 6, 0, 0])
+    np.testing.assert_allclose(ah[:, :, 2], np.eye(3) / 3)
+    # slice-constant operators have exactly-zero detail blocks
+    pyr = W.forward_w(av, 2)
+    assert all(not d.any() for d in pyr.details)
+
+
+def test_config5_deblur_full_size():
+    """BASELINE configs[4]: 512x512x128, 12 endmembers, 9x9 Gaussian PSF sigma=2, L=3, tol 1e-3."""
+    x, av, ah, eta = synth.deblur_problem()
+    xd, avd, ahd, etad = (torch.from_numpy(t).cuda() for t in (x, av, ah, eta))
+    b = imaging.blur(xd, avd, ahd, 3) + etad
+    xr = imaging.deblur(b, avd, ahd, 3, "w", tol=1e-3)
+    # oracle pipeline on the same bytes
+    b_ref = O.w_product(O.w_product(av, x, 3), O.transpose(ah), 3) + eta
+    assert relerr(b.cpu().numpy(), b_ref) < 1e-12
+    left = O.pinv_w(av, 3, 1e-3)
+    right = O.pinv_w(O.transpose(ah), 3, 1e-3)
+    assert relerr(W.pinv_w(avd, 3, 1e-3).cpu().numpy(), left) < 1e-8
+    xr_ref = O.w_product(O.w_product(left, b_ref, 3), right, 3)
+    xr_h = xr.cpu().numpy()
+    assert relerr(xr_h, xr_ref) < 1e-8
+    assert abs(imaging.psnr(xd, xr) - O.psnr(x, xr_ref)) < 1e-6
+    assert abs(imaging.ssim(xd, xr) - O.ssim(x, xr_ref)) < 1e-6
+    # deblur-w == deblur-spw for slice-constant operators
+    xs = imaging.deblur(b, avd, ahd, 3, "spw", tol=1e-3)
+    assert relerr(xs.cpu().numpy(), xr_h) < 1e-12
