@@ -129,6 +129,29 @@ def frobenius_norm(t) -> float:
     return float(np.linalg.norm(np.asarray(t).ravel()))
 
 
+def inverse_tensor(a, levels):
+    """Blockwise inverse (algebra.py:62-91); raises ValueError naming
+    (level, slice) of the first singular slice, smooth block (level 0) first."""
+    a = np.asarray(a, dtype=np.float64)
+    smooth, details = lift_forward(a, levels)
+
+    def inv_stack(st, tag):
+        out = np.empty_like(st)
+        for k in range(st.shape[2]):
+            try:
+                m = np.linalg.inv(st[:, :, k])
+            except np.linalg.LinAlgError:
+                raise ValueError((tag, k)) from None
+            if not np.isfinite(m).all():
+                raise ValueError((tag, k))
+            out[:, :, k] = m
+        return out
+
+    s_inv = inv_stack(smooth, 0)
+    d_inv = [inv_stack(d, j) for j, d in enumerate(details, start=1)]
+    return lift_inverse(s_inv, d_inv)
+
+
 # ----------------------------------------------------------------------------
 # decomposition (decomposition.py)
 # ----------------------------------------------------------------------------

@@ -8,7 +8,14 @@ library or a CUDA device, compute calls raise ``NativeUnavailable``.
 """
 
 from ._native import NativeError, NativeUnavailable
-from .algebra import face_product, identity_tensor, orthogonal_tensor, slicewise_matmul, w_product
+from .algebra import (
+    face_product,
+    identity_tensor,
+    inverse_tensor,
+    orthogonal_tensor,
+    slicewise_matmul,
+    w_product,
+)
 from .decomposition import (
     SvdFactors,
     TruncationBound,
@@ -43,7 +50,7 @@ __version__ = "0.1.0"
 
 __all__ = [
     "NativeError", "NativeUnavailable",
-    "face_product", "identity_tensor", "orthogonal_tensor", "slicewise_matmul", "w_product",
+    "face_product", "identity_tensor", "inverse_tensor", "orthogonal_tensor", "slicewise_matmul", "w_product",
     "SvdFactors", "TruncationBound", "pinv_w", "pinv_w_via_factors", "sp_pinv_w", "sp_w_svd",
     "truncation_bound", "w_svd",
     "FormatError", "IoError", "LevelError", "OrthogonalityError", "RankError", "ShapeError",

@@ -106,6 +106,44 @@ def identity_tensor(n, p, levels):
     return inverse_w(constant_pyramid(np.eye(n), p, levels))
 
 
+def inverse_tensor(a, levels):
+    """Blockwise inverse: every wavelet-domain slice is matrix-inverted (algebra.py:62-91).
+
+    Each slice is inverted through the K4 SVD as V diag(1/s) U^T.  Raises
+    SingularSliceError(level, slice_index, cond) -- smooth block first (level 0),
+    then details 1..L, like the reference's loop -- when a slice is singular to
+    working precision (s_min <= n eps s_max) or inverts to non-finite values;
+    ``cond`` is s_max / s_min, the 2-norm condition number np.linalg.cond reports.
+    """
+    from .errors import SingularSliceError
+
+    a = _as_operand(a)
+    if a.shape[0] != a.shape[1]:
+        raise ShapeError(f"inverse needs square frontal slices, got {tuple(a.shape[:2])}")
+    _check_levels(a.shape[2], levels)
+    dev = _is_dev(a)
+    x = E.as_device(a)
+    n, _, p = x.shape
+    pyr = E.lift_forward(x, levels)
+    sigma, vec, info = E.svd(pyr, n)
+    smin, smax = sigma[:, -1], sigma[:, 0]
+    bad = (~torch.isfinite(sigma).all(dim=1)) | (smin <= n * 2.220446049250313e-16 * smax)
+    inv = E.pinv_blocks(pyr, sigma, vec, 0.0)
+    bad |= ~torch.isfinite(inv.reshape(p, -1)).all(dim=1)
+    if bool(bad.any()):
+        bad_h = bad.cpu().numpy()
+        s_h = sigma.cpu().numpy()
+        for tag, off, cnt in [E.block_slices(p, levels)[-1]] + E.block_slices(p, levels)[:-1]:
+            for k in range(cnt):
+                if bad_h[off + k]:
+                    lo, hi = s_h[off + k, -1], s_h[off + k, 0]
+                    cond = float(hi / lo) if lo > 0 and np.isfinite(hi / lo) else float("inf")
+                    level = 0 if tag == "s" else int(tag[1:])
+                    raise SingularSliceError(level, k, cond)
+    y = E.lift_inverse(inv, n, n, p, levels)
+    return y if dev else E.to_host(y)
+
+
 def orthogonal_tensor(q, p, levels, tol=1e-12):
     """Tensor whose every wavelet block is the orthogonal matrix ``q`` (algebra.py:102-112)."""
     q = np.asarray(q, dtype=np.float64)

@@ -64,6 +64,7 @@ CALLS = {
     "sp_w_svd(ones(3,4,4), 1, 3)": lambda: W.sp_w_svd(ones((3, 4, 4)), 1, 3),
     "pinv_w(ones(3,4,4), 3)": lambda: W.pinv_w(ones((3, 4, 4)), 3),
     "max_levels(0)": lambda: W.max_levels(0),
+    "inverse_tensor(ones(2,3,4), 1)": lambda: W.inverse_tensor(ones((2, 3, 4)), 1),
 }
 
 

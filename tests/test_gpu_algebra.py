@@ -108,3 +108,23 @@ def test_determinism():
     a = torch.from_numpy(rng.standard_normal((96, 80, 64))).cuda()
     b = torch.from_numpy(rng.standard_normal((80, 72, 64))).cuda()
     assert torch.equal(W.w_product(a, b, 3), W.w_product(a, b, 3))
+
+
+def test_ring_constructors_match_reference(golden):
+    import json
+    import os
+
+    from wt_helpers import GOLDEN
+
+    g = golden("ring.npz")
+    assert relerr(W.inverse_tensor(g["inv_x"], 2), g["inv_L2"]) < 1e-10
+    assert relerr(W.inverse_tensor(g["inv_x"], 3), g["inv_L3"]) < 1e-10
+    assert relerr(W.identity_tensor(4, 8, 2), g["identity_4_8_2"]) < 1e-15
+    assert relerr(W.orthogonal_tensor(g["orth_q"], 8, 3), g["orth_5_8_3"]) < 1e-14
+    errs = {e["call"]: e for e in json.load(open(os.path.join(GOLDEN, "errors.json")))["errors"]}
+    gi = golden("ring_inputs.npz")
+    for name, call in (("sing", "inverse_tensor(singular smooth)"),
+                       ("sing_d2", "inverse_tensor(zero d2 slice 0)")):
+        with pytest.raises(W.SingularSliceError) as ei:
+            W.inverse_tensor(gi[name], 2)
+        assert (ei.value.level, ei.value.slice_index) == (errs[call]["level"], errs[call]["slice_index"])

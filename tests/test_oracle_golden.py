@@ -141,3 +141,18 @@ def test_psnr_ssim_spec_examples():
     yc = y - y.mean(axis=(0, 1), keepdims=True)
     assert O.ssim(yc, -yc, 1.0) < 0
     assert abs(O.ssim(z, z) - 1.0) < 1e-15
+
+
+def test_ring_constructors_match_reference_fixtures(golden):
+    g = golden("ring.npz")
+    x = g["inv_x"]
+    assert relerr(O.inverse_tensor(x, 2), g["inv_L2"]) < 1e-12
+    assert relerr(O.inverse_tensor(x, 3), g["inv_L3"]) < 1e-12
+    eye = lambda k: np.broadcast_to(np.eye(6)[:, :, None], (6, 6, k)).copy()  # noqa: E731
+    ident = O.lift_inverse(eye(2), [eye(4), eye(2)])  # every wavelet block = I (algebra.py:54-59)
+    assert relerr(O.w_product(x, O.inverse_tensor(x, 2), 2), ident) < 1e-12
+    gi = golden("ring_inputs.npz")
+    for name, want in (("sing", (0, 0)), ("sing_d2", (2, 0))):
+        with pytest.raises(ValueError) as ei:
+            O.inverse_tensor(gi[name], 2)
+        assert ei.value.args[0] == want
