@@ -489,7 +489,8 @@ def main():
     _native.require_gpu()
 
     if args.workloads == "default":
-        wl = ["wsvd", "spwsvd", "deblur", "wproduct"] if ws == 1 else ["spwsvd_sharded"]
+        wl = (["wsvd", "spwsvd", "deblur", "wproduct"] if ws == 1
+              else ["spwsvd_fused", "spwsvd_sharded"])
     elif args.workloads == "none":
         wl = []
     else:
@@ -507,10 +508,11 @@ def main():
                 workloads[name] = deblur_workload(args)
             elif name == "wproduct":
                 workloads[name] = wproduct_workload(args)
-            elif name == "spwsvd_sharded":
+            elif name in ("spwsvd_sharded", "spwsvd_fused"):
                 from paper_2601_08228_b200 import sharded
 
-                workloads[name] = sharded.bench_sp_w_svd(dist, timed_region, steps=3, warmup=1)
+                workloads[name] = sharded.bench_sp_w_svd(dist, timed_region, steps=3, warmup=1,
+                                                         fused=name == "spwsvd_fused")
         except Exception as e:  # noqa: BLE001
             workloads[name] = {"error": f"{type(e).__name__}: {e}"}
 

@@ -80,6 +80,20 @@ int wt_lift_inv_f64(const double* pyr, int64_t n1, int64_t n2, int64_t p, int le
                     void* stream);
 
 /*
+ * K1 / K2 with the rows -> slices exchange fused in (multi-GPU, sharded.py).
+ * Same transform; packed slice s (slice_base <= s < p) of the caller's tubes is
+ * stored to / loaded from (double*)slice_ptrs[s - slice_base] + tube, where
+ * slice_ptrs (a DEVICE array) may point into other GPUs' symmetric-memory
+ * buffers: the stores / loads of the lifting kernel are the all-to-all.
+ */
+int wt_lift_fwd_f64_peer(const double* x, int64_t n1, int64_t n2, int64_t p, int levels,
+                         const unsigned long long* slice_ptrs, int64_t slice_base,
+                         uint64_t level_mask, void* stream);
+int wt_lift_inv_f64_peer(const unsigned long long* slice_ptrs, int64_t n1, int64_t n2, int64_t p,
+                         int levels, int64_t slice_base, uint64_t level_mask, double* y,
+                         void* stream);
+
+/*
  * K3 -- strided-batched FP64 GEMM on the DMMA tensor pipe (mma.sync f64).
  * Replaces the per-slice cblas_dgemm of slicewise_matmul (algebra.py:18-28),
  * _truncated_blocks (decomposition.py:70-72) and _pinv_stack (:162).

@@ -31,7 +31,11 @@ SIGNATURES = {
                                        ctypes.c_int, i64, u64, ctypes.c_void_p]),
     "wt_lift_inv_f64": (ctypes.c_int, [c_double_p, i64, i64, i64, ctypes.c_int, ctypes.c_int,
                                        i64, u64, c_double_p, ctypes.c_void_p]),
-    "wt_gemm_f64": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, i64, i64, i64, ctypes.c_double,
+    "wt_lift_fwd_f64_peer": (ctypes.c_int, [c_double_p, i64, i64, i64, ctypes.c_int, ctypes.c_void_p,
+                                            i64, u64, ctypes.c_void_p]),
+    "wt_lift_inv_f64_peer": (ctypes.c_int, [ctypes.c_void_p, i64, i64, i64, ctypes.c_int, i64, u64,
+                                            c_double_p, ctypes.c_void_p]),
+    "wt_gemm_f64":(ctypes.c_int, [ctypes.c_int, ctypes.c_int, i64, i64, i64, ctypes.c_double,
                                    c_double_p, i64, i64, c_double_p, i64, i64, ctypes.c_double,
                                    c_double_p, i64, i64, i64, ctypes.c_void_p]),
     "wt_svd_workspace_bytes": (ctypes.c_size_t, [i64, i64, i64]),

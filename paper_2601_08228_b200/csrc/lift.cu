@@ -254,9 +254,11 @@ int validate(int64_t n1, int64_t n2, int64_t p, int levels, int layout, int64_t 
 }  // namespace
 
 int lift_fwd_fast(const double* x, int64_t ntubes, int64_t p, int L, double* out,
-                  int64_t slice_base, uint64_t mask, cudaStream_t st);
+                  int64_t slice_base, uint64_t mask, cudaStream_t st,
+                  const unsigned long long* tab = nullptr);
 int lift_inv_fast(const double* pyr, int64_t ntubes, int64_t p, int L, double* y,
-                  int64_t slice_base, uint64_t mask, cudaStream_t st);
+                  int64_t slice_base, uint64_t mask, cudaStream_t st,
+                  const unsigned long long* tab = nullptr);
 }  // namespace wt
 
 using namespace wt;
@@ -311,4 +313,33 @@ extern "C" int wt_lift_inv_f64(const double* pyr, int64_t n1, int64_t n2, int64_
   WT_REQUIRE(grid.y <= 65535, "lifting: too many band chunks");
   lift_inv_kernel<<<grid, kThreads, smem, (cudaStream_t)stream>>>(pyr, y, g, bulk);
   return check_launch("wt_lift_inv_f64");
+}
+
+extern "C" int wt_lift_fwd_f64_peer(const double* x, int64_t n1, int64_t n2, int64_t p, int levels,
+                                    const unsigned long long* slice_ptrs, int64_t slice_base,
+                                    uint64_t level_mask, void* stream) {
+  int st = validate(n1, n2, p, levels, WT_LAYOUT_SLICE_MAJOR, slice_base);
+  if (st) return st;
+  WT_REQUIRE(slice_ptrs != nullptr, "lifting: null slice pointer table");
+  if (n1 * n2 == 0) return WT_OK;
+  // dummy non-null base: every address comes from the table
+  st = lift_fwd_fast(x, n1 * n2, p, levels, reinterpret_cast<double*>(16), slice_base, level_mask,
+                     (cudaStream_t)stream, slice_ptrs);
+  if (st == WT_ERR_UNSUPPORTED)
+    set_error("wt_lift_fwd_f64_peer: needs levels >= 1, even p, 16-byte aligned x");
+  return st;
+}
+
+extern "C" int wt_lift_inv_f64_peer(const unsigned long long* slice_ptrs, int64_t n1, int64_t n2,
+                                    int64_t p, int levels, int64_t slice_base, uint64_t level_mask,
+                                    double* y, void* stream) {
+  int st = validate(n1, n2, p, levels, WT_LAYOUT_SLICE_MAJOR, slice_base);
+  if (st) return st;
+  WT_REQUIRE(slice_ptrs != nullptr, "lifting: null slice pointer table");
+  if (n1 * n2 == 0) return WT_OK;
+  st = lift_inv_fast(reinterpret_cast<const double*>(16), n1 * n2, p, levels, y, slice_base,
+                     level_mask, (cudaStream_t)stream, slice_ptrs);
+  if (st == WT_ERR_UNSUPPORTED)
+    set_error("wt_lift_inv_f64_peer: needs levels >= 1, even p, even n1*n2, aligned y");
+  return st;
 }

@@ -33,7 +33,18 @@ struct FGeom {
   int64_t slice_base;
   uint64_t mask;
   uint32_t nqt, ntiles;
+  // Optional per-slice row pointers (peer / symmetric-memory addressing): when
+  // set, packed slice s of this rank's tubes lives at (double*)tab[s - slice_base]
+  // (+ tube index) instead of out + (s - slice_base) * ntubes.  This is how the
+  // sharded pipeline fuses its rows -> slices exchange into K1 / K2: the stores
+  // (loads) go straight to (from) the owning GPU's buffer over NVLink.
+  const unsigned long long* tab;
 };
+
+__device__ __forceinline__ double* slice_row(const FGeom& g, double* base, int64_t s) {
+  return g.tab ? reinterpret_cast<double*>(g.tab[s - g.slice_base])
+               : base + (s - g.slice_base) * g.ntubes;
+}
 
 __device__ __forceinline__ int64_t doff(int64_t p, int j) { return p - (p >> (j - 1)); }
 __device__ __forceinline__ int64_t soff(int64_t p, int L) { return p - (p >> L); }
@@ -70,19 +81,19 @@ __device__ __forceinline__ void fwd_stage(const double* src, int ps, double* dst
       const int lev = l0 + w + 1;
       const int n = V >> (w + 1);
       const bool want = (g.mask >> lev) & 1;
-      double* o = out + (doff(g.p, lev) + (t0 >> lev) + (int64_t)c * n - g.slice_base) * g.ntubes + q0 + r;
+      const int64_t s0 = doff(g.p, lev) + (t0 >> lev) + (int64_t)c * n;
 #pragma unroll
       for (int i = 0; i < (V >> 1); ++i) {
         if (i < n) {
           const double d = __dsub_rn(v[2 * i], v[2 * i + 1]);
           const double s = __dadd_rn(v[2 * i + 1], __dmul_rn(d, 0.5));
-          if (want) o[(int64_t)i * g.ntubes] = d;
+          if (want) slice_row(g, out, s0 + i)[q0 + r] = d;
           v[i] = s;
         }
       }
     }
     if (last) {
-      if (g.mask & 1) out[(soff(g.p, g.L) + (t0 >> g.L) + c - g.slice_base) * g.ntubes + q0 + r] = v[0];
+      if (g.mask & 1) slice_row(g, out, soff(g.p, g.L) + (t0 >> g.L) + c)[q0 + r] = v[0];
     } else {
       dst[r * pd + c] = v[0];
     }
@@ -218,11 +229,11 @@ __global__ void __launch_bounds__(kT) inv_persistent(const double* __restrict__ 
       const int rows = smooth ? (CT >> g.L) : (CT >> j);
       const int row0 = smooth ? CT - (CT >> g.L) : drow(CT, j);
       const int64_t s0 = smooth ? soff(g.p, g.L) + (t0 >> g.L) : doff(g.p, j) + (t0 >> j);
-      const double* base = pyr + (s0 - g.slice_base) * g.ntubes + q0;
       for (int e = threadIdx.x; e < rows * CPR; e += kT) {
         const int rr = e / CPR, v = (e % CPR) * 2;
         const bool ok = v < tq;
-        cp_async_zfill<16>(dstb + (row0 + rr) * TQ + v, base + (int64_t)rr * g.ntubes + (ok ? v : 0), ok);
+        const double* src = slice_row(g, const_cast<double*>(pyr), s0 + rr) + q0 + (ok ? v : 0);
+        cp_async_zfill<16>(dstb + (row0 + rr) * TQ + v, src, ok);
       }
     }
     cp_async_commit();
@@ -304,10 +315,11 @@ int launch(K kern, size_t smem, uint32_t ntiles, cudaStream_t st, const double* 
 
 // Returns WT_ERR_UNSUPPORTED when the fast path does not apply (caller falls back).
 int lift_fwd_fast(const double* x, int64_t ntubes, int64_t p, int L, double* out,
-                  int64_t slice_base, uint64_t mask, cudaStream_t st) {
+                  int64_t slice_base, uint64_t mask, cudaStream_t st,
+                  const unsigned long long* tab) {
   using namespace fast;
   if (L < 1 || p % 2 || (uintptr_t)x % 16) return WT_ERR_UNSUPPORTED;
-  FGeom g{ntubes, p, L, 0, 0, 0, 0, slice_base, mask, 0, 0};
+  FGeom g{ntubes, p, L, 0, 0, 0, 0, slice_base, mask, 0, 0, tab};
   int TQ = 0;
   if (!plan(g, TQ)) return WT_ERR_UNSUPPORTED;
   const size_t smem = ((size_t)2 * TQ * g.LDT + (size_t)TQ * (g.LDA0 + g.LDA1)) * sizeof(double);
@@ -320,11 +332,12 @@ int lift_fwd_fast(const double* x, int64_t ntubes, int64_t p, int L, double* out
 }
 
 int lift_inv_fast(const double* pyr, int64_t ntubes, int64_t p, int L, double* y,
-                  int64_t slice_base, uint64_t mask, cudaStream_t st) {
+                  int64_t slice_base, uint64_t mask, cudaStream_t st,
+                  const unsigned long long* tab) {
   using namespace fast;
   if (L < 1 || p % 2 || ntubes % 2 || (uintptr_t)y % 16 || (uintptr_t)pyr % 16)
     return WT_ERR_UNSUPPORTED;
-  FGeom g{ntubes, p, L, 0, 0, 0, 0, slice_base, mask, 0, 0};
+  FGeom g{ntubes, p, L, 0, 0, 0, 0, slice_base, mask, 0, 0, tab};
   int TQ = 0;
   if (!plan(g, TQ)) return WT_ERR_UNSUPPORTED;
   const size_t smem = ((size_t)2 * g.CT * TQ + (size_t)2 * TQ * g.LDA0) * sizeof(double);

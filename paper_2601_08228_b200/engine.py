@@ -99,6 +99,29 @@ def lift_inverse(buf: torch.Tensor, n1: int, n2: int, p: int, levels: int,
     return out
 
 
+def lift_forward_peer(x: torch.Tensor, levels: int, table: torch.Tensor, mask: int = N.MASK_ALL,
+                      slice_base: int = 0) -> None:
+    """K1 storing packed slice s of x's tubes at table[s - slice_base] (device int64 addresses,
+    possibly on peer GPUs): the fused rows -> slices exchange."""
+    lib = N.require_gpu()
+    n1, n2, p = x.shape
+    assert table.dtype == torch.int64 and table.is_cuda and table.numel() == p - slice_base
+    N.check(lib.wt_lift_fwd_f64_peer(_ptr(x), n1, n2, p, levels, _ptr(table), slice_base,
+                                     mask & N.MASK_ALL, _stream()), "wt_lift_fwd_f64_peer")
+
+
+def lift_inverse_peer(table: torch.Tensor, n1: int, n2: int, p: int, levels: int,
+                      mask: int = N.MASK_ALL, slice_base: int = 0,
+                      out: torch.Tensor | None = None) -> torch.Tensor:
+    """K2 loading packed slice s of this rank's tubes from table[s - slice_base]."""
+    lib = N.require_gpu()
+    if out is None:
+        out = torch.empty((n1, n2, p), dtype=F64, device=table.device)
+    N.check(lib.wt_lift_inv_f64_peer(_ptr(table), n1, n2, p, levels, slice_base, mask & N.MASK_ALL,
+                                     _ptr(out), _stream()), "wt_lift_inv_f64_peer")
+    return out
+
+
 # ------------------------------------------------------------------ GEMM ----
 
 def gemm(a: torch.Tensor, b: torch.Tensor, trans_a: bool = False, trans_b: bool = False,

@@ -183,8 +183,85 @@ def pinv_w_sharded(x_local, levels, n1, tol=1e-12, group=None, ops=None):
     return ops.inverse(back, out_rows[me], n1, p, levels, N.MASK_ALL, 0)
 
 
+def peer_slice_table(ptrs, ks, row0, n1, n2, elem=8):
+    """Address of this rank's row block in the owner's slice buffer, per coarse slice.
+
+    Slice s (0 <= s < sum(ks)) is owned by the rank g with offsets(ks)[g] <= s <
+    offsets(ks)[g] + ks[g]; the owner's buffer holds its slices as full
+    (n1, n2) row-major matrices, and this rank's rows start at row ``row0``.
+    Pure integer math (tested on CPU); ``ptrs`` are the symmetric buffers' base
+    addresses on every rank.
+    """
+    starts = offsets(ks)
+    tab = []
+    for g, (st, k) in enumerate(zip(starts, ks)):
+        for j in range(k):
+            tab.append(int(ptrs[g]) + ((j * n1 + row0) * n2) * elem)
+    return tab
+
+
+_SYMM = {}
+
+
+def _symm_pair(numel, device, group):
+    """Two cached symmetric-memory buffers (+ handles) of `numel` doubles."""
+    import torch.distributed._symmetric_memory as symm_mem
+
+    gname = (group or dist.group.WORLD).group_name
+    key = (numel, str(device), gname)
+    if key not in _SYMM:
+        bufs = []
+        for _ in range(2):
+            t = symm_mem.empty(numel, dtype=torch.float64, device=device)
+            bufs.append((t, symm_mem.rendezvous(t, gname)))
+        _SYMM[key] = bufs
+    return _SYMM[key]
+
+
+def sp_w_svd_fused(x_local, r, levels, n1, group=None):
+    """sp-w-svd of a row-sharded cube with the exchange fused into K1 / K2.
+
+    K1 stores each coarse slice row block straight into the owning GPU's
+    symmetric-memory buffer (peer stores over NVLink), so the owner holds full
+    (n1, n2) slices without an all-to-all or a permute; after a device-side
+    barrier every rank decomposes its slices in place into a second symmetric
+    buffer, and K2 loads its rows of every reconstructed slice from the owners
+    (peer loads).  Same result as :func:`sp_w_svd_sharded`.
+    """
+    G = dist.get_world_size(group)
+    me = dist.get_rank(group)
+    R, n2, p = x_local.shape
+    rows = splits(n1, G)
+    assert R == rows[me], f"rank {me} holds {R} rows, expected {rows[me]}"
+    _check_rank(r, n1, n2)
+    _check_levels(p, levels)
+    m = p >> levels
+    K, base = 2 * m, p - 2 * m
+    ks = splits(K, G)
+    row0 = sum(rows[:me])
+    mask = E.level_mask(levels, smooth=True, details=[levels])
+    dev = x_local.device
+    (recv, h_recv), (recb, h_rec) = _symm_pair(max(ks) * n1 * n2, dev, group)
+    tab_f = torch.tensor(peer_slice_table(h_recv.buffer_ptrs, ks, row0, n1, n2), dtype=torch.int64,
+                         device=dev)
+    tab_i = torch.tensor(peer_slice_table(h_rec.buffer_ptrs, ks, row0, n1, n2), dtype=torch.int64,
+                         device=dev)
+    E.lift_forward_peer(x_local.contiguous(), levels, tab_f, mask, base)
+    h_recv.barrier(channel=0)                   # every rank's peer stores have landed
+    k_me = ks[me]
+    if k_me:
+        full = recv[:k_me * n1 * n2].view(k_me, n1, n2)
+        sigma, vec, info = E.svd(full, r)
+        E.raise_if_failed(info)
+        E.truncated_recon(full, sigma, vec, r, out=recb[:k_me * n1 * n2].view(k_me, n1, n2))
+    h_rec.barrier(channel=0)                    # every owner's reconstruction is ready
+    y = E.lift_inverse_peer(tab_i, R, n2, p, levels, mask, base)
+    h_rec.barrier(channel=1)                    # all peer loads done before buffers are reused
+    return y
+
+
 def bench_sp_w_svd(dist_mod, timed_region, steps=3, warmup=1, shape=(1024, 1024, 256), r=30,
-                   levels=4):
+                   levels=4, fused=False):
     """Config 4 strong-scaled over the group (rows sharded; see bench.py)."""
     from . import synth
 
@@ -198,13 +275,17 @@ def bench_sp_w_svd(dist_mod, timed_region, steps=3, warmup=1, shape=(1024, 1024,
     del cube
     out = {}
 
+    fn = sp_w_svd_fused if fused else sp_w_svd_sharded
+
     def step(record):
-        out["y"] = sp_w_svd_sharded(x, r, levels, n1)
+        out["y"] = fn(x, r, levels, n1)
 
     ms = timed_region(step, steps, warmup, dist_mod)
     total = n1 * n2 * p
     k = 2 * (p >> levels)
+    how = ("peer stores/loads fused into K1/K2 (symmetric memory)" if fused
+           else "NCCL all-to-all")
     return {"config": f"sp_w_svd {n1}x{n2}x{p} rank {r} L={levels}, rows sharded over {G} GPUs, "
-                      f"{k} coarse slices exchanged by NCCL all-to-all",
+                      f"{k} coarse slices exchanged by {how}",
             "metric": "tensor-elems/s", "value": total * steps / (ms * 1e-3), "ms_per_call": ms / steps,
             "scaling": "strong", "exchange_bytes_per_rank": 2 * 8 * k * rows[me] * n2}

@@ -41,3 +41,13 @@ def test_sharded_equals_single_gpu(nccl1):
     assert relerr(ws.cpu().numpy(), O.w_svd(x, 6, 2)["recon"]) < 1e-10
     pv = sharded.pinv_w_sharded(xd, 2, 64)
     assert relerr(pv.cpu().numpy(), O.pinv_w(x, 2)) < 1e-9
+
+
+def test_fused_exchange_equals_nccl_path(nccl1):
+    """K1/K2 with the exchange fused in (peer-pointer tables over symmetric memory)."""
+    x = np.random.default_rng(32).standard_normal((64, 48, 32))
+    xd = torch.from_numpy(x).cuda()
+    for _ in range(2):  # second call reuses the cached symmetric buffers
+        fz = sharded.sp_w_svd_fused(xd, 6, 3, 64)
+        assert torch.equal(fz, sharded.sp_w_svd_sharded(xd, 6, 3, 64))
+    assert relerr(fz.cpu().numpy(), O.sp_w_svd(x, 6, 3)) < 1e-10

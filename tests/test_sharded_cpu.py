@@ -101,6 +101,54 @@ def test_sharded_pipelines_match_oracle(ws, case):
     np.testing.assert_allclose(pv, O.pinv_w(x, L), rtol=0, atol=1e-10)
 
 
+@pytest.mark.parametrize("G,n1,n2,p,L", [(2, 12, 10, 16, 3), (3, 10, 7, 8, 2), (4, 9, 6, 8, 3),
+                                         (8, 16, 4, 32, 4)])
+def test_fused_peer_tables_assemble_full_slices(G, n1, n2, p, L):
+    """Simulate G ranks' fused K1 stores / K2 loads through sharded.peer_slice_table
+    with fake per-rank base addresses: every owner must end up holding full
+    coarse slices, and every rank must read back exactly its rows."""
+    from paper_2601_08228_b200 import sharded
+
+    x = np.random.default_rng(5).standard_normal((n1, n2, p))
+    m = p >> L
+    K, base = 2 * m, p - 2 * m
+    ks = sharded.splits(K, G)
+    rows = sharded.splits(n1, G)
+    span = 1 << 40
+    ptrs = [(g + 1) * span for g in range(G)]
+    bufs = [np.full(max(ks) * n1 * n2, np.nan) for _ in range(G)]
+
+    def locate(addr):
+        g = addr // span - 1
+        off = addr - ptrs[g]
+        assert off % 8 == 0
+        return g, off // 8
+
+    r0 = 0
+    for me in range(G):                      # K1 of every rank: stores via its table
+        tab = sharded.peer_slice_table(ptrs, ks, r0, n1, n2)
+        assert len(tab) == K
+        s, d = O.lift_forward(x[r0:r0 + rows[me]], L)
+        coarse = O.packed_slices(s, d)[base:]            # (K, R, n2) of my rows
+        for k in range(K):
+            g, off = locate(tab[k])
+            bufs[g][off:off + rows[me] * n2] = coarse[k].ravel()
+        r0 += rows[me]
+    s, d = O.lift_forward(x, L)
+    full = O.packed_slices(s, d)[base:]
+    for g, st in enumerate(sharded.offsets(ks)):          # owners hold full slices
+        got = bufs[g][:ks[g] * n1 * n2].reshape(ks[g], n1, n2)
+        assert np.array_equal(got, full[st:st + ks[g]])
+    r0 = 0
+    for me in range(G):                      # K2 of every rank: loads via its table
+        tab = sharded.peer_slice_table(ptrs, ks, r0, n1, n2)
+        for k in range(K):
+            g, off = locate(tab[k])
+            assert np.array_equal(bufs[g][off:off + rows[me] * n2].reshape(rows[me], n2),
+                                  full[k, r0:r0 + rows[me]])
+        r0 += rows[me]
+
+
 def test_splits():
     from paper_2601_08228_b200 import sharded
 
