@@ -37,12 +37,14 @@ struct GemmArgs {
 
 template <int BM, int BN, bool TA, bool TB>
 struct SmemLayout {
-  // A tile: !TA -> [BM][BK+4] (k fastest), TA -> [BK][BM+4] (m fastest)
-  static constexpr int A_LD = TA ? (BM + 4) : (BK + 4);
-  static constexpr int A_ELEMS = TA ? BK * (BM + 4) : BM * (BK + 4);
-  // B tile: !TB -> [BK][BN+4] (n fastest), TB -> [BN][BK+4] (k fastest)
-  static constexpr int B_LD = TB ? (BK + 4) : (BN + 4);
-  static constexpr int B_ELEMS = TB ? BN * (BK + 4) : BK * (BN + 4);
+  // Fragments are read for k pairs (2k, 2k+1) per lane.  k-contiguous tiles
+  // ([m][k], [n][k]) are read as LDS.128 with a pitch = 8 (mod 16) doubles;
+  // m/n-contiguous tiles ([k][m], [k][n]) as two LDS.64 with a pitch
+  // = 2 (mod 16): both patterns are bank-conflict-free.
+  static constexpr int A_LD = TA ? (BM + 2) : (BK + 8);
+  static constexpr int A_ELEMS = TA ? BK * A_LD : BM * A_LD;
+  static constexpr int B_LD = TB ? (BK + 8) : (BN + 2);
+  static constexpr int B_ELEMS = TB ? BN * B_LD : BK * B_LD;
   static constexpr int STAGE_ELEMS = A_ELEMS + B_ELEMS;
   static constexpr size_t BYTES = (size_t)STAGES * STAGE_ELEMS * sizeof(double);
 };
@@ -120,24 +122,32 @@ __global__ void __launch_bounds__(WM* WN * 32) gemm_f64_kernel(GemmArgs g) {
       }
       const double* As = smem + (kt % STAGES) * SL::STAGE_ELEMS;
       const double* Bs = As + SL::A_ELEMS;
+      // Each lane feeds the k-slot pair (2k, 2k+1), k = lane%4, of an 8-wide
+      // k-step into two DMMAs (any fixed k -> slot map is valid as long as
+      // the A and B fragments use the same one).
 #pragma unroll
-      for (int ks = 0; ks < BK; ks += 4) {
-        double af[FM], bf[FN];
-        const int kk = ks + (lane & 3);
+      for (int ks = 0; ks < BK; ks += 8) {
+        double2 af[FM], bf[FN];
+        const int kk = ks + 2 * (lane & 3);
 #pragma unroll
         for (int i = 0; i < FM; ++i) {
           const int mm = wm0 + i * 8 + (lane >> 2);
-          af[i] = TA ? As[kk * SL::A_LD + mm] : As[mm * SL::A_LD + kk];
+          if (TA) af[i] = make_double2(As[kk * SL::A_LD + mm], As[(kk + 1) * SL::A_LD + mm]);
+          else af[i] = *reinterpret_cast<const double2*>(As + mm * SL::A_LD + kk);
         }
 #pragma unroll
         for (int j = 0; j < FN; ++j) {
           const int nn = wn0 + j * 8 + (lane >> 2);
-          bf[j] = TB ? Bs[nn * SL::B_LD + kk] : Bs[kk * SL::B_LD + nn];
+          if (TB) bf[j] = *reinterpret_cast<const double2*>(Bs + nn * SL::B_LD + kk);
+          else bf[j] = make_double2(Bs[kk * SL::B_LD + nn], Bs[(kk + 1) * SL::B_LD + nn]);
         }
 #pragma unroll
         for (int i = 0; i < FM; ++i)
 #pragma unroll
-          for (int j = 0; j < FN; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+          for (int j = 0; j < FN; ++j) {
+            dmma884(acc[i][j][0], acc[i][j][1], af[i].x, bf[j].x);
+            dmma884(acc[i][j][0], acc[i][j][1], af[i].y, bf[j].y);
+          }
       }
     }
     cp_async_wait<0>();
@@ -152,13 +162,17 @@ __global__ void __launch_bounds__(WM* WN * 32) gemm_f64_kernel(GemmArgs g) {
       for (int j = 0; j < FN; ++j) {
         const int64_t gn = n0 + wn0 + j * 8 + 2 * (lane & 3);
         double* cp = C + gm * g.ldc + gn;
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          if (gn + h < g.N) {
-            double v = g.alpha * acc[i][j][h];
-            if (g.beta != 0.0) v = fma(g.beta, cp[h], v);
-            cp[h] = v;
+        double v0 = g.alpha * acc[i][j][0], v1 = g.alpha * acc[i][j][1];
+        if (gn + 1 < g.N && ((reinterpret_cast<uintptr_t>(cp) & 15) == 0)) {
+          if (g.beta != 0.0) {
+            const double2 o = *reinterpret_cast<const double2*>(cp);
+            v0 = fma(g.beta, o.x, v0);
+            v1 = fma(g.beta, o.y, v1);
           }
+          *reinterpret_cast<double2*>(cp) = make_double2(v0, v1);
+        } else {
+          if (gn < g.N) cp[0] = g.beta != 0.0 ? fma(g.beta, cp[0], v0) : v0;
+          if (gn + 1 < g.N) cp[1] = g.beta != 0.0 ? fma(g.beta, cp[1], v1) : v1;
         }
       }
     }
