@@ -15,6 +15,10 @@
 //   * the tile height TQ (tubes) is a compile-time constant, so every index
 //     split is a shift/mask; consecutive threads own consecutive tubes, so each
 //     packed slice row is written / read as TQ*8-byte bursts.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <stdlib.h>
+
 #include <algorithm>
 
 #include "wt_common.cuh"
@@ -24,6 +28,7 @@ namespace fast {
 
 constexpr int kT = 256;
 constexpr int kMaxElems = 4096;  // TQ * CT per tile (32 KB)
+constexpr int kMaxTmaLevels = 12;
 
 struct FGeom {
   int64_t ntubes, p;
@@ -209,20 +214,64 @@ __device__ __forceinline__ void inv_stage(const double* I, const double* ssrc, i
   }
 }
 
-template <int TQ>
+// One 2-D TMA descriptor per detail level j (box: TQ tubes x CT>>j slices of the
+// packed buffer viewed as [slices][tubes]); the smooth block reuses level L's.
+struct TmaMaps {
+  CUtensorMap m[kMaxTmaLevels + 1];
+};
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int x, int y,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(bar))
+      : "memory");
+}
+
+template <int TQ, bool TMA>
 __global__ void __launch_bounds__(kT) inv_persistent(const double* __restrict__ pyr,
-                                                     double* __restrict__ y, FGeom g) {
+                                                     double* __restrict__ y, FGeom g,
+                                                     const __grid_constant__ TmaMaps maps) {
   extern __shared__ __align__(128) double sm[];
+  __shared__ __align__(8) uint64_t bar[2];
   const int CT = g.CT;
   // pointer arithmetic on `sm` (not arrays of pointers) keeps every access LDS/STS
   double* const aux0 = sm + 2 * CT * TQ;
   double* const aux1 = aux0 + TQ * g.LDA0;
   constexpr int CPR = TQ / 2;  // 16-byte chunks per row
+  if (TMA) {
+    if (threadIdx.x == 0) {
+      mbar_init(&bar[0], 1);
+      mbar_init(&bar[1], 1);
+      fence_mbar_init();
+    }
+    __syncthreads();
+  }
   auto issue = [&](uint32_t t, int buf) {
     int64_t q0, t0;
     int tq;
     tile_at<TQ>(g, t, q0, tq, t0);
     double* dstb = sm + buf * (CT * TQ);
+    if (TMA) {
+      // thread 0 issues one 2-D TMA box per level block (SASS UTMALDG);
+      // out-of-range tubes of the last tile arrive zero-filled
+      if (threadIdx.x == 0) {
+        uint32_t bytes = 0;
+        for (int j = 1; j <= g.L + 1; ++j)
+          if ((g.mask >> (j > g.L ? 0 : j)) & 1) bytes += (CT >> min(j, g.L)) * TQ * 8;
+        mbar_expect_tx(&bar[buf], bytes);
+        for (int j = 1; j <= g.L + 1; ++j) {
+          const bool smooth = j > g.L;
+          if (!((g.mask >> (smooth ? 0 : j)) & 1)) continue;
+          const int row0 = smooth ? CT - (CT >> g.L) : drow(CT, j);
+          const int64_t s0 = smooth ? soff(g.p, g.L) + (t0 >> g.L) : doff(g.p, j) + (t0 >> j);
+          tma_load_2d(dstb + row0 * TQ, &maps.m[smooth ? g.L : j], (int)q0,
+                      (int)(s0 - g.slice_base), &bar[buf]);
+        }
+      }
+      return;
+    }
     for (int j = 1; j <= g.L + 1; ++j) {
       const bool smooth = j > g.L;
       if (!((g.mask >> (smooth ? 0 : j)) & 1)) continue;
@@ -240,13 +289,17 @@ __global__ void __launch_bounds__(kT) inv_persistent(const double* __restrict__ 
   };
   uint32_t t = blockIdx.x;
   if (t < g.ntiles) issue(t, 0);
-  else cp_async_commit();
+  else if (!TMA) cp_async_commit();
   for (int i = 0; t < g.ntiles; ++i, t += gridDim.x) {
     const int buf = i & 1;
     if (t + gridDim.x < g.ntiles) issue(t + gridDim.x, buf ^ 1);
-    else cp_async_commit();
-    cp_async_wait<1>();
-    __syncthreads();
+    else if (!TMA) cp_async_commit();
+    if (TMA) {
+      mbar_wait(&bar[buf], (i >> 1) & 1);
+    } else {
+      cp_async_wait<1>();
+      __syncthreads();
+    }
     int64_t q0, t0;
     int tq;
     tile_at<TQ>(g, t, q0, tq, t0);
@@ -272,7 +325,7 @@ __global__ void __launch_bounds__(kT) inv_persistent(const double* __restrict__ 
     }
     __syncthreads();  // input buffer / stage buffers are reused by later tiles
   }
-  cp_async_wait<0>();
+  if (!TMA) cp_async_wait<0>();
 }
 
 bool plan(FGeom& g, int& TQ) {
@@ -299,16 +352,49 @@ bool plan(FGeom& g, int& TQ) {
   return false;
 }
 
-template <typename K>
+template <typename K, typename... Extra>
 int launch(K kern, size_t smem, uint32_t ntiles, cudaStream_t st, const double* a, double* b,
-           const FGeom& g, const char* what) {
+           const FGeom& g, const char* what, const Extra&... extra) {
   WT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int per_sm = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kT, smem) != cudaSuccess || per_sm < 1)
     per_sm = 1;
   const int grid = (int)std::min<int64_t>(ntiles, (int64_t)num_sms() * per_sm);
-  kern<<<grid, kT, smem, st>>>(a, b, g);
+  kern<<<grid, kT, smem, st>>>(a, b, g, extra...);
   return check_launch(what);
+}
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda).
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+// Descriptors for the packed buffer [nslices][ntubes] with boxes TQ x (CT >> j).
+bool make_maps(TmaMaps& M, const double* pyr, const FGeom& g, int TQ) {
+  auto enc = encode_fn();
+  if (!enc || g.L > kMaxTmaLevels) return false;
+  const int64_t nslices = g.p - g.slice_base;
+  const cuuint64_t dims[2] = {(cuuint64_t)g.ntubes, (cuuint64_t)nslices};
+  const cuuint64_t strides[1] = {(cuuint64_t)g.ntubes * sizeof(double)};
+  const cuuint32_t estr[2] = {1, 1};
+  for (int j = 1; j <= g.L; ++j) {
+    const cuuint32_t box[2] = {(cuuint32_t)TQ, (cuuint32_t)(g.CT >> j)};
+    if (enc(&M.m[j], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(pyr), dims, strides, box,
+            estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return false;
+  }
+  return true;
 }
 
 }  // namespace fast
@@ -342,11 +428,16 @@ int lift_inv_fast(const double* pyr, int64_t ntubes, int64_t p, int L, double* y
   if (!plan(g, TQ)) return WT_ERR_UNSUPPORTED;
   const size_t smem = ((size_t)2 * g.CT * TQ + (size_t)2 * TQ * g.LDA0) * sizeof(double);
   if (smem > 200 * 1024) return WT_ERR_UNSUPPORTED;
+  static TmaMaps maps;  // host copy; passed by value as a __grid_constant__ parameter
+  // TMA boxes: 16 tubes (128-byte rows) x <= 256 slices, 16-byte-multiple stride
+  if (!tab && TQ == 16 && (g.CT >> 1) <= 256 && !getenv("WT_LIFT_NO_TMA") &&
+      make_maps(maps, pyr, g, TQ))
+    return launch(inv_persistent<16, true>, smem, g.ntiles, st, pyr, y, g, "wt_lift_inv_f64", maps);
   switch (TQ) {
-    case 16: return launch(inv_persistent<16>, smem, g.ntiles, st, pyr, y, g, "wt_lift_inv_f64");
-    case 8: return launch(inv_persistent<8>, smem, g.ntiles, st, pyr, y, g, "wt_lift_inv_f64");
-    case 4: return launch(inv_persistent<4>, smem, g.ntiles, st, pyr, y, g, "wt_lift_inv_f64");
-    default: return launch(inv_persistent<2>, smem, g.ntiles, st, pyr, y, g, "wt_lift_inv_f64");
+    case 16: return launch(inv_persistent<16, false>, smem, g.ntiles, st, pyr, y, g, "wt_lift_inv_f64", maps);
+    case 8: return launch(inv_persistent<8, false>, smem, g.ntiles, st, pyr, y, g, "wt_lift_inv_f64", maps);
+    case 4: return launch(inv_persistent<4, false>, smem, g.ntiles, st, pyr, y, g, "wt_lift_inv_f64", maps);
+    default: return launch(inv_persistent<2, false>, smem, g.ntiles, st, pyr, y, g, "wt_lift_inv_f64", maps);
   }
 }
 
