@@ -68,19 +68,35 @@ template <int TQ, int W>
 __device__ __forceinline__ void fwd_stage(const double* src, int ps, double* dst, int pd, int l0,
                                           int len, const FGeom g, double* __restrict__ out,
                                           int64_t q0, int tq, int64_t t0) {
+  // A thread lifts the same 2^W-band chunk of TWO adjacent tubes (r, r+1), so
+  // every detail / smooth output is one 16-byte store (adjacent tubes are
+  // adjacent in a packed slice row): half the store instructions, full sectors.
   constexpr int V = 1 << W;
-  const int items = TQ * (len >> W);
+  constexpr int HQ = TQ / 2;
+  const int items = HQ * (len >> W);
   const bool last = (l0 + W == g.L);
   for (int e = threadIdx.x; e < items; e += kT) {
-    const int r = e & (TQ - 1), c = e / TQ;
+    const int r = 2 * (e & (HQ - 1)), c = e / HQ;
     if (r >= tq) continue;
-    double v[V];
+    const bool two = r + 1 < tq;
+    double v[2][V];
 #pragma unroll
-    for (int i = 0; i < V; i += 2) {
-      const double2 t2 = *reinterpret_cast<const double2*>(src + r * ps + c * V + i);
-      v[i] = t2.x;
-      v[i + 1] = t2.y;
-    }
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+      for (int i = 0; i < V; i += 2) {
+        const double2 t2 = *reinterpret_cast<const double2*>(src + (r + h) * ps + c * V + i);
+        v[h][i] = t2.x;
+        v[h][i + 1] = t2.y;
+      }
+    auto put = [&](int64_t s, double a, double b) {
+      double* o = slice_row(g, out, s) + q0 + r;
+      if (two && ((reinterpret_cast<uintptr_t>(o) & 15) == 0)) {
+        *reinterpret_cast<double2*>(o) = make_double2(a, b);
+      } else {
+        o[0] = a;
+        if (two) o[1] = b;
+      }
+    };
 #pragma unroll
     for (int w = 0; w < W; ++w) {
       const int lev = l0 + w + 1;
@@ -90,17 +106,21 @@ __device__ __forceinline__ void fwd_stage(const double* src, int ps, double* dst
 #pragma unroll
       for (int i = 0; i < (V >> 1); ++i) {
         if (i < n) {
-          const double d = __dsub_rn(v[2 * i], v[2 * i + 1]);
-          const double s = __dadd_rn(v[2 * i + 1], __dmul_rn(d, 0.5));
-          if (want) slice_row(g, out, s0 + i)[q0 + r] = d;
-          v[i] = s;
+          double d[2];
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            d[h] = __dsub_rn(v[h][2 * i], v[h][2 * i + 1]);
+            v[h][i] = __dadd_rn(v[h][2 * i + 1], __dmul_rn(d[h], 0.5));
+          }
+          if (want) put(s0 + i, d[0], d[1]);
         }
       }
     }
     if (last) {
-      if (g.mask & 1) slice_row(g, out, soff(g.p, g.L) + (t0 >> g.L) + c)[q0 + r] = v[0];
+      if (g.mask & 1) put(soff(g.p, g.L) + (t0 >> g.L) + c, v[0][0], v[1][0]);
     } else {
-      dst[r * pd + c] = v[0];
+      dst[r * pd + c] = v[0][0];
+      if (two) dst[(r + 1) * pd + c] = v[1][0];
     }
   }
 }
