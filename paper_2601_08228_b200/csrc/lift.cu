@@ -219,6 +219,79 @@ __global__ void __launch_bounds__(kThreads) lift_inv_kernel(const double* __rest
   }
 }
 
+// ----------------------------------------------------------------------------
+// Per-level fallback for 2^L-band chunks larger than one tile (L > 13): one
+// launch per level through stream-ordered scratch.  Same arithmetic, any L.
+__global__ void lift_fwd_level(const double* __restrict__ src, int64_t len, double* __restrict__ dst,
+                               double* __restrict__ out, LiftGeom g, int j) {
+  const int64_t half = len / 2, total = g.ntubes * half;
+  const bool want_d = (g.mask >> j) & 1, last = (j == g.L);
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t q = e / half, k = e - q * half;
+    const double a = src[q * len + 2 * k], b = src[q * len + 2 * k + 1];
+    const double d = __dsub_rn(a, b);
+    const double s = __dadd_rn(b, __dmul_rn(d, 0.5));
+    if (want_d) out[pyr_index(g, detail_off(g.p, j), half, q, k)] = d;
+    if (!last) dst[q * half + k] = s;
+    else if (g.mask & 1) out[pyr_index(g, smooth_off(g.p, g.L), half, q, k)] = s;
+  }
+}
+
+__global__ void lift_inv_level(const double* __restrict__ src, const double* __restrict__ pyr,
+                               double* __restrict__ dst, LiftGeom g, int j) {
+  const int64_t half = g.p >> j, total = g.ntubes * half;
+  const bool have_d = (g.mask >> j) & 1, top = (j == g.L);
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t q = e / half, k = e - q * half;
+    const double s = top ? ((g.mask & 1) ? pyr[pyr_index(g, smooth_off(g.p, g.L), half, q, k)] : 0.0)
+                         : src[q * half + k];
+    const double d = have_d ? pyr[pyr_index(g, detail_off(g.p, j), half, q, k)] : 0.0;
+    const double x1 = __dsub_rn(s, __dmul_rn(d, 0.5));
+    dst[q * 2 * half + 2 * k] = __dadd_rn(d, x1);
+    dst[q * 2 * half + 2 * k + 1] = x1;
+  }
+}
+
+int levelwise_forward(const double* x, double* out, const LiftGeom& g, cudaStream_t st) {
+  double *t0 = nullptr, *t1 = nullptr;
+  const size_t bytes = sizeof(double) * (size_t)g.ntubes * (size_t)(g.p / 2);
+  WT_CUDA(cudaMallocAsync(&t0, bytes, st));
+  WT_CUDA(cudaMallocAsync(&t1, bytes, st));
+  const double* src = x;
+  int64_t len = g.p;
+  for (int j = 1; j <= g.L; ++j) {
+    double* dst = (j & 1) ? t0 : t1;
+    const int64_t total = g.ntubes * (len / 2);
+    const unsigned grid = (unsigned)std::min<int64_t>((total + 255) / 256, (int64_t)num_sms() * 16);
+    lift_fwd_level<<<grid, 256, 0, st>>>(src, len, dst, out, g, j);
+    src = dst;
+    len /= 2;
+  }
+  WT_CUDA(cudaFreeAsync(t0, st));
+  WT_CUDA(cudaFreeAsync(t1, st));
+  return check_launch("wt_lift_fwd_f64 (levelwise)");
+}
+
+int levelwise_inverse(const double* pyr, double* y, const LiftGeom& g, cudaStream_t st) {
+  double *t0 = nullptr, *t1 = nullptr;
+  const size_t bytes = sizeof(double) * (size_t)g.ntubes * (size_t)(g.p / 2);
+  WT_CUDA(cudaMallocAsync(&t0, bytes, st));
+  WT_CUDA(cudaMallocAsync(&t1, bytes, st));
+  const double* src = nullptr;
+  for (int j = g.L; j >= 1; --j) {
+    double* dst = j == 1 ? y : ((j & 1) ? t0 : t1);
+    const int64_t total = g.ntubes * (g.p >> j);
+    const unsigned grid = (unsigned)std::min<int64_t>((total + 255) / 256, (int64_t)num_sms() * 16);
+    lift_inv_level<<<grid, 256, 0, st>>>(src, pyr, dst, g, j);
+    src = dst;
+  }
+  WT_CUDA(cudaFreeAsync(t0, st));
+  WT_CUDA(cudaFreeAsync(t1, st));
+  return check_launch("wt_lift_inv_f64 (levelwise)");
+}
+
 // Choose the tile: TQ tubes x CT bands, CT = 2^L * d with d | p/2^L.
 int plan_tiles(LiftGeom& g) {
   const int64_t unit = (int64_t)1 << g.L;
@@ -234,9 +307,7 @@ int plan_tiles(LiftGeom& g) {
     g.LDT = g.CT + (g.CT % 2 == 0 ? 2 : 1);
     return WT_OK;
   }
-  set_error("lifting: 2^levels = %lld band chunk exceeds the single-pass tile (%d)",
-            (long long)unit, kMaxTileElems);
-  return WT_ERR_UNSUPPORTED;
+  return WT_ERR_UNSUPPORTED;  // caller switches to the per-level path
 }
 
 int validate(int64_t n1, int64_t n2, int64_t p, int levels, int layout, int64_t slice_base) {
@@ -274,7 +345,7 @@ extern "C" int wt_lift_fwd_f64(const double* x, int64_t n1, int64_t n2, int64_t 
     st = lift_fwd_fast(x, g.ntubes, p, levels, out, slice_base, level_mask, (cudaStream_t)stream);
     if (st != WT_ERR_UNSUPPORTED) return st;
   }
-  if ((st = plan_tiles(g))) return st;
+  if (plan_tiles(g) != WT_OK) return levelwise_forward(x, out, g, (cudaStream_t)stream);
   const bool bulk = (g.CT % 2 == 0) && (p % 2 == 0) && ((uintptr_t)x % 16 == 0);
   const size_t smem = (size_t)g.TQ * g.LDT * sizeof(double);
   static bool attr = false;
@@ -300,7 +371,7 @@ extern "C" int wt_lift_inv_f64(const double* pyr, int64_t n1, int64_t n2, int64_
     st = lift_inv_fast(pyr, g.ntubes, p, levels, y, slice_base, level_mask, (cudaStream_t)stream);
     if (st != WT_ERR_UNSUPPORTED) return st;
   }
-  if ((st = plan_tiles(g))) return st;
+  if (plan_tiles(g) != WT_OK) return levelwise_inverse(pyr, y, g, (cudaStream_t)stream);
   const bool bulk = (g.CT % 2 == 0) && (p % 2 == 0) && ((uintptr_t)y % 16 == 0);
   const size_t smem = (size_t)g.TQ * g.LDT * sizeof(double);
   static bool attr = false;

@@ -150,3 +150,26 @@ def test_energy_ratio_and_empty():
     e = W.forward_w(np.zeros((0, 3, 4)), 1)
     assert e.smooth.shape == (0, 3, 2)
     assert W.inverse_w(e).shape == (0, 3, 4)
+
+
+@pytest.mark.parametrize("shape,L", [((2, 3, 1 << 14), 14), ((3, 1, 1 << 15), 15), ((2, 2, 1 << 14), 13)])
+def test_very_deep_levels_per_level_path(shape, L):
+    """2^L-band chunks beyond one tile (L > 13) take the per-level path; still bit-exact."""
+    x = np.random.default_rng(L).standard_normal(shape)
+    s_ref, d_ref = O.lift_forward(x, L)
+    pyr = W.forward_w(x, L)
+    assert np.array_equal(pyr.smooth, s_ref)
+    assert all(np.array_equal(a, b) for a, b in zip(pyr.details, d_ref))
+    assert np.array_equal(W.inverse_w(pyr), O.lift_inverse(s_ref, d_ref))
+    buf = E.lift_forward(torch.from_numpy(x).cuda(), L)
+    assert np.array_equal(buf.cpu().numpy(), O.packed_slices(s_ref, d_ref))
+    y = E.lift_inverse(buf, shape[0], shape[1], shape[2], L)
+    assert np.array_equal(y.cpu().numpy(), O.lift_inverse(s_ref, d_ref))
+
+
+def test_odd_band_counts_in_transposes():
+    x = np.random.default_rng(8).standard_normal((5, 4, 7))
+    b = np.random.default_rng(9).standard_normal((4, 3, 7))
+    assert np.array_equal(W.transpose(x), O.transpose(x))
+    got = W.slicewise_matmul(x, b)
+    assert np.max(np.abs(got - O.face_matmul(x, b))) < 1e-14
