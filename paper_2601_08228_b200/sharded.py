@@ -270,9 +270,14 @@ def bench_sp_w_svd(dist_mod, timed_region, steps=3, warmup=1, shape=(1024, 1024,
     n1, n2, p = shape
     rows = splits(n1, G)
     r0 = sum(rows[:me])
-    cube = synth.hyperspectral_cube(n1, n2, p, seed=0)
-    x = torch.from_numpy(cube[r0:r0 + rows[me]].copy()).cuda()
-    del cube
+    # rank 0 generates the cube once and broadcasts it (NVLink); each rank keeps its rows
+    if me == 0:
+        full = torch.from_numpy(synth.hyperspectral_cube(n1, n2, p, seed=0)).cuda()
+    else:
+        full = torch.empty((n1, n2, p), dtype=torch.float64, device="cuda")
+    dist_mod.broadcast(full, src=0)
+    x = full[r0:r0 + rows[me]].contiguous()
+    del full
     out = {}
 
     fn = sp_w_svd_fused if fused else sp_w_svd_sharded
