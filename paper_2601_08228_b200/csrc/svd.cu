@@ -40,7 +40,10 @@ constexpr double kFloorEps = 1e3 * 2.220446049250313e-16;  // null-column floor 
 constexpr int kMaxInnerSweeps = 16;
 
 struct SvdWs {
-  double* X;        // batch * npad * mpad
+  double* X;        // batch * npad * mpad (buffer 0)
+  double* X2;       // batch * npad * mpad (buffer 1, target of the between-sweep reordering)
+  int* xsel;        // batch: which buffer holds matrix b (reordering skips converged matrices)
+  int* active;      // compacted list of the matrices still iterating (grid.y indexes it)
   unsigned long long* offmax;  // batch  (bit pattern of a non-negative double)
   int* conv;        // batch: 1 = converged, 2 = non-finite
   int* pending;     // 1 counter (matrices still iterating)
@@ -49,6 +52,10 @@ struct SvdWs {
 };
 
 __host__ __device__ inline int64_t round_up(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
+
+__device__ __forceinline__ double* mat_ptr(const SvdWs& ws, int64_t b, int64_t npad, int64_t mpad) {
+  return (ws.xsel[b] ? ws.X2 : ws.X) + b * npad * mpad;
+}
 
 // ------------------------------------------------------------- copy in -----
 __global__ void svd_copy_in(const double* __restrict__ A, int64_t lda, int64_t sA, bool right,
@@ -97,12 +104,12 @@ __global__ void __launch_bounds__(kThreads, 3) svd_pair_kernel(SvdWs ws, int64_t
                                                                int round, double tol, int inner_sweeps) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   PairSmem& S = *reinterpret_cast<PairSmem*>(smem_raw);
-  const int b = blockIdx.y;
+  const int b = ws.active[blockIdx.y];
   if (ws.conv[b]) return;
   const int nb = (int)(npad / HB);
   const int I = rr_index(blockIdx.x, round, nb), J = rr_index(nb - 1 - blockIdx.x, round, nb);
   const int colI = I * HB, colJ = J * HB;
-  double* Xb = ws.X + (int64_t)b * npad * mpad;
+  double* Xb = mat_ptr(ws, b, npad, mpad);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nch = (int)(mpad / RCH);
 
@@ -347,7 +354,7 @@ __global__ void svd_end_sweep(SvdWs ws, int batch, double tol) {
     const double off = __longlong_as_double((long long)ws.offmax[b]);
     if (isnan(off) || isinf(off)) ws.conv[b] = 2;
     else if (off < tol) ws.conv[b] = 1;
-    else atomicAdd(ws.pending, 1);
+    else ws.active[atomicAdd(ws.pending, 1)] = b;  // order is irrelevant: matrices are independent
     ws.offmax[b] = 0ull;
   }
 }
@@ -359,8 +366,9 @@ __global__ void svd_norms_sort(SvdWs ws, int64_t mpad, int64_t npad, int64_t n, 
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double* key = reinterpret_cast<double*>(smem_raw);
   int* idx = reinterpret_cast<int*>(key + npow2);
-  const int b = blockIdx.x;
-  const double* Xb = ws.X + (int64_t)b * npad * mpad;
+  const int b = sigma == nullptr ? ws.active[blockIdx.x] : blockIdx.x;
+  if (sigma == nullptr && ws.conv[b]) return;  // reordering: converged matrices stay put
+  const double* Xb = mat_ptr(ws, b, npad, mpad);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   for (int c = warp; c < npow2; c += nw) {
     double s = 0.0;
@@ -424,24 +432,37 @@ __global__ void svd_gather(SvdWs ws, int64_t mpad, int64_t npad, int64_t m, int6
   const int c = ws.perm[b * npad + i];
   const double s = ws.sig[b * npad + i];
   const double inv = (s > 0.0 && isfinite(s)) ? 1.0 / s : 0.0;
-  const double* col = ws.X + (b * npad + c) * mpad;
+  const double* col = mat_ptr(ws, b, npad, mpad) + (int64_t)c * mpad;
   double* dst = vec + (b * nvec + i) * m;
   for (int64_t r = threadIdx.x; r < m; r += blockDim.x) dst[r] = col[r] * inv;
 }
 
-// X2[b][i] = X[b][perm[b][i]] (whole columns), for the between-sweep reordering.
-__global__ void svd_permute_cols(const double* __restrict__ X, double* __restrict__ X2,
-                                 const int* __restrict__ perm, int64_t mpad, int64_t npad) {
-  const int64_t i = blockIdx.x, b = blockIdx.y;
-  const int c = perm[b * npad + i];
-  const double2* src = reinterpret_cast<const double2*>(X + (b * npad + c) * mpad);
-  double2* dst = reinterpret_cast<double2*>(X2 + (b * npad + i) * mpad);
+// other[b][i] = cur[b][perm[b][i]] (whole columns) for every matrix still
+// iterating; svd_flip then makes `other` current for those matrices.
+__global__ void svd_permute_cols(SvdWs ws, int64_t mpad, int64_t npad) {
+  const int64_t i = blockIdx.x, b = ws.active[blockIdx.y];
+  if (ws.conv[b]) return;
+  const int c = ws.perm[b * npad + i];
+  const bool sel = ws.xsel[b];
+  const double* cur = (sel ? ws.X2 : ws.X) + b * npad * mpad;
+  double* oth = (sel ? ws.X : ws.X2) + b * npad * mpad;
+  const double2* src = reinterpret_cast<const double2*>(cur + (int64_t)c * mpad);
+  double2* dst = reinterpret_cast<double2*>(oth + i * mpad);
   for (int64_t r = threadIdx.x; r < mpad / 2; r += blockDim.x) dst[r] = src[r];
+}
+
+__global__ void svd_iota(int* a, int n) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) a[i] = i;
+}
+
+__global__ void svd_flip(SvdWs ws, int batch) {
+  for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < batch; b += gridDim.x * blockDim.x)
+    if (!ws.conv[b]) ws.xsel[b] ^= 1;
 }
 
 struct WsLayout {
   int64_t m, n, mpad, npad;
-  size_t off_X, off_X2, off_off, off_conv, off_pending, off_sig, off_perm, total;
+  size_t off_X, off_X2, off_xsel, off_active, off_off, off_conv, off_pending, off_sig, off_perm, total;
 };
 
 WsLayout ws_layout(int64_t n1, int64_t n2, int64_t batch) {
@@ -454,6 +475,8 @@ WsLayout ws_layout(int64_t n1, int64_t n2, int64_t batch) {
   auto take = [&](size_t bytes) { size_t r = o; o = (o + bytes + 255) / 256 * 256; return r; };
   L.off_X = take(sizeof(double) * (size_t)(batch * L.npad * L.mpad));
   L.off_X2 = take(sizeof(double) * (size_t)(batch * L.npad * L.mpad));
+  L.off_xsel = take(sizeof(int) * (size_t)batch);
+  L.off_active = take(sizeof(int) * (size_t)batch);
   L.off_off = take(sizeof(unsigned long long) * (size_t)batch);
   L.off_conv = take(sizeof(int) * (size_t)batch);
   L.off_pending = take(sizeof(int) * 4);
@@ -497,7 +520,8 @@ extern "C" int wt_svd_jacobi_f64(const double* A, int64_t lda, int64_t strideA, 
   WT_REQUIRE(npow2 <= 8192, "svd: min(n1, n2) = %lld above the 8192 sort limit", (long long)L.n);
   cudaStream_t st = (cudaStream_t)stream;
   char* base = static_cast<char*>(workspace);
-  SvdWs ws{reinterpret_cast<double*>(base + L.off_X),
+  SvdWs ws{reinterpret_cast<double*>(base + L.off_X), reinterpret_cast<double*>(base + L.off_X2),
+           reinterpret_cast<int*>(base + L.off_xsel), reinterpret_cast<int*>(base + L.off_active),
            reinterpret_cast<unsigned long long*>(base + L.off_off),
            reinterpret_cast<int*>(base + L.off_conv), reinterpret_cast<int*>(base + L.off_pending),
            reinterpret_cast<double*>(base + L.off_sig), reinterpret_cast<int*>(base + L.off_perm)};
@@ -512,6 +536,9 @@ extern "C" int wt_svd_jacobi_f64(const double* A, int64_t lda, int64_t strideA, 
   }
   WT_CUDA(cudaMemsetAsync(ws.offmax, 0, sizeof(unsigned long long) * batch, st));
   WT_CUDA(cudaMemsetAsync(ws.conv, 0, sizeof(int) * batch, st));
+  WT_CUDA(cudaMemsetAsync(ws.xsel, 0, sizeof(int) * batch, st));
+  svd_iota<<<(unsigned)((batch + 255) / 256), 256, 0, st>>>(ws.active, (int)batch);
+  int64_t n_active = batch;
   WT_CUDA(cudaMemsetAsync(ws.pending, 0, sizeof(int) * 2, st));
 
   static bool attr = false;
@@ -534,22 +561,20 @@ extern "C" int wt_svd_jacobi_f64(const double* A, int64_t lda, int64_t strideA, 
   // config-3/4 slices 13 -> 12 and 17 -> 16 sweeps, -10% time (round 1).
   int sort_mode = 2;
   if (const char* e = getenv("WT_SVD_SORT")) sort_mode = atoi(e);
-  double* X2 = reinterpret_cast<double*>(base + L.off_X2);
   const size_t sort_smem = (size_t)npow2 * (sizeof(double) + sizeof(int));
   WT_CUDA(cudaFuncSetAttribute(svd_norms_sort, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                8192 * (int)(sizeof(double) + sizeof(int))));
   for (int sweep = 0; sweep < max_sweeps; ++sweep) {
     if (sort_mode == 2 || (sort_mode == 1 && sweep == 0)) {
       // columns in descending norm order before the sweep (de Rijk-style)
-      svd_norms_sort<<<(unsigned)batch, 512, sort_smem, st>>>(ws, L.mpad, L.npad, L.n, npow2,
+      svd_norms_sort<<<(unsigned)n_active, 512, sort_smem, st>>>(ws, L.mpad, L.npad, L.n, npow2,
                                                               nullptr, nullptr, 0);
-      svd_permute_cols<<<dim3((unsigned)L.npad, (unsigned)batch), 128, 0, st>>>(ws.X, X2, ws.perm,
-                                                                                 L.mpad, L.npad);
-      std::swap(ws.X, X2);
+      svd_permute_cols<<<dim3((unsigned)L.npad, (unsigned)n_active), 128, 0, st>>>(ws, L.mpad, L.npad);
+      svd_flip<<<(unsigned)((batch + 255) / 256), 256, 0, st>>>(ws, (int)batch);
       if (int e = check_launch("svd reorder")) return e;
     }
     for (int round = 0; round < nb - 1; ++round) {
-      svd_pair_kernel<<<dim3(nb / 2, (unsigned)batch), kThreads, sizeof(PairSmem), st>>>(
+      svd_pair_kernel<<<dim3(nb / 2, (unsigned)n_active), kThreads, sizeof(PairSmem), st>>>(
           ws, L.mpad, L.npad, round, tol, inner);
     }
     if (int e = check_launch("svd_pair_kernel")) return e;
@@ -579,6 +604,7 @@ extern "C" int wt_svd_jacobi_f64(const double* A, int64_t lda, int64_t strideA, 
     WT_CUDA(cudaStreamSynchronize(st));
     g_last_sweeps = sweep + 1;
     if (*h_pending == 0) { hit_max = false; break; }
+    n_active = *h_pending;  // svd_end_sweep compacted the survivors into ws.active
   }
   {
     const size_t sm = (size_t)npow2 * (sizeof(double) + sizeof(int));
