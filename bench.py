@@ -434,7 +434,7 @@ def wproduct_workload(args, steps=20, warmup=3):
 
 # ----------------------------------------------------------- CPU legs ----
 
-def cpu_transform_sample(x_host, reps=2, rows=128):
+def cpu_transform_sample(x_host, reps=2, rows=512):
     """Oracle (numpy port of lifting.py) on a bounded slab of the config-2 cube."""
     from oracle import wten_oracle as O
 
@@ -459,7 +459,7 @@ def run_reference(args):
     from oracle import wten_oracle as O  # noqa: F401
 
     x = np.random.default_rng(0).standard_normal(CFG2)
-    rows = 64
+    rows = 128
     slab = np.ascontiguousarray(x[:rows])
     n = slab.size
     for _ in range(max(0, min(args.warmup, 1))):
