@@ -8,13 +8,16 @@
 //   X = A otherwise.  Columns are grouped in blocks of 16; each sweep visits
 //   every block pair once in round-robin order (nblk-1 rounds of nblk/2
 //   disjoint pairs, one CTA per pair and matrix).  Per pair:
-//     1. G = Z^T Z for the 32-column panel Z = [X_I X_J] (DMMA, rows streamed
-//        through shared memory with cp.async double buffering);
-//     2. if max_{i<j} |G_ij| / sqrt(G_ii G_jj) < tol the pair is skipped;
-//        otherwise G = Q diag Q^T by cyclic parallel two-sided Jacobi in
-//        shared memory (16 disjoint rotations per step);
-//     3. Z <- Z Q (DMMA, streamed again, written back in place).
-//   A sweep in which no pair exceeded tol ends the iteration for that matrix.
+//     1. G = Z^T Z for the 32-column panel Z = [X_I X_J] (DMMA on the 10 upper
+//        8x8 tiles, rows streamed through shared memory with cp.async double
+//        buffering, rows split over the warps, fixed-order tree reduction);
+//     2. if every |G_ij| <= tol sqrt(G_ii G_jj) (+ a null-column floor) the
+//        pair is skipped; otherwise one sweep of cyclic parallel two-sided
+//        Jacobi on G in shared memory (16 disjoint rotations per step) gives Q;
+//     3. Z <- Z Q (DMMA, streamed again -- mostly from L2 -- written back).
+//   Before every sweep the columns are reordered by descending norm.  A sweep
+//   in which no pair exceeded tol retires the matrix: later launches only run
+//   over the compacted list of matrices still iterating.
 //   Finally sigma_c = ||X_c|| and the columns are sorted descending; the
 //   normalised columns are the long-side singular vectors.
 // Everything is deterministic: fixed reduction orders, no floating atomics.
