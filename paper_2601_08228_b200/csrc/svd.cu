@@ -41,12 +41,21 @@ constexpr int LDG = BW + 1;  // Gram / Q pitch
 constexpr int kThreads = 256;
 constexpr double kFloorEps = 1e3 * 2.220446049250313e-16;  // null-column floor (see the test)
 constexpr int kMaxInnerSweeps = 16;
+#ifndef WT_EIG_WARPS
+#define WT_EIG_WARPS 8
+#endif
+constexpr int kEigWarps = WT_EIG_WARPS;  // warps running the 32x32 eigen steps
+
+__device__ __forceinline__ void eig_barrier() {
+  asm volatile("bar.sync 1, %0;" ::"n"(kEigWarps * 32) : "memory");
+}
 
 struct SvdWs {
   double* X;        // batch * npad * mpad (buffer 0)
   double* X2;       // batch * npad * mpad (buffer 1, target of the between-sweep reordering)
   int* xsel;        // batch: which buffer holds matrix b (reordering skips converged matrices)
   int* active;      // compacted list of the matrices still iterating (grid.y indexes it)
+  unsigned long long* prof;  // optional phase-cycle counters (WT_SVD_PROFILE diagnostics)
   unsigned long long* offmax;  // batch  (bit pattern of a non-negative double)
   int* conv;        // batch: 1 = converged, 2 = non-finite
   int* pending;     // 1 counter (matrices still iterating)
@@ -89,6 +98,7 @@ struct PairSmem {
   double G[2][BW * LDG];
   double Q[BW * LDG];
   double warp_off[kThreads / 32];
+  int any_rot;
 };
 
 __device__ __forceinline__ void load_chunk(double* Zs, const double* Xb, int64_t mpad, int colI,
@@ -116,6 +126,7 @@ __global__ void __launch_bounds__(kThreads, 3) svd_pair_kernel(SvdWs ws, int64_t
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nch = (int)(mpad / RCH);
 
+  const long long t_start = clock64();
   // ---------------- 1. Gram G = Z^T Z: upper 10 of the 16 8x8 tiles --------
   // Rows are split over the 8 warps (warp w owns rows w*8 .. w*8+7 of every
   // chunk).  One LDS.128 per column group feeds two DMMAs: lane (r, k) holds
@@ -226,19 +237,26 @@ __global__ void __launch_bounds__(kThreads, 3) svd_pair_kernel(SvdWs ws, int64_t
   if (tid == 0) atomicAdd(ws.pending + 1, 1);  // rotated-pair counter (diagnostics)
   if (isinf(off)) return;
 
+  const long long t_gram = clock64();
   // ---------------- 3. eigen-decomposition of G (cyclic parallel Jacobi) ----
-  // 16 groups of 16 threads; group g owns rotation pair g of every step, computes
-  // its (c, s) redundantly (no shared round trip), then applies G <- G J,
-  // Q <- Q J (columns p, q) and, after a barrier, G <- J^T G (rows p, q).
+  // Only the first kEigWarps warps run the steps (named barrier 1); the rest
+  // wait at the CTA barrier after it.  16 groups of TPG threads: group g owns
+  // rotation pair g of every step, computes its (c, s) redundantly (no shared
+  // round trip), then applies G <- G J, Q <- Q J (columns p, q) and, after a
+  // barrier, G <- J^T G (rows p, q).  Fewer warps = fewer redundant FP64
+  // rotation chains per SM: the step was issue-bound with all 8 warps (clock64
+  // phase counters, WT_SVD_PROFILE).
   for (int e = tid; e < BW * BW; e += kThreads) {
     const int i = e / BW, j = e % BW;
     S.Q[i * LDG + j] = (i == j) ? 1.0 : 0.0;
   }
   __syncthreads();
-  {
+  if (warp < kEigWarps) {
+    constexpr int TPG = kEigWarps * 32 / (BW / 2);  // threads per rotation group
+    constexpr int RPT = BW / TPG;                   // rows (columns) per thread
     double* G = S.G[0];
     double* Q = S.Q;
-    const int grp = tid >> 4, sub = tid & 15;
+    const int grp = tid / TPG, sub = tid % TPG;
     for (int sweep = 0; sweep < inner_sweeps; ++sweep) {
       int my_rot = 0;
       for (int step = 0; step < BW - 1; ++step) {
@@ -247,54 +265,76 @@ __global__ void __launch_bounds__(kThreads, 3) svd_pair_kernel(SvdWs ws, int64_t
         const double gpp = G[p * LDG + p], gqq = G[q * LDG + q], gpq = G[p * LDG + q];
         // rotate iff |g_pq| > tol * max(sqrt(g_pp g_qq), floor_c g_max)  (squared: no sqrt)
         const double fl = floor_c * gmax;
+        const double psc = gmax > 0.0 ? ldexp(1.0, -ilogb(gmax)) : 1.0;  // keeps a^2 + b^2 in range
         const bool rot = gpq * gpq > tol * tol * fmax(gpp * gqq, fl * fl);
         __syncwarp();
         double c = 1.0, s = 0.0;
         if (rot) {
-          // Rutishauser's rotation with reciprocal / rsqrt instead of divisions
-          // and sqrt (the dependent FP64 chain was the top stall in ncu)
-          const double tau = (gqq - gpp) * __drcp_rn(2.0 * gpq);
-          const double at = fabs(tau);
-          double t;
-          if (at < 1e100) {
-            const double w = fma(tau, tau, 1.0);
-            t = __drcp_rn(at + w * rsqrt(w));
-          } else {
-            t = 0.5 / at;
-          }
-          if (tau < 0.0) t = -t;
-          c = rsqrt(fma(t, t, 1.0));
-          s = t * c;
+          // Jacobi rotation from two rsqrt and no division (the dependent FP64
+          // MUFU chain bounds the step): with a = g_qq - g_pp, b = 2 g_pq
+          // (scaled by a power of two ~ 1/g_max), cos 2phi = |a| / r,
+          // c = sqrt((1 + cos 2phi) / 2), s = sign(a) b / (2 r c), |phi| <= pi/4
+          // -- the same rotation as Rutishauser's t = sgn(tau)/(|tau|+sqrt(1+tau^2)).
+          const double a = (gqq - gpp) * psc, bb = 2.0 * gpq * psc;
+          const double rinv = rsqrt(fma(a, a, bb * bb));
+          const double h = fma(0.5, fabs(a) * rinv, 0.5);
+          const double rh = rsqrt(h);
+          c = h * rh;
+          s = (a >= 0.0 ? 0.5 : -0.5) * bb * rinv * rh;
+          // one Newton step on c^2 + s^2 = 1 keeps the accumulated Q orthogonal
+          const double f = fma(-0.5, fma(c, c, s * s), 1.5);
+          c *= f;
+          s *= f;
           my_rot = 1;
+          double ga[RPT], gb[RPT], qa[RPT], qb[RPT];
 #pragma unroll
-          for (int h = 0; h < 2; ++h) {  // columns: G <- G J, Q <- Q J
-            const int i = sub + 16 * h;
-            const double a = G[i * LDG + p], bq = G[i * LDG + q];
-            G[i * LDG + p] = c * a - s * bq;
-            G[i * LDG + q] = s * a + c * bq;
-            const double qa = Q[i * LDG + p], qb = Q[i * LDG + q];
-            Q[i * LDG + p] = c * qa - s * qb;
-            Q[i * LDG + q] = s * qa + c * qb;
+          for (int h = 0; h < RPT; ++h) {  // columns: G <- G J, Q <- Q J (loads first)
+            const int i = sub + TPG * h;
+            ga[h] = G[i * LDG + p];
+            gb[h] = G[i * LDG + q];
+            qa[h] = Q[i * LDG + p];
+            qb[h] = Q[i * LDG + q];
+          }
+#pragma unroll
+          for (int h = 0; h < RPT; ++h) {
+            const int i = sub + TPG * h;
+            G[i * LDG + p] = c * ga[h] - s * gb[h];
+            G[i * LDG + q] = s * ga[h] + c * gb[h];
+            Q[i * LDG + p] = c * qa[h] - s * qb[h];
+            Q[i * LDG + q] = s * qa[h] + c * qb[h];
           }
         }
-        __syncthreads();
+        eig_barrier();
         if (rot) {
+          double ra[RPT], rb[RPT];
 #pragma unroll
-          for (int h = 0; h < 2; ++h) {  // rows: G <- J^T G
-            const int j = sub + 16 * h;
-            const double a = G[p * LDG + j], bq = G[q * LDG + j];
-            double np = c * a - s * bq, nq = s * a + c * bq;
+          for (int h = 0; h < RPT; ++h) {
+            const int j = sub + TPG * h;
+            ra[h] = G[p * LDG + j];
+            rb[h] = G[q * LDG + j];
+          }
+#pragma unroll
+          for (int h = 0; h < RPT; ++h) {  // rows: G <- J^T G
+            const int j = sub + TPG * h;
+            double np = c * ra[h] - s * rb[h], nq = s * ra[h] + c * rb[h];
             if (j == q) np = 0.0;  // annihilated pair
             if (j == p) nq = 0.0;
             G[p * LDG + j] = np;
             G[q * LDG + j] = nq;
           }
         }
-        __syncthreads();
+        eig_barrier();
       }
-      if (!__syncthreads_or(my_rot)) break;
+      S.any_rot = 0;
+      eig_barrier();
+      if (my_rot) S.any_rot = 1;
+      eig_barrier();
+      if (!S.any_rot) break;
+      eig_barrier();
     }
   }
+  __syncthreads();
+  const long long t_eig = clock64();
   // ---------------- 4. Z <- Z Q, streamed, written back in place -----------
   // warp w: chunk rows rt*16 .. rt*16+15 (two 8-row tiles) x output n-tiles
   // {2nh, 2nh+1}; its Q b-fragments Q[kk*4 + lane%4][n*8 + lane/4] stay in
@@ -347,6 +387,12 @@ __global__ void __launch_bounds__(kThreads, 3) svd_pair_kernel(SvdWs ws, int64_t
           *reinterpret_cast<const double2*>(Zs + c * LDZ + rv);
     }
     __syncthreads();
+  }
+  if (ws.prof && tid == 0) {
+    atomicAdd(ws.prof + 0, (unsigned long long)(t_gram - t_start));
+    atomicAdd(ws.prof + 1, (unsigned long long)(t_eig - t_gram));
+    atomicAdd(ws.prof + 2, (unsigned long long)(clock64() - t_eig));
+    atomicAdd(ws.prof + 3, 1ull);
   }
 }
 
@@ -525,6 +571,7 @@ extern "C" int wt_svd_jacobi_f64(const double* A, int64_t lda, int64_t strideA, 
   char* base = static_cast<char*>(workspace);
   SvdWs ws{reinterpret_cast<double*>(base + L.off_X), reinterpret_cast<double*>(base + L.off_X2),
            reinterpret_cast<int*>(base + L.off_xsel), reinterpret_cast<int*>(base + L.off_active),
+           nullptr,
            reinterpret_cast<unsigned long long*>(base + L.off_off),
            reinterpret_cast<int*>(base + L.off_conv), reinterpret_cast<int*>(base + L.off_pending),
            reinterpret_cast<double*>(base + L.off_sig), reinterpret_cast<int*>(base + L.off_perm)};
@@ -551,6 +598,13 @@ extern "C" int wt_svd_jacobi_f64(const double* A, int64_t lda, int64_t strideA, 
     attr = true;
   }
   g_last_sweeps = 0;
+  static unsigned long long* d_prof = nullptr;
+  const bool profile = getenv("WT_SVD_PROFILE") != nullptr;
+  if (profile) {
+    if (!d_prof) WT_CUDA(cudaMalloc(&d_prof, 4 * sizeof(unsigned long long)));
+    WT_CUDA(cudaMemsetAsync(d_prof, 0, 4 * sizeof(unsigned long long), st));
+    ws.prof = d_prof;
+  }
   static int* h_pending = nullptr;
   if (!h_pending) WT_CUDA(cudaMallocHost(&h_pending, sizeof(int)));
   const int nb = (int)(L.npad / HB);
@@ -608,6 +662,14 @@ extern "C" int wt_svd_jacobi_f64(const double* A, int64_t lda, int64_t strideA, 
     g_last_sweeps = sweep + 1;
     if (*h_pending == 0) { hit_max = false; break; }
     n_active = *h_pending;  // svd_end_sweep compacted the survivors into ws.active
+  }
+  if (profile) {
+    unsigned long long h[4];
+    WT_CUDA(cudaMemcpyAsync(h, d_prof, sizeof(h), cudaMemcpyDeviceToHost, st));
+    WT_CUDA(cudaStreamSynchronize(st));
+    const double n = h[3] ? (double)h[3] : 1.0;
+    fprintf(stderr, "[wt_svd] %llu rotated pair visits; mean cycles per visit: gram+test %.0f, "
+            "eigen %.0f, rotate %.0f\n", h[3], h[0] / n, h[1] / n, h[2] / n);
   }
   {
     const size_t sm = (size_t)npow2 * (sizeof(double) + sizeof(int));
