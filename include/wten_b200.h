@@ -158,8 +158,11 @@ size_t wt_slice_reduce_scratch(int64_t n, int64_t nslices);
 int wt_slice_reduce_f64(const double* x, const double* y, int64_t n, int64_t nslices,
                         int mode, double* out, void* stream);
 
-/* Sweeps used by the last wt_svd_jacobi_f64 call on the calling thread. */
+/* Sweeps used by the last wt_svd_jacobi_f64 call on the calling thread, and
+ * the FP64 flops its Jacobi iteration executed (Gram + rotation tiles of every
+ * rotated pair visit) -- the denominator-free work measure for the roofline. */
 int wt_svd_last_sweeps(void);
+double wt_svd_last_jacobi_flops(void);
 
 #ifdef __cplusplus
 }

@@ -545,6 +545,16 @@ static thread_local int g_last_sweeps = 0;
 // Sweeps used by the last wt_svd_jacobi_f64 call on this thread (diagnostics).
 extern "C" int wt_svd_last_sweeps(void) { return g_last_sweeps; }
 
+static thread_local long long g_last_rotations = 0;
+static thread_local long long g_last_panel_rows = 0;
+
+// FP64 flops executed by the Jacobi iteration of the last call on this thread:
+// every rotated pair visit = Gram (10 of 16 8x8 tiles) + Z Q on an mpad x 32
+// panel, i.e. 2 * mpad * 32 * 32 * (10/16 + 1) flops.
+extern "C" double wt_svd_last_jacobi_flops(void) {
+  return (double)g_last_rotations * 2.0 * (double)g_last_panel_rows * 32.0 * 32.0 * (26.0 / 16.0);
+}
+
 extern "C" size_t wt_svd_workspace_bytes(int64_t n1, int64_t n2, int64_t batch) {
   if (n1 < 0 || n2 < 0 || batch < 0) return 0;
   return ws_layout(n1, n2, batch).total;
@@ -598,6 +608,8 @@ extern "C" int wt_svd_jacobi_f64(const double* A, int64_t lda, int64_t strideA, 
     attr = true;
   }
   g_last_sweeps = 0;
+  g_last_rotations = 0;
+  int dbg_prev = 0;
   static unsigned long long* d_prof = nullptr;
   const bool profile = getenv("WT_SVD_PROFILE") != nullptr;
   if (profile) {
@@ -650,10 +662,10 @@ extern "C" int wt_svd_jacobi_f64(const double* A, int64_t lda, int64_t strideA, 
       }
       int rotated = 0;
       WT_CUDA(cudaMemcpy(&rotated, ws.pending + 1, sizeof(int), cudaMemcpyDeviceToHost));
-      WT_CUDA(cudaMemset(ws.pending + 1, 0, sizeof(int)));
       fprintf(stderr, "[wt_svd] sweep %d: max off %.3e (tol %.1e), %d/%lld matrices above tol, "
-              "%d/%lld pair visits rotated\n", sweep, mx, tol, active, (long long)batch, rotated,
-              (long long)(nb / 2) * (nb - 1) * batch);
+              "%d/%lld pair visits rotated\n", sweep, mx, tol, active, (long long)batch,
+              rotated - dbg_prev, (long long)(nb / 2) * (nb - 1) * batch);
+      dbg_prev = rotated;
     }
     WT_CUDA(cudaMemsetAsync(ws.pending, 0, sizeof(int), st));
     svd_end_sweep<<<(unsigned)((batch + 255) / 256), 256, 0, st>>>(ws, (int)batch, tol);
@@ -662,6 +674,12 @@ extern "C" int wt_svd_jacobi_f64(const double* A, int64_t lda, int64_t strideA, 
     g_last_sweeps = sweep + 1;
     if (*h_pending == 0) { hit_max = false; break; }
     n_active = *h_pending;  // svd_end_sweep compacted the survivors into ws.active
+  }
+  {
+    int rotated = 0;  // stream is idle here (synchronised at the end of the last sweep)
+    WT_CUDA(cudaMemcpy(&rotated, ws.pending + 1, sizeof(int), cudaMemcpyDeviceToHost));
+    g_last_rotations = rotated;
+    g_last_panel_rows = L.mpad;
   }
   if (profile) {
     unsigned long long h[4];

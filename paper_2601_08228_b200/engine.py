@@ -196,6 +196,12 @@ def svd(a: torch.Tensor, nvec: int, tol: float = 0.0, max_sweeps: int = 0):
     info = torch.empty((batch,), dtype=torch.int32, device=a.device)
     if batch == 0:
         return sigma, vec, info
+    if batch > 65535:  # grid.y limit of K4: run in chunks of slices
+        for s0 in range(0, batch, 65535):
+            s1 = min(batch, s0 + 65535)
+            sg, vc, nf = svd(a[s0:s1], nvec, tol, max_sweeps)
+            sigma[s0:s1], vec[s0:s1], info[s0:s1] = sg, vc, nf
+        return sigma, vec, info
     wsb = int(lib.wt_svd_workspace_bytes(n1, n2, batch))
     ws = torch.empty((wsb,), dtype=torch.uint8, device=a.device)
     N.check(lib.wt_svd_jacobi_f64(_ptr(a), a.stride(1), a.stride(0), n1, n2, batch, _ptr(sigma),
@@ -206,6 +212,11 @@ def svd(a: torch.Tensor, nvec: int, tol: float = 0.0, max_sweeps: int = 0):
 
 def last_sweeps() -> int:
     return int(N.load().wt_svd_last_sweeps())
+
+
+def last_jacobi_flops() -> float:
+    """FP64 flops executed by the last K4 call's Jacobi iteration (this thread)."""
+    return float(N.load().wt_svd_last_jacobi_flops())
 
 
 def raise_if_failed(info: torch.Tensor):
