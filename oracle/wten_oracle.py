@@ -291,3 +291,106 @@ def ssim(x1, x2, mpp=None) -> float:
         vals.append(((2 * ma * mb + c1) * (2 * cab + c2))
                     / ((ma * ma + mb * mb + c1) * (va + vb + c2)))
     return float(np.mean(vals))
+
+
+# ----------------------------------------------------------------------------
+# comparator products (baselines.py) -- restated with numpy's FFT / LAPACK
+# ----------------------------------------------------------------------------
+
+
+def dct_matrix(p: int) -> np.ndarray:
+    """Orthonormal DCT-II matrix, the default m-product transform (baselines.py:53-56).
+
+    Closed form M[k, n] = f_k cos(pi k (2n + 1) / (2p)), f_0 = sqrt(1/p), else sqrt(2/p)."""
+    k = np.arange(p)[:, None]
+    n = np.arange(p)[None, :]
+    m = np.cos(np.pi * k * (2 * n + 1) / (2 * p)) * np.sqrt(2.0 / p)
+    m[0] *= np.sqrt(0.5)
+    return m
+
+
+def _mode3_dft(a):
+    """Frequency-major DFT stack (p, n1, n2) -- baselines.py:68-69."""
+    return np.ascontiguousarray(np.fft.fft(a, axis=2).transpose(2, 0, 1))
+
+
+def _mode3_idft_real(fc):
+    """Real part of the inverse DFT of a (p, n1, n2) stack -- baselines.py:71-72."""
+    return np.ascontiguousarray(np.fft.ifft(np.ascontiguousarray(fc.transpose(1, 2, 0)), axis=2).real)
+
+
+def t_product(a, b):
+    """baselines.py:63-73: FFT along mode 3, facewise complex product, real inverse."""
+    a = np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    return _mode3_idft_real(np.matmul(_mode3_dft(a), _mode3_dft(b)))
+
+
+def t_product_circulant(a, b):
+    """Brute-force block-circulant t-product: C_k = sum_j A_j B_(k-j mod p)."""
+    a = np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    p = a.shape[2]
+    c = np.zeros((a.shape[0], b.shape[1], p))
+    for k in range(p):
+        for j in range(p):
+            c[:, :, k] += a[:, :, j] @ b[:, :, (k - j) % p]
+    return c
+
+
+def tube_identity(n, p):
+    """baselines.py:77-82."""
+    out = np.zeros((n, n, p))
+    out[:, :, 0] = np.eye(n)
+    return out
+
+
+def apply_mode3(t, m):
+    """hat[i, j, k'] = sum_k m[k', k] t[i, j, k] -- baselines.py:85-87."""
+    return np.einsum("ijk,lk->ijl", np.asarray(t, dtype=np.float64), m)
+
+
+def m_product(a, b, m, minv):
+    """baselines.py:90-103: mode-3 transform, facewise product, inverse transform."""
+    ha = apply_mode3(a, m)
+    hb = apply_mode3(b, m)
+    return apply_mode3(face_matmul(ha, hb), minv)
+
+
+def m_identity(n, p, minv):
+    """baselines.py:106-109."""
+    return apply_mode3(np.broadcast_to(np.eye(n)[:, :, None], (n, n, p)), minv)
+
+
+def t_svd(a, r):
+    """baselines.py:112-124: rank-r truncation of every DFT-domain slice."""
+    a = np.asarray(a, dtype=np.float64)
+    u, s, vh = np.linalg.svd(_mode3_dft(a), full_matrices=False)
+    return _mode3_idft_real(np.matmul(u[:, :, :r], s[:, :r, None] * vh[:, :r, :]))
+
+
+def t_pinv(a, tol=1e-12):
+    """baselines.py:127-138: per-DFT-slice Moore-Penrose inverse, cutoff tol * sigma_max."""
+    a = np.asarray(a, dtype=np.float64)
+    u, s, vh = np.linalg.svd(_mode3_dft(a), full_matrices=False)
+    cutoff = tol * s.max(axis=1, keepdims=True)
+    keep = s > cutoff
+    sinv = np.zeros_like(s)
+    sinv[keep] = 1.0 / s[keep]
+    fp = np.matmul(np.conj(vh).transpose(0, 2, 1), sinv[:, :, None] * np.conj(u).transpose(0, 2, 1))
+    return _mode3_idft_real(fp)
+
+
+def op_count(kind, n1, n2, n3, p) -> int:
+    """baselines.py:156-190 (closed-form product operation counts)."""
+    cross = n1 * n2 + n2 * n3 + n1 * n3
+    base = n1 * n2 * n3 * p
+    if kind == "m":
+        return base + cross * p * p
+    if kind == "t":
+        if p & (p - 1) == 0:
+            return base + cross * p * (p.bit_length() - 1)
+        return base + round(cross * p * np.log2(p))
+    if kind == "w":
+        return base + 2 * p * cross
+    raise ValueError(kind)

@@ -7,6 +7,7 @@ The compute runs in ``libwten_b200.so`` (hand-written CUDA for sm_100a, C ABI in
 library or a CUDA device, compute calls raise ``NativeUnavailable``.
 """
 
+from . import baselines
 from ._native import NativeError, NativeUnavailable
 from .algebra import (
     face_product,
@@ -49,6 +50,7 @@ from .tensor import as_tensor3, frobenius_norm, frontal_slice, matrix_svd, set_f
 __version__ = "0.1.0"
 
 __all__ = [
+    "baselines",
     "NativeError", "NativeUnavailable",
     "face_product", "identity_tensor", "inverse_tensor", "orthogonal_tensor", "slicewise_matmul", "w_product",
     "SvdFactors", "TruncationBound", "pinv_w", "pinv_w_via_factors", "sp_pinv_w", "sp_w_svd",

@@ -144,6 +144,30 @@ extern "C" int wt_copy2d_f64(const double* src, int64_t lds, int64_t strideS, do
   return check_launch("wt_copy2d_f64");
 }
 
+// Tube deltas for the comparator DFT: out[t][0] = x[t][0], out[t][k] = x[t][k] - x[t][0].
+// A DFT row k' != 0 sums to zero, so it can be applied to the deltas instead of
+// the samples; constant tubes then give exactly zero off-DC coefficients, as
+// an FFT's butterflies do (baselines.py:68 np.fft.fft).
+__global__ void tube_delta_kernel(const double* __restrict__ x, int64_t total, int64_t p,
+                                  double* __restrict__ out) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t k = e % p;
+    const double v = x[e];
+    out[e] = k == 0 ? v : __dsub_rn(v, x[e - k]);
+  }
+}
+
+extern "C" int wt_tube_delta_f64(const double* x, int64_t ntubes, int64_t p, double* out,
+                                 void* stream) {
+  WT_REQUIRE(ntubes >= 0 && p >= 1, "tube_delta: bad shape");
+  const int64_t total = ntubes * p;
+  if (total == 0) return WT_OK;
+  const int64_t blocks = std::min<int64_t>((total + 255) / 256, 148 * 16);
+  tube_delta_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(x, total, p, out);
+  return check_launch("wt_tube_delta_f64");
+}
+
 size_t wt_band_reduce_parts(int64_t ntubes) {
   return (size_t)std::max<int64_t>(1, std::min<int64_t>(1184, (ntubes + 63) / 64));
 }

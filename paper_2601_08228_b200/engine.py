@@ -272,6 +272,16 @@ def pinv_blocks(a: torch.Tensor, sigma: torch.Tensor, vec: torch.Tensor, tol: fl
     return gemm(t, vec, out=out)                      # (batch, n2, n1)
 
 
+def tube_delta(x: torch.Tensor) -> torch.Tensor:
+    """(n1, n2, p) -> deltas from each tube's first sample (first sample kept)."""
+    lib = N.require_gpu()
+    assert x.is_contiguous()
+    out = torch.empty_like(x)
+    N.check(lib.wt_tube_delta_f64(_ptr(x), x.numel() // max(1, x.shape[-1]), x.shape[-1], _ptr(out),
+                                  _stream()), "wt_tube_delta_f64")
+    return out
+
+
 # ------------------------------------------------------------ reductions ----
 
 def band_sums(x: torch.Tensor, y: torch.Tensor | None, mode: int) -> torch.Tensor:

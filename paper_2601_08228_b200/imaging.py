@@ -86,10 +86,17 @@ def blur(x, a_v, a_h, levels):
 
 
 def deblur(b, a_v, a_h, levels, method="w", tol=1e-12):
-    """A_V^+ *_w B *_w (A_H^T)^+ with the w (pinv_w) or spw (sp_pinv_w) inverse."""
-    inv = pinv_w if method == "w" else sp_pinv_w
-    if method not in ("w", "spw"):
+    """A_V^+ * B * (A_H^T)^+ (SPEC.md:495-503): method "w" (pinv_w), "spw" (sp_pinv_w)
+    under the w-product, or "t" (t_pinv under the t-product, the paper's comparator)."""
+    if method not in ("w", "spw", "t"):
         raise ValueError(f"unknown deblur method {method!r}")
+    if method == "t":
+        from .baselines import t_pinv, t_product
+
+        left = t_pinv(a_v, tol)
+        right = t_pinv(transpose(a_h), tol)
+        return t_product(t_product(left, b), right)
+    inv = pinv_w if method == "w" else sp_pinv_w
     left = inv(a_v, levels, tol)
     right = inv(transpose(a_h), levels, tol)
     return w_product(w_product(left, b, levels), right, levels)

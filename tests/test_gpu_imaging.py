@@ -59,3 +59,18 @@ def test_config5_deblur_full_size():
     # deblur-w == deblur-spw for slice-constant operators
     xs = imaging.deblur(b, avd, ahd, 3, "spw", tol=1e-3)
     assert relerr(xs.cpu().numpy(), xr_h) < 1e-12
+
+
+def test_deblur_t_method_matches_oracle():
+    """SPEC.md:495-499 method t: t_pinv sandwich under the t-product (the paper's comparator)."""
+    x, av, ah, eta = synth.deblur_problem(n=96, p=24, endmembers=6, noise=0.005)
+    b = O.t_product(O.t_product(av, x), O.transpose(ah)) + eta
+    got = imaging.deblur(b, av, ah, 3, "t", tol=1e-3)
+    left = O.t_pinv(av, 1e-3)
+    right = O.t_pinv(O.transpose(ah), 1e-3)
+    want = O.t_product(O.t_product(left, b), right)
+    assert relerr(got, want) < 1e-8
+    assert abs(imaging.psnr(x, got) - O.psnr(x, want)) < 1e-6
+    # the slice-constant operator's t-pseudo-inverse is itself slice-constant
+    tp = W.baselines.t_pinv(av, 1e-3)
+    assert np.abs(tp - tp[:, :, :1]).max() <= 1e-15 * np.abs(tp).max()

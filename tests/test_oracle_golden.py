@@ -156,3 +156,49 @@ def test_ring_constructors_match_reference_fixtures(golden):
         with pytest.raises(ValueError) as ei:
             O.inverse_tensor(gi[name], 2)
         assert ei.value.args[0] == want
+
+
+# ------------------------------------------------ comparator products ----
+
+BL_PRODUCTS = ["t1", "t2", "t3", "t4", "t5"]
+
+
+@pytest.mark.parametrize("name", BL_PRODUCTS)
+def test_t_and_m_product_match_reference_fixtures(golden, name):
+    g = golden("baselines.npz")
+    a, b = g[f"{name}_a"], g[f"{name}_b"]
+    assert relerr(O.t_product(a, b), g[f"{name}_t"]) < 1e-13
+    if f"{name}_m" in g.files:
+        m = O.dct_matrix(a.shape[2])
+        assert np.abs(m - g[f"{name}_dct"]).max() < 1e-14
+        assert relerr(O.m_product(a, b, m, m.T), g[f"{name}_m"]) < 1e-13
+
+
+@pytest.mark.parametrize("seed", range(20))
+def test_t_product_equals_block_circulant_product(seed):
+    """FFT t-product == brute-force block-circulant product to 1e-10."""
+    rng = np.random.default_rng(seed)
+    n1, n2, n3 = (int(v) for v in rng.integers(1, 7, size=3))
+    p = int(rng.integers(1, 9))
+    a = rng.standard_normal((n1, n2, p))
+    b = rng.standard_normal((n2, n3, p))
+    assert relerr(O.t_product(a, b), O.t_product_circulant(a, b)) < 1e-10
+
+
+@pytest.mark.parametrize("name", ["s1", "s2", "s3"])
+def test_t_svd_t_pinv_match_reference_fixtures(golden, name):
+    g = golden("baselines.npz")
+    x = g[f"{name}_x"]
+    r = {"s1": 2, "s2": 3, "s3": 7}[name]
+    assert relerr(O.t_svd(x, r), g[f"{name}_tsvd"]) < 1e-12
+    assert relerr(O.t_pinv(x), g[f"{name}_tpinv"]) < 1e-12
+    assert relerr(O.t_pinv(x, 1e-1), g[f"{name}_tpinv_1e-1"]) < 1e-12
+
+
+def test_identities_and_constant_tubes_match_reference(golden):
+    g = golden("baselines.npz")
+    assert np.array_equal(O.tube_identity(3, 5), g["tube_identity_3_5"])
+    m = O.dct_matrix(6)
+    assert np.abs(O.m_identity(3, 6, m.T) - g["m_identity_3_6"]).max() < 1e-14
+    assert relerr(O.t_pinv(g["const_x"]), g["const_tpinv"]) < 1e-12
+    assert relerr(O.t_svd(g["const_x"], 2), g["const_tsvd_2"]) < 1e-12
