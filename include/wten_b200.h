@@ -148,10 +148,10 @@ int wt_copy2d_f64(const double* src, int64_t lds, int64_t strideS, double* dst, 
                   int64_t strideD, int64_t rows, int64_t cols, int64_t batch, int trans,
                   void* stream);
 
-/* Comparator-DFT helper: out[t][0] = x[t][0], out[t][k] = x[t][k] - x[t][0]
- * over ntubes tubes of p samples (tube-fastest).  Feeds the mode-3 DFT GEMM of
- * the t-product baselines so constant tubes transform to exact zeros off DC,
- * as np.fft.fft does (reference baselines.py:68,118,129). */
+/* Comparator-DFT helper: out[t][k] = x[t][k] - x[t][0] over ntubes tubes of p
+ * samples (tube-fastest).  The t-product baselines FFT these deltas and add
+ * p * x[t][0] to DC, so constant tubes transform to exact zeros off DC, as
+ * np.fft.fft does (reference baselines.py:68,118,129). */
 int wt_tube_delta_f64(const double* x, int64_t ntubes, int64_t p, double* out, void* stream);
 
 /* Deterministic per-band reductions used by the quality metrics (PSNR/SSIM,

@@ -2,26 +2,25 @@
 operation-count model -- drop-in for ``wten.baselines``
 (/root/reference/pkg/src/wten/baselines.py).
 
-These are the products the paper ranks the w-product against; on the GPU they
-reuse the w-path kernels instead of an FFT library:
+These are the products the paper ranks the w-product against, built on the
+w-path kernels plus cuFFT for the t-product's DFT (an O(p log p) transform, so
+the w-vs-t comparison stays fair):
 
-* mode-3 transforms are ONE K3 GEMM per operand: a (q x p) transform matrix
-  times the (n1 n2 x p) tube matrix, written straight into the frequency-major
-  (q, n1, n2) stack the facewise product needs (no transposition copies).  The
-  t-product's DFT is the real half-spectrum pair [cos; -sin] (q = 2(p//2 + 1)
-  rows, exact for any p, conjugate symmetry supplies the other half); the
-  inverse is one more GEMM against the weighted [cos, -sin] synthesis matrix,
-  which produces the real part the reference keeps (baselines.py:71-72).  The
-  DFT GEMM reads tube deltas x_k - x_0 (wt_tube_delta_f64), so a constant tube
-  has exactly zero off-DC coefficients, as numpy's FFT butterflies give; t_pinv
-  of slice-constant operators (the deblurring comparison) depends on it.
-* the complex facewise product is four real K3 GEMMs (re.re - im.im, re.im +
-  im.re) accumulated in place;
-* the complex per-slice SVD / pinv of t_svd / t_pinv run K4 on the real
-  embedding [[Re, -Im], [Im, Re]]: its singular values are those of the complex
-  slice, each twice, and truncation to 2r (or inversion with the same
-  tol * sigma_max cutoff) commutes with the embedding, so the re/im blocks of
-  the result are the complex rank-r truncation (pseudo-inverse).
+* t-product: half-spectrum rfft along mode 3 of the tube deltas x_k - x_0
+  (wt_tube_delta_f64; DC restored with p x_0), so a constant tube has exactly
+  zero off-DC coefficients as numpy's FFT butterflies give -- t_pinv of the
+  slice-constant blur operators depends on it; the complex facewise product is
+  four real K3 GEMMs (re.re - im.im, re.im + im.re) accumulated in place over
+  the p//2 + 1 frequencies; irfft returns the real part the reference keeps
+  (baselines.py:71-72).
+* m-product: the mode-3 transforms are ONE K3 GEMM per operand, a (p x p)
+  transform matrix times the (n1 n2 x p) tube matrix, written straight into
+  the slice-major (p, n1, n2) stack the facewise K3 product needs.
+* t_svd / t_pinv run K4 on the real embedding [[Re, -Im], [Im, Re]] of each
+  frequency slice: its singular values are those of the complex slice, each
+  twice, and truncation to 2r (or inversion with the same tol * sigma_max
+  cutoff) commutes with the embedding, so the re/im blocks of the result are
+  the complex rank-r truncation (pseudo-inverse).
 
 Only the half spectrum (p//2 + 1 frequencies) is decomposed; numpy decomposes
 all p and discards the imaginary residue.
@@ -88,49 +87,32 @@ def dct_transform(p):
     return ModeTransform(kind="matrix", M=m, Minv=np.ascontiguousarray(m.T))
 
 
-def _unit_circle(p: int):
-    """cos / sin of 2 pi t / p for t = 0..p-1, exact at multiples of p/4."""
-    t = np.arange(p)
-    c = np.cos(2.0 * np.pi * t / p)
-    s = np.sin(2.0 * np.pi * t / p)
-    quarter = (4 * t) % p == 0
-    q = (4 * t[quarter]) // p
-    c[quarter] = np.array([1.0, 0.0, -1.0, 0.0])[q]
-    s[quarter] = np.array([0.0, 1.0, 0.0, -1.0])[q]
-    return c, s
+def _spectrum(x: torch.Tensor, neg_imag: bool = False) -> torch.Tensor:
+    """Half-spectrum mode-3 DFT of (n1, n2, p) as a frequency-major stack
+    (2h, n1, n2) = [Re; Im] (plus [-Im] rows when ``neg_imag``), h = p//2 + 1.
 
-
-_DFT_CACHE: dict = {}
-
-
-def _dft_mats(p: int, device, neg_imag: bool = False):
-    """Analysis (rows [cos; -sin] (; +sin), applied to tube deltas) and synthesis
-    (p x 2h) matrices, h = p//2 + 1."""
-    key = (p, str(device), neg_imag)
-    if key in _DFT_CACHE:
-        return _DFT_CACHE[key]
+    cuFFT transforms the tube deltas x_k - x_0 (wt_tube_delta_f64) and the DC
+    term gets p * x_0 back, so constant tubes have exactly zero off-DC
+    coefficients (np.fft.fft's butterflies give the same, baselines.py:68)."""
+    n1, n2, p = x.shape
     h = p // 2 + 1
-    c, s = _unit_circle(p)
-    kk = np.outer(np.arange(h), np.arange(p)) % p          # (h, p) frequency x sample
-    rows = [c[kk], -s[kk]] + ([s[kk]] if neg_imag else [])
-    fwd = np.concatenate(rows, axis=0)
-    # applied to tube deltas (x_0, x_1 - x_0, ...): rows k' != 0 sum to zero, so
-    # the x_0 column drops out of them and the DC row weights it by p.
-    fwd[:, 0] = 0.0
-    fwd[0, 0] = float(p)
-    w = np.full(h, 2.0)
-    w[0] = 1.0
-    if p % 2 == 0:
-        w[h - 1] = 1.0
-    kt = kk.T                                               # (p, h) sample x frequency
-    inv = np.concatenate([c[kt] * w, -s[kt] * w], axis=1) / p
-    mats = (torch.from_numpy(fwd).to(device), torch.from_numpy(np.ascontiguousarray(inv)).to(device))
-    _DFT_CACHE[key] = mats
-    return mats
+    spec = torch.fft.rfft(E.tube_delta(x), dim=2)            # (n1, n2, h) complex
+    spec[:, :, 0] += p * x[:, :, 0]
+    ri = torch.view_as_real(spec).permute(3, 2, 0, 1)        # (2, h, n1, n2)
+    parts = [ri] + ([-ri[1:]] if neg_imag else [])
+    return torch.cat(parts, dim=0).reshape(-1, n1, n2).contiguous()
+
+
+def _synthesis(fc: torch.Tensor, p: int) -> torch.Tensor:
+    """Real part of the inverse DFT of a Hermitian half spectrum [Re; Im] (2h, n1, n2)."""
+    h = fc.shape[0] // 2
+    n1, n2 = fc.shape[1], fc.shape[2]
+    spec = torch.view_as_complex(fc.view(2, h, n1, n2).permute(2, 3, 1, 0).contiguous())
+    return torch.fft.irfft(spec, n=p, dim=2).contiguous()
 
 
 def _mode3(x: torch.Tensor, f: torch.Tensor) -> torch.Tensor:
-    """hat[k', i, j] = sum_k f[k', k] x[i, j, k] as a frequency-major (q, n1, n2) stack (K3)."""
+    """hat[k', i, j] = sum_k f[k', k] x[i, j, k] as a slice-major (q, n1, n2) stack (K3)."""
     n1, n2, p = x.shape
     out = E.gemm(f[None], x.reshape(1, n1 * n2, p), trans_b=True)   # (1, q, n1 n2)
     return out.view(f.shape[0], n1, n2)
@@ -181,16 +163,14 @@ def t_product(a, b):
         return torch.from_numpy(z).cuda() if dev else z
     da, db = E.as_device(a), E.as_device(b)
     h = p // 2 + 1
-    fwd, inv = _dft_mats(p, da.device)
-    fa = _mode3(E.tube_delta(da), fwd)                     # (2h, n1, n2)
-    fb = _mode3(E.tube_delta(db), fwd)                     # (2h, n2, n3)
+    fa, fb = _spectrum(da), _spectrum(db)                     # (2h, n1, n2), (2h, n2, n3)
     are, aim, bre, bim = fa[:h], fa[h:], fb[:h], fb[h:]
     fc = torch.empty((2 * h, n1, n3), dtype=F64, device=da.device)
     E.gemm(are, bre, out=fc[:h])
     E.gemm(aim, bim, alpha=-1.0, beta=1.0, out=fc[:h])
     E.gemm(are, bim, out=fc[h:])
     E.gemm(aim, bre, beta=1.0, out=fc[h:])
-    return _out(_unmode3(fc, inv), dev)
+    return _out(_synthesis(fc, p), dev)
 
 
 def tube_identity(n, p):
@@ -234,14 +214,13 @@ def _embedded_spectrum(x: torch.Tensor):
     """Half-spectrum real embeddings [[Re, -Im], [Im, Re]] of every DFT slice: (h, 2n1, 2n2)."""
     n1, n2, p = x.shape
     h = p // 2 + 1
-    fwd, inv = _dft_mats(p, x.device, neg_imag=True)
-    f = _mode3(E.tube_delta(x), fwd)                          # (3h, n1, n2): Re, Im, -Im
+    f = _spectrum(x, neg_imag=True)                           # (3h, n1, n2): Re, Im, -Im
     emb = torch.empty((h, 2 * n1, 2 * n2), dtype=F64, device=x.device)
     E.copy2d(f[:h], False, out=emb[:, :n1, :n2])
     E.copy2d(f[:h], False, out=emb[:, n1:, n2:])
     E.copy2d(f[h:2 * h], False, out=emb[:, n1:, :n2])
     E.copy2d(f[2 * h:], False, out=emb[:, :n1, n2:])
-    return emb, inv
+    return emb
 
 
 def _unembed(blocks: torch.Tensor, rows: int, cols: int) -> torch.Tensor:
@@ -262,11 +241,11 @@ def t_svd(a, r):
                         f"for {a.shape[0]}x{a.shape[1]} slices")
     n1, n2, p = a.shape
     _check_p(p)
-    emb, inv = _embedded_spectrum(E.as_device(a))
+    emb = _embedded_spectrum(E.as_device(a))
     sigma, vec, info = E.svd(emb, 2 * r)
     E.raise_if_failed(info)
     rec = E.truncated_recon(emb, sigma, vec, 2 * r)
-    return _out(_unmode3(_unembed(rec, n1, n2), inv), dev)
+    return _out(_synthesis(_unembed(rec, n1, n2), p), dev)
 
 
 def t_pinv(a, tol=1e-12):
@@ -279,11 +258,11 @@ def t_pinv(a, tol=1e-12):
     if n1 * n2 == 0:
         z = np.zeros((n2, n1, p))
         return torch.from_numpy(z).cuda() if dev else z
-    emb, inv = _embedded_spectrum(E.as_device(a))
+    emb = _embedded_spectrum(E.as_device(a))
     sigma, vec, info = E.svd(emb, 2 * min(n1, n2))
     E.raise_if_failed(info)
     blocks = E.pinv_blocks(emb, sigma, vec, tol)              # (h, 2 n2, 2 n1)
-    return _out(_unmode3(_unembed(blocks, n2, n1), inv), dev)
+    return _out(_synthesis(_unembed(blocks, n2, n1), p), dev)
 
 
 # ------------------------------------------------------------ op counts ----

@@ -348,10 +348,26 @@ __global__ void __launch_bounds__(kT) inv_persistent(const double* __restrict__ 
   if (!TMA) cp_async_wait<0>();
 }
 
-bool plan(FGeom& g, int& TQ) {
+// Tile height cap.  Forward: taller tiles write longer runs per packed slice
+// row (TQ * 8 bytes); measured at config 2 (tools/lift_tq_probe.py, round 1,
+// GB/s): L=1-3 best at 32 (+2%), L=4-6 at 64 (+7..14%), L=7 at 32 (+14%), L=8
+// needs CT = 256 so stays at 16.  Inverse: 16 (taller tiles cost 30%: the
+// tube-major final stores scatter over more tubes per warp).
+// WT_LIFT_TQ_MAX overrides both (diagnostics).
+int tq_max(bool fwd, int L) {
+  static const int env = [] {
+    const char* e = getenv("WT_LIFT_TQ_MAX");
+    return e ? atoi(e) : 0;
+  }();
+  if (env > 0) return env;
+  if (!fwd) return 16;
+  return (L >= 4 && L <= 6) ? 64 : 32;
+}
+
+bool plan(FGeom& g, int& TQ, bool fwd) {
   const int64_t unit = (int64_t)1 << g.L;
   const int64_t munits = g.p / unit;
-  for (int tq = 16; tq >= 2; tq >>= 1) {
+  for (int tq = tq_max(fwd, g.L); tq >= 2; tq >>= 1) {
     const int64_t cap = kMaxElems / tq;
     if (unit > cap) continue;
     int64_t best = 0;
@@ -427,9 +443,11 @@ int lift_fwd_fast(const double* x, int64_t ntubes, int64_t p, int L, double* out
   if (L < 1 || p % 2 || (uintptr_t)x % 16) return WT_ERR_UNSUPPORTED;
   FGeom g{ntubes, p, L, 0, 0, 0, 0, slice_base, mask, 0, 0, tab};
   int TQ = 0;
-  if (!plan(g, TQ)) return WT_ERR_UNSUPPORTED;
+  if (!plan(g, TQ, true)) return WT_ERR_UNSUPPORTED;
   const size_t smem = ((size_t)2 * TQ * g.LDT + (size_t)TQ * (g.LDA0 + g.LDA1)) * sizeof(double);
   switch (TQ) {
+    case 64: return launch(fwd_persistent<64>, smem, g.ntiles, st, x, out, g, "wt_lift_fwd_f64");
+    case 32: return launch(fwd_persistent<32>, smem, g.ntiles, st, x, out, g, "wt_lift_fwd_f64");
     case 16: return launch(fwd_persistent<16>, smem, g.ntiles, st, x, out, g, "wt_lift_fwd_f64");
     case 8: return launch(fwd_persistent<8>, smem, g.ntiles, st, x, out, g, "wt_lift_fwd_f64");
     case 4: return launch(fwd_persistent<4>, smem, g.ntiles, st, x, out, g, "wt_lift_fwd_f64");
@@ -445,14 +463,19 @@ int lift_inv_fast(const double* pyr, int64_t ntubes, int64_t p, int L, double* y
     return WT_ERR_UNSUPPORTED;
   FGeom g{ntubes, p, L, 0, 0, 0, 0, slice_base, mask, 0, 0, tab};
   int TQ = 0;
-  if (!plan(g, TQ)) return WT_ERR_UNSUPPORTED;
+  if (!plan(g, TQ, false)) return WT_ERR_UNSUPPORTED;
   const size_t smem = ((size_t)2 * g.CT * TQ + (size_t)2 * TQ * g.LDA0) * sizeof(double);
   if (smem > 200 * 1024) return WT_ERR_UNSUPPORTED;
   static TmaMaps maps;  // host copy; passed by value as a __grid_constant__ parameter
   // TMA boxes: 16 tubes (128-byte rows) x <= 256 slices, 16-byte-multiple stride
-  if (!tab && TQ == 16 && (g.CT >> 1) <= 256 && !getenv("WT_LIFT_NO_TMA") &&
-      make_maps(maps, pyr, g, TQ))
+  if (!tab && TQ >= 16 && (g.CT >> 1) <= 256 && !getenv("WT_LIFT_NO_TMA") &&
+      make_maps(maps, pyr, g, TQ)) {
+    if (TQ == 64)
+      return launch(inv_persistent<64, true>, smem, g.ntiles, st, pyr, y, g, "wt_lift_inv_f64", maps);
+    if (TQ == 32)
+      return launch(inv_persistent<32, true>, smem, g.ntiles, st, pyr, y, g, "wt_lift_inv_f64", maps);
     return launch(inv_persistent<16, true>, smem, g.ntiles, st, pyr, y, g, "wt_lift_inv_f64", maps);
+  }
   switch (TQ) {
     case 16: return launch(inv_persistent<16, false>, smem, g.ntiles, st, pyr, y, g, "wt_lift_inv_f64", maps);
     case 8: return launch(inv_persistent<8, false>, smem, g.ntiles, st, pyr, y, g, "wt_lift_inv_f64", maps);

@@ -144,17 +144,14 @@ extern "C" int wt_copy2d_f64(const double* src, int64_t lds, int64_t strideS, do
   return check_launch("wt_copy2d_f64");
 }
 
-// Tube deltas for the comparator DFT: out[t][0] = x[t][0], out[t][k] = x[t][k] - x[t][0].
-// A DFT row k' != 0 sums to zero, so it can be applied to the deltas instead of
-// the samples; constant tubes then give exactly zero off-DC coefficients, as
-// an FFT's butterflies do (baselines.py:68 np.fft.fft).
+// Tube deltas for the comparator DFT: out[t][k] = x[t][k] - x[t][0] (so out[t][0] = 0).
+// DFT(x) = DFT(out) + p x_0 e_0: constant tubes then give exactly zero off-DC
+// coefficients, as an FFT's butterflies do (baselines.py:68 np.fft.fft).
 __global__ void tube_delta_kernel(const double* __restrict__ x, int64_t total, int64_t p,
                                   double* __restrict__ out) {
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t k = e % p;
-    const double v = x[e];
-    out[e] = k == 0 ? v : __dsub_rn(v, x[e - k]);
+    out[e] = __dsub_rn(x[e], x[e - e % p]);
   }
 }
 

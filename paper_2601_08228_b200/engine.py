@@ -273,7 +273,7 @@ def pinv_blocks(a: torch.Tensor, sigma: torch.Tensor, vec: torch.Tensor, tol: fl
 
 
 def tube_delta(x: torch.Tensor) -> torch.Tensor:
-    """(n1, n2, p) -> deltas from each tube's first sample (first sample kept)."""
+    """(n1, n2, p) -> x[..., k] - x[..., 0] per tube (K: wt_tube_delta_f64)."""
     lib = N.require_gpu()
     assert x.is_contiguous()
     out = torch.empty_like(x)
