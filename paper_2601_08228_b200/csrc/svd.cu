@@ -114,7 +114,8 @@ __device__ __forceinline__ void load_chunk(double* Zs, const double* Xb, int64_t
 }
 
 __global__ void __launch_bounds__(kThreads, 3) svd_pair_kernel(SvdWs ws, int64_t mpad, int64_t npad,
-                                                               int round, double tol, int inner_sweeps) {
+                                                               int round, double tol, int inner_sweeps,
+                                                               int cross_only) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   PairSmem& S = *reinterpret_cast<PairSmem*>(smem_raw);
   const int b = ws.active[blockIdx.y];
@@ -213,7 +214,9 @@ __global__ void __launch_bounds__(kThreads, 3) svd_pair_kernel(SvdWs ws, int64_t
     double mx = 0.0;
     for (int e = tid; e < BW * BW; e += kThreads) {
       const int i = e / BW, j = e % BW;
-      if (i < j) {
+      // cross-only visits answer for the block I x block J pairs alone (the
+      // within-block pairs are tested and rotated at the sweep's round 0)
+      if (i < j && !(cross_only && (i < HB) == (j < HB))) {
         const double gii = S.G[0][i * LDG + i], gjj = S.G[0][j * LDG + j];
         const double gij = S.G[0][i * LDG + j];
         const double den = fmax(sqrt(gii * gjj), floor_c * gmax);
@@ -259,9 +262,17 @@ __global__ void __launch_bounds__(kThreads, 3) svd_pair_kernel(SvdWs ws, int64_t
     const int grp = tid / TPG, sub = tid % TPG;
     for (int sweep = 0; sweep < inner_sweeps; ++sweep) {
       int my_rot = 0;
-      for (int step = 0; step < BW - 1; ++step) {
-        int p = rr_index(grp, step, BW), q = rr_index(BW - 1 - grp, step, BW);
-        if (p > q) { const int t = p; p = q; q = t; }
+      const int nsteps = cross_only ? HB : BW - 1;
+      for (int step = 0; step < nsteps; ++step) {
+        int p, q;
+        if (cross_only) {  // block I x block J pairs only: 16 steps of 16 disjoint pairs
+          p = grp;
+          q = HB + (grp + step) % HB;
+        } else {           // all 496 pairs of the 32 columns: 31 round-robin steps
+          p = rr_index(grp, step, BW);
+          q = rr_index(BW - 1 - grp, step, BW);
+          if (p > q) { const int t = p; p = q; q = t; }
+        }
         const double gpp = G[p * LDG + p], gqq = G[q * LDG + q], gpq = G[p * LDG + q];
         // rotate iff |g_pq| > tol * max(sqrt(g_pp g_qq), floor_c g_max)  (squared: no sqrt)
         const double fl = floor_c * gmax;
@@ -626,6 +637,15 @@ extern "C" int wt_svd_jacobi_f64(const double* A, int64_t lda, int64_t strideA, 
   int inner = 1;
   if (const char* e = getenv("WT_SVD_INNER_SWEEPS")) inner = std::max(1, std::min(kMaxInnerSweeps, atoi(e)));
   bool hit_max = true;
+  // Round 0 of a sweep visits every block once with the full 32-column inner
+  // sweep (all within-block pairs); later rounds rotate (and test) only the
+  // cross-block pairs, so every column pair is still covered once per sweep (a
+  // cyclic ordering) with 16 instead of 31 eigen steps per visit.  Costs ~1-2
+  // extra sweeps; measured (round 1, tools/svd_probe.py, compare_products.py):
+  // 256 columns -9%, 1024 -3.5%, 384 (t-svd embeddings) -22%, but 128 +5%
+  // (few rounds per sweep, latency-bound), hence only from 16 blocks up.
+  int cross = nb >= 16;
+  if (const char* e = getenv("WT_SVD_CROSS")) cross = atoi(e);
   // Reorder the columns by descending norm before every sweep: measured on the
   // config-3/4 slices 13 -> 12 and 17 -> 16 sweeps, -10% time (round 1).
   int sort_mode = 2;
@@ -644,7 +664,7 @@ extern "C" int wt_svd_jacobi_f64(const double* A, int64_t lda, int64_t strideA, 
     }
     for (int round = 0; round < nb - 1; ++round) {
       svd_pair_kernel<<<dim3(nb / 2, (unsigned)n_active), kThreads, sizeof(PairSmem), st>>>(
-          ws, L.mpad, L.npad, round, tol, inner);
+          ws, L.mpad, L.npad, round, tol, inner, cross && round > 0);
     }
     if (int e = check_launch("svd_pair_kernel")) return e;
     if (getenv("WT_SVD_DEBUG")) {  // per-sweep convergence trace (diagnostics only)
