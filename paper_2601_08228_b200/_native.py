@@ -12,7 +12,7 @@ import ctypes
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libwten_b200.so")
+LIB_PATH = os.environ.get("WT_LIB_PATH") or os.path.join(HERE, "libwten_b200.so")  # override: A/B builds
 
 c_double_p = ctypes.c_void_p  # device pointers travel as integers
 i64 = ctypes.c_int64

@@ -20,8 +20,14 @@
 namespace wt {
 namespace {
 
-constexpr int BK = 16;
-constexpr int STAGES = 3;
+#ifndef WT_GEMM_BK
+#define WT_GEMM_BK 16
+#endif
+#ifndef WT_GEMM_STAGES
+#define WT_GEMM_STAGES 3
+#endif
+constexpr int BK = WT_GEMM_BK;
+constexpr int STAGES = WT_GEMM_STAGES;
 
 struct GemmArgs {
   int64_t M, N, K;
@@ -62,6 +68,40 @@ __global__ void __launch_bounds__(WM* WN * 32) gemm_f64_kernel(GemmArgs g) {
   const int64_t m0 = (int64_t)blockIdx.y * BM, n0 = (int64_t)blockIdx.x * BN;
   const int nk = (int)((g.K + BK - 1) / BK);
 
+  // Loader geometry, fixed for the whole kernel: each thread owns A_IT (B_IT)
+  // 16-byte chunks of every stage at the same tile position; only the k offset
+  // moves, so a stage's addresses are one multiply-add per chunk (ncu: the
+  // per-chunk index math of the first version was 40% of the stall samples).
+  constexpr int A_ROWS = TA ? BK : BM, A_COLS = TA ? BM : BK;
+  constexpr int B_ROWS = TB ? BN : BK, B_COLS = TB ? BK : BN;
+  constexpr int A_CH = A_ROWS * A_COLS / VEC, B_CH = B_ROWS * B_COLS / VEC;
+  constexpr int A_IT = (A_CH + NT - 1) / NT, B_IT = (B_CH + NT - 1) / NT;
+  int64_t a_go[A_IT], b_go[B_IT];  // global element offset at k0 = 0
+  int a_so[A_IT], b_so[B_IT];      // shared element offset within a stage
+  int a_k[A_IT], b_k[B_IT];        // k index of the chunk at k0 = 0 (-1: outside M / N)
+#pragma unroll
+  for (int it = 0; it < A_IT; ++it) {
+    const int c = tid + it * NT;
+    const int r = c / (A_COLS / VEC), cc = (c % (A_COLS / VEC)) * VEC;
+    const int64_t gm = m0 + (TA ? cc : r);
+    const int kk = TA ? r : cc;
+    a_so[it] = r * SL::A_LD + cc;
+    a_go[it] = TA ? (int64_t)kk * g.lda + gm : gm * g.lda + kk;
+    a_k[it] = (c < A_CH && gm < g.M) ? kk : -1;
+  }
+#pragma unroll
+  for (int it = 0; it < B_IT; ++it) {
+    const int c = tid + it * NT;
+    const int r = c / (B_COLS / VEC), cc = (c % (B_COLS / VEC)) * VEC;
+    const int64_t gn = n0 + (TB ? r : cc);
+    const int kk = TB ? cc : r;
+    b_so[it] = r * SL::B_LD + cc;
+    b_go[it] = TB ? gn * g.ldb + kk : (int64_t)kk * g.ldb + gn;
+    b_k[it] = (c < B_CH && gn < g.N) ? kk : -1;
+  }
+  const int64_t a_kstep = TA ? (int64_t)BK * g.lda : BK;  // element step per k tile
+  const int64_t b_kstep = TB ? BK : (int64_t)BK * g.ldb;
+
   for (int64_t b = blockIdx.z; b < g.batch; b += gridDim.z) {
     const double* __restrict__ A = g.A + b * g.sA;
     const double* __restrict__ B = g.B + b * g.sB;
@@ -70,34 +110,18 @@ __global__ void __launch_bounds__(WM* WN * 32) gemm_f64_kernel(GemmArgs g) {
     auto load_stage = [&](int stage, int kt) {
       double* As = smem + stage * SL::STAGE_ELEMS;
       double* Bs = As + SL::A_ELEMS;
-      const int64_t k0 = (int64_t)kt * BK;
-      // A: logical (m, k) tile BM x BK
-      {
-        constexpr int ROWS = TA ? BK : BM;   // smem rows
-        constexpr int COLS = TA ? BM : BK;   // contiguous extent
-        constexpr int CHUNKS = ROWS * COLS / VEC;
-        for (int c = tid; c < CHUNKS; c += NT) {
-          const int r = c / (COLS / VEC), cc = (c % (COLS / VEC)) * VEC;
-          int64_t gm, gk;
-          if (TA) { gk = k0 + r; gm = m0 + cc; } else { gm = m0 + r; gk = k0 + cc; }
-          const bool ok = (gm < g.M) && (gk < g.K);
-          const double* src = ok ? (TA ? A + gk * g.lda + gm : A + gm * g.lda + gk) : A;
-          cp_async_zfill<VEC * 8>(As + r * SL::A_LD + cc, src, ok);
-        }
+      const int k0 = kt * BK;
+#pragma unroll
+      for (int it = 0; it < A_IT; ++it) {
+        if (A_CH % NT != 0 && tid + it * NT >= A_CH) break;
+        const bool ok = a_k[it] >= 0 && a_k[it] + k0 < g.K;
+        cp_async_zfill<VEC * 8>(As + a_so[it], ok ? A + a_go[it] + kt * a_kstep : A, ok);
       }
-      // B: logical (k, n) tile BK x BN
-      {
-        constexpr int ROWS = TB ? BN : BK;
-        constexpr int COLS = TB ? BK : BN;
-        constexpr int CHUNKS = ROWS * COLS / VEC;
-        for (int c = tid; c < CHUNKS; c += NT) {
-          const int r = c / (COLS / VEC), cc = (c % (COLS / VEC)) * VEC;
-          int64_t gk, gn;
-          if (TB) { gn = n0 + r; gk = k0 + cc; } else { gk = k0 + r; gn = n0 + cc; }
-          const bool ok = (gn < g.N) && (gk < g.K);
-          const double* src = ok ? (TB ? B + gn * g.ldb + gk : B + gk * g.ldb + gn) : B;
-          cp_async_zfill<VEC * 8>(Bs + r * SL::B_LD + cc, src, ok);
-        }
+#pragma unroll
+      for (int it = 0; it < B_IT; ++it) {
+        if (B_CH % NT != 0 && tid + it * NT >= B_CH) break;
+        const bool ok = b_k[it] >= 0 && b_k[it] + k0 < g.K;
+        cp_async_zfill<VEC * 8>(Bs + b_so[it], ok ? B + b_go[it] + kt * b_kstep : B, ok);
       }
     };
 
