@@ -41,6 +41,9 @@ constexpr int LDG = BW + 1;  // Gram / Q pitch
 constexpr int kThreads = 256;
 constexpr double kFloorEps = 1e3 * 2.220446049250313e-16;  // null-column floor (see the test)
 constexpr int kMaxInnerSweeps = 16;
+#ifndef WT_SVD_MINB
+#define WT_SVD_MINB 3
+#endif
 #ifndef WT_EIG_WARPS
 #define WT_EIG_WARPS 8
 #endif
@@ -95,9 +98,10 @@ __device__ __forceinline__ int rr_index(int pos, int round, int nb) {
 
 struct PairSmem {
   double Z[2][BW * LDZ];
-  double G[2][BW * LDG];
+  double G[1][BW * LDG];
   double Q[BW * LDG];
   double warp_off[kThreads / 32];
+  double gmax;
   int any_rot;
 };
 
@@ -113,7 +117,7 @@ __device__ __forceinline__ void load_chunk(double* Zs, const double* Xb, int64_t
   }
 }
 
-__global__ void __launch_bounds__(kThreads, 3) svd_pair_kernel(SvdWs ws, int64_t mpad, int64_t npad,
+__global__ void __launch_bounds__(kThreads, WT_SVD_MINB) svd_pair_kernel(SvdWs ws, int64_t mpad, int64_t npad,
                                                                int round, double tol, int inner_sweeps,
                                                                int cross_only) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -195,6 +199,11 @@ __global__ void __launch_bounds__(kThreads, 3) svd_pair_kernel(SvdWs ws, int64_t
               S.G[0][c * LDG + r] = acc[t][h];
             }
           }
+      __syncwarp();
+      double gm = S.G[0][lane * LDG + lane];  // largest squared column norm of the panel
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) gm = fmax(gm, __shfl_xor_sync(0xffffffffu, gm, o));
+      if (lane == 0) S.gmax = gm;
     }
     __syncthreads();
   }
@@ -206,11 +215,12 @@ __global__ void __launch_bounds__(kThreads, 3) svd_pair_kernel(SvdWs ws, int64_t
   // ~1e-13 |z_max|), whose directions are rounding noise and must not keep
   // the iteration alive; real columns are held to the relative tolerance.
   // `off` is the largest |g_ij| / (that bound) * tol, so off < tol <=> converged.
-  double gmax = 0.0;
-#pragma unroll 4
-  for (int i = 0; i < BW; ++i) gmax = fmax(gmax, S.G[0][i * LDG + i]);
+  const double gmax = S.gmax;
   const double floor_c = kFloorEps * kFloorEps / tol;
   {
+    // 1 / max(sqrt(g_ii g_jj), floor_c g_max) = min(rsqrt(g_ii g_jj), 1 / (floor_c g_max)):
+    // no sqrt and no division per pair (the test was ~10% of the kernel's stall samples)
+    const double rfl = 1.0 / (floor_c * gmax);
     double mx = 0.0;
     for (int e = tid; e < BW * BW; e += kThreads) {
       const int i = e / BW, j = e % BW;
@@ -219,9 +229,8 @@ __global__ void __launch_bounds__(kThreads, 3) svd_pair_kernel(SvdWs ws, int64_t
       if (i < j && !(cross_only && (i < HB) == (j < HB))) {
         const double gii = S.G[0][i * LDG + i], gjj = S.G[0][j * LDG + j];
         const double gij = S.G[0][i * LDG + j];
-        const double den = fmax(sqrt(gii * gjj), floor_c * gmax);
         double c = 0.0;
-        if (gij != 0.0) c = den > 0.0 ? fabs(gij) / den : INFINITY;
+        if (gij != 0.0) c = fabs(gij) * fmin(rsqrt(gii * gjj), rfl);
         if (isnan(gii) || isnan(gjj)) c = gii + gjj;
         mx = nanmax(mx, c);
       }
@@ -260,6 +269,10 @@ __global__ void __launch_bounds__(kThreads, 3) svd_pair_kernel(SvdWs ws, int64_t
     double* G = S.G[0];
     double* Q = S.Q;
     const int grp = tid / TPG, sub = tid % TPG;
+    const double fl = floor_c * gmax;
+    const double rot_floor = tol * tol * (fl * fl);
+    const double tol2 = tol * tol;
+    const double psc = gmax > 0.0 ? ldexp(1.0, -ilogb(gmax)) : 1.0;  // keeps a^2 + b^2 in range
     for (int sweep = 0; sweep < inner_sweeps; ++sweep) {
       int my_rot = 0;
       const int nsteps = cross_only ? HB : BW - 1;
@@ -275,9 +288,7 @@ __global__ void __launch_bounds__(kThreads, 3) svd_pair_kernel(SvdWs ws, int64_t
         }
         const double gpp = G[p * LDG + p], gqq = G[q * LDG + q], gpq = G[p * LDG + q];
         // rotate iff |g_pq| > tol * max(sqrt(g_pp g_qq), floor_c g_max)  (squared: no sqrt)
-        const double fl = floor_c * gmax;
-        const double psc = gmax > 0.0 ? ldexp(1.0, -ilogb(gmax)) : 1.0;  // keeps a^2 + b^2 in range
-        const bool rot = gpq * gpq > tol * tol * fmax(gpp * gqq, fl * fl);
+        const bool rot = gpq * gpq > fmax(tol2 * (gpp * gqq), rot_floor);
         __syncwarp();
         double c = 1.0, s = 0.0;
         if (rot) {
