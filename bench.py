@@ -451,6 +451,38 @@ def wproduct_workload(args, steps=20, warmup=3):
             "value": ms / steps * 1e3}
 
 
+def comparators_workload(args):
+    """Paper-style ratios on B200 (SPEC acceptance 8): w- vs t- vs m-product
+    on a p = 256 cube and w-svd / sp-w-svd vs t-svd on the config-3 cube, device-resident."""
+    import torch
+
+    import paper_2601_08228_b200 as W
+    from paper_2601_08228_b200 import baselines as B, synth
+
+    p = 256
+    g = torch.Generator(device="cuda").manual_seed(7)
+    a = torch.randn((p, p, p), dtype=torch.float64, device="cuda", generator=g)
+    b = torch.randn((p, p, p), dtype=torch.float64, device="cuda", generator=g)
+    tr = B.dct_transform(p)
+    L = W.max_levels(p)
+    out = {"config": f"cube {p}^3 products (L={L}); w_svd / sp_w_svd / t_svd on 256x256x192 r=20 L=3",
+           "metric": "ms per call (device-resident)"}
+    for k, fn in (("w_product", lambda: W.w_product(a, b, L)), ("t_product", lambda: B.t_product(a, b)),
+                  ("m_product", lambda: B.m_product(a, b, tr))):
+        out[k + "_ms"] = timed_region(lambda rec: fn(), 5, 2) / 5
+    x = torch.from_numpy(synth.hyperspectral_cube(256, 256, 192, seed=0)).cuda()
+    for k, fn in (("w_svd", lambda: W.w_svd(x, 20, 3)), ("sp_w_svd", lambda: W.sp_w_svd(x, 20, 3)),
+                  ("t_svd", lambda: B.t_svd(x, 20))):
+        out[k + "_ms"] = timed_region(lambda rec: fn(), 3, 1) / 3
+    out["speedup_w_vs_t_product"] = out["t_product_ms"] / out["w_product_ms"]
+    out["speedup_w_vs_t_svd"] = out["t_svd_ms"] / out["w_svd_ms"]
+    out["speedup_spw_vs_t_svd"] = out["t_svd_ms"] / out["sp_w_svd_ms"]
+    out["op_counts"] = {k: B.op_count(k, p, p, p, p).count for k in "mtw"}
+    out["note"] = ("t-product family: cuFFT along mode 3 + the same DMMA GEMM / Jacobi SVD kernels "
+                   "(complex slices via 4 real GEMMs / the real embedding), p//2+1 frequencies")
+    return out
+
+
 # ----------------------------------------------------------- CPU legs ----
 
 def cpu_transform_sample(x_host, reps=2, rows=512):
@@ -528,7 +560,7 @@ def main():
     _native.require_gpu()
 
     if args.workloads == "default":
-        wl = (["wsvd", "spwsvd", "deblur", "wproduct"] if ws == 1
+        wl = (["wsvd", "spwsvd", "deblur", "wproduct", "comparators"] if ws == 1
               else ["spwsvd_fused", "spwsvd_sharded"])
     elif args.workloads == "none":
         wl = []
@@ -547,6 +579,8 @@ def main():
                 workloads[name] = deblur_workload(args)
             elif name == "wproduct":
                 workloads[name] = wproduct_workload(args)
+            elif name == "comparators":
+                workloads[name] = comparators_workload(args)
             elif name in ("spwsvd_sharded", "spwsvd_fused"):
                 from paper_2601_08228_b200 import sharded
 

@@ -6,17 +6,18 @@ These are the products the paper ranks the w-product against, built on the
 w-path kernels plus cuFFT for the t-product's DFT (an O(p log p) transform, so
 the w-vs-t comparison stays fair):
 
-* t-product: half-spectrum rfft along mode 3 of the tube deltas x_k - x_0
-  (wt_tube_delta_f64; DC restored with p x_0), so a constant tube has exactly
-  zero off-DC coefficients as numpy's FFT butterflies give -- t_pinv of the
-  slice-constant blur operators depends on it; the complex facewise product is
-  four real K3 GEMMs (re.re - im.im, re.im + im.re) accumulated in place over
-  the p//2 + 1 frequencies; irfft returns the real part the reference keeps
-  (baselines.py:71-72).
+* t-product: half-spectrum rfft along mode 3; the complex facewise product
+  of each of the p//2 + 1 frequencies is ONE real K3 GEMM,
+  [Re A | Im A] [[Re B, Im B], [-Im B, Re B]] = [Re C | Im C]; irfft returns
+  the real part the reference keeps (baselines.py:71-72).
 * m-product: the mode-3 transforms are ONE K3 GEMM per operand, a (p x p)
   transform matrix times the (n1 n2 x p) tube matrix, written straight into
   the slice-major (p, n1, n2) stack the facewise K3 product needs.
-* t_svd / t_pinv run K4 on the real embedding [[Re, -Im], [Im, Re]] of each
+* t_svd / t_pinv transform the tube deltas x_k - x_0 (wt_tube_delta_f64; DC
+  restored with p x_0), so a constant tube has exactly zero off-DC
+  coefficients as numpy's FFT butterflies give -- the relative pinv cutoff on
+  the slice-constant blur operators depends on it -- and run K4 on the real
+  embedding [[Re, -Im], [Im, Re]] of each
   frequency slice: its singular values are those of the complex slice, each
   twice, and truncation to 2r (or inversion with the same tol * sigma_max
   cutoff) commutes with the embedding, so the re/im blocks of the result are
@@ -87,20 +88,29 @@ def dct_transform(p):
     return ModeTransform(kind="matrix", M=m, Minv=np.ascontiguousarray(m.T))
 
 
-def _spectrum(x: torch.Tensor, neg_imag: bool = False) -> torch.Tensor:
+def _spectrum(x: torch.Tensor, neg_imag: bool = False, exact_dc: bool = True) -> torch.Tensor:
     """Half-spectrum mode-3 DFT of (n1, n2, p) as a frequency-major stack
     (2h, n1, n2) = [Re; Im] (plus [-Im] rows when ``neg_imag``), h = p//2 + 1.
 
-    cuFFT transforms the tube deltas x_k - x_0 (wt_tube_delta_f64) and the DC
-    term gets p * x_0 back, so constant tubes have exactly zero off-DC
-    coefficients (np.fft.fft's butterflies give the same, baselines.py:68)."""
+    With ``exact_dc`` cuFFT transforms the tube deltas x_k - x_0
+    (wt_tube_delta_f64) and the DC term gets p * x_0 back, so constant tubes
+    have exactly zero off-DC coefficients (np.fft.fft's butterflies give the
+    same, baselines.py:68) -- the pseudo-inverse's relative cutoff needs that;
+    the products do not (one memory pass less)."""
     n1, n2, p = x.shape
-    h = p // 2 + 1
-    spec = torch.fft.rfft(E.tube_delta(x), dim=2)            # (n1, n2, h) complex
-    spec[:, :, 0] += p * x[:, :, 0]
-    ri = torch.view_as_real(spec).permute(3, 2, 0, 1)        # (2, h, n1, n2)
-    parts = [ri] + ([-ri[1:]] if neg_imag else [])
-    return torch.cat(parts, dim=0).reshape(-1, n1, n2).contiguous()
+    if exact_dc:
+        spec = torch.fft.rfft(E.tube_delta(x), dim=2)        # (n1, n2, h) complex
+        spec[:, :, 0] += p * x[:, :, 0]
+    else:
+        spec = torch.fft.rfft(x, dim=2)
+    h = spec.shape[2]
+    ri = torch.view_as_real(spec).permute(3, 2, 0, 1)        # (2, h, n1, n2) view
+    # a fresh tensor: standard strides even for size-1 dims (the GEMM reads stride(1))
+    out = torch.empty(((3 if neg_imag else 2) * h, n1, n2), dtype=F64, device=x.device)
+    out[:2 * h].view(2, h, n1, n2).copy_(ri)
+    if neg_imag:
+        torch.neg(out[h:2 * h], out=out[2 * h:])
+    return out
 
 
 def _synthesis(fc: torch.Tensor, p: int) -> torch.Tensor:
@@ -163,14 +173,21 @@ def t_product(a, b):
         return torch.from_numpy(z).cuda() if dev else z
     da, db = E.as_device(a), E.as_device(b)
     h = p // 2 + 1
-    fa, fb = _spectrum(da), _spectrum(db)                     # (2h, n1, n2), (2h, n2, n3)
-    are, aim, bre, bim = fa[:h], fa[h:], fb[:h], fb[h:]
-    fc = torch.empty((2 * h, n1, n3), dtype=F64, device=da.device)
-    E.gemm(are, bre, out=fc[:h])
-    E.gemm(aim, bim, alpha=-1.0, beta=1.0, out=fc[:h])
-    E.gemm(are, bim, out=fc[h:])
-    E.gemm(aim, bre, beta=1.0, out=fc[h:])
-    return _out(_synthesis(fc, p), dev)
+    # per frequency k: [Re A | Im A] (n1 x 2n2) times [[Re B, Im B], [-Im B, Re B]]
+    # (2n2 x 2n3) = [Re C | Im C]: the complex facewise product as ONE real K3
+    # GEMM (four real products, N = 2 n3 keeps the tiles full)
+    sa = torch.view_as_real(torch.fft.rfft(da, dim=2))       # (n1, n2, h, 2)
+    sb = torch.view_as_real(torch.fft.rfft(db, dim=2))       # (n2, n3, h, 2)
+    acat = torch.empty((h, n1, 2, n2), dtype=F64, device=da.device)
+    acat.copy_(sa.permute(2, 0, 3, 1))
+    bemb = torch.empty((h, 2, n2, 2, n3), dtype=F64, device=da.device)
+    sbp = sb.permute(2, 0, 3, 1)                             # (h, n2, 2, n3) view
+    bemb[:, 0].copy_(sbp)                                    # [Re B | Im B]
+    bemb[:, 1, :, 0].copy_(sbp[:, :, 1]).neg_()              # -Im B
+    bemb[:, 1, :, 1].copy_(sbp[:, :, 0])                     #  Re B
+    ccat = E.gemm(acat.view(h, n1, 2 * n2), bemb.view(h, 2 * n2, 2 * n3))   # (h, n1, 2 n3)
+    spec = torch.view_as_complex(ccat.view(h, n1, 2, n3).permute(1, 3, 0, 2).contiguous())
+    return _out(torch.fft.irfft(spec, n=p, dim=2).contiguous(), dev)
 
 
 def tube_identity(n, p):
