@@ -148,6 +148,34 @@ int wt_copy2d_f64(const double* src, int64_t lds, int64_t strideS, double* dst, 
                   int64_t strideD, int64_t rows, int64_t cols, int64_t batch, int trans,
                   void* stream);
 
+/*
+ * K5 / K6 / K7 -- the SVD epilogues, from K4's outputs (sigma, the long-side
+ * vectors `vec`: nvec rows of length max(n1, n2)) and the matrices A that K4
+ * decomposed (unchanged by K4).  Composed stream-ordered from K3 + the column
+ * scaling / copy kernels; no hidden allocation.
+ *
+ * wt_svd_truncate_f64 -- _truncated_blocks (decomposition.py:70-72): rank-r
+ *   reconstruction recon[b] (n1 x n2, pitch ldr) = U_r diag(s_r) V_r^T, via
+ *   T = A V_r (n1 <= n2) or T = A^T U_r (n1 > n2); T (batch x min(n1,n2) x r,
+ *   caller-allocated) keeps that projection for wt_svd_factors_f64.
+ * wt_svd_factors_f64 -- _factor_blocks (decomposition.py:75-82): U (batch, n1, r)
+ *   and V (batch, n2, r) row-major from T, vec and sigma (1/s of a zero
+ *   singular value gives a zero column).
+ * wt_pinv_from_svd_f64 -- _pinv_stack (decomposition.py:157-163): out[b]
+ *   (n2 x n1, pitch ldo) = V diag(s+) U^T with s+ = 1/s for s > tol * s_max,
+ *   else 0; needs the full K4 output (nvec = min(n1, n2)) and T of
+ *   batch x min(n1,n2)^2 doubles.
+ */
+int wt_svd_truncate_f64(const double* A, int64_t lda, int64_t strideA, int64_t n1, int64_t n2,
+                        int64_t batch, const double* vec, int64_t nvec, int64_t r, double* recon,
+                        int64_t ldr, int64_t strideR, double* T, void* stream);
+int wt_svd_factors_f64(const double* T, const double* vec, int64_t nvec, const double* sigma,
+                       int64_t n1, int64_t n2, int64_t batch, int64_t r, double* U, double* V,
+                       void* stream);
+int wt_pinv_from_svd_f64(const double* A, int64_t lda, int64_t strideA, int64_t n1, int64_t n2,
+                         int64_t batch, const double* sigma, const double* vec, double tol,
+                         double* out, int64_t ldo, int64_t strideO, double* T, void* stream);
+
 /* Comparator-DFT helper: out[t][k] = x[t][k] - x[t][0] over ntubes tubes of p
  * samples (tube-fastest).  The t-product baselines FFT these deltas and add
  * p * x[t][0] to DC, so constant tubes transform to exact zeros off DC, as

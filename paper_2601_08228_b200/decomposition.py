@@ -19,7 +19,6 @@ from dataclasses import dataclass
 import numpy as np
 import torch
 
-from . import _native as N
 from . import engine as E
 from .errors import LevelError, RankError
 from .lifting import _is_dev, fine_detail_energy_ratio, forward_w  # noqa: F401  (re-export)
@@ -84,15 +83,9 @@ def w_svd_device(x: torch.Tensor, r: int, levels: int, tol: float = 0.0):
     pyr = E.lift_forward(x, levels)                                  # (p, n1, n2)
     sigma, vec, info = E.svd(pyr, r, tol=tol)
     E.raise_if_failed(info)
-    rec, t = E.truncated_recon(pyr, sigma, vec, r, keep_t=True)       # t = A V_r | A^T U_r
+    rec, t = E.truncated_recon(pyr, sigma, vec, r, keep_t=True)       # K5; t = A V_r | A^T U_r
     recon = E.lift_inverse(rec, n1, n2, p, levels)
-    vr = vec[:, :r, :]
-    if n1 <= n2:   # vec rows are right vectors
-        ub = E.scale_cols(t, sigma, N.SCALE_DIV, ncols=r)            # (p, n1, r) = U_r
-        vb = E.copy2d(vr, trans=True)                                 # (p, n2, r)
-    else:          # vec rows are left vectors
-        ub = E.copy2d(vr, trans=True)                                 # (p, n1, r)
-        vb = E.scale_cols(t, sigma, N.SCALE_DIV, ncols=r)            # (p, n2, r)
+    ub, vb = E.svd_factors(t, vec, sigma, n1, n2, r)                  # K6: (p, n1, r), (p, n2, r)
     sb = torch.diag_embed(sigma[:, :r]).contiguous()                  # (p, r, r) diagonal blocks
     U = E.lift_inverse(ub, n1, r, p, levels)
     S = E.lift_inverse(sb, r, r, p, levels)

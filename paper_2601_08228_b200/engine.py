@@ -238,42 +238,60 @@ def raise_if_failed(info: torch.Tensor):
 
 def truncated_recon(a: torch.Tensor, sigma: torch.Tensor, vec: torch.Tensor, r: int,
                     out: torch.Tensor | None = None, keep_t: bool = False):
-    """K5: rank-r reconstruction of every slice from the long-side vectors.
+    """K5 (wt_svd_truncate_f64): rank-r reconstruction of every slice from the long-side vectors.
 
     Right side (n1 <= n2): T = A V_r (n1 x r) and recon = T V_r^T.
     Left side  (n1 >  n2): T = A^T U_r (n2 x r) and recon = U_r T^T.
     Equal to U_r diag(s_r) V_r^T of decomposition.py:70-72.
     """
-    n1, n2 = a.shape[1], a.shape[2]
-    vr = vec[:, :r, :]
-    if n1 <= n2:
-        t = gemm(a, vr, trans_b=True)                 # (batch, n1, r)
-        rec = gemm(t, vr, out=out)                    # (batch, n1, n2)
-    else:
-        t = gemm(a, vr, trans_a=True, trans_b=True)   # (batch, n2, r)
-        rec = gemm(vr, t, trans_a=True, trans_b=True, out=out)
-    return (rec, t) if keep_t else rec
+    lib = N.require_gpu()
+    batch, n1, n2 = a.shape
+    assert a.stride(2) == 1 and vec.is_contiguous()
+    t = torch.empty((batch, min(n1, n2), r), dtype=F64, device=a.device)
+    if out is None:
+        out = torch.empty((batch, n1, n2), dtype=F64, device=a.device)
+    assert out.stride(2) == 1
+    N.check(lib.wt_svd_truncate_f64(_ptr(a), a.stride(1), a.stride(0), n1, n2, batch, _ptr(vec),
+                                    vec.shape[1], r, _ptr(out), out.stride(1), out.stride(0), _ptr(t),
+                                    _stream()), "wt_svd_truncate_f64")
+    return (out, t) if keep_t else out
+
+
+def svd_factors(t: torch.Tensor, vec: torch.Tensor, sigma: torch.Tensor, n1: int, n2: int, r: int):
+    """K6 (wt_svd_factors_f64): U (batch, n1, r), V (batch, n2, r) from K5's T (decomposition.py:75-82)."""
+    lib = N.require_gpu()
+    batch = t.shape[0]
+    assert t.is_contiguous() and vec.is_contiguous() and sigma.is_contiguous()
+    u = torch.empty((batch, n1, r), dtype=F64, device=t.device)
+    v = torch.empty((batch, n2, r), dtype=F64, device=t.device)
+    N.check(lib.wt_svd_factors_f64(_ptr(t), _ptr(vec), vec.shape[1], _ptr(sigma), n1, n2, batch, r,
+                                   _ptr(u), _ptr(v), _stream()), "wt_svd_factors_f64")
+    return u, v
 
 
 def pinv_blocks(a: torch.Tensor, sigma: torch.Tensor, vec: torch.Tensor, tol: float,
                 out: torch.Tensor | None = None) -> torch.Tensor:
-    """K7: per-slice Moore-Penrose inverse (n2 x n1) with cutoff tol*sigma_max.
+    """K7 (wt_pinv_from_svd_f64): per-slice Moore-Penrose inverse (n2 x n1), cutoff tol*sigma_max.
 
     decomposition.py:157-163: A+ = V diag(s+) U^T, s+ = 1/s for s > tol*s_max.
     Right side: A+ = V (A V)^T weighted by s+^2; left side: A+ = (A^T U) s+^2 U^T.
     """
-    n1, n2 = a.shape[1], a.shape[2]
-    if n1 <= n2:
-        t = gemm(a, vec, trans_b=True)                # (batch, n1, q) = A V
-        scale_cols(t, sigma, N.SCALE_PINV2, tol)
-        return gemm(vec, t, trans_a=True, trans_b=True, out=out)  # (batch, n2, n1)
-    t = gemm(a, vec, trans_a=True, trans_b=True)      # (batch, n2, q) = A^T U
-    scale_cols(t, sigma, N.SCALE_PINV2, tol)
-    return gemm(t, vec, out=out)                      # (batch, n2, n1)
+    lib = N.require_gpu()
+    batch, n1, n2 = a.shape
+    q = min(n1, n2)
+    assert a.stride(2) == 1 and vec.is_contiguous() and vec.shape[1] == q and sigma.is_contiguous()
+    t = torch.empty((batch, q, q), dtype=F64, device=a.device)
+    if out is None:
+        out = torch.empty((batch, n2, n1), dtype=F64, device=a.device)
+    assert out.stride(2) == 1
+    N.check(lib.wt_pinv_from_svd_f64(_ptr(a), a.stride(1), a.stride(0), n1, n2, batch, _ptr(sigma),
+                                     _ptr(vec), float(tol), _ptr(out), out.stride(1), out.stride(0),
+                                     _ptr(t), _stream()), "wt_pinv_from_svd_f64")
+    return out
 
 
 def tube_delta(x: torch.Tensor) -> torch.Tensor:
-    """(n1, n2, p) -> x[..., k] - x[..., 0] per tube (K: wt_tube_delta_f64)."""
+    """(n1, n2, p) -> x[..., k] - x[..., 0] per tube (wt_tube_delta_f64)."""
     lib = N.require_gpu()
     assert x.is_contiguous()
     out = torch.empty_like(x)
