@@ -45,6 +45,7 @@ from .lifting import (
     inverse_w,
     max_levels,
 )
+from .tensor_io import load_tensor, save_preview, save_tensor
 from .tensor import as_tensor3, frobenius_norm, frontal_slice, matrix_svd, set_frontal_slice, trace, transpose
 
 __version__ = "0.1.0"
@@ -61,4 +62,5 @@ __all__ = [
     "forward_w", "inverse_w", "max_levels",
     "as_tensor3", "frobenius_norm", "frontal_slice", "matrix_svd", "set_frontal_slice", "trace",
     "transpose",
+    "load_tensor", "save_preview", "save_tensor",
 ]
