@@ -322,6 +322,37 @@ int validate(int64_t n1, int64_t n2, int64_t p, int levels, int layout, int64_t 
   return WT_OK;
 }
 
+// dst (b x a) = transpose of src (a x b), both densely row-major, through
+// wt_copy2d_f64 in batches that respect its grid limits.
+int transpose_dense(const double* src, int64_t a, int64_t b, double* dst, cudaStream_t st) {
+  constexpr int64_t kRows = 1 << 20;  // dst rows per batch item (grid.y = kRows / 32)
+  int64_t done = 0;
+  while (done < b) {
+    const int64_t rows = std::min<int64_t>(kRows, b - done);
+    const int64_t batch = std::min<int64_t>((b - done) / rows, 65535);
+    int e = wt_copy2d_f64(src + done, b, rows, dst + done * a, a, rows * a, rows, a, batch, 1, st);
+    if (e) return e;
+    done += rows * batch;
+  }
+  return WT_OK;
+}
+
+// Tube-major (reference-layout) pyramids through the slice-major fast kernels:
+// each packed block is one dense transpose away from the other layout, so the
+// TUBE layout costs one extra HBM pass per block instead of the one-tile-per-CTA
+// per-level kernel above (~1.3-3.3 TB/s, tools/lift_tq_probe.py round 1).
+template <typename F>
+int for_each_block(int64_t p, int L, int64_t slice_base, uint64_t mask, F f) {
+  for (int j = 1; j <= L + 1; ++j) {
+    const bool smooth = j > L;
+    const int64_t off = smooth ? smooth_off(p, L) : detail_off(p, j);
+    const int64_t cnt = p >> (smooth ? L : j);
+    if (!((mask >> (smooth ? 0 : j)) & 1) || off < slice_base) continue;
+    if (int e = f(off - slice_base, cnt)) return e;
+  }
+  return WT_OK;
+}
+
 }  // namespace
 
 int lift_fwd_fast(const double* x, int64_t ntubes, int64_t p, int L, double* out,
@@ -344,6 +375,17 @@ extern "C" int wt_lift_fwd_f64(const double* x, int64_t n1, int64_t n2, int64_t 
   if (layout == WT_LAYOUT_SLICE_MAJOR) {
     st = lift_fwd_fast(x, g.ntubes, p, levels, out, slice_base, level_mask, (cudaStream_t)stream);
     if (st != WT_ERR_UNSUPPORTED) return st;
+  } else if (levels >= 1 && p % 2 == 0 && (uintptr_t)x % 16 == 0) {
+    cudaStream_t cs = (cudaStream_t)stream;
+    double* tmp = nullptr;
+    WT_CUDA(cudaMallocAsync(&tmp, (size_t)(p - slice_base) * g.ntubes * sizeof(double), cs));
+    st = lift_fwd_fast(x, g.ntubes, p, levels, tmp, slice_base, level_mask, cs);
+    if (st == WT_OK)
+      st = for_each_block(p, levels, slice_base, level_mask, [&](int64_t o, int64_t cnt) {
+        return transpose_dense(tmp + o * g.ntubes, cnt, g.ntubes, out + o * g.ntubes, cs);
+      });
+    WT_CUDA(cudaFreeAsync(tmp, cs));
+    if (st != WT_ERR_UNSUPPORTED) return st ? st : check_launch("wt_lift_fwd_f64 (tube layout)");
   }
   if (plan_tiles(g) != WT_OK) return levelwise_forward(x, out, g, (cudaStream_t)stream);
   const bool bulk = (g.CT % 2 == 0) && (p % 2 == 0) && ((uintptr_t)x % 16 == 0);
@@ -370,6 +412,16 @@ extern "C" int wt_lift_inv_f64(const double* pyr, int64_t n1, int64_t n2, int64_
   if (layout == WT_LAYOUT_SLICE_MAJOR) {
     st = lift_inv_fast(pyr, g.ntubes, p, levels, y, slice_base, level_mask, (cudaStream_t)stream);
     if (st != WT_ERR_UNSUPPORTED) return st;
+  } else if (levels >= 1 && p % 2 == 0 && g.ntubes % 2 == 0 && (uintptr_t)y % 16 == 0) {
+    cudaStream_t cs = (cudaStream_t)stream;
+    double* tmp = nullptr;
+    WT_CUDA(cudaMallocAsync(&tmp, (size_t)(p - slice_base) * g.ntubes * sizeof(double), cs));
+    st = for_each_block(p, levels, slice_base, level_mask, [&](int64_t o, int64_t cnt) {
+      return transpose_dense(pyr + o * g.ntubes, g.ntubes, cnt, tmp + o * g.ntubes, cs);
+    });
+    if (st == WT_OK) st = lift_inv_fast(tmp, g.ntubes, p, levels, y, slice_base, level_mask, cs);
+    WT_CUDA(cudaFreeAsync(tmp, cs));
+    if (st != WT_ERR_UNSUPPORTED) return st ? st : check_launch("wt_lift_inv_f64 (tube layout)");
   }
   if (plan_tiles(g) != WT_OK) return levelwise_inverse(pyr, y, g, (cudaStream_t)stream);
   const bool bulk = (g.CT % 2 == 0) && (p % 2 == 0) && ((uintptr_t)y % 16 == 0);

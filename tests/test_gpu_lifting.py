@@ -173,3 +173,26 @@ def test_odd_band_counts_in_transposes():
     assert np.array_equal(W.transpose(x), O.transpose(x))
     got = W.slicewise_matmul(x, b)
     assert np.max(np.abs(got - O.face_matmul(x, b))) < 1e-14
+
+
+@pytest.mark.parametrize("shape,L", [((6, 10, 16), 2), ((64, 64, 256), 8), ((33, 7, 96), 5), ((512, 9, 64), 1)])
+def test_tube_major_fast_route_masks_and_bases(shape, L):
+    """TUBE layout through the fast slice-major kernels + block transposes
+    (wt_lift_*_f64 with WT_LAYOUT_TUBE_MAJOR): full, compact [dL|sL] and round trip."""
+    n1, n2, p = shape
+    x = np.random.default_rng(p + L).standard_normal(shape)
+    s_ref, d_ref = O.lift_forward(x, L)
+    xd = torch.from_numpy(x).cuda()
+    buf = E.lift_forward(xd, L, layout=N.LAYOUT_TUBE)
+    want = np.concatenate([d.ravel() for d in d_ref] + [s_ref.ravel()])
+    assert np.array_equal(buf.cpu().numpy().ravel(), want)
+    y = E.lift_inverse(buf, n1, n2, p, L, layout=N.LAYOUT_TUBE)
+    assert np.array_equal(y.cpu().numpy(), O.lift_inverse(s_ref, d_ref))
+    m = p >> L
+    mask = E.level_mask(L, smooth=True, details=[L])
+    coarse = E.lift_forward(xd, L, layout=N.LAYOUT_TUBE, mask=mask, slice_base=p - 2 * m)
+    assert np.array_equal(coarse.cpu().numpy().ravel(),
+                          np.concatenate([d_ref[-1].ravel(), s_ref.ravel()]))
+    y2 = E.lift_inverse(coarse, n1, n2, p, L, layout=N.LAYOUT_TUBE, mask=mask, slice_base=p - 2 * m)
+    zeros = [np.zeros_like(d) for d in d_ref[:-1]] + [d_ref[-1]]
+    assert np.array_equal(y2.cpu().numpy(), O.lift_inverse(s_ref, zeros))
