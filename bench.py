@@ -540,12 +540,35 @@ def run_reference(args):
                              "sample": f"oracle/wten_oracle.py (numpy port of lifting.py:63-120) on a "
                                        f"{rows}x512x256 slab, L=1,2,4,8, {args.steps} steps"},
             "e2e": {"value": round(gbs, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(line), flush=True)
+    emit(line)
 
 
 # ----------------------------------------------------------------- main ----
 
+_JSON_FD = None
+
+
+def _quiet_stdout():
+    """Send everything written to fd 1 (NCCL's version banner, library prints)
+    to stderr; the JSON line goes to the saved stdout so it stays the only line."""
+    global _JSON_FD
+    if _JSON_FD is None:
+        sys.stdout.flush()
+        _JSON_FD = os.dup(1)
+        os.dup2(2, 1)
+
+
+def emit(line):
+    data = (json.dumps(line) + "\n").encode()
+    if _JSON_FD is None:
+        sys.stdout.write(data.decode())
+        sys.stdout.flush()
+    else:
+        os.write(_JSON_FD, data)
+
+
 def main():
+    _quiet_stdout()
     args = parse()
     if args.impl == "reference":
         run_reference(args)
@@ -617,7 +640,7 @@ def main():
             "round_trip_relerr": tr["round_trip_relerr"],
             "workloads": workloads,
         }
-        print(json.dumps(line), flush=True)
+        emit(line)
     if dist is not None:
         dist.barrier()
         dist.destroy_process_group()
