@@ -217,11 +217,7 @@ template <int BM, int BN, int WM, int WN, bool TA, bool TB, int VEC>
 int launch_cfg(const GemmArgs& g, cudaStream_t st) {
   using SL = SmemLayout<BM, BN, TA, TB>;
   auto kern = gemm_f64_kernel<BM, BN, WM, WN, TA, TB, VEC>;
-  static bool attr = false;
-  if (!attr) {
-    WT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SL::BYTES));
-    attr = true;
-  }
+  if (int e = ensure_smem(kern, SL::BYTES)) return e;
   dim3 grid((unsigned)((g.N + BN - 1) / BN), (unsigned)((g.M + BM - 1) / BM),
             (unsigned)std::min<int64_t>(g.batch, 65535));
   WT_REQUIRE(grid.y <= 65535, "gemm: M too large");

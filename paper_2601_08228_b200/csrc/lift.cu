@@ -390,12 +390,7 @@ extern "C" int wt_lift_fwd_f64(const double* x, int64_t n1, int64_t n2, int64_t 
   if (plan_tiles(g) != WT_OK) return levelwise_forward(x, out, g, (cudaStream_t)stream);
   const bool bulk = (g.CT % 2 == 0) && (p % 2 == 0) && ((uintptr_t)x % 16 == 0);
   const size_t smem = (size_t)g.TQ * g.LDT * sizeof(double);
-  static bool attr = false;
-  if (!attr) {
-    WT_CUDA(cudaFuncSetAttribute(lift_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 kMaxTileElems * 8 + 4096));
-    attr = true;
-  }
+  if (int e = ensure_smem(lift_fwd_kernel, kMaxTileElems * 8 + 4096)) return e;
   dim3 grid((unsigned)((g.ntubes + g.TQ - 1) / g.TQ), (unsigned)(p / g.CT));
   WT_REQUIRE(grid.y <= 65535, "lifting: too many band chunks");
   lift_fwd_kernel<<<grid, kThreads, smem, (cudaStream_t)stream>>>(x, out, g, bulk);
@@ -426,12 +421,7 @@ extern "C" int wt_lift_inv_f64(const double* pyr, int64_t n1, int64_t n2, int64_
   if (plan_tiles(g) != WT_OK) return levelwise_inverse(pyr, y, g, (cudaStream_t)stream);
   const bool bulk = (g.CT % 2 == 0) && (p % 2 == 0) && ((uintptr_t)y % 16 == 0);
   const size_t smem = (size_t)g.TQ * g.LDT * sizeof(double);
-  static bool attr = false;
-  if (!attr) {
-    WT_CUDA(cudaFuncSetAttribute(lift_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 kMaxTileElems * 8 + 4096));
-    attr = true;
-  }
+  if (int e = ensure_smem(lift_inv_kernel, kMaxTileElems * 8 + 4096)) return e;
   dim3 grid((unsigned)((g.ntubes + g.TQ - 1) / g.TQ), (unsigned)(p / g.CT));
   WT_REQUIRE(grid.y <= 65535, "lifting: too many band chunks");
   lift_inv_kernel<<<grid, kThreads, smem, (cudaStream_t)stream>>>(pyr, y, g, bulk);

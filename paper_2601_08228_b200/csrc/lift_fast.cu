@@ -391,7 +391,7 @@ bool plan(FGeom& g, int& TQ, bool fwd) {
 template <typename K, typename... Extra>
 int launch(K kern, size_t smem, uint32_t ntiles, cudaStream_t st, const double* a, double* b,
            const FGeom& g, const char* what, const Extra&... extra) {
-  WT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  if (int e = ensure_smem(kern, smem)) return e;
   int per_sm = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kT, smem) != cudaSuccess || per_sm < 1)
     per_sm = 1;
@@ -466,7 +466,7 @@ int lift_inv_fast(const double* pyr, int64_t ntubes, int64_t p, int L, double* y
   if (!plan(g, TQ, false)) return WT_ERR_UNSUPPORTED;
   const size_t smem = ((size_t)2 * g.CT * TQ + (size_t)2 * TQ * g.LDA0) * sizeof(double);
   if (smem > 200 * 1024) return WT_ERR_UNSUPPORTED;
-  static TmaMaps maps;  // host copy; passed by value as a __grid_constant__ parameter
+  TmaMaps maps{};  // host copy, passed by value as a __grid_constant__ parameter
   // TMA boxes: 16 tubes (128-byte rows) x <= 256 slices, 16-byte-multiple stride
   if (!tab && TQ >= 16 && (g.CT >> 1) <= 256 && !getenv("WT_LIFT_NO_TMA") &&
       make_maps(maps, pyr, g, TQ)) {

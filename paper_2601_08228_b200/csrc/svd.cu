@@ -623,12 +623,7 @@ extern "C" int wt_svd_jacobi_f64(const double* A, int64_t lda, int64_t strideA, 
   int64_t n_active = batch;
   WT_CUDA(cudaMemsetAsync(ws.pending, 0, sizeof(int) * 2, st));
 
-  static bool attr = false;
-  if (!attr) {
-    WT_CUDA(cudaFuncSetAttribute(svd_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)sizeof(PairSmem)));
-    attr = true;
-  }
+  if (int e = ensure_smem(svd_pair_kernel, sizeof(PairSmem))) return e;
   g_last_sweeps = 0;
   g_last_rotations = 0;
   int dbg_prev = 0;
@@ -639,7 +634,7 @@ extern "C" int wt_svd_jacobi_f64(const double* A, int64_t lda, int64_t strideA, 
     WT_CUDA(cudaMemsetAsync(d_prof, 0, 4 * sizeof(unsigned long long), st));
     ws.prof = d_prof;
   }
-  static int* h_pending = nullptr;
+  static thread_local int* h_pending = nullptr;  // per host thread: concurrent calls on other streams
   if (!h_pending) WT_CUDA(cudaMallocHost(&h_pending, sizeof(int)));
   const int nb = (int)(L.npad / HB);
   // One inner Jacobi sweep per pair visit: measured on the config-3/4 slices it
@@ -662,8 +657,7 @@ extern "C" int wt_svd_jacobi_f64(const double* A, int64_t lda, int64_t strideA, 
   int sort_mode = 2;
   if (const char* e = getenv("WT_SVD_SORT")) sort_mode = atoi(e);
   const size_t sort_smem = (size_t)npow2 * (sizeof(double) + sizeof(int));
-  WT_CUDA(cudaFuncSetAttribute(svd_norms_sort, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               8192 * (int)(sizeof(double) + sizeof(int))));
+  if (int e = ensure_smem(svd_norms_sort, 8192 * (sizeof(double) + sizeof(int)))) return e;
   for (int sweep = 0; sweep < max_sweeps; ++sweep) {
     if (sort_mode == 2 || (sort_mode == 1 && sweep == 0)) {
       // columns in descending norm order before the sweep (de Rijk-style)
@@ -722,12 +716,7 @@ extern "C" int wt_svd_jacobi_f64(const double* A, int64_t lda, int64_t strideA, 
   }
   {
     const size_t sm = (size_t)npow2 * (sizeof(double) + sizeof(int));
-    static bool attr2 = false;
-    if (!attr2) {
-      WT_CUDA(cudaFuncSetAttribute(svd_norms_sort, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   8192 * (int)(sizeof(double) + sizeof(int))));
-      attr2 = true;
-    }
+    if (int e = ensure_smem(svd_norms_sort, 8192 * (sizeof(double) + sizeof(int)))) return e;
     svd_norms_sort<<<(unsigned)batch, 512, sm, st>>>(ws, L.mpad, L.npad, L.n, npow2, sigma, info,
                                                      hit_max ? 1 : 0);
     if (int e = check_launch("svd_norms_sort")) return e;

@@ -33,6 +33,14 @@ int check_launch(const char* what);
     }                                                                              \
   } while (0)
 
+// Raise a kernel's dynamic shared-memory limit to `bytes` on the CURRENT
+// device (the attribute is per device; cached per (device, kernel), thread-safe).
+int smem_attr(const void* kernel, int bytes);
+template <typename K>
+inline int ensure_smem(K kernel, size_t bytes) {
+  return smem_attr(reinterpret_cast<const void*>(kernel), (int)bytes);
+}
+
 constexpr int kNumSMs = 148;  // B200; queried at runtime where it matters
 
 inline int num_sms() {

@@ -2,6 +2,10 @@
 #include <stdarg.h>
 #include <stdio.h>
 
+#include <map>
+#include <mutex>
+#include <utility>
+
 #include "wt_common.cuh"
 
 namespace wt {
@@ -21,6 +25,24 @@ int check_launch(const char* what) {
     set_error("%s: kernel launch failed: %s", what, cudaGetErrorString(e));
     return WT_ERR_CUDA;
   }
+  return WT_OK;
+}
+
+int smem_attr(const void* kernel, int bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<int, const void*>, int> done;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) dev = -1;
+  std::lock_guard<std::mutex> lock(mu);
+  int& have = done[{dev, kernel}];
+  if (have >= bytes) return WT_OK;
+  cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e != cudaSuccess) {
+    set_error("cudaFuncSetAttribute(MaxDynamicSharedMemorySize = %d) failed: %s", bytes,
+              cudaGetErrorString(e));
+    return WT_ERR_CUDA;
+  }
+  have = bytes;
   return WT_OK;
 }
 

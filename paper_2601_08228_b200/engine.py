@@ -9,6 +9,8 @@ block order ``[d1 | ... | dL | sL]`` (include/wten_b200.h).
 
 from __future__ import annotations
 
+import threading
+
 import numpy as np
 import torch
 
@@ -52,6 +54,7 @@ def level_mask(levels: int, smooth: bool = True, details=None) -> int:
 _STAGE_ELEMS = 4 << 20   # 32 MB pinned staging chunks
 _STAGE_SLOTS = 3
 _stage_ring: list = []
+_stage_lock = threading.Lock()  # the ring is shared: one uploader at a time
 
 
 def _upload(host: torch.Tensor, device) -> torch.Tensor:
@@ -59,6 +62,11 @@ def _upload(host: torch.Tensor, device) -> torch.Tensor:
     (multi-threaded) host copy of chunk i+1 overlaps the DMA of chunk i.  A
     pageable tensor.to("cuda") runs at ~9 GB/s on the B200 boxes; this at the
     PCIe rate (tools/h2d_probe.py)."""
+    with _stage_lock:
+        return _upload_locked(host, device)
+
+
+def _upload_locked(host: torch.Tensor, device) -> torch.Tensor:
     global _stage_ring
     if not _stage_ring:
         _stage_ring = [(torch.empty(_STAGE_ELEMS, dtype=F64, pin_memory=True), torch.cuda.Event())

@@ -2,7 +2,8 @@
 ``wten.lifting`` (/root/reference/pkg/src/wten/lifting.py).
 
 Same names, signatures, error types and messages.  Arithmetic runs on the GPU
-(K1/K2 in csrc/lift.cu) and is bit-identical to the reference.
+(K1/K2 in csrc/lift_fast.cu, general layouts in csrc/lift.cu) and is
+bit-identical to the reference.
 
 Two calling modes:
   * host arrays (numpy, lists, ...): inputs are copied to the GPU and results

@@ -137,3 +137,32 @@ def test_determinism():
     r1 = W.sp_w_svd(x, 8, 2)
     r2 = W.sp_w_svd(x, 8, 2)
     assert torch.equal(r1, r2)
+
+
+def test_concurrent_host_threads_on_own_streams():
+    """The API is pure (SPEC concurrency sections): host threads driving their own
+    CUDA streams get the serial results bit for bit (per-thread host state in K4)."""
+    import threading
+
+    xs = [np.random.default_rng(50 + i).standard_normal((48, 40, 16)) for i in range(4)]
+    serial = [W.sp_w_svd(x, 5, 2) for x in xs] + [W.pinv_w(x, 2) for x in xs]
+    out = [None] * (2 * len(xs))
+    errs = []
+
+    def work(i):
+        try:
+            with torch.cuda.stream(torch.cuda.Stream()):
+                out[i] = W.sp_w_svd(xs[i], 5, 2)
+                out[len(xs) + i] = W.pinv_w(xs[i], 2)
+                torch.cuda.current_stream().synchronize()
+        except Exception as e:  # noqa: BLE001
+            errs.append(e)
+
+    ts = [threading.Thread(target=work, args=(i,)) for i in range(len(xs))]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errs, errs
+    for a, b in zip(out, serial):
+        assert np.array_equal(a, b)
