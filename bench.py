@@ -333,6 +333,30 @@ def svd_flops(n1, n2):
     return 14 * m * n * n + 8 * n ** 3
 
 
+def api_e2e(fn, reps):
+    """Wall time (ms) of a synchronous public-API call on host (numpy) inputs: the
+    H2D of the inputs and the D2H of every returned array are inside."""
+    import torch
+
+    fn()
+    torch.cuda.synchronize()
+    t = time.perf_counter()
+    for _ in range(reps):
+        fn()
+    torch.cuda.synchronize()
+    return (time.perf_counter() - t) / reps * 1e3
+
+
+def oracle_sample(fn, scale, sample):
+    """Bounded CPU run of the oracle port (numpy + OpenBLAS LAPACK on all host
+    threads) scaled to the full workload."""
+    t = time.perf_counter()
+    fn()
+    dt = time.perf_counter() - t
+    return {"ms_per_call": round(dt * scale * 1e3, 1), "cores": host_threads(), "kind": "port",
+            "sample": f"{sample} ({dt:.2f} s, x{scale} to the full call)"}
+
+
 def wsvd_workload(args, steps=3, warmup=1):
     import torch
 
@@ -340,8 +364,12 @@ def wsvd_workload(args, steps=3, warmup=1):
     from paper_2601_08228_b200 import synth
     from paper_2601_08228_b200.decomposition import w_svd_device
 
+    import paper_2601_08228_b200 as W
+    from oracle import wten_oracle as O
+
     n1, n2, p, r, L = 256, 256, 192, 20, 3
-    x = torch.from_numpy(synth.hyperspectral_cube(n1, n2, p, seed=0)).cuda()
+    x_host = synth.hyperspectral_cube(n1, n2, p, seed=0)
+    x = torch.from_numpy(x_host).cuda()
     flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device="cuda")
     sweeps = []
 
@@ -361,7 +389,12 @@ def wsvd_workload(args, steps=3, warmup=1):
             "roofline": {"bound": "tensor", "achieved": round(ach, 2), "peak": peak,
                          "unit": "TFLOP/s", "frac": round(ach / peak, 4), "peak_source": src,
                          "flops_model": "192 x (14 m n^2 + 8 n^3) Golub-Kahan thin-SVD count (SURVEY 8d)"},
-            "l2": "256 MB flush before each call"}
+            "l2": "256 MB flush before each call",
+            "e2e": {"ms_per_call": round(api_e2e(lambda: W.w_svd(x_host, r, L), 2), 2),
+                    "api": "w_svd(numpy cube, 20, 3) -> (SvdFactors of numpy arrays, numpy recon)",
+                    "h2d_bytes_per_call": 8 * N, "d2h_bytes_per_call": 8 * (N + p * (n1 + n2 + r) * r)},
+            "cpu_baseline": oracle_sample(lambda: O.w_svd(x_host[:, :, :24], r, L), 8,
+                                          "oracle w_svd on 24 of the 192 bands (L=3)")}
 
 
 def spwsvd_workload(args, steps=3, warmup=1):
@@ -371,8 +404,12 @@ def spwsvd_workload(args, steps=3, warmup=1):
     from paper_2601_08228_b200 import synth
     from paper_2601_08228_b200.decomposition import sp_w_svd_device
 
+    import paper_2601_08228_b200 as W
+    from oracle import wten_oracle as O
+
     n1, n2, p, r, L = 1024, 1024, 256, 30, 4
-    x = torch.from_numpy(synth.hyperspectral_cube(n1, n2, p, seed=0)).cuda()
+    x_host = synth.hyperspectral_cube(n1, n2, p, seed=0)
+    x = torch.from_numpy(x_host).cuda()
     out = torch.empty_like(x)
     sweeps = []
 
@@ -391,7 +428,13 @@ def spwsvd_workload(args, steps=3, warmup=1):
             "roofline": {"bound": "tensor", "achieved": round(ach, 2), "peak": peak, "unit": "TFLOP/s",
                          "frac": round(ach / peak, 4), "peak_source": src,
                          "flops_model": "32 x 22 n^3 thin-SVD count (SURVEY 8d)"},
-            "l2": "2 GiB input > L2"}
+            "l2": "2 GiB input > L2",
+            "e2e": {"ms_per_call": round(api_e2e(lambda: W.sp_w_svd(x_host, r, L), 1), 2),
+                    "api": "sp_w_svd(numpy cube, 30, 4) -> numpy recon",
+                    "h2d_bytes_per_call": 8 * N, "d2h_bytes_per_call": 8 * N},
+            "cpu_baseline": oracle_sample(lambda: O.sp_w_svd(x_host[:, :, :32], r, L), 8,
+                                          "oracle sp_w_svd on 32 of the 256 bands (L=4: 4 coarse "
+                                          "1024^2 SVDs of the 32)")}
 
 
 def deblur_workload(args, steps=2, warmup=1):
