@@ -218,6 +218,41 @@ def _symm_pair(numel, device, group):
     return _SYMM[key]
 
 
+def _fused_exchange(x_local, levels, n1, mask, base, decompose, out_rows, out_cols, group):
+    """rows -> owners' slices (peer stores in K1), ``decompose`` in place on the owner,
+    owners' result slices -> rows (peer loads in K2).
+
+    Packed slices ``base .. p-1`` (as selected by ``mask``) are dealt to the ranks
+    in contiguous runs; ``decompose(full, out)`` maps the owner's (k, n1, n2)
+    slices to (k, out_rows, out_cols) result slices; this rank gets back its
+    ``splits(out_rows, G)`` share of the result rows as an (rows, out_cols, p) tensor.
+    """
+    G = dist.get_world_size(group)
+    me = dist.get_rank(group)
+    R, n2, p = x_local.shape
+    rows = splits(n1, G)
+    assert R == rows[me], f"rank {me} holds {R} rows, expected {rows[me]}"
+    K = p - base
+    ks = splits(K, G)
+    orows = splits(out_rows, G)
+    dev = x_local.device
+    (recv, h_recv), (recb, h_rec) = _symm_pair(max(ks) * n1 * n2, dev, group)
+    tab_f = torch.tensor(peer_slice_table(h_recv.buffer_ptrs, ks, sum(rows[:me]), n1, n2),
+                         dtype=torch.int64, device=dev)
+    tab_i = torch.tensor(peer_slice_table(h_rec.buffer_ptrs, ks, sum(orows[:me]), out_rows, out_cols),
+                         dtype=torch.int64, device=dev)
+    E.lift_forward_peer(x_local.contiguous(), levels, tab_f, mask, base)
+    h_recv.barrier(channel=0)                   # every rank's peer stores have landed
+    k_me = ks[me]
+    if k_me:
+        decompose(recv[:k_me * n1 * n2].view(k_me, n1, n2),
+                  recb[:k_me * out_rows * out_cols].view(k_me, out_rows, out_cols))
+    h_rec.barrier(channel=0)                    # every owner's result is ready
+    y = E.lift_inverse_peer(tab_i, orows[me], out_cols, p, levels, mask, base)
+    h_rec.barrier(channel=1)                    # all peer loads done before buffers are reused
+    return y
+
+
 def sp_w_svd_fused(x_local, r, levels, n1, group=None):
     """sp-w-svd of a row-sharded cube with the exchange fused into K1 / K2.
 
@@ -228,36 +263,47 @@ def sp_w_svd_fused(x_local, r, levels, n1, group=None):
     buffer, and K2 loads its rows of every reconstructed slice from the owners
     (peer loads).  Same result as :func:`sp_w_svd_sharded`.
     """
-    G = dist.get_world_size(group)
-    me = dist.get_rank(group)
     R, n2, p = x_local.shape
-    rows = splits(n1, G)
-    assert R == rows[me], f"rank {me} holds {R} rows, expected {rows[me]}"
     _check_rank(r, n1, n2)
     _check_levels(p, levels)
     m = p >> levels
-    K, base = 2 * m, p - 2 * m
-    ks = splits(K, G)
-    row0 = sum(rows[:me])
-    mask = E.level_mask(levels, smooth=True, details=[levels])
-    dev = x_local.device
-    (recv, h_recv), (recb, h_rec) = _symm_pair(max(ks) * n1 * n2, dev, group)
-    tab_f = torch.tensor(peer_slice_table(h_recv.buffer_ptrs, ks, row0, n1, n2), dtype=torch.int64,
-                         device=dev)
-    tab_i = torch.tensor(peer_slice_table(h_rec.buffer_ptrs, ks, row0, n1, n2), dtype=torch.int64,
-                         device=dev)
-    E.lift_forward_peer(x_local.contiguous(), levels, tab_f, mask, base)
-    h_recv.barrier(channel=0)                   # every rank's peer stores have landed
-    k_me = ks[me]
-    if k_me:
-        full = recv[:k_me * n1 * n2].view(k_me, n1, n2)
+
+    def decompose(full, out):
         sigma, vec, info = E.svd(full, r)
         E.raise_if_failed(info)
-        E.truncated_recon(full, sigma, vec, r, out=recb[:k_me * n1 * n2].view(k_me, n1, n2))
-    h_rec.barrier(channel=0)                    # every owner's reconstruction is ready
-    y = E.lift_inverse_peer(tab_i, R, n2, p, levels, mask, base)
-    h_rec.barrier(channel=1)                    # all peer loads done before buffers are reused
-    return y
+        E.truncated_recon(full, sigma, vec, r, out=out)
+
+    mask = E.level_mask(levels, smooth=True, details=[levels])
+    return _fused_exchange(x_local, levels, n1, mask, p - 2 * m, decompose, n1, n2, group)
+
+
+def w_svd_recon_fused(x_local, r, levels, n1, group=None):
+    """Rank-r w-svd reconstruction of a row-sharded cube, all p wavelet slices
+    exchanged by the peer stores / loads of K1 / K2 (see :func:`sp_w_svd_fused`)."""
+    R, n2, p = x_local.shape
+    _check_rank(r, n1, n2)
+    _check_levels(p, levels)
+
+    def decompose(full, out):
+        sigma, vec, info = E.svd(full, r)
+        E.raise_if_failed(info)
+        E.truncated_recon(full, sigma, vec, r, out=out)
+
+    return _fused_exchange(x_local, levels, n1, N.MASK_ALL, 0, decompose, n1, n2, group)
+
+
+def pinv_w_fused(x_local, levels, n1, tol=1e-12, group=None):
+    """w-pinv of a row-sharded cube with the fused exchange; returns this rank's
+    ``splits(n2, G)`` rows of the (n2, n1, p) pseudo-inverse."""
+    R, n2, p = x_local.shape
+    _check_levels(p, levels)
+
+    def decompose(full, out):
+        sigma, vec, info = E.svd(full, min(n1, n2))
+        E.raise_if_failed(info)
+        E.pinv_blocks(full, sigma, vec, tol, out=out)
+
+    return _fused_exchange(x_local, levels, n1, N.MASK_ALL, 0, decompose, n2, n1, group)
 
 
 def bench_sp_w_svd(dist_mod, timed_region, steps=3, warmup=1, shape=(1024, 1024, 256), r=30,

@@ -51,3 +51,17 @@ def test_fused_exchange_equals_nccl_path(nccl1):
         fz = sharded.sp_w_svd_fused(xd, 6, 3, 64)
         assert torch.equal(fz, sharded.sp_w_svd_sharded(xd, 6, 3, 64))
     assert relerr(fz.cpu().numpy(), O.sp_w_svd(x, 6, 3)) < 1e-10
+
+
+def test_fused_w_svd_and_pinv_equal_nccl_path(nccl1):
+    """Full-pyramid exchanges (all p slices) fused into K1/K2: w-svd recon and w-pinv
+    (the pinv's result slices are n2 x n1, its rows split over n2)."""
+    x = np.random.default_rng(33).standard_normal((40, 56, 16))
+    xd = torch.from_numpy(x).cuda()
+    ws = sharded.w_svd_recon_fused(xd, 5, 2, 40)
+    assert torch.equal(ws, sharded.w_svd_recon_sharded(xd, 5, 2, 40))
+    assert relerr(ws.cpu().numpy(), O.w_svd(x, 5, 2)["recon"]) < 1e-10
+    pv = sharded.pinv_w_fused(xd, 2, 40)
+    assert pv.shape == (56, 40, 16)
+    assert torch.equal(pv, sharded.pinv_w_sharded(xd, 2, 40))
+    assert relerr(pv.cpu().numpy(), O.pinv_w(x, 2)) < 1e-9

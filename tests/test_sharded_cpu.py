@@ -149,6 +149,31 @@ def test_fused_peer_tables_assemble_full_slices(G, n1, n2, p, L):
         r0 += rows[me]
 
 
+@pytest.mark.parametrize("G,n1,n2,p,L", [(2, 12, 10, 16, 3), (3, 10, 7, 8, 2), (8, 9, 20, 16, 1)])
+def test_fused_pinv_tables_transposed_results(G, n1, n2, p, L):
+    """w-pinv fused exchange: owners hold (n2, n1) result slices; rank g reads back
+    its splits(n2, G) rows of every slice through the K2 table (all p slices)."""
+    from paper_2601_08228_b200 import sharded
+
+    ks = sharded.splits(p, G)
+    orows = sharded.splits(n2, G)
+    span = 1 << 40
+    ptrs = [(g + 1) * span for g in range(G)]
+    res = np.random.default_rng(7).standard_normal((p, n2, n1))     # the owners' pinv slices
+    bufs = [np.zeros(max(ks) * n1 * n2) for _ in range(G)]
+    for g, st in enumerate(sharded.offsets(ks)):
+        bufs[g][:ks[g] * n1 * n2] = res[st:st + ks[g]].ravel()
+    r0 = 0
+    for me in range(G):
+        tab = sharded.peer_slice_table(ptrs, ks, r0, n2, n1)
+        assert len(tab) == p
+        for k in range(p):
+            g, off = tab[k] // span - 1, (tab[k] % span) // 8
+            got = bufs[g][off:off + orows[me] * n1].reshape(orows[me], n1)
+            assert np.array_equal(got, res[k, r0:r0 + orows[me]])
+        r0 += orows[me]
+
+
 def test_splits():
     from paper_2601_08228_b200 import sharded
 
