@@ -116,8 +116,10 @@ int wt_gemm_f64(int transA, int transB, int64_t M, int64_t N, int64_t K, double 
  *       right vector v_i if n1 <= n2, else left vector u_i; unit norm
  *       (zero vector when sigma_i == 0).
  *   info[b] : 0 ok, 1 non-finite input/result, 2 no convergence in max_sweeps.
- * The short-side vectors follow from one GEMM with A (done by the caller).
- * `workspace` must hold wt_svd_workspace_bytes(n1, n2, batch) bytes.
+ * The short-side vectors follow from one GEMM with A (wt_svd_truncate_f64 /
+ * wt_svd_factors_f64 / wt_pinv_from_svd_f64).
+ * `workspace` must hold wt_svd_workspace_bytes(n1, n2, min(batch, 65535)) bytes
+ * (larger batches run in chunks of 65535 matrices through that workspace).
  * tol <= 0 selects the default; max_sweeps <= 0 selects 40.
  * The call synchronizes `stream` once per sweep to test convergence.
  */

@@ -589,7 +589,24 @@ extern "C" int wt_svd_jacobi_f64(const double* A, int64_t lda, int64_t strideA, 
   WT_REQUIRE(n1 >= 1 && n2 >= 1 && batch >= 0, "svd: bad shape %lld x %lld", (long long)n1,
              (long long)n2);
   if (batch == 0) return WT_OK;
-  WT_REQUIRE(batch <= 65535, "svd: batch %lld exceeds 65535", (long long)batch);
+  if (batch > 65535) {  // grid.y limit: chunks of matrices through a prefix of the workspace
+    const int64_t q = n1 < n2 ? n1 : n2, ln = n1 < n2 ? n2 : n1;
+    WT_REQUIRE(workspace_bytes >= wt_svd_workspace_bytes(n1, n2, 65535),
+               "svd: workspace too small for 65535-matrix chunks");
+    long long sweeps = 0, rotations = 0;
+    for (int64_t b0 = 0; b0 < batch; b0 += 65535) {
+      const int64_t nb = std::min<int64_t>(65535, batch - b0);
+      int e = wt_svd_jacobi_f64(A + b0 * strideA, lda, strideA, n1, n2, nb, sigma + b0 * q,
+                                vec ? vec + b0 * nvec * ln : vec, nvec, info + b0, tol, max_sweeps,
+                                workspace, workspace_bytes, stream);
+      if (e) return e;
+      sweeps = std::max<long long>(sweeps, g_last_sweeps);
+      rotations += g_last_rotations;
+    }
+    g_last_sweeps = (int)sweeps;
+    g_last_rotations = rotations;
+    return WT_OK;
+  }
   WT_REQUIRE(lda >= n2, "svd: lda < n2");
   const WsLayout L = ws_layout(n1, n2, batch);
   WT_REQUIRE(nvec >= 0 && nvec <= L.n, "svd: nvec %lld outside [0, %lld]", (long long)nvec,

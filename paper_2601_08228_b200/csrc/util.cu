@@ -117,12 +117,14 @@ extern "C" int wt_scale_cols_f64(double* M, int64_t rows, int64_t ncols, int64_t
   WT_REQUIRE(rows >= 0 && ncols >= 0 && batch >= 0 && ncols <= q && ld >= ncols,
              "scale_cols: bad arguments");
   WT_REQUIRE(mode >= WT_SCALE_MUL && mode <= WT_SCALE_PINV2, "scale_cols: bad mode %d", mode);
-  WT_REQUIRE(batch <= 65535, "scale_cols: batch too large");
   if (rows == 0 || ncols == 0 || batch == 0) return WT_OK;
   const int64_t total = rows * ncols;
-  dim3 grid((unsigned)std::min<int64_t>((total + 255) / 256, 2048), (unsigned)batch);
-  scale_cols_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(M, rows, ncols, ld, strideM, s, q,
-                                                            mode, tol);
+  for (int64_t b0 = 0; b0 < batch; b0 += 65535) {  // grid.y limit
+    const int64_t nb = std::min<int64_t>(65535, batch - b0);
+    dim3 grid((unsigned)std::min<int64_t>((total + 255) / 256, 2048), (unsigned)nb);
+    scale_cols_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(M + b0 * strideM, rows, ncols, ld,
+                                                              strideM, s + b0 * q, q, mode, tol);
+  }
   return check_launch("wt_scale_cols_f64");
 }
 
@@ -130,17 +132,26 @@ extern "C" int wt_copy2d_f64(const double* src, int64_t lds, int64_t strideS, do
                              int64_t ldd, int64_t strideD, int64_t rows, int64_t cols,
                              int64_t batch, int trans, void* stream) {
   WT_REQUIRE(rows >= 0 && cols >= 0 && batch >= 0, "copy2d: negative size");
-  WT_REQUIRE(batch <= 65535, "copy2d: batch too large");
   if (rows == 0 || cols == 0 || batch == 0) return WT_OK;
-  dim3 grid((unsigned)((cols + 31) / 32), (unsigned)((rows + 31) / 32), (unsigned)batch);
-  WT_REQUIRE(grid.y <= 65535, "copy2d: too many rows");
+  WT_REQUIRE((cols + 31) / 32 < (1LL << 31), "copy2d: too many columns");
+  constexpr int64_t kRowChunk = 65535LL * 32;  // grid.y limit
   dim3 block(32, 8);
-  if (trans)
-    copy2d_kernel<true><<<grid, block, 0, (cudaStream_t)stream>>>(src, lds, strideS, dst, ldd,
-                                                                  strideD, rows, cols);
-  else
-    copy2d_kernel<false><<<grid, block, 0, (cudaStream_t)stream>>>(src, lds, strideS, dst, ldd,
-                                                                   strideD, rows, cols);
+  for (int64_t b0 = 0; b0 < batch; b0 += 65535) {  // grid.z limit
+    const int64_t nb = std::min<int64_t>(65535, batch - b0);
+    for (int64_t r0 = 0; r0 < rows; r0 += kRowChunk) {
+      const int64_t nr = std::min<int64_t>(kRowChunk, rows - r0);
+      // dst rows r0.. read src rows r0.. (copy) or src columns r0.. (transpose)
+      const double* S = src + b0 * strideS + (trans ? r0 : r0 * lds);
+      double* D = dst + b0 * strideD + r0 * ldd;
+      dim3 grid((unsigned)((cols + 31) / 32), (unsigned)((nr + 31) / 32), (unsigned)nb);
+      if (trans)
+        copy2d_kernel<true><<<grid, block, 0, (cudaStream_t)stream>>>(S, lds, strideS, D, ldd,
+                                                                      strideD, nr, cols);
+      else
+        copy2d_kernel<false><<<grid, block, 0, (cudaStream_t)stream>>>(S, lds, strideS, D, ldd,
+                                                                       strideD, nr, cols);
+    }
+  }
   return check_launch("wt_copy2d_f64");
 }
 

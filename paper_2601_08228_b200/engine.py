@@ -231,13 +231,8 @@ def svd(a: torch.Tensor, nvec: int, tol: float = 0.0, max_sweeps: int = 0):
     info = torch.empty((batch,), dtype=torch.int32, device=a.device)
     if batch == 0:
         return sigma, vec, info
-    if batch > 65535:  # grid.y limit of K4: run in chunks of slices
-        for s0 in range(0, batch, 65535):
-            s1 = min(batch, s0 + 65535)
-            sg, vc, nf = svd(a[s0:s1], nvec, tol, max_sweeps)
-            sigma[s0:s1], vec[s0:s1], info[s0:s1] = sg, vc, nf
-        return sigma, vec, info
-    wsb = int(lib.wt_svd_workspace_bytes(n1, n2, batch))
+    # (K4 runs batches above 65535 matrices in chunks through a workspace prefix)
+    wsb = int(lib.wt_svd_workspace_bytes(n1, n2, min(batch, 65535)))
     ws = torch.empty((wsb,), dtype=torch.uint8, device=a.device)
     N.check(lib.wt_svd_jacobi_f64(_ptr(a), a.stride(1), a.stride(0), n1, n2, batch, _ptr(sigma),
                                   _ptr(vec), nvec, _ptr(info), float(tol), int(max_sweeps),

@@ -166,3 +166,17 @@ def test_concurrent_host_threads_on_own_streams():
     assert not errs, errs
     for a, b in zip(out, serial):
         assert np.array_equal(a, b)
+
+
+def test_batches_above_grid_limit():
+    """K4 and the epilogue kernels chunk batches above 65535 matrices internally."""
+    rng = np.random.default_rng(61)
+    a = rng.standard_normal((70001, 3, 2))
+    at = torch.from_numpy(a).cuda()
+    sigma, vec, info = E.svd(at, 2)
+    assert int(info.abs().max()) == 0
+    np.testing.assert_allclose(sigma.cpu().numpy(), np.linalg.svd(a, compute_uv=False), rtol=0, atol=1e-13)
+    pinv = E.pinv_blocks(at, sigma, vec, 1e-12).cpu().numpy()
+    np.testing.assert_allclose(pinv, np.linalg.pinv(a), rtol=0, atol=1e-10)
+    rec = E.truncated_recon(at, sigma, vec, 2).cpu().numpy()
+    np.testing.assert_allclose(rec, a, rtol=0, atol=1e-12)
