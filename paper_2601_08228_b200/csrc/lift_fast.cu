@@ -182,6 +182,62 @@ __global__ void __launch_bounds__(kT) fwd_persistent(const double* __restrict__ 
   }
 }
 
+// Deep-L variant (L > 3): ONE tile buffer of TQ = 32 tubes x CT bands.  Stage 0
+// reads the whole input tile into registers, so the next tile's TMA load is
+// issued right after stage 0's barrier and overlaps the later stages.
+template <int TQ>
+__global__ void __launch_bounds__(kT) fwd_persistent1(const double* __restrict__ x,
+                                                      double* __restrict__ out, FGeom g) {
+  extern __shared__ __align__(128) double sm[];
+  __shared__ __align__(8) uint64_t bar;
+  double* const aux0 = sm + TQ * g.LDT;
+  double* const aux1 = aux0 + TQ * g.LDA0;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  auto issue = [&](uint32_t t) {
+    if (threadIdx.x < 32) {
+      int64_t q0, t0;
+      int tq;
+      tile_at<TQ>(g, t, q0, tq, t0);
+      if (threadIdx.x == 0) mbar_expect_tx(&bar, (uint32_t)(tq * g.CT * 8));
+      __syncwarp();
+      for (int r = threadIdx.x; r < tq; r += 32)
+        bulk_g2s(sm + r * g.LDT, x + (q0 + r) * g.p + t0, (uint32_t)(g.CT * 8), &bar);
+    }
+  };
+  uint32_t t = blockIdx.x;
+  if (t < g.ntiles) issue(t);
+  for (int i = 0; t < g.ntiles; ++i, t += gridDim.x) {
+    mbar_wait(&bar, i & 1);
+    int64_t q0, t0;
+    int tq;
+    tile_at<TQ>(g, t, q0, tq, t0);
+    const double* src = sm;
+    int ps = g.LDT, len = g.CT, l0 = 0, stage = 0;
+    while (l0 < g.L) {
+      const int W = min(3, g.L - l0);
+      double* dst = (stage & 1) ? aux1 : aux0;
+      const int pd = (stage & 1) ? g.LDA1 : g.LDA0;
+      if (W == 3) fwd_stage<TQ, 3>(src, ps, dst, pd, l0, len, g, out, q0, tq, t0);
+      else if (W == 2) fwd_stage<TQ, 2>(src, ps, dst, pd, l0, len, g, out, q0, tq, t0);
+      else fwd_stage<TQ, 1>(src, ps, dst, pd, l0, len, g, out, q0, tq, t0);
+      l0 += W;
+      len >>= W;
+      if (l0 < g.L) {
+        __syncthreads();
+        if (stage == 0 && t + gridDim.x < g.ntiles) issue(t + gridDim.x);  // tile buffer is free
+        src = dst;
+        ps = pd;
+        ++stage;
+      }
+    }
+    __syncthreads();
+  }
+}
+
 // ------------------------------------------------------------- inverse ----
 // Tile-local rows of the prefetched slice-major input follow the packed order
 // [d1 | ... | dL | sL] with the tile's CT bands in place of p.
@@ -351,7 +407,7 @@ __global__ void __launch_bounds__(kT) inv_persistent(const double* __restrict__ 
 // Tile height cap.  Forward: taller tiles write longer runs per packed slice
 // row (TQ * 8 bytes); measured at config 2 (tools/lift_tq_probe.py, round 1,
 // GB/s): L=1-3 best at 32 (+2%), L=4-6 at 64 (+7..14%), L=7 at 32 (+14%), L=8
-// needs CT = 256 so stays at 16.  Inverse: 16 (taller tiles cost 30%: the
+// needs CT = 256 so stays at 16 (L >= 6 take fwd_persistent1 by default).  Inverse: 16 (taller tiles cost 30%: the
 // tube-major final stores scatter over more tubes per warp).
 // WT_LIFT_TQ_MAX overrides both (diagnostics).
 int tq_max(bool fwd, int L) {
@@ -445,6 +501,28 @@ int lift_fwd_fast(const double* x, int64_t ntubes, int64_t p, int L, double* out
   int TQ = 0;
   if (!plan(g, TQ, true)) return WT_ERR_UNSUPPORTED;
   const size_t smem = ((size_t)2 * TQ * g.LDT + (size_t)TQ * (g.LDA0 + g.LDA1)) * sizeof(double);
+  static const int deep1 = [] {
+    const char* e = getenv("WT_LIFT_DEEP1");
+    return e ? atoi(e) : 1;
+  }();
+  // L = 6..8: single-buffered 32-tube tiles of 256 bands (fwd_persistent1);
+  // measured at config 2 (tools/lift_tq_probe.py, TB/s): L=6 5.58 -> 5.96,
+  // L=7 5.83 -> 5.89, L=8 5.09 -> 5.89; L=4, 5 tie with the TQ=64 tiles.
+  const int64_t unit = (int64_t)1 << g.L;
+  if (deep1 && unit >= (deep1 >= 2 ? 16 : 64) && unit <= 256 && g.p % 256 == 0) {
+    FGeom g1 = g;
+    constexpr int TQ1 = 32;
+    {
+      g1.CT = 256;
+      g1.LDT = g1.CT + 2;
+      g1.LDA0 = std::max(2, g1.CT / 8) + 2;
+      g1.LDA1 = std::max(2, g1.CT / 64) + 2;
+      g1.nqt = (uint32_t)((g.ntubes + TQ1 - 1) / TQ1);
+      g1.ntiles = (uint32_t)(g1.nqt * (g.p / g1.CT));
+      const size_t smem1 = ((size_t)TQ1 * g1.LDT + (size_t)TQ1 * (g1.LDA0 + g1.LDA1)) * sizeof(double);
+      return launch(fwd_persistent1<32>, smem1, g1.ntiles, st, x, out, g1, "wt_lift_fwd_f64");
+    }
+  }
   switch (TQ) {
     case 64: return launch(fwd_persistent<64>, smem, g.ntiles, st, x, out, g, "wt_lift_fwd_f64");
     case 32: return launch(fwd_persistent<32>, smem, g.ntiles, st, x, out, g, "wt_lift_fwd_f64");
