@@ -245,17 +245,21 @@ def transform_workload(args, dist, rank, ws):
     per_launch = 16 * N
     ach_f = per_launch / (f_ms * 1e-3) / 1e9
     ach_i = per_launch / (i_ms * 1e-3) / 1e9
-    # kernel names as in the ncu launch list (csrc/lift_fast.cu): K1 fwd_persistent<TQ>
-    # (TQ = 16 / 32 / 64 by level count), K2 inv_persistent<16, TMA>
-    dom = "fwd_persistent" if f_ms >= i_ms else "inv_persistent"
-    ach = ach_f if dom == "fwd_persistent" else ach_i
+    # kernel names as in the ncu launch list (csrc/lift_fast.cu): K1 = fwd_shallow<W>
+    # (L <= 3), fwd_persistent<TQ> (L = 4, 5), fwd_persistent1<32> (L >= 6);
+    # K2 = inv_persistent<16, TMA>
+    dom = "K1_forward" if f_ms >= i_ms else "K2_inverse"
+    ach = ach_f if dom == "K1_forward" else ach_i
     roofline = {"bound": "hbm", "kernel": dom, "achieved": round(ach, 1), "peak": peak,
                 "unit": "GB/s", "frac": round(ach / peak, 4), "peak_source": peak_src,
                 "traffic": traffic_of(dom), "algorithmic_bytes_per_launch": per_launch,
-                "per_kernel": {"fwd_persistent": {"ms": round(f_ms, 4), "GBps": round(ach_f, 1),
-                                                  "frac": round(ach_f / peak, 4)},
-                               "inv_persistent": {"ms": round(i_ms, 4), "GBps": round(ach_i, 1),
-                                                  "frac": round(ach_i / peak, 4)}}}
+                "kernels": {"K1_forward": "fwd_shallow<1|2> (L=1,2), fwd_persistent<64> (L=4), "
+                                          "fwd_persistent1<32> (L=8)",
+                            "K2_inverse": "inv_persistent<16, TMA>"},
+                "per_kernel": {"K1_forward": {"ms": round(f_ms, 4), "GBps": round(ach_f, 1),
+                                              "frac": round(ach_f / peak, 4)},
+                               "K2_inverse": {"ms": round(i_ms, 4), "GBps": round(ach_i, 1),
+                                              "frac": round(ach_i / peak, 4)}}}
 
     # e2e: the public API (forward_w / inverse_w on CUDA tensors) with the
     # step's input copied in from pinned host memory and its result read back

@@ -238,6 +238,96 @@ __global__ void __launch_bounds__(kT) fwd_persistent1(const double* __restrict__
   }
 }
 
+// Shallow variant (L = W <= 3, one stage): ONE 32 x 256 tile buffer; every
+// thread first pulls its 2^W-band chunks of two tubes into registers, one CTA
+// barrier frees the buffer, the next tile's TMA load is issued, and the lift +
+// stores run while it is in flight.
+template <int W>
+__global__ void __launch_bounds__(kT) fwd_shallow(const double* __restrict__ x,
+                                                  double* __restrict__ out, FGeom g) {
+  constexpr int TQ = 32, CT = 256, V = 1 << W, HQ = TQ / 2;
+  constexpr int ITEMS = HQ * (CT >> W), MAXI = ITEMS / kT;
+  extern __shared__ __align__(128) double sm[];
+  __shared__ __align__(8) uint64_t bar;
+  constexpr int LDT = CT + 2;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  auto issue = [&](uint32_t t) {
+    if (threadIdx.x < 32) {
+      int64_t q0, t0;
+      int tq;
+      tile_at<TQ>(g, t, q0, tq, t0);
+      if (threadIdx.x == 0) mbar_expect_tx(&bar, (uint32_t)(tq * CT * 8));
+      __syncwarp();
+      for (int r = threadIdx.x; r < tq; r += 32)
+        bulk_g2s(sm + r * LDT, x + (q0 + r) * g.p + t0, (uint32_t)(CT * 8), &bar);
+    }
+  };
+  uint32_t t = blockIdx.x;
+  if (t < g.ntiles) issue(t);
+  for (int it = 0; t < g.ntiles; ++it, t += gridDim.x) {
+    mbar_wait(&bar, it & 1);
+    int64_t q0, t0;
+    int tq;
+    tile_at<TQ>(g, t, q0, tq, t0);
+    double v[MAXI][2][V];
+#pragma unroll
+    for (int k = 0; k < MAXI; ++k) {
+      const int e = threadIdx.x + k * kT;
+      const int r = 2 * (e & (HQ - 1)), c = e / HQ;
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int i = 0; i < V; i += 2) {
+          const double2 t2 = *reinterpret_cast<const double2*>(sm + (r + h) * LDT + c * V + i);
+          v[k][h][i] = t2.x;
+          v[k][h][i + 1] = t2.y;
+        }
+    }
+    __syncthreads();                                   // the tile buffer is free
+    if (t + gridDim.x < g.ntiles) issue(t + gridDim.x);
+#pragma unroll
+    for (int k = 0; k < MAXI; ++k) {
+      const int e = threadIdx.x + k * kT;
+      const int r = 2 * (e & (HQ - 1)), c = e / HQ;
+      if (r >= tq) continue;
+      const bool two = r + 1 < tq;
+      auto put = [&](int64_t s, double a, double b) {
+        double* o = slice_row(g, out, s) + q0 + r;
+        if (two && ((reinterpret_cast<uintptr_t>(o) & 15) == 0)) {
+          *reinterpret_cast<double2*>(o) = make_double2(a, b);
+        } else {
+          o[0] = a;
+          if (two) o[1] = b;
+        }
+      };
+#pragma unroll
+      for (int w = 0; w < W; ++w) {
+        const int lev = w + 1;
+        const int n = V >> (w + 1);
+        const bool want = (g.mask >> lev) & 1;
+        const int64_t s0 = doff(g.p, lev) + (t0 >> lev) + (int64_t)c * n;
+#pragma unroll
+        for (int i = 0; i < (V >> 1); ++i) {
+          if (i < n) {
+            double d[2];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              d[h] = __dsub_rn(v[k][h][2 * i], v[k][h][2 * i + 1]);
+              v[k][h][i] = __dadd_rn(v[k][h][2 * i + 1], __dmul_rn(d[h], 0.5));
+            }
+            if (want) put(s0 + i, d[0], d[1]);
+          }
+        }
+      }
+      if (g.mask & 1) put(soff(g.p, W) + (t0 >> W) + c, v[k][0][0], v[k][1][0]);
+    }
+  }
+}
+
 // ------------------------------------------------------------- inverse ----
 // Tile-local rows of the prefetched slice-major input follow the packed order
 // [d1 | ... | dL | sL] with the tile's CT bands in place of p.
@@ -509,6 +599,21 @@ int lift_fwd_fast(const double* x, int64_t ntubes, int64_t p, int L, double* out
   // measured at config 2 (tools/lift_tq_probe.py, TB/s): L=6 5.58 -> 5.96,
   // L=7 5.83 -> 5.89, L=8 5.09 -> 5.89; L=4, 5 tie with the TQ=64 tiles.
   const int64_t unit = (int64_t)1 << g.L;
+  static const int shallow = [] {
+    const char* e = getenv("WT_LIFT_SHALLOW");
+    return e ? atoi(e) : 1;
+  }();
+  if (shallow && g.L <= 3 && g.p % 256 == 0) {
+    FGeom g1 = g;
+    g1.CT = 256;
+    g1.LDT = 258;
+    g1.nqt = (uint32_t)((g.ntubes + 31) / 32);
+    g1.ntiles = (uint32_t)(g1.nqt * (g.p / 256));
+    const size_t smem1 = (size_t)32 * 258 * sizeof(double);
+    if (g.L == 1) return launch(fwd_shallow<1>, smem1, g1.ntiles, st, x, out, g1, "wt_lift_fwd_f64");
+    if (g.L == 2) return launch(fwd_shallow<2>, smem1, g1.ntiles, st, x, out, g1, "wt_lift_fwd_f64");
+    return launch(fwd_shallow<3>, smem1, g1.ntiles, st, x, out, g1, "wt_lift_fwd_f64");
+  }
   if (deep1 && unit >= (deep1 >= 2 ? 16 : 64) && unit <= 256 && g.p % 256 == 0) {
     FGeom g1 = g;
     constexpr int TQ1 = 32;

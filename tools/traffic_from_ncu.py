@@ -20,8 +20,8 @@ def mb(v, u):
     scale = {"byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1.0, "Gbyte": 1e3}.get(u, 1.0)
     return float(v.replace(",", "")) * scale
 res = {}
-for name, key in (("fwd_persistent", "fwd_persistent"), ("inv_persistent", "inv_persistent")):
-    sel = [l for l in launches if key in l["Kernel Name"]]
+for name, keys in (("K1_forward", ("fwd_persistent", "fwd_shallow")), ("K2_inverse", ("inv_persistent",))):
+    sel = [l for l in launches if any(k in l["Kernel Name"] for k in keys)]
     if not sel:
         continue
     ur, uw = units[idx["dram__bytes_read.sum"]], units[idx["dram__bytes_write.sum"]]
@@ -33,4 +33,4 @@ res["source"] = ("ncu --set full --clock-control none on tools/lift_one.py 1 2 4
 res["units"] = {"dram__bytes_read.sum": units[idx["dram__bytes_read.sum"]]}
 res["per_launch"] = launches
 json.dump(res, open(out, "w"), indent=1)
-print({k: v for k, v in res.items() if k.endswith("persistent")})
+print({k: v for k, v in res.items() if k.startswith("K")})
