@@ -337,8 +337,9 @@ __device__ __forceinline__ int drow(int CT, int j) { return CT - (CT >> (j - 1))
 // s_{hi-W} using the prefetched details; the final stage (down to level 1)
 // stores the 2^W consecutive bands straight to y.
 template <int TQ, int W>
-__device__ __forceinline__ void inv_stage(const double* I, const double* ssrc, int pss, bool s_in,
-                                          double* dst, int pd, int hi, const FGeom g,
+__device__ __forceinline__ void inv_stage(const double* __restrict__ I,
+                                          const double* __restrict__ ssrc, int pss, bool s_in,
+                                          double* __restrict__ dst, int pd, int hi, const FGeom g,
                                           double* __restrict__ y, int64_t q0, int tq, int64_t t0) {
   constexpr int V = 1 << W;
   const int CT = g.CT;
