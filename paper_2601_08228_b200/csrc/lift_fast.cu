@@ -44,6 +44,7 @@ struct FGeom {
   // sharded pipeline fuses its rows -> slices exchange into K1 / K2: the stores
   // (loads) go straight to (from) the owning GPU's buffer over NVLink.
   const unsigned long long* tab;
+  int inv_path;  // K2: from this L up (0 = never), levels above 3 by per-thread ancestor chains
 };
 
 __device__ __forceinline__ double* slice_row(const FGeom& g, double* base, int64_t s) {
@@ -340,7 +341,8 @@ template <int TQ, int W>
 __device__ __forceinline__ void inv_stage(const double* __restrict__ I,
                                           const double* __restrict__ ssrc, int pss, bool s_in,
                                           double* __restrict__ dst, int pd, int hi, const FGeom g,
-                                          double* __restrict__ y, int64_t q0, int tq, int64_t t0) {
+                                          double* __restrict__ y, int64_t q0, int tq, int64_t t0,
+                                          bool path = false) {
   constexpr int V = 1 << W;
   const int CT = g.CT;
   const int nval = CT >> hi;
@@ -352,7 +354,21 @@ __device__ __forceinline__ void inv_stage(const double* __restrict__ I,
     const int r = e & (TQ - 1), c = e / TQ;
     if (r >= tq) continue;
     double v[V];
-    v[0] = s_in ? (have_s ? I[(srow + c) * TQ + r] : 0.0) : ssrc[r * pss + c];
+    if (path) {
+      // s_hi[c] straight from s_L along c's ancestor chain (levels L .. hi+1):
+      // the same two roundings per level as the level-by-level inverse, no
+      // stage barriers (lifting.py:69-74)
+      double sv = have_s ? I[(srow + (c >> (g.L - hi))) * TQ + r] : 0.0;
+      for (int j = g.L; j > hi; --j) {
+        const int k = c >> (j - hi);
+        const double d = ((g.mask >> j) & 1) ? I[(drow(CT, j) + k) * TQ + r] : 0.0;
+        const double x1 = __dsub_rn(sv, __dmul_rn(d, 0.5));
+        sv = ((c >> (j - hi - 1)) & 1) ? x1 : __dadd_rn(d, x1);
+      }
+      v[0] = sv;
+    } else {
+      v[0] = s_in ? (have_s ? I[(srow + c) * TQ + r] : 0.0) : ssrc[r * pss + c];
+    }
 #pragma unroll
     for (int w = 0; w < W; ++w) {
       const int lev = hi - w;
@@ -474,6 +490,10 @@ __global__ void __launch_bounds__(kT) inv_persistent(const double* __restrict__ 
     int hi = g.L, stage = 0;
     const double* ssrc = nullptr;
     int pss = 0;
+    if (g.inv_path && g.L >= g.inv_path) {  // one barrier-free pass: levels L..4 by ancestor chains
+      inv_stage<TQ, 3>(I, ssrc, pss, false, aux0, g.LDA0, 3, g, y, q0, tq, t0, true);
+      hi = 0;
+    }
     while (hi > 0) {
       const int W = (hi - 1) % 3 + 1;  // top stage absorbs the remainder: final stage is 3 wide
       double* dst = (stage & 1) ? aux1 : aux0;
@@ -646,6 +666,14 @@ int lift_inv_fast(const double* pyr, int64_t ntubes, int64_t p, int L, double* y
   if (L < 1 || p % 2 || ntubes % 2 || (uintptr_t)y % 16 || (uintptr_t)pyr % 16)
     return WT_ERR_UNSUPPORTED;
   FGeom g{ntubes, p, L, 0, 0, 0, 0, slice_base, mask, 0, 0, tab};
+  // measured at config 2 (tools/lift_tq_probe.py, 3 alternating runs): L = 7
+  // +2% over the staged inverse, L = 8 even, L = 4..6 -2..7% (the chains'
+  // redundant loads outweigh the saved barriers while the top levels are short)
+  static const int inv_path = [] {
+    const char* e = getenv("WT_LIFT_INV_PATH");
+    return e ? atoi(e) : 7;
+  }();
+  g.inv_path = inv_path;
   int TQ = 0;
   if (!plan(g, TQ, false)) return WT_ERR_UNSUPPORTED;
   const size_t smem = ((size_t)2 * g.CT * TQ + (size_t)2 * TQ * g.LDA0) * sizeof(double);
