@@ -179,7 +179,8 @@ __global__ void __launch_bounds__(kT) fwd_persistent(const double* __restrict__ 
         ++stage;
       }
     }
-    __syncthreads();  // tile buffer `buf` is refilled two iterations later
+    fence_proxy_async_smem();  // generic reads of `buf` before its TMA refill
+    __syncthreads();  // tile buffer `buf` is refilled by the next iteration's issue
   }
 }
 
@@ -228,6 +229,7 @@ __global__ void __launch_bounds__(kT) fwd_persistent1(const double* __restrict__
       l0 += W;
       len >>= W;
       if (l0 < g.L) {
+        if (stage == 0) fence_proxy_async_smem();  // tile reads before the TMA refill
         __syncthreads();
         if (stage == 0 && t + gridDim.x < g.ntiles) issue(t + gridDim.x);  // tile buffer is free
         src = dst;
@@ -288,6 +290,7 @@ __global__ void __launch_bounds__(kT) fwd_shallow(const double* __restrict__ x,
           v[k][h][i + 1] = t2.y;
         }
     }
+    fence_proxy_async_smem();                          // reads before the TMA refill
     __syncthreads();                                   // the tile buffer is free
     if (t + gridDim.x < g.ntiles) issue(t + gridDim.x);
 #pragma unroll
@@ -510,9 +513,108 @@ __global__ void __launch_bounds__(kT) inv_persistent(const double* __restrict__ 
         ++stage;
       }
     }
+    // No proxy fence before the TMA refill of this buffer (issued right after
+    // the barrier): every shared-memory load of the tile has been consumed by
+    // the lift and the global stores before the thread reaches the barrier, so
+    // no read is still in flight.  (A fence here costs 4%.  The single-buffered
+    // kernels that hold raw tile values across the barrier do fence: without
+    // it inv_shallow read refilled data.)
     __syncthreads();  // input buffer / stage buffers are reused by later tiles
   }
   if (!TMA) cp_async_wait<0>();
+}
+
+// Shallow inverse (L = W <= 3, one stage), TMA input: ONE 16 x 256 tile buffer;
+// every thread pulls its items' smooth + detail values into registers, one CTA
+// barrier frees the buffer, the next tile's boxes are issued, and the lift and
+// the tube stores run while they are in flight.
+template <int W>
+__global__ void __launch_bounds__(kT) inv_shallow(const double* __restrict__ pyr,
+                                                  double* __restrict__ y, FGeom g,
+                                                  const __grid_constant__ TmaMaps maps) {
+  constexpr int TQ = 16, CT = 256, V = 1 << W, NV = CT >> W, MAXI = TQ * NV / kT;
+  extern __shared__ __align__(128) double sm[];
+  __shared__ __align__(8) uint64_t bar;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  auto issue = [&](uint32_t t) {
+    if (threadIdx.x != 0) return;
+    int64_t q0, t0;
+    int tq;
+    tile_at<TQ>(g, t, q0, tq, t0);
+    uint32_t bytes = 0;
+    for (int j = 1; j <= W + 1; ++j)
+      if ((g.mask >> (j > W ? 0 : j)) & 1) bytes += (CT >> min(j, W)) * TQ * 8;
+    mbar_expect_tx(&bar, bytes);
+    for (int j = 1; j <= W + 1; ++j) {
+      const bool smooth = j > W;
+      if (!((g.mask >> (smooth ? 0 : j)) & 1)) continue;
+      const int row0 = smooth ? CT - (CT >> W) : drow(CT, j);
+      const int64_t s0 = smooth ? soff(g.p, W) + (t0 >> W) : doff(g.p, j) + (t0 >> j);
+      tma_load_2d(sm + row0 * TQ, &maps.m[smooth ? W : j], (int)q0, (int)(s0 - g.slice_base), &bar);
+    }
+  };
+  const bool have_s = g.mask & 1;
+  uint32_t t = blockIdx.x;
+  if (t < g.ntiles) issue(t);
+  for (int it = 0; t < g.ntiles; ++it, t += gridDim.x) {
+    mbar_wait(&bar, it & 1);
+    int64_t q0, t0;
+    int tq;
+    tile_at<TQ>(g, t, q0, tq, t0);
+    const double* vs = sm;
+    double v[MAXI][V], dd[MAXI][V];  // dd: level W (1 value), W-1 (2), ..., 1 (V/2)
+#pragma unroll
+    for (int k = 0; k < MAXI; ++k) {
+      const int e = threadIdx.x + k * kT;
+      const int r = e & (TQ - 1), c = e / TQ;
+      v[k][0] = have_s ? vs[(CT - NV + c) * TQ + r] : 0.0;
+      int o = 0;
+#pragma unroll
+      for (int w = 0; w < W; ++w) {
+        const int lev = W - w, n = 1 << w;
+        const bool have_d = (g.mask >> lev) & 1;
+#pragma unroll
+        for (int i = 0; i < n; ++i, ++o)
+          dd[k][o] = have_d ? vs[(drow(CT, lev) + c * n + i) * TQ + r] : 0.0;
+      }
+    }
+    // generic-proxy reads of the buffer are ordered before the TMA (async-proxy)
+    // refill only by a proxy fence: without it the refill raced the reads
+    fence_proxy_async_smem();
+    __syncthreads();                                   // the tile buffer is free
+    if (t + gridDim.x < g.ntiles) issue(t + gridDim.x);
+#pragma unroll
+    for (int k = 0; k < MAXI; ++k) {
+      const int e = threadIdx.x + k * kT;
+      const int r = e & (TQ - 1), c = e / TQ;
+      int o = 0;
+#pragma unroll
+      for (int w = 0; w < W; ++w) {
+        const int n = 1 << w;
+        // level W - w: n smooth values -> 2n (in place, high to low)
+#pragma unroll
+        for (int i = (V >> 1) - 1; i >= 0; --i) {
+          if (i < n) {
+            const double d = dd[k][o + i];
+            const double x1 = __dsub_rn(v[k][i], __dmul_rn(d, 0.5));
+            v[k][2 * i] = __dadd_rn(d, x1);
+            v[k][2 * i + 1] = x1;
+          }
+        }
+        o += n;
+      }
+      if (r < tq) {
+        double* out = y + (q0 + r) * g.p + t0 + (int64_t)c * V;
+#pragma unroll
+        for (int i = 0; i < V; i += 2)
+          *reinterpret_cast<double2*>(out + i) = make_double2(v[k][i], v[k][i + 1]);
+      }
+    }
+  }
 }
 
 // Tile height cap.  Forward: taller tiles write longer runs per packed slice
@@ -679,6 +781,24 @@ int lift_inv_fast(const double* pyr, int64_t ntubes, int64_t p, int L, double* y
   const size_t smem = ((size_t)2 * g.CT * TQ + (size_t)2 * TQ * g.LDA0) * sizeof(double);
   if (smem > 200 * 1024) return WT_ERR_UNSUPPORTED;
   TmaMaps maps{};  // host copy, passed by value as a __grid_constant__ parameter
+  // single-buffered shallow inverse: correct (with its proxy fence) but slower
+  // than the double-buffered kernel (L=1-3: -7..12%), kept for experiments
+  static const int inv_shallow_on = [] {
+    const char* e = getenv("WT_LIFT_INV_SHALLOW");
+    return e ? atoi(e) : 0;
+  }();
+  if (inv_shallow_on && !tab && L <= 3 && p % 256 == 0 && !getenv("WT_LIFT_NO_TMA")) {
+    FGeom g1 = g;
+    g1.CT = 256;
+    g1.nqt = (uint32_t)((ntubes + 15) / 16);
+    g1.ntiles = (uint32_t)(g1.nqt * (p / 256));
+    if (make_maps(maps, pyr, g1, 16)) {
+      const size_t smem1 = (size_t)16 * 256 * sizeof(double);
+      if (L == 1) return launch(inv_shallow<1>, smem1, g1.ntiles, st, pyr, y, g1, "wt_lift_inv_f64", maps);
+      if (L == 2) return launch(inv_shallow<2>, smem1, g1.ntiles, st, pyr, y, g1, "wt_lift_inv_f64", maps);
+      return launch(inv_shallow<3>, smem1, g1.ntiles, st, pyr, y, g1, "wt_lift_inv_f64", maps);
+    }
+  }
   // TMA boxes: 16 tubes (128-byte rows) x <= 256 slices, 16-byte-multiple stride
   if (!tab && TQ >= 16 && (g.CT >> 1) <= 256 && !getenv("WT_LIFT_NO_TMA") &&
       make_maps(maps, pyr, g, TQ)) {
