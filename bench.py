@@ -653,7 +653,7 @@ def main():
 
     if args.workloads == "default":
         wl = (["wsvd", "spwsvd", "deblur", "wproduct", "comparators"] if ws == 1
-              else ["spwsvd_fused", "spwsvd_sharded"])
+              else ["spwsvd_fused", "spwsvd_sharded", "wsvd_fused", "wsvd_sharded"])
     elif args.workloads == "none":
         wl = []
     else:
@@ -678,6 +678,12 @@ def main():
 
                 workloads[name] = sharded.bench_sp_w_svd(dist, timed_region, steps=3, warmup=1,
                                                          fused=name == "spwsvd_fused")
+            elif name in ("wsvd_sharded", "wsvd_fused"):  # config 3, all p slices exchanged
+                from paper_2601_08228_b200 import sharded
+
+                workloads[name] = sharded.bench_sp_w_svd(dist, timed_region, steps=3, warmup=1,
+                                                         shape=(256, 256, 192), r=20, levels=3,
+                                                         fused=name == "wsvd_fused", full=True)
         except Exception as e:  # noqa: BLE001
             workloads[name] = {"error": f"{type(e).__name__}: {e}"}
 

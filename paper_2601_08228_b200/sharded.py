@@ -307,8 +307,9 @@ def pinv_w_fused(x_local, levels, n1, tol=1e-12, group=None):
 
 
 def bench_sp_w_svd(dist_mod, timed_region, steps=3, warmup=1, shape=(1024, 1024, 256), r=30,
-                   levels=4, fused=False):
-    """Config 4 strong-scaled over the group (rows sharded; see bench.py)."""
+                   levels=4, fused=False, full=False):
+    """Config 4 sp-w-svd (or, with ``full``, config 3 w-svd reconstruction over all
+    p wavelet slices) strong-scaled over the group (rows sharded; see bench.py)."""
     from . import synth
 
     G = dist_mod.get_world_size()
@@ -318,25 +319,29 @@ def bench_sp_w_svd(dist_mod, timed_region, steps=3, warmup=1, shape=(1024, 1024,
     r0 = sum(rows[:me])
     # rank 0 generates the cube once and broadcasts it (NVLink); each rank keeps its rows
     if me == 0:
-        full = torch.from_numpy(synth.hyperspectral_cube(n1, n2, p, seed=0)).cuda()
+        cube = torch.from_numpy(synth.hyperspectral_cube(n1, n2, p, seed=0)).cuda()
     else:
-        full = torch.empty((n1, n2, p), dtype=torch.float64, device="cuda")
-    dist_mod.broadcast(full, src=0)
-    x = full[r0:r0 + rows[me]].contiguous()
-    del full
+        cube = torch.empty((n1, n2, p), dtype=torch.float64, device="cuda")
+    dist_mod.broadcast(cube, src=0)
+    x = cube[r0:r0 + rows[me]].contiguous()
+    del cube
     out = {}
 
-    fn = sp_w_svd_fused if fused else sp_w_svd_sharded
+    if full:
+        fn = w_svd_recon_fused if fused else w_svd_recon_sharded
+    else:
+        fn = sp_w_svd_fused if fused else sp_w_svd_sharded
 
     def step(record):
         out["y"] = fn(x, r, levels, n1)
 
     ms = timed_region(step, steps, warmup, dist_mod)
     total = n1 * n2 * p
-    k = 2 * (p >> levels)
+    k = p if full else 2 * (p >> levels)
     how = ("peer stores/loads fused into K1/K2 (symmetric memory)" if fused
            else "NCCL all-to-all")
-    return {"config": f"sp_w_svd {n1}x{n2}x{p} rank {r} L={levels}, rows sharded over {G} GPUs, "
-                      f"{k} coarse slices exchanged by {how}",
+    what = "w_svd recon" if full else "sp_w_svd"
+    return {"config": f"{what} {n1}x{n2}x{p} rank {r} L={levels}, rows sharded over {G} GPUs, "
+                      f"{k} wavelet slices exchanged by {how}",
             "metric": "tensor-elems/s", "value": total * steps / (ms * 1e-3), "ms_per_call": ms / steps,
             "scaling": "strong", "exchange_bytes_per_rank": 2 * 8 * k * rows[me] * n2}
