@@ -107,6 +107,104 @@ def to_host(t: torch.Tensor) -> np.ndarray:
     return h.numpy()
 
 
+# ------------------------------------------------- host-streamed transform ----
+
+_PIPE_STREAMS: dict = {}
+_CHUNK_BYTES = 32 << 20
+
+
+def _pipe_streams():
+    dev = torch.cuda.current_device()
+    if dev not in _PIPE_STREAMS:
+        _PIPE_STREAMS[dev] = tuple(torch.cuda.Stream() for _ in range(3))
+    return _PIPE_STREAMS[dev]
+
+
+def _row_chunks(n1: int, row_elems: int):
+    rows = max(1, min(n1, _CHUNK_BYTES // max(1, 8 * row_elems)))
+    return rows, [(r0, min(n1, r0 + rows)) for r0 in range(0, n1, rows)]
+
+
+def host_lift(src, n1: int, n2: int, p: int, levels: int, forward: bool) -> torch.Tensor:
+    """The numpy drop-in transform, streamed through the GPU in row chunks.
+
+    forward: ``src`` is the (n1, n2, p) host cube; returns the tube-major packed
+    pyramid (the reference's per-level arrays back to back) in pinned memory.
+    inverse: ``src`` is that pinned packed pyramid; returns the pinned cube.
+    Per chunk of rows: host -> pinned staging (forward only), H2D, K1 / K2, and
+    D2H straight into the pinned result run on three streams, so the staging
+    copy, both PCIe directions and the kernels overlap (the transform is
+    row-separable: a chunk's rows are contiguous in every tube-major block).
+    """
+    lib = N.require_gpu()  # noqa: F841  (fail loudly without the library / a GPU)
+    nt = n1 * n2
+    rows, chunks = _row_chunks(n1, n2 * p)
+    blocks = [(off, cnt) for _, off, cnt in block_slices(p, levels)]
+    out = torch.empty(nt * p, dtype=F64, pin_memory=True)
+    s_in, s_cmp, s_out = _pipe_streams()
+    main = torch.cuda.current_stream()
+    for st in (s_in, s_cmp, s_out):
+        st.wait_stream(main)
+    cap = rows * n2 * p
+    with _stage_lock:
+        if forward and not _stage_ring:
+            _upload_locked(torch.empty(0, dtype=F64), "cuda")  # allocate the pinned ring
+        dx = [torch.empty(cap, dtype=F64, device="cuda") for _ in range(2)]
+        dy = [torch.empty(cap, dtype=F64, device="cuda") for _ in range(2)]
+        free_in = [None, None]   # dx[b] consumed by the kernel
+        free_out = [None, None]  # dy[b] drained by the D2H
+        for i, (r0, r1) in enumerate(chunks):
+            b = i % 2
+            rn = (r1 - r0) * n2
+            n = rn * p
+            with torch.cuda.stream(s_in):
+                if free_in[b] is not None:
+                    s_in.wait_event(free_in[b])
+                if forward:
+                    stage, ev = _stage_ring[i % _STAGE_SLOTS]
+                    ev.synchronize()
+                    part = torch.from_numpy(src[r0:r1]).reshape(-1)
+                    for c0 in range(0, n, _STAGE_ELEMS):    # chunks above the ring slot size
+                        m = min(_STAGE_ELEMS, n - c0)
+                        if c0:
+                            ev.record(s_in)
+                            ev.synchronize()
+                        stage[:m].copy_(part[c0:c0 + m])
+                        dx[b][c0:c0 + m].copy_(stage[:m], non_blocking=True)
+                    ev.record(s_in)
+                else:
+                    for off, cnt in blocks:  # this chunk's rows of every block
+                        dx[b][off * rn:(off + cnt) * rn].copy_(
+                            src[off * nt + r0 * n2 * cnt:off * nt + r1 * n2 * cnt], non_blocking=True)
+                loaded = torch.cuda.Event()
+                loaded.record(s_in)
+            with torch.cuda.stream(s_cmp):
+                s_cmp.wait_event(loaded)
+                if free_out[b] is not None:
+                    s_cmp.wait_event(free_out[b])
+                if forward:
+                    lift_forward(dx[b][:n].view(r1 - r0, n2, p), levels, layout=N.LAYOUT_TUBE,
+                                 out=dy[b][:n].view(p, r1 - r0, n2))
+                else:
+                    lift_inverse(dx[b][:n], r1 - r0, n2, p, levels, layout=N.LAYOUT_TUBE,
+                                 out=dy[b][:n].view(r1 - r0, n2, p))
+                free_in[b] = torch.cuda.Event()
+                free_in[b].record(s_cmp)
+            with torch.cuda.stream(s_out):
+                s_out.wait_event(free_in[b])
+                if forward:
+                    for off, cnt in blocks:
+                        out[off * nt + r0 * n2 * cnt:off * nt + r1 * n2 * cnt].copy_(
+                            dy[b][off * rn:(off + cnt) * rn], non_blocking=True)
+                else:
+                    out[r0 * n2 * p:r1 * n2 * p].copy_(dy[b][:n], non_blocking=True)
+                free_out[b] = torch.cuda.Event()
+                free_out[b].record(s_out)
+        s_out.synchronize()
+        main.wait_stream(s_out)
+    return out
+
+
 # --------------------------------------------------------------- lifting ----
 
 def lift_forward(x: torch.Tensor, levels: int, layout: int = N.LAYOUT_SLICE,

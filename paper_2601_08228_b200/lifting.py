@@ -30,6 +30,9 @@ def max_levels(p):
     return ((p & -p).bit_length()) - 1
 
 
+_STREAM_MIN = 1 << 22  # host inputs from 4 M elements (32 MB) stream through the GPU in row chunks
+
+
 def _is_dev(x) -> bool:
     return isinstance(x, torch.Tensor) and x.is_cuda
 
@@ -162,12 +165,14 @@ def forward_w(t, levels):
     n1, n2 = t.shape[0], t.shape[1]
     if n1 * n2 * p == 0:
         return _empty_pyramid(t, levels)
-    x = E.as_device(t)
     if dev:
-        return _pyramid_from_packed(E.lift_forward(x, levels), levels, n1, n2, p)
+        return _pyramid_from_packed(E.lift_forward(E.as_device(t), levels), levels, n1, n2, p)
     # host mode: tube-major blocks = the reference's own per-level arrays, all
     # views of one pinned host buffer (inverse_w re-uploads it without packing)
-    host = E.to_host(E.lift_forward(x, levels, layout=N.LAYOUT_TUBE)).reshape(-1)
+    if n1 * n2 * p >= _STREAM_MIN and t.flags.c_contiguous:
+        host = E.host_lift(t, n1, n2, p, levels, forward=True).numpy()
+    else:
+        host = E.to_host(E.lift_forward(E.as_device(t), levels, layout=N.LAYOUT_TUBE)).reshape(-1)
     nt = n1 * n2
     blocks = {tag: host[off * nt:(off + cnt) * nt].reshape(n1, n2, cnt)
               for tag, off, cnt in E.block_slices(p, levels)}
@@ -216,6 +221,9 @@ def inverse_w(pyr):
         return np.zeros((n1, n2, p), dtype=np.float64)
     hf = getattr(pyr, "_host_flat", None)
     if hf is not None and pyr._same_views(hf[1]):
+        if n1 * n2 * p >= _STREAM_MIN:          # streamed H2D | K2 | D2H in row chunks
+            return E.host_lift(torch.from_numpy(hf[0]), n1, n2, p, levels,
+                               forward=False).numpy().reshape(n1, n2, p)
         flat, dev = E.as_device(hf[0]), False   # blocks are still views of the pinned buffer
     else:
         flat, dev = _pack_blocks(pyr)
