@@ -196,3 +196,23 @@ def test_tube_major_fast_route_masks_and_bases(shape, L):
     y2 = E.lift_inverse(coarse, n1, n2, p, L, layout=N.LAYOUT_TUBE, mask=mask, slice_base=p - 2 * m)
     zeros = [np.zeros_like(d) for d in d_ref[:-1]] + [d_ref[-1]]
     assert np.array_equal(y2.cpu().numpy(), O.lift_inverse(s_ref, zeros))
+
+
+def test_host_input_conventions_and_streamed_path():
+    """np.asarray(x, float64) semantics (lifting.py:83): lists, float32, Fortran order and
+    strided views all work; cubes from 4 M elements take the chunked host pipeline."""
+    rng = np.random.default_rng(77)
+    x = rng.standard_normal((130, 129, 256))           # 4.3 M elements -> streamed path
+    for src in (x, np.asfortranarray(x), x.astype(np.float32)):
+        s_ref, d_ref = O.lift_forward(np.asarray(src, dtype=np.float64), 4)
+        pyr = W.forward_w(src, 4)
+        assert np.array_equal(pyr.smooth, s_ref) and all(np.array_equal(a, b) for a, b in zip(pyr.details, d_ref))
+        y = W.inverse_w(pyr)
+        assert isinstance(y, np.ndarray) and y.flags.c_contiguous
+        assert np.array_equal(y, O.lift_inverse(s_ref, d_ref))
+    f32 = x.astype(np.float32)
+    assert np.array_equal(W.forward_w(f32, 2).smooth, O.lift_forward(f32.astype(np.float64), 2)[0])
+    view = x[::2, 1:, :128]                              # strided view
+    assert np.array_equal(W.forward_w(view, 3).smooth, O.lift_forward(np.ascontiguousarray(view), 3)[0])
+    lst = x[:2, :3, :8].tolist()
+    assert np.array_equal(W.forward_w(lst, 1).smooth, O.lift_forward(np.asarray(lst), 1)[0])
