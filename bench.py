@@ -475,10 +475,12 @@ def deblur_workload(args, steps=2, warmup=1):
             "psnr_db": imaging.psnr(xd, res["x"]), "ssim": imaging.ssim(xd, res["x"]),
             "psnr_db_blurred_input": imaging.psnr(xd, b), "ssim_blurred_input": imaging.ssim(xd, b),
             "quality_note": ("PSNR paper-verbatim 10 log10(N MPP / ||e||^2) (PAPER.md:878); matches the "
-                             "oracle (tests/test_gpu_imaging.py). The 9x9 sigma=2 Gaussian Toeplitz operators "
-                             "keep singular values down to 1e-3 sigma_max, so the pseudo-inverse amplifies the "
-                             "sigma=0.005 noise ~1e3x per side: the recovery is poor by construction of the "
-                             "config (the paper's own Table IV deblur reaches 9.7 dB)"),
+                             "oracle (tests/test_gpu_imaging.py). Under the lazy-wavelet w-product a "
+                             "slice-constant operator has zero detail blocks, so blur keeps only the 8-band "
+                             "means (L=3) and the recovery is at best the band-averaged cube; the 9x9 sigma=2 "
+                             "Toeplitz operators also amplify the sigma=0.005 noise up to 1e3x per side. The "
+                             "recovery is poor by construction of the config (the paper's own Table IV deblur "
+                             "reaches 9.7 dB)"),
             "w_product_ms": gms / 3,
             "w_product_roofline": {"bound": "tensor", "achieved": round(gflops / (gms / 3 * 1e-3) / 1e12, 2),
                                    "peak": peak, "unit": "TFLOP/s",
