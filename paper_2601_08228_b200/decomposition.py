@@ -162,6 +162,22 @@ def pinv_w_device(x: torch.Tensor, levels: int, tol: float = 1e-12,
     return E.lift_inverse(blocks, n2, n1, p, levels, out=out)
 
 
+def pinv_w_device_many(xs, levels: int, tol: float = 1e-12):
+    """pinv_w_device of several (n1, n2, p) tensors of one shape through ONE batched
+    K4 call over all their wavelet slices (independent per slice, so the result
+    is the same as one call each; small batches fill the GPU together)."""
+    if len({tuple(x.shape) for x in xs}) != 1:
+        return [pinv_w_device(x, levels, tol) for x in xs]
+    n1, n2, p = xs[0].shape
+    pyr = torch.empty((len(xs) * p, n1, n2), dtype=torch.float64, device=xs[0].device)
+    for i, x in enumerate(xs):
+        E.lift_forward(x.contiguous(), levels, out=pyr[i * p:(i + 1) * p])
+    sigma, vec, info = E.svd(pyr, min(n1, n2))
+    E.raise_if_failed(info)
+    blocks = E.pinv_blocks(pyr, sigma, vec, tol)                      # (k p, n2, n1)
+    return [E.lift_inverse(blocks[i * p:(i + 1) * p], n2, n1, p, levels) for i in range(len(xs))]
+
+
 def pinv_w(a, levels, tol=1e-12):
     """Moore-Penrose inverse under the w-product (decomposition.py:166-177)."""
     a, dev = _prep(a)

@@ -96,6 +96,17 @@ def deblur(b, a_v, a_h, levels, method="w", tol=1e-12):
         left = t_pinv(a_v, tol)
         right = t_pinv(transpose(a_h), tol)
         return t_product(t_product(left, b), right)
+    if method == "w" and _is_dev(a_v) == _is_dev(a_h) and tuple(a_v.shape) == tuple(a_h.shape):
+        # both operators' wavelet slices in one batched K4 call (independent per slice)
+        from .decomposition import _check_levels, pinv_w_device_many
+
+        dev = _is_dev(b) or _is_dev(a_v) or _is_dev(a_h)
+        av = E.as_device(a_v)
+        aht = E.as_device(transpose(a_h))
+        _check_levels(av.shape[2], levels)
+        left, right = pinv_w_device_many([av, aht], levels, tol)
+        out = w_product(w_product(left, E.as_device(b), levels), right, levels)
+        return out if dev else E.to_host(out)
     inv = pinv_w if method == "w" else sp_pinv_w
     left = inv(a_v, levels, tol)
     right = inv(transpose(a_h), levels, tol)
