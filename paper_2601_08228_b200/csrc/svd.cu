@@ -47,7 +47,11 @@ constexpr int kMaxInnerSweeps = 16;
 #ifndef WT_EIG_WARPS
 #define WT_EIG_WARPS 8
 #endif
-constexpr int kEigWarps = WT_EIG_WARPS;  // warps running the 32x32 eigen steps
+constexpr int kEigWarps = WT_EIG_WARPS;
+#ifndef WT_SVD_NZ
+#define WT_SVD_NZ 3
+#endif
+constexpr int kNZ = WT_SVD_NZ;  // chunk buffers in the streamed Gram / rotation pipelines  // warps running the 32x32 eigen steps
 
 __device__ __forceinline__ void eig_barrier() {
   asm volatile("bar.sync 1, %0;" ::"n"(kEigWarps * 32) : "memory");
@@ -97,7 +101,7 @@ __device__ __forceinline__ int rr_index(int pos, int round, int nb) {
 }
 
 struct PairSmem {
-  double Z[2][BW * LDZ];
+  double Z[kNZ][BW * LDZ];
   double G[1][BW * LDG];
   double Q[BW * LDG];
   double warp_off[kThreads / 32];
@@ -141,14 +145,18 @@ __global__ void __launch_bounds__(kThreads, WT_SVD_MINB) svd_pair_kernel(SvdWs w
   double acc[10][2];
 #pragma unroll
   for (int t = 0; t < 10; ++t) acc[t][0] = acc[t][1] = 0.0;
-  load_chunk(S.Z[0], Xb, mpad, colI, colJ, 0);
-  cp_async_commit();
-  for (int ch = 0; ch < nch; ++ch) {
-    if (ch + 1 < nch) load_chunk(S.Z[(ch + 1) & 1], Xb, mpad, colI, colJ, (int64_t)(ch + 1) * RCH);
+#pragma unroll
+  for (int s0 = 0; s0 < kNZ - 1; ++s0) {
+    if (s0 < nch) load_chunk(S.Z[s0], Xb, mpad, colI, colJ, (int64_t)s0 * RCH);
     cp_async_commit();
-    cp_async_wait<1>();
+  }
+  for (int ch = 0; ch < nch; ++ch) {
+    const int nx = ch + kNZ - 1;
+    if (nx < nch) load_chunk(S.Z[nx % kNZ], Xb, mpad, colI, colJ, (int64_t)nx * RCH);
+    cp_async_commit();
+    cp_async_wait<kNZ - 1>();
     __syncthreads();
-    const double* Zs = S.Z[ch & 1];
+    const double* Zs = S.Z[ch % kNZ];
     double2 f[4];
 #pragma unroll
     for (int tj = 0; tj < 4; ++tj)
@@ -367,14 +375,18 @@ __global__ void __launch_bounds__(kThreads, WT_SVD_MINB) svd_pair_kernel(SvdWs w
   for (int kk = 0; kk < 8; ++kk)
 #pragma unroll
     for (int j = 0; j < 2; ++j) qf[kk][j] = S.Q[(kk * 4 + (lane & 3)) * LDG + (2 * nh + j) * 8 + (lane >> 2)];
-  load_chunk(S.Z[0], Xb, mpad, colI, colJ, 0);
-  cp_async_commit();
-  for (int ch = 0; ch < nch; ++ch) {
-    if (ch + 1 < nch) load_chunk(S.Z[(ch + 1) & 1], Xb, mpad, colI, colJ, (int64_t)(ch + 1) * RCH);
+#pragma unroll
+  for (int s0 = 0; s0 < kNZ - 1; ++s0) {
+    if (s0 < nch) load_chunk(S.Z[s0], Xb, mpad, colI, colJ, (int64_t)s0 * RCH);
     cp_async_commit();
-    cp_async_wait<1>();
+  }
+  for (int ch = 0; ch < nch; ++ch) {
+    const int nx = ch + kNZ - 1;
+    if (nx < nch) load_chunk(S.Z[nx % kNZ], Xb, mpad, colI, colJ, (int64_t)nx * RCH);
+    cp_async_commit();
+    cp_async_wait<kNZ - 1>();
     __syncthreads();
-    double* Zs = S.Z[ch & 1];
+    double* Zs = S.Z[ch % kNZ];
     double o[2][2][2];
 #pragma unroll
     for (int i = 0; i < 2; ++i)
