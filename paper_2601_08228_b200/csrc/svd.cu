@@ -404,23 +404,20 @@ __global__ void __launch_bounds__(kThreads, WT_SVD_MINB) svd_pair_kernel(SvdWs w
         dmma884(o[1][j][0], o[1][j][1], a.y, qf[kk][j]);
       }
     }
-    __syncthreads();  // every warp has read its rows (the other n-half reads them too)
+    // results straight from the DMMA fragments to global, in place: a lane
+    // holds rows r0, r0+1 of 4 output columns, so the 8 lanes sharing lane%4
+    // write 128 contiguous bytes of one column (no smem round trip)
+    const int64_t rbase = (int64_t)ch * RCH;
 #pragma unroll
     for (int j = 0; j < 2; ++j)
 #pragma unroll
-      for (int h = 0; h < 2; ++h)
-        *reinterpret_cast<double2*>(Zs + ((2 * nh + j) * 8 + 2 * (lane & 3) + h) * LDZ + r0) =
+      for (int h = 0; h < 2; ++h) {
+        const int c = (2 * nh + j) * 8 + 2 * (lane & 3) + h;
+        const int gc = c < HB ? colI + c : colJ + c - HB;
+        *reinterpret_cast<double2*>(Xb + (int64_t)gc * mpad + rbase + r0) =
             make_double2(o[0][j][h], o[1][j][h]);
-    __syncthreads();
-    // chunk -> global (each column: RCH contiguous doubles)
-    const int64_t rbase = (int64_t)ch * RCH;
-    for (int v = tid; v < BW * (RCH / 2); v += kThreads) {
-      const int c = v / (RCH / 2), rv = (v % (RCH / 2)) * 2;
-      const int gc = c < HB ? colI + c : colJ + c - HB;
-      *reinterpret_cast<double2*>(Xb + (int64_t)gc * mpad + rbase + rv) =
-          *reinterpret_cast<const double2*>(Zs + c * LDZ + rv);
-    }
-    __syncthreads();
+      }
+    __syncthreads();  // every warp has read the chunk before its buffer is refilled
   }
   if (ws.prof && tid == 0) {
     atomicAdd(ws.prof + 0, (unsigned long long)(t_gram - t_start));
