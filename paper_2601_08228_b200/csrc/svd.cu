@@ -68,6 +68,8 @@ struct SvdWs {
   int* pending;     // 1 counter (matrices still iterating)
   double* sig;      // batch * npad  (scratch for the final sort)
   int* perm;        // batch * npad
+  int* bdone;       // batch * nblk: rounds of the current sweep finished per column block
+  int* ticket;      // 1 counter: next visit of the current sweep (persistent sweeps)
 };
 
 __host__ __device__ inline int64_t round_up(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
@@ -121,15 +123,12 @@ __device__ __forceinline__ void load_chunk(double* Zs, const double* Xb, int64_t
   }
 }
 
-__global__ void __launch_bounds__(kThreads, WT_SVD_MINB) svd_pair_kernel(SvdWs ws, int64_t mpad, int64_t npad,
-                                                               int round, double tol, int inner_sweeps,
-                                                               int cross_only) {
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  PairSmem& S = *reinterpret_cast<PairSmem*>(smem_raw);
-  const int b = ws.active[blockIdx.y];
+// One pair visit (matrix b, column blocks I and J).  Every early return is
+// CTA-uniform (it depends on global flags / shared values only).
+__device__ __forceinline__ void pair_visit(PairSmem& S, const SvdWs& ws, int b, int I, int J,
+                                           int64_t mpad, int64_t npad, double tol, int inner_sweeps,
+                                           int cross_only) {
   if (ws.conv[b]) return;
-  const int nb = (int)(npad / HB);
-  const int I = rr_index(blockIdx.x, round, nb), J = rr_index(nb - 1 - blockIdx.x, round, nb);
   const int colI = I * HB, colJ = J * HB;
   double* Xb = mat_ptr(ws, b, npad, mpad);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -427,6 +426,72 @@ __global__ void __launch_bounds__(kThreads, WT_SVD_MINB) svd_pair_kernel(SvdWs w
   }
 }
 
+// One launch per round: CTA (x, y) visits pair x of active matrix y.
+__global__ void __launch_bounds__(kThreads, WT_SVD_MINB) svd_pair_kernel(SvdWs ws, int64_t mpad, int64_t npad,
+                                                               int round, double tol, int inner_sweeps,
+                                                               int cross_only) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  PairSmem& S = *reinterpret_cast<PairSmem*>(smem_raw);
+  const int nb = (int)(npad / HB);
+  const int I = rr_index(blockIdx.x, round, nb), J = rr_index(nb - 1 - blockIdx.x, round, nb);
+  pair_visit(S, ws, ws.active[blockIdx.y], I, J, mpad, npad, tol, inner_sweeps, cross_only);
+}
+
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void st_release(int* p, int v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// One persistent launch per sweep: CTAs take visits from a global ticket in
+// (round, matrix, pair) order and start a visit as soon as the two visits of
+// the previous round that held its blocks have finished (per-block round
+// counters ws.bdone), so a round's tail overlaps the next round's start
+// instead of draining the GPU at every kernel boundary.  A visit only waits on
+// smaller tickets, which running CTAs already hold: no deadlock.
+__global__ void __launch_bounds__(kThreads, WT_SVD_MINB) svd_sweep_kernel(SvdWs ws, int64_t mpad, int64_t npad,
+                                                                int n_active, double tol, int inner_sweeps,
+                                                                int cross) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  PairSmem& S = *reinterpret_cast<PairSmem*>(smem_raw);
+  __shared__ int s_item[4];  // ticket, then (matrix, block I, block J) of the visit
+  const int nb = (int)(npad / HB);
+  const int per_round = n_active * (nb / 2);
+  const int total = per_round * (nb - 1);
+  for (;;) {
+    if (threadIdx.x == 0) {
+      const int t = atomicAdd(ws.ticket, 1);
+      s_item[0] = t;
+      if (t < total) {
+        const int round = t / per_round, rem = t - round * per_round;
+        const int ai = rem / (nb / 2), k = rem - ai * (nb / 2);
+        const int b = ws.active[ai];
+        const int I = rr_index(k, round, nb), J = rr_index(nb - 1 - k, round, nb);
+        s_item[1] = b;
+        s_item[2] = I;
+        s_item[3] = J;
+        while (ld_acquire(ws.bdone + (int64_t)b * nb + I) < round) __nanosleep(100);
+        while (ld_acquire(ws.bdone + (int64_t)b * nb + J) < round) __nanosleep(100);
+      }
+    }
+    __syncthreads();
+    const int t = s_item[0];
+    if (t >= total) return;
+    const int round = t / per_round;
+    pair_visit(S, ws, s_item[1], s_item[2], s_item[3], mpad, npad, tol, inner_sweeps, cross && round > 0);
+    __syncthreads();  // every store of the visit precedes the release below (and s_item reuse)
+    if (threadIdx.x == 0) {
+      __threadfence();
+      st_release(ws.bdone + (int64_t)s_item[1] * nb + s_item[2], round + 1);
+      st_release(ws.bdone + (int64_t)s_item[1] * nb + s_item[3], round + 1);
+    }
+  }
+}
+
 // ------------------------------------------------------ sweep bookkeeping --
 __global__ void svd_end_sweep(SvdWs ws, int batch, double tol) {
   for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < batch; b += gridDim.x * blockDim.x) {
@@ -542,7 +607,8 @@ __global__ void svd_flip(SvdWs ws, int batch) {
 
 struct WsLayout {
   int64_t m, n, mpad, npad;
-  size_t off_X, off_X2, off_xsel, off_active, off_off, off_conv, off_pending, off_sig, off_perm, total;
+  size_t off_X, off_X2, off_xsel, off_active, off_off, off_conv, off_pending, off_sig, off_perm, off_bdone,
+      total;
 };
 
 WsLayout ws_layout(int64_t n1, int64_t n2, int64_t batch) {
@@ -562,6 +628,7 @@ WsLayout ws_layout(int64_t n1, int64_t n2, int64_t batch) {
   L.off_pending = take(sizeof(int) * 4);
   L.off_sig = take(sizeof(double) * (size_t)(batch * L.npad));
   L.off_perm = take(sizeof(int) * (size_t)(batch * L.npad));
+  L.off_bdone = take(sizeof(int) * (size_t)(batch * (L.npad / HB)));
   L.total = o;
   return L;
 }
@@ -632,7 +699,8 @@ extern "C" int wt_svd_jacobi_f64(const double* A, int64_t lda, int64_t strideA, 
            nullptr,
            reinterpret_cast<unsigned long long*>(base + L.off_off),
            reinterpret_cast<int*>(base + L.off_conv), reinterpret_cast<int*>(base + L.off_pending),
-           reinterpret_cast<double*>(base + L.off_sig), reinterpret_cast<int*>(base + L.off_perm)};
+           reinterpret_cast<double*>(base + L.off_sig), reinterpret_cast<int*>(base + L.off_perm),
+           reinterpret_cast<int*>(base + L.off_bdone), reinterpret_cast<int*>(base + L.off_pending) + 2};
   if (tol <= 0.0) tol = 4.0 * 2.220446049250313e-16 * sqrt((double)L.m) + 1e-15;
   if (max_sweeps <= 0) max_sweeps = 40;
   const bool right = n1 <= n2;
@@ -647,9 +715,23 @@ extern "C" int wt_svd_jacobi_f64(const double* A, int64_t lda, int64_t strideA, 
   WT_CUDA(cudaMemsetAsync(ws.xsel, 0, sizeof(int) * batch, st));
   svd_iota<<<(unsigned)((batch + 255) / 256), 256, 0, st>>>(ws.active, (int)batch);
   int64_t n_active = batch;
-  WT_CUDA(cudaMemsetAsync(ws.pending, 0, sizeof(int) * 2, st));
+  WT_CUDA(cudaMemsetAsync(ws.pending, 0, sizeof(int) * 3, st));
 
   if (int e = ensure_smem(svd_pair_kernel, sizeof(PairSmem))) return e;
+  if (int e = ensure_smem(svd_sweep_kernel, sizeof(PairSmem))) return e;
+  // Persistent sweeps (one launch per sweep, visits scheduled by block
+  // dependencies) unless WT_SVD_PERSIST=0 (one launch per round).
+  int persist = 1;
+  if (const char* e = getenv("WT_SVD_PERSIST")) persist = atoi(e);
+  int sweep_ctas = 0;
+  if (persist) {
+    int dev = 0, per_sm = 0;
+    WT_CUDA(cudaGetDevice(&dev));
+    int sms = 0;
+    WT_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    WT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, svd_sweep_kernel, kThreads, sizeof(PairSmem)));
+    sweep_ctas = sms * std::max(per_sm, 1);
+  }
   g_last_sweeps = 0;
   g_last_rotations = 0;
   int dbg_prev = 0;
@@ -693,9 +775,17 @@ extern "C" int wt_svd_jacobi_f64(const double* A, int64_t lda, int64_t strideA, 
       svd_flip<<<(unsigned)((batch + 255) / 256), 256, 0, st>>>(ws, (int)batch);
       if (int e = check_launch("svd reorder")) return e;
     }
-    for (int round = 0; round < nb - 1; ++round) {
-      svd_pair_kernel<<<dim3(nb / 2, (unsigned)n_active), kThreads, sizeof(PairSmem), st>>>(
-          ws, L.mpad, L.npad, round, tol, inner, cross && round > 0);
+    if (persist && n_active * (int64_t)(nb / 2) * (nb - 1) < (1ll << 30)) {  // int tickets
+      WT_CUDA(cudaMemsetAsync(ws.bdone, 0, sizeof(int) * (size_t)batch * nb, st));
+      WT_CUDA(cudaMemsetAsync(ws.ticket, 0, sizeof(int), st));
+      const int64_t visits = n_active * (int64_t)(nb / 2) * (nb - 1);
+      svd_sweep_kernel<<<(unsigned)std::min<int64_t>(visits, sweep_ctas), kThreads, sizeof(PairSmem), st>>>(
+          ws, L.mpad, L.npad, (int)n_active, tol, inner, cross);
+    } else {
+      for (int round = 0; round < nb - 1; ++round) {
+        svd_pair_kernel<<<dim3(nb / 2, (unsigned)n_active), kThreads, sizeof(PairSmem), st>>>(
+            ws, L.mpad, L.npad, round, tol, inner, cross && round > 0);
+      }
     }
     if (int e = check_launch("svd_pair_kernel")) return e;
     if (getenv("WT_SVD_DEBUG")) {  // per-sweep convergence trace (diagnostics only)
