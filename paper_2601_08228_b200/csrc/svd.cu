@@ -35,19 +35,27 @@ namespace {
 
 constexpr int BW = 32;       // pair panel width (2 blocks of 16 columns)
 constexpr int HB = BW / 2;   // block width
-constexpr int RCH = 64;      // rows per streamed chunk
+#ifndef WT_SVD_THREADS
+#define WT_SVD_THREADS 256
+#endif
+constexpr int kThreads = WT_SVD_THREADS;
+constexpr int kWarps = kThreads / 32;
+constexpr int RCH = 8 * kWarps;  // rows per streamed chunk (8 per warp in the Gram)
 constexpr int LDZ = RCH + 8; // chunk column pitch (doubles), = 8 mod 16: conflict-free LDS.128 Gram frags
 constexpr int LDG = BW + 1;  // Gram / Q pitch
-constexpr int kThreads = 256;
+static_assert(kWarps == 4 || kWarps == 8, "K4 CTA shape: 4 or 8 warps");
 constexpr double kFloorEps = 1e3 * 2.220446049250313e-16;  // null-column floor (see the test)
 constexpr int kMaxInnerSweeps = 16;
 #ifndef WT_SVD_MINB
 #define WT_SVD_MINB 3
 #endif
 #ifndef WT_EIG_WARPS
-#define WT_EIG_WARPS 8
+#define WT_EIG_WARPS WT_SVD_THREADS / 32
 #endif
 constexpr int kEigWarps = WT_EIG_WARPS;
+#ifndef WT_SVD_FLATRED
+#define WT_SVD_FLATRED 1
+#endif
 #ifndef WT_SVD_NZ
 #define WT_SVD_NZ 3
 #endif
@@ -109,6 +117,8 @@ struct PairSmem {
   double warp_off[kThreads / 32];
   double gmax;
   int any_rot;
+  unsigned long long gmax_bits;
+  long long ts[2];  // WT_SVD_PROFILE: end of the Gram stream, end of the reduction
 };
 
 __device__ __forceinline__ void load_chunk(double* Zs, const double* Xb, int64_t mpad, int colI,
@@ -170,11 +180,46 @@ __device__ __forceinline__ void pair_visit(PairSmem& S, const SvdWs& ws, int b, 
       }
     __syncthreads();
   }
+  if (tid == 0) S.ts[0] = clock64();
   {
+#if WT_SVD_FLATRED
+    // every warp parks its partial tiles in the (now free) chunk buffers; each
+    // thread then sums fixed entries over the warps in warp order (deterministic),
+    // writes them and their mirror into G and folds the diagonal into gmax
+    // (shared 64-bit max of the bit patterns: non-negative doubles order as
+    // integers; NaN is skipped like fmax does).  2 barriers instead of a tree.
+    static_assert(kWarps * 10 * 64 <= kNZ * BW * LDZ, "partial tiles exceed the chunk buffers");
+    double* red = S.Z[0];  // kWarps x 10 x 64 doubles
+#pragma unroll
+    for (int t = 0; t < 10; ++t) {
+      red[(warp * 10 + t) * 64 + 2 * lane] = acc[t][0];
+      red[(warp * 10 + t) * 64 + 2 * lane + 1] = acc[t][1];
+    }
+    if (tid == 0) S.gmax_bits = 0ull;
+    __syncthreads();
+    for (int e = tid; e < 640; e += kThreads) {
+      double v = red[e];
+#pragma unroll
+      for (int w = 1; w < kWarps; ++w) v += red[w * 640 + e];
+      const int t = e >> 6, l = (e & 63) >> 1, h = e & 1;
+      // tile t -> (ta, tb), ta <= tb, in the order of the accumulation loop
+      const int ta = t < 4 ? 0 : t < 7 ? 1 : t < 9 ? 2 : 3;
+      const int tb = ta + t - (ta == 0 ? 0 : ta == 1 ? 4 : ta == 2 ? 7 : 9);
+      const int r = ta * 8 + (l >> 2), c = tb * 8 + 2 * (l & 3) + h;
+      if (ta < tb || r <= c) {
+        S.G[0][r * LDG + c] = v;
+        S.G[0][c * LDG + r] = v;
+        if (r == c && !isnan(v)) atomicMax(&S.gmax_bits, (unsigned long long)__double_as_longlong(v));
+      }
+    }
+    __syncthreads();
+  }
+#else
     // deterministic tree over the 8 warps through the (now free) chunk buffers
     double* red = S.Z[0];  // 4 x 10 x 64 doubles
 #pragma unroll
-    for (int half = 4; half >= 1; half >>= 1) {
+    static_assert((kWarps / 2) * 10 * 64 <= kNZ * BW * LDZ, "tree buffer exceeds the chunk buffers");
+    for (int half = kWarps / 2; half >= 1; half >>= 1) {
       if (warp >= half && warp < 2 * half) {
 #pragma unroll
         for (int t = 0; t < 10; ++t) {
@@ -214,6 +259,7 @@ __device__ __forceinline__ void pair_visit(PairSmem& S, const SvdWs& ws, int b, 
     }
     __syncthreads();
   }
+#endif
 
   // ---------------- 2. convergence test on this pair -----------------------
   // Pair (i, j) is orthogonal enough when
@@ -222,7 +268,12 @@ __device__ __forceinline__ void pair_visit(PairSmem& S, const SvdWs& ws, int b, 
   // ~1e-13 |z_max|), whose directions are rounding noise and must not keep
   // the iteration alive; real columns are held to the relative tolerance.
   // `off` is the largest |g_ij| / (that bound) * tol, so off < tol <=> converged.
+  if (tid == 0) S.ts[1] = clock64();
+#if WT_SVD_FLATRED
+  const double gmax = __longlong_as_double((long long)S.gmax_bits);
+#else
   const double gmax = S.gmax;
+#endif
   const double floor_c = kFloorEps * kFloorEps / tol;
   {
     // 1 / max(sqrt(g_ii g_jj), floor_c g_max) = min(rsqrt(g_ii g_jj), 1 / (floor_c g_max)):
@@ -368,7 +419,8 @@ __device__ __forceinline__ void pair_visit(PairSmem& S, const SvdWs& ws, int b, 
   // warp w: chunk rows rt*16 .. rt*16+15 (two 8-row tiles) x output n-tiles
   // {2nh, 2nh+1}; its Q b-fragments Q[kk*4 + lane%4][n*8 + lane/4] stay in
   // registers for the whole stream.
-  const int rt = warp & 3, nh = warp >> 2;
+  constexpr int RT = RCH / 16;  // 16-row tiles per chunk; warps = RT x 2 column halves
+  const int rt = warp % RT, nh = warp / RT;
   double qf[8][2];
 #pragma unroll
   for (int kk = 0; kk < 8; ++kk)
@@ -423,6 +475,8 @@ __device__ __forceinline__ void pair_visit(PairSmem& S, const SvdWs& ws, int b, 
     atomicAdd(ws.prof + 1, (unsigned long long)(t_eig - t_gram));
     atomicAdd(ws.prof + 2, (unsigned long long)(clock64() - t_eig));
     atomicAdd(ws.prof + 3, 1ull);
+    atomicAdd(ws.prof + 4, (unsigned long long)(S.ts[0] - t_start));
+    atomicAdd(ws.prof + 5, (unsigned long long)(S.ts[1] - S.ts[0]));
   }
 }
 
@@ -738,8 +792,8 @@ extern "C" int wt_svd_jacobi_f64(const double* A, int64_t lda, int64_t strideA, 
   static unsigned long long* d_prof = nullptr;
   const bool profile = getenv("WT_SVD_PROFILE") != nullptr;
   if (profile) {
-    if (!d_prof) WT_CUDA(cudaMalloc(&d_prof, 4 * sizeof(unsigned long long)));
-    WT_CUDA(cudaMemsetAsync(d_prof, 0, 4 * sizeof(unsigned long long), st));
+    if (!d_prof) WT_CUDA(cudaMalloc(&d_prof, 8 * sizeof(unsigned long long)));
+    WT_CUDA(cudaMemsetAsync(d_prof, 0, 8 * sizeof(unsigned long long), st));
     ws.prof = d_prof;
   }
   static thread_local int* h_pending = nullptr;  // per host thread: concurrent calls on other streams
@@ -823,12 +877,13 @@ extern "C" int wt_svd_jacobi_f64(const double* A, int64_t lda, int64_t strideA, 
     g_last_panel_rows = L.mpad;
   }
   if (profile) {
-    unsigned long long h[4];
+    unsigned long long h[8];
     WT_CUDA(cudaMemcpyAsync(h, d_prof, sizeof(h), cudaMemcpyDeviceToHost, st));
     WT_CUDA(cudaStreamSynchronize(st));
     const double n = h[3] ? (double)h[3] : 1.0;
     fprintf(stderr, "[wt_svd] %llu rotated pair visits; mean cycles per visit: gram+test %.0f, "
-            "eigen %.0f, rotate %.0f\n", h[3], h[0] / n, h[1] / n, h[2] / n);
+            "eigen %.0f, rotate %.0f (gram: stream %.0f, reduce %.0f, test %.0f)\n", h[3], h[0] / n,
+            h[1] / n, h[2] / n, h[4] / n, h[5] / n, (h[0] - h[4] - h[5]) / n);
   }
   {
     const size_t sm = (size_t)npow2 * (sizeof(double) + sizeof(int));
