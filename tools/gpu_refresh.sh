@@ -1,0 +1,7 @@
+set -x
+timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/gputests.log 2>&1; echo rc=$? >> gpurun_out/gputests.log
+timeout 400 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err
+timeout 400 python bench.py --impl reference > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 1 > gpurun_out/ncu_launch.log 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:svd_sweep_kernel --launch-skip 6 -c 1 -o gpurun_out/k4_cfg3 -f python tools/svd_one.py 3 > gpurun_out/ncu_k4_3.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:svd_sweep_kernel --launch-skip 6 -c 1 -o gpurun_out/k4_cfg4 -f python tools/svd_one.py 4 > gpurun_out/ncu_k4_4.log 2>&1
