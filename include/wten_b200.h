@@ -177,6 +177,15 @@ int wt_svd_factors_f64(const double* T, const double* vec, int64_t nvec, const d
 int wt_pinv_from_svd_f64(const double* A, int64_t lda, int64_t strideA, int64_t n1, int64_t n2,
                          int64_t batch, const double* sigma, const double* vec, double tol,
                          double* out, int64_t ldo, int64_t strideO, double* T, void* stream);
+/* Same result as wt_pinv_from_svd_f64, with the GEMMs limited per slice to the
+ * k_b kept singular values (s > tol * s_max): the projection computes only
+ * k_b columns of T and the assembly sums only k_b terms, so an all-zero slice
+ * (k_b = 0) costs no GEMM work and yields exact zeros.  rank_ws: batch ints
+ * (device, caller-owned); on return rank_ws[b] = k_b. */
+int wt_pinv_from_svd_ranked_f64(const double* A, int64_t lda, int64_t strideA, int64_t n1,
+                                int64_t n2, int64_t batch, const double* sigma, const double* vec,
+                                double tol, double* out, int64_t ldo, int64_t strideO, double* T,
+                                int* rank_ws, void* stream);
 
 /* Comparator-DFT helper: out[t][k] = x[t][k] - x[t][0] over ntubes tubes of p
  * samples (tube-fastest).  The t-product baselines FFT these deltas and add

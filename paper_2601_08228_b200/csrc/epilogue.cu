@@ -57,29 +57,69 @@ extern "C" int wt_svd_factors_f64(const double* T, const double* vec, int64_t nv
   return wt_copy2d_f64(vec, ln, sV, longf, r, ln * r, ln, r, batch, 1, stream);
 }
 
-extern "C" int wt_pinv_from_svd_f64(const double* A, int64_t lda, int64_t strideA, int64_t n1,
-                                    int64_t n2, int64_t batch, const double* sigma,
-                                    const double* vec, double tol, double* out, int64_t ldo,
-                                    int64_t strideO, double* T, void* stream) {
+namespace {
+// k_b = #{i : s_i > tol * s_0 and s_i > 0} (sigma descending): the columns
+// WT_SCALE_PINV2 keeps (decomposition.py:160-161).
+__global__ void pinv_rank_kernel(const double* __restrict__ s, int64_t q, double tol, int* rank) {
+  const int64_t b = blockIdx.x;
+  const double smax = s[b * q];
+  int cnt = 0;
+  for (int64_t i = threadIdx.x; i < q; i += blockDim.x) {
+    const double v = s[b * q + i];
+    cnt += (v > tol * smax && v > 0.0) ? 1 : 0;
+  }
+  __shared__ int tot;
+  if (threadIdx.x == 0) tot = 0;
+  __syncthreads();
+  atomicAdd(&tot, cnt);  // integer: order-independent
+  __syncthreads();
+  if (threadIdx.x == 0) rank[b] = tot;
+}
+}  // namespace
+
+extern "C" int wt_pinv_from_svd_ranked_f64(const double* A, int64_t lda, int64_t strideA, int64_t n1,
+                                           int64_t n2, int64_t batch, const double* sigma,
+                                           const double* vec, double tol, double* out, int64_t ldo,
+                                           int64_t strideO, double* T, int* rank_ws, void* stream) {
   const int64_t q = n1 < n2 ? n1 : n2, ln = n1 < n2 ? n2 : n1;
   WT_REQUIRE(n1 >= 1 && n2 >= 1 && batch >= 0, "pinv_from_svd: bad shape");
   WT_REQUIRE(A && sigma && vec && out && T, "pinv_from_svd: null pointer");
   if (batch == 0) return WT_OK;
+  if (rank_ws) {
+    for (int64_t b0 = 0; b0 < batch; b0 += 65535) {
+      const int64_t nb = batch - b0 < 65535 ? batch - b0 : 65535;
+      pinv_rank_kernel<<<(unsigned)nb, 128, 0, (cudaStream_t)stream>>>(sigma + b0 * q, q, tol,
+                                                                       rank_ws + b0);
+    }
+    if (int e = wt::check_launch("pinv_rank_kernel")) return e;
+  }
   const int64_t sV = q * ln, sT = q * q;
   int st;
   if (n1 <= n2) {
-    // T = A V (n1 x q) = U diag(s); scale by s+^2 -> U diag(s+); out = V T^T (n2 x n1)
-    st = wt_gemm_f64(0, 1, n1, q, n2, 1.0, A, lda, strideA, vec, ln, sV, 0.0, T, q, sT, batch, stream);
+    // T = A V (n1 x q) = U diag(s), first k_b columns; scale by s+^2 -> U diag(s+);
+    // out = V T^T (n2 x n1) over the k_b kept terms
+    st = wt::gemm_f64_lim(0, 1, n1, q, n2, 1.0, A, lda, strideA, vec, ln, sV, 0.0, T, q, sT, batch,
+                          nullptr, rank_ws, stream);
     if (st) return st;
     st = wt_scale_cols_f64(T, n1, q, q, sT, sigma, q, batch, WT_SCALE_PINV2, tol, stream);
     if (st) return st;
-    return wt_gemm_f64(1, 1, n2, n1, q, 1.0, vec, ln, sV, T, q, sT, 0.0, out, ldo, strideO, batch,
-                       stream);
+    return wt::gemm_f64_lim(1, 1, n2, n1, q, 1.0, vec, ln, sV, T, q, sT, 0.0, out, ldo, strideO,
+                            batch, rank_ws, nullptr, stream);
   }
-  // T = A^T U (n2 x q) = V diag(s); out = T diag(s+^2) U^T (n2 x n1)
-  st = wt_gemm_f64(1, 1, n2, q, n1, 1.0, A, lda, strideA, vec, ln, sV, 0.0, T, q, sT, batch, stream);
+  // T = A^T U (n2 x q) = V diag(s), first k_b columns; out = T diag(s+^2) U^T (n2 x n1)
+  st = wt::gemm_f64_lim(1, 1, n2, q, n1, 1.0, A, lda, strideA, vec, ln, sV, 0.0, T, q, sT, batch,
+                        nullptr, rank_ws, stream);
   if (st) return st;
   st = wt_scale_cols_f64(T, n2, q, q, sT, sigma, q, batch, WT_SCALE_PINV2, tol, stream);
   if (st) return st;
-  return wt_gemm_f64(0, 0, n2, n1, q, 1.0, T, q, sT, vec, ln, sV, 0.0, out, ldo, strideO, batch, stream);
+  return wt::gemm_f64_lim(0, 0, n2, n1, q, 1.0, T, q, sT, vec, ln, sV, 0.0, out, ldo, strideO, batch,
+                          rank_ws, nullptr, stream);
+}
+
+extern "C" int wt_pinv_from_svd_f64(const double* A, int64_t lda, int64_t strideA, int64_t n1,
+                                    int64_t n2, int64_t batch, const double* sigma,
+                                    const double* vec, double tol, double* out, int64_t ldo,
+                                    int64_t strideO, double* T, void* stream) {
+  return wt_pinv_from_svd_ranked_f64(A, lda, strideA, n1, n2, batch, sigma, vec, tol, out, ldo,
+                                     strideO, T, nullptr, stream);
 }

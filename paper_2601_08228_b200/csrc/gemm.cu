@@ -39,6 +39,8 @@ struct GemmArgs {
   double* C;
   int64_t ldc, sC;
   int64_t batch;
+  const int* klim;  // per-matrix inner-dimension limit (nullable)
+  const int* nlim;  // per-matrix output-column limit (nullable)
 };
 
 template <int BM, int BN, bool TA, bool TB>
@@ -66,8 +68,6 @@ __global__ void __launch_bounds__(WM* WN * 32) gemm_f64_kernel(GemmArgs g) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm0 = (warp / WN) * WTM, wn0 = (warp % WN) * WTN;
   const int64_t m0 = (int64_t)blockIdx.y * BM, n0 = (int64_t)blockIdx.x * BN;
-  const int nk = (int)((g.K + BK - 1) / BK);
-
   // Loader geometry, fixed for the whole kernel: each thread owns A_IT (B_IT)
   // 16-byte chunks of every stage at the same tile position; only the k offset
   // moves, so a stage's addresses are one multiply-add per chunk (ncu: the
@@ -103,6 +103,9 @@ __global__ void __launch_bounds__(WM* WN * 32) gemm_f64_kernel(GemmArgs g) {
   const int64_t b_kstep = TB ? BK : (int64_t)BK * g.ldb;
 
   for (int64_t b = blockIdx.z; b < g.batch; b += gridDim.z) {
+    if (g.nlim && n0 >= g.nlim[b]) continue;  // no output column of this tile is wanted
+    const int64_t Kb = g.klim ? std::min<int64_t>(g.K, std::max(g.klim[b], 0)) : g.K;
+    const int nk = (int)((Kb + BK - 1) / BK);
     const double* __restrict__ A = g.A + b * g.sA;
     const double* __restrict__ B = g.B + b * g.sB;
     double* __restrict__ C = g.C + b * g.sC;
@@ -114,13 +117,13 @@ __global__ void __launch_bounds__(WM* WN * 32) gemm_f64_kernel(GemmArgs g) {
 #pragma unroll
       for (int it = 0; it < A_IT; ++it) {
         if (A_CH % NT != 0 && tid + it * NT >= A_CH) break;
-        const bool ok = a_k[it] >= 0 && a_k[it] + k0 < g.K;
+        const bool ok = a_k[it] >= 0 && a_k[it] + k0 < Kb;
         cp_async_zfill<VEC * 8>(As + a_so[it], ok ? A + a_go[it] + kt * a_kstep : A, ok);
       }
 #pragma unroll
       for (int it = 0; it < B_IT; ++it) {
         if (B_CH % NT != 0 && tid + it * NT >= B_CH) break;
-        const bool ok = b_k[it] >= 0 && b_k[it] + k0 < g.K;
+        const bool ok = b_k[it] >= 0 && b_k[it] + k0 < Kb;
         cp_async_zfill<VEC * 8>(Bs + b_so[it], ok ? B + b_go[it] + kt * b_kstep : B, ok);
       }
     };
@@ -250,10 +253,10 @@ int dispatch_vec(const GemmArgs& g, cudaStream_t st) {
 
 using namespace wt;
 
-extern "C" int wt_gemm_f64(int transA, int transB, int64_t M, int64_t N, int64_t K, double alpha,
-                           const double* A, int64_t lda, int64_t strideA, const double* B,
-                           int64_t ldb, int64_t strideB, double beta, double* C, int64_t ldc,
-                           int64_t strideC, int64_t batch, void* stream) {
+int wt::gemm_f64_lim(int transA, int transB, int64_t M, int64_t N, int64_t K, double alpha,
+                     const double* A, int64_t lda, int64_t strideA, const double* B, int64_t ldb,
+                     int64_t strideB, double beta, double* C, int64_t ldc, int64_t strideC,
+                     int64_t batch, const int* klim, const int* nlim, void* stream) {
   WT_REQUIRE(M >= 0 && N >= 0 && K >= 0 && batch >= 0, "gemm: negative dimension");
   if (M == 0 || N == 0 || batch == 0) return WT_OK;
   WT_REQUIRE(ldc >= N, "gemm: ldc < N");
@@ -265,10 +268,18 @@ extern "C" int wt_gemm_f64(int transA, int transB, int64_t M, int64_t N, int64_t
     gemm_scale_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(C, M, N, ldc, strideC, beta);
     return check_launch("wt_gemm_f64(K=0)");
   }
-  GemmArgs g{M, N, K, alpha, beta, A, lda, strideA, B, ldb, strideB, C, ldc, strideC, batch};
+  GemmArgs g{M, N, K, alpha, beta, A, lda, strideA, B, ldb, strideB, C, ldc, strideC, batch, klim, nlim};
   cudaStream_t st = (cudaStream_t)stream;
   if (!transA && !transB) return dispatch_vec<false, false>(g, st);
   if (!transA && transB) return dispatch_vec<false, true>(g, st);
   if (transA && !transB) return dispatch_vec<true, false>(g, st);
   return dispatch_vec<true, true>(g, st);
+}
+
+extern "C" int wt_gemm_f64(int transA, int transB, int64_t M, int64_t N, int64_t K, double alpha,
+                           const double* A, int64_t lda, int64_t strideA, const double* B,
+                           int64_t ldb, int64_t strideB, double beta, double* C, int64_t ldc,
+                           int64_t strideC, int64_t batch, void* stream) {
+  return gemm_f64_lim(transA, transB, M, N, K, alpha, A, lda, strideA, B, ldb, strideB, beta, C,
+                      ldc, strideC, batch, nullptr, nullptr, stream);
 }

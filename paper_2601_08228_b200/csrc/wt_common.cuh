@@ -15,6 +15,14 @@ namespace wt {
 void set_error(const char* fmt, ...);
 int check_launch(const char* what);
 
+// K3 with per-matrix limits (device arrays, nullable): the inner dimension of
+// matrix b is min(K, klim[b]) (operands beyond it read as zeros) and output
+// column tiles starting at or beyond nlim[b] are skipped (not written).
+int gemm_f64_lim(int transA, int transB, int64_t M, int64_t N, int64_t K, double alpha,
+                 const double* A, int64_t lda, int64_t strideA, const double* B, int64_t ldb,
+                 int64_t strideB, double beta, double* C, int64_t ldc, int64_t strideC,
+                 int64_t batch, const int* klim, const int* nlim, void* stream);
+
 #define WT_REQUIRE(cond, ...)        \
   do {                               \
     if (!(cond)) {                   \

@@ -412,9 +412,12 @@ def pinv_blocks(a: torch.Tensor, sigma: torch.Tensor, vec: torch.Tensor, tol: fl
     if out is None:
         out = torch.empty((batch, n2, n1), dtype=F64, device=a.device)
     assert out.stride(2) == 1
-    N.check(lib.wt_pinv_from_svd_f64(_ptr(a), a.stride(1), a.stride(0), n1, n2, batch, _ptr(sigma),
-                                     _ptr(vec), float(tol), _ptr(out), out.stride(1), out.stride(0),
-                                     _ptr(t), _stream()), "wt_pinv_from_svd_f64")
+    rank = torch.empty((batch,), dtype=torch.int32, device=a.device)
+    # GEMMs limited per slice to the kept singular values (zero slices cost nothing)
+    N.check(lib.wt_pinv_from_svd_ranked_f64(_ptr(a), a.stride(1), a.stride(0), n1, n2, batch,
+                                            _ptr(sigma), _ptr(vec), float(tol), _ptr(out), out.stride(1),
+                                            out.stride(0), _ptr(t), _ptr(rank), _stream()),
+            "wt_pinv_from_svd_ranked_f64")
     return out
 
 

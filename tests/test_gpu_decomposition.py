@@ -180,3 +180,37 @@ def test_batches_above_grid_limit():
     np.testing.assert_allclose(pinv, np.linalg.pinv(a), rtol=0, atol=1e-10)
     rec = E.truncated_recon(at, sigma, vec, 2).cpu().numpy()
     np.testing.assert_allclose(rec, a, rtol=0, atol=1e-12)
+
+
+@pytest.mark.parametrize("n1,n2", [(40, 24), (24, 40), (33, 33)])
+def test_ranked_pinv_matches_full_and_oracle(n1, n2):
+    """K7 with per-slice rank limits (wt_pinv_from_svd_ranked_f64, used by pinv_blocks):
+    zero slices, rank-deficient slices and tol cutoffs give the same bits as the
+    full-width assembly (wt_pinv_from_svd_f64) and match the oracle's _pinv_stack."""
+    from paper_2601_08228_b200 import _native as N
+
+    rng = np.random.default_rng(5)
+    k = 9
+    a = rng.standard_normal((k, n1, n2))
+    a[1] = 0.0                                                    # all-zero slice: rank 0
+    a[2] = np.outer(rng.standard_normal(n1), rng.standard_normal(n2))  # rank 1
+    q = min(n1, n2)
+    u = np.linalg.qr(rng.standard_normal((n1, q)))[0]
+    v = np.linalg.qr(rng.standard_normal((n2, q)))[0]
+    a[3] = (u * np.logspace(0, -6, q)) @ v.T                      # graded: cutoff inside
+    ad = torch.from_numpy(a).cuda()
+    for tol in (1e-12, 1e-3):
+        sigma, vec, info = E.svd(ad, q)
+        E.raise_if_failed(info)
+        got = E.pinv_blocks(ad, sigma, vec, tol).cpu().numpy()
+        full = torch.empty((k, n2, n1), dtype=torch.float64, device="cuda")
+        t = torch.empty((k, q, q), dtype=torch.float64, device="cuda")
+        lib = N.require_gpu()
+        N.check(lib.wt_pinv_from_svd_f64(ad.data_ptr(), n2, n1 * n2, n1, n2, k, sigma.data_ptr(),
+                                         vec.data_ptr(), tol, full.data_ptr(), n1, n1 * n2,
+                                         t.data_ptr(), torch.cuda.current_stream().cuda_stream),
+                "wt_pinv_from_svd_f64")
+        assert np.array_equal(got, full.cpu().numpy())
+        assert not got[1].any()
+        want = np.stack([O.pinv_stack(a[i][:, :, None], tol)[:, :, 0] for i in range(k)])
+        assert relerr(got, want) < 1e-8
