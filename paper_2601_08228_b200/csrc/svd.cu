@@ -121,6 +121,17 @@ struct PairSmem {
   long long ts[2];  // WT_SVD_PROFILE: end of the Gram stream, end of the reduction
 };
 
+// Squared column norms of the panel (the Gram's diagonal; after the eigen
+// steps, that of the rotated panel) into ws.sig: the between-sweep reordering
+// sorts by them instead of re-reading every matrix.  The last visit of a block
+// in a sweep writes last (visits of a block are ordered by the block counters).
+__device__ __forceinline__ void store_norms(const double* G, double* cn, int colI, int colJ) {
+  if (threadIdx.x < BW) {
+    const int c = threadIdx.x;
+    cn[c < HB ? colI + c : colJ + c - HB] = G[c * LDG + c];
+  }
+}
+
 __device__ __forceinline__ void load_chunk(double* Zs, const double* Xb, int64_t mpad, int colI,
                                            int colJ, int64_t r0) {
   // 32 columns x RCH rows, 16-byte cp.async; column c of the panel maps to
@@ -303,9 +314,11 @@ __device__ __forceinline__ void pair_visit(PairSmem& S, const SvdWs& ws, int b, 
   for (int w = 0; w < kThreads / 32; ++w) off = nanmax(off, S.warp_off[w]);
   // NaN-propagating max through the bit pattern (non-negative doubles order as uint64)
   if (tid == 0) atomicMax(&ws.offmax[b], (unsigned long long)__double_as_longlong(off));
-  if (!(off >= tol)) return;  // converged pair (or NaN: recorded above, stop touching data)
+  if (!(off >= tol) || isinf(off)) {  // converged pair (or NaN / inf: recorded above)
+    store_norms(S.G[0], ws.sig + (int64_t)b * npad, colI, colJ);
+    return;
+  }
   if (tid == 0) atomicAdd(ws.pending + 1, 1);  // rotated-pair counter (diagnostics)
-  if (isinf(off)) return;
 
   const long long t_gram = clock64();
   // ---------------- 3. eigen-decomposition of G (cyclic parallel Jacobi) ----
@@ -414,6 +427,7 @@ __device__ __forceinline__ void pair_visit(PairSmem& S, const SvdWs& ws, int b, 
     }
   }
   __syncthreads();
+  store_norms(S.G[0], ws.sig + (int64_t)b * npad, colI, colJ);  // rotated Gram's diagonal
   const long long t_eig = clock64();
   // ---------------- 4. Z <- Z Q, streamed, written back in place -----------
   // warp w: chunk rows rt*16 .. rt*16+15 (two 8-row tiles) x output n-tiles
@@ -561,7 +575,8 @@ __global__ void svd_end_sweep(SvdWs ws, int batch, double tol) {
 // ------------------------------------------------------------- finalize ----
 // One CTA per matrix: column norms, descending sort (ties by index), sigma out.
 __global__ void svd_norms_sort(SvdWs ws, int64_t mpad, int64_t npad, int64_t n, int npow2,
-                               double* __restrict__ sigma, int* __restrict__ info, int max_sweeps_hit) {
+                               double* __restrict__ sigma, int* __restrict__ info, int max_sweeps_hit,
+                               int use_cn = 0) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double* key = reinterpret_cast<double*>(smem_raw);
   int* idx = reinterpret_cast<int*>(key + npow2);
@@ -569,6 +584,12 @@ __global__ void svd_norms_sort(SvdWs ws, int64_t mpad, int64_t npad, int64_t n, 
   if (sigma == nullptr && ws.conv[b]) return;  // reordering: converged matrices stay put
   const double* Xb = mat_ptr(ws, b, npad, mpad);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  if (sigma == nullptr && use_cn) {  // reordering from the norms the last visits left in ws.sig
+    for (int c = threadIdx.x; c < npow2; c += blockDim.x) {
+      key[c] = c < n ? ws.sig[(int64_t)b * npad + c] : -1.0;  // squared norms: same order
+      idx[c] = c;
+    }
+  } else
   for (int c = warp; c < npow2; c += nw) {
     double s = 0.0;
     if (c < n) {
@@ -817,6 +838,10 @@ extern "C" int wt_svd_jacobi_f64(const double* A, int64_t lda, int64_t strideA, 
   // Reorder the columns by descending norm before every sweep: measured on the
   // config-3/4 slices 13 -> 12 and 17 -> 16 sweeps, -10% time (round 1).
   int sort_mode = 2;
+  // From sweep 1 on, sort by the column norms the visits leave behind (no
+  // pass over the matrices); WT_SVD_VISIT_NORMS=0 recomputes them.
+  int visit_norms = 1;
+  if (const char* e = getenv("WT_SVD_VISIT_NORMS")) visit_norms = atoi(e);
   if (const char* e = getenv("WT_SVD_SORT")) sort_mode = atoi(e);
   const size_t sort_smem = (size_t)npow2 * (sizeof(double) + sizeof(int));
   if (int e = ensure_smem(svd_norms_sort, 8192 * (sizeof(double) + sizeof(int)))) return e;
@@ -824,7 +849,8 @@ extern "C" int wt_svd_jacobi_f64(const double* A, int64_t lda, int64_t strideA, 
     if (sort_mode == 2 || (sort_mode == 1 && sweep == 0)) {
       // columns in descending norm order before the sweep (de Rijk-style)
       svd_norms_sort<<<(unsigned)n_active, 512, sort_smem, st>>>(ws, L.mpad, L.npad, L.n, npow2,
-                                                              nullptr, nullptr, 0);
+                                                              nullptr, nullptr, 0,
+                                                              sweep > 0 && visit_norms ? 1 : 0);
       svd_permute_cols<<<dim3((unsigned)L.npad, (unsigned)n_active), 128, 0, st>>>(ws, L.mpad, L.npad);
       svd_flip<<<(unsigned)((batch + 255) / 256), 256, 0, st>>>(ws, (int)batch);
       if (int e = check_launch("svd reorder")) return e;
