@@ -101,7 +101,7 @@ extern "C" int wt_pinv_from_svd_ranked_f64(const double* A, int64_t lda, int64_t
     st = wt::gemm_f64_lim(0, 1, n1, q, n2, 1.0, A, lda, strideA, vec, ln, sV, 0.0, T, q, sT, batch,
                           nullptr, rank_ws, stream);
     if (st) return st;
-    st = wt_scale_cols_f64(T, n1, q, q, sT, sigma, q, batch, WT_SCALE_PINV2, tol, stream);
+    st = wt::scale_cols_lim(T, n1, q, q, sT, sigma, q, batch, WT_SCALE_PINV2, tol, rank_ws, stream);
     if (st) return st;
     return wt::gemm_f64_lim(1, 1, n2, n1, q, 1.0, vec, ln, sV, T, q, sT, 0.0, out, ldo, strideO,
                             batch, rank_ws, nullptr, stream);
@@ -110,7 +110,7 @@ extern "C" int wt_pinv_from_svd_ranked_f64(const double* A, int64_t lda, int64_t
   st = wt::gemm_f64_lim(1, 1, n2, q, n1, 1.0, A, lda, strideA, vec, ln, sV, 0.0, T, q, sT, batch,
                         nullptr, rank_ws, stream);
   if (st) return st;
-  st = wt_scale_cols_f64(T, n2, q, q, sT, sigma, q, batch, WT_SCALE_PINV2, tol, stream);
+  st = wt::scale_cols_lim(T, n2, q, q, sT, sigma, q, batch, WT_SCALE_PINV2, tol, rank_ws, stream);
   if (st) return st;
   return wt::gemm_f64_lim(0, 0, n2, n1, q, 1.0, T, q, sT, vec, ln, sV, 0.0, out, ldo, strideO, batch,
                           rank_ws, nullptr, stream);

@@ -627,6 +627,9 @@ __global__ void svd_norms_sort(SvdWs ws, int64_t mpad, int64_t npad, int64_t n, 
     }
   }
   if (sigma == nullptr) {  // reordering pass between sweeps: permutation only
+    // an all-zero matrix (largest norm exactly 0, e.g. the detail slices of a
+    // slice-constant operator) is already diagonal: retire it before any visit
+    if (threadIdx.x == 0 && key[0] == 0.0) ws.conv[b] = 1;
     for (int i = threadIdx.x; i < npad; i += blockDim.x) ws.perm[(int64_t)b * npad + i] = idx[i];
     return;
   }

@@ -10,16 +10,19 @@
 namespace wt {
 namespace {
 
+// CTA (x, b): rows x, x + gridDim.x, ... of matrix b; threads own columns, so
+// each thread forms its column factors once (no per-element index division)
+// and every row access is coalesced.  clim (nullable): columns >= clim[b] are
+// left untouched (the ranked pseudo-inverse never reads them).
 __global__ void scale_cols_kernel(double* __restrict__ M, int64_t rows, int64_t ncols, int64_t ld,
                                   int64_t sM, const double* __restrict__ s, int64_t q, int mode,
-                                  double tol) {
+                                  double tol, const int* __restrict__ clim) {
   const int64_t b = blockIdx.y;
-  const int64_t total = rows * ncols;
+  const int64_t nc = clim ? std::min<int64_t>(ncols, std::max(clim[b], 0)) : ncols;
   const double* sb = s + b * q;
   const double smax = sb[0];
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t i = e / ncols, j = e - i * ncols;
+  double* Mb = M + b * sM;
+  for (int64_t j = threadIdx.x; j < nc; j += blockDim.x) {
     const double sv = sb[j];
     double f;
     if (mode == WT_SCALE_MUL) {
@@ -30,8 +33,7 @@ __global__ void scale_cols_kernel(double* __restrict__ M, int64_t rows, int64_t 
       const double inv = (sv > tol * smax && sv > 0.0) ? 1.0 / sv : 0.0;
       f = inv * inv;
     }
-    double* p = M + b * sM + i * ld + j;
-    *p = *p * f;
+    for (int64_t i = blockIdx.x; i < rows; i += gridDim.x) Mb[i * ld + j] *= f;
   }
 }
 
@@ -111,21 +113,30 @@ __global__ void band_reduce_final(const double* __restrict__ part, int64_t npart
 
 using namespace wt;
 
-extern "C" int wt_scale_cols_f64(double* M, int64_t rows, int64_t ncols, int64_t ld,
-                                 int64_t strideM, const double* s, int64_t q, int64_t batch,
-                                 int mode, double tol, void* stream) {
+int wt::scale_cols_lim(double* M, int64_t rows, int64_t ncols, int64_t ld, int64_t strideM,
+                       const double* s, int64_t q, int64_t batch, int mode, double tol,
+                       const int* clim, void* stream) {
   WT_REQUIRE(rows >= 0 && ncols >= 0 && batch >= 0 && ncols <= q && ld >= ncols,
              "scale_cols: bad arguments");
   WT_REQUIRE(mode >= WT_SCALE_MUL && mode <= WT_SCALE_PINV2, "scale_cols: bad mode %d", mode);
   if (rows == 0 || ncols == 0 || batch == 0) return WT_OK;
-  const int64_t total = rows * ncols;
+  const int threads = ncols >= 256 ? 256 : (int)((ncols + 31) / 32 * 32);
+  // enough CTAs to cover the GPU several times over, each streaming a few rows
+  const int64_t want = std::max<int64_t>(1, 8 * num_sms() / std::max<int64_t>(batch, 1));
+  const unsigned gx = (unsigned)std::min<int64_t>(rows, want);
   for (int64_t b0 = 0; b0 < batch; b0 += 65535) {  // grid.y limit
     const int64_t nb = std::min<int64_t>(65535, batch - b0);
-    dim3 grid((unsigned)std::min<int64_t>((total + 255) / 256, 2048), (unsigned)nb);
-    scale_cols_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(M + b0 * strideM, rows, ncols, ld,
-                                                              strideM, s + b0 * q, q, mode, tol);
+    scale_cols_kernel<<<dim3(gx, (unsigned)nb), threads, 0, (cudaStream_t)stream>>>(
+        M + b0 * strideM, rows, ncols, ld, strideM, s + b0 * q, q, mode, tol,
+        clim ? clim + b0 : nullptr);
   }
   return check_launch("wt_scale_cols_f64");
+}
+
+extern "C" int wt_scale_cols_f64(double* M, int64_t rows, int64_t ncols, int64_t ld,
+                                 int64_t strideM, const double* s, int64_t q, int64_t batch,
+                                 int mode, double tol, void* stream) {
+  return scale_cols_lim(M, rows, ncols, ld, strideM, s, q, batch, mode, tol, nullptr, stream);
 }
 
 extern "C" int wt_copy2d_f64(const double* src, int64_t lds, int64_t strideS, double* dst,

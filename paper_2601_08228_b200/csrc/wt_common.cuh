@@ -22,6 +22,10 @@ int gemm_f64_lim(int transA, int transB, int64_t M, int64_t N, int64_t K, double
                  const double* A, int64_t lda, int64_t strideA, const double* B, int64_t ldb,
                  int64_t strideB, double beta, double* C, int64_t ldc, int64_t strideC,
                  int64_t batch, const int* klim, const int* nlim, void* stream);
+// wt_scale_cols_f64 with an optional per-matrix column limit (columns >= clim[b] untouched).
+int scale_cols_lim(double* M, int64_t rows, int64_t ncols, int64_t ld, int64_t strideM,
+                   const double* s, int64_t q, int64_t batch, int mode, double tol,
+                   const int* clim, void* stream);
 
 #define WT_REQUIRE(cond, ...)        \
   do {                               \
