@@ -270,7 +270,7 @@ def transform_workload(args, dist, rank, ws):
     x_pin = torch.from_numpy(x_host).pin_memory()
     y_pin = torch.empty_like(x_pin).pin_memory()
     s_in, s_cmp, s_out = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
-    chunks = 8
+    chunks = int(os.environ.get("WT_E2E_CHUNKS", "8"))  # row chunks per L (pipeline fill/drain ~1/chunks)
     rows = n1 // chunks
 
     def e2e_step(record):
@@ -298,7 +298,7 @@ def transform_workload(args, dist, rank, ws):
     e2e = {"value": round(ws * bytes_step * e2e_steps / (e2e_ms * 1e-3) / 1e9, 3), "unit": "GB/s",
            "h2d_bytes_per_step": len(CFG2_LEVELS) * 8 * N,
            "d2h_bytes_per_step": len(CFG2_LEVELS) * 8 * N,
-           "api": "y = inverse_w(forward_w(x_cuda, L)) per L on 8 row chunks; x H2D from pinned, "
+           "api": f"y = inverse_w(forward_w(x_cuda, L)) per L on {chunks} row chunks; x H2D from pinned, "
                   "y D2H to pinned, copies overlapped with the transform on 3 streams",
            "steps": e2e_steps}
     # the numpy drop-in path (reference call shapes: host arrays in, host pyramid out/in)
