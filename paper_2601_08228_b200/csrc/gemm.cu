@@ -168,13 +168,17 @@ __global__ void __launch_bounds__(WM* WN * 32) gemm_f64_kernel(GemmArgs g) {
           if (TB) bf[j] = *reinterpret_cast<const double2*>(Bs + nn * SL::B_LD + kk);
           else bf[j] = make_double2(Bs[kk * SL::B_LD + nn], Bs[(kk + 1) * SL::B_LD + nn]);
         }
+        // all even-k products first, then all odd-k ones: the two DMMAs that
+        // accumulate into one tile are FM*FN instructions apart instead of
+        // back to back (ncu: the dependent second DMMA was the top stall)
 #pragma unroll
         for (int i = 0; i < FM; ++i)
 #pragma unroll
-          for (int j = 0; j < FN; ++j) {
-            dmma884(acc[i][j][0], acc[i][j][1], af[i].x, bf[j].x);
-            dmma884(acc[i][j][0], acc[i][j][1], af[i].y, bf[j].y);
-          }
+          for (int j = 0; j < FN; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[i].x, bf[j].x);
+#pragma unroll
+        for (int i = 0; i < FM; ++i)
+#pragma unroll
+          for (int j = 0; j < FN; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[i].y, bf[j].y);
       }
     }
     cp_async_wait<0>();
@@ -231,8 +235,18 @@ int launch_cfg(const GemmArgs& g, cudaStream_t st) {
 template <bool TA, bool TB, int VEC>
 int dispatch_tile(const GemmArgs& g, cudaStream_t st) {
   const int64_t big_tiles = ((g.M + 127) / 128) * ((g.N + 127) / 128) * g.batch;
+#ifndef WT_GEMM_BIG
+#define WT_GEMM_BIG 1
+#endif
+#if WT_GEMM_BIG == 1
+  // 128 x 64 CTA tiles of 4 warps (64 x 32 warp tiles), two CTAs per SM: one
+  // CTA's k-tile barrier overlaps the other's DMMA stream
+  if (g.M >= 128 && g.N >= 64 && big_tiles >= num_sms())
+    return launch_cfg<128, 64, 2, 2, TA, TB, VEC>(g, st);
+#else
   if (g.M >= 128 && g.N >= 128 && big_tiles >= num_sms())
     return launch_cfg<128, 128, 2, 4, TA, TB, VEC>(g, st);
+#endif
   if (g.M >= 64 && g.N >= 64) return launch_cfg<64, 64, 2, 2, TA, TB, VEC>(g, st);
   return launch_cfg<32, 32, 2, 2, TA, TB, VEC>(g, st);
 }
