@@ -243,7 +243,10 @@ int dispatch_tile(const GemmArgs& g, cudaStream_t st) {
   // CTA's k-tile barrier overlaps the other's DMMA stream
   if (g.M >= 128 && g.N >= 64 && big_tiles >= num_sms())
     return launch_cfg<128, 64, 2, 2, TA, TB, VEC>(g, st);
-#else
+#elif WT_GEMM_BIG == 2
+  if (g.M >= 64 && g.N >= 128 && big_tiles >= num_sms())
+    return launch_cfg<64, 128, 2, 2, TA, TB, VEC>(g, st);
+#elif WT_GEMM_BIG == 0
   if (g.M >= 128 && g.N >= 128 && big_tiles >= num_sms())
     return launch_cfg<128, 128, 2, 4, TA, TB, VEC>(g, st);
 #endif

@@ -337,6 +337,27 @@ __global__ void __launch_bounds__(kT) fwd_shallow(const double* __restrict__ x,
 // [d1 | ... | dL | sL] with the tile's CT bands in place of p.
 __device__ __forceinline__ int drow(int CT, int j) { return CT - (CT >> (j - 1)); }
 
+// s_hi[c] of tube r from s_L and the D = L - hi details on c's ancestor chain
+// (loads first, then the dependent unlift chain; same roundings as level by level).
+template <int TQ, int D>
+__device__ __forceinline__ double path_chain(const double* __restrict__ I, int CT, int L, int hi,
+                                             int c, int r, uint64_t mask, bool have_s, int srow) {
+  double d[D];
+#pragma unroll
+  for (int u = 0; u < D; ++u) {
+    const int j = L - u;
+    d[u] = ((mask >> j) & 1) ? I[(drow(CT, j) + (c >> (j - hi))) * TQ + r] : 0.0;
+  }
+  double sv = have_s ? I[(srow + (c >> (L - hi))) * TQ + r] : 0.0;
+#pragma unroll
+  for (int u = 0; u < D; ++u) {
+    const int j = L - u;
+    const double x1 = __dsub_rn(sv, __dmul_rn(d[u], 0.5));
+    sv = ((c >> (j - hi - 1)) & 1) ? x1 : __dadd_rn(d[u], x1);
+  }
+  return sv;
+}
+
 // Levels hi .. hi-W+1: each thread expands one s_hi value into 2^W values of
 // s_{hi-W} using the prefetched details; the final stage (down to level 1)
 // stores the 2^W consecutive bands straight to y.
@@ -360,15 +381,28 @@ __device__ __forceinline__ void inv_stage(const double* __restrict__ I,
     if (path) {
       // s_hi[c] straight from s_L along c's ancestor chain (levels L .. hi+1):
       // the same two roundings per level as the level-by-level inverse, no
-      // stage barriers (lifting.py:69-74)
-      double sv = have_s ? I[(srow + (c >> (g.L - hi))) * TQ + r] : 0.0;
-      for (int j = g.L; j > hi; --j) {
-        const int k = c >> (j - hi);
-        const double d = ((g.mask >> j) & 1) ? I[(drow(CT, j) + k) * TQ + r] : 0.0;
-        const double x1 = __dsub_rn(sv, __dmul_rn(d, 0.5));
-        sv = ((c >> (j - hi - 1)) & 1) ? x1 : __dadd_rn(d, x1);
+      // stage barriers (lifting.py:69-74).  Depths are compile-time so every
+      // detail load of the chain is issued before the dependent arithmetic
+      // (ncu: the rolled loop waited on each shared load in turn).
+      switch (g.L - hi) {
+        case 4: v[0] = path_chain<TQ, 4>(I, CT, g.L, hi, c, r, g.mask, have_s, srow); break;
+        case 5: v[0] = path_chain<TQ, 5>(I, CT, g.L, hi, c, r, g.mask, have_s, srow); break;
+        case 6: v[0] = path_chain<TQ, 6>(I, CT, g.L, hi, c, r, g.mask, have_s, srow); break;
+        case 7: v[0] = path_chain<TQ, 7>(I, CT, g.L, hi, c, r, g.mask, have_s, srow); break;
+        case 8: v[0] = path_chain<TQ, 8>(I, CT, g.L, hi, c, r, g.mask, have_s, srow); break;
+        case 9: v[0] = path_chain<TQ, 9>(I, CT, g.L, hi, c, r, g.mask, have_s, srow); break;
+        case 10: v[0] = path_chain<TQ, 10>(I, CT, g.L, hi, c, r, g.mask, have_s, srow); break;
+        default: {
+          double sv = have_s ? I[(srow + (c >> (g.L - hi))) * TQ + r] : 0.0;
+          for (int j = g.L; j > hi; --j) {
+            const int k = c >> (j - hi);
+            const double d = ((g.mask >> j) & 1) ? I[(drow(CT, j) + k) * TQ + r] : 0.0;
+            const double x1 = __dsub_rn(sv, __dmul_rn(d, 0.5));
+            sv = ((c >> (j - hi - 1)) & 1) ? x1 : __dadd_rn(d, x1);
+          }
+          v[0] = sv;
+        }
       }
-      v[0] = sv;
     } else {
       v[0] = s_in ? (have_s ? I[(srow + c) * TQ + r] : 0.0) : ssrc[r * pss + c];
     }
