@@ -46,6 +46,7 @@ constexpr int LDG = BW + 1;  // Gram / Q pitch
 static_assert(kWarps == 4 || kWarps == 8, "K4 CTA shape: 4 or 8 warps");
 constexpr double kFloorEps = 1e3 * 2.220446049250313e-16;  // null-column floor (see the test)
 constexpr int kMaxInnerSweeps = 16;
+constexpr int kSkipMaxBlocks = 128;  // pair-skip records: nblk^2 per matrix (<= 2048 columns)
 #ifndef WT_SVD_MINB
 #define WT_SVD_MINB 3
 #endif
@@ -78,6 +79,8 @@ struct SvdWs {
   int* perm;        // batch * npad
   int* bdone;       // batch * nblk: rounds of the current sweep finished per column block
   int* ticket;      // 1 counter: next visit of the current sweep (persistent sweeps)
+  int* bver;        // batch * nblk: version of every column block (bumped when its data changes)
+  unsigned long long* pclean;  // batch * nblk * nblk: (ver_I, ver_J) when pair (I, J) last tested clean
 };
 
 __host__ __device__ inline int64_t round_up(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
@@ -117,6 +120,7 @@ struct PairSmem {
   double warp_off[kThreads / 32];
   double gmax;
   int any_rot;
+  int skip;
   unsigned long long gmax_bits;
   long long ts[2];  // WT_SVD_PROFILE: end of the Gram stream, end of the reduction
 };
@@ -153,6 +157,20 @@ __device__ __forceinline__ void pair_visit(PairSmem& S, const SvdWs& ws, int b, 
   const int colI = I * HB, colJ = J * HB;
   double* Xb = mat_ptr(ws, b, npad, mpad);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // A pair found clean whose two blocks have not changed since (same data, or
+  // the same column sets after a reordering) is still clean: skip the visit
+  // without touching the panel (the late sweeps are mostly such visits).
+  const int nbk = (int)(npad / HB);
+  if (ws.pclean) {
+    if (tid == 0) {
+      const unsigned long long cur =
+          ((unsigned long long)(unsigned)__ldcg(ws.bver + (int64_t)b * nbk + I) << 32) |
+          (unsigned)__ldcg(ws.bver + (int64_t)b * nbk + J);
+      S.skip = __ldcg(ws.pclean + ((int64_t)b * nbk + I) * nbk + J) == cur;
+    }
+    __syncthreads();
+    if (S.skip) return;
+  }
   const int nch = (int)(mpad / RCH);
 
   const long long t_start = clock64();
@@ -316,6 +334,10 @@ __device__ __forceinline__ void pair_visit(PairSmem& S, const SvdWs& ws, int b, 
   if (tid == 0) atomicMax(&ws.offmax[b], (unsigned long long)__double_as_longlong(off));
   if (!(off >= tol) || isinf(off)) {  // converged pair (or NaN / inf: recorded above)
     store_norms(S.G[0], ws.sig + (int64_t)b * npad, colI, colJ);
+    if (ws.pclean && tid == 0 && off < tol)  // certified clean at the blocks' current versions
+      __stcg(ws.pclean + ((int64_t)b * nbk + I) * nbk + J,
+             ((unsigned long long)(unsigned)__ldcg(ws.bver + (int64_t)b * nbk + I) << 32) |
+                 (unsigned)__ldcg(ws.bver + (int64_t)b * nbk + J));
     return;
   }
   if (tid == 0) atomicAdd(ws.pending + 1, 1);  // rotated-pair counter (diagnostics)
@@ -484,6 +506,10 @@ __device__ __forceinline__ void pair_visit(PairSmem& S, const SvdWs& ws, int b, 
       }
     __syncthreads();  // every warp has read the chunk before its buffer is refilled
   }
+  if (ws.pclean && tid == 0) {  // both blocks changed (the visit owns them exclusively)
+    __stcg(ws.bver + (int64_t)b * nbk + I, __ldcg(ws.bver + (int64_t)b * nbk + I) + 1);
+    __stcg(ws.bver + (int64_t)b * nbk + J, __ldcg(ws.bver + (int64_t)b * nbk + J) + 1);
+  }
   if (ws.prof && tid == 0) {
     atomicAdd(ws.prof + 0, (unsigned long long)(t_gram - t_start));
     atomicAdd(ws.prof + 1, (unsigned long long)(t_eig - t_gram));
@@ -601,7 +627,8 @@ __global__ void svd_norms_sort(SvdWs ws, int64_t mpad, int64_t npad, int64_t n, 
       for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
     }
     if (lane == 0) {
-      key[c] = c < n ? sqrt(s) : -1.0;
+      // the reordering pass sorts squared norms (the units the visits leave in ws.sig)
+      key[c] = c < n ? (sigma == nullptr ? s : sqrt(s)) : -1.0;
       idx[c] = c;
     }
   }
@@ -631,6 +658,16 @@ __global__ void svd_norms_sort(SvdWs ws, int64_t mpad, int64_t npad, int64_t n, 
     // slice-constant operator) is already diagonal: retire it before any visit
     if (threadIdx.x == 0 && key[0] == 0.0) ws.conv[b] = 1;
     for (int i = threadIdx.x; i < npad; i += blockDim.x) ws.perm[(int64_t)b * npad + i] = idx[i];
+    // the norms follow their columns (blocks skipped in the next sweep keep them valid)
+    for (int i = threadIdx.x; i < n; i += blockDim.x) ws.sig[(int64_t)b * npad + i] = key[i];
+    if (ws.bver) {  // a block whose column set changed has new data
+      const int nbk = (int)(npad / HB);
+      for (int B = threadIdx.x; B < nbk; B += blockDim.x) {
+        bool moved = false;
+        for (int i = B * HB; i < (B + 1) * HB; ++i) moved |= (idx[i] / HB) != B;
+        if (moved) ws.bver[(int64_t)b * nbk + B] += 1;
+      }
+    }
     return;
   }
   bool bad = false;
@@ -686,7 +723,8 @@ __global__ void svd_flip(SvdWs ws, int batch) {
 struct WsLayout {
   int64_t m, n, mpad, npad;
   size_t off_X, off_X2, off_xsel, off_active, off_off, off_conv, off_pending, off_sig, off_perm, off_bdone,
-      total;
+      off_bver, off_pclean, total;
+  bool skip;  // pair-skip bookkeeping (nblk <= kSkipMaxBlocks)
 };
 
 WsLayout ws_layout(int64_t n1, int64_t n2, int64_t batch) {
@@ -707,6 +745,10 @@ WsLayout ws_layout(int64_t n1, int64_t n2, int64_t batch) {
   L.off_sig = take(sizeof(double) * (size_t)(batch * L.npad));
   L.off_perm = take(sizeof(int) * (size_t)(batch * L.npad));
   L.off_bdone = take(sizeof(int) * (size_t)(batch * (L.npad / HB)));
+  const int64_t nbk = L.npad / HB;
+  L.skip = nbk <= kSkipMaxBlocks;
+  L.off_bver = take(L.skip ? sizeof(int) * (size_t)(batch * nbk) : 0);
+  L.off_pclean = take(L.skip ? sizeof(unsigned long long) * (size_t)(batch * nbk * nbk) : 0);
   L.total = o;
   return L;
 }
@@ -778,7 +820,18 @@ extern "C" int wt_svd_jacobi_f64(const double* A, int64_t lda, int64_t strideA, 
            reinterpret_cast<unsigned long long*>(base + L.off_off),
            reinterpret_cast<int*>(base + L.off_conv), reinterpret_cast<int*>(base + L.off_pending),
            reinterpret_cast<double*>(base + L.off_sig), reinterpret_cast<int*>(base + L.off_perm),
-           reinterpret_cast<int*>(base + L.off_bdone), reinterpret_cast<int*>(base + L.off_pending) + 2};
+           reinterpret_cast<int*>(base + L.off_bdone), reinterpret_cast<int*>(base + L.off_pending) + 2,
+           nullptr, nullptr};
+  int pair_skip = 1;
+  if (const char* e = getenv("WT_SVD_PAIR_SKIP")) pair_skip = atoi(e);
+  if (L.skip && pair_skip) {
+    ws.bver = reinterpret_cast<int*>(base + L.off_bver);
+    ws.pclean = reinterpret_cast<unsigned long long*>(base + L.off_pclean);
+    const int64_t nbk = L.npad / HB;
+    WT_CUDA(cudaMemsetAsync(ws.bver, 0, sizeof(int) * (size_t)(batch * nbk), (cudaStream_t)stream));
+    WT_CUDA(cudaMemsetAsync(ws.pclean, 0xff, sizeof(unsigned long long) * (size_t)(batch * nbk * nbk),
+                            (cudaStream_t)stream));
+  }
   if (tol <= 0.0) tol = 4.0 * 2.220446049250313e-16 * sqrt((double)L.m) + 1e-15;
   if (max_sweeps <= 0) max_sweeps = 40;
   const bool right = n1 <= n2;
