@@ -1,6 +1,11 @@
 """CPU emulation: sweeps of cyclic one-sided Jacobi (de Rijk sorting) on config-3/4 wavelet
 slices, plain vs preconditioned by V0 = eigenvectors of the Gram (f64 / f32) -- the numbers
 behind DESIGN.md section 8 item 1.  usage: python tools/jacobi_precond_probe.py 3|4"""
+import os
+import sys
+
+import numpy as np
+
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2601_08228_b200 import synth
 from oracle import wten_oracle as O
