@@ -139,6 +139,23 @@ def test_determinism():
     assert torch.equal(r1, r2)
 
 
+@pytest.mark.parametrize("knob", ["WT_SVD_PERSIST", "WT_SVD_PAIR_SKIP"])
+def test_scheduling_knobs_do_not_change_bits(monkeypatch, knob):
+    """K4's persistent dependency-scheduled sweeps and the clean-pair skip only
+    change WHEN visits run or drop visits that rotate nothing: sigma and vectors
+    are bit-identical with either switched off (one launch per round / every
+    pair re-tested).  256 columns: cross-only rounds and 16 blocks."""
+    a = torch.from_numpy(np.random.default_rng(29).standard_normal((6, 300, 256))).cuda()
+    outs = []
+    for v in ("1", "0"):
+        monkeypatch.setenv(knob, v)
+        sigma, vec, info = E.svd(a, 256)
+        E.raise_if_failed(info)
+        outs.append((sigma.clone(), vec.clone(), E.last_sweeps()))
+    assert torch.equal(outs[0][0], outs[1][0]) and torch.equal(outs[0][1], outs[1][1])
+    assert outs[0][2] == outs[1][2]
+
+
 def test_concurrent_host_threads_on_own_streams():
     """The API is pure (SPEC concurrency sections): host threads driving their own
     CUDA streams get the serial results bit for bit (per-thread host state in K4)."""
