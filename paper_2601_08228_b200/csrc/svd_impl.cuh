@@ -267,10 +267,22 @@ __device__ __forceinline__ void pair_visit(PairSmem& S, const SvdWs& ws, int b, 
     // no sqrt and no division per pair (the test was ~10% of the kernel's stall samples)
     const double rfl = 1.0 / (floor_c * gmax);
     double mx = 0.0;
+    auto test_pair = [&](int i, int j) {
+      const double gii = S.G[0][i * LDG + i], gjj = S.G[0][j * LDG + j];
+      const double gij = S.G[0][i * LDG + j];
+      double c = 0.0;
+      if (gij != 0.0) c = fabs(gij) * fmin(rsqrt(gii * gjj), rfl);
+      if (isnan(gii) || isnan(gjj)) c = gii + gjj;
+      mx = nanmax(mx, c);
+    };
+    if (cross_only && HB * HB == kThreads) {
+      // cross-only visits answer for the block I x block J pairs alone (the
+      // within-block pairs are tested and rotated at the sweep's round 0):
+      // exactly one pair per thread
+      test_pair(tid / HB, HB + tid % HB);
+    } else
     for (int e = tid; e < BW * BW; e += kThreads) {
       const int i = e / BW, j = e % BW;
-      // cross-only visits answer for the block I x block J pairs alone (the
-      // within-block pairs are tested and rotated at the sweep's round 0)
       if (i < j && !(cross_only && (i < HB) == (j < HB))) {
         const double gii = S.G[0][i * LDG + i], gjj = S.G[0][j * LDG + j];
         const double gij = S.G[0][i * LDG + j];
