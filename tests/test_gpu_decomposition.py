@@ -231,3 +231,16 @@ def test_ranked_pinv_matches_full_and_oracle(n1, n2):
         assert not got[1].any()
         want = np.stack([O.pinv_stack(a[i][:, :, None], tol)[:, :, 0] for i in range(k)])
         assert relerr(got, want) < 1e-8
+
+
+@pytest.mark.parametrize("n1,n2", [(2048, 2048), (700, 2100)])
+def test_large_slices_against_lapack(n1, n2):
+    """Large single slices: 128 column blocks (the largest with the clean-pair
+    records) and 2100 columns (132 blocks: records off), against LAPACK."""
+    rng = np.random.default_rng(31)
+    a = rng.standard_normal((1, n1, n2))
+    a[0, :, ::7] *= 1e-3                                   # a graded spectrum
+    sigma, vec, info = E.svd(torch.from_numpy(a).cuda(), 8)
+    E.raise_if_failed(info)
+    want = np.linalg.svd(a[0], compute_uv=False)[None]
+    assert sigma_err(sigma.cpu().numpy(), want) < TOL
