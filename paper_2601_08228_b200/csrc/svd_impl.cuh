@@ -804,7 +804,7 @@ int jacobi(const double* A, int64_t lda, int64_t strideA, int64_t n1,
   g_last_sweeps = 0;
   g_last_rotations = 0;
   int dbg_prev = 0;
-  static unsigned long long* d_prof = nullptr;
+  static thread_local unsigned long long* d_prof = nullptr;  // WT_SVD_PROFILE diagnostics
   const bool profile = getenv("WT_SVD_PROFILE") != nullptr;
   if (profile) {
     if (!d_prof) WT_CUDA(cudaMalloc(&d_prof, 8 * sizeof(unsigned long long)));

@@ -56,12 +56,12 @@ inline int ensure_smem(K kernel, size_t bytes) {
 constexpr int kNumSMs = 148;  // B200; queried at runtime where it matters
 
 inline int num_sms() {
-  static int n = 0;
-  if (n == 0) {
-    int dev = 0;
+  static const int n = [] {  // thread-safe one-time init (one GPU model per process)
+    int dev = 0, v = 0;
     cudaGetDevice(&dev);
-    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) n = kNumSMs;
-  }
+    return cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && v > 0 ? v
+                                                                                                : kNumSMs;
+  }();
   return n;
 }
 
