@@ -655,7 +655,7 @@ def main():
 
     if args.workloads == "default":
         wl = (["wsvd", "spwsvd", "deblur", "wproduct", "comparators"] if ws == 1
-              else ["spwsvd_fused", "spwsvd_sharded", "wsvd_fused", "wsvd_sharded"])
+              else ["spwsvd_fused", "spwsvd_sharded", "wsvd_fused", "wsvd_sharded", "wproduct_sharded"])
     elif args.workloads == "none":
         wl = []
     else:
@@ -717,6 +717,10 @@ def main():
 
                 workloads[name] = sharded.bench_sp_w_svd(dist, timed_region, steps=3, warmup=1,
                                                          fused=name == "spwsvd_fused")
+            elif name == "wproduct_sharded":  # config-5-sized w-product, rows sharded
+                from paper_2601_08228_b200 import sharded
+
+                workloads[name] = sharded.bench_w_product(dist, timed_region)
             elif name in ("wsvd_sharded", "wsvd_fused"):  # config 3, all p slices exchanged
                 from paper_2601_08228_b200 import sharded
 

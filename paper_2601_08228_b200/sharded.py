@@ -71,6 +71,11 @@ class CudaOps:
         E.raise_if_failed(info)
         return E.pinv_blocks(slices, sigma, vec, tol)
 
+    def gemm(self, a, b):
+        if a.shape[1] == 0:
+            return self.empty((a.shape[0], 0, b.shape[2]))
+        return E.gemm(a, b)
+
 
 def _a2a(out, inp, out_splits, in_splits, group):
     dist.all_to_all_single(out, inp, out_splits, in_splits, group=group)
@@ -181,6 +186,50 @@ def pinv_w_sharded(x_local, levels, n1, tol=1e-12, group=None, ops=None):
     out_rows = splits(n2, G)
     back = slices_to_rows(ops, inv, ks, out_rows, group)        # (p, n2_me, n1)
     return ops.inverse(back, out_rows[me], n1, p, levels, N.MASK_ALL, 0)
+
+
+def gather_rows(ops, local, rows, group):
+    """All ranks' row blocks (rank order) of a row-sharded (R_me, ...) tensor ->
+    the full (sum rows, ...) tensor on every rank (NCCL all-gather; uneven
+    splits are padded to the largest block)."""
+    G = dist.get_world_size(group)
+    R = max(rows)
+    tail = tuple(local.shape[1:])
+    pad = ops.empty((R,) + tail)
+    if local.shape[0]:
+        pad[:local.shape[0]].copy_(local)
+    allb = ops.empty((G * R,) + tail)
+    dist.all_gather_into_tensor(allb, pad, group=group)
+    full = ops.empty((sum(rows),) + tail)
+    r0 = 0
+    for g in range(G):
+        full[r0:r0 + rows[g]].copy_(allb[g * R:g * R + rows[g]])
+        r0 += rows[g]
+    return full
+
+
+def w_product_sharded(a_local, b_local, levels, n1, group=None, ops=None):
+    """w-product C = A *_w B with A (n1, n2, p) and B (n2, n3, p) both sharded by
+    rows (algebra.py:43-51).  The facewise product is row-separable in A, so C's
+    rows follow A's: every rank transforms its rows of A locally (no exchange),
+    all-gathers B (the small-right-operand layout of SURVEY.md section 8(e)),
+    runs K3 on its rows of every wavelet slice and inverts them locally.
+    Returns this rank's rows of C (the split of A's rows)."""
+    ops = ops or CudaOps()
+    G = dist.get_world_size(group)
+    me = dist.get_rank(group)
+    R, n2, p = a_local.shape
+    rows = splits(n1, G)
+    assert R == rows[me], f"rank {me} holds {R} rows of A, expected {rows[me]}"
+    brows = splits(n2, G)
+    assert b_local.shape[0] == brows[me] and b_local.shape[2] == p
+    _check_levels(p, levels)
+    n3 = b_local.shape[1]
+    b = gather_rows(ops, b_local, brows, group)                     # (n2, n3, p)
+    pa = ops.forward(a_local, levels, N.MASK_ALL, 0)                 # (p, R, n2)
+    pb = ops.forward(b, levels, N.MASK_ALL, 0)                       # (p, n2, n3)
+    pc = ops.gemm(pa, pb)                                            # (p, R, n3)
+    return ops.inverse(pc, R, n3, p, levels, N.MASK_ALL, 0)
 
 
 def peer_slice_table(ptrs, ks, row0, n1, n2, elem=8):
@@ -304,6 +353,29 @@ def pinv_w_fused(x_local, levels, n1, tol=1e-12, group=None):
         E.pinv_blocks(full, sigma, vec, tol, out=out)
 
     return _fused_exchange(x_local, levels, n1, N.MASK_ALL, 0, decompose, n2, n1, group)
+
+
+def bench_w_product(dist_mod, timed_region, steps=3, warmup=1, n=512, p=128, levels=3):
+    """Config-5-sized w-product (A, B: n x n x p) with both operands row-sharded
+    over the group (strong scaling; B all-gathered, no all-to-all)."""
+    G = dist_mod.get_world_size()
+    me = dist_mod.get_rank()
+    rows = splits(n, G)
+    r0 = sum(rows[:me])
+    gen = torch.Generator(device="cuda").manual_seed(5)
+    a = torch.rand((rows[me], n, p), dtype=torch.float64, device="cuda", generator=gen)
+    b = torch.rand((rows[me], n, p), dtype=torch.float64, device="cuda", generator=gen)
+    out = {}
+
+    def step(record):
+        out["c"] = w_product_sharded(a, b, levels, n)
+
+    ms = timed_region(step, steps, warmup, dist_mod)
+    flops = 2.0 * n * n * n * p
+    return {"config": f"w_product {n}x{n}x{p} * {n}x{n}x{p} L={levels}, rows of A and B sharded over "
+                      f"{G} GPUs, B all-gathered (NCCL)",
+            "metric": "TFLOP/s (facewise products)", "value": flops * steps / (ms * 1e-3) / 1e12,
+            "ms_per_call": ms / steps, "scaling": "strong", "row0": r0}
 
 
 def bench_sp_w_svd(dist_mod, timed_region, steps=3, warmup=1, shape=(1024, 1024, 256), r=30,

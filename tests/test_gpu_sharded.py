@@ -65,3 +65,14 @@ def test_fused_w_svd_and_pinv_equal_nccl_path(nccl1):
     assert pv.shape == (56, 40, 16)
     assert torch.equal(pv, sharded.pinv_w_sharded(xd, 2, 40))
     assert relerr(pv.cpu().numpy(), O.pinv_w(x, 2)) < 1e-9
+
+
+def test_w_product_sharded_equals_single_gpu(nccl1):
+    """Row-sharded w-product (A's rows local, B all-gathered) with the product ops."""
+    rng = np.random.default_rng(34)
+    a = rng.standard_normal((64, 48, 32))
+    b = rng.standard_normal((48, 40, 32))
+    ad, bd = torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()
+    c = sharded.w_product_sharded(ad, bd, 3, 64)
+    assert torch.equal(c, W.w_product(ad, bd, 3))
+    assert relerr(c.cpu().numpy(), O.w_product(a, b, 3)) < 1e-10

@@ -49,6 +49,9 @@ class OracleOps:
         st = np.moveaxis(slices.numpy(), 0, 2)
         return torch.from_numpy(np.ascontiguousarray(np.moveaxis(O.truncated(*O.stack_svd(st), r), 2, 0)))
 
+    def gemm(self, a, b):
+        return torch.from_numpy(np.matmul(a.numpy(), b.numpy()))
+
     def pinv(self, slices, tol):
         k, n1, n2 = slices.shape
         if k == 0:
@@ -80,7 +83,12 @@ def _worker(rank, ws, port, outdir, case):
     sp = sharded.sp_w_svd_sharded(xl, r, L, n1, ops=ops)
     ws_rec = sharded.w_svd_recon_sharded(xl, r, L, n1, ops=ops)
     pv = sharded.pinv_w_sharded(xl, L, n1, tol=1e-12, ops=ops)
-    np.savez(os.path.join(outdir, f"r{rank}.npz"), sp=sp.numpy(), ws=ws_rec.numpy(), pv=pv.numpy())
+    b = np.random.default_rng(8).standard_normal((n2, 5, p))
+    brows = sharded.splits(n2, ws)
+    b0 = sum(brows[:rank])
+    wp = sharded.w_product_sharded(xl, torch.from_numpy(b[b0:b0 + brows[rank]].copy()), L, n1, ops=ops)
+    np.savez(os.path.join(outdir, f"r{rank}.npz"), sp=sp.numpy(), ws=ws_rec.numpy(), pv=pv.numpy(),
+             wp=wp.numpy())
     dist.barrier()
     dist.destroy_process_group()
 
@@ -95,7 +103,10 @@ def test_sharded_pipelines_match_oracle(ws, case):
         sp = np.concatenate([q["sp"] for q in parts], axis=0)
         wsr = np.concatenate([q["ws"] for q in parts], axis=0)
         pv = np.concatenate([q["pv"] for q in parts], axis=0)
+        wp = np.concatenate([q["wp"] for q in parts], axis=0)
     x = np.random.default_rng(7).standard_normal((n1, n2, p))
+    b = np.random.default_rng(8).standard_normal((n2, 5, p))
+    np.testing.assert_allclose(wp, O.w_product(x, b, L), rtol=0, atol=1e-12)
     np.testing.assert_allclose(sp, O.sp_w_svd(x, r, L), rtol=0, atol=1e-12)
     np.testing.assert_allclose(wsr, O.w_svd(x, r, L)["recon"], rtol=0, atol=1e-12)
     np.testing.assert_allclose(pv, O.pinv_w(x, L), rtol=0, atol=1e-10)
