@@ -193,6 +193,12 @@ int wt_pinv_from_svd_ranked_f64(const double* A, int64_t lda, int64_t strideA, i
  * np.fft.fft does (reference baselines.py:68,118,129). */
 int wt_tube_delta_f64(const double* x, int64_t ntubes, int64_t p, double* out, void* stream);
 
+/* Slicewise transpose of a spatial tensor (reference tensor.py:50-52):
+ * y (n2, n1, p) with y[j][i][:] = x[i][j][:], both C-contiguous, tube-fastest:
+ * one pass of whole-tube copies (no trip through the slice-major layout). */
+int wt_tube_transpose_f64(const double* x, int64_t n1, int64_t n2, int64_t p, double* y,
+                          void* stream);
+
 /* Deterministic per-band reductions used by the quality metrics (PSNR/SSIM,
  * PAPER.md:876-887) and parity norms: x, y are spatial tensors viewed as
  * (n tubes, nslices bands) tube-major; out[k] = sum over tubes of f(x, y) with

@@ -214,3 +214,44 @@ extern "C" int wt_slice_reduce_f64(const double* x, const double* y, int64_t n, 
 extern "C" size_t wt_slice_reduce_scratch(int64_t n, int64_t nslices) {
   return (size_t)nslices * (1 + wt_band_reduce_parts(n)) * sizeof(double);
 }
+
+namespace wt {
+namespace {
+// one warp per tube: source tubes in order (coalesced reads across warps), each
+// tube copied with 16-byte vectors when p is even and the tubes 16-byte aligned
+template <bool V2>
+__global__ void tube_transpose_kernel(const double* __restrict__ x, int64_t n1, int64_t n2, int64_t p,
+                                      double* __restrict__ y) {
+  const int lane = threadIdx.x & 31;
+  const int64_t wpb = blockDim.x >> 5;
+  const int64_t nt = n1 * n2;
+  for (int64_t t = blockIdx.x * wpb + (threadIdx.x >> 5); t < nt; t += (int64_t)gridDim.x * wpb) {
+    const int64_t i = t / n2, j = t - i * n2;
+    const double* src = x + t * p;
+    double* dst = y + (j * n1 + i) * p;
+    if (V2) {
+      const double2* s2 = reinterpret_cast<const double2*>(src);
+      double2* d2 = reinterpret_cast<double2*>(dst);
+      for (int64_t k = lane; k < p / 2; k += 32) d2[k] = s2[k];
+    } else {
+      for (int64_t k = lane; k < p; k += 32) dst[k] = src[k];
+    }
+  }
+}
+}  // namespace
+}  // namespace wt
+
+extern "C" int wt_tube_transpose_f64(const double* x, int64_t n1, int64_t n2, int64_t p, double* y,
+                                     void* stream) {
+  WT_REQUIRE(n1 >= 0 && n2 >= 0 && p >= 0, "tube_transpose: negative dimension");
+  if (n1 * n2 * p == 0) return WT_OK;
+  WT_REQUIRE(x && y, "tube_transpose: null pointer");
+  const int64_t nt = n1 * n2;
+  const unsigned grid = (unsigned)std::min<int64_t>((nt + 7) / 8, (int64_t)num_sms() * 16);
+  const bool v2 = p % 2 == 0 && (uintptr_t)x % 16 == 0 && (uintptr_t)y % 16 == 0;
+  if (v2)
+    tube_transpose_kernel<true><<<grid, 256, 0, (cudaStream_t)stream>>>(x, n1, n2, p, y);
+  else
+    tube_transpose_kernel<false><<<grid, 256, 0, (cudaStream_t)stream>>>(x, n1, n2, p, y);
+  return check_launch("wt_tube_transpose_f64");
+}

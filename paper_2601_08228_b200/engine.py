@@ -421,6 +421,16 @@ def pinv_blocks(a: torch.Tensor, sigma: torch.Tensor, vec: torch.Tensor, tol: fl
     return out
 
 
+def tube_transpose(x: torch.Tensor) -> torch.Tensor:
+    """(n1, n2, p) -> (n2, n1, p) slicewise transpose (wt_tube_transpose_f64)."""
+    lib = N.require_gpu()
+    x = x.contiguous()
+    n1, n2, p = x.shape
+    out = torch.empty((n2, n1, p), dtype=F64, device=x.device)
+    N.check(lib.wt_tube_transpose_f64(_ptr(x), n1, n2, p, _ptr(out), _stream()), "wt_tube_transpose_f64")
+    return out
+
+
 def tube_delta(x: torch.Tensor) -> torch.Tensor:
     """(n1, n2, p) -> x[..., k] - x[..., 0] per tube (wt_tube_delta_f64)."""
     lib = N.require_gpu()

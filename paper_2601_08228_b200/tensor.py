@@ -50,8 +50,7 @@ def set_frontal_slice(t, k, m):
 def transpose(t):
     """Slicewise transpose: result[i, j, k] = t[j, i, k] (tensor.py:50-52).
 
-    Device path: K1 at level 0 (tubes -> slices), a batched tile transpose,
-    K2 at level 0 (slices -> tubes).
+    Device path: one pass of whole-tube copies (wt_tube_transpose_f64).
     """
     dev = _is_dev(t)
     x = E.as_device(t)
@@ -59,9 +58,7 @@ def transpose(t):
     if n1 * n2 * p == 0:
         z = torch.zeros((n2, n1, p), dtype=torch.float64, device=x.device)
         return z if dev else z.cpu().numpy()
-    sl = E.lift_forward(x, 0)                 # (p, n1, n2)
-    st = E.copy2d(sl, trans=True)             # (p, n2, n1)
-    y = E.lift_inverse(st, n2, n1, p, 0)      # (n2, n1, p)
+    y = E.tube_transpose(x)                   # (n2, n1, p)
     return y if dev else E.to_host(y)
 
 

@@ -128,3 +128,14 @@ def test_ring_constructors_match_reference(golden):
         with pytest.raises(W.SingularSliceError) as ei:
             W.inverse_tensor(gi[name], 2)
         assert (ei.value.level, ei.value.slice_index) == (errs[call]["level"], errs[call]["slice_index"])
+
+
+@pytest.mark.parametrize("shape", [(7, 5, 3), (33, 17, 1), (64, 48, 32), (5, 9, 130)])
+def test_transpose_one_pass_exact(shape):
+    """wt_tube_transpose_f64: bit-exact slicewise transpose for odd / unit / even p,
+    including a view whose data pointer is not 16-byte aligned."""
+    x = np.random.default_rng(41).standard_normal(shape)
+    assert np.array_equal(W.transpose(x), O.transpose(x))
+    big = torch.from_numpy(np.random.default_rng(42).standard_normal((shape[0] + 1,) + shape[1:])).cuda()
+    view = big[1:]  # contiguous, offset by one row of tubes
+    assert torch.equal(W.transpose(view), view.permute(1, 0, 2).contiguous())
