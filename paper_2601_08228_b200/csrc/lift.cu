@@ -372,6 +372,12 @@ extern "C" int wt_lift_fwd_f64(const double* x, int64_t n1, int64_t n2, int64_t 
   if (st) return st;
   LiftGeom g{n1 * n2, p, levels, 0, 0, 0, slice_base, layout, level_mask};
   if (g.ntubes == 0) return WT_OK;
+  if (levels == 0 && layout == WT_LAYOUT_SLICE_MAJOR && slice_base == 0 && (level_mask & 1)) {
+    // level 0 is the plain tube -> slice relayout (slicewise_matmul staging,
+    // algebra.py:26-27): one dense transpose at copy bandwidth
+    st = transpose_dense(x, g.ntubes, p, out, (cudaStream_t)stream);
+    return st ? st : check_launch("wt_lift_fwd_f64 (level 0)");
+  }
   if (layout == WT_LAYOUT_SLICE_MAJOR) {
     st = lift_fwd_fast(x, g.ntubes, p, levels, out, slice_base, level_mask, (cudaStream_t)stream);
     if (st != WT_ERR_UNSUPPORTED) return st;
@@ -404,6 +410,10 @@ extern "C" int wt_lift_inv_f64(const double* pyr, int64_t n1, int64_t n2, int64_
   if (st) return st;
   LiftGeom g{n1 * n2, p, levels, 0, 0, 0, slice_base, layout, level_mask};
   if (g.ntubes == 0) return WT_OK;
+  if (levels == 0 && layout == WT_LAYOUT_SLICE_MAJOR && slice_base == 0 && (level_mask & 1)) {
+    st = transpose_dense(pyr, p, g.ntubes, y, (cudaStream_t)stream);  // slices -> tubes
+    return st ? st : check_launch("wt_lift_inv_f64 (level 0)");
+  }
   if (layout == WT_LAYOUT_SLICE_MAJOR) {
     st = lift_inv_fast(pyr, g.ntubes, p, levels, y, slice_base, level_mask, (cudaStream_t)stream);
     if (st != WT_ERR_UNSUPPORTED) return st;

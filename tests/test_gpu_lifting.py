@@ -95,11 +95,12 @@ def test_unaligned_input_takes_plain_path():
     assert np.array_equal(out.cpu().numpy(), O.lift_inverse(s_ref, d_ref))
 
 
-def test_level0_is_a_transpose():
-    x = np.random.default_rng(1).standard_normal((5, 6, 7))
+@pytest.mark.parametrize("shape", [(5, 6, 7), (300, 257, 33), (1, 1, 1)])
+def test_level0_is_a_transpose(shape):
+    x = np.random.default_rng(1).standard_normal(shape)
     buf = E.lift_forward(torch.from_numpy(x).cuda(), 0)
     assert np.array_equal(buf.cpu().numpy(), np.moveaxis(x, 2, 0))
-    y = E.lift_inverse(buf, 5, 6, 7, 0)
+    y = E.lift_inverse(buf, *shape, 0)
     assert np.array_equal(y.cpu().numpy(), x)
 
 
