@@ -61,6 +61,23 @@ __global__ void svd_copy_in(const double* __restrict__ A, int64_t lda, int64_t s
   }
 }
 
+// ------------------------------------------------------ cluster helpers ----
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ int cluster_rank() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return (int)r;
+}
+// generic address of `p` (this CTA's shared memory) in CTA `rank` of the cluster
+template <typename T>
+__device__ __forceinline__ T* cluster_map(T* p, int rank) {
+  uint64_t out;
+  asm volatile("mapa.u64 %0, %1, %2;" : "=l"(out) : "l"(reinterpret_cast<uint64_t>(p)), "r"(rank));
+  return reinterpret_cast<T*>(out);
+}
+
 // ---------------------------------------------------------- pair kernel ----
 __device__ __forceinline__ double nanmax(double a, double b) {
   return (isnan(a) || isnan(b)) ? (a + b) : fmax(a, b);
@@ -108,10 +125,17 @@ __device__ __forceinline__ void load_chunk(double* Zs, const double* Xb, int64_t
 
 // One pair visit (matrix b, column blocks I and J).  Every early return is
 // CTA-uniform (it depends on global flags / shared values only).
+// SPLIT > 1: the visit is shared by the SPLIT CTAs of a thread-block cluster,
+// CTA `rank` owning a contiguous range of the panel's row chunks.  Each CTA
+// streams its rows' partial Gram, the partials are summed in rank order through
+// distributed shared memory (every CTA ends with the same G, bit for bit), every
+// CTA runs the same eigen steps redundantly (same Q) and rotates its own rows.
+// The sweep kernel's cluster leader has already done the skip / converged checks.
+template <int SPLIT>
 __device__ __forceinline__ void pair_visit(PairSmem& S, const SvdWs& ws, int b, int I, int J,
                                            int64_t mpad, int64_t npad, double tol, int inner_sweeps,
-                                           int cross_only) {
-  if (ws.conv[b]) return;
+                                           int cross_only, int rank = 0) {
+  if (SPLIT == 1 && ws.conv[b]) return;
   const int colI = I * HB, colJ = J * HB;
   double* Xb = mat_ptr(ws, b, npad, mpad);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -119,7 +143,7 @@ __device__ __forceinline__ void pair_visit(PairSmem& S, const SvdWs& ws, int b, 
   // the same column sets after a reordering) is still clean: skip the visit
   // without touching the panel (the late sweeps are mostly such visits).
   const int nbk = (int)(npad / HB);
-  if (ws.pclean) {
+  if (SPLIT == 1 && ws.pclean) {
     if (tid == 0) {
       const unsigned long long cur =
           ((unsigned long long)(unsigned)__ldcg(ws.bver + (int64_t)b * nbk + I) << 32) |
@@ -130,6 +154,10 @@ __device__ __forceinline__ void pair_visit(PairSmem& S, const SvdWs& ws, int b, 
     if (S.skip) return;
   }
   const int nch = (int)(mpad / RCH);
+  // this CTA's row chunks [c0, c1) of the panel (all of them without a split)
+  const int c0 = SPLIT == 1 ? 0 : (int)((int64_t)rank * nch / SPLIT);
+  const int ncl = SPLIT == 1 ? nch : (int)((int64_t)(rank + 1) * nch / SPLIT) - c0;
+  const bool lead = SPLIT == 1 || rank == 0;  // writes the visit's bookkeeping
 
   const long long t_start = clock64();
   // ---------------- 1. Gram G = Z^T Z: upper 10 of the 16 8x8 tiles --------
@@ -143,12 +171,12 @@ __device__ __forceinline__ void pair_visit(PairSmem& S, const SvdWs& ws, int b, 
   for (int t = 0; t < 10; ++t) acc[t][0] = acc[t][1] = 0.0;
 #pragma unroll
   for (int s0 = 0; s0 < kNZ - 1; ++s0) {
-    if (s0 < nch) load_chunk(S.Z[s0], Xb, mpad, colI, colJ, (int64_t)s0 * RCH);
+    if (s0 < ncl) load_chunk(S.Z[s0], Xb, mpad, colI, colJ, (int64_t)(c0 + s0) * RCH);
     cp_async_commit();
   }
-  for (int ch = 0; ch < nch; ++ch) {
+  for (int ch = 0; ch < ncl; ++ch) {
     const int nx = ch + kNZ - 1;
-    if (nx < nch) load_chunk(S.Z[nx % kNZ], Xb, mpad, colI, colJ, (int64_t)nx * RCH);
+    if (nx < ncl) load_chunk(S.Z[nx % kNZ], Xb, mpad, colI, colJ, (int64_t)(c0 + nx) * RCH);
     cp_async_commit();
     cp_async_wait<kNZ - 1>();
     __syncthreads();
@@ -184,10 +212,31 @@ __device__ __forceinline__ void pair_visit(PairSmem& S, const SvdWs& ws, int b, 
     }
     if (tid == 0) S.gmax_bits = 0ull;
     __syncthreads();
+    if constexpr (SPLIT > 1) {
+      // this CTA's partial after the warp sum, then the cluster's partials in rank order
+      static_assert((kWarps + 1) * 640 <= kNZ * BW * LDZ, "cluster partial exceeds the chunk buffers");
+      double* part = red + kWarps * 640;
+      for (int e = tid; e < 640; e += kThreads) {
+        double v = red[e];
+#pragma unroll
+        for (int w = 1; w < kWarps; ++w) v += red[w * 640 + e];
+        part[e] = v;
+      }
+      cluster_sync();
+      for (int e = tid; e < 640; e += kThreads) {
+        double v = *cluster_map(part + e, 0);
+#pragma unroll
+        for (int r = 1; r < SPLIT; ++r) v += *cluster_map(part + e, r);
+        red[e] = v;  // own warp-0 partial slot is free: the loop below reads red[e] (w = 0 only)
+      }
+      __syncthreads();
+    }
     for (int e = tid; e < 640; e += kThreads) {
       double v = red[e];
+      if (SPLIT == 1) {
 #pragma unroll
-      for (int w = 1; w < kWarps; ++w) v += red[w * 640 + e];
+        for (int w = 1; w < kWarps; ++w) v += red[w * 640 + e];
+      }
       const int t = e >> 6, l = (e & 63) >> 1, h = e & 1;
       // tile t -> (ta, tb), ta <= tb, in the order of the accumulation loop
       const int ta = t < 4 ? 0 : t < 7 ? 1 : t < 9 ? 2 : 3;
@@ -303,14 +352,14 @@ __device__ __forceinline__ void pair_visit(PairSmem& S, const SvdWs& ws, int b, 
   // NaN-propagating max through the bit pattern (non-negative doubles order as uint64)
   if (tid == 0) atomicMax(&ws.offmax[b], (unsigned long long)__double_as_longlong(off));
   if (!(off >= tol) || isinf(off)) {  // converged pair (or NaN / inf: recorded above)
-    store_norms(S.G[0], ws.sig + (int64_t)b * npad, colI, colJ);
-    if (ws.pclean && tid == 0 && off < tol)  // certified clean at the blocks' current versions
+    if (lead) store_norms(S.G[0], ws.sig + (int64_t)b * npad, colI, colJ);
+    if (lead && ws.pclean && tid == 0 && off < tol)  // certified clean at the blocks' current versions
       __stcg(ws.pclean + ((int64_t)b * nbk + I) * nbk + J,
              ((unsigned long long)(unsigned)__ldcg(ws.bver + (int64_t)b * nbk + I) << 32) |
                  (unsigned)__ldcg(ws.bver + (int64_t)b * nbk + J));
     return;
   }
-  if (tid == 0) atomicAdd(ws.pending + 1, 1);  // rotated-pair counter (diagnostics)
+  if (lead && tid == 0) atomicAdd(ws.pending + 1, 1);  // rotated-pair counter (diagnostics)
 
   const long long t_gram = clock64();
   // ---------------- 3. eigen-decomposition of G (cyclic parallel Jacobi) ----
@@ -418,8 +467,10 @@ __device__ __forceinline__ void pair_visit(PairSmem& S, const SvdWs& ws, int b, 
       eig_barrier();
     }
   }
-  __syncthreads();
-  store_norms(S.G[0], ws.sig + (int64_t)b * npad, colI, colJ);  // rotated Gram's diagonal
+  // (split: every CTA of the cluster has read the others' Gram partials, which
+  // live in the chunk buffers the rotation stream refills next)
+  if constexpr (SPLIT > 1) cluster_sync(); else __syncthreads();
+  if (lead) store_norms(S.G[0], ws.sig + (int64_t)b * npad, colI, colJ);  // rotated Gram's diagonal
   const long long t_eig = clock64();
   // ---------------- 4. Z <- Z Q, streamed, written back in place -----------
   // warp w: chunk rows rt*16 .. rt*16+15 (two 8-row tiles) x output n-tiles
@@ -434,12 +485,12 @@ __device__ __forceinline__ void pair_visit(PairSmem& S, const SvdWs& ws, int b, 
     for (int j = 0; j < 2; ++j) qf[kk][j] = S.Q[(kk * 4 + (lane & 3)) * LDG + (2 * nh + j) * 8 + (lane >> 2)];
 #pragma unroll
   for (int s0 = 0; s0 < kNZ - 1; ++s0) {
-    if (s0 < nch) load_chunk(S.Z[s0], Xb, mpad, colI, colJ, (int64_t)s0 * RCH);
+    if (s0 < ncl) load_chunk(S.Z[s0], Xb, mpad, colI, colJ, (int64_t)(c0 + s0) * RCH);
     cp_async_commit();
   }
-  for (int ch = 0; ch < nch; ++ch) {
+  for (int ch = 0; ch < ncl; ++ch) {
     const int nx = ch + kNZ - 1;
-    if (nx < nch) load_chunk(S.Z[nx % kNZ], Xb, mpad, colI, colJ, (int64_t)nx * RCH);
+    if (nx < ncl) load_chunk(S.Z[nx % kNZ], Xb, mpad, colI, colJ, (int64_t)(c0 + nx) * RCH);
     cp_async_commit();
     cp_async_wait<kNZ - 1>();
     __syncthreads();
@@ -464,7 +515,7 @@ __device__ __forceinline__ void pair_visit(PairSmem& S, const SvdWs& ws, int b, 
     // results straight from the DMMA fragments to global, in place: a lane
     // holds rows r0, r0+1 of 4 output columns, so the 8 lanes sharing lane%4
     // write 128 contiguous bytes of one column (no smem round trip)
-    const int64_t rbase = (int64_t)ch * RCH;
+    const int64_t rbase = (int64_t)(c0 + ch) * RCH;
 #pragma unroll
     for (int j = 0; j < 2; ++j)
 #pragma unroll
@@ -476,11 +527,11 @@ __device__ __forceinline__ void pair_visit(PairSmem& S, const SvdWs& ws, int b, 
       }
     __syncthreads();  // every warp has read the chunk before its buffer is refilled
   }
-  if (ws.pclean && tid == 0) {  // both blocks changed (the visit owns them exclusively)
+  if (lead && ws.pclean && tid == 0) {  // both blocks changed (the visit owns them exclusively)
     __stcg(ws.bver + (int64_t)b * nbk + I, __ldcg(ws.bver + (int64_t)b * nbk + I) + 1);
     __stcg(ws.bver + (int64_t)b * nbk + J, __ldcg(ws.bver + (int64_t)b * nbk + J) + 1);
   }
-  if (ws.prof && tid == 0) {
+  if (lead && ws.prof && tid == 0) {
     atomicAdd(ws.prof + 0, (unsigned long long)(t_gram - t_start));
     atomicAdd(ws.prof + 1, (unsigned long long)(t_eig - t_gram));
     atomicAdd(ws.prof + 2, (unsigned long long)(clock64() - t_eig));
@@ -498,7 +549,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) svd_pair_kernel(SvdWs ws
   PairSmem& S = *reinterpret_cast<PairSmem*>(smem_raw);
   const int nb = (int)(npad / HB);
   const int I = rr_index(blockIdx.x, round, nb), J = rr_index(nb - 1 - blockIdx.x, round, nb);
-  pair_visit(S, ws, ws.active[blockIdx.y], I, J, mpad, npad, tol, inner_sweeps, cross_only);
+  pair_visit<1>(S, ws, ws.active[blockIdx.y], I, J, mpad, npad, tol, inner_sweeps, cross_only);
 }
 
 __device__ __forceinline__ int ld_acquire(const int* p) {
@@ -517,17 +568,22 @@ __device__ __forceinline__ void st_release(int* p, int v) {
 // counters ws.bdone), so a round's tail overlaps the next round's start
 // instead of draining the GPU at every kernel boundary.  A visit only waits on
 // smaller tickets, which running CTAs already hold: no deadlock.
+// SPLIT > 1 (launched with SPLIT-CTA clusters): the cluster is the unit that
+// takes tickets; its leader CTA schedules (ticket, dependency wait, converged /
+// clean-pair skip) and the others read the item from the leader's shared memory.
+template <int SPLIT>
 __global__ void __launch_bounds__(kThreads, kMinBlocks) svd_sweep_kernel(SvdWs ws, int64_t mpad, int64_t npad,
                                                                 int n_active, double tol, int inner_sweeps,
                                                                 int cross) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   PairSmem& S = *reinterpret_cast<PairSmem*>(smem_raw);
-  __shared__ int s_item[4];  // ticket, then (matrix, block I, block J) of the visit
+  __shared__ int s_item[5];  // ticket, (matrix, block I, block J) of the visit, skip (SPLIT > 1)
   const int nb = (int)(npad / HB);
   const int per_round = n_active * (nb / 2);
   const int total = per_round * (nb - 1);
+  const int rank = SPLIT == 1 ? 0 : cluster_rank();
   for (;;) {
-    if (threadIdx.x == 0) {
+    if (threadIdx.x == 0 && rank == 0) {
       const int t = atomicAdd(ws.ticket, 1);
       s_item[0] = t;
       if (t < total) {
@@ -540,18 +596,43 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) svd_sweep_kernel(SvdWs w
         s_item[3] = J;
         while (ld_acquire(ws.bdone + (int64_t)b * nb + I) < round) __nanosleep(100);
         while (ld_acquire(ws.bdone + (int64_t)b * nb + J) < round) __nanosleep(100);
+        if (SPLIT > 1) {
+          int skip = ws.conv[b] != 0;
+          if (!skip && ws.pclean) {
+            const unsigned long long cur =
+                ((unsigned long long)(unsigned)__ldcg(ws.bver + (int64_t)b * nb + I) << 32) |
+                (unsigned)__ldcg(ws.bver + (int64_t)b * nb + J);
+            skip = __ldcg(ws.pclean + ((int64_t)b * nb + I) * nb + J) == cur;
+          }
+          s_item[4] = skip;
+        }
       }
     }
-    __syncthreads();
-    const int t = s_item[0];
-    if (t >= total) return;
+    int t, b, I, J, skip = 0;
+    if constexpr (SPLIT == 1) {
+      __syncthreads();
+      t = s_item[0], b = s_item[1], I = s_item[2], J = s_item[3];
+    } else {
+      cluster_sync();
+      const int* li = cluster_map(s_item, 0);
+      t = li[0], b = li[1], I = li[2], J = li[3], skip = li[4];
+    }
+    if (t >= total) {
+      if constexpr (SPLIT > 1) cluster_sync();  // the leader's item stays readable until all have read it
+      return;
+    }
     const int round = t / per_round;
-    pair_visit(S, ws, s_item[1], s_item[2], s_item[3], mpad, npad, tol, inner_sweeps, cross && round > 0);
-    __syncthreads();  // every store of the visit precedes the release below (and s_item reuse)
-    if (threadIdx.x == 0) {
+    if (!skip) pair_visit<SPLIT>(S, ws, b, I, J, mpad, npad, tol, inner_sweeps, cross && round > 0, rank);
+    if constexpr (SPLIT > 1) {
+      __threadfence();  // every CTA's stores of the visit, before the leader's release below
+      cluster_sync();
+    } else {
+      __syncthreads();  // every store of the visit precedes the release below (and s_item reuse)
+    }
+    if (threadIdx.x == 0 && rank == 0) {
       __threadfence();
-      st_release(ws.bdone + (int64_t)s_item[1] * nb + s_item[2], round + 1);
-      st_release(ws.bdone + (int64_t)s_item[1] * nb + s_item[3], round + 1);
+      st_release(ws.bdone + (int64_t)b * nb + I, round + 1);
+      st_release(ws.bdone + (int64_t)b * nb + J, round + 1);
     }
   }
 }
@@ -729,6 +810,37 @@ WsLayout ws_layout(int64_t n1, int64_t n2, int64_t batch) {
 namespace wt {
 namespace SVD_NS {
 
+// One persistent sweep launch; SPLIT > 1 runs every visit on a SPLIT-CTA
+// cluster (rows split), as many clusters as can be resident.
+template <int SPLIT>
+int launch_sweep(const SvdWs& ws, int64_t mpad, int64_t npad, int n_active, double tol, int inner,
+                 int cross, int64_t visits, int max_ctas, cudaStream_t st) {
+  auto kern = svd_sweep_kernel<SPLIT>;
+  if (int e = ensure_smem(kern, sizeof(PairSmem))) return e;
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = SPLIT;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = sizeof(PairSmem);
+  cfg.stream = st;
+  cfg.attrs = attr;
+  cfg.numAttrs = SPLIT > 1 ? 1 : 0;
+  int64_t units = std::max(max_ctas / SPLIT, 1);
+  if (SPLIT > 1) {
+    cfg.gridDim = dim3((unsigned)(SPLIT * units));
+    int nc = 0;
+    WT_CUDA(cudaOccupancyMaxActiveClusters(&nc, kern, &cfg));
+    if (nc > 0) units = std::min<int64_t>(units, nc);
+  }
+  units = std::min<int64_t>(units, visits);
+  cfg.gridDim = dim3((unsigned)(SPLIT * units));
+  WT_CUDA(cudaLaunchKernelEx(&cfg, kern, ws, mpad, npad, n_active, tol, inner, cross));
+  return WT_OK;
+}
+
 size_t workspace_bytes(int64_t n1, int64_t n2, int64_t batch) {
   if (n1 < 0 || n2 < 0 || batch < 0) return 0;
   return ws_layout(n1, n2, batch).total;
@@ -787,18 +899,22 @@ int jacobi(const double* A, int64_t lda, int64_t strideA, int64_t n1,
   WT_CUDA(cudaMemsetAsync(ws.pending, 0, sizeof(int) * 3, st));
 
   if (int e = ensure_smem(svd_pair_kernel, sizeof(PairSmem))) return e;
-  if (int e = ensure_smem(svd_sweep_kernel, sizeof(PairSmem))) return e;
   // Persistent sweeps (one launch per sweep, visits scheduled by block
   // dependencies) unless WT_SVD_PERSIST=0 (one launch per round).
   int persist = 1;
   if (const char* e = getenv("WT_SVD_PERSIST")) persist = atoi(e);
   int sweep_ctas = 0;
+  int split_env = 0;
+  if (const char* e = getenv("WT_SVD_SPLIT")) split_env = atoi(e);
+  int n_sms = kNumSMs;
   if (persist) {
     int dev = 0, per_sm = 0;
     WT_CUDA(cudaGetDevice(&dev));
     int sms = 0;
     WT_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    WT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, svd_sweep_kernel, kThreads, sizeof(PairSmem)));
+    n_sms = sms;
+    WT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, svd_sweep_kernel<1>, kThreads, sizeof(PairSmem)));
+    if (int e = ensure_smem(svd_sweep_kernel<1>, sizeof(PairSmem))) return e;
     sweep_ctas = sms * std::max(per_sm, 1);
   }
   g_last_sweeps = 0;
@@ -853,8 +969,32 @@ int jacobi(const double* A, int64_t lda, int64_t strideA, int64_t n1,
       WT_CUDA(cudaMemsetAsync(ws.bdone, 0, sizeof(int) * (size_t)batch * nb, st));
       WT_CUDA(cudaMemsetAsync(ws.ticket, 0, sizeof(int), st));
       const int64_t visits = n_active * (int64_t)(nb / 2) * (nb - 1);
-      svd_sweep_kernel<<<(unsigned)std::min<int64_t>(visits, sweep_ctas), kThreads, sizeof(PairSmem), st>>>(
-          ws, L.mpad, L.npad, (int)n_active, tol, inner, cross);
+      // Latency-bound sweeps (too few concurrent visits to fill the resident
+      // CTA slots: few matrices, e.g. the 8-GPU share of config 4 or the
+      // config-5 operator slices) split every visit's rows over a cluster of up
+      // to 8 CTAs; WT_SVD_SPLIT forces a size.  A split saves streaming time in
+      // proportion to the rows but costs a cluster reduction (~3k cycles) and
+      // slower eigen steps on busier SMs, so (measured, round 1: 4 x 1024^2
+      // 45.4 -> 38.8 ms, 1 x 512^2 13.8 -> 11.6 ms, 24 x 256^2 5.6 -> 6.1 ms
+      // when split) it doubles only while every CTA keeps >= 128 rows, the
+      // clusters fit the resident slots, and the SMs stay at <= 1 CTA each
+      // unless the CTAs keep >= 512 rows.
+      const int64_t conc = n_active * (int64_t)(nb / 2);
+      int split = 1;
+      if (split_env > 0) split = split_env;
+      else
+        while (split < 8 && L.mpad / (2 * split) >= 128 && conc * split * 2 <= sweep_ctas &&
+               (conc * split * 2 <= n_sms || L.mpad / (2 * split) >= 512))
+          split *= 2;
+      while (split > 1 && split > L.mpad / RCH) split >>= 1;  // at least one row chunk per CTA
+      int e = WT_OK;
+      switch (split >= 8 ? 8 : split >= 4 ? 4 : split >= 2 ? 2 : 1) {
+        case 8: e = launch_sweep<8>(ws, L.mpad, L.npad, (int)n_active, tol, inner, cross, visits, sweep_ctas, st); break;
+        case 4: e = launch_sweep<4>(ws, L.mpad, L.npad, (int)n_active, tol, inner, cross, visits, sweep_ctas, st); break;
+        case 2: e = launch_sweep<2>(ws, L.mpad, L.npad, (int)n_active, tol, inner, cross, visits, sweep_ctas, st); break;
+        default: e = launch_sweep<1>(ws, L.mpad, L.npad, (int)n_active, tol, inner, cross, visits, sweep_ctas, st);
+      }
+      if (e) return e;
     } else {
       for (int round = 0; round < nb - 1; ++round) {
         svd_pair_kernel<<<dim3(nb / 2, (unsigned)n_active), kThreads, sizeof(PairSmem), st>>>(

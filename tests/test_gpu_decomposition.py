@@ -144,8 +144,11 @@ def test_scheduling_knobs_do_not_change_bits(monkeypatch, knob):
     """K4's persistent dependency-scheduled sweeps and the clean-pair skip only
     change WHEN visits run or drop visits that rotate nothing: sigma and vectors
     are bit-identical with either switched off (one launch per round / every
-    pair re-tested).  256 columns: cross-only rounds and 16 blocks."""
+    pair re-tested).  256 columns: cross-only rounds and 16 blocks.  The
+    one-launch-per-round path has no cluster-split visits, so the comparison
+    pins the split to 1 (a split changes the Gram's summation order)."""
     a = torch.from_numpy(np.random.default_rng(29).standard_normal((6, 300, 256))).cuda()
+    monkeypatch.setenv("WT_SVD_SPLIT", "1")
     outs = []
     for v in ("1", "0"):
         monkeypatch.setenv(knob, v)
@@ -154,6 +157,32 @@ def test_scheduling_knobs_do_not_change_bits(monkeypatch, knob):
         outs.append((sigma.clone(), vec.clone(), E.last_sweeps()))
     assert torch.equal(outs[0][0], outs[1][0]) and torch.equal(outs[0][1], outs[1][1])
     assert outs[0][2] == outs[1][2]
+
+
+@pytest.mark.parametrize("split", ["1", "2", "4", "8", "0"])
+def test_cluster_split_visits(monkeypatch, split):
+    """Visits split over 2/4/8-CTA clusters (rows of the panel, partial Grams
+    summed in rank order through distributed shared memory; 9 row chunks, so
+    uneven row ranges): sigma against LAPACK, orthonormal vectors, and the
+    clean-pair skip (decided by the cluster leader) leaves the bits unchanged."""
+    rng = np.random.default_rng(31)
+    a_np = rng.standard_normal((3, 520, 512)) * np.linspace(1.0, 1e-3, 512)
+    a = torch.from_numpy(a_np).cuda()
+    monkeypatch.setenv("WT_SVD_SPLIT", split)
+    outs = []
+    for skip in ("1", "0"):
+        monkeypatch.setenv("WT_SVD_PAIR_SKIP", skip)
+        sigma, vec, info = E.svd(a, 512)
+        E.raise_if_failed(info)
+        outs.append((sigma.cpu().numpy(), vec.cpu().numpy()))
+    assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
+    sigma, vec = outs[0]
+    ref = np.linalg.svd(a_np, compute_uv=False)
+    assert np.max(np.abs(sigma - ref) / ref[:, :1]) < 1e-12
+    # long side (520) singular vectors, orthonormal
+    for b in range(3):
+        g = vec[b] @ vec[b].T
+        assert np.max(np.abs(g - np.eye(512))) < 1e-11
 
 
 def test_concurrent_host_threads_on_own_streams():
