@@ -832,8 +832,11 @@ int launch_sweep(const SvdWs& ws, int64_t mpad, int64_t npad, int n_active, doub
   if (SPLIT > 1) {
     cfg.gridDim = dim3((unsigned)(SPLIT * units));
     int nc = 0;
-    WT_CUDA(cudaOccupancyMaxActiveClusters(&nc, kern, &cfg));
-    if (nc > 0) units = std::min<int64_t>(units, nc);
+    if (cudaOccupancyMaxActiveClusters(&nc, kern, &cfg) != cudaSuccess || nc <= 0) {
+      (void)cudaGetLastError();  // clusters of this shape cannot be resident: caller runs S = 1
+      return WT_ERR_UNSUPPORTED;
+    }
+    units = std::min<int64_t>(units, nc);
   }
   units = std::min<int64_t>(units, visits);
   cfg.gridDim = dim3((unsigned)(SPLIT * units));
@@ -994,6 +997,8 @@ int jacobi(const double* A, int64_t lda, int64_t strideA, int64_t n1,
         case 2: e = launch_sweep<2>(ws, L.mpad, L.npad, (int)n_active, tol, inner, cross, visits, sweep_ctas, st); break;
         default: e = launch_sweep<1>(ws, L.mpad, L.npad, (int)n_active, tol, inner, cross, visits, sweep_ctas, st);
       }
+      if (e == WT_ERR_UNSUPPORTED)
+        e = launch_sweep<1>(ws, L.mpad, L.npad, (int)n_active, tol, inner, cross, visits, sweep_ctas, st);
       if (e) return e;
     } else {
       for (int round = 0; round < nb - 1; ++round) {
