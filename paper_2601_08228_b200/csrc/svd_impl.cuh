@@ -916,8 +916,11 @@ int jacobi(const double* A, int64_t lda, int64_t strideA, int64_t n1,
     int sms = 0;
     WT_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     n_sms = sms;
-    WT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, svd_sweep_kernel<1>, kThreads, sizeof(PairSmem)));
+    // (the dynamic shared-memory limit must be raised before the occupancy
+    // query, or the first call in a process sees 0 resident CTAs)
     if (int e = ensure_smem(svd_sweep_kernel<1>, sizeof(PairSmem))) return e;
+    WT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, svd_sweep_kernel<1>, kThreads, sizeof(PairSmem)));
+    if (const char* e = getenv("WT_SVD_CTAS_PER_SM")) per_sm = std::min(per_sm, std::max(1, atoi(e)));
     sweep_ctas = sms * std::max(per_sm, 1);
   }
   g_last_sweeps = 0;
@@ -974,31 +977,37 @@ int jacobi(const double* A, int64_t lda, int64_t strideA, int64_t n1,
       const int64_t visits = n_active * (int64_t)(nb / 2) * (nb - 1);
       // Latency-bound sweeps (too few concurrent visits to fill the resident
       // CTA slots: few matrices, e.g. the 8-GPU share of config 4 or the
-      // config-5 operator slices) split every visit's rows over a cluster of up
-      // to 8 CTAs; WT_SVD_SPLIT forces a size.  A split saves streaming time in
-      // proportion to the rows but costs a cluster reduction (~3k cycles) and
-      // slower eigen steps on busier SMs, so (measured, round 1: 4 x 1024^2
-      // 45.4 -> 38.8 ms, 1 x 512^2 13.8 -> 11.6 ms, 24 x 256^2 5.6 -> 6.1 ms
-      // when split) it doubles only while every CTA keeps >= 128 rows, the
-      // clusters fit the resident slots, and the SMs stay at <= 1 CTA each
-      // unless the CTAs keep >= 512 rows.
+      // config-5 operator slices).  Two levers, measured on one B200 (round 1,
+      // tools/svd_concurrency.py, ms):
+      //  * resident CTAs per SM: just enough for one round's visits, so that a
+      //    visit does not share its SM when it need not (the persistent grid
+      //    otherwise parks idle CTAs next to running visits): 4 x 1024^2
+      //    38.7 -> 33.5 at 1 CTA/SM, 16 x 512^2 19.7 -> 17.7 and 24 x 256^2
+      //    5.52 -> 5.14 at 2;
+      //  * cluster-split visits (rows over S CTAs, partial Grams summed in
+      //    DSMEM) while every visit still has SMs to itself and each CTA keeps
+      //    >= 128 rows: 1 x 512^2 12.96 (S = 1) -> 10.68 (S = 4), 1 CTA/SM.
+      // Throughput-bound batches (configs 3 and 4 on one GPU) keep S = 1 and
+      // all resident CTAs.  WT_SVD_SPLIT forces S, WT_SVD_CTAS_PER_SM caps k.
       const int64_t conc = n_active * (int64_t)(nb / 2);
       int split = 1;
       if (split_env > 0) split = split_env;
       else
-        while (split < 8 && L.mpad / (2 * split) >= 128 && conc * split * 2 <= sweep_ctas &&
-               (conc * split * 2 <= n_sms || L.mpad / (2 * split) >= 512))
-          split *= 2;
+        while (split < 8 && L.mpad / (2 * split) >= 128 && conc * split * 2 <= n_sms) split *= 2;
       while (split > 1 && split > L.mpad / RCH) split >>= 1;  // at least one row chunk per CTA
+      split = split >= 8 ? 8 : split >= 4 ? 4 : split >= 2 ? 2 : 1;
+      const int64_t per_sm_max = std::max<int64_t>(sweep_ctas / std::max(n_sms, 1), 1);
+      const int64_t k_sm = std::min<int64_t>(std::max<int64_t>((conc * split + n_sms - 1) / n_sms, 1), per_sm_max);
+      const int max_ctas = (int)std::max<int64_t>(n_sms * k_sm, split);
       int e = WT_OK;
-      switch (split >= 8 ? 8 : split >= 4 ? 4 : split >= 2 ? 2 : 1) {
-        case 8: e = launch_sweep<8>(ws, L.mpad, L.npad, (int)n_active, tol, inner, cross, visits, sweep_ctas, st); break;
-        case 4: e = launch_sweep<4>(ws, L.mpad, L.npad, (int)n_active, tol, inner, cross, visits, sweep_ctas, st); break;
-        case 2: e = launch_sweep<2>(ws, L.mpad, L.npad, (int)n_active, tol, inner, cross, visits, sweep_ctas, st); break;
-        default: e = launch_sweep<1>(ws, L.mpad, L.npad, (int)n_active, tol, inner, cross, visits, sweep_ctas, st);
+      switch (split) {
+        case 8: e = launch_sweep<8>(ws, L.mpad, L.npad, (int)n_active, tol, inner, cross, visits, max_ctas, st); break;
+        case 4: e = launch_sweep<4>(ws, L.mpad, L.npad, (int)n_active, tol, inner, cross, visits, max_ctas, st); break;
+        case 2: e = launch_sweep<2>(ws, L.mpad, L.npad, (int)n_active, tol, inner, cross, visits, max_ctas, st); break;
+        default: e = launch_sweep<1>(ws, L.mpad, L.npad, (int)n_active, tol, inner, cross, visits, max_ctas, st);
       }
       if (e == WT_ERR_UNSUPPORTED)
-        e = launch_sweep<1>(ws, L.mpad, L.npad, (int)n_active, tol, inner, cross, visits, sweep_ctas, st);
+        e = launch_sweep<1>(ws, L.mpad, L.npad, (int)n_active, tol, inner, cross, visits, max_ctas, st);
       if (e) return e;
     } else {
       for (int round = 0; round < nb - 1; ++round) {
