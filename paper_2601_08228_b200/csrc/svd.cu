@@ -42,6 +42,12 @@
 #ifndef WT_SVD_FLATRED
 #define WT_SVD_FLATRED 1
 #endif
+#ifndef WT_SVD_SPIN_NS
+#define WT_SVD_SPIN_NS 100
+#endif
+#ifndef WT_SVD_LIGHT_RELEASE
+#define WT_SVD_LIGHT_RELEASE 1
+#endif
 #ifndef WT_SVD_NZ
 #define WT_SVD_NZ 3
 #endif

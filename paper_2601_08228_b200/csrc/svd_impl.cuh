@@ -558,6 +558,10 @@ __device__ __forceinline__ int ld_acquire(const int* p) {
   return v;
 }
 
+__device__ __forceinline__ void st_relaxed(int* p, int v) {
+  asm volatile("st.relaxed.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
 __device__ __forceinline__ void st_release(int* p, int v) {
   asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -594,8 +598,8 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) svd_sweep_kernel(SvdWs w
         s_item[1] = b;
         s_item[2] = I;
         s_item[3] = J;
-        while (ld_acquire(ws.bdone + (int64_t)b * nb + I) < round) __nanosleep(100);
-        while (ld_acquire(ws.bdone + (int64_t)b * nb + J) < round) __nanosleep(100);
+        while (ld_acquire(ws.bdone + (int64_t)b * nb + I) < round) __nanosleep(WT_SVD_SPIN_NS);
+        while (ld_acquire(ws.bdone + (int64_t)b * nb + J) < round) __nanosleep(WT_SVD_SPIN_NS);
         if (SPLIT > 1) {
           int skip = ws.conv[b] != 0;
           if (!skip && ws.pclean) {
@@ -630,9 +634,17 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) svd_sweep_kernel(SvdWs w
       __syncthreads();  // every store of the visit precedes the release below (and s_item reuse)
     }
     if (threadIdx.x == 0 && rank == 0) {
+#if WT_SVD_LIGHT_RELEASE
+      // one acq_rel fence then two relaxed stores: a release of both counters
+      // (the CTA / cluster barrier above orders every thread's stores first)
+      asm volatile("fence.acq_rel.gpu;" ::: "memory");
+      st_relaxed(ws.bdone + (int64_t)b * nb + I, round + 1);
+      st_relaxed(ws.bdone + (int64_t)b * nb + J, round + 1);
+#else
       __threadfence();
       st_release(ws.bdone + (int64_t)b * nb + I, round + 1);
       st_release(ws.bdone + (int64_t)b * nb + J, round + 1);
+#endif
     }
   }
 }
