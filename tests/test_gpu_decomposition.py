@@ -185,6 +185,17 @@ def test_cluster_split_visits(monkeypatch, split):
         assert np.max(np.abs(g - np.eye(512))) < 1e-11
 
 
+@pytest.mark.parametrize("shape", [(1, 70, 130), (2, 200, 33), (5, 64, 64)])
+def test_cluster_split_small_and_ragged(monkeypatch, shape):
+    """Forced 8-CTA clusters on panels with fewer row chunks than CTAs (the host
+    clamps the split to one chunk per CTA), wide and tall slices."""
+    a_np = np.random.default_rng(sum(shape)).standard_normal(shape)
+    monkeypatch.setenv("WT_SVD_SPLIT", "8")
+    sigma, vec, info = E.svd(torch.from_numpy(a_np).cuda(), min(shape[1:]))
+    E.raise_if_failed(info)
+    assert sigma_err(sigma.cpu().numpy(), np.linalg.svd(a_np, compute_uv=False)) < 1e-12
+
+
 def test_concurrent_host_threads_on_own_streams():
     """The API is pure (SPEC concurrency sections): host threads driving their own
     CUDA streams get the serial results bit for bit (per-thread host state in K4)."""

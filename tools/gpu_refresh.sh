@@ -10,3 +10,4 @@ timeout 600 ncu --set full --clock-control none --import-source on -k regex:svd_
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:svd_sweep_kernel --launch-skip 6 -c 1 -o gpurun_out/k4_cfg4 -f python tools/svd_one.py 4 > gpurun_out/ncu_k4_4.log 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:gemm_f64_kernel -c 1 -o gpurun_out/gemm -f python tools/gemm_one.py > gpurun_out/ncu_gemm.log 2>&1
 timeout 600 ncu --set full --clock-control none -k regex:"fwd_|inv_" -c 8 -o gpurun_out/lift -f python tools/lift_one.py 1 2 4 8 > gpurun_out/ncu_lift.log 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:svd_sweep_kernel --launch-skip 6 -c 1 -o gpurun_out/k4_split -f python tools/svd_split_one.py > gpurun_out/ncu_k4_split.log 2>&1
