@@ -83,6 +83,19 @@ __device__ __forceinline__ double nanmax(double a, double b) {
   return (isnan(a) || isnan(b)) ? (a + b) : fmax(a, b);
 }
 
+// Rounds whose visits rotate only the block I x block J pairs.  cross = 0:
+// none; cross = 1: every round but round 0; cross = F >= 2: all but F evenly
+// spaced "full" rounds (round 0 and the last round among them), which also
+// rotate the within-block pairs.
+__host__ __device__ __forceinline__ int cross_only_round(int cross, int round, int nb) {
+  if (!cross || round == 0) return 0;
+  if (cross == 1) return 1;
+  const int last = nb - 2;
+  for (int j = 1; j < cross; ++j)
+    if (round == (j * last) / (cross - 1)) return 0;
+  return 1;
+}
+
 __device__ __forceinline__ int rr_index(int pos, int round, int nb) {
   // circle method: position 0 fixed, the others rotate by `round`
   return pos == 0 ? 0 : 1 + (pos - 1 + round) % (nb - 1);
@@ -626,7 +639,8 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) svd_sweep_kernel(SvdWs w
       return;
     }
     const int round = t / per_round;
-    if (!skip) pair_visit<SPLIT>(S, ws, b, I, J, mpad, npad, tol, inner_sweeps, cross && round > 0, rank);
+    const int cross_only = cross_only_round(cross, round, nb);
+    if (!skip) pair_visit<SPLIT>(S, ws, b, I, J, mpad, npad, tol, inner_sweeps, cross_only, rank);
     if constexpr (SPLIT > 1) {
       __threadfence();  // every CTA's stores of the visit, before the leader's release below
       cluster_sync();
@@ -954,14 +968,19 @@ int jacobi(const double* A, int64_t lda, int64_t strideA, int64_t n1,
   int inner = 1;
   if (const char* e = getenv("WT_SVD_INNER_SWEEPS")) inner = std::max(1, std::min(kMaxInnerSweeps, atoi(e)));
   bool hit_max = true;
-  // Round 0 of a sweep visits every block once with the full 32-column inner
-  // sweep (all within-block pairs); later rounds rotate (and test) only the
-  // cross-block pairs, so every column pair is still covered once per sweep (a
-  // cyclic ordering) with 16 instead of 31 eigen steps per visit.  Costs ~1-2
-  // extra sweeps; measured (round 1, tools/svd_probe.py, compare_products.py):
-  // 256 columns -9%, 1024 -3.5%, 384 (t-svd embeddings) -22%, but 128 +5%
-  // (few rounds per sweep, latency-bound), hence only from 16 blocks up.
-  int cross = nb >= 16;
+  // Full rounds visit every block once with the full 32-column inner sweep
+  // (all within-block pairs); the other rounds rotate (and test) only the
+  // cross-block pairs, so every column pair is still covered at least once per
+  // sweep with 16 instead of 31 eigen steps per visit.  Round 0 alone full
+  // (round 1: 256 columns -9%, 1024 -3.5%, 384 (t-svd embeddings) -22%, 128
+  // +5%, hence only from 16 blocks up) cost 1-4 extra sweeps: the cross
+  // rotations disturb the within-block pairs for a whole sweep.  F = nb / 8
+  // evenly spaced full rounds (2..4, round 0 and the last among them) win back
+  // the sweeps (session 3, tools/svd_concurrency.py, ms / sweeps): config 3
+  // 20.5 / 14 -> 18.6 / 12 (F = 2), config 4 158 / 16 -> 143 / 15 (F = 4),
+  // the config-5 operators' pseudo-inverse pair 28.1 -> 24.2 (F = 4),
+  // 4 x 1024^2 33.7 / 15 -> 31.2 / 13.
+  int cross = nb >= 16 ? std::max(2, std::min(4, nb / 8)) : 0;
   if (const char* e = getenv("WT_SVD_CROSS")) cross = atoi(e);
   // Reorder the columns by descending norm before every sweep: measured on the
   // config-3/4 slices 13 -> 12 and 17 -> 16 sweeps, -10% time (round 1).
@@ -1024,7 +1043,7 @@ int jacobi(const double* A, int64_t lda, int64_t strideA, int64_t n1,
     } else {
       for (int round = 0; round < nb - 1; ++round) {
         svd_pair_kernel<<<dim3(nb / 2, (unsigned)n_active), kThreads, sizeof(PairSmem), st>>>(
-            ws, L.mpad, L.npad, round, tol, inner, cross && round > 0);
+            ws, L.mpad, L.npad, round, tol, inner, cross_only_round(cross, round, nb));
       }
     }
     if (int e = check_launch("svd_pair_kernel")) return e;
