@@ -1,19 +1,26 @@
 #!/usr/bin/env python
-"""Benchmark of the w-product hot path on B200 (contract: see DESIGN.md section 7).
+"""Benchmark of the w-product hot path on B200 (contract: DESIGN.md section 7).
 
-Primary line (BASELINE.json configs[1]): forward + inverse lifting transform of a
-512x512x256 float64 cube at L = 1, 2, 4, 8; one step = the four round trips;
-metric = algorithmic HBM bytes moved per second (16 B per element per direction).
-`workloads` adds the other configs measured in the same run (N=1):
-w-svd (config 3) and sp-w-svd (config 4) tensor-elems/s, the config-5 deblur
-recovery and the config-1 w-product.
+Headline (BASELINE.json metric "w-svd rank-k reconstruct tensor-elems/s ...
+1/2/4/8 GPU", configs[3]): ``sp_w_svd`` rank-30 reconstruction of the
+1024x1024x256 float64 hyperspectral cube at L = 4.  One step = one call on the
+device-resident cube (2 GiB in, 2 GiB out: larger than L2); value = tensor
+elements reconstructed per second.  N > 1 (torchrun, one rank per GPU): the
+same cube, rows sharded over the ranks (strong scaling); K1 stores the coarse
+wavelet slices straight into the owning GPU's buffer, K4 decomposes them there
+and K2 loads the reconstructed rows back (``sharded.sp_w_svd_fused``).
+
+Secondary keys of the same line: ``transform`` (BASELINE configs[1], lifting
+round trips at L = 1, 2, 4, 8, HBM GB/s) and, at N = 1, ``workloads`` for
+configs 1, 3 and 5, each with a same-run CPU baseline (the multi-threaded
+oracle port, full size, median of 3) and the roofline of its dominant kernel.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                  [--workloads transform,wsvd,spwsvd,deblur,wproduct | none]
+                  [--workloads wsvd,deblur,wproduct,comparators | none]
 
-N > 1: one process per GPU under torchrun; the transform is weak-scaled (one
-cube per rank, no collective), sp-w-svd is sharded (rows -> all-to-all ->
-slices) across the ranks.
+``--impl reference`` times the reference algorithm on the host cores (the
+oracle port, ``oracle/parallel.py``: numpy + LAPACK dgesdd, all host threads)
+on the same workload, metric and config.
 """
 
 from __future__ import annotations
@@ -31,9 +38,25 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+METRIC = "w-svd rank-k reconstruct tensor-elems/s"
+UNIT = "tensor-elems/s"
+CFG4 = (1024, 1024, 256)
+CFG4_RANK, CFG4_LEVELS = 30, 4
 CFG2 = (512, 512, 256)
 CFG2_LEVELS = (1, 2, 4, 8)
-METRIC = "lifting transform HBM GB/s (fwd+inv, L=1,2,4,8); w-svd rank-k reconstruct tensor-elems/s in workloads"
+DATA = ("synthetic: seeded hyperspectral cube (paper_2601_08228_b200/synth.py, BASELINE configs[2-4] "
+        "generator; the paper's datasets are not available); i.i.d. normal cube for the transform key")
+
+
+def headline_config():
+    """Identical in both arms (the driver compares them)."""
+    n1, n2, p = CFG4
+    return {"workload": f"sp_w_svd rank-{CFG4_RANK} reconstruction of the {n1}x{n2}x{p} f64 hyperspectral "
+                        f"cube, L={CFG4_LEVELS} (BASELINE configs[3]); one call per step",
+            "cube": list(CFG4), "rank": CFG4_RANK, "levels": CFG4_LEVELS,
+            "generator": "synth.hyperspectral_cube(1024, 1024, 256, seed=0): 10 endmembers, Dirichlet(0.5) "
+                         "abundances smoothed sigma=4 px, 3-bump spectra, noise 0.01, clipped to [0, 1]",
+            "l2": "2 GiB input and 2 GiB output per step, larger than the 126 MB L2"}
 
 
 def parse():
@@ -58,7 +81,7 @@ def dist_env():
     return ws, rank, local
 
 
-def load_peaks():
+def hbm_peak():
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
         d = json.load(open(path))
@@ -68,7 +91,8 @@ def load_peaks():
 
 
 def fp64_peak():
-    """DMMA FP64 peak measured on this pool (tools/fp64_peak.cu -> profiles/fp64_peak_r01.jsonl)."""
+    """DMMA FP64 peak measured on this pool (tools/fp64_peak.cu -> profiles/fp64_peak_r01.jsonl);
+    MEASURED_PEAKS.json has no FP64 entry."""
     path = os.path.join(ROOT, "profiles", "fp64_peak_r01.jsonl")
     try:
         best = 0.0
@@ -83,12 +107,23 @@ def fp64_peak():
     return 37.0, "fallback (B200 FP64 tensor, measured 36.99 TF in round 1)"
 
 
-def traffic_of(kernel):
-    path = os.path.join(ROOT, "profiles", "traffic_r01.json")
+def profile_value(name, key):
+    """Per-launch DRAM traffic etc. recorded from an ncu capture (profiles/traffic_r02.json)."""
+    for fn in ("traffic_r02.json", "traffic_r01.json"):
+        try:
+            v = json.load(open(os.path.join(ROOT, "profiles", fn))).get(name)
+        except Exception:  # noqa: BLE001
+            continue
+        if v is not None:
+            return v.get(key) if isinstance(v, dict) else v
+    return None
+
+
+def host_threads() -> int:
     try:
-        return json.load(open(path)).get(kernel)
-    except Exception:  # noqa: BLE001
-        return None
+        return max(1, len(os.sched_getaffinity(0)))
+    except AttributeError:  # pragma: no cover
+        return max(1, os.cpu_count() or 1)
 
 
 class ClockSampler:
@@ -148,29 +183,6 @@ class ClockSampler:
 
 # --------------------------------------------------------------- timing ----
 
-class KernelTimer:
-    """CUDA events around each launch of the dominant kernel, on its stream."""
-
-    def __init__(self):
-        self.pairs = []
-
-    def wrap(self, fn):
-        import torch
-
-        s = torch.cuda.Event(enable_timing=True)
-        e = torch.cuda.Event(enable_timing=True)
-        s.record()
-        out = fn()
-        e.record()
-        self.pairs.append((s, e))
-        return out
-
-    def mean_ms(self):
-        if not self.pairs:
-            return None
-        return sum(s.elapsed_time(e) for s, e in self.pairs) / len(self.pairs)
-
-
 def timed_region(step_fn, steps, warmup, dist=None, sampler=None):
     """W warm-up steps, then exactly K steps bracketed by barrier + synchronize;
     returns the max over ranks of the device time (ms) of the K steps."""
@@ -209,9 +221,233 @@ class _Null:
         return False
 
 
-# ----------------------------------------------------------- workloads ----
+class PhaseTimer:
+    """CUDA events around every call of selected engine entry points (K4 = E.svd,
+    K3 = E.gemm), recorded on the stream they launch on (torch's current stream)
+    while `on` is set; mean device ms per call of each."""
 
-def transform_workload(args, dist, rank, ws):
+    def __init__(self, names=("svd", "gemm")):
+        from paper_2601_08228_b200 import engine as E
+
+        self.E = E
+        self.names = names
+        self.pairs = {n: [] for n in names}
+        self.on = False
+        self._orig = {}
+
+    def __enter__(self):
+        import torch
+
+        for n in self.names:
+            orig = getattr(self.E, n)
+            self._orig[n] = orig
+
+            def wrapped(*a, _orig=orig, _n=n, **k):
+                if not self.on:
+                    return _orig(*a, **k)
+                s = torch.cuda.Event(enable_timing=True)
+                e = torch.cuda.Event(enable_timing=True)
+                s.record()
+                out = _orig(*a, **k)
+                e.record()
+                self.pairs[_n].append((s, e))
+                return out
+
+            setattr(self.E, n, wrapped)
+        return self
+
+    def __exit__(self, *exc):
+        for n, f in self._orig.items():
+            setattr(self.E, n, f)
+        return False
+
+    def total_ms(self, name):
+        return sum(s.elapsed_time(e) for s, e in self.pairs[name])
+
+    def calls(self, name):
+        return len(self.pairs[name])
+
+
+def count_launches(fn):
+    """Kernels of the repo's own library launched by one call of fn (CUPTI via
+    torch.profiler; torch / NCCL / library kernels excluded).  Returns (count, names)."""
+    import torch
+    from torch.profiler import ProfilerActivity, profile
+
+    torch.cuda.synchronize()
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        fn()
+        torch.cuda.synchronize()
+    names = {}
+    foreign = ("at::", "nccl", "cublas", "cutlass", "xmma", "Memcpy", "Memset", "cudnn", "triton", "c10::",
+               "elementwise_kernel", "reduce_kernel")
+    for ev in prof.events():
+        if getattr(ev, "device_type", None) is None or "CUDA" not in str(ev.device_type):
+            continue
+        nm = ev.name
+        if any(f in nm for f in foreign):
+            continue
+        names[nm] = names.get(nm, 0) + 1
+    return sum(names.values()), names
+
+
+# ------------------------------------------------------------ CPU legs ----
+
+def cpu_median(fn, reps=3, warm=1):
+    for _ in range(warm):
+        fn()
+    ts = []
+    for _ in range(reps):
+        t = time.perf_counter()
+        fn()
+        ts.append(time.perf_counter() - t)
+    return statistics.median(ts), ts
+
+
+def cpu_port_baseline(fn, unit_value, unit, sample, reps=3):
+    """Same-run CPU baseline: the oracle port (oracle/parallel.py) on the FULL
+    workload, all host threads, 1 warm-up + median of `reps` calls."""
+    from oracle import parallel as P
+
+    with P.Pool() as pool:
+        med, ts = cpu_median(lambda: fn(pool), reps)
+        threads = pool.threads
+    return {"value": unit_value(med), "unit": unit, "cores": threads, "kind": "port",
+            "ms_per_call": round(med * 1e3, 1), "calls_s": [round(t, 3) for t in ts],
+            "sample": f"{sample}; full size, 1 warm-up + median of {reps} calls, numpy + LAPACK dgesdd / "
+                      f"BLAS dgemm (oracle/parallel.py) over {threads} host threads"}
+
+
+# ------------------------------------------------------------ headline ----
+
+def cfg4_cube(rank=0):
+    from paper_2601_08228_b200 import synth
+
+    n1, n2, p = CFG4
+    return synth.hyperspectral_cube(n1, n2, p, seed=0)
+
+
+def svd_flops(n1, n2):
+    """Golub-Kahan thin-SVD count: 14 m n^2 + 8 n^3, m >= n."""
+    m, n = max(n1, n2), min(n1, n2)
+    return 14 * m * n * n + 8 * n ** 3
+
+
+def headline_single(args, x_host, sampler):
+    import torch
+
+    from paper_2601_08228_b200 import engine as E
+    import paper_2601_08228_b200 as W
+    from paper_2601_08228_b200.decomposition import sp_w_svd_device
+
+    n1, n2, p = CFG4
+    r, L = CFG4_RANK, CFG4_LEVELS
+    N = n1 * n2 * p
+    x = torch.from_numpy(x_host).cuda()
+    out = torch.empty_like(x)
+    info = {}
+    with PhaseTimer() as pt:
+        def step(record):
+            pt.on = record
+            sp_w_svd_device(x, r, L, out=out)
+            if record:
+                info["sweeps"] = E.last_sweeps()
+                info["jflops"] = E.last_jacobi_flops()
+
+        ms = timed_region(step, args.steps, args.warmup, None, sampler)
+        k4_ms = pt.total_ms("svd") / max(pt.calls("svd"), 1)
+        k3_ms = pt.total_ms("gemm") / max(pt.calls("gemm"), 1) if pt.calls("gemm") else None
+    per_call = ms / args.steps
+    peak, src = fp64_peak()
+    flops = 2 * (p >> L) * svd_flops(n1, n2)
+    ach = flops / (k4_ms * 1e-3) / 1e12
+    roofline = {"bound": "tensor", "kernel": "K4 wt_svd_jacobi_f64 (every launch of one call: preconditioner + "
+                                              "Jacobi sweeps + sort; the 32 coarse 1024^2 slices)",
+                "achieved": round(ach, 3), "peak": peak, "unit": "TFLOP/s", "frac": round(ach / peak, 4),
+                "peak_source": src, "traffic": profile_value("K4_cfg4", "dram_bytes_per_call"),
+                "flops_per_launch": flops,
+                "flops_model": "32 x (14 m n^2 + 8 n^3), m = n = 1024 (Golub-Kahan thin SVD, SURVEY 8(d))",
+                "k4_ms_per_call": round(k4_ms, 3), "share_of_step": round(k4_ms / per_call, 4),
+                "executed_jacobi_tflops": round(info["jflops"] / (k4_ms * 1e-3) / 1e12, 3),
+                "jacobi_sweeps": info["sweeps"]}
+    n_launch, names = count_launches(lambda: sp_w_svd_device(x, r, L, out=out))
+    # e2e: the public API on host (numpy) arrays -- H2D of the cube and D2H of the
+    # reconstruction inside every call (decomposition.sp_w_svd)
+    e2e_steps = max(1, min(args.steps, 5))
+    W.sp_w_svd(x_host, r, L)
+    torch.cuda.synchronize()
+    t = time.perf_counter()
+    for _ in range(e2e_steps):
+        y_host = W.sp_w_svd(x_host, r, L)
+    e2e_s = (time.perf_counter() - t) / e2e_steps
+    e2e = {"value": round(N / e2e_s, 1), "unit": UNIT, "h2d_bytes_per_step": 8 * N, "d2h_bytes_per_step": 8 * N,
+           "ms_per_call": round(e2e_s * 1e3, 2), "steps": e2e_steps,
+           "api": "sp_w_svd(numpy cube, 30, 4) -> numpy reconstruction (pinned staging, H2D and D2H inside)"}
+    return {"ms": ms, "value": N * args.steps / (ms * 1e-3), "roofline": roofline, "e2e": e2e,
+            "gpu_launches": n_launch * args.steps, "launch_names": names, "y_host": y_host,
+            "k3_ms": k3_ms}
+
+
+def headline_sharded(args, dist, sampler):
+    """Strong scaling: one cube, rows sharded over the ranks (sharded.sp_w_svd_fused)."""
+    import torch
+
+    from paper_2601_08228_b200 import sharded as SH
+
+    ws, rank = dist.get_world_size(), dist.get_rank()
+    n1, n2, p = CFG4
+    r, L = CFG4_RANK, CFG4_LEVELS
+    N = n1 * n2 * p
+    rows = SH.splits(n1, ws)
+    r0 = sum(rows[:rank])
+    if rank == 0:
+        cube = torch.from_numpy(cfg4_cube()).cuda()
+    else:
+        cube = torch.empty(CFG4, dtype=torch.float64, device="cuda")
+    dist.broadcast(cube, src=0)
+    x = cube[r0:r0 + rows[rank]].contiguous()
+    x_host = cube[r0:r0 + rows[rank]].cpu().pin_memory()
+    del cube
+    info = {}
+
+    def step(record):
+        info["y"] = SH.sp_w_svd_fused(x, r, L, n1)
+
+    ms = timed_region(step, args.steps, args.warmup, dist, sampler)
+    # per-phase device times of one call (events inside the fused exchange)
+    phases = SH.sp_w_svd_fused(x, r, L, n1, phase_times=True)[1]
+    ms_nccl = timed_region(lambda rec: SH.sp_w_svd_sharded(x, r, L, n1), 3, 1, dist)
+    peak, src = fp64_peak()
+    m = p >> L
+    ks = SH.splits(2 * m, ws)
+    flops = ks[rank] * svd_flops(n1, n2)
+    k4 = phases.get("k4_ms") or 0.0
+    ach = flops / (k4 * 1e-3) / 1e12 if k4 > 0 else 0.0
+    roofline = {"bound": "tensor", "kernel": f"K4 on this rank's {ks[rank]} coarse 1024^2 slices (rank {rank})",
+                "achieved": round(ach, 3), "peak": peak, "unit": "TFLOP/s", "frac": round(ach / peak, 4),
+                "peak_source": src, "traffic": None, "flops_per_launch": flops}
+    y_pin = torch.empty_like(x_host).pin_memory()
+
+    def e2e_step(record):
+        xd = x_host.to("cuda", non_blocking=True)
+        y = SH.sp_w_svd_fused(xd, r, L, n1)
+        y_pin.copy_(y, non_blocking=True)
+
+    e2e_steps = max(1, min(args.steps, 5))
+    e2e_ms = timed_region(e2e_step, e2e_steps, 1, dist)
+    e2e = {"value": round(N * e2e_steps / (e2e_ms * 1e-3), 1), "unit": UNIT,
+           "h2d_bytes_per_step": 8 * N, "d2h_bytes_per_step": 8 * N,
+           "api": "per rank: its pinned host rows H2D, sharded.sp_w_svd_fused, its rows of the result D2H"}
+    return {"ms": ms, "value": N * args.steps / (ms * 1e-3), "roofline": roofline, "e2e": e2e,
+            "phases_ms_rank": phases, "nccl_variant_ms_per_call": ms_nccl / 3,
+            "gpu_launches": None}
+
+
+# ----------------------------------------------------------- transform ----
+
+def transform_key(args, dist, rank, ws, with_cpu):
+    """BASELINE configs[1]: forward + inverse lifting at L = 1, 2, 4, 8 on a
+    resident 512x512x256 cube per rank (weak: one cube per rank), HBM GB/s."""
     import torch
 
     from paper_2601_08228_b200 import engine as E
@@ -223,126 +459,125 @@ def transform_workload(args, dist, rank, ws):
     x = torch.from_numpy(x_host).cuda()
     bufs = {L: torch.empty((p, n1, n2), dtype=torch.float64, device="cuda") for L in CFG2_LEVELS}
     y = torch.empty_like(x)
-    kt_f, kt_i = KernelTimer(), KernelTimer()
+    ev = {"f": [], "i": []}
 
     def step(record):
         for L in CFG2_LEVELS:
             if record:
-                kt_f.wrap(lambda: E.lift_forward(x, L, out=bufs[L]))
-                kt_i.wrap(lambda: E.lift_inverse(bufs[L], n1, n2, p, L, out=y))
+                for k, fn in (("f", lambda: E.lift_forward(x, L, out=bufs[L])),
+                              ("i", lambda: E.lift_inverse(bufs[L], n1, n2, p, L, out=y))):
+                    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    s.record()
+                    fn()
+                    e.record()
+                    ev[k].append((s, e))
             else:
                 E.lift_forward(x, L, out=bufs[L])
                 E.lift_inverse(bufs[L], n1, n2, p, L, out=y)
 
-    sampler = ClockSampler(torch.cuda.current_device())
-    ms = timed_region(step, args.steps, args.warmup, dist, sampler)
-    # parity of the last step (bit-exact round trip is checked by the tests)
-    rt = float((y - x).norm() / x.norm())
+    steps = max(3, min(args.steps, 10))
+    ms = timed_region(step, steps, 2, dist)
+    assert float((y - x).norm() / x.norm()) < 1e-12
     bytes_step = len(CFG2_LEVELS) * 2 * 16 * N
-    value = ws * bytes_step * args.steps / (ms * 1e-3) / 1e9
-    peak, peak_src = load_peaks()
-    f_ms, i_ms = kt_f.mean_ms(), kt_i.mean_ms()
-    per_launch = 16 * N
-    ach_f = per_launch / (f_ms * 1e-3) / 1e9
-    ach_i = per_launch / (i_ms * 1e-3) / 1e9
-    # kernel names as in the ncu launch list (csrc/lift_fast.cu): K1 = fwd_shallow<W>
-    # (L <= 3), fwd_persistent<TQ> (L = 4, 5), fwd_persistent1<32> (L >= 6);
-    # K2 = inv_persistent<16, TMA>
-    dom = "K1_forward" if f_ms >= i_ms else "K2_inverse"
-    ach = ach_f if dom == "K1_forward" else ach_i
-    roofline = {"bound": "hbm", "kernel": dom, "achieved": round(ach, 1), "peak": peak,
-                "unit": "GB/s", "frac": round(ach / peak, 4), "peak_source": peak_src,
-                "traffic": traffic_of(dom), "algorithmic_bytes_per_launch": per_launch,
-                "kernels": {"K1_forward": "fwd_shallow<1|2> (L=1,2), fwd_persistent<64> (L=4), "
-                                          "fwd_persistent1<32> (L=8)",
-                            "K2_inverse": "inv_persistent<16, TMA>"},
-                "per_kernel": {"K1_forward": {"ms": round(f_ms, 4), "GBps": round(ach_f, 1),
-                                              "frac": round(ach_f / peak, 4)},
-                               "K2_inverse": {"ms": round(i_ms, 4), "GBps": round(ach_i, 1),
-                                              "frac": round(ach_i / peak, 4)}}}
-
-    # e2e: the public API (forward_w / inverse_w on CUDA tensors) with the
-    # step's input copied in from pinned host memory and its result read back
-    # into pinned host memory, every step, inside the timed region.
-    # The transform is row-separable, so the harness streams the cube through
-    # the API in row chunks on three CUDA streams (H2D | transform | D2H
-    # overlap, PCIe full duplex) -- the way a user would drive it.
-    x_pin = torch.from_numpy(x_host).pin_memory()
-    y_pin = torch.empty_like(x_pin).pin_memory()
-    s_in, s_cmp, s_out = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
-    chunks = int(os.environ.get("WT_E2E_CHUNKS", "8"))  # row chunks per L (pipeline fill/drain ~1/chunks)
-    rows = n1 // chunks
-
-    # The step's input is the one cube (uploaded once per step, chunk by
-    # chunk); its results are the four round trips y_L, each read back.
-    def e2e_step(record):
-        main = torch.cuda.current_stream()
-        s_in.wait_stream(main)
-        for c in range(chunks):
-            sl = slice(c * rows, (c + 1) * rows)
-            with torch.cuda.stream(s_in):
-                xd = x_pin[sl].to("cuda", non_blocking=True)
-            s_cmp.wait_stream(s_in)
-            for L in CFG2_LEVELS:
-                with torch.cuda.stream(s_cmp):
-                    xd.record_stream(s_cmp)
-                    yd = W.inverse_w(W.forward_w(xd, L))
-                s_out.wait_stream(s_cmp)
-                with torch.cuda.stream(s_out):
-                    yd.record_stream(s_out)
-                    y_pin[sl].copy_(yd, non_blocking=True)
-        main.wait_stream(s_out)
-
-    e2e_steps = max(1, min(args.steps, 5))
-    e2e_ms = timed_region(e2e_step, e2e_steps, 1, dist)
-    # a lifting round trip reproduces x to rounding (not bit-exactly): SPEC.md:124
-    assert float((y_pin - x_pin).norm() / x_pin.norm()) < 1e-12
-    e2e = {"value": round(ws * bytes_step * e2e_steps / (e2e_ms * 1e-3) / 1e9, 3), "unit": "GB/s",
-           "h2d_bytes_per_step": 8 * N,
-           "d2h_bytes_per_step": len(CFG2_LEVELS) * 8 * N,
-           "api": f"y_L = inverse_w(forward_w(x_cuda, L)) for L = 1, 2, 4, 8 on {chunks} row chunks; "
-                  "x H2D from pinned once per step, every y_L D2H to pinned, copies overlapped with "
-                  "the transform on 3 streams",
-           "steps": e2e_steps}
-    # the numpy drop-in path (reference call shapes: host arrays in, host pyramid out/in)
-    for L in CFG2_LEVELS:  # warm-up: pinned staging / result buffers enter the host caching allocator
-        out = W.inverse_w(W.forward_w(x_host, L))
-    del out
+    peak, src = hbm_peak()
+    f_ms = sum(s.elapsed_time(e) for s, e in ev["f"]) / len(ev["f"])
+    i_ms = sum(s.elapsed_time(e) for s, e in ev["i"]) / len(ev["i"])
+    per = 16 * N
+    af, ai = per / (f_ms * 1e-3) / 1e9, per / (i_ms * 1e-3) / 1e9
+    out = {"config": "forward+inverse lifting 512x512x256 f64, L=1,2,4,8 per step (BASELINE configs[1]); "
+                     "one cube per rank", "metric": "HBM GB/s (algorithmic 16 B per element per direction)",
+           "value": round(ws * bytes_step * steps / (ms * 1e-3) / 1e9, 2), "unit": "GB/s", "steps": steps,
+           "roofline": {"bound": "hbm", "kernel": "K2_inverse" if i_ms >= f_ms else "K1_forward",
+                        "achieved": round(min(af, ai), 1), "peak": peak, "unit": "GB/s",
+                        "frac": round(min(af, ai) / peak, 4), "peak_source": src,
+                        "traffic": profile_value("K2_inverse" if i_ms >= f_ms else "K1_forward",
+                                                 "dram_bytes_per_launch"),
+                        "algorithmic_bytes_per_launch": per,
+                        "per_kernel": {"K1_forward": {"ms": round(f_ms, 4), "GBps": round(af, 1),
+                                                      "frac": round(af / peak, 4)},
+                                       "K2_inverse": {"ms": round(i_ms, 4), "GBps": round(ai, 1),
+                                                      "frac": round(ai / peak, 4)}}}}
+    # public API on host arrays (pyramid returned to the host, then inverted from it)
+    for L in CFG2_LEVELS:
+        W.inverse_w(W.forward_w(x_host, L))
     t = time.perf_counter()
-    n_np = 2
-    for _ in range(n_np):
-        for L in CFG2_LEVELS:
-            out = W.inverse_w(W.forward_w(x_host, L))
-    np_s = time.perf_counter() - t
-    assert float(np.linalg.norm((out - x_host).ravel()) / np.linalg.norm(x_host.ravel())) < 1e-12
-    e2e["numpy_dropin"] = {"value": round(bytes_step * n_np / np_s / 1e9, 3), "unit": "GB/s",
-                           "api": "inverse_w(forward_w(numpy, L)) per L (pyramid returned to host)",
-                           "h2d_bytes_per_step": len(CFG2_LEVELS) * 16 * N,
-                           "d2h_bytes_per_step": len(CFG2_LEVELS) * 16 * N}
-    return {"ms": ms, "value": value, "roofline": roofline, "e2e": e2e, "round_trip_relerr": rt,
-            "clocks": sampler.summary(), "launches": args.steps * len(CFG2_LEVELS) * 2,
-            "N": N, "x_host": x_host}
+    for L in CFG2_LEVELS:
+        o = W.inverse_w(W.forward_w(x_host, L))
+    dt = time.perf_counter() - t
+    assert float(np.linalg.norm((o - x_host).ravel()) / np.linalg.norm(x_host.ravel())) < 1e-12
+    out["e2e"] = {"value": round(bytes_step / dt / 1e9, 2), "unit": "GB/s",
+                  "api": "inverse_w(forward_w(numpy, L)) for L = 1, 2, 4, 8 (pyramid returned to host)",
+                  "h2d_bytes_per_step": len(CFG2_LEVELS) * 16 * N, "d2h_bytes_per_step": len(CFG2_LEVELS) * 16 * N}
+    if with_cpu:
+        from oracle import parallel as P
+
+        def run(pool):
+            for L in CFG2_LEVELS:
+                s, d = P.lift_forward(pool, x_host, L)
+                P.lift_inverse(pool, s, d)
+
+        out["cpu_baseline"] = cpu_port_baseline(run, lambda s: round(bytes_step / s / 1e9, 3), "GB/s",
+                                                "oracle forward + inverse transform, L = 1, 2, 4, 8, rows split "
+                                                "over the threads", reps=2)
+    return out
 
 
-def executed_roofline(jacobi_flops, ms_per_call):
-    """FP64 flops the Jacobi iteration actually executed (K4 Gram + rotation tiles,
-    counted by the kernel) per call, against the measured DMMA peak."""
+# ----------------------------------------------------------- workloads ----
+
+def wsvd_workload(args, steps=3, warmup=1):
+    """Config 3: w_svd rank 20 of the 256x256x192 cube, L = 3."""
+    import torch
+
+    from paper_2601_08228_b200 import engine as E
+    from paper_2601_08228_b200 import synth
+    from paper_2601_08228_b200.decomposition import w_svd_device
+    import paper_2601_08228_b200 as W
+
+    n1, n2, p, r, L = 256, 256, 192, 20, 3
+    x_host = synth.hyperspectral_cube(n1, n2, p, seed=0)
+    x = torch.from_numpy(x_host).cuda()
+    flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device="cuda")
+    info = {}
+    with PhaseTimer() as pt:
+        def step(record):
+            flush.zero_()  # 256 MB > L2: every call starts cold
+            pt.on = record
+            info["out"] = w_svd_device(x, r, L)
+            pt.on = False
+            info["sweeps"] = E.last_sweeps()
+
+        ms = timed_region(step, steps, warmup)
+        k4 = pt.total_ms("svd") / max(pt.calls("svd"), 1)
+    call_ms = ms / steps
+    N = n1 * n2 * p
+    flops = p * svd_flops(n1, n2)
     peak, src = fp64_peak()
-    ach = jacobi_flops / (ms_per_call * 1e-3) / 1e12
-    return {"bound": "tensor", "achieved": round(ach, 2), "peak": peak, "unit": "TFLOP/s",
-            "frac": round(ach / peak, 4), "peak_source": src,
-            "flops_model": "executed: 2 * mpad * 32^2 * (10/16 + 1) per rotated pair visit (wt_svd_last_jacobi_flops)",
-            "note": "whole sp/w-svd call time in the denominator (transforms, epilogues included)"}
+    ach = flops / (k4 * 1e-3) / 1e12
+    recon = info["out"][4].cpu().numpy()
+    from oracle import parallel as P
 
+    ref = {}
 
-def svd_flops(n1, n2):
-    m, n = max(n1, n2), min(n1, n2)
-    return 14 * m * n * n + 8 * n ** 3
+    def run(pool):
+        ref["o"] = P.w_svd(pool, x_host, r, L)
+
+    cpu = cpu_port_baseline(run, lambda s: round(N / s, 1), UNIT, "oracle w_svd(cube, 20, 3)")
+    rel = float(np.linalg.norm((recon - ref["o"]["recon"]).ravel()) / np.linalg.norm(ref["o"]["recon"].ravel()))
+    return {"config": "w_svd 256x256x192 rank 20 L=3 (BASELINE configs[2])", "metric": UNIT,
+            "value": N / (call_ms * 1e-3), "ms_per_call": call_ms, "jacobi_sweeps": info["sweeps"],
+            "roofline": {"bound": "tensor", "kernel": "K4 (192 wavelet slices 256^2)", "achieved": round(ach, 3),
+                         "peak": peak, "unit": "TFLOP/s", "frac": round(ach / peak, 4), "peak_source": src,
+                         "k4_ms_per_call": round(k4, 3),
+                         "flops_model": "192 x (14 m n^2 + 8 n^3) Golub-Kahan thin-SVD count (SURVEY 8d)"},
+            "l2": "256 MB flush before each call",
+            "e2e": {"ms_per_call": round(api_e2e(lambda: W.w_svd(x_host, r, L), 2), 2),
+                    "api": "w_svd(numpy cube, 20, 3) -> (SvdFactors of numpy arrays, numpy recon)",
+                    "h2d_bytes_per_call": 8 * N, "d2h_bytes_per_call": 8 * (N + p * (n1 + n2 + r) * r)},
+            "cpu_baseline": cpu, "recon_relerr_vs_cpu": rel}
 
 
 def api_e2e(fn, reps):
-    """Wall time (ms) of a synchronous public-API call on host (numpy) inputs: the
-    H2D of the inputs and the D2H of every returned array are inside."""
+    """Wall ms of a synchronous public-API call on host (numpy) inputs (H2D and D2H inside)."""
     import torch
 
     fn()
@@ -354,97 +589,8 @@ def api_e2e(fn, reps):
     return (time.perf_counter() - t) / reps * 1e3
 
 
-def oracle_sample(fn, scale, sample):
-    """Bounded CPU run of the oracle port (numpy + OpenBLAS LAPACK on all host
-    threads) scaled to the full workload."""
-    t = time.perf_counter()
-    fn()
-    dt = time.perf_counter() - t
-    return {"ms_per_call": round(dt * scale * 1e3, 1), "cores": host_threads(), "kind": "port",
-            "sample": f"{sample} ({dt:.2f} s, x{scale} to the full call)"}
-
-
-def wsvd_workload(args, steps=3, warmup=1):
-    import torch
-
-    from paper_2601_08228_b200 import engine as E
-    from paper_2601_08228_b200 import synth
-    from paper_2601_08228_b200.decomposition import w_svd_device
-
-    import paper_2601_08228_b200 as W
-    from oracle import wten_oracle as O
-
-    n1, n2, p, r, L = 256, 256, 192, 20, 3
-    x_host = synth.hyperspectral_cube(n1, n2, p, seed=0)
-    x = torch.from_numpy(x_host).cuda()
-    flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device="cuda")
-    sweeps = []
-
-    def step(record):
-        flush.zero_()  # 256 MB > L2: every step starts cold
-        w_svd_device(x, r, L)
-        sweeps.append((E.last_sweeps(), E.last_jacobi_flops()))
-
-    ms = timed_region(step, steps, warmup)
-    N = n1 * n2 * p
-    flops = p * svd_flops(n1, n2)
-    peak, src = fp64_peak()
-    ach = flops / (ms / steps * 1e-3) / 1e12
-    return {"config": "w_svd 256x256x192 rank 20 L=3 (BASELINE configs[2])", "metric": "tensor-elems/s",
-            "value": N * steps / (ms * 1e-3), "ms_per_call": ms / steps, "jacobi_sweeps": sweeps[-1][0],
-            "roofline_executed": executed_roofline(sweeps[-1][1], ms / steps),
-            "roofline": {"bound": "tensor", "achieved": round(ach, 2), "peak": peak,
-                         "unit": "TFLOP/s", "frac": round(ach / peak, 4), "peak_source": src,
-                         "flops_model": "192 x (14 m n^2 + 8 n^3) Golub-Kahan thin-SVD count (SURVEY 8d)"},
-            "l2": "256 MB flush before each call",
-            "e2e": {"ms_per_call": round(api_e2e(lambda: W.w_svd(x_host, r, L), 2), 2),
-                    "api": "w_svd(numpy cube, 20, 3) -> (SvdFactors of numpy arrays, numpy recon)",
-                    "h2d_bytes_per_call": 8 * N, "d2h_bytes_per_call": 8 * (N + p * (n1 + n2 + r) * r)},
-            "cpu_baseline": oracle_sample(lambda: O.w_svd(x_host[:, :, :24], r, L), 8,
-                                          "oracle w_svd on 24 of the 192 bands (L=3)")}
-
-
-def spwsvd_workload(args, steps=3, warmup=1):
-    import torch
-
-    from paper_2601_08228_b200 import engine as E
-    from paper_2601_08228_b200 import synth
-    from paper_2601_08228_b200.decomposition import sp_w_svd_device
-
-    import paper_2601_08228_b200 as W
-    from oracle import wten_oracle as O
-
-    n1, n2, p, r, L = 1024, 1024, 256, 30, 4
-    x_host = synth.hyperspectral_cube(n1, n2, p, seed=0)
-    x = torch.from_numpy(x_host).cuda()
-    out = torch.empty_like(x)
-    sweeps = []
-
-    def step(record):
-        sp_w_svd_device(x, r, L, out=out)
-        sweeps.append((E.last_sweeps(), E.last_jacobi_flops()))
-
-    ms = timed_region(step, steps, warmup)
-    N = n1 * n2 * p
-    flops = 2 * (p >> L) * svd_flops(n1, n2)
-    peak, src = fp64_peak()
-    ach = flops / (ms / steps * 1e-3) / 1e12
-    return {"config": "sp_w_svd 1024x1024x256 rank 30 L=4 (BASELINE configs[3])", "metric": "tensor-elems/s",
-            "value": N * steps / (ms * 1e-3), "ms_per_call": ms / steps, "jacobi_sweeps": sweeps[-1][0],
-            "roofline_executed": executed_roofline(sweeps[-1][1], ms / steps),
-            "roofline": {"bound": "tensor", "achieved": round(ach, 2), "peak": peak, "unit": "TFLOP/s",
-                         "frac": round(ach / peak, 4), "peak_source": src,
-                         "flops_model": "32 x 22 n^3 thin-SVD count (SURVEY 8d)"},
-            "l2": "2 GiB input > L2",
-            "e2e": {"ms_per_call": round(api_e2e(lambda: W.sp_w_svd(x_host, r, L), 1), 2),
-                    "api": "sp_w_svd(numpy cube, 30, 4) -> numpy recon",
-                    "h2d_bytes_per_call": 8 * N, "d2h_bytes_per_call": 8 * N},
-            "cpu_baseline": oracle_sample(lambda: O.sp_w_svd(x_host[:, :, :32], r, L), 8,
-                                          "oracle sp_w_svd on 32 of the 256 bands (L=4: 4 coarse "
-                                          "1024^2 SVDs of the 32)")}
-
-
 def deblur_workload(args, steps=2, warmup=1):
+    """Config 5: w-pinv deblurring recovery (2 pinv_w + 2 w_product), 512x512x128, L = 3."""
     import torch
 
     import paper_2601_08228_b200 as W
@@ -457,45 +603,65 @@ def deblur_workload(args, steps=2, warmup=1):
     aht = W.transpose(ahd)
     b = w_product_device(w_product_device(avd, xd, 3), aht, 3) + torch.from_numpy(eta).cuda()
     res = {}
+    with PhaseTimer() as pt:
+        def step(record):
+            pt.on = record
+            # imaging.deblur's device path: both pseudo-inverses in one batched K4 call
+            left, right = pinv_w_device_many([avd, aht], 3, 1e-3)
+            res["x"] = w_product_device(w_product_device(left, b, 3), right, 3)
+            pt.on = False
 
-    def step(record):
-        # imaging.deblur's device path: both pseudo-inverses in one batched K4 call
-        left, right = pinv_w_device_many([avd, aht], 3, 1e-3)
-        res["x"] = w_product_device(w_product_device(left, b, 3), right, 3)
-
-    ms = timed_region(step, steps, warmup)
-    # GEMM share: one w-product alone
-    g = {}
-
-    def gstep(record):
-        g["c"] = w_product_device(xd, avd, 3)
-
-    gms = timed_region(gstep, 3, 1)
+        ms = timed_region(step, steps, warmup)
+        k4 = pt.total_ms("svd") / max(pt.calls("svd"), 1)
+        k3 = pt.total_ms("gemm") / max(pt.calls("gemm"), 1)
+        k3_calls = pt.calls("gemm") / steps
     peak, src = fp64_peak()
-    gflops = 2 * 512 ** 3 * 128
+    svd_f = 2 * 128 * svd_flops(512, 512)
+    gemm_f = 2 * 512 ** 3 * 128
+    xr = res["x"].cpu().numpy()
+    b_host = b.cpu().numpy()
+    from oracle import parallel as P
+    from oracle import wten_oracle as O
+
+    ref = {}
+
+    def run(pool):
+        ref["x"] = P.deblur(pool, b_host, av, O.transpose(ah), 3, 1e-3)
+
+    cpu = cpu_port_baseline(run, lambda s: round(s, 3), "s per recovery",
+                            "oracle recovery w_product(w_product(pinv_w(A_V), B), pinv_w(A_H^T)), L=3, tol 1e-3")
+    rel = float(np.linalg.norm((xr - ref["x"]).ravel()) / np.linalg.norm(ref["x"].ravel()))
     return {"config": "w-pinv deblur 512x512x128, 9x9 Gaussian PSF sigma=2, L=3, tol 1e-3 (BASELINE configs[4])",
-            "metric": "s per recovery", "value": ms / steps / 1e3,
+            "metric": "s per recovery", "value": ms / steps / 1e3, "higher_is_better": False,
             "psnr_db": imaging.psnr(xd, res["x"]), "ssim": imaging.ssim(xd, res["x"]),
             "psnr_db_blurred_input": imaging.psnr(xd, b), "ssim_blurred_input": imaging.ssim(xd, b),
-            "quality_note": ("PSNR paper-verbatim 10 log10(N MPP / ||e||^2) (PAPER.md:878); matches the "
-                             "oracle (tests/test_gpu_imaging.py). Under the lazy-wavelet w-product a "
-                             "slice-constant operator has zero detail blocks, so blur keeps only the 8-band "
-                             "means (L=3) and the recovery is at best the band-averaged cube; the 9x9 sigma=2 "
-                             "Toeplitz operators also amplify the sigma=0.005 noise up to 1e3x per side. The "
-                             "recovery is poor by construction of the config (the paper's own Table IV deblur "
-                             "reaches 9.7 dB)"),
-            "w_product_ms": gms / 3,
-            "w_product_roofline": {"bound": "tensor", "achieved": round(gflops / (gms / 3 * 1e-3) / 1e12, 2),
-                                   "peak": peak, "unit": "TFLOP/s",
-                                   "frac": round(gflops / (gms / 3 * 1e-3) / 1e12 / peak, 4),
-                                   "peak_source": src, "note": "whole w-product incl. transforms"}}
+            "quality_note": ("PSNR paper-verbatim 10 log10(N MPP / ||e||^2) (PAPER.md:878). Under the lazy-wavelet "
+                             "w-product a slice-constant operator has zero detail blocks, so blur keeps only the "
+                             "8-band means and the 9x9 sigma=2 Toeplitz operators amplify the noise up to 1e3x "
+                             "per side: the recovery is poor by construction of the config"),
+            "roofline_k4_pinv": {"bound": "tensor", "kernel": "K4 on both operators' 256 wavelet slices of 512^2 "
+                                 "(224 exactly zero: retired at the first sort)",
+                                 "achieved": round(svd_f / (k4 * 1e-3) / 1e12, 3), "peak": peak, "unit": "TFLOP/s",
+                                 "frac": round(svd_f / (k4 * 1e-3) / 1e12 / peak, 4), "peak_source": src,
+                                 "k4_ms_per_call": round(k4, 3),
+                                 "flops_model": "2 x 128 x (14 m n^2 + 8 n^3), dense as the reference executes it"},
+            "roofline_k3_face_gemm": {"bound": "tensor", "kernel": "K3 face GEMM (128 x 512^3 per w-product)",
+                                      "achieved": round(gemm_f / (k3 * 1e-3) / 1e12, 3) if k3 else None,
+                                      "peak": peak, "unit": "TFLOP/s",
+                                      "frac": round(gemm_f / (k3 * 1e-3) / 1e12 / peak, 4) if k3 else None,
+                                      "gemm_calls_per_recovery": k3_calls, "k3_ms_per_call": round(k3, 4),
+                                      "note": "per K3 call of the two w-products (the pinv epilogue GEMMs are "
+                                              "smaller and excluded from the flop model)"},
+            "cpu_baseline": cpu, "recovery_relerr_vs_cpu": rel}
 
 
-def wproduct_workload(args, steps=20, warmup=3):
+def wproduct_workload(args, steps=50, warmup=5):
+    """Config 1: w_product 64x48x32 * 48x40x32, L = 1 (latency-bound)."""
     import torch
 
     from paper_2601_08228_b200 import synth
     from paper_2601_08228_b200.algebra import w_product_device
+    import paper_2601_08228_b200 as W
 
     a, b = synth.uniform_pair(0)
     ad, bd = torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()
@@ -504,13 +670,22 @@ def wproduct_workload(args, steps=20, warmup=3):
         w_product_device(ad, bd, 1)
 
     ms = timed_region(step, steps, warmup)
+    from oracle import wten_oracle as O
+
+    cpu_s, ts = cpu_median(lambda: O.w_product(a, b, 1), reps=5, warm=2)
     return {"config": "w_product 64x48x32 * 48x40x32 L=1 (BASELINE configs[0])", "metric": "us per call",
-            "value": ms / steps * 1e3}
+            "value": ms / steps * 1e3, "higher_is_better": False,
+            "roofline": {"bound": "latency", "note": "7.9 MFLOP and 3.9 MB per call: four launches "
+                         "(K1, K1, K3, K2) and their host overhead set the time"},
+            "e2e_us": round(api_e2e(lambda: W.w_product(a, b, 1), 20) * 1e3, 1),
+            "cpu_baseline": {"value": round(cpu_s * 1e6, 1), "unit": "us per call", "cores": 1, "kind": "port",
+                             "sample": "oracle w_product (numpy, one thread: the call is too small to split), "
+                                       "2 warm-ups + median of 5, full size"}}
 
 
 def comparators_workload(args):
-    """Paper-style ratios on B200 (SPEC acceptance 8): w- vs t- vs m-product
-    on a p = 256 cube and w-svd / sp-w-svd vs t-svd on the config-3 cube, device-resident."""
+    """Paper-style ratios on B200: w- vs t- vs m-product on a
+    p = 256 cube and w-svd / sp-w-svd vs t-svd on the config-3 cube, device-resident."""
     import torch
 
     import paper_2601_08228_b200 as W
@@ -535,80 +710,56 @@ def comparators_workload(args):
     out["speedup_w_vs_t_svd"] = out["t_svd_ms"] / out["w_svd_ms"]
     out["speedup_spw_vs_t_svd"] = out["t_svd_ms"] / out["sp_w_svd_ms"]
     out["op_counts"] = {k: B.op_count(k, p, p, p, p).count for k in "mtw"}
-    out["note"] = ("t-product family: cuFFT along mode 3 + the same DMMA GEMM / Jacobi SVD kernels "
-                   "(complex slices via 4 real GEMMs / the real embedding), p//2+1 frequencies")
     return out
 
 
-# ----------------------------------------------------------- CPU legs ----
-
-def host_threads() -> int:
-    try:
-        return max(1, len(os.sched_getaffinity(0)))
-    except AttributeError:  # pragma: no cover
-        return max(1, os.cpu_count() or 1)
-
-
-def oracle_round_trips(slab, reps, threads):
-    """reps x (forward + inverse at L = 1, 2, 4, 8) of the oracle port over `slab`,
-    row-split over `threads` host threads (the transform is row-separable; numpy
-    releases the GIL inside its strided ufunc loops).  Returns wall seconds."""
-    from concurrent.futures import ThreadPoolExecutor
-
-    from oracle import wten_oracle as O
-
-    parts = [p for p in np.array_split(slab, threads, axis=0) if p.shape[0]]
-
-    def one(part):
-        for L in CFG2_LEVELS:
-            s, d = O.lift_forward(part, L)
-            O.lift_inverse(s, d)
-
-    with ThreadPoolExecutor(max_workers=len(parts)) as pool:
-        t = time.perf_counter()
-        for _ in range(reps):
-            list(pool.map(one, parts))
-        return time.perf_counter() - t
-
-
-def cpu_transform_sample(x_host, reps=2, rows=512):
-    """Oracle (numpy port of lifting.py) on a bounded slab of the config-2 cube,
-    on all the host threads this process may use."""
-    slab = np.ascontiguousarray(x_host[:rows])
-    threads = host_threads()
-    dt = oracle_round_trips(slab, reps, threads)
-    gbs = reps * len(CFG2_LEVELS) * 32 * slab.size / dt / 1e9
-    return {"value": round(gbs, 4), "unit": "GB/s", "cores": threads, "kind": "port",
-            "sample": f"oracle lift_forward+lift_inverse, L=1,2,4,8, slab {rows}x512x256 of the config-2 cube "
-                      f"row-split over {threads} threads, {reps} reps ({dt:.1f} s)"}
-
+# ------------------------------------------------------- reference arm ----
 
 def run_reference(args):
+    """The reference algorithm (oracle port: numpy + LAPACK dgesdd over all host
+    threads, oracle/parallel.py) on the headline workload; rank 0 only."""
     ws, rank, local = dist_env()
     if rank != 0:
         return
-    from oracle import wten_oracle as O  # noqa: F401
+    from oracle import parallel as P
 
-    x = np.random.default_rng(0).standard_normal(CFG2)
-    threads = host_threads()
-    rows = 512 if threads >= 8 else 128        # bounded sample: a few s per step at most
-    slab = np.ascontiguousarray(x[:rows])
-    n = slab.size
-    oracle_round_trips(slab, max(0, min(args.warmup, 1)), threads)
-    dt = oracle_round_trips(slab, args.steps, threads)
-    gbs = args.steps * len(CFG2_LEVELS) * 32 * n / dt / 1e9
-    cores = threads
-    line = {"impl": "reference", "metric": METRIC, "value": round(gbs, 4), "unit": "GB/s", "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (seeded standard normal, BASELINE configs[1])",
-            "config": {"workload": "forward+inverse lifting transform 512x512x256 f64, L=1,2,4,8",
-                       "sample": f"{rows}x512x256 slab per step"},
-            "cpu_baseline": {"value": round(gbs, 4), "unit": "GB/s", "cores": cores, "kind": "port",
-                             "sample": f"oracle/wten_oracle.py (numpy port of lifting.py:63-120) on a "
-                                       f"{rows}x512x256 slab row-split over {threads} threads, "
-                                       f"L=1,2,4,8, {args.steps} steps"},
-            "e2e": {"value": round(gbs, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    x = cfg4_cube()
+    n1, n2, p = CFG4
+    N = n1 * n2 * p
+    with P.Pool() as pool:
+        def call():
+            P.sp_w_svd(pool, x, CFG4_RANK, CFG4_LEVELS)
+
+        t = time.perf_counter()
+        call()  # first warm-up call sizes the run
+        first = time.perf_counter() - t
+        budget = float(os.environ.get("WT_REF_BUDGET_S", "420"))
+        warm, steps, note = args.warmup, args.steps, None
+        if first * (warm - 1 + steps) > budget:
+            # bounded run on a slow host: no further warm-ups, as many full calls as fit
+            warm = 1
+            steps = max(1, min(steps, int(budget / first)))
+            note = (f"time budget {budget:.0f} s at {first:.1f} s per call: {steps} of {args.steps} steps "
+                    f"timed after 1 warm-up")
+        for _ in range(warm - 1):
+            call()
+        t = time.perf_counter()
+        for _ in range(steps):
+            call()
+        dt = time.perf_counter() - t
+        threads = pool.threads
+    v = N * steps / dt
+    line = {"impl": "reference", "metric": METRIC, "value": round(v, 1), "unit": UNIT, "n_gpus": args.gpus,
+            "steps": steps, "warmup": args.warmup, "ms_per_step": round(dt / steps * 1e3, 2),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": DATA,
+            "config": headline_config(),
+            "cpu_baseline": {"value": round(v, 1), "unit": UNIT, "cores": threads, "kind": "port",
+                             "sample": "oracle/parallel.py sp_w_svd (numpy port of decomposition.py:140-154, "
+                                       f"LAPACK dgesdd per slice) on the full cube over {threads} host threads, "
+                                       "one full call per step"},
+            "e2e": {"value": round(v, 1), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    if note:
+        line["note"] = note
     emit(line)
 
 
@@ -618,8 +769,8 @@ _JSON_FD = None
 
 
 def _quiet_stdout():
-    """Send everything written to fd 1 (NCCL's version banner, library prints)
-    to stderr; the JSON line goes to the saved stdout so it stays the only line."""
+    """Send everything written to fd 1 (NCCL's banner, library prints) to stderr;
+    the JSON line goes to the saved stdout so it stays the only line."""
     global _JSON_FD
     if _JSON_FD is None:
         sys.stdout.flush()
@@ -655,90 +806,73 @@ def main():
     from paper_2601_08228_b200 import _native
 
     _native.require_gpu()
+    n1, n2, p = CFG4
+    N = n1 * n2 * p
+    sampler = ClockSampler(torch.cuda.current_device())
+    if dist is None:
+        x_host = cfg4_cube()
+        head = headline_single(args, x_host, sampler)
+    else:
+        x_host = None
+        head = headline_sharded(args, dist, sampler)
 
     if args.workloads == "default":
-        wl = (["wsvd", "spwsvd", "deblur", "wproduct", "comparators"] if ws == 1
-              else ["spwsvd_fused", "spwsvd_sharded", "wsvd_fused", "wsvd_sharded", "wproduct_sharded"])
+        wl = ["wsvd", "deblur", "wproduct", "comparators"] if dist is None else []
     elif args.workloads == "none":
         wl = []
     else:
-        wl = [w for w in args.workloads.split(",") if w and w != "transform"]
-
-    tr = transform_workload(args, dist, rank, ws)
-    workloads = {}
-
-    def make_line(cpu):
-        return {
-            "metric": METRIC, "value": round(tr["value"], 2), "unit": "GB/s", "n_gpus": ws,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(tr["ms"] / args.steps, 4),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic: seeded i.i.d. standard normal cube per rank (BASELINE configs[1]); "
-                    "hyperspectral generator for configs 3-5 (paper_2601_08228_b200/synth.py)",
-            "config": {"workload": "forward+inverse lifting transform 512x512x256 f64, L=1,2,4,8 per step",
-                       "per_rank_cube": list(CFG2), "levels": list(CFG2_LEVELS),
-                       "parallelism": f"replicas{ws}" if ws > 1 else "single",
-                       "l2": "inputs larger than L2 (2 GiB cube, 2 GiB pyramid)",
-                       "bytes_per_step_per_rank": len(CFG2_LEVELS) * 2 * 16 * tr["N"]},
-            "roofline": tr["roofline"],
-            "cpu_baseline": cpu,
-            "e2e": tr["e2e"],
-            "gpu_launches": tr["launches"],
-            "clocks": tr["clocks"],
-            "round_trip_relerr": tr["round_trip_relerr"],
-            "workloads": workloads,
-        }
-
-    # Watchdog for the secondary workloads (the multi-GPU ones have collectives
-    # and peer exchanges that were only exercised on one GPU): if they do not
-    # finish in time, rank 0 still prints the primary line with what finished,
-    # and every rank exits cleanly instead of hanging the run.
-    budget = float(os.environ.get("WT_BENCH_WORKLOAD_TIMEOUT", "600"))
-    done = threading.Event()
-
-    def watchdog():
-        if not done.wait(budget):
-            if rank == 0:
-                workloads["timeout"] = f"secondary workloads exceeded {budget:.0f} s; not all ran"
-                emit(make_line(None))
-            os._exit(0)
-
-    threading.Thread(target=watchdog, daemon=True).start()
-    for name in wl:
-        try:
-            if name == "wsvd":
-                workloads[name] = wsvd_workload(args)
-            elif name == "spwsvd":
-                workloads[name] = spwsvd_workload(args)
-            elif name == "deblur":
-                workloads[name] = deblur_workload(args)
-            elif name == "wproduct":
-                workloads[name] = wproduct_workload(args)
-            elif name == "comparators":
-                workloads[name] = comparators_workload(args)
-            elif name in ("spwsvd_sharded", "spwsvd_fused"):
-                from paper_2601_08228_b200 import sharded
-
-                workloads[name] = sharded.bench_sp_w_svd(dist, timed_region, steps=3, warmup=1,
-                                                         fused=name == "spwsvd_fused")
-            elif name == "wproduct_sharded":  # config-5-sized w-product, rows sharded
-                from paper_2601_08228_b200 import sharded
-
-                workloads[name] = sharded.bench_w_product(dist, timed_region)
-            elif name in ("wsvd_sharded", "wsvd_fused"):  # config 3, all p slices exchanged
-                from paper_2601_08228_b200 import sharded
-
-                workloads[name] = sharded.bench_sp_w_svd(dist, timed_region, steps=3, warmup=1,
-                                                         shape=(256, 256, 192), r=20, levels=3,
-                                                         fused=name == "wsvd_fused", full=True)
-        except Exception as e:  # noqa: BLE001
-            workloads[name] = {"error": f"{type(e).__name__}: {e}"}
-    done.set()
+        wl = [w for w in args.workloads.split(",") if w]
+    want_cpu = rank == 0 and dist is None and not args.no_cpu_baseline
 
     cpu = None
-    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
-        cpu = cpu_transform_sample(tr["x_host"])
+    if want_cpu:
+        ref = {}
+
+        def run(pool):
+            from oracle import parallel as P
+
+            ref["y"] = P.sp_w_svd(pool, x_host, CFG4_RANK, CFG4_LEVELS)
+
+        cpu = cpu_port_baseline(run, lambda s: round(N / s, 1), UNIT,
+                                "oracle sp_w_svd(cube, 30, 4) (decomposition.py:140-154)")
+        y = head["y_host"]
+        cpu["gpu_vs_cpu_recon_relerr"] = float(np.linalg.norm((y - ref["y"]).ravel())
+                                               / np.linalg.norm(ref["y"].ravel()))
+        del ref
+
+    transform = transform_key(args, dist, rank, ws, want_cpu)
+    workloads = {}
+    budget = float(os.environ.get("WT_BENCH_WORKLOAD_TIMEOUT", "900"))
+    t_start = time.time()
+    for name in wl:
+        if time.time() - t_start > budget:
+            workloads[name] = {"skipped": f"workload budget {budget:.0f} s spent"}
+            continue
+        try:
+            fn = {"wsvd": wsvd_workload, "deblur": deblur_workload, "wproduct": wproduct_workload,
+                  "comparators": comparators_workload}[name]
+            workloads[name] = fn(args)
+        except Exception as e:  # noqa: BLE001
+            workloads[name] = {"error": f"{type(e).__name__}: {e}"}
+
     if rank == 0:
-        line = make_line(cpu)
+        line = {
+            "metric": METRIC, "value": round(head["value"], 1), "unit": UNIT, "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(head["ms"] / args.steps, 3),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": DATA,
+            "config": headline_config(),
+            "parallelism": "single GPU" if dist is None else f"rows sharded over {ws} GPUs (sp_w_svd_fused)",
+            "roofline": head["roofline"],
+            "cpu_baseline": cpu,
+            "e2e": head["e2e"],
+            "gpu_launches": head["gpu_launches"],
+            "clocks": sampler.summary(),
+            "transform": transform,
+            "workloads": workloads,
+        }
+        for k in ("phases_ms_rank", "nccl_variant_ms_per_call", "launch_names"):
+            if k in head:
+                line[k] = head[k]
         emit(line)
     if dist is not None:
         dist.barrier()

@@ -182,6 +182,7 @@ __global__ void __launch_bounds__(kT) fwd_persistent(const double* __restrict__ 
     fence_proxy_async_smem();  // generic reads of `buf` before its TMA refill
     __syncthreads();  // tile buffer `buf` is refilled by the next iteration's issue
   }
+  if (g.tab) __threadfence_system();  // peer stores: system-scope release before the exchange barrier
 }
 
 // Deep-L variant (L > 3): ONE tile buffer of TQ = 32 tubes x CT bands.  Stage 0
@@ -239,6 +240,7 @@ __global__ void __launch_bounds__(kT) fwd_persistent1(const double* __restrict__
     }
     __syncthreads();
   }
+  if (g.tab) __threadfence_system();  // peer stores: system-scope release before the exchange barrier
 }
 
 // Shallow variant (L = W <= 3, one stage): ONE 32 x 256 tile buffer; every
@@ -330,6 +332,7 @@ __global__ void __launch_bounds__(kT) fwd_shallow(const double* __restrict__ x,
       if (g.mask & 1) put(soff(g.p, W) + (t0 >> W) + c, v[k][0][0], v[k][1][0]);
     }
   }
+  if (g.tab) __threadfence_system();  // peer stores: system-scope release before the exchange barrier
 }
 
 // ------------------------------------------------------------- inverse ----

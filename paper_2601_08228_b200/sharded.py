@@ -267,7 +267,7 @@ def _symm_pair(numel, device, group):
     return _SYMM[key]
 
 
-def _fused_exchange(x_local, levels, n1, mask, base, decompose, out_rows, out_cols, group):
+def _fused_exchange(x_local, levels, n1, mask, base, decompose, out_rows, out_cols, group, phases=None):
     """rows -> owners' slices (peer stores in K1), ``decompose`` in place on the owner,
     owners' result slices -> rows (peer loads in K2).
 
@@ -290,19 +290,39 @@ def _fused_exchange(x_local, levels, n1, mask, base, decompose, out_rows, out_co
                          dtype=torch.int64, device=dev)
     tab_i = torch.tensor(peer_slice_table(h_rec.buffer_ptrs, ks, sum(orows[:me]), out_rows, out_cols),
                          dtype=torch.int64, device=dev)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(6)] if phases is not None else None
+    mark = (lambda i: ev[i].record()) if ev else (lambda i: None)
+    mark(0)
+    # Memory ordering: K1's peer stores are followed (stream order) by the
+    # symmetric-memory barrier kernel, whose signal is a system-scope release and
+    # whose wait is a system-scope acquire; K1 also ends every CTA with a
+    # system-scope fence after its last peer store (lift_fast.cu, peer variant).
     E.lift_forward_peer(x_local.contiguous(), levels, tab_f, mask, base)
+    mark(1)
     h_recv.barrier(channel=0)                   # every rank's peer stores have landed
+    mark(2)
     k_me = ks[me]
     if k_me:
         decompose(recv[:k_me * n1 * n2].view(k_me, n1, n2),
                   recb[:k_me * out_rows * out_cols].view(k_me, out_rows, out_cols))
+    mark(3)
     h_rec.barrier(channel=0)                    # every owner's result is ready
+    mark(4)
     y = E.lift_inverse_peer(tab_i, orows[me], out_cols, p, levels, mask, base)
     h_rec.barrier(channel=1)                    # all peer loads done before buffers are reused
+    mark(5)
+    if ev:
+        ev[5].synchronize()
+        phases.update({"k1_peer_store_ms": ev[0].elapsed_time(ev[1]),
+                       "exchange_barrier_ms": ev[1].elapsed_time(ev[2]),
+                       "k4_ms": ev[2].elapsed_time(ev[3]),
+                       "owners_barrier_ms": ev[3].elapsed_time(ev[4]),
+                       "k2_peer_load_ms": ev[4].elapsed_time(ev[5]),
+                       "slices_owned": k_me, "rows_owned": R})
     return y
 
 
-def sp_w_svd_fused(x_local, r, levels, n1, group=None):
+def sp_w_svd_fused(x_local, r, levels, n1, group=None, phase_times=False):
     """sp-w-svd of a row-sharded cube with the exchange fused into K1 / K2.
 
     K1 stores each coarse slice row block straight into the owning GPU's
@@ -323,7 +343,9 @@ def sp_w_svd_fused(x_local, r, levels, n1, group=None):
         E.truncated_recon(full, sigma, vec, r, out=out)
 
     mask = E.level_mask(levels, smooth=True, details=[levels])
-    return _fused_exchange(x_local, levels, n1, mask, p - 2 * m, decompose, n1, n2, group)
+    phases = {} if phase_times else None
+    y = _fused_exchange(x_local, levels, n1, mask, p - 2 * m, decompose, n1, n2, group, phases)
+    return (y, phases) if phase_times else y
 
 
 def w_svd_recon_fused(x_local, r, levels, n1, group=None):
