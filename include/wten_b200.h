@@ -213,6 +213,9 @@ int wt_slice_reduce_f64(const double* x, const double* y, int64_t n, int64_t nsl
  * the FP64 flops its Jacobi iteration executed (Gram + rotation tiles of every
  * rotated pair visit) -- the denominator-free work measure for the roofline. */
 int wt_svd_last_sweeps(void);
+/* Matrices of the last wt_svd_jacobi_f64 call (this thread) whose Gram-eigenbasis
+ * preconditioner fell back to the identity, or -1 when the call ran without it. */
+int wt_svd_last_fallbacks(void);
 double wt_svd_last_jacobi_flops(void);
 
 #ifdef __cplusplus

@@ -44,6 +44,7 @@ SIGNATURES = {
                                          ctypes.c_int, ctypes.c_void_p, ctypes.c_size_t,
                                          ctypes.c_void_p]),
     "wt_svd_last_sweeps": (ctypes.c_int, []),
+    "wt_svd_last_fallbacks": (ctypes.c_int, []),
     "wt_svd_last_jacobi_flops": (ctypes.c_double, []),
     "wt_scale_cols_f64": (ctypes.c_int, [c_double_p, i64, i64, i64, i64, c_double_p, i64, i64,
                                          ctypes.c_int, ctypes.c_double, ctypes.c_void_p]),

@@ -1,0 +1,1015 @@
+// K4 preconditioner: the eigenbasis V0 of the Gram X^T X of every slice, so
+// that the one-sided Jacobi sweeps start from X V0 (nearly orthogonal columns,
+// quadratic convergence from the first sweep) instead of from X.
+//
+// Why: plain cyclic one-sided Jacobi spends 9-15 of its 12-17 sweeps on the
+// wavelet slices of configs 3-5 with pair cosines still at 0.3-0.9
+// (profiles/r01_summary.md, convergence traces); started from X V0 it needs 3
+// (tools/jacobi_precond_probe.py).  The Gram squares the
+// condition number, so V0 is only a preconditioner: the FP64 Jacobi on X V0
+// keeps its own convergence test and delivers the singular values, so the
+// accuracy is that of the Jacobi method (replacing _stack_svd,
+// decomposition.py:64-67, as before).
+//
+// Pipeline (all batched over the slices, stream-ordered, FP64):
+//   1. G = X^T X                                   K3 GEMM
+//   2. G = Q T Q^T, T tridiagonal                  panels of NB columns:
+//        tridiag_panel<C> (lazy latrd-style column updates, lower-triangle
+//        symv, one CTA or a C-CTA cluster per matrix; rows of the trailing
+//        block dealt cyclically over the cluster, partial sums exchanged in
+//        distributed shared memory) + the symmetric rank-2NB trailing update
+//        on K3 (lower tiles only).  The panel's Householder vectors overwrite
+//        its (dead) columns of G.
+//   3. eigenvalues of T: bisection, one thread per eigenvalue (Sturm counts
+//      by the scaled determinant recurrence: one FMA per step on the chain)
+//   4. eigenvectors of T: inverse iteration (2 solves with the LDL^T factors of
+//      T - lambda I), one thread per eigenvalue              -> Z
+//   5. Newton-Schulz Z <- Z (3 I - Z^T Z) / 2 until orthogonal to rounding
+//      (K3; matrices where it cannot converge fall back to V0 = I)
+//   6. V0 = Q Z: compact-WY blocks of NBT reflectors (larft + 3 K3 GEMMs each)
+//   7. Y = X V0                                      K3 GEMM
+// Deterministic: fixed thread -> data maps and reduction orders.
+#include <math.h>
+#include <stdint.h>
+#include <string.h>
+
+#include <algorithm>
+#include <vector>
+
+#include "wt_common.cuh"
+
+namespace wt {
+namespace eig {
+
+constexpr int NB = 32;     // tridiagonalization panel width
+constexpr int NBT = 64;    // back-transformation block (reflectors per compact-WY block)
+constexpr int PT = 256;    // panel kernel threads
+constexpr int NW = PT / 32;
+constexpr int CH = 256;    // symv column chunk (CH / 64 double2 register accumulators per lane)
+constexpr int NCH2 = CH / 64;
+constexpr int RB = 4;      // rows per warp in flight in the symv
+constexpr int MAXR = 256;  // own rows per CTA (the panel's V, W rows of a CTA live in shared memory)
+constexpr int PREF_R = 128;  // preferred own rows per CTA (two CTAs per SM)
+constexpr int VP = 2 * NB + 1;  // shared pitch of a [V | W] row
+
+__device__ __forceinline__ void cl_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ int cl_rank() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return (int)r;
+}
+template <typename T>
+__device__ __forceinline__ T* cl_map(T* p, int rank) {
+  uint64_t out;
+  asm volatile("mapa.u64 %0, %1, %2;" : "=l"(out) : "l"(reinterpret_cast<uint64_t>(p)), "r"(rank));
+  return reinterpret_cast<T*>(out);
+}
+template <int C>
+__device__ __forceinline__ void csync() {
+  if constexpr (C > 1) cl_sync(); else __syncthreads();
+}
+template <int C, typename T>
+__device__ __forceinline__ const T* remote(const T* p, int rank) {
+  if constexpr (C > 1) return cl_map(const_cast<T*>(p), rank);
+  else return p;
+}
+
+// deterministic CTA sum (warp shuffles, then warps in order); result valid in every thread
+__device__ __forceinline__ double block_sum(double v, double* red) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  double s = 0.0;
+#pragma unroll
+  for (int w = 0; w < NW; ++w) s += red[w];
+  return s;
+}
+
+struct PanelSmem {
+  static size_t bytes(int n, int C) {
+    const int R = (n + C - 1) / C;
+    return sizeof(double) * ((size_t)R * VP + 1 + 2 * (size_t)n + 2 + 2 * (size_t)R + (size_t)NW * CH + 4 + 2 +
+                             2 * NB + 2 * NW + 7 * NB + NW * (2 * NB + 1));
+  }
+};
+
+// One panel (columns k0 .. k0+jb-1) of the lower Householder tridiagonalization
+// (LAPACK dsytrd / dlatrd semantics, lower storage).  Per column k:
+//   a   = A[k:, k] - V W[k, :]^T - W V[k, :]^T          (lazy panel updates)
+//   v   = Householder vector of a[k+1:], tau, e[k] = beta, d[k] = a[k]
+//   p   = A22 v - V (W^T v) - W (V^T v)                 (A22 = A[k+1:, k+1:], pre-panel)
+//   w   = tau p - (tau^2 / 2)(p^T v - 2 (W^T v).(V^T v)) v
+// Rows are dealt cyclically over the C CTAs of a cluster (row i -> CTA i % C,
+// local row i / C); a CTA keeps its rows of the panel's V and W in shared
+// memory, so the lazy updates never wait on global memory.  VW = [V | W] and
+// WV = [W | V] (n x 2NB, row-major, global) feed the trailing update A22 -=
+// VW WV^T on K3; the panel's V block overwrites its dead columns of A.
+// Four cluster barriers per column: S1 norm partials, S2 v, S3 symv partials, S4 w.
+template <int C>
+__global__ void __launch_bounds__(PT, 2) tridiag_panel(double* __restrict__ Gall, double* __restrict__ VWall,
+                                                    double* __restrict__ WVall, double* __restrict__ dall,
+                                                    double* __restrict__ eall, double* __restrict__ tauall,
+                                                    const int* __restrict__ flag, int n, int k0) {
+  extern __shared__ __align__(16) double sm[];
+  const int R = (n + C - 1) / C;  // local rows (upper bound)
+  double* vws = sm;                    // [R][VP]  my rows of [V | W]
+  double* vsm = vws + ((R * VP + 1) & ~1);  // [n + 2]  v (full; 16-byte aligned, zero beyond n)
+  double* csum = vsm + n + 2;          // [n]  CTA partial column part of A22 v (DSMEM-visible)
+  double* prow = csum + n;             // [R]  my rows: row part of A22 v
+  double* diag = prow + R;             // [R]  my rows: A[i][i] (pre-panel)
+  double* wacc = diag + R;             // [NW][CH] per-warp column accumulators
+  double* part1 = wacc + NW * CH;      // [4]  ss, alpha (S1)
+  double* part3 = part1 + 4;           // [2 + 2NB] pv, -, yW[NB], yV[NB] (S3)
+  double* red = part3 + 2 + 2 * NB;    // [2NW]
+  double* ys = red + 2 * NW;           // [2NB] cluster sums of yW, yV
+  double* rk = ys + 2 * NB;            // [2NB] row k of [V | W]
+  double* dpan = rk + 2 * NB;          // [3NB] d, e, tau of the panel's columns (written at the end)
+  double* ywacc = dpan + 3 * NB;       // [NW][2NB + 1] per-warp partials of yW, yV, v^T A22 v
+  const int rank = C == 1 ? 0 : cl_rank();
+  const int b = blockIdx.x / C;
+  if (!flag[b]) return;  // cluster-uniform
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  double* A = Gall + (int64_t)b * n * n;
+  double* VW = VWall + (int64_t)b * n * 2 * NB;
+  double* WV = WVall + (int64_t)b * n * 2 * NB;
+  double* d = dall + (int64_t)b * n;
+  double* e = eall + (int64_t)b * n;
+  double* tau = tauall + (int64_t)b * n;
+  const int jb = min(NB, n - k0);
+  const int nloc = (n - rank + C - 1) / C;  // my rows: i = rank + C q, q < nloc
+  auto row_of = [&](int q) { return rank + C * q; };
+  auto q_first = [&](int lo) { return lo <= rank ? 0 : (lo - rank + C - 1) / C; };  // first q with row >= lo
+
+  for (int q = tid; q < nloc; q += PT) {
+    diag[q] = A[(int64_t)row_of(q) * n + row_of(q)];
+    for (int t = 0; t < 2 * NB; ++t) vws[q * VP + t] = 0.0;
+  }
+  for (int i = tid; i < n + 2; i += PT) vsm[i] = 0.0;
+  // prefetch of my rows' entries of column k (pre-panel values)
+  double anext[(MAXR + PT - 1) / PT];
+#pragma unroll
+  for (int u = 0; u < (MAXR + PT - 1) / PT; ++u) {
+    const int q = tid + u * PT;
+    anext[u] = (q < nloc && row_of(q) >= k0) ? A[(int64_t)row_of(q) * n + k0] : 0.0;
+  }
+  __syncthreads();
+
+  for (int j = 0; j < jb; ++j) {
+    const int k = k0 + j;
+    // ---------------- A: column update of my rows i >= k -------------------
+    double ss = 0.0, alpha_own = 0.0;
+#pragma unroll
+    for (int u = 0; u < (MAXR + PT - 1) / PT; ++u) {
+      const int q = tid + u * PT;
+      const int i = row_of(q);
+      if (q < nloc && i >= k) {
+        // a = A[i][k] - V[i, :j] W[k, :j]^T - W[i, :j] V[k, :j]^T in four independent chains
+        const double* ri = vws + q * VP;
+        double a0 = anext[u], a1 = 0.0, a2 = 0.0, a3 = 0.0;
+        int t = 0;
+        for (; t + 2 <= j; t += 2) {
+          a0 = fma(-ri[t], rk[NB + t], a0);
+          a1 = fma(-ri[NB + t], rk[t], a1);
+          a2 = fma(-ri[t + 1], rk[NB + t + 1], a2);
+          a3 = fma(-ri[NB + t + 1], rk[t + 1], a3);
+        }
+        if (t < j) {
+          a0 = fma(-ri[t], rk[NB + t], a0);
+          a1 = fma(-ri[NB + t], rk[t], a1);
+        }
+        const double a = (a0 + a1) + (a2 + a3);
+        vsm[i] = a;
+        if (i >= k + 2) ss = fma(a, a, ss);
+        if (i == k) dpan[j] = a;
+        if (i == k + 1) alpha_own = a;
+      }
+    }
+    // (only the owner of row k+1 contributes alpha)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      ss += __shfl_xor_sync(0xffffffffu, ss, o);
+      alpha_own += __shfl_xor_sync(0xffffffffu, alpha_own, o);
+    }
+    if (lane == 0) {
+      red[warp] = ss;
+      red[NW + warp] = alpha_own;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+      for (int w = 0; w < NW; ++w) {
+        s0 += red[w];
+        s1 += red[NW + w];
+      }
+      part1[0] = s0;
+      part1[1] = s1;
+    }
+    csync<C>();  // S1
+    // ---------------- B: Householder vector ---------------------------------
+    double sst = 0.0;
+#pragma unroll
+    for (int r = 0; r < C; ++r) sst += remote<C>(part1, r)[0];
+    const double alpha = remote<C>(part1, (k + 1) % C)[1];
+    double tk = 0.0, scale = 0.0, beta = alpha;
+    const bool last = k >= n - 2;
+    if (!last && sst > 0.0) {
+      beta = -copysign(sqrt(fma(alpha, alpha, sst)), alpha);
+      tk = (beta - alpha) / beta;
+      scale = 1.0 / (alpha - beta);
+    }
+    if (tid == 0) {
+      dpan[NB + j] = beta;  // e[k] (k < n - 1)
+      dpan[2 * NB + j] = k < n - 1 ? tk : 0.0;
+    }
+    if (k == n - 1) break;  // the last column only has its diagonal
+    for (int q = tid; q < nloc; q += PT) {
+      const int i = row_of(q);
+      double v = 0.0;
+      if (i >= k + 2) v = vsm[i] * scale;
+      else if (i == k + 1) v = tk != 0.0 ? 1.0 : 0.0;
+      vsm[i] = v;
+      vws[q * VP + j] = v;
+    }
+    // L2 prefetch of my rows' part of the next column's symv (A22 is constant
+    // within the panel): one bulk prefetch per row, issued a column ahead
+    if (j + 1 < jb) {
+      const int c0 = (k + 2) & ~1;
+      for (int q = q_first(k + 2) + tid; q < nloc; q += PT) {
+        const int i = row_of(q);
+        const int len = ((i + 1 - c0) * 8 + 15) & ~15;
+        if (len > 0 && (n & 1) == 0)
+          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(A + (int64_t)i * n + c0), "r"(len)
+                       : "memory");
+      }
+    }
+    csync<C>();  // S2: every CTA's v entries are written
+    if constexpr (C > 1) {
+      for (int i = k + 1 + tid; i < n; i += PT)
+        if (i % C != rank) vsm[i] = *cl_map(vsm + i, i % C);
+      if (tid == 0) vsm[k] = 0.0;  // (a row that left the trailing block)
+      __syncthreads();
+    }
+    // prefetch of my rows' entries of the next column (not changed by this panel);
+    // issued here so that no load is outstanding at the cluster barriers S1 / S2
+    // (their release semantics wait for it), consumed by the next column's step A
+#pragma unroll
+    for (int u = 0; u < (MAXR + PT - 1) / PT; ++u) {
+      const int q = tid + u * PT;
+      const int i = row_of(q);
+      anext[u] = (q < nloc && k + 1 < n && i >= k + 1) ? A[(int64_t)i * n + k + 1] : 0.0;
+    }
+    // ---------------- C: p = A22 v (lower triangle, my rows) ----------------
+    // row part  prow[q] = sum_{c = k+1}^{i} A[i][c] v[c]
+    // col part  csum[c] = sum_{my rows i > c} A[i][c] v[i]
+    const int cstart = (k + 1) & ~1;  // 16-byte aligned double2 loads (n even)
+    const int qk = q_first(k + 1);
+    for (int q = qk + tid; q < nloc; q += PT) prow[q] = 0.0;
+    __syncthreads();
+    double yv_l = 0.0, yw_l = 0.0;  // lane t: sum over my rows of V[i][t] v_i, W[i][t] v_i
+    for (int cb = cstart; cb < n; cb += CH) {
+      double acc[NCH2][2];
+#pragma unroll
+      for (int t = 0; t < NCH2; ++t) acc[t][0] = acc[t][1] = 0.0;
+      // my rows with entries in this chunk: i >= max(k+1, cb); RB rows per warp at a time
+      const int q0 = q_first(max(k + 1, cb));
+      for (int qb = q0 + warp * RB; qb < nloc; qb += NW * RB) {
+        double av[RB][NCH2][2];
+#pragma unroll
+        for (int r = 0; r < RB; ++r) {
+          const int q = qb + r;
+          const int i = row_of(q);
+          const double* Ar = A + (int64_t)i * n;
+          const int cend = min(i, cb + CH - 1);  // inclusive (diagonal)
+#pragma unroll
+          for (int t = 0; t < NCH2; ++t) {
+            const int c = cb + 64 * t + 2 * lane;
+            av[r][t][0] = av[r][t][1] = 0.0;
+            if (q < nloc && c <= cend) {
+              if ((n & 1) == 0) {
+                const double2 x = *reinterpret_cast<const double2*>(Ar + c);
+                av[r][t][0] = x.x;
+                av[r][t][1] = c + 1 <= cend ? x.y : 0.0;  // (upper triangle beyond the diagonal)
+              } else {
+                av[r][t][0] = Ar[c];
+                if (c + 1 <= cend) av[r][t][1] = Ar[c + 1];
+              }
+            }
+          }
+        }
+        // row parts: v[c] = 0 for c <= k, so columns left of the block need no mask;
+        // column parts include the diagonal (subtracted again in step D)
+        double rp[RB];
+#pragma unroll
+        for (int r = 0; r < RB; ++r) {
+          const int i = row_of(qb + r);
+          const double vi = qb + r < nloc ? vsm[i] : 0.0;
+          if (cb == cstart && qb + r < nloc) {  // every row >= k+1 is visited in the first chunk
+            yv_l = fma(vws[(qb + r) * VP + lane], vi, yv_l);
+            yw_l = fma(vws[(qb + r) * VP + NB + lane], vi, yw_l);
+          }
+          rp[r] = 0.0;
+#pragma unroll
+          for (int t = 0; t < NCH2; ++t) {
+            const int c = cb + 64 * t + 2 * lane;
+            const double2 vv = *reinterpret_cast<const double2*>(vsm + c);
+            rp[r] = fma(av[r][t][0], vv.x, fma(av[r][t][1], vv.y, rp[r]));
+            acc[t][0] = fma(av[r][t][0], vi, acc[t][0]);
+            acc[t][1] = fma(av[r][t][1], vi, acc[t][1]);
+          }
+        }
+        // 4 row sums across the warp in 6 shuffles (pairwise halving, then a butterfly)
+        {
+          const bool hi16 = lane & 16, hi8 = lane & 8;
+          double x0 = hi16 ? rp[0] : rp[1], y0 = hi16 ? rp[1] : rp[0];
+          y0 += __shfl_xor_sync(0xffffffffu, x0, 16);  // row 0 (lanes < 16) / row 1 (lanes >= 16)
+          double x1 = hi16 ? rp[2] : rp[3], y1 = hi16 ? rp[3] : rp[2];
+          y1 += __shfl_xor_sync(0xffffffffu, x1, 16);  // row 2 / row 3
+          double x2 = hi8 ? y0 : y1, y2 = hi8 ? y1 : y0;
+          y2 += __shfl_xor_sync(0xffffffffu, x2, 8);   // lane&8 ? rows 2|3 : rows 0|1
+#pragma unroll
+          for (int o = 4; o > 0; o >>= 1) y2 += __shfl_xor_sync(0xffffffffu, y2, o);
+          if ((lane & 7) == 0) {
+            const int r = (hi8 ? 2 : 0) + (hi16 ? 1 : 0);
+            if (qb + r < nloc) prow[qb + r] += y2;
+          }
+        }
+      }
+      // flush the warp accumulators: csum[c] = sum over warps (fixed order)
+#pragma unroll
+      for (int t = 0; t < NCH2; ++t) {
+        wacc[warp * CH + 64 * t + 2 * lane] = acc[t][0];
+        wacc[warp * CH + 64 * t + 2 * lane + 1] = acc[t][1];
+      }
+      __syncthreads();
+      for (int c = tid; c < CH && cb + c < n; c += PT) {
+        double sacc = 0.0;
+#pragma unroll
+        for (int w = 0; w < NW; ++w) sacc += wacc[w * CH + c];
+        csum[cb + c] = sacc;
+      }
+      __syncthreads();
+    }
+    // v^T A22 v over my rows: sum_i v_i (2 rowpart_i - A_ii v_i); with the y
+    // partials through one shared pass (fixed warp order)
+    double pv_own = 0.0;
+    for (int q = qk + tid; q < nloc; q += PT) {
+      const double vi = vsm[row_of(q)];
+      pv_own = fma(vi, 2.0 * prow[q] - diag[q] * vi, pv_own);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) pv_own += __shfl_xor_sync(0xffffffffu, pv_own, o);
+    ywacc[warp * (2 * NB + 1) + lane] = yw_l;          // yW[t] partials (t = lane)
+    ywacc[warp * (2 * NB + 1) + NB + lane] = yv_l;     // yV[t]
+    if (lane == 0) ywacc[warp * (2 * NB + 1) + 2 * NB] = pv_own;
+    __syncthreads();
+    for (int t = tid; t <= 2 * NB; t += PT) {
+      double sacc = 0.0;
+#pragma unroll
+      for (int w = 0; w < NW; ++w) sacc += ywacc[w * (2 * NB + 1) + t];
+      if (t == 2 * NB) part3[0] = sacc;
+      else part3[2 + t] = sacc;
+    }
+    csync<C>();  // S3: csum, part3 of every CTA are complete
+    // ---------------- D: w -------------------------------------------------
+    double pvt = 0.0;
+#pragma unroll
+    for (int r = 0; r < C; ++r) pvt += remote<C>(part3, r)[0];
+    for (int t = tid; t < 2 * NB; t += PT) {
+      double sacc = 0.0;
+      if ((t < NB && t < j) || (t >= NB && t - NB < j)) {
+#pragma unroll
+        for (int r = 0; r < C; ++r) sacc += remote<C>(part3, r)[2 + t];
+      }
+      ys[t] = sacc;
+    }
+    __syncthreads();
+    double ywv = 0.0;
+    for (int t = 0; t < j; ++t) ywv = fma(ys[t], ys[NB + t], ywv);
+    const double alpha2 = -0.5 * tk * tk * (pvt - 2.0 * ywv);
+    for (int q = tid; q < nloc; q += PT) {
+      const int i = row_of(q);
+      double w = 0.0;
+      if (i >= k + 1) {
+        double p = prow[q] - diag[q] * vsm[i];  // the column parts include the diagonal
+#pragma unroll
+        for (int r = 0; r < C; ++r) p += remote<C>(csum, r)[i];
+        const double* ri = vws + q * VP;
+        double p1 = 0.0, p2 = 0.0, p3 = 0.0;
+        int t = 0;
+        for (; t + 2 <= j; t += 2) {
+          p = fma(-ri[t], ys[t], p);
+          p1 = fma(-ri[NB + t], ys[NB + t], p1);
+          p2 = fma(-ri[t + 1], ys[t + 1], p2);
+          p3 = fma(-ri[NB + t + 1], ys[NB + t + 1], p3);
+        }
+        if (t < j) {
+          p = fma(-ri[t], ys[t], p);
+          p1 = fma(-ri[NB + t], ys[NB + t], p1);
+        }
+        p = (p + p1) + (p2 + p3);
+        w = fma(alpha2, vsm[i], tk * p);
+      }
+      vws[q * VP + NB + j] = w;
+    }
+    csync<C>();  // S4: W column j complete in every CTA
+    // row k+1 of [V | W] for the next column's update (from its owner's shared memory)
+    if (j + 1 < jb) {
+      const int ow = (k + 1) % C, qo = (k + 1) / C;
+      for (int t = tid; t < 2 * NB; t += PT) rk[t] = remote<C>(vws, ow)[qo * VP + t];
+    }
+    __syncthreads();
+  }
+  // Global results, written once per panel (no global stores inside the column
+  // loop, so the cluster barriers do not wait on them): [V | W], [W | V] rows for
+  // the trailing update, d / e / tau, and the panel's Householder vectors over
+  // its (dead) columns of A -- the Y block of the back-transformation.
+  for (int q = warp; q < nloc; q += NW) {
+    const int i = row_of(q);
+    double* vw = VW + (int64_t)i * 2 * NB;
+    double* wv = WV + (int64_t)i * 2 * NB;
+    for (int t = lane; t < NB; t += 32) {
+      const double v = t < jb ? vws[q * VP + t] : 0.0, w = t < jb ? vws[q * VP + NB + t] : 0.0;
+      vw[t] = v;
+      vw[NB + t] = w;
+      wv[t] = w;
+      wv[NB + t] = v;
+      if (t < jb) A[(int64_t)i * n + k0 + t] = v;
+    }
+  }
+  for (int t = tid; t < jb; t += PT) {
+    if ((k0 + t) % C == rank) d[k0 + t] = dpan[t];  // (the diagonal is known to its row's owner)
+    if (rank == 0) {
+      if (k0 + t < n - 1) e[k0 + t] = dpan[NB + t];
+      tau[k0 + t] = dpan[2 * NB + t];
+    }
+  }
+  if constexpr (C > 1) cl_sync();  // no CTA exits while others may still read its shared memory
+}
+
+// Per matrix: flag = (G finite and nonzero); Gershgorin interval and pivmin of T
+// (after tridiagonalization); glim = flag ? INT_MAX : 0 (K3 per-matrix column limit)
+__global__ void gram_flag(const double* __restrict__ G, int n, int* flag, int* glim) {
+  const int b = blockIdx.x;
+  const double* g = G + (int64_t)b * n * n;
+  __shared__ double red[NW];
+  double tr = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) tr += g[(int64_t)i * n + i];
+  tr = block_sum(tr, red);
+  if (threadIdx.x == 0) {
+    const int ok = (tr > 0.0 && isfinite(tr)) ? 1 : 0;
+    flag[b] = ok;
+    glim[b] = ok ? 0x7fffffff : 0;
+  }
+}
+
+// Sturm count (eigenvalues of T below x) by the scaled determinant recurrence
+// p_i = (d_i - x) p_{i-1} - e_{i-1}^2 p_{i-2}: one FMA per step on the
+// dependent chain; renormalised by an exact power of two every 8 steps (T is
+// scaled to norm ~1, so 8 steps cannot leave the exponent range).  A zero
+// leading minor is replaced by -pivmin times the previous one (the LAPACK
+// pivmin convention in product form).  d, e2 in shared memory.
+__device__ __forceinline__ int sturm_count(const double* __restrict__ d, const double* __restrict__ e2, int n,
+                                           double x, double pivmin) {
+  double p2 = 1.0, p1 = d[0] - x;
+  if (p1 == 0.0) p1 = -pivmin;
+  int cnt = p1 < 0.0;
+  int i = 1;
+  for (; i + 8 <= n; i += 8) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      double p = fma(d[i + u] - x, p1, -e2[i + u - 1] * p2);
+      if (p == 0.0) p = -pivmin * p1;
+      cnt += (p < 0.0) != (p1 < 0.0);
+      p2 = p1;
+      p1 = p;
+    }
+    // exact power-of-two renormalisation: 2^-ex with ex = exponent of p1
+    const long long bits = __double_as_longlong(p1);
+    const int ex = (int)((bits >> 52) & 0x7ff) - 1023;
+    const double f = __longlong_as_double((long long)(1023 - ex) << 52);
+    p1 *= f;
+    p2 *= f;
+  }
+  for (; i < n; ++i) {
+    double p = fma(d[i] - x, p1, -e2[i - 1] * p2);
+    if (p == 0.0) p = -pivmin * p1;
+    cnt += (p < 0.0) != (p1 < 0.0);
+    p2 = p1;
+    p1 = p;
+  }
+  return cnt;
+}
+
+// scale T to norm ~1 (power of two), squares of e; per-matrix scale/pivmin
+__global__ void tri_prepare(double* __restrict__ dall, double* __restrict__ eall, double* __restrict__ e2all,
+                            double* __restrict__ info, const int* flag, int n) {
+  const int b = blockIdx.x;
+  if (!flag[b]) return;
+  double* d = dall + (int64_t)b * n;
+  double* e = eall + (int64_t)b * n;
+  double* e2 = e2all + (int64_t)b * n;
+  __shared__ double red[NW];
+  __shared__ double s_lo[NW], s_hi[NW];
+  double mx = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    mx = fmax(mx, fabs(d[i]));
+    if (i < n - 1) mx = fmax(mx, fabs(e[i]));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  mx = 0.0;
+  for (int w = 0; w < (int)(blockDim.x >> 5); ++w) mx = fmax(mx, red[w]);
+  const double sc = mx > 0.0 ? ldexp(1.0, -ilogb(mx)) : 1.0;
+  __syncthreads();
+  double lo = 1e300, hi = -1e300;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const double di = d[i] * sc;
+    const double em = i > 0 ? fabs(e[i - 1] * sc) : 0.0, ep = i < n - 1 ? fabs(e[i] * sc) : 0.0;
+    lo = fmin(lo, di - em - ep);
+    hi = fmax(hi, di + em + ep);
+  }
+  __syncthreads();  // every thread read its d/e before the in-place scaling below
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    d[i] *= sc;
+    if (i < n - 1) {
+      e[i] *= sc;
+      e2[i] = e[i] * e[i];
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+    hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    s_lo[threadIdx.x >> 5] = lo;
+    s_hi[threadIdx.x >> 5] = hi;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
+      lo = fmin(lo, s_lo[w]);
+      hi = fmax(hi, s_hi[w]);
+    }
+    lo = fmin(lo, s_lo[0]);
+    hi = fmax(hi, s_hi[0]);
+    const double span = fmax(fabs(lo), fabs(hi));
+    info[b * 4 + 0] = lo - 2.2e-16 * span - 1e-300;
+    info[b * 4 + 1] = hi + 2.2e-16 * span + 1e-300;
+    info[b * 4 + 2] = span;
+    info[b * 4 + 3] = sc;
+  }
+}
+
+// One thread per eigenvalue: lam[b][j] = j-th smallest eigenvalue of (scaled) T
+__global__ void tri_bisect(const double* __restrict__ dall, const double* __restrict__ e2all,
+                           const double* __restrict__ info, const int* flag, int n, double* __restrict__ lam) {
+  extern __shared__ double tsm[];  // d[n], e2[n]
+  const int b = blockIdx.y;
+  if (!flag[b]) return;
+  double* ds = tsm;
+  double* e2s = tsm + n;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    ds[i] = dall[(int64_t)b * n + i];
+    e2s[i] = i < n - 1 ? e2all[(int64_t)b * n + i] : 0.0;
+  }
+  __syncthreads();
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  double lo = info[b * 4 + 0], hi = info[b * 4 + 1];
+  const double span = info[b * 4 + 2];
+  const double tol = 4.0 * 2.220446049250313e-16 * span;
+  const double pivmin = 1e-30 * span + 1e-300;
+  for (int it = 0; it < 64 && hi - lo > tol; ++it) {
+    const double mid = 0.5 * (lo + hi);
+    if (sturm_count(ds, e2s, n, mid, pivmin) <= j) lo = mid;
+    else hi = mid;
+  }
+  lam[(int64_t)b * n + j] = 0.5 * (lo + hi);
+}
+
+__device__ __forceinline__ double hash_unit(uint32_t i, uint32_t j) {
+  uint32_t h = i * 0x9E3779B1u ^ (j + 0x7F4A7C15u) * 0x85EBCA77u;
+  h ^= h >> 15;
+  h *= 0x2C1B3C6Du;
+  h ^= h >> 12;
+  h *= 0x297A2D39u;
+  h ^= h >> 15;
+  return (double)(h & 0xFFFFFF) * (2.0 / 16777216.0) - 1.0 + 1.0 / 16777216.0;
+}
+
+// One thread per eigenvalue: inverse iteration with the LDL^T factors of
+// T - lambda I (tiny pivots replaced by +-eps * ||T||), two solves from a fixed
+// pseudo-random start, normalised.  Column n-1-j of Z (descending order).
+// Scratch L, Dinv: [i][j] layout (coalesced over the eigenvalue threads).
+__global__ void tri_inviter(const double* __restrict__ dall, const double* __restrict__ eall,
+                            const double* __restrict__ info, const double* __restrict__ lamall, const int* flag,
+                            int n, double* __restrict__ Zall, double* __restrict__ Lall, double* __restrict__ Dall) {
+  const int b = blockIdx.y;
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (!flag[b] || j >= n) return;
+  const double* d = dall + (int64_t)b * n;
+  const double* e = eall + (int64_t)b * n;
+  const int64_t nn = (int64_t)n * n;
+  double* Z = Zall + b * nn;
+  double* L = Lall + b * nn;
+  double* Di = Dall + b * nn;
+  const double lam = lamall[(int64_t)b * n + j];
+  const double span = info[b * 4 + 2];
+  const double small = 2.220446049250313e-16 * span + 1e-300;
+  const int col = n - 1 - j;
+  // factor
+  double D = d[0] - lam;
+  for (int i = 0; i < n; ++i) {
+    if (fabs(D) < small) D = D < 0.0 ? -small : small;
+    const double inv = 1.0 / D;
+    Di[(int64_t)i * n + j] = inv;
+    if (i < n - 1) {
+      const double l = e[i] * inv;
+      L[(int64_t)i * n + j] = l;
+      D = (d[i + 1] - lam) - l * e[i];
+    }
+  }
+  double s = 1.0;
+  for (int it = 0; it < 2; ++it) {
+    // forward: w_i = x_i - l_{i-1} w_{i-1}
+    double w = 0.0;
+    for (int i = 0; i < n; ++i) {
+      const double x = it == 0 ? hash_unit(i, j) : Z[(int64_t)i * n + col] * s;
+      w = i == 0 ? x : fma(-L[(int64_t)(i - 1) * n + j], w, x);
+      Z[(int64_t)i * n + col] = w;
+    }
+    // back: y_i = w_i / D_i - l_i y_{i+1}
+    double y = 0.0, nrm = 0.0;
+    for (int i = n - 1; i >= 0; --i) {
+      const double wi = Z[(int64_t)i * n + col] * Di[(int64_t)i * n + j];
+      y = i == n - 1 ? wi : fma(-L[(int64_t)i * n + j], y, wi);
+      Z[(int64_t)i * n + col] = y;
+      nrm = fma(y, y, nrm);
+    }
+    s = nrm > 0.0 && isfinite(nrm) ? 1.0 / sqrt(nrm) : 0.0;
+  }
+  for (int i = 0; i < n; ++i) Z[(int64_t)i * n + col] *= s;
+}
+
+// P = Z^T Z given in its lower triangle (K3 lower tiles): delta[b] = max |P - I|
+// over the lower triangle (bit-pattern max; NaN propagates); mirrors P's lower
+// triangle into its upper one.
+__global__ void ns_delta(const double* __restrict__ Pall, int n, const int* flag, const int* mode,
+                         unsigned long long* __restrict__ delta) {
+  const int b = blockIdx.y;
+  if (!flag[b] || mode[b] == 0) return;
+  const double* P = Pall + (int64_t)b * n * n;
+  double mx = 0.0;
+  const int64_t nn = (int64_t)n * n;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nn; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e / n, c = e - r * n;
+    if (c > r) continue;
+    const double pv = P[e];
+    if (c < r) const_cast<double*>(P)[c * n + r] = pv;  // symmetric P for the P^2 GEMM
+    const double dv = fabs(pv - (r == c ? 1.0 : 0.0));
+    mx = (isnan(dv) || dv > mx) ? dv : mx;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double t = __shfl_xor_sync(0xffffffffu, mx, o);
+    mx = (isnan(t) || t > mx) ? t : mx;
+  }
+  if ((threadIdx.x & 31) == 0) {
+    const unsigned long long bits = isnan(mx) ? 0x7ff8000000000000ull : (unsigned long long)__double_as_longlong(mx);
+    atomicMax(delta + b, bits);
+  }
+}
+
+#ifndef WT_NS_ORDER2_ONLY
+#define WT_NS_ORDER2_ONLY 0
+#endif
+constexpr bool kNsOrder2Only = WT_NS_ORDER2_ONLY;
+// Per-matrix Newton-Schulz decision from delta (independent of the other
+// matrices of the batch, so results do not depend on the batch composition).
+// With P = Z^T Z = I + E, |E| = delta:
+//   order 2: Z (3I - P)/2                       -> error ~ 3/4 delta^2
+//   order 3: Z (15I - 10P + 3P^2)/8             -> error ~ 5/16 delta^3
+// mode[b]: 0 = orthogonal (no update, P = I), 1 = order 2, 2 = order 3, -1 = fell back (V0 = I).
+// glim2[b] enables the P^2 GEMM for the order-3 matrices.
+__global__ void ns_decide(const unsigned long long* __restrict__ delta, int batch, double tol, double limit,
+                          int* flag, int* glim, int* mode, int* glim2, int* counts) {
+  for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < batch; b += gridDim.x * blockDim.x) {
+    glim2[b] = 0;
+    if (!flag[b] || mode[b] == 0) {
+      mode[b] = flag[b] ? 0 : -1;
+      continue;
+    }
+    const double dl = __longlong_as_double((long long)delta[b]);
+    if (dl <= tol) {
+      mode[b] = 0;
+    } else if (!(dl <= limit)) {
+      flag[b] = 0;
+      glim[b] = 0;
+      mode[b] = -1;
+    } else if (0.75 * dl * dl <= tol || kNsOrder2Only) {
+      mode[b] = 1;
+      atomicAdd(counts, 1);
+    } else {
+      mode[b] = 2;
+      glim2[b] = 0x7fffffff;
+      atomicAdd(counts, 1);
+      if (0.3125 * dl * dl * dl > tol) atomicAdd(counts + 1, 1);  // will need another round
+    }
+  }
+}
+
+// P (lower triangle of Z^T Z) and Q (lower triangle of P^2, order-3 matrices)
+// -> the full symmetric update polynomial in P.
+__global__ void ns_form(double* __restrict__ Pall, const double* __restrict__ Qall, int n, const int* mode) {
+  const int b = blockIdx.y;
+  const int md = mode[b];
+  if (md < 0) return;
+  double* P = Pall + (int64_t)b * n * n;
+  const double* Q = Qall + (int64_t)b * n * n;
+  const int64_t nn = (int64_t)n * n;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nn; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e / n, c = e - r * n;
+    if (c > r) continue;  // lower triangle + its mirror, one thread per pair
+    const double dg = r == c ? 1.0 : 0.0;
+    double v;
+    if (md == 0) v = dg;
+    else if (md == 1) v = fma(-0.5, P[e], 1.5 * dg);
+    else v = (15.0 * dg - 10.0 * P[e] + 3.0 * Q[e]) * 0.125;
+    P[e] = v;
+    if (c < r) P[c * n + r] = v;
+  }
+}
+
+// Compact-WY factor T (NBT x NBT upper triangular) of the block of reflectors
+// Y (columns k0 .. k0 + nb - 1 of the stored panels), from S = Y^T Y:
+// T_ii = tau_i, T[0:i, i] = -tau_i T[0:i, 0:i] S[0:i, i]   (dlarft, forward, columnwise)
+__global__ void wy_larft(const double* __restrict__ Sall, const double* __restrict__ tauall, const int* flag,
+                         int n, int k0, int nb, double* __restrict__ Tall) {
+  const int b = blockIdx.x;
+  if (!flag[b]) return;
+  extern __shared__ double T[];  // [NBT][NBT + 1]
+  const double* S = Sall + (int64_t)b * NBT * NBT;  // (read through L1)
+  const double* tau = tauall + (int64_t)b * n + k0;
+  for (int e = threadIdx.x; e < NBT * NBT; e += blockDim.x) T[(e / NBT) * (NBT + 1) + e % NBT] = 0.0;
+  __syncthreads();
+  for (int i = 0; i < nb; ++i) {
+    const double ti = tau[i];
+    const int r = threadIdx.x;
+    double s = 0.0;
+    if (r < i) {
+      for (int c = r; c < i; ++c) s = fma(T[r * (NBT + 1) + c], __ldg(S + c * NBT + i), s);
+    }
+    __syncthreads();
+    if (r < i) T[r * (NBT + 1) + i] = -ti * s;
+    if (r == i) T[r * (NBT + 1) + i] = ti;
+    __syncthreads();
+  }
+  double* Tg = Tall + (int64_t)b * NBT * NBT;
+  for (int e = threadIdx.x; e < NBT * NBT; e += blockDim.x) Tg[e] = T[(e / NBT) * (NBT + 1) + e % NBT];
+}
+
+// V0 = I for the matrices that fall back
+__global__ void set_identity(double* __restrict__ Vall, int n, const int* flag) {
+  const int b = blockIdx.y;
+  if (flag[b]) return;
+  double* V = Vall + (int64_t)b * n * n;
+  const int64_t nn = (int64_t)n * n;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nn; e += (int64_t)gridDim.x * blockDim.x)
+    V[e] = (e / n == e % n) ? 1.0 : 0.0;
+}
+
+struct Layout {
+  size_t G, Z, Z2, P, VW, WV, d, e, e2, tau, lam, info, S, T, M1, M2, delta, flag, glim, done, glim2, cnt, total;
+};
+
+Layout layout(int64_t n, int64_t batch) {
+  Layout L{};
+  size_t o = 0;
+  auto take = [&](size_t bytes) { size_t r = o; o = (o + bytes + 255) / 256 * 256; return r; };
+  const size_t nn = (size_t)(n * n * batch) * sizeof(double);
+  L.G = take(nn);
+  L.Z = take(nn);
+  L.Z2 = take(nn);
+  L.P = take(nn);  // also the inverse-iteration L factors; Z2 holds their 1/D
+  L.VW = take(sizeof(double) * (size_t)(batch * n * 2 * NB));
+  L.WV = take(sizeof(double) * (size_t)(batch * n * 2 * NB));
+  L.d = take(sizeof(double) * (size_t)(batch * n));
+  L.e = take(sizeof(double) * (size_t)(batch * n));
+  L.e2 = take(sizeof(double) * (size_t)(batch * n));
+  L.tau = take(sizeof(double) * (size_t)(batch * n));
+  L.lam = take(sizeof(double) * (size_t)(batch * n));
+  L.info = take(sizeof(double) * (size_t)(batch * 4));
+  L.S = take(sizeof(double) * (size_t)(batch * NBT * NBT));
+  L.T = take(sizeof(double) * (size_t)(batch * NBT * NBT));
+  L.M1 = take(sizeof(double) * (size_t)(batch * NBT * n));
+  L.M2 = take(sizeof(double) * (size_t)(batch * NBT * n));
+  L.delta = take(sizeof(unsigned long long) * (size_t)batch);
+  L.flag = take(sizeof(int) * (size_t)batch);
+  L.glim = take(sizeof(int) * (size_t)batch);
+  L.done = take(sizeof(int) * (size_t)batch);
+  L.glim2 = take(sizeof(int) * (size_t)batch);
+  L.cnt = take(sizeof(int) * 4);
+  L.total = o;
+  return L;
+}
+
+template <int C>
+int launch_panel(double* G, double* VW, double* WV, double* d, double* e, double* tau, const int* flag, int n,
+                 int k0, int64_t batch, cudaStream_t st) {
+  auto kern = tridiag_panel<C>;
+  const size_t smem = PanelSmem::bytes(n, C);
+  if (int r = ensure_smem(kern, smem)) return r;
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = C;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.gridDim = dim3((unsigned)(batch * C));
+  cfg.blockDim = dim3(PT);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cfg.attrs = attr;
+  cfg.numAttrs = C > 1 ? 1 : 0;
+  WT_CUDA(cudaLaunchKernelEx(&cfg, kern, G, VW, WV, d, e, tau, flag, n, k0));
+  return WT_OK;
+}
+
+}  // namespace eig
+
+size_t eig_workspace_bytes(int64_t n, int64_t batch) { return eig::layout(n, batch).total; }
+
+int eig_precondition(const double* Xt, double* Yt, int64_t m, int64_t n, int64_t ldx, int64_t sx, int64_t batch,
+                     void* ws, size_t ws_bytes, int* n_fallback, cudaStream_t st) {
+  using namespace eig;
+  const Layout L = layout(n, batch);
+  WT_REQUIRE(ws != nullptr && ws_bytes >= L.total, "eig: workspace too small");
+  WT_REQUIRE(n >= 3 && n <= 8 * MAXR, "eig: n = %lld unsupported", (long long)n);
+  char* base = static_cast<char*>(ws);
+  auto D = [&](size_t off) { return reinterpret_cast<double*>(base + off); };
+  double *G = D(L.G), *Z = D(L.Z), *Z2 = D(L.Z2), *P = D(L.P), *VW = D(L.VW), *WV = D(L.WV);
+  double *dd = D(L.d), *ee = D(L.e), *e2 = D(L.e2), *tau = D(L.tau), *lam = D(L.lam), *info = D(L.info);
+  double *S = D(L.S), *T = D(L.T), *M1 = D(L.M1), *M2 = D(L.M2);
+  auto* delta = reinterpret_cast<unsigned long long*>(base + L.delta);
+  int* flag = reinterpret_cast<int*>(base + L.flag);
+  int* glim = reinterpret_cast<int*>(base + L.glim);
+  const int64_t nn = n * n;
+  const int ni = (int)n;
+  // WT_EIG_PROFILE=1: per-phase device times on stderr (diagnostics)
+  static const bool prof = getenv("WT_EIG_PROFILE") != nullptr;
+  cudaEvent_t ev[8] = {};
+  int nev = 0;
+  auto mark = [&]() {
+    if (!prof) return;
+    cudaEventCreate(&ev[nev]);
+    cudaEventRecord(ev[nev++], st);
+  };
+  mark();
+
+  // 1. G = X^T X (rows of Xt are the columns of X)
+  if (int r = gemm_f64_lim(0, 1, n, n, m, 1.0, Xt, ldx, sx, Xt, ldx, sx, 0.0, G, n, nn, batch, nullptr, nullptr, st,
+                           1))  // lower tiles: the tridiagonalization reads only the lower triangle
+    return r;
+  gram_flag<<<(unsigned)batch, PT, 0, st>>>(G, ni, flag, glim);
+  mark();
+  WT_CUDA(cudaMemsetAsync(VW, 0, sizeof(double) * (size_t)(batch * n * 2 * NB), st));
+  WT_CUDA(cudaMemsetAsync(WV, 0, sizeof(double) * (size_t)(batch * n * 2 * NB), st));
+  // cluster size: enough CTAs per matrix to occupy the SMs, >= 64 rows per CTA
+  // (at most MAXR rows per CTA: the panel's rows of V and W stay in shared memory)
+  // (C depends on n only, so that a matrix gets the same bits in any batch)
+  int C = 1;
+  while (C < 8 && n > (int64_t)C * PREF_R) C *= 2;
+  // 2. tridiagonalization, panel by panel
+  for (int64_t k0 = 0; k0 < n; k0 += NB) {
+    int r = WT_OK;
+    switch (C) {
+      case 8: r = launch_panel<8>(G, VW, WV, dd, ee, tau, flag, ni, (int)k0, batch, st); break;
+      case 4: r = launch_panel<4>(G, VW, WV, dd, ee, tau, flag, ni, (int)k0, batch, st); break;
+      case 2: r = launch_panel<2>(G, VW, WV, dd, ee, tau, flag, ni, (int)k0, batch, st); break;
+      default: r = launch_panel<1>(G, VW, WV, dd, ee, tau, flag, ni, (int)k0, batch, st);
+    }
+    if (r) return r;
+    const int64_t k1 = k0 + NB;
+    if (k1 < n) {  // A22 -= [V W] [W V]^T, lower tiles only
+      const int64_t off = k1 * n + k1, offp = k1 * 2 * NB;
+      if (int r2 = gemm_f64_lim(0, 1, n - k1, n - k1, 2 * NB, -1.0, VW + offp, 2 * NB, n * 2 * NB, WV + offp, 2 * NB,
+                                n * 2 * NB, 1.0, G + off, n, nn, batch, nullptr, glim, st, 1))
+        return r2;
+    }
+  }
+  if (int r = check_launch("eig tridiagonalization")) return r;
+  mark();
+  // 3-4. eigenvalues (bisection) and eigenvectors (inverse iteration) of T
+  tri_prepare<<<(unsigned)batch, PT, 0, st>>>(dd, ee, e2, info, flag, ni);
+  {
+    dim3 grid((unsigned)((n + 127) / 128), (unsigned)batch);
+    if (int r = ensure_smem(tri_bisect, 2 * sizeof(double) * (size_t)n)) return r;
+    tri_bisect<<<grid, 128, 2 * sizeof(double) * (size_t)n, st>>>(dd, e2, info, flag, ni, lam);
+    tri_inviter<<<grid, 128, 0, st>>>(dd, ee, info, lam, flag, ni, Z, P, Z2);
+  }
+  if (int r = check_launch("eig bisection / inverse iteration")) return r;
+  mark();
+  // 5. Newton-Schulz on Z until orthogonal to rounding (delta = max |Z^T Z - I|),
+  //    order 2 or 3 per matrix as its delta needs (ns_decide); every decision is
+  //    per matrix, so the result does not depend on the batch.
+  const double done_tol = 64.0 * 2.220446049250313e-16 * sqrt((double)n);
+  constexpr int kMaxNs = 3;
+  int* mode = reinterpret_cast<int*>(base + L.done);
+  int* glim2 = reinterpret_cast<int*>(base + L.glim2);
+  int* counts = reinterpret_cast<int*>(base + L.cnt);
+  WT_CUDA(cudaMemsetAsync(mode, 0xff, sizeof(int) * (size_t)batch, st));  // -1 != 0: not yet known
+  int h_counts[2] = {0, 0};
+  for (int it = 0; it < kMaxNs; ++it) {
+    if (int r = gemm_f64_lim(1, 0, n, n, n, 1.0, Z, n, nn, Z, n, nn, 0.0, P, n, nn, batch, nullptr, glim, st, 1))
+      return r;
+    WT_CUDA(cudaMemsetAsync(delta, 0, sizeof(unsigned long long) * (size_t)batch, st));
+    WT_CUDA(cudaMemsetAsync(counts, 0, 2 * sizeof(int), st));
+    const dim3 grid((unsigned)std::min<int64_t>((nn + 255) / 256, 64), (unsigned)batch);
+    ns_delta<<<grid, 256, 0, st>>>(P, ni, flag, mode, delta);
+    // last iteration: keep only the matrices this update brings to rounding
+    const double lim = it == kMaxNs - 1 ? cbrt(done_tol / 0.3125) : 0.25;
+    ns_decide<<<(unsigned)((batch + 255) / 256), 256, 0, st>>>(delta, (int)batch, done_tol, lim, flag, glim, mode,
+                                                             glim2, counts);
+    WT_CUDA(cudaMemcpyAsync(h_counts, counts, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
+    WT_CUDA(cudaStreamSynchronize(st));
+    if (h_counts[0] == 0) break;  // every matrix orthogonal (or fallen back)
+    // P^2 for the order-3 matrices (lower tiles; P still holds the lower triangle of Z^T Z)
+    if (int r = gemm_f64_lim(0, 1, n, n, n, 1.0, P, n, nn, P, n, nn, 0.0, Z2, n, nn, batch, nullptr, glim2, st, 1))
+      return r;
+    ns_form<<<grid, 256, 0, st>>>(P, Z2, ni, mode);
+    if (int r = gemm_f64_lim(0, 0, n, n, n, 1.0, Z, n, nn, P, n, nn, 0.0, Z2, n, nn, batch, nullptr, glim, st))
+      return r;
+    std::swap(Z, Z2);
+    if (h_counts[1] == 0) break;  // every update reached rounding: no further check needed
+    // (the next P of the matrices already at rounding: mode 0 is kept via ns_delta's skip)
+  }
+  // (after kMaxNs iterations every matrix left is done or fell back: see lim)
+  std::vector<int> hflag((size_t)batch);
+  WT_CUDA(cudaMemcpyAsync(hflag.data(), flag, sizeof(int) * (size_t)batch, cudaMemcpyDeviceToHost, st));
+  mark();
+  // 6. V0 = Q Z: blocks of NBT reflectors, last block first
+  const int64_t nref = n - 2;  // reflectors 0 .. n-3 (tau = 0 beyond)
+  for (int64_t k0 = ((nref - 1) / NBT) * NBT; k0 >= 0; k0 -= NBT) {
+    const int64_t nb = std::min<int64_t>(NBT, nref - k0);
+    const int64_t r0 = k0 + 1;  // first nonzero row of the block
+    const double* Y = G + r0 * n + k0;  // rows r0.., columns k0.. (ld n)
+    // S = Y^T Y
+    if (int r = gemm_f64_lim(1, 0, nb, nb, n - r0, 1.0, Y, n, nn, Y, n, nn, 0.0, S, NBT, NBT * NBT, batch, nullptr,
+                             glim, st))
+      return r;
+    if (nb < NBT) WT_CUDA(cudaMemsetAsync(T, 0, sizeof(double) * (size_t)(batch * NBT * NBT), st));
+    const size_t tsm = sizeof(double) * NBT * (NBT + 1);
+    if (int r = ensure_smem(wy_larft, tsm)) return r;
+    wy_larft<<<(unsigned)batch, NBT, tsm, st>>>(S, tau, flag, ni, (int)k0, (int)nb, T);
+    // M1 = Y^T Z (nb x n), M2 = T M1, Z[r0:, :] -= Y M2
+    if (int r = gemm_f64_lim(1, 0, nb, n, n - r0, 1.0, Y, n, nn, Z + r0 * n, n, nn, 0.0, M1, n, NBT * n, batch,
+                             nullptr, glim, st))
+      return r;
+    if (int r = gemm_f64_lim(0, 0, nb, n, nb, 1.0, T, NBT, NBT * NBT, M1, n, NBT * n, 0.0, M2, n, NBT * n, batch,
+                             nullptr, glim, st))
+      return r;
+    if (int r = gemm_f64_lim(0, 0, n - r0, n, nb, -1.0, Y, n, nn, M2, n, NBT * n, 1.0, Z + r0 * n, n, nn, batch,
+                             nullptr, glim, st))
+      return r;
+  }
+  {
+    dim3 grid((unsigned)std::min<int64_t>((nn + 255) / 256, 256), (unsigned)batch);
+    set_identity<<<grid, 256, 0, st>>>(Z, ni, flag);
+  }
+  if (int r = check_launch("eig back-transformation")) return r;
+  mark();
+  // 7. Y = X V0  (Yt = V0^T Xt)
+  if (int r = gemm_f64_lim(1, 0, n, m, n, 1.0, Z, n, nn, Xt, ldx, sx, 0.0, Yt, ldx, sx, batch, nullptr, nullptr, st))
+    return r;
+  mark();
+  if (prof && nev > 1) {
+    cudaEventSynchronize(ev[nev - 1]);
+    static const char* names[] = {"gram", "tridiag", "bisect+inviter", "newton-schulz", "backtransform", "X V0"};
+    fprintf(stderr, "[wt_eig] n=%lld batch=%lld C=%d:", (long long)n, (long long)batch, C);
+    for (int i = 1; i < nev; ++i) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, ev[i - 1], ev[i]);
+      fprintf(stderr, " %s %.3f ms", i - 1 < 6 ? names[i - 1] : "?", ms);
+    }
+    fprintf(stderr, "\n");
+    for (int i = 0; i < nev; ++i) cudaEventDestroy(ev[i]);
+  }
+  if (n_fallback) {
+    WT_CUDA(cudaStreamSynchronize(st));
+    int active = 0;
+    for (int64_t b = 0; b < batch; ++b) active += hflag[b] != 0;
+    *n_fallback = (int)batch - active;
+  }
+  return WT_OK;
+}
+
+}  // namespace wt

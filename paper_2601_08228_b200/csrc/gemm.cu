@@ -41,6 +41,7 @@ struct GemmArgs {
   int64_t batch;
   const int* klim;  // per-matrix inner-dimension limit (nullable)
   const int* nlim;  // per-matrix output-column limit (nullable)
+  int lower;        // 1: only tiles touching the lower triangle (n0 < m0 + BM) are computed
 };
 
 template <int BM, int BN, bool TA, bool TB>
@@ -68,6 +69,7 @@ __global__ void __launch_bounds__(WM* WN * 32, (WM * WN == 8 && BN == 64) ? 2 : 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm0 = (warp / WN) * WTM, wn0 = (warp % WN) * WTN;
   const int64_t m0 = (int64_t)blockIdx.y * BM, n0 = (int64_t)blockIdx.x * BN;
+  if (g.lower && n0 >= m0 + BM) return;  // tile strictly above the diagonal (symmetric updates)
   // Loader geometry, fixed for the whole kernel: each thread owns A_IT (B_IT)
   // 16-byte chunks of every stage at the same tile position; only the k offset
   // moves, so a stage's addresses are one multiply-add per chunk (ncu: the
@@ -281,7 +283,7 @@ using namespace wt;
 int wt::gemm_f64_lim(int transA, int transB, int64_t M, int64_t N, int64_t K, double alpha,
                      const double* A, int64_t lda, int64_t strideA, const double* B, int64_t ldb,
                      int64_t strideB, double beta, double* C, int64_t ldc, int64_t strideC,
-                     int64_t batch, const int* klim, const int* nlim, void* stream) {
+                     int64_t batch, const int* klim, const int* nlim, void* stream, int lower) {
   WT_REQUIRE(M >= 0 && N >= 0 && K >= 0 && batch >= 0, "gemm: negative dimension");
   if (M == 0 || N == 0 || batch == 0) return WT_OK;
   WT_REQUIRE(ldc >= N, "gemm: ldc < N");
@@ -293,7 +295,8 @@ int wt::gemm_f64_lim(int transA, int transB, int64_t M, int64_t N, int64_t K, do
     gemm_scale_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(C, M, N, ldc, strideC, beta);
     return check_launch("wt_gemm_f64(K=0)");
   }
-  GemmArgs g{M, N, K, alpha, beta, A, lda, strideA, B, ldb, strideB, C, ldc, strideC, batch, klim, nlim};
+  GemmArgs g{M, N, K, alpha, beta, A, lda, strideA, B, ldb, strideB, C, ldc, strideC, batch, klim, nlim,
+             lower};
   cudaStream_t st = (cudaStream_t)stream;
   if (!transA && !transB) return dispatch_vec<false, false>(g, st);
   if (!transA && transB) return dispatch_vec<false, true>(g, st);

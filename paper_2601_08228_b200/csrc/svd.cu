@@ -58,6 +58,7 @@ static thread_local int g_last_sweeps = 0;
 static thread_local long long g_last_rotations = 0;
 static thread_local long long g_last_panel_rows = 0;
 static thread_local int g_last_hb = 16;
+static thread_local int g_last_fallbacks = -1;  // -1: no preconditioning; else matrices that fell back to V0 = I
 }  // namespace wt
 
 #define SVD_NS hb16
@@ -70,6 +71,10 @@ using namespace wt;
 
 // Sweeps used by the last wt_svd_jacobi_f64 call on this thread (diagnostics).
 extern "C" int wt_svd_last_sweeps(void) { return g_last_sweeps; }
+
+// Matrices of the last call that were not preconditioned (V0 = I fallback), or
+// -1 if the call ran without the preconditioner (diagnostics).
+extern "C" int wt_svd_last_fallbacks(void) { return g_last_fallbacks; }
 
 // FP64 flops executed by the Jacobi iteration of the last call on this thread:
 // every rotated pair visit = Gram (upper 8x8 tiles) + Z Q on an mpad x BW

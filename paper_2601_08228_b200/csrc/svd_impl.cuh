@@ -788,6 +788,10 @@ __global__ void svd_permute_cols(SvdWs ws, int64_t mpad, int64_t npad) {
   for (int64_t r = threadIdx.x; r < mpad / 2; r += blockDim.x) dst[r] = src[r];
 }
 
+__global__ void svd_fill_int(int* a, int n, int v) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) a[i] = v;
+}
+
 __global__ void svd_iota(int* a, int n) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) a[i] = i;
 }
@@ -800,9 +804,22 @@ __global__ void svd_flip(SvdWs ws, int batch) {
 struct WsLayout {
   int64_t m, n, mpad, npad;
   size_t off_X, off_X2, off_xsel, off_active, off_off, off_conv, off_pending, off_sig, off_perm, off_bdone,
-      off_bver, off_pclean, total;
-  bool skip;  // pair-skip bookkeeping (nblk <= kSkipMaxBlocks)
+      off_bver, off_pclean, off_eig, eig_bytes, total;
+  bool skip;     // pair-skip bookkeeping (nblk <= kSkipMaxBlocks)
+  bool precond;  // Gram-eigenbasis preconditioner (eig.cu) before the sweeps
 };
+
+// Slices with at least this many short-side columns start the sweeps from
+// X V0, V0 = eigenbasis of X^T X (eig.cu): 3 sweeps instead of 12-17 on the
+// config 3-5 slices.  Below it plain Jacobi is cheap enough.
+constexpr int64_t kPrecondMinN = 128;
+inline bool precond_enabled(int64_t n) {
+  static const int env = [] {
+    const char* e = getenv("WT_SVD_PRECOND");
+    return e ? atoi(e) : 1;
+  }();
+  return env != 0 && n >= kPrecondMinN && n <= 2048;
+}
 
 WsLayout ws_layout(int64_t n1, int64_t n2, int64_t batch) {
   WsLayout L{};
@@ -826,6 +843,9 @@ WsLayout ws_layout(int64_t n1, int64_t n2, int64_t batch) {
   L.skip = nbk <= kSkipMaxBlocks;
   L.off_bver = take(L.skip ? sizeof(int) * (size_t)(batch * nbk) : 0);
   L.off_pclean = take(L.skip ? sizeof(unsigned long long) * (size_t)(batch * nbk * nbk) : 0);
+  L.precond = precond_enabled(L.n);
+  L.eig_bytes = L.precond ? eig_workspace_bytes(L.n, batch) : 0;
+  L.off_eig = take(L.eig_bytes);
   L.total = o;
   return L;
 }
@@ -923,6 +943,18 @@ int jacobi(const double* A, int64_t lda, int64_t strideA, int64_t n1,
   WT_CUDA(cudaMemsetAsync(ws.offmax, 0, sizeof(unsigned long long) * batch, st));
   WT_CUDA(cudaMemsetAsync(ws.conv, 0, sizeof(int) * batch, st));
   WT_CUDA(cudaMemsetAsync(ws.xsel, 0, sizeof(int) * batch, st));
+  g_last_fallbacks = -1;
+  if (L.precond) {
+    // X2 <- X V0 (rows n .. npad-1 of the column-major panels stay zero), then
+    // every matrix starts from buffer 1
+    WT_CUDA(cudaMemsetAsync(ws.X2, 0, sizeof(double) * (size_t)(batch * L.npad * L.mpad), st));
+    int fallback = 0;
+    if (int e = eig_precondition(ws.X, ws.X2, L.mpad, L.n, L.mpad, L.npad * L.mpad, batch, base + L.off_eig,
+                                 L.eig_bytes, &fallback, st))
+      return e;
+    g_last_fallbacks = fallback;
+    svd_fill_int<<<(unsigned)((batch + 255) / 256), 256, 0, st>>>(ws.xsel, (int)batch, 1);
+  }
   svd_iota<<<(unsigned)((batch + 255) / 256), 256, 0, st>>>(ws.active, (int)batch);
   int64_t n_active = batch;
   WT_CUDA(cudaMemsetAsync(ws.pending, 0, sizeof(int) * 3, st));
