@@ -45,12 +45,19 @@ constexpr int NB = 32;     // tridiagonalization panel width
 constexpr int NBT = 64;    // back-transformation block (reflectors per compact-WY block)
 constexpr int PT = 256;    // panel kernel threads
 constexpr int NW = PT / 32;
-constexpr int CH = 256;    // symv column chunk (CH / 64 double2 register accumulators per lane)
+#ifndef WT_EIG_CH
+#define WT_EIG_CH 256
+#endif
+#ifndef WT_EIG_RB
+#define WT_EIG_RB 4
+#endif
+constexpr int CH = WT_EIG_CH;  // symv column chunk (CH / 64 double2 register accumulators per lane)
 constexpr int NCH2 = CH / 64;
-constexpr int RB = 4;      // rows per warp in flight in the symv
+constexpr int RB = WT_EIG_RB;  // rows per warp in flight in the symv
+static_assert(RB == 4, "the symv's row-sum reduction handles exactly 4 rows per warp");
 constexpr int MAXR = 256;  // own rows per CTA (the panel's V, W rows of a CTA live in shared memory)
 constexpr int PREF_R = 128;  // preferred own rows per CTA (two CTAs per SM)
-constexpr int VP = 2 * NB + 1;  // shared pitch of a [V | W] row
+constexpr int VP = 2 * NB + 2;  // shared pitch of a [V | W] row (even: 16-byte aligned rows)
 
 __device__ __forceinline__ void cl_sync() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
@@ -93,7 +100,7 @@ __device__ __forceinline__ double block_sum(double v, double* red) {
 struct PanelSmem {
   static size_t bytes(int n, int C) {
     const int R = (n + C - 1) / C;
-    return sizeof(double) * ((size_t)R * VP + 1 + 2 * (size_t)n + 2 + 2 * (size_t)R + (size_t)NW * CH + 4 + 2 +
+    return sizeof(double) * ((size_t)R * VP + 8 + 2 * (size_t)n + 2 + 2 * (size_t)R + (size_t)NW * CH + 4 + 2 +
                              2 * NB + 2 * NW + 7 * NB + NW * (2 * NB + 1));
   }
 };
@@ -119,10 +126,11 @@ __global__ void __launch_bounds__(PT, 2) tridiag_panel(double* __restrict__ Gall
   const int R = (n + C - 1) / C;  // local rows (upper bound)
   double* vws = sm;                    // [R][VP]  my rows of [V | W]
   double* vsm = vws + ((R * VP + 1) & ~1);  // [n + 2]  v (full; 16-byte aligned, zero beyond n)
-  double* csum = vsm + n + 2;          // [n]  CTA partial column part of A22 v (DSMEM-visible)
-  double* prow = csum + n;             // [R]  my rows: row part of A22 v
-  double* diag = prow + R;             // [R]  my rows: A[i][i] (pre-panel)
-  double* wacc = diag + R;             // [NW][CH] per-warp column accumulators
+  // (every array starts 16-byte aligned: double2 accesses)
+  double* csum = vsm + ((n + 3) & ~1); // [n]  CTA partial column part of A22 v (DSMEM-visible)
+  double* prow = csum + ((n + 1) & ~1);  // [R]  my rows: row part of A22 v
+  double* diag = prow + ((R + 1) & ~1);  // [R]  my rows: A[i][i] (pre-panel)
+  double* wacc = diag + ((R + 1) & ~1);  // [NW][CH] per-warp column accumulators
   double* part1 = wacc + NW * CH;      // [4]  ss, alpha (S1)
   double* part3 = part1 + 4;           // [2 + 2NB] pv, -, yW[NB], yV[NB] (S3)
   double* red = part3 + 2 + 2 * NB;    // [2NW]
@@ -173,10 +181,14 @@ __global__ void __launch_bounds__(PT, 2) tridiag_panel(double* __restrict__ Gall
         double a0 = anext[u], a1 = 0.0, a2 = 0.0, a3 = 0.0;
         int t = 0;
         for (; t + 2 <= j; t += 2) {
-          a0 = fma(-ri[t], rk[NB + t], a0);
-          a1 = fma(-ri[NB + t], rk[t], a1);
-          a2 = fma(-ri[t + 1], rk[NB + t + 1], a2);
-          a3 = fma(-ri[NB + t + 1], rk[t + 1], a3);
+          const double2 v2 = *reinterpret_cast<const double2*>(ri + t);
+          const double2 w2 = *reinterpret_cast<const double2*>(ri + NB + t);
+          const double2 kv = *reinterpret_cast<const double2*>(rk + t);
+          const double2 kw = *reinterpret_cast<const double2*>(rk + NB + t);
+          a0 = fma(-v2.x, kw.x, a0);
+          a1 = fma(-w2.x, kv.x, a1);
+          a2 = fma(-v2.y, kw.y, a2);
+          a3 = fma(-w2.y, kv.y, a3);
         }
         if (t < j) {
           a0 = fma(-ri[t], rk[NB + t], a0);
@@ -403,10 +415,14 @@ __global__ void __launch_bounds__(PT, 2) tridiag_panel(double* __restrict__ Gall
         double p1 = 0.0, p2 = 0.0, p3 = 0.0;
         int t = 0;
         for (; t + 2 <= j; t += 2) {
-          p = fma(-ri[t], ys[t], p);
-          p1 = fma(-ri[NB + t], ys[NB + t], p1);
-          p2 = fma(-ri[t + 1], ys[t + 1], p2);
-          p3 = fma(-ri[NB + t + 1], ys[NB + t + 1], p3);
+          const double2 v2 = *reinterpret_cast<const double2*>(ri + t);
+          const double2 w2 = *reinterpret_cast<const double2*>(ri + NB + t);
+          const double2 yw = *reinterpret_cast<const double2*>(ys + t);
+          const double2 yv = *reinterpret_cast<const double2*>(ys + NB + t);
+          p = fma(-v2.x, yw.x, p);
+          p1 = fma(-w2.x, yv.x, p1);
+          p2 = fma(-v2.y, yw.y, p2);
+          p3 = fma(-w2.y, yv.y, p3);
         }
         if (t < j) {
           p = fma(-ri[t], ys[t], p);
@@ -638,22 +654,51 @@ __global__ void tri_inviter(const double* __restrict__ dall, const double* __res
       D = (d[i + 1] - lam) - l * e[i];
     }
   }
+  // two solves; the per-step operands are loaded in batches of IB ahead of the
+  // dependent chains (the loads do not depend on the chain: latency overlaps)
+  constexpr int IB = 16;
   double s = 1.0;
   for (int it = 0; it < 2; ++it) {
     // forward: w_i = x_i - l_{i-1} w_{i-1}
     double w = 0.0;
-    for (int i = 0; i < n; ++i) {
-      const double x = it == 0 ? hash_unit(i, j) : Z[(int64_t)i * n + col] * s;
-      w = i == 0 ? x : fma(-L[(int64_t)(i - 1) * n + j], w, x);
-      Z[(int64_t)i * n + col] = w;
+    for (int i0 = 0; i0 < n; i0 += IB) {
+      double xb[IB], lb[IB];
+#pragma unroll
+      for (int u = 0; u < IB; ++u) {
+        const int i = i0 + u;
+        xb[u] = i < n ? (it == 0 ? hash_unit(i, j) : Z[(int64_t)i * n + col] * s) : 0.0;
+        lb[u] = (i > 0 && i < n) ? L[(int64_t)(i - 1) * n + j] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < IB; ++u) {
+        const int i = i0 + u;
+        if (i < n) {
+          w = i == 0 ? xb[u] : fma(-lb[u], w, xb[u]);
+          Z[(int64_t)i * n + col] = w;
+        }
+      }
     }
     // back: y_i = w_i / D_i - l_i y_{i+1}
     double y = 0.0, nrm = 0.0;
-    for (int i = n - 1; i >= 0; --i) {
-      const double wi = Z[(int64_t)i * n + col] * Di[(int64_t)i * n + j];
-      y = i == n - 1 ? wi : fma(-L[(int64_t)i * n + j], y, wi);
-      Z[(int64_t)i * n + col] = y;
-      nrm = fma(y, y, nrm);
+    for (int i1 = n - 1; i1 >= 0; i1 -= IB) {
+      double wb[IB], db[IB], lb[IB];
+#pragma unroll
+      for (int u = 0; u < IB; ++u) {
+        const int i = i1 - u;
+        wb[u] = i >= 0 ? Z[(int64_t)i * n + col] : 0.0;
+        db[u] = i >= 0 ? Di[(int64_t)i * n + j] : 0.0;
+        lb[u] = (i >= 0 && i < n - 1) ? L[(int64_t)i * n + j] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < IB; ++u) {
+        const int i = i1 - u;
+        if (i >= 0) {
+          const double wi = wb[u] * db[u];
+          y = i == n - 1 ? wi : fma(-lb[u], y, wi);
+          Z[(int64_t)i * n + col] = y;
+          nrm = fma(y, y, nrm);
+        }
+      }
     }
     s = nrm > 0.0 && isfinite(nrm) ? 1.0 / sqrt(nrm) : 0.0;
   }
@@ -866,7 +911,7 @@ int eig_precondition(const double* Xt, double* Yt, int64_t m, int64_t n, int64_t
   const int ni = (int)n;
   // WT_EIG_PROFILE=1: per-phase device times on stderr (diagnostics)
   static const bool prof = getenv("WT_EIG_PROFILE") != nullptr;
-  cudaEvent_t ev[8] = {};
+  cudaEvent_t ev[10] = {};
   int nev = 0;
   auto mark = [&]() {
     if (!prof) return;
@@ -914,6 +959,7 @@ int eig_precondition(const double* Xt, double* Yt, int64_t m, int64_t n, int64_t
     dim3 grid((unsigned)((n + 127) / 128), (unsigned)batch);
     if (int r = ensure_smem(tri_bisect, 2 * sizeof(double) * (size_t)n)) return r;
     tri_bisect<<<grid, 128, 2 * sizeof(double) * (size_t)n, st>>>(dd, e2, info, flag, ni, lam);
+    mark();
     tri_inviter<<<grid, 128, 0, st>>>(dd, ee, info, lam, flag, ni, Z, P, Z2);
   }
   if (int r = check_launch("eig bisection / inverse iteration")) return r;
@@ -993,12 +1039,13 @@ int eig_precondition(const double* Xt, double* Yt, int64_t m, int64_t n, int64_t
   mark();
   if (prof && nev > 1) {
     cudaEventSynchronize(ev[nev - 1]);
-    static const char* names[] = {"gram", "tridiag", "bisect+inviter", "newton-schulz", "backtransform", "X V0"};
+    static const char* names[] = {"gram", "tridiag", "prep+bisect", "inviter", "newton-schulz", "backtransform",
+                                  "X V0"};
     fprintf(stderr, "[wt_eig] n=%lld batch=%lld C=%d:", (long long)n, (long long)batch, C);
     for (int i = 1; i < nev; ++i) {
       float ms = 0.f;
       cudaEventElapsedTime(&ms, ev[i - 1], ev[i]);
-      fprintf(stderr, " %s %.3f ms", i - 1 < 6 ? names[i - 1] : "?", ms);
+      fprintf(stderr, " %s %.3f ms", i - 1 < 7 ? names[i - 1] : "?", ms);
     }
     fprintf(stderr, "\n");
     for (int i = 0; i < nev; ++i) cudaEventDestroy(ev[i]);
