@@ -141,11 +141,32 @@ def sp_w_svd_device(x: torch.Tensor, r: int, levels: int, tol: float = 0.0,
     return E.lift_inverse(rec, n1, n2, p, levels, mask=mask, slice_base=base, out=out)
 
 
+_STREAM_MIN_BYTES = 64 << 20  # host cubes from this size stream through the GPU in row chunks
+
+
+def _coarse_truncate(r, tol=0.0):
+    def decompose(coarse):
+        sigma, vec, info = E.svd(coarse, r, tol=tol)
+        E.raise_if_failed(info)
+        return E.truncated_recon(coarse, sigma, vec, r)
+    return decompose
+
+
 def sp_w_svd(a, r, levels):
-    """Sparse rank-r reconstruction: truncate only the coarsest stacks (decomposition.py:140-154)."""
+    """Sparse rank-r reconstruction: truncate only the coarsest stacks (decomposition.py:140-154).
+
+    Host (numpy) cubes of 64 MB and more stream through the GPU: the H2D of row
+    chunk i+1 overlaps K1 of chunk i, and the D2H of the reconstruction overlaps
+    K2 (engine.host_slices_pipeline); the arithmetic is the device path's."""
     a, dev = _prep(a)
     _check_rank(r, a.shape[0], a.shape[1])
     _check_levels(a.shape[2], levels)
+    n1, n2, p = a.shape
+    if not dev and a.nbytes >= _STREAM_MIN_BYTES and n2 % 2 == 0:
+        m = p >> levels
+        mask = E.level_mask(levels, smooth=True, details=[levels])
+        return E.host_slices_pipeline(np.ascontiguousarray(a), levels, mask, p - 2 * m, _coarse_truncate(r),
+                                      n1, n2)
     return _out(sp_w_svd_device(E.as_device(a), r, levels), dev)
 
 

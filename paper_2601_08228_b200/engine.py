@@ -205,6 +205,97 @@ def host_lift(src, n1: int, n2: int, p: int, levels: int, forward: bool) -> torc
     return out
 
 
+def host_slices_pipeline(src: np.ndarray, levels: int, mask: int, base: int, decompose,
+                         out_rows: int, out_cols: int) -> np.ndarray:
+    """Host cube in, host cube out, with the PCIe traffic overlapped with K1 / K2.
+
+    ``src`` is the (n1, n2, p) host array.  Row chunks of it are staged through
+    the pinned ring, copied H2D and lifted by K1, which stores each chunk's rows
+    of packed slices ``base .. p-1`` (as selected by ``mask``) straight into the
+    device slice buffer (p - base, n1, n2) through a per-chunk table of row-block
+    addresses (wt_lift_fwd_f64_peer), so H2D of chunk i+1 overlaps K1 of chunk i.
+    ``decompose(slices)`` returns the (p - base, out_rows, out_cols) result slices;
+    K2 then loads them back chunk by chunk of result rows (wt_lift_inv_f64_peer)
+    while the D2H of the previous chunk drains into the pinned result.  Returns
+    the (out_rows, out_cols, p) result as a numpy view of pinned memory.
+    """
+    lib = N.require_gpu()  # noqa: F841  (fail loudly without the library / a GPU)
+    n1, n2, p = src.shape
+    K = p - base
+    dev = torch.device("cuda", torch.cuda.current_device())
+    slices = torch.empty((K, n1, n2), dtype=F64, device=dev)
+    s_in, s_cmp, s_out = _pipe_streams()
+    main = torch.cuda.current_stream()
+    for st in (s_in, s_cmp, s_out):
+        st.wait_stream(main)
+
+    def tables(buf, rows_total, cols, chunks):
+        base_ptr = buf.data_ptr()
+        t = np.empty((len(chunks), K), dtype=np.int64)
+        for c, (r0, _) in enumerate(chunks):
+            t[c] = base_ptr + (np.arange(K, dtype=np.int64) * rows_total + r0) * cols * 8
+        return torch.from_numpy(t).to(dev)
+
+    rows, chunks = _row_chunks(n1, n2 * p)
+    tab_f = tables(slices, n1, n2, chunks)
+    cap = rows * n2 * p
+    with _stage_lock:
+        if not _stage_ring:
+            _upload_locked(torch.empty(0, dtype=F64), dev)  # allocate the pinned ring
+        dx = [torch.empty(cap, dtype=F64, device=dev) for _ in range(2)]
+        free_in = [None, None]
+        for i, (r0, r1) in enumerate(chunks):
+            b = i % 2
+            n = (r1 - r0) * n2 * p
+            with torch.cuda.stream(s_in):
+                if free_in[b] is not None:
+                    s_in.wait_event(free_in[b])
+                part = torch.from_numpy(src[r0:r1]).reshape(-1)
+                for c0 in range(0, n, _STAGE_ELEMS):
+                    stage, ev = _stage_ring[(i + c0 // _STAGE_ELEMS) % _STAGE_SLOTS]
+                    ev.synchronize()
+                    m = min(_STAGE_ELEMS, n - c0)
+                    stage[:m].copy_(part[c0:c0 + m])
+                    dx[b][c0:c0 + m].copy_(stage[:m], non_blocking=True)
+                    ev.record(s_in)
+                loaded = torch.cuda.Event()
+                loaded.record(s_in)
+            with torch.cuda.stream(s_cmp):
+                s_cmp.wait_event(loaded)
+                lift_forward_peer(dx[b][:n].view(r1 - r0, n2, p), levels, tab_f[i], mask, base)
+                free_in[b] = torch.cuda.Event()
+                free_in[b].record(s_cmp)
+    main.wait_stream(s_cmp)
+    result = decompose(slices)                                  # (K, out_rows, out_cols)
+    for st in (s_cmp, s_out):
+        st.wait_stream(main)
+    orows, ochunks = _row_chunks(out_rows, out_cols * p)
+    tab_i = tables(result, out_rows, out_cols, ochunks)
+    out = torch.empty(out_rows * out_cols * p, dtype=F64, pin_memory=True)
+    ocap = orows * out_cols * p
+    dy = [torch.empty(ocap, dtype=F64, device=dev) for _ in range(2)]
+    free_out = [None, None]
+    for i, (r0, r1) in enumerate(ochunks):
+        b = i % 2
+        n = (r1 - r0) * out_cols * p
+        with torch.cuda.stream(s_cmp):
+            if free_out[b] is not None:
+                s_cmp.wait_event(free_out[b])
+            lift_inverse_peer(tab_i[i], r1 - r0, out_cols, p, levels, mask, base,
+                              out=dy[b][:n].view(r1 - r0, out_cols, p))
+            done = torch.cuda.Event()
+            done.record(s_cmp)
+        with torch.cuda.stream(s_out):
+            s_out.wait_event(done)
+            out[r0 * out_cols * p:r1 * out_cols * p].copy_(dy[b][:n], non_blocking=True)
+            free_out[b] = torch.cuda.Event()
+            free_out[b].record(s_out)
+    s_out.synchronize()
+    main.wait_stream(s_out)
+    result.record_stream(s_cmp)
+    return out.numpy().reshape(out_rows, out_cols, p)
+
+
 # --------------------------------------------------------------- lifting ----
 
 def lift_forward(x: torch.Tensor, levels: int, layout: int = N.LAYOUT_SLICE,

@@ -130,6 +130,9 @@ def test_config4_full_size():
     assert relerr(got, want) < TOL
     # piecewise constant in blocks of 2^(L-1) bands (finer details zeroed)
     assert np.array_equal(got[..., 0::8], got[..., 7::8])
+    # the numpy drop-in call streams the cube through the GPU in row chunks
+    # (engine.host_slices_pipeline): same kernels on the same bytes -> same bits
+    assert np.array_equal(W.sp_w_svd(x, 30, 4), got)
 
 
 def test_determinism():
