@@ -199,6 +199,24 @@ int wt_tube_delta_f64(const double* x, int64_t ntubes, int64_t p, double* out, v
 int wt_tube_transpose_f64(const double* x, int64_t n1, int64_t n2, int64_t p, double* y,
                           void* stream);
 
+/* Orthonormal completion of singular-vector columns: M[b] is rows x r (pitch ld,
+ * stride strideM), its columns in the order of s[b*q + 0 ..] (descending).  Every
+ * column j with s_j <= tau * s_0 (or s_j == 0 / non-finite) is re-orthonormalised
+ * against columns 0..j-1 (classical Gram-Schmidt twice); a column with no
+ * independent part (zero singular value) becomes the first unit vector that has
+ * one.  The short-side factor (A v_j) / s_j of wt_svd_factors_f64 and
+ * tensor.matrix_svd goes through it with tau = 1, the long-side vectors with
+ * tau = 0 -- LAPACK returns orthonormal U and V for rank-deficient slices too
+ * (reference tensor.py:70-77, decomposition.py:75-82). */
+int wt_orthonormal_fixup_f64(double* M, int64_t rows, int64_t r, int64_t ld, int64_t strideM,
+                             const double* s, int64_t q, int64_t batch, double tau, void* stream);
+
+/* inverse_tensor's singularity rule (reference algebra.py:77-83, np.linalg.inv ->
+ * LAPACK dgetrf): Gaussian elimination with partial pivoting, IN PLACE on the batch
+ * of n x n row-major matrices W (pass a copy); info[b] = 1 + the first column with
+ * an exactly zero pivot, else 0. */
+int wt_lu_pivot_check_f64(double* W, int64_t n, int64_t batch, int* info, void* stream);
+
 /* Deterministic per-band reductions used by the quality metrics (PSNR/SSIM,
  * PAPER.md:876-887) and parity norms: x, y are spatial tensors viewed as
  * (n tubes, nslices bands) tube-major; out[k] = sum over tubes of f(x, y) with

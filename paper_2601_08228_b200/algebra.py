@@ -109,11 +109,13 @@ def identity_tensor(n, p, levels):
 def inverse_tensor(a, levels):
     """Blockwise inverse: every wavelet-domain slice is matrix-inverted (algebra.py:62-91).
 
-    Each slice is inverted through the K4 SVD as V diag(1/s) U^T.  Raises
-    SingularSliceError(level, slice_index, cond) -- smooth block first (level 0),
-    then details 1..L, like the reference's loop -- when a slice is singular to
-    working precision (s_min <= n eps s_max) or inverts to non-finite values;
-    ``cond`` is s_max / s_min, the 2-norm condition number np.linalg.cond reports.
+    Singularity follows the reference's np.linalg.inv (LAPACK dgetrf): a slice is
+    singular when Gaussian elimination with partial pivoting meets an exactly
+    zero pivot (wt_lu_pivot_check_f64), or when its inverse is not finite;
+    finite ill-conditioned slices are inverted, as numpy does.  The inverse
+    itself is V diag(1/s) U^T from K4.  Raises SingularSliceError(level,
+    slice_index, cond) -- smooth block first (level 0), then details 1..L, like
+    the reference's loop; ``cond`` is s_max / s_min (np.linalg.cond).
     """
     from .errors import SingularSliceError
 
@@ -125,9 +127,9 @@ def inverse_tensor(a, levels):
     x = E.as_device(a)
     n, _, p = x.shape
     pyr = E.lift_forward(x, levels)
+    singular = E.lu_zero_pivot(pyr) != 0
     sigma, vec, info = E.svd(pyr, n)
-    smin, smax = sigma[:, -1], sigma[:, 0]
-    bad = (~torch.isfinite(sigma).all(dim=1)) | (smin <= n * 2.220446049250313e-16 * smax)
+    bad = singular | ~torch.isfinite(sigma).all(dim=1)
     inv = E.pinv_blocks(pyr, sigma, vec, 0.0)
     bad |= ~torch.isfinite(inv.reshape(p, -1)).all(dim=1)
     if bool(bad.any()):

@@ -53,8 +53,16 @@ extern "C" int wt_svd_factors_f64(const double* T, const double* vec, int64_t nv
   if (st) return st;
   st = wt_scale_cols_f64(shortf, srows, r, r, srows * r, sigma, q, batch, WT_SCALE_DIV, 0.0, stream);
   if (st) return st;
-  // long-side factor = first r long-side vectors, transposed to (ln x r)
-  return wt_copy2d_f64(vec, ln, sV, longf, r, ln * r, ln, r, batch, 1, stream);
+  // (A v_j) / s_j is orthogonal only to ~eps s_max / s_j and zero for s_j = 0:
+  // re-orthonormalise in sigma order (LAPACK's U and V are orthonormal blocks)
+  st = wt_orthonormal_fixup_f64(shortf, srows, r, r, srows * r, sigma, q, batch, 1.0, stream);
+  if (st) return st;
+  // long-side factor = first r long-side vectors, transposed to (ln x r); the
+  // numerically null ones (s_j <= ~1e-12 s_max: the Jacobi test leaves their
+  // directions unconstrained; zero vectors for s_j = 0) are completed likewise
+  st = wt_copy2d_f64(vec, ln, sV, longf, r, ln * r, ln, r, batch, 1, stream);
+  if (st) return st;
+  return wt_orthonormal_fixup_f64(longf, ln, r, r, ln * r, sigma, q, batch, 1e-12, stream);
 }
 
 namespace {

@@ -39,6 +39,7 @@ struct SvdWs {
   int* ticket;      // 1 counter: next visit of the current sweep (persistent sweeps)
   int* bver;        // batch * nblk: version of every column block (bumped when its data changes)
   unsigned long long* pclean;  // batch * nblk * nblk: (ver_I, ver_J) when pair (I, J) last tested clean
+  double* scale;    // batch: power-of-two input scale (svd_absmax_scale)
 };
 
 __host__ __device__ inline int64_t round_up(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
@@ -48,15 +49,44 @@ __device__ __forceinline__ double* mat_ptr(const SvdWs& ws, int64_t b, int64_t n
 }
 
 // ------------------------------------------------------------- copy in -----
+// Per-matrix power-of-two scale that brings max |A_b| into [1, 2): the Gram
+// entries the iteration forms (squares of the data) then stay far from the
+// subnormal / overflow ranges, as LAPACK's dgesdd scales out-of-range inputs.
+// The singular values are scaled back at the end (exact: powers of two).
+__global__ void svd_absmax_scale(const double* __restrict__ A, int64_t lda, int64_t sA, int64_t n1,
+                                 int64_t n2, double* __restrict__ scale) {
+  const int64_t b = blockIdx.x;
+  double mx = 0.0;
+  for (int64_t e = threadIdx.x; e < n1 * n2; e += blockDim.x) {
+    const double v = fabs(A[b * sA + (e / n2) * lda + e % n2]);
+    mx = (v > mx || isnan(v)) ? v : mx;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double t = __shfl_xor_sync(0xffffffffu, mx, o);
+    mx = (t > mx || isnan(t)) ? t : mx;
+  }
+  __shared__ double red[32];
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) mx = (red[w] > mx || isnan(red[w])) ? red[w] : mx;
+    mx = fmax(mx, red[0]);
+    scale[b] = (mx > 0.0 && isfinite(mx)) ? ldexp(1.0, -ilogb(mx)) : 1.0;
+  }
+}
+
 __global__ void svd_copy_in(const double* __restrict__ A, int64_t lda, int64_t sA, bool right,
-                            int64_t m, int64_t n, int64_t mpad, int64_t npad, double* __restrict__ X) {
+                            int64_t m, int64_t n, int64_t mpad, int64_t npad, const double* __restrict__ scale,
+                            double* __restrict__ X) {
   const int64_t b = blockIdx.y;
   const int64_t total = npad * mpad;
+  const double f = scale[b];
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t c = e / mpad, r = e - c * mpad;
     double v = 0.0;
-    if (c < n && r < m) v = right ? A[b * sA + c * lda + r] : A[b * sA + r * lda + c];
+    if (c < n && r < m) v = f * (right ? A[b * sA + c * lda + r] : A[b * sA + r * lda + c]);
     X[b * total + e] = v;
   }
 }
@@ -749,7 +779,7 @@ __global__ void svd_norms_sort(SvdWs ws, int64_t mpad, int64_t npad, int64_t n, 
   }
   bool bad = false;
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    sigma[(int64_t)b * n + i] = key[i];
+    sigma[(int64_t)b * n + i] = key[i] / ws.scale[b];  // (exact: a power of two)
     ws.perm[(int64_t)b * npad + i] = idx[i];
     ws.sig[(int64_t)b * npad + i] = key[i];
     if (!isfinite(key[i])) bad = true;
@@ -804,7 +834,7 @@ __global__ void svd_flip(SvdWs ws, int batch) {
 struct WsLayout {
   int64_t m, n, mpad, npad;
   size_t off_X, off_X2, off_xsel, off_active, off_off, off_conv, off_pending, off_sig, off_perm, off_bdone,
-      off_bver, off_pclean, off_eig, eig_bytes, total;
+      off_bver, off_pclean, off_scale, off_eig, eig_bytes, total;
   bool skip;     // pair-skip bookkeeping (nblk <= kSkipMaxBlocks)
   bool precond;  // Gram-eigenbasis preconditioner (eig.cu) before the sweeps
 };
@@ -843,6 +873,7 @@ WsLayout ws_layout(int64_t n1, int64_t n2, int64_t batch) {
   L.skip = nbk <= kSkipMaxBlocks;
   L.off_bver = take(L.skip ? sizeof(int) * (size_t)(batch * nbk) : 0);
   L.off_pclean = take(L.skip ? sizeof(unsigned long long) * (size_t)(batch * nbk * nbk) : 0);
+  L.off_scale = take(sizeof(double) * (size_t)batch);
   L.precond = precond_enabled(L.n);
   L.eig_bytes = L.precond ? eig_workspace_bytes(L.n, batch) : 0;
   L.off_eig = take(L.eig_bytes);
@@ -920,7 +951,7 @@ int jacobi(const double* A, int64_t lda, int64_t strideA, int64_t n1,
            reinterpret_cast<int*>(base + L.off_conv), reinterpret_cast<int*>(base + L.off_pending),
            reinterpret_cast<double*>(base + L.off_sig), reinterpret_cast<int*>(base + L.off_perm),
            reinterpret_cast<int*>(base + L.off_bdone), reinterpret_cast<int*>(base + L.off_pending) + 2,
-           nullptr, nullptr};
+           nullptr, nullptr, reinterpret_cast<double*>(base + L.off_scale)};
   int pair_skip = 1;
   if (const char* e = getenv("WT_SVD_PAIR_SKIP")) pair_skip = atoi(e);
   if (L.skip && pair_skip) {
@@ -937,7 +968,8 @@ int jacobi(const double* A, int64_t lda, int64_t strideA, int64_t n1,
 
   {
     dim3 grid((unsigned)std::min<int64_t>((L.npad * L.mpad + 255) / 256, 4096), (unsigned)batch);
-    svd_copy_in<<<grid, 256, 0, st>>>(A, lda, strideA, right, L.m, L.n, L.mpad, L.npad, ws.X);
+    svd_absmax_scale<<<(unsigned)batch, 256, 0, st>>>(A, lda, strideA, n1, n2, ws.scale);
+    svd_copy_in<<<grid, 256, 0, st>>>(A, lda, strideA, right, L.m, L.n, L.mpad, L.npad, ws.scale, ws.X);
     if (int e = check_launch("svd_copy_in")) return e;
   }
   WT_CUDA(cudaMemsetAsync(ws.offmax, 0, sizeof(unsigned long long) * batch, st));

@@ -29,9 +29,11 @@ __global__ void scale_cols_kernel(double* __restrict__ M, int64_t rows, int64_t 
       f = sv;
     } else if (mode == WT_SCALE_DIV) {
       f = sv != 0.0 ? 1.0 / sv : 0.0;
-    } else {  // WT_SCALE_PINV2: (1/s)^2 on kept values (decomposition.py:160-161)
+    } else {  // WT_SCALE_PINV2: 1/s applied twice on kept values (decomposition.py:160-161);
+              // (x / s) / s, never x * (1/s)^2: 1/s^2 overflows for s < ~1.5e-154
       const double inv = (sv > tol * smax && sv > 0.0) ? 1.0 / sv : 0.0;
-      f = inv * inv;
+      for (int64_t i = blockIdx.x; i < rows; i += gridDim.x) Mb[i * ld + j] = (Mb[i * ld + j] * inv) * inv;
+      continue;
     }
     for (int64_t i = blockIdx.x; i < rows; i += gridDim.x) Mb[i * ld + j] *= f;
   }
@@ -254,4 +256,182 @@ extern "C" int wt_tube_transpose_f64(const double* x, int64_t n1, int64_t n2, in
   else
     tube_transpose_kernel<false><<<grid, 256, 0, (cudaStream_t)stream>>>(x, n1, n2, p, y);
   return check_launch("wt_tube_transpose_f64");
+}
+
+// ----------------------------------------------------- orthonormal columns --
+// Short-side singular vectors formed as (A v_j) / s_j lose orthogonality like
+// eps s_max / s_j and are zero for s_j = 0 (K6, tensor.matrix_svd).  For every
+// column j with s_j <= tau * s_max (in descending-sigma order) this kernel
+// re-orthonormalises it against columns 0..j-1 by classical Gram-Schmidt done
+// twice, and replaces a column with no independent part left (zero singular
+// value) by the first unit vector e_k that has one -- so the columns are
+// orthonormal to rounding, as LAPACK's are, and U diag(s) V^T is unchanged up
+// to s_j times the correction.  One CTA per matrix; deterministic.
+namespace wt {
+namespace ortho {
+constexpr int OT = 256;
+
+__device__ double ortho_block_sum(double v, double* red) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  double s = 0.0;
+  for (int w = 0; w < OT / 32; ++w) s += red[w];
+  return s;
+}
+
+__global__ void __launch_bounds__(OT) ortho_fixup_kernel(double* __restrict__ M, int64_t rows, int64_t r,
+                                                         int64_t ld, int64_t sM, const double* __restrict__ s,
+                                                         int64_t q, double tau) {
+  extern __shared__ double osm[];  // dots [r], red [8]
+  double* dots = osm;
+  double* red = osm + r;
+  const int64_t b = blockIdx.x;
+  double* Mb = M + b * sM;
+  const double* sb = s + b * q;
+  const double smax = sb[0];
+  int64_t next_e = 0;  // next unit-vector candidate
+  for (int64_t j = 0; j < r; ++j) {
+    const double sj = sb[j];
+    if (sj > tau * smax && sj > 0.0 && isfinite(sj)) continue;  // orthogonal to rounding already
+    bool fresh = false;
+    for (int attempt = 0; attempt <= rows; ++attempt) {
+      if (fresh) {  // candidate e_k
+        for (int64_t i = threadIdx.x; i < rows; i += OT) Mb[i * ld + j] = (i == next_e) ? 1.0 : 0.0;
+        ++next_e;
+        __syncthreads();
+      }
+      double nrm0 = 0.0;
+      for (int64_t i = threadIdx.x; i < rows; i += OT) nrm0 = fma(Mb[i * ld + j], Mb[i * ld + j], nrm0);
+      nrm0 = sqrt(ortho_block_sum(nrm0, red));
+      if (!(nrm0 > 0.0) || !isfinite(nrm0)) {  // nothing to orthogonalise: take a unit vector
+        fresh = true;
+        continue;
+      }
+      for (int pass = 0; pass < 2; ++pass) {
+        // dots with the previous columns (warp per column, lanes over rows)
+        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+        for (int64_t c = warp; c < j; c += OT / 32) {
+          double d = 0.0;
+          for (int64_t i = lane; i < rows; i += 32) d = fma(Mb[i * ld + c], Mb[i * ld + j], d);
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+          if (lane == 0) dots[c] = d;
+        }
+        __syncthreads();
+        for (int64_t i = threadIdx.x; i < rows; i += OT) {
+          double v = Mb[i * ld + j];
+          for (int64_t c = 0; c < j; ++c) v = fma(-dots[c], Mb[i * ld + c], v);
+          Mb[i * ld + j] = v;
+        }
+        __syncthreads();
+      }
+      double nrm = 0.0;
+      for (int64_t i = threadIdx.x; i < rows; i += OT) nrm = fma(Mb[i * ld + j], Mb[i * ld + j], nrm);
+      nrm = sqrt(ortho_block_sum(nrm, red));
+      if (nrm > 0.5 * nrm0) {  // an independent direction survived: normalise it
+        const double inv = 1.0 / nrm;
+        for (int64_t i = threadIdx.x; i < rows; i += OT) Mb[i * ld + j] *= inv;
+        __syncthreads();
+        break;
+      }
+      if (!fresh && nrm > 1e-8 * nrm0) {  // mostly dependent but not empty: keep its independent part
+        const double inv = 1.0 / nrm;
+        for (int64_t i = threadIdx.x; i < rows; i += OT) Mb[i * ld + j] *= inv;
+        __syncthreads();
+        // one more round of orthogonalisation in the next attempt
+        continue;
+      }
+      fresh = true;
+    }
+  }
+}
+}  // namespace ortho
+}  // namespace wt
+
+extern "C" int wt_orthonormal_fixup_f64(double* M, int64_t rows, int64_t r, int64_t ld, int64_t strideM,
+                                        const double* s, int64_t q, int64_t batch, double tau, void* stream) {
+  WT_REQUIRE(rows >= 0 && r >= 0 && r <= q && r <= rows && batch >= 0 && ld >= r, "orthonormal_fixup: bad shape");
+  if (batch == 0 || r == 0) return WT_OK;
+  WT_REQUIRE(batch <= 2147483647, "orthonormal_fixup: batch too large");
+  const size_t smem = sizeof(double) * (size_t)(r + wt::ortho::OT / 32);
+  if (int e = ensure_smem(wt::ortho::ortho_fixup_kernel, smem)) return e;
+  wt::ortho::ortho_fixup_kernel<<<(unsigned)batch, wt::ortho::OT, smem, (cudaStream_t)stream>>>(M, rows, r, ld,
+                                                                                                 strideM, s, q, tau);
+  return check_launch("wt_orthonormal_fixup_f64");
+}
+
+// ------------------------------------------------------------ LU pivots --
+// inverse_tensor's singularity rule (algebra.py:77-83: np.linalg.inv raises
+// LinAlgError when LAPACK dgetrf meets an exactly zero pivot): Gaussian
+// elimination with partial pivoting on a copy of every n x n slice; info[b] =
+// 1 + the first column whose pivot is exactly zero, else 0.  One CTA per slice
+// (off the hot path: only the ring constructor inverse_tensor calls it).
+namespace wt {
+namespace ortho {
+__global__ void __launch_bounds__(OT) lu_pivot_kernel(double* __restrict__ W, int64_t n, int64_t sW,
+                                                      int* __restrict__ info) {
+  __shared__ double sval[OT / 32];
+  __shared__ int64_t sidx[OT / 32];
+  __shared__ int64_t piv;
+  const int64_t b = blockIdx.x;
+  double* A = W + b * sW;
+  int res = 0;
+  for (int64_t k = 0; k < n; ++k) {
+    // pivot: largest |A[i][k]|, i >= k (lowest index on ties, as idamax)
+    double best = -1.0;
+    int64_t bi = n;
+    for (int64_t i = k + threadIdx.x; i < n; i += OT) {
+      const double v = fabs(A[i * n + k]);
+      if (v > best || (v == best && i < bi)) { best = v; bi = i; }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, best, o);
+      const int64_t oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ov > best || (ov == best && oi < bi)) { best = ov; bi = oi; }
+    }
+    if ((threadIdx.x & 31) == 0) { sval[threadIdx.x >> 5] = best; sidx[threadIdx.x >> 5] = bi; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double bv = sval[0];
+      int64_t bx = sidx[0];
+      for (int w = 1; w < OT / 32; ++w)
+        if (sval[w] > bv || (sval[w] == bv && sidx[w] < bx)) { bv = sval[w]; bx = sidx[w]; }
+      piv = bv == 0.0 ? -1 : (bx < n ? bx : k);  // (a NaN column: no pivot order; the inverse check reports it)
+    }
+    __syncthreads();
+    const int64_t p = piv;
+    if (p < 0) { res = (int)k + 1; break; }  // exactly singular (uniform)
+    if (p != k)
+      for (int64_t c = threadIdx.x; c < n; c += OT) {
+        const double t = A[k * n + c];
+        A[k * n + c] = A[p * n + c];
+        A[p * n + c] = t;
+      }
+    __syncthreads();
+    const double inv = 1.0 / A[k * n + k];
+    for (int64_t e = threadIdx.x; e < (n - k - 1) * (n - k); e += OT) {
+      const int64_t i = k + 1 + e / (n - k), c = k + e % (n - k);
+      const double l = A[i * n + k] * inv;
+      if (c > k) A[i * n + c] = fma(-l, A[k * n + c], A[i * n + c]);
+    }
+    __syncthreads();
+    for (int64_t i = k + 1 + threadIdx.x; i < n; i += OT) A[i * n + k] *= inv;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) info[b] = res;
+}
+}  // namespace ortho
+}  // namespace wt
+
+extern "C" int wt_lu_pivot_check_f64(double* W, int64_t n, int64_t batch, int* info, void* stream) {
+  WT_REQUIRE(n >= 0 && batch >= 0, "lu_pivot_check: bad shape");
+  if (batch == 0) return WT_OK;
+  if (n == 0) return cudaMemsetAsync(info, 0, sizeof(int) * (size_t)batch, (cudaStream_t)stream) == cudaSuccess
+                         ? WT_OK : WT_ERR_CUDA;
+  wt::ortho::lu_pivot_kernel<<<(unsigned)batch, wt::ortho::OT, 0, (cudaStream_t)stream>>>(W, n, n * n, info);
+  return check_launch("wt_lu_pivot_check_f64");
 }

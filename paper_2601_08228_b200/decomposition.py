@@ -209,6 +209,11 @@ def pinv_w(a, levels, tol=1e-12):
 def sp_pinv_w(a, levels, tol=1e-12, warn_ratio=0.01):
     """Sparse pseudo-inverse: invert only the coarsest stacks, zero the rest (decomposition.py:180-203)."""
     a, dev = _prep(a)
+    n1, n2, p = a.shape
+    if n1 * n2 * p == 0:  # forward_w of an empty cube has no packed buffer
+        _check_levels(p, levels)
+        z = torch.zeros((n2, n1, p), dtype=torch.float64, device="cuda") if dev else np.zeros((n2, n1, p))
+        return z
     pyr = forward_w(E.as_device(a), levels)
     ratio = fine_detail_energy_ratio(pyr)
     if ratio > warn_ratio:

@@ -73,14 +73,17 @@ def _upload_locked(host: torch.Tensor, device) -> torch.Tensor:
                        for _ in range(_STAGE_SLOTS)]
     out = torch.empty(host.shape, dtype=F64, device=device)
     src, dst = host.reshape(-1), out.view(-1)
-    stream = torch.cuda.current_stream()
-    for i, s0 in enumerate(range(0, src.numel(), _STAGE_ELEMS)):
-        buf, ev = _stage_ring[i % _STAGE_SLOTS]
-        ev.synchronize()                     # the slot's previous DMA has drained
-        m = min(_STAGE_ELEMS, src.numel() - s0)
-        buf[:m].copy_(src[s0:s0 + m])
-        dst[s0:s0 + m].copy_(buf[:m], non_blocking=True)
-        ev.record(stream)
+    # the copies run on (and the slot events record) the DESTINATION device's
+    # stream, so an event tracks its DMA even when `device` is not the current one
+    with torch.cuda.device(out.device):
+        stream = torch.cuda.current_stream()
+        for i, s0 in enumerate(range(0, src.numel(), _STAGE_ELEMS)):
+            buf, ev = _stage_ring[i % _STAGE_SLOTS]
+            ev.synchronize()                     # the slot's previous DMA has drained
+            m = min(_STAGE_ELEMS, src.numel() - s0)
+            buf[:m].copy_(src[s0:s0 + m])
+            dst[s0:s0 + m].copy_(buf[:m], non_blocking=True)
+            ev.record(stream)
     return out
 
 
@@ -400,6 +403,27 @@ def scale_cols(m: torch.Tensor, s: torch.Tensor, mode: int, tol: float = 0.0,
 
 
 # ------------------------------------------------------------------- SVD ----
+
+def orthonormal_fixup(m: torch.Tensor, s: torch.Tensor, tau: float) -> torch.Tensor:
+    """In place: re-orthonormalise the columns j of m[k] (rows x r) with s[k][j] <= tau * s[k][0]
+    (wt_orthonormal_fixup_f64); m's column order is s's (descending)."""
+    lib = N.require_gpu()
+    batch, rows, r = m.shape
+    assert m.stride(2) == 1 and s.is_contiguous()
+    N.check(lib.wt_orthonormal_fixup_f64(_ptr(m), rows, r, m.stride(1), m.stride(0), _ptr(s), s.shape[-1], batch,
+                                         float(tau), _stream()), "wt_orthonormal_fixup_f64")
+    return m
+
+
+def lu_zero_pivot(a: torch.Tensor) -> torch.Tensor:
+    """(batch, n, n) -> int32 (batch,): 1 + first exactly-zero pivot of partial-pivoting LU, else 0."""
+    lib = N.require_gpu()
+    w = a.contiguous().clone()
+    batch, n, _ = w.shape
+    info = torch.empty((batch,), dtype=torch.int32, device=a.device)
+    N.check(lib.wt_lu_pivot_check_f64(_ptr(w), n, batch, _ptr(info), _stream()), "wt_lu_pivot_check_f64")
+    return info
+
 
 class SvdNotConverged(RuntimeError):
     pass

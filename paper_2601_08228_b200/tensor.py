@@ -96,12 +96,15 @@ def matrix_svd(m):
     long_vecs = vec[0].t().contiguous()                       # (len, q)
     if n1 <= n2:   # long side = right vectors; U = A V / s
         other = E.gemm(a[None], vec, trans_b=True)[0]          # (n1, q)
-        other = E.scale_cols(other[None].contiguous(), sigma, 1)[0]
-        u, v = other, long_vecs
     else:
         other = E.gemm(a[None], vec, trans_a=True, trans_b=True)[0]  # (n2, q)
-        other = E.scale_cols(other[None].contiguous(), sigma, 1)[0]
-        u, v = long_vecs, other
+    other = E.scale_cols(other[None].contiguous(), sigma, 1)
+    # orthonormal columns to rounding for every rank, zero matrix included (LAPACK's
+    # U and V are): the short side re-orthonormalised in sigma order, the long side's
+    # numerically null columns (s_j <= 1e-12 s_max) completed
+    other = E.orthonormal_fixup(other, sigma, 1.0)[0]
+    long_vecs = E.orthonormal_fixup(long_vecs[None], sigma, 1e-12)[0]
+    u, v = (other, long_vecs) if n1 <= n2 else (long_vecs, other)
     if dev:
         return u, s, v
     return u.cpu().numpy(), s.cpu().numpy(), v.cpu().numpy()

@@ -139,3 +139,33 @@ def test_transpose_one_pass_exact(shape):
     big = torch.from_numpy(np.random.default_rng(42).standard_normal((shape[0] + 1,) + shape[1:])).cuda()
     view = big[1:]  # contiguous, offset by one row of tubes
     assert torch.equal(W.transpose(view), view.permute(1, 0, 2).contiguous())
+
+
+def test_inverse_tensor_follows_lu_semantics():
+    """inverse_tensor raises only where np.linalg.inv does (an exactly zero LU pivot, or a
+    non-finite inverse): finite ill-conditioned slices are inverted (algebra.py:77-83)."""
+    from paper_2601_08228_b200.errors import SingularSliceError
+
+    rng = np.random.default_rng(11)
+    q = np.linalg.qr(rng.standard_normal((4, 4)))[0]
+    ill = (q * np.array([1.0, 1e-3, 1e-7, 1e-12])) @ q.T          # cond 1e12, no zero pivot
+    # wavelet domain (L = 1): smooth slices [ill, I], detail slices [2 I, ill^T]
+    sm = np.stack([ill, np.eye(4)], axis=2)
+    dt = np.stack([2 * np.eye(4), ill.T.copy()], axis=2)
+    a = O.lift_inverse(sm, [dt])
+    # a slice-constant cube has exactly zero detail slices: both raise, same (level, slice)
+    with pytest.raises(ValueError):
+        O.inverse_tensor(np.stack([ill] * 4, axis=2), 1)
+    with pytest.raises(SingularSliceError):
+        W.inverse_tensor(np.stack([ill] * 4, axis=2), 1)
+    got = W.inverse_tensor(a, 1)                                      # reference inverts: no error
+    want = O.inverse_tensor(a, 1)
+    assert np.all(np.isfinite(got))
+    assert relerr(got, want) < 1e-3                                    # agreement ~ eps * cond
+    # smooth slice exactly singular (dyadic values: the round trip is exact), detail slice I
+    sing = O.lift_inverse(np.array([[1.0, 2.0], [2.0, 4.0]])[:, :, None], [np.eye(2)[:, :, None]])
+    with pytest.raises(SingularSliceError) as e:
+        W.inverse_tensor(sing, 1)
+    with pytest.raises(ValueError) as e2:
+        O.inverse_tensor(sing, 1)
+    assert (e.value.level, e.value.slice_index) == e2.value.args[0]

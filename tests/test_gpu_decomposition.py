@@ -287,3 +287,32 @@ def test_large_slices_against_lapack(n1, n2):
     E.raise_if_failed(info)
     want = np.linalg.svd(a[0], compute_uv=False)[None]
     assert sigma_err(sigma.cpu().numpy(), want) < TOL
+
+
+def test_sweep_limit_raises_linalgerror_like_dgesdd():
+    """K4 info == 2 (no convergence within max_sweeps) raises LinAlgError('SVD did not
+    converge') like np.linalg.svd when dgesdd fails (decomposition.py:66)."""
+    a = torch.from_numpy(np.random.default_rng(0).standard_normal((2, 64, 64))).cuda()
+    sigma, vec, info = E.svd(a, 0, max_sweeps=1)
+    assert int(info.max()) == 2
+    with pytest.raises(np.linalg.LinAlgError, match="SVD did not converge"):
+        E.raise_if_failed(info)
+
+
+def test_pinv_tiny_and_huge_scales():
+    """pinv of 1e-160 * I and 1e+150 * I: 1/s is applied twice on the operands, never
+    squared (1/s^2 overflows below ~1.5e-154 and underflows above ~1e154)."""
+    ident = W.identity_tensor(4, 8, 2)
+    for scale in (1e-160, 1e150):
+        a = ident * scale
+        x = W.pinv_w(a, 2)
+        assert np.all(np.isfinite(x))
+        assert relerr(x * scale, ident) < 1e-12
+        y = W.inverse_tensor(a, 2)
+        assert relerr(y * scale, ident) < 1e-12
+
+
+def test_sp_pinv_w_empty():
+    for shape in [(0, 3, 4), (3, 0, 4)]:
+        out = W.sp_pinv_w(np.zeros(shape), 1)
+        assert out.shape == (shape[1], shape[0], shape[2]) and not out.any()

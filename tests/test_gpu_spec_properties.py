@@ -108,13 +108,77 @@ def test_ac5_eckart_young_and_invariant_sweep():
         # U * S * V^T == recon
         usv = W.w_product(W.w_product(f.U, f.S, L), W.transpose(f.V), L)
         assert relerr(usv, rec) < 1e-10
-        # wavelet-domain U blocks orthonormal where sigma > 0
-        pu = E.lift_forward(torch.from_numpy(np.ascontiguousarray(f.U)).cuda(), L).cpu().numpy()
-        sig = np.concatenate([s for _, s in f.sigma_table])
-        for k2 in range(p):
-            keep = sig[k2, :r] > 1e-12 * max(sig[k2, 0], 1e-300)
-            u = pu[k2][:, keep]
-            assert np.abs(u.T @ u - np.eye(u.shape[1])).max() < 1e-10
+        # wavelet-domain U and V blocks orthonormal, every column --
+        # zero / rank-deficient slices included (K6 completes them like LAPACK)
+        for fac in (f.U, f.V):
+            pu = E.lift_forward(torch.from_numpy(np.ascontiguousarray(fac)).cuda(), L).cpu().numpy()
+            for k2 in range(p):
+                u = pu[k2]
+                assert np.abs(u.T @ u - np.eye(u.shape[1])).max() < 1e-10
     # sp-w-svd == w-svd at L = 1
     a = rng.standard_normal((9, 7, 8))
     assert relerr(W.sp_w_svd(a, 3, 1), W.w_svd(a, 3, 1)[1]) < 1e-14
+
+
+def graded_cube(n1, n2, p, lo_exp, seed):
+    """(n1, n2, p) cube whose every frontal slice has singular values logspace(0, lo_exp)."""
+    rng = np.random.default_rng(seed)
+    q = min(n1, n2)
+    out = np.empty((n1, n2, p))
+    for k in range(p):
+        u = np.linalg.qr(rng.standard_normal((n1, q)))[0]
+        v = np.linalg.qr(rng.standard_normal((n2, q)))[0]
+        out[:, :, k] = (u * np.logspace(0, lo_exp, q)) @ v.T
+    return out
+
+
+@pytest.mark.parametrize("shape", [(48, 40, 8), (40, 48, 8), (160, 144, 4)])
+def test_graded_spectrum_full_rank_w_svd(shape):
+    """sigma down to 1e-10 sigma_1, full rank: singular values and the
+    reconstruction vs the oracle, U / V wavelet blocks orthonormal to 1e-10 (K6's
+    short-side factor (A v) / s is re-orthonormalised), U * S * V^T == recon."""
+    n1, n2, p = shape
+    L = 2
+    r = min(n1, n2)
+    a = graded_cube(n1, n2, p, -10.0, seed=n1)
+    f, rec = W.w_svd(a, r, L)
+    want = O.w_svd(a, r, L)
+    assert relerr(rec, want["recon"]) < 1e-8
+    for (_, s1), (_, s2) in zip(f.sigma_table, want["sigma_table"]):
+        assert np.max(np.abs(s1 - s2) / s2[:, :1]) < 1e-8
+    for fac in (f.U, f.V):
+        pu = E.lift_forward(torch.from_numpy(np.ascontiguousarray(fac)).cuda(), L).cpu().numpy()
+        for k in range(p):
+            assert np.abs(pu[k].T @ pu[k] - np.eye(r)).max() < 1e-10
+    usv = W.w_product(W.w_product(f.U, f.S, L), W.transpose(f.V), L)
+    assert relerr(usv, rec) < 1e-10
+
+
+def test_graded_spectrum_pinv_via_factors():
+    """pinv_w_via_factors on sigma down to 1e-10 sigma_1 (full rank): equals pinv_w and the
+    oracle to the conditioning (cond 1e10 -> agreement ~eps * cond), and the Penrose
+    identities A A+ A = A, A+ A A+ = A+ hold."""
+    a = graded_cube(32, 32, 8, -10.0, seed=3)
+    L = 2
+    x1 = W.pinv_w_via_factors(a, L)
+    x2 = W.pinv_w(a, L)
+    ref = O.pinv_w(a, L)
+    assert relerr(x1, ref) < 1e-4 and relerr(x2, ref) < 1e-4
+    assert relerr(x1, x2) < 1e-4
+    aa = W.w_product(W.w_product(a, x2, L), a, L)
+    assert relerr(aa, a) < 1e-6  # eps * cond(1e10)
+
+
+def test_matrix_svd_orthonormal_for_zero_and_rank_one():
+    """tensor.matrix_svd (SPEC: U^T U = I to 1e-12, zero matrix included)."""
+    rng = np.random.default_rng(5)
+    cases = [np.zeros((3, 3)), np.zeros((5, 2)), np.outer(rng.standard_normal(7), rng.standard_normal(4)),
+             np.outer(rng.standard_normal(3), rng.standard_normal(6)), rng.standard_normal((6, 6))]
+    for m in cases:
+        u, s, v = W.matrix_svd(m)
+        q = min(m.shape)
+        assert u.shape == (m.shape[0], q) and v.shape == (m.shape[1], q)
+        assert np.abs(u.T @ u - np.eye(q)).max() < 1e-12
+        assert np.abs(v.T @ v - np.eye(q)).max() < 1e-12
+        assert np.abs((u * s) @ v.T - m).max() <= 1e-12 * max(1.0, np.abs(m).max())
+        np.testing.assert_allclose(s, np.linalg.svd(m, compute_uv=False), atol=1e-12 * max(1.0, s.max()))
