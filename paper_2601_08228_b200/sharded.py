@@ -77,7 +77,18 @@ class CudaOps:
         return E.gemm(a, b)
 
 
+def _host_staged(t, group) -> bool:
+    """CUDA tensors over a gloo group (the multi-process tests on one GPU) go through
+    host buffers; NCCL exchanges device memory directly."""
+    return t.is_cuda and dist.get_backend(group) == "gloo"
+
+
 def _a2a(out, inp, out_splits, in_splits, group):
+    if _host_staged(out, group):
+        o = torch.empty(out.shape, dtype=out.dtype)
+        dist.all_to_all_single(o, inp.cpu(), out_splits, in_splits, group=group)
+        out.copy_(o)
+        return
     dist.all_to_all_single(out, inp, out_splits, in_splits, group=group)
 
 
@@ -199,7 +210,12 @@ def gather_rows(ops, local, rows, group):
     if local.shape[0]:
         pad[:local.shape[0]].copy_(local)
     allb = ops.empty((G * R,) + tail)
-    dist.all_gather_into_tensor(allb, pad, group=group)
+    if _host_staged(allb, group):
+        h = torch.empty(allb.shape, dtype=allb.dtype)
+        dist.all_gather_into_tensor(h, pad.cpu(), group=group)
+        allb.copy_(h)
+    else:
+        dist.all_gather_into_tensor(allb, pad, group=group)
     full = ops.empty((sum(rows),) + tail)
     r0 = 0
     for g in range(G):
