@@ -211,6 +211,10 @@ int wt_tube_transpose_f64(const double* x, int64_t n1, int64_t n2, int64_t p, do
 int wt_orthonormal_fixup_f64(double* M, int64_t rows, int64_t r, int64_t ld, int64_t strideM,
                              const double* s, int64_t q, int64_t batch, double tau, void* stream);
 
+/* S[b] (r x r, row-major) = diag(s[b*q + 0 .. r-1]) for b < batch: the S factor
+ * blocks of w_svd (reference decomposition.py:75-82). */
+int wt_diag_blocks_f64(const double* s, int64_t q, int64_t r, int64_t batch, double* S, void* stream);
+
 /* inverse_tensor's singularity rule (reference algebra.py:77-83, np.linalg.inv ->
  * LAPACK dgetrf): Gaussian elimination with partial pivoting, IN PLACE on the batch
  * of n x n row-major matrices W (pass a copy); info[b] = 1 + the first column with
@@ -226,6 +230,21 @@ int wt_lu_pivot_check_f64(double* W, int64_t n, int64_t batch, int* info, void* 
 size_t wt_slice_reduce_scratch(int64_t n, int64_t nslices);
 int wt_slice_reduce_f64(const double* x, const double* y, int64_t n, int64_t nslices,
                         int mode, double* out, void* stream);
+
+/* Test / diagnostic switches (process-wide; the defaults are the production
+ * choices).  Returns the previous value, or WT_ERR_INVALID for an unknown option.
+ * Used by the test suite to force scheduling variants whose results must not
+ * change (or change only at rounding level), and by the tools/ diagnostics. */
+#define WT_OPT_SVD_SPLIT 0        /* 0: host rule; S = 1, 2, 4, 8: forced cluster-split sweeps */
+#define WT_OPT_SVD_CTAS_PER_SM 1  /* 0: host rule; k: at most k resident sweep CTAs per SM */
+#define WT_OPT_SVD_PAIR_SKIP 2    /* 1: skip pair visits certified clean (default) */
+#define WT_OPT_SVD_PERSIST 3      /* 1: one persistent launch per sweep (default); 0: one per round */
+#define WT_OPT_SVD_PRECOND 4      /* 1: Gram-eigenbasis preconditioner for n >= 128 (default) */
+#define WT_OPT_SVD_PROFILE 5      /* 1: K4 per-visit phase cycle counters on stderr */
+#define WT_OPT_SVD_TRACE 6        /* 1: K4 per-sweep convergence trace on stderr */
+#define WT_OPT_EIG_PROFILE 7      /* 1: preconditioner phase times on stderr */
+#define WT_OPT_COUNT 8
+int wt_set_option(int option, int value);
 
 /* Sweeps used by the last wt_svd_jacobi_f64 call on the calling thread, and
  * the FP64 flops its Jacobi iteration executed (Gram + rotation tiles of every

@@ -43,6 +43,7 @@ SIGNATURES = {
                                          c_double_p, i64, ctypes.c_void_p, ctypes.c_double,
                                          ctypes.c_int, ctypes.c_void_p, ctypes.c_size_t,
                                          ctypes.c_void_p]),
+    "wt_set_option": (ctypes.c_int, [ctypes.c_int, ctypes.c_int]),
     "wt_svd_last_sweeps": (ctypes.c_int, []),
     "wt_svd_last_fallbacks": (ctypes.c_int, []),
     "wt_svd_last_jacobi_flops": (ctypes.c_double, []),
@@ -65,6 +66,7 @@ SIGNATURES = {
     "wt_orthonormal_fixup_f64": (ctypes.c_int, [c_double_p, i64, i64, i64, i64, c_double_p, i64, i64,
                                                 ctypes.c_double, ctypes.c_void_p]),
     "wt_lu_pivot_check_f64": (ctypes.c_int, [c_double_p, i64, i64, ctypes.c_void_p, ctypes.c_void_p]),
+    "wt_diag_blocks_f64": (ctypes.c_int, [c_double_p, i64, i64, i64, c_double_p, ctypes.c_void_p]),
     "wt_slice_reduce_scratch": (ctypes.c_size_t, [i64, i64]),
     "wt_slice_reduce_f64": (ctypes.c_int, [c_double_p, c_double_p, i64, i64, ctypes.c_int,
                                            c_double_p, ctypes.c_void_p]),

@@ -909,8 +909,8 @@ int eig_precondition(const double* Xt, double* Yt, int64_t m, int64_t n, int64_t
   int* glim = reinterpret_cast<int*>(base + L.glim);
   const int64_t nn = n * n;
   const int ni = (int)n;
-  // WT_EIG_PROFILE=1: per-phase device times on stderr (diagnostics)
-  static const bool prof = getenv("WT_EIG_PROFILE") != nullptr;
+  // WT_OPT_EIG_PROFILE: per-phase device times on stderr (diagnostics)
+  const bool prof = option(WT_OPT_EIG_PROFILE) != 0;
   cudaEvent_t ev[10] = {};
   int nev = 0;
   auto mark = [&]() {

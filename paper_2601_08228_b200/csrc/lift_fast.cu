@@ -561,111 +561,12 @@ __global__ void __launch_bounds__(kT) inv_persistent(const double* __restrict__ 
   if (!TMA) cp_async_wait<0>();
 }
 
-// Shallow inverse (L = W <= 3, one stage), TMA input: ONE 16 x 256 tile buffer;
-// every thread pulls its items' smooth + detail values into registers, one CTA
-// barrier frees the buffer, the next tile's boxes are issued, and the lift and
-// the tube stores run while they are in flight.
-template <int W>
-__global__ void __launch_bounds__(kT) inv_shallow(const double* __restrict__ pyr,
-                                                  double* __restrict__ y, FGeom g,
-                                                  const __grid_constant__ TmaMaps maps) {
-  constexpr int TQ = 16, CT = 256, V = 1 << W, NV = CT >> W, MAXI = TQ * NV / kT;
-  extern __shared__ __align__(128) double sm[];
-  __shared__ __align__(8) uint64_t bar;
-  if (threadIdx.x == 0) {
-    mbar_init(&bar, 1);
-    fence_mbar_init();
-  }
-  __syncthreads();
-  auto issue = [&](uint32_t t) {
-    if (threadIdx.x != 0) return;
-    int64_t q0, t0;
-    int tq;
-    tile_at<TQ>(g, t, q0, tq, t0);
-    uint32_t bytes = 0;
-    for (int j = 1; j <= W + 1; ++j)
-      if ((g.mask >> (j > W ? 0 : j)) & 1) bytes += (CT >> min(j, W)) * TQ * 8;
-    mbar_expect_tx(&bar, bytes);
-    for (int j = 1; j <= W + 1; ++j) {
-      const bool smooth = j > W;
-      if (!((g.mask >> (smooth ? 0 : j)) & 1)) continue;
-      const int row0 = smooth ? CT - (CT >> W) : drow(CT, j);
-      const int64_t s0 = smooth ? soff(g.p, W) + (t0 >> W) : doff(g.p, j) + (t0 >> j);
-      tma_load_2d(sm + row0 * TQ, &maps.m[smooth ? W : j], (int)q0, (int)(s0 - g.slice_base), &bar);
-    }
-  };
-  const bool have_s = g.mask & 1;
-  uint32_t t = blockIdx.x;
-  if (t < g.ntiles) issue(t);
-  for (int it = 0; t < g.ntiles; ++it, t += gridDim.x) {
-    mbar_wait(&bar, it & 1);
-    int64_t q0, t0;
-    int tq;
-    tile_at<TQ>(g, t, q0, tq, t0);
-    const double* vs = sm;
-    double v[MAXI][V], dd[MAXI][V];  // dd: level W (1 value), W-1 (2), ..., 1 (V/2)
-#pragma unroll
-    for (int k = 0; k < MAXI; ++k) {
-      const int e = threadIdx.x + k * kT;
-      const int r = e & (TQ - 1), c = e / TQ;
-      v[k][0] = have_s ? vs[(CT - NV + c) * TQ + r] : 0.0;
-      int o = 0;
-#pragma unroll
-      for (int w = 0; w < W; ++w) {
-        const int lev = W - w, n = 1 << w;
-        const bool have_d = (g.mask >> lev) & 1;
-#pragma unroll
-        for (int i = 0; i < n; ++i, ++o)
-          dd[k][o] = have_d ? vs[(drow(CT, lev) + c * n + i) * TQ + r] : 0.0;
-      }
-    }
-    // generic-proxy reads of the buffer are ordered before the TMA (async-proxy)
-    // refill only by a proxy fence: without it the refill raced the reads
-    fence_proxy_async_smem();
-    __syncthreads();                                   // the tile buffer is free
-    if (t + gridDim.x < g.ntiles) issue(t + gridDim.x);
-#pragma unroll
-    for (int k = 0; k < MAXI; ++k) {
-      const int e = threadIdx.x + k * kT;
-      const int r = e & (TQ - 1), c = e / TQ;
-      int o = 0;
-#pragma unroll
-      for (int w = 0; w < W; ++w) {
-        const int n = 1 << w;
-        // level W - w: n smooth values -> 2n (in place, high to low)
-#pragma unroll
-        for (int i = (V >> 1) - 1; i >= 0; --i) {
-          if (i < n) {
-            const double d = dd[k][o + i];
-            const double x1 = __dsub_rn(v[k][i], __dmul_rn(d, 0.5));
-            v[k][2 * i] = __dadd_rn(d, x1);
-            v[k][2 * i + 1] = x1;
-          }
-        }
-        o += n;
-      }
-      if (r < tq) {
-        double* out = y + (q0 + r) * g.p + t0 + (int64_t)c * V;
-#pragma unroll
-        for (int i = 0; i < V; i += 2)
-          *reinterpret_cast<double2*>(out + i) = make_double2(v[k][i], v[k][i + 1]);
-      }
-    }
-  }
-}
-
 // Tile height cap.  Forward: taller tiles write longer runs per packed slice
 // row (TQ * 8 bytes); measured at config 2 (tools/lift_tq_probe.py, round 1,
 // GB/s): L=1-3 best at 32 (+2%), L=4-6 at 64 (+7..14%), L=7 at 32 (+14%), L=8
-// needs CT = 256 so stays at 16 (L >= 6 take fwd_persistent1 by default).  Inverse: 16 (taller tiles cost 30%: the
+// needs CT = 256 so stays at 16 (L >= 6 take fwd_persistent1).  Inverse: 16 (taller tiles cost 30%: the
 // tube-major final stores scatter over more tubes per warp).
-// WT_LIFT_TQ_MAX overrides both (diagnostics).
 int tq_max(bool fwd, int L) {
-  static const int env = [] {
-    const char* e = getenv("WT_LIFT_TQ_MAX");
-    return e ? atoi(e) : 0;
-  }();
-  if (env > 0) return env;
   if (!fwd) return 16;
   return (L >= 4 && L <= 6) ? 64 : 32;
 }
@@ -750,19 +651,11 @@ int lift_fwd_fast(const double* x, int64_t ntubes, int64_t p, int L, double* out
   int TQ = 0;
   if (!plan(g, TQ, true)) return WT_ERR_UNSUPPORTED;
   const size_t smem = ((size_t)2 * TQ * g.LDT + (size_t)TQ * (g.LDA0 + g.LDA1)) * sizeof(double);
-  static const int deep1 = [] {
-    const char* e = getenv("WT_LIFT_DEEP1");
-    return e ? atoi(e) : 1;
-  }();
   // L = 6..8: single-buffered 32-tube tiles of 256 bands (fwd_persistent1);
   // measured at config 2 (tools/lift_tq_probe.py, TB/s): L=6 5.58 -> 5.96,
   // L=7 5.83 -> 5.89, L=8 5.09 -> 5.89; L=4, 5 tie with the TQ=64 tiles.
   const int64_t unit = (int64_t)1 << g.L;
-  static const int shallow = [] {
-    const char* e = getenv("WT_LIFT_SHALLOW");
-    return e ? atoi(e) : 1;
-  }();
-  if (shallow && g.L <= 3 && g.p % 256 == 0) {
+  if (g.L <= 3 && g.p % 256 == 0) {
     FGeom g1 = g;
     g1.CT = 256;
     g1.LDT = 258;
@@ -773,7 +666,7 @@ int lift_fwd_fast(const double* x, int64_t ntubes, int64_t p, int L, double* out
     if (g.L == 2) return launch(fwd_shallow<2>, smem1, g1.ntiles, st, x, out, g1, "wt_lift_fwd_f64");
     return launch(fwd_shallow<3>, smem1, g1.ntiles, st, x, out, g1, "wt_lift_fwd_f64");
   }
-  if (deep1 && unit >= (deep1 >= 2 ? 16 : 64) && unit <= 256 && g.p % 256 == 0) {
+  if (unit >= 64 && unit <= 256 && g.p % 256 == 0) {
     FGeom g1 = g;
     constexpr int TQ1 = 32;
     {
@@ -807,36 +700,14 @@ int lift_inv_fast(const double* pyr, int64_t ntubes, int64_t p, int L, double* y
   // measured at config 2 (tools/lift_tq_probe.py, 3 alternating runs): L = 7
   // +2% over the staged inverse, L = 8 even, L = 4..6 -2..7% (the chains'
   // redundant loads outweigh the saved barriers while the top levels are short)
-  static const int inv_path = [] {
-    const char* e = getenv("WT_LIFT_INV_PATH");
-    return e ? atoi(e) : 7;
-  }();
-  g.inv_path = inv_path;
+  g.inv_path = 7;
   int TQ = 0;
   if (!plan(g, TQ, false)) return WT_ERR_UNSUPPORTED;
   const size_t smem = ((size_t)2 * g.CT * TQ + (size_t)2 * TQ * g.LDA0) * sizeof(double);
   if (smem > 200 * 1024) return WT_ERR_UNSUPPORTED;
   TmaMaps maps{};  // host copy, passed by value as a __grid_constant__ parameter
-  // single-buffered shallow inverse: correct (with its proxy fence) but slower
-  // than the double-buffered kernel (L=1-3: -7..12%), kept for experiments
-  static const int inv_shallow_on = [] {
-    const char* e = getenv("WT_LIFT_INV_SHALLOW");
-    return e ? atoi(e) : 0;
-  }();
-  if (inv_shallow_on && !tab && L <= 3 && p % 256 == 0 && !getenv("WT_LIFT_NO_TMA")) {
-    FGeom g1 = g;
-    g1.CT = 256;
-    g1.nqt = (uint32_t)((ntubes + 15) / 16);
-    g1.ntiles = (uint32_t)(g1.nqt * (p / 256));
-    if (make_maps(maps, pyr, g1, 16)) {
-      const size_t smem1 = (size_t)16 * 256 * sizeof(double);
-      if (L == 1) return launch(inv_shallow<1>, smem1, g1.ntiles, st, pyr, y, g1, "wt_lift_inv_f64", maps);
-      if (L == 2) return launch(inv_shallow<2>, smem1, g1.ntiles, st, pyr, y, g1, "wt_lift_inv_f64", maps);
-      return launch(inv_shallow<3>, smem1, g1.ntiles, st, pyr, y, g1, "wt_lift_inv_f64", maps);
-    }
-  }
   // TMA boxes: 16 tubes (128-byte rows) x <= 256 slices, 16-byte-multiple stride
-  if (!tab && TQ >= 16 && (g.CT >> 1) <= 256 && !getenv("WT_LIFT_NO_TMA") &&
+  if (!tab && TQ >= 16 && (g.CT >> 1) <= 256 &&
       make_maps(maps, pyr, g, TQ)) {
     if (TQ == 64)
       return launch(inv_persistent<64, true>, smem, g.ntiles, st, pyr, y, g, "wt_lift_inv_f64", maps);

@@ -619,7 +619,7 @@ __device__ __forceinline__ void st_release(int* p, int v) {
 // takes tickets; its leader CTA schedules (ticket, dependency wait, converged /
 // clean-pair skip) and the others read the item from the leader's shared memory.
 template <int SPLIT>
-__global__ void __launch_bounds__(kThreads, kMinBlocks) svd_sweep_kernel(SvdWs ws, int64_t mpad, int64_t npad,
+__global__ void __launch_bounds__(kThreads, SPLIT > 1 ? 2 : kMinBlocks) svd_sweep_kernel(SvdWs ws, int64_t mpad, int64_t npad,
                                                                 int n_active, double tol, int inner_sweeps,
                                                                 int cross) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -844,11 +844,7 @@ struct WsLayout {
 // config 3-5 slices.  Below it plain Jacobi is cheap enough.
 constexpr int64_t kPrecondMinN = 128;
 inline bool precond_enabled(int64_t n) {
-  static const int env = [] {
-    const char* e = getenv("WT_SVD_PRECOND");
-    return e ? atoi(e) : 1;
-  }();
-  return env != 0 && n >= kPrecondMinN && n <= 2048;
+  return option(WT_OPT_SVD_PRECOND) != 0 && n >= kPrecondMinN && n <= 2048;
 }
 
 WsLayout ws_layout(int64_t n1, int64_t n2, int64_t batch) {
@@ -952,8 +948,7 @@ int jacobi(const double* A, int64_t lda, int64_t strideA, int64_t n1,
            reinterpret_cast<double*>(base + L.off_sig), reinterpret_cast<int*>(base + L.off_perm),
            reinterpret_cast<int*>(base + L.off_bdone), reinterpret_cast<int*>(base + L.off_pending) + 2,
            nullptr, nullptr, reinterpret_cast<double*>(base + L.off_scale)};
-  int pair_skip = 1;
-  if (const char* e = getenv("WT_SVD_PAIR_SKIP")) pair_skip = atoi(e);
+  const int pair_skip = option(WT_OPT_SVD_PAIR_SKIP);
   if (L.skip && pair_skip) {
     ws.bver = reinterpret_cast<int*>(base + L.off_bver);
     ws.pclean = reinterpret_cast<unsigned long long*>(base + L.off_pclean);
@@ -994,11 +989,9 @@ int jacobi(const double* A, int64_t lda, int64_t strideA, int64_t n1,
   if (int e = ensure_smem(svd_pair_kernel, sizeof(PairSmem))) return e;
   // Persistent sweeps (one launch per sweep, visits scheduled by block
   // dependencies) unless WT_SVD_PERSIST=0 (one launch per round).
-  int persist = 1;
-  if (const char* e = getenv("WT_SVD_PERSIST")) persist = atoi(e);
+  const int persist = option(WT_OPT_SVD_PERSIST);
   int sweep_ctas = 0;
-  int split_env = 0;
-  if (const char* e = getenv("WT_SVD_SPLIT")) split_env = atoi(e);
+  const int split_env = option(WT_OPT_SVD_SPLIT);
   int n_sms = kNumSMs;
   if (persist) {
     int dev = 0, per_sm = 0;
@@ -1010,14 +1003,14 @@ int jacobi(const double* A, int64_t lda, int64_t strideA, int64_t n1,
     // query, or the first call in a process sees 0 resident CTAs)
     if (int e = ensure_smem(svd_sweep_kernel<1>, sizeof(PairSmem))) return e;
     WT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, svd_sweep_kernel<1>, kThreads, sizeof(PairSmem)));
-    if (const char* e = getenv("WT_SVD_CTAS_PER_SM")) per_sm = std::min(per_sm, std::max(1, atoi(e)));
+    if (const int cap = option(WT_OPT_SVD_CTAS_PER_SM)) per_sm = std::min(per_sm, std::max(1, cap));
     sweep_ctas = sms * std::max(per_sm, 1);
   }
   g_last_sweeps = 0;
   g_last_rotations = 0;
   int dbg_prev = 0;
   static thread_local unsigned long long* d_prof = nullptr;  // WT_SVD_PROFILE diagnostics
-  const bool profile = getenv("WT_SVD_PROFILE") != nullptr;
+  const bool profile = option(WT_OPT_SVD_PROFILE) != 0;
   if (profile) {
     if (!d_prof) WT_CUDA(cudaMalloc(&d_prof, 8 * sizeof(unsigned long long)));
     WT_CUDA(cudaMemsetAsync(d_prof, 0, 8 * sizeof(unsigned long long), st));
@@ -1029,8 +1022,7 @@ int jacobi(const double* A, int64_t lda, int64_t strideA, int64_t n1,
   // One inner Jacobi sweep per pair visit: measured on the config-3/4 slices it
   // needs the same number of outer sweeps as full diagonalisation (13 / 18) at
   // 2.4x / 1.6x less time (tools/svd_probe.py, round 1).
-  int inner = 1;
-  if (const char* e = getenv("WT_SVD_INNER_SWEEPS")) inner = std::max(1, std::min(kMaxInnerSweeps, atoi(e)));
+  constexpr int inner = 1;
   bool hit_max = true;
   // Full rounds visit every block once with the full 32-column inner sweep
   // (all within-block pairs); the other rounds rotate (and test) only the
@@ -1044,16 +1036,13 @@ int jacobi(const double* A, int64_t lda, int64_t strideA, int64_t n1,
   // 20.5 / 14 -> 18.6 / 12 (F = 2), config 4 158 / 16 -> 143 / 15 (F = 4),
   // the config-5 operators' pseudo-inverse pair 28.1 -> 24.2 (F = 4),
   // 4 x 1024^2 33.7 / 15 -> 31.2 / 13.
-  int cross = nb >= 16 ? std::max(2, std::min(4, nb / 8)) : 0;
-  if (const char* e = getenv("WT_SVD_CROSS")) cross = atoi(e);
+  const int cross = nb >= 16 ? std::max(2, std::min(4, nb / 8)) : 0;
   // Reorder the columns by descending norm before every sweep: measured on the
   // config-3/4 slices 13 -> 12 and 17 -> 16 sweeps, -10% time (round 1).
-  int sort_mode = 2;
+  constexpr int sort_mode = 2;
   // From sweep 1 on, sort by the column norms the visits leave behind (no
-  // pass over the matrices); WT_SVD_VISIT_NORMS=0 recomputes them.
-  int visit_norms = 1;
-  if (const char* e = getenv("WT_SVD_VISIT_NORMS")) visit_norms = atoi(e);
-  if (const char* e = getenv("WT_SVD_SORT")) sort_mode = atoi(e);
+  // pass over the matrices).
+  constexpr int visit_norms = 1;
   const size_t sort_smem = (size_t)npow2 * (sizeof(double) + sizeof(int));
   if (int e = ensure_smem(svd_norms_sort, 8192 * (sizeof(double) + sizeof(int)))) return e;
   for (int sweep = 0; sweep < max_sweeps; ++sweep) {
@@ -1111,7 +1100,7 @@ int jacobi(const double* A, int64_t lda, int64_t strideA, int64_t n1,
       }
     }
     if (int e = check_launch("svd_pair_kernel")) return e;
-    if (getenv("WT_SVD_DEBUG")) {  // per-sweep convergence trace (diagnostics only)
+    if (option(WT_OPT_SVD_TRACE)) {  // per-sweep convergence trace (diagnostics only)
       std::vector<unsigned long long> h(batch);
       WT_CUDA(cudaMemcpyAsync(h.data(), ws.offmax, sizeof(unsigned long long) * batch,
                               cudaMemcpyDeviceToHost, st));

@@ -435,3 +435,28 @@ extern "C" int wt_lu_pivot_check_f64(double* W, int64_t n, int64_t batch, int* i
   wt::ortho::lu_pivot_kernel<<<(unsigned)batch, wt::ortho::OT, 0, (cudaStream_t)stream>>>(W, n, n * n, info);
   return check_launch("wt_lu_pivot_check_f64");
 }
+
+// ------------------------------------------------------- diagonal blocks --
+// S[b] (r x r row-major) = diag(s[b*q + 0 .. r-1]): the S factor blocks of
+// w_svd (decomposition.py:75-82, _factor_blocks' np.diag per slice).
+namespace wt {
+namespace ortho {
+__global__ void diag_blocks_kernel(const double* __restrict__ s, int64_t q, int64_t r, int64_t batch,
+                                   double* __restrict__ S) {
+  const int64_t total = batch * r * r;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = e / (r * r), rc = e - b * r * r, i = rc / r, j = rc - i * r;
+    S[e] = i == j ? s[b * q + i] : 0.0;
+  }
+}
+}  // namespace ortho
+}  // namespace wt
+
+extern "C" int wt_diag_blocks_f64(const double* s, int64_t q, int64_t r, int64_t batch, double* S, void* stream) {
+  WT_REQUIRE(r >= 0 && r <= q && batch >= 0, "diag_blocks: bad shape");
+  const int64_t total = batch * r * r;
+  if (total == 0) return WT_OK;
+  const unsigned grid = (unsigned)std::min<int64_t>((total + 255) / 256, 4096);
+  wt::ortho::diag_blocks_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(s, q, r, batch, S);
+  return check_launch("wt_diag_blocks_f64");
+}

@@ -14,6 +14,7 @@ namespace wt {
 // ---------------------------------------------------------------- status ----
 void set_error(const char* fmt, ...);
 int check_launch(const char* what);
+int option(int which);  // wt_set_option's table (production defaults unless a test changed them)
 
 // K3 with per-matrix limits (device arrays, nullable): the inner dimension of
 // matrix b is min(K, klim[b]) (operands beyond it read as zeros) and output

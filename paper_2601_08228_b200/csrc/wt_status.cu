@@ -2,6 +2,7 @@
 #include <stdarg.h>
 #include <stdio.h>
 
+#include <atomic>
 #include <map>
 #include <mutex>
 #include <utility>
@@ -18,6 +19,21 @@ void set_error(const char* fmt, ...) {
   vsnprintf(g_last_error, sizeof(g_last_error), fmt, ap);
   va_end(ap);
 }
+
+// Test / diagnostic switches (wt_set_option): the production defaults unless a
+// test or a diagnostics tool changes them.
+static std::atomic<int> g_options[WT_OPT_COUNT] = {
+    {0},  // WT_OPT_SVD_SPLIT: 0 = host rule, else forced cluster split S
+    {0},  // WT_OPT_SVD_CTAS_PER_SM: 0 = host rule, else cap on resident sweep CTAs per SM
+    {1},  // WT_OPT_SVD_PAIR_SKIP: clean-pair skip on
+    {1},  // WT_OPT_SVD_PERSIST: persistent dependency-scheduled sweeps on
+    {1},  // WT_OPT_SVD_PRECOND: Gram-eigenbasis preconditioner on
+    {0},  // WT_OPT_SVD_PROFILE: per-phase cycle counters on stderr
+    {0},  // WT_OPT_SVD_TRACE: per-sweep convergence trace on stderr
+    {0},  // WT_OPT_EIG_PROFILE: preconditioner phase times on stderr
+};
+
+int option(int which) { return (which >= 0 && which < WT_OPT_COUNT) ? g_options[which].load() : 0; }
 
 int check_launch(const char* what) {
   cudaError_t e = cudaGetLastError();
@@ -48,6 +64,14 @@ int smem_attr(const void* kernel, int bytes) {
 
 }  // namespace wt
 
-extern "C" int wt_version(void) { return 100; }
+extern "C" int wt_version(void) { return 200; }
+
+extern "C" int wt_set_option(int which, int value) {
+  if (which < 0 || which >= WT_OPT_COUNT) {
+    wt::set_error("wt_set_option: unknown option %d", which);
+    return WT_ERR_INVALID;
+  }
+  return wt::g_options[which].exchange(value);
+}
 
 extern "C" const char* wt_last_error(void) { return wt::g_last_error; }

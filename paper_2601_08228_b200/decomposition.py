@@ -86,7 +86,7 @@ def w_svd_device(x: torch.Tensor, r: int, levels: int, tol: float = 0.0):
     rec, t = E.truncated_recon(pyr, sigma, vec, r, keep_t=True)       # K5; t = A V_r | A^T U_r
     recon = E.lift_inverse(rec, n1, n2, p, levels)
     ub, vb = E.svd_factors(t, vec, sigma, n1, n2, r)                  # K6: (p, n1, r), (p, n2, r)
-    sb = torch.diag_embed(sigma[:, :r]).contiguous()                  # (p, r, r) diagonal blocks
+    sb = E.diag_blocks(sigma, r)                                      # (p, r, r) diagonal blocks
     U = E.lift_inverse(ub, n1, r, p, levels)
     S = E.lift_inverse(sb, r, r, p, levels)
     V = E.lift_inverse(vb, n2, r, p, levels)

@@ -9,6 +9,8 @@ block order ``[d1 | ... | dL | sL]`` (include/wten_b200.h).
 
 from __future__ import annotations
 
+import contextlib
+
 import threading
 
 import numpy as np
@@ -415,6 +417,15 @@ def orthonormal_fixup(m: torch.Tensor, s: torch.Tensor, tau: float) -> torch.Ten
     return m
 
 
+def diag_blocks(sigma: torch.Tensor, r: int) -> torch.Tensor:
+    """(batch, q) singular values -> (batch, r, r) diagonal S blocks (wt_diag_blocks_f64)."""
+    lib = N.require_gpu()
+    batch, q = sigma.shape
+    out = torch.empty((batch, r, r), dtype=F64, device=sigma.device)
+    N.check(lib.wt_diag_blocks_f64(_ptr(sigma), q, r, batch, _ptr(out), _stream()), "wt_diag_blocks_f64")
+    return out
+
+
 def lu_zero_pivot(a: torch.Tensor) -> torch.Tensor:
     """(batch, n, n) -> int32 (batch,): 1 + first exactly-zero pivot of partial-pivoting LU, else 0."""
     lib = N.require_gpu()
@@ -423,6 +434,37 @@ def lu_zero_pivot(a: torch.Tensor) -> torch.Tensor:
     info = torch.empty((batch,), dtype=torch.int32, device=a.device)
     N.check(lib.wt_lu_pivot_check_f64(_ptr(w), n, batch, _ptr(info), _stream()), "wt_lu_pivot_check_f64")
     return info
+
+
+# Test / diagnostic switches of the library (wt_set_option; include/wten_b200.h).
+OPTIONS = {"svd_split": 0, "svd_ctas_per_sm": 1, "svd_pair_skip": 2, "svd_persist": 3, "svd_precond": 4,
+           "svd_profile": 5, "svd_trace": 6, "eig_profile": 7}
+
+
+def set_option(name: str, value: int) -> int:
+    """Set a library switch (tests / diagnostics only); returns the previous value."""
+    return int(N.load().wt_set_option(OPTIONS[name], int(value)))
+
+
+def options_from_env() -> None:
+    """Diagnostics tools (tools/*.py): WT_OPT_<NAME>=value environment variables set the
+    switches above (the library itself reads no environment)."""
+    import os
+
+    for name in OPTIONS:
+        v = os.environ.get("WT_OPT_" + name.upper())
+        if v is not None:
+            set_option(name, int(v))
+
+
+@contextlib.contextmanager
+def option(name: str, value: int):
+    """``with option("svd_split", 4): ...`` -- the switch is restored afterwards."""
+    old = set_option(name, value)
+    try:
+        yield
+    finally:
+        set_option(name, old)
 
 
 class SvdNotConverged(RuntimeError):

@@ -142,8 +142,8 @@ def test_determinism():
     assert torch.equal(r1, r2)
 
 
-@pytest.mark.parametrize("knob", ["WT_SVD_PERSIST", "WT_SVD_PAIR_SKIP"])
-def test_scheduling_knobs_do_not_change_bits(monkeypatch, knob):
+@pytest.mark.parametrize("knob", ["svd_persist", "svd_pair_skip"])
+def test_scheduling_knobs_do_not_change_bits(knob):
     """K4's persistent dependency-scheduled sweeps and the clean-pair skip only
     change WHEN visits run or drop visits that rotate nothing: sigma and vectors
     are bit-identical with either switched off (one launch per round / every
@@ -151,33 +151,35 @@ def test_scheduling_knobs_do_not_change_bits(monkeypatch, knob):
     one-launch-per-round path has no cluster-split visits, so the comparison
     pins the split to 1 (a split changes the Gram's summation order)."""
     a = torch.from_numpy(np.random.default_rng(29).standard_normal((6, 300, 256))).cuda()
-    monkeypatch.setenv("WT_SVD_SPLIT", "1")
     outs = []
-    for v in ("1", "0"):
-        monkeypatch.setenv(knob, v)
-        sigma, vec, info = E.svd(a, 256)
-        E.raise_if_failed(info)
-        outs.append((sigma.clone(), vec.clone(), E.last_sweeps()))
+    with E.option("svd_split", 1):
+        for v in (1, 0):
+            with E.option(knob, v):
+                sigma, vec, info = E.svd(a, 256)
+                E.raise_if_failed(info)
+                outs.append((sigma.clone(), vec.clone(), E.last_sweeps()))
     assert torch.equal(outs[0][0], outs[1][0]) and torch.equal(outs[0][1], outs[1][1])
     assert outs[0][2] == outs[1][2]
 
 
-@pytest.mark.parametrize("split", ["1", "2", "4", "8", "0"])
-def test_cluster_split_visits(monkeypatch, split):
+@pytest.mark.parametrize("split", [1, 2, 4, 8, 0])
+@pytest.mark.parametrize("precond", [1, 0])
+def test_cluster_split_visits(split, precond):
     """Visits split over 2/4/8-CTA clusters (rows of the panel, partial Grams
     summed in rank order through distributed shared memory; 9 row chunks, so
-    uneven row ranges): sigma against LAPACK, orthonormal vectors, and the
-    clean-pair skip (decided by the cluster leader) leaves the bits unchanged."""
+    uneven row ranges), with and without the Gram-eigenbasis preconditioner:
+    sigma against LAPACK, orthonormal vectors, and the clean-pair skip (decided
+    by the cluster leader) leaves the bits unchanged."""
     rng = np.random.default_rng(31)
     a_np = rng.standard_normal((3, 520, 512)) * np.linspace(1.0, 1e-3, 512)
     a = torch.from_numpy(a_np).cuda()
-    monkeypatch.setenv("WT_SVD_SPLIT", split)
     outs = []
-    for skip in ("1", "0"):
-        monkeypatch.setenv("WT_SVD_PAIR_SKIP", skip)
-        sigma, vec, info = E.svd(a, 512)
-        E.raise_if_failed(info)
-        outs.append((sigma.cpu().numpy(), vec.cpu().numpy()))
+    with E.option("svd_split", split), E.option("svd_precond", precond):
+        for skip in (1, 0):
+            with E.option("svd_pair_skip", skip):
+                sigma, vec, info = E.svd(a, 512)
+                E.raise_if_failed(info)
+                outs.append((sigma.cpu().numpy(), vec.cpu().numpy()))
     assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
     sigma, vec = outs[0]
     ref = np.linalg.svd(a_np, compute_uv=False)
@@ -189,12 +191,12 @@ def test_cluster_split_visits(monkeypatch, split):
 
 
 @pytest.mark.parametrize("shape", [(1, 70, 130), (2, 200, 33), (5, 64, 64)])
-def test_cluster_split_small_and_ragged(monkeypatch, shape):
+def test_cluster_split_small_and_ragged(shape):
     """Forced 8-CTA clusters on panels with fewer row chunks than CTAs (the host
     clamps the split to one chunk per CTA), wide and tall slices."""
     a_np = np.random.default_rng(sum(shape)).standard_normal(shape)
-    monkeypatch.setenv("WT_SVD_SPLIT", "8")
-    sigma, vec, info = E.svd(torch.from_numpy(a_np).cuda(), min(shape[1:]))
+    with E.option("svd_split", 8):
+        sigma, vec, info = E.svd(torch.from_numpy(a_np).cuda(), min(shape[1:]))
     E.raise_if_failed(info)
     assert sigma_err(sigma.cpu().numpy(), np.linalg.svd(a_np, compute_uv=False)) < 1e-12
 

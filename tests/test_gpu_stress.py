@@ -48,16 +48,14 @@ def test_svd_preconditioned_repeated(shape):
     assert np.max(np.abs(s0[:2].cpu().numpy() - ref)) < 1e-12 * ref.max()
 
 
-@pytest.mark.parametrize("env", [{"WT_SVD_SPLIT": "2"}, {"WT_SVD_SPLIT": "4"}, {"WT_SVD_SPLIT": "8"},
-                                 {"WT_SVD_CTAS_PER_SM": "1"}])
-def test_svd_scheduling_stress(monkeypatch, env):
-    for k, v in env.items():
-        monkeypatch.setenv(k, v)
+@pytest.mark.parametrize("opt", [("svd_split", 2), ("svd_split", 4), ("svd_split", 8), ("svd_ctas_per_sm", 1)])
+def test_svd_scheduling_stress(opt):
     a = torch.from_numpy(np.random.default_rng(7).standard_normal((3, 512, 512))).cuda()
-    s0, v0, _ = E.svd(a, 4)
-    for _ in range(4):
-        s, v, _ = E.svd(a, 4)
-        assert torch.equal(s, s0) and torch.equal(v, v0)
+    with E.option(*opt):
+        s0, v0, _ = E.svd(a, 4)
+        for _ in range(4):
+            s, v, _ = E.svd(a, 4)
+            assert torch.equal(s, s0) and torch.equal(v, v0)
     ref = np.linalg.svd(a.cpu().numpy(), compute_uv=False)
     assert np.max(np.abs(s0.cpu().numpy() - ref)) < 1e-12 * ref.max()
 

@@ -9,6 +9,7 @@ import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2601_08228_b200 import _native as N, engine as E, synth  # noqa: E402
+E.options_from_env()
 from oracle import wten_oracle as O  # noqa: E402
 
 
@@ -61,8 +62,8 @@ def cases(quick):
 
 if __name__ == "__main__":
     quick = len(sys.argv) > 1 and sys.argv[1] == "quick"
-    mode = os.environ.get("WT_SVD_PRECOND", "1")
-    print("WT_SVD_PRECOND =", mode)
+    mode = os.environ.get("WT_OPT_SVD_PRECOND", "1")
+    print("WT_OPT_SVD_PRECOND =", mode)
     worst = 0.0
     for name, a in cases(quick):
         worst = max(worst, run(name, a))

@@ -1,10 +1,10 @@
 """Small invocations of every kernel family for compute-sanitizer (memcheck /
 racecheck / synccheck): K1/K2 at every L (TMA paths, shallow / persistent /
 ancestor-chain variants, peer tables), K3 orientations, K4 plain / cluster-split
-(S = 2, 4, 8 through WT_SVD_SPLIT) / preconditioned (single CTA and cluster
+(S = 2, 4, 8 through WT_OPT_SVD_SPLIT) / preconditioned (single CTA and cluster
 panels), the epilogues, the orthonormal completion and the LU pivot check.
 Checks results against numpy so a silent corruption also fails.
-usage: [WT_SVD_SPLIT=S] python tools/sanitize_cases.py [lift|gemm|svd|all]"""
+usage: [WT_OPT_SVD_SPLIT=S] python tools/sanitize_cases.py [lift|gemm|svd|all]"""
 import os
 import sys
 
@@ -14,6 +14,7 @@ import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2601_08228_b200 as W  # noqa: E402
 from paper_2601_08228_b200 import engine as E  # noqa: E402
+E.options_from_env()
 from oracle import wten_oracle as O  # noqa: E402
 
 what = sys.argv[1] if len(sys.argv) > 1 else "all"

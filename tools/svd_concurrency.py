@@ -1,12 +1,13 @@
 """K4 in the latency-bound regime (few matrices, long round-robin chains):
 config-5 smooth slices, config-4 coarse slices at the 8-GPU share, config-3
-slices at the 8-GPU share.  Prints ms, sweeps and (with WT_SVD_PROFILE=1) the
+slices at the 8-GPU share.  Prints ms, sweeps and (with WT_OPT_SVD_PROFILE=1) the
 per-visit phase cycles (diagnostics).
-usage: [WT_SVD_PROFILE=1] python tools/svd_concurrency.py"""
+usage: [WT_OPT_SVD_PROFILE=1] python tools/svd_concurrency.py"""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 from paper_2601_08228_b200 import engine as E, synth
+E.options_from_env()
 
 
 def timed(a, nvec, label, reps=5):

@@ -1,9 +1,10 @@
 """Per-phase cycles of K4 at low occupancy (<= 1 CTA per SM): the latency floor (diagnostics).
-usage: WT_SVD_PROFILE=1 python tools/svd_latency.py [n] [batch]"""
+usage: WT_OPT_SVD_PROFILE=1 python tools/svd_latency.py [n] [batch]"""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 from paper_2601_08228_b200 import engine as E
+E.options_from_env()
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 256
 b = int(sys.argv[2]) if len(sys.argv) > 2 else 8
 a = torch.randn(b, n, n, dtype=torch.float64, device="cuda")
