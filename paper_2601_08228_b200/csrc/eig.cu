@@ -705,6 +705,47 @@ __global__ void tri_inviter(const double* __restrict__ dall, const double* __res
   for (int i = 0; i < n; ++i) Z[(int64_t)i * n + col] *= s;
 }
 
+// Eigenvalues that coincide to rounding (gap <= 1e-13 ||T||: e.g. the doubled
+// singular values of the t-svd real embeddings) leave inverse iteration
+// without a preferred direction: their vectors come out as independent but
+// arbitrary combinations inside the eigenspace.  One CTA per matrix walks the
+// ascending eigenvalues and orthonormalises each such cluster's vectors
+// (modified Gram-Schmidt, two passes), so Newton-Schulz starts near-orthogonal.
+__global__ void tri_cluster_mgs(const double* __restrict__ lamall, const double* __restrict__ info,
+                                const int* flag, int n, double* __restrict__ Zall) {
+  const int b = blockIdx.x;
+  if (!flag[b]) return;
+  const double* lam = lamall + (int64_t)b * n;
+  double* Z = Zall + (int64_t)b * n * n;
+  const double ctol = 1e-13 * info[b * 4 + 2];
+  __shared__ double red[NW];
+  int j0 = 0;
+  while (j0 < n) {
+    int j1 = j0 + 1;
+    while (j1 < n && lam[j1] - lam[j1 - 1] <= ctol) ++j1;  // cluster [j0, j1)
+    for (int j = j0 + 1; j < j1; ++j) {
+      const int cj = n - 1 - j;
+      for (int pass = 0; pass < 2; ++pass) {
+        for (int t = j0; t < j; ++t) {
+          const int ct = n - 1 - t;
+          double dsum = 0.0;
+          for (int i = threadIdx.x; i < n; i += blockDim.x) dsum = fma(Z[(int64_t)i * n + ct], Z[(int64_t)i * n + cj], dsum);
+          dsum = block_sum(dsum, red);
+          for (int i = threadIdx.x; i < n; i += blockDim.x) Z[(int64_t)i * n + cj] = fma(-dsum, Z[(int64_t)i * n + ct], Z[(int64_t)i * n + cj]);
+          __syncthreads();
+        }
+      }
+      double nrm = 0.0;
+      for (int i = threadIdx.x; i < n; i += blockDim.x) nrm = fma(Z[(int64_t)i * n + cj], Z[(int64_t)i * n + cj], nrm);
+      nrm = block_sum(nrm, red);
+      const double inv = nrm > 0.0 ? 1.0 / sqrt(nrm) : 0.0;
+      for (int i = threadIdx.x; i < n; i += blockDim.x) Z[(int64_t)i * n + cj] *= inv;
+      __syncthreads();
+    }
+    j0 = j1;
+  }
+}
+
 // P = Z^T Z given in its lower triangle (K3 lower tiles): delta[b] = max |P - I|
 // over the lower triangle (bit-pattern max; NaN propagates); mirrors P's lower
 // triangle into its upper one.
@@ -961,6 +1002,7 @@ int eig_precondition(const double* Xt, double* Yt, int64_t m, int64_t n, int64_t
     tri_bisect<<<grid, 128, 2 * sizeof(double) * (size_t)n, st>>>(dd, e2, info, flag, ni, lam);
     mark();
     tri_inviter<<<grid, 128, 0, st>>>(dd, ee, info, lam, flag, ni, Z, P, Z2);
+    tri_cluster_mgs<<<(unsigned)batch, PT, 0, st>>>(lam, info, flag, ni, Z);
   }
   if (int r = check_launch("eig bisection / inverse iteration")) return r;
   mark();
