@@ -842,20 +842,29 @@ __global__ void wy_larft(const double* __restrict__ Sall, const double* __restri
                          int n, int k0, int nb, double* __restrict__ Tall) {
   const int b = blockIdx.x;
   if (!flag[b]) return;
-  extern __shared__ double T[];  // [NBT][NBT + 1]
-  const double* S = Sall + (int64_t)b * NBT * NBT;  // (read through L1)
+  extern __shared__ double T[];  // [NBT][NBT + 1], then S [NBT][NBT + 1]
+  double* Ss = T + NBT * (NBT + 1);
+  const double* S = Sall + (int64_t)b * NBT * NBT;
   const double* tau = tauall + (int64_t)b * n + k0;
-  for (int e = threadIdx.x; e < NBT * NBT; e += blockDim.x) T[(e / NBT) * (NBT + 1) + e % NBT] = 0.0;
+  for (int e = threadIdx.x; e < NBT * NBT; e += blockDim.x) {
+    T[(e / NBT) * (NBT + 1) + e % NBT] = 0.0;
+    Ss[(e / NBT) * (NBT + 1) + e % NBT] = S[e];
+  }
   __syncthreads();
   for (int i = 0; i < nb; ++i) {
     const double ti = tau[i];
     const int r = threadIdx.x;
-    double s = 0.0;
+    double s0 = 0.0, s1 = 0.0;
     if (r < i) {
-      for (int c = r; c < i; ++c) s = fma(T[r * (NBT + 1) + c], __ldg(S + c * NBT + i), s);
+      int c = r;
+      for (; c + 1 < i; c += 2) {
+        s0 = fma(T[r * (NBT + 1) + c], Ss[c * (NBT + 1) + i], s0);
+        s1 = fma(T[r * (NBT + 1) + c + 1], Ss[(c + 1) * (NBT + 1) + i], s1);
+      }
+      if (c < i) s0 = fma(T[r * (NBT + 1) + c], Ss[c * (NBT + 1) + i], s0);
     }
     __syncthreads();
-    if (r < i) T[r * (NBT + 1) + i] = -ti * s;
+    if (r < i) T[r * (NBT + 1) + i] = -ti * (s0 + s1);
     if (r == i) T[r * (NBT + 1) + i] = ti;
     __syncthreads();
   }
@@ -1055,7 +1064,7 @@ int eig_precondition(const double* Xt, double* Yt, int64_t m, int64_t n, int64_t
                              glim, st))
       return r;
     if (nb < NBT) WT_CUDA(cudaMemsetAsync(T, 0, sizeof(double) * (size_t)(batch * NBT * NBT), st));
-    const size_t tsm = sizeof(double) * NBT * (NBT + 1);
+    const size_t tsm = 2 * sizeof(double) * NBT * (NBT + 1);
     if (int r = ensure_smem(wy_larft, tsm)) return r;
     wy_larft<<<(unsigned)batch, NBT, tsm, st>>>(S, tau, flag, ni, (int)k0, (int)nb, T);
     // M1 = Y^T Z (nb x n), M2 = T M1, Z[r0:, :] -= Y M2
