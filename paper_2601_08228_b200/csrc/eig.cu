@@ -55,6 +55,7 @@ constexpr int CH = WT_EIG_CH;  // symv column chunk (CH / 64 double2 register ac
 constexpr int NCH2 = CH / 64;
 constexpr int RB = WT_EIG_RB;  // rows per warp in flight in the symv
 static_assert(RB == 4, "the symv's row-sum reduction handles exactly 4 rows per warp");
+static_assert(CH >= 2 * NB + 1, "the y partials alias the symv's per-warp accumulators");
 constexpr int MAXR = 256;  // own rows per CTA (the panel's V, W rows of a CTA live in shared memory)
 constexpr int PREF_R = 128;  // preferred own rows per CTA (two CTAs per SM)
 constexpr int VP = 2 * NB + 2;  // shared pitch of a [V | W] row (even: 16-byte aligned rows)
@@ -100,8 +101,8 @@ __device__ __forceinline__ double block_sum(double v, double* red) {
 struct PanelSmem {
   static size_t bytes(int n, int C) {
     const int R = (n + C - 1) / C;
-    return sizeof(double) * ((size_t)R * VP + 8 + 2 * (size_t)n + 2 + 2 * (size_t)R + (size_t)NW * CH + 4 + 2 +
-                             2 * NB + 2 * NW + 7 * NB + NW * (2 * NB + 1));
+    return sizeof(double) * ((size_t)R * VP + 10 + 3 * (size_t)n + 2 + 2 * (size_t)R + (size_t)NW * CH + 4 + 2 +
+                             2 * NB + 2 * NW + 7 * NB);
   }
 };
 
@@ -116,7 +117,10 @@ struct PanelSmem {
 // memory, so the lazy updates never wait on global memory.  VW = [V | W] and
 // WV = [W | V] (n x 2NB, row-major, global) feed the trailing update A22 -=
 // VW WV^T on K3; the panel's V block overwrites its dead columns of A.
-// Four cluster barriers per column: S1 norm partials, S2 v, S3 symv partials, S4 w.
+// Two cluster barriers per column: S1 (my rows' updated column entries and
+// norm partials; every CTA then forms the whole v from the owners' entries)
+// and S3 (symv partials); w of row k+1, needed by every CTA's next lazy
+// update, is evaluated redundantly by every CTA with its owner's expression.
 template <int C>
 __global__ void __launch_bounds__(PT, 2) tridiag_panel(double* __restrict__ Gall, double* __restrict__ VWall,
                                                     double* __restrict__ WVall, double* __restrict__ dall,
@@ -127,7 +131,8 @@ __global__ void __launch_bounds__(PT, 2) tridiag_panel(double* __restrict__ Gall
   double* vws = sm;                    // [R][VP]  my rows of [V | W]
   double* vsm = vws + ((R * VP + 1) & ~1);  // [n + 2]  v (full; 16-byte aligned, zero beyond n)
   // (every array starts 16-byte aligned: double2 accesses)
-  double* csum = vsm + ((n + 3) & ~1); // [n]  CTA partial column part of A22 v (DSMEM-visible)
+  double* aw = vsm + ((n + 3) & ~1);   // [n]  my rows' updated column entries a_i (DSMEM-visible)
+  double* csum = aw + ((n + 1) & ~1);  // [n]  CTA partial column part of A22 v (DSMEM-visible)
   double* prow = csum + ((n + 1) & ~1);  // [R]  my rows: row part of A22 v
   double* diag = prow + ((R + 1) & ~1);  // [R]  my rows: A[i][i] (pre-panel)
   double* wacc = diag + ((R + 1) & ~1);  // [NW][CH] per-warp column accumulators
@@ -137,7 +142,8 @@ __global__ void __launch_bounds__(PT, 2) tridiag_panel(double* __restrict__ Gall
   double* ys = red + 2 * NW;           // [2NB] cluster sums of yW, yV
   double* rk = ys + 2 * NB;            // [2NB] row k of [V | W]
   double* dpan = rk + 2 * NB;          // [3NB] d, e, tau of the panel's columns (written at the end)
-  double* ywacc = dpan + 3 * NB;       // [NW][2NB + 1] per-warp partials of yW, yV, v^T A22 v
+  double* ywacc = wacc;                // [NW][2NB + 1] per-warp partials of yW, yV, v^T A22 v (aliases
+                                       // wacc: written after the symv's last flush has been consumed)
   const int rank = C == 1 ? 0 : cl_rank();
   const int b = blockIdx.x / C;
   if (!flag[b]) return;  // cluster-uniform
@@ -195,7 +201,7 @@ __global__ void __launch_bounds__(PT, 2) tridiag_panel(double* __restrict__ Gall
           a1 = fma(-ri[NB + t], rk[t], a1);
         }
         const double a = (a0 + a1) + (a2 + a3);
-        vsm[i] = a;
+        aw[i] = a;
         if (i >= k + 2) ss = fma(a, a, ss);
         if (i == k) dpan[j] = a;
         if (i == k + 1) alpha_own = a;
@@ -240,14 +246,16 @@ __global__ void __launch_bounds__(PT, 2) tridiag_panel(double* __restrict__ Gall
       dpan[2 * NB + j] = k < n - 1 ? tk : 0.0;
     }
     if (k == n - 1) break;  // the last column only has its diagonal
-    for (int q = tid; q < nloc; q += PT) {
-      const int i = row_of(q);
+    // v for every row of the trailing block, from the owners' a values (no
+    // barrier between: the a values stay untouched until after the next S3)
+    for (int i = tid; i < n; i += PT) {
       double v = 0.0;
-      if (i >= k + 2) v = vsm[i] * scale;
+      if (i >= k + 2) v = remote<C>(aw, i % C)[i] * scale;
       else if (i == k + 1) v = tk != 0.0 ? 1.0 : 0.0;
       vsm[i] = v;
-      vws[q * VP + j] = v;
     }
+    __syncthreads();
+    for (int q = tid; q < nloc; q += PT) vws[q * VP + j] = vsm[row_of(q)];
     // L2 prefetch of my rows' part of the next column's symv (A22 is constant
     // within the panel): one bulk prefetch per row, issued a column ahead
     if (j + 1 < jb) {
@@ -260,15 +268,8 @@ __global__ void __launch_bounds__(PT, 2) tridiag_panel(double* __restrict__ Gall
                        : "memory");
       }
     }
-    csync<C>();  // S2: every CTA's v entries are written
-    if constexpr (C > 1) {
-      for (int i = k + 1 + tid; i < n; i += PT)
-        if (i % C != rank) vsm[i] = *cl_map(vsm + i, i % C);
-      if (tid == 0) vsm[k] = 0.0;  // (a row that left the trailing block)
-      __syncthreads();
-    }
     // prefetch of my rows' entries of the next column (not changed by this panel);
-    // issued here so that no load is outstanding at the cluster barriers S1 / S2
+    // issued here so that no load is outstanding at the cluster barrier S1
     // (their release semantics wait for it), consumed by the next column's step A
 #pragma unroll
     for (int u = 0; u < (MAXR + PT - 1) / PT; ++u) {
@@ -404,40 +405,48 @@ __global__ void __launch_bounds__(PT, 2) tridiag_panel(double* __restrict__ Gall
     double ywv = 0.0;
     for (int t = 0; t < j; ++t) ywv = fma(ys[t], ys[NB + t], ywv);
     const double alpha2 = -0.5 * tk * tk * (pvt - 2.0 * ywv);
+    // w_i = tau (A22 v - V yW - W yV)_i + alpha2 v_i from the owner's row part,
+    // diagonal and [V | W] row, and every CTA's column part (one expression,
+    // evaluated by the owner for its rows and by every CTA for row k+1)
+    auto w_of = [&](const double* prow_o, const double* diag_o, const double* ri, int qo, int i) {
+      double p = prow_o[qo] - diag_o[qo] * vsm[i];  // the column parts include the diagonal
+#pragma unroll
+      for (int r = 0; r < C; ++r) p += remote<C>(csum, r)[i];
+      double p1 = 0.0, p2 = 0.0, p3 = 0.0;
+      int t = 0;
+      for (; t + 2 <= j; t += 2) {
+        const double2 v2 = *reinterpret_cast<const double2*>(ri + t);
+        const double2 w2 = *reinterpret_cast<const double2*>(ri + NB + t);
+        const double2 yw = *reinterpret_cast<const double2*>(ys + t);
+        const double2 yv = *reinterpret_cast<const double2*>(ys + NB + t);
+        p = fma(-v2.x, yw.x, p);
+        p1 = fma(-w2.x, yv.x, p1);
+        p2 = fma(-v2.y, yw.y, p2);
+        p3 = fma(-w2.y, yv.y, p3);
+      }
+      if (t < j) {
+        p = fma(-ri[t], ys[t], p);
+        p1 = fma(-ri[NB + t], ys[NB + t], p1);
+      }
+      p = (p + p1) + (p2 + p3);
+      return fma(alpha2, vsm[i], tk * p);
+    };
     for (int q = tid; q < nloc; q += PT) {
       const int i = row_of(q);
-      double w = 0.0;
-      if (i >= k + 1) {
-        double p = prow[q] - diag[q] * vsm[i];  // the column parts include the diagonal
-#pragma unroll
-        for (int r = 0; r < C; ++r) p += remote<C>(csum, r)[i];
-        const double* ri = vws + q * VP;
-        double p1 = 0.0, p2 = 0.0, p3 = 0.0;
-        int t = 0;
-        for (; t + 2 <= j; t += 2) {
-          const double2 v2 = *reinterpret_cast<const double2*>(ri + t);
-          const double2 w2 = *reinterpret_cast<const double2*>(ri + NB + t);
-          const double2 yw = *reinterpret_cast<const double2*>(ys + t);
-          const double2 yv = *reinterpret_cast<const double2*>(ys + NB + t);
-          p = fma(-v2.x, yw.x, p);
-          p1 = fma(-w2.x, yv.x, p1);
-          p2 = fma(-v2.y, yw.y, p2);
-          p3 = fma(-w2.y, yv.y, p3);
-        }
-        if (t < j) {
-          p = fma(-ri[t], ys[t], p);
-          p1 = fma(-ri[NB + t], ys[NB + t], p1);
-        }
-        p = (p + p1) + (p2 + p3);
-        w = fma(alpha2, vsm[i], tk * p);
-      }
-      vws[q * VP + NB + j] = w;
+      vws[q * VP + NB + j] = i >= k + 1 ? w_of(prow, diag, vws + q * VP, q, i) : 0.0;
     }
-    csync<C>();  // S4: W column j complete in every CTA
-    // row k+1 of [V | W] for the next column's update (from its owner's shared memory)
+    // row k+1 of [V | W] for the next column's lazy update: columns < j from its
+    // owner's shared memory (written before the last barrier), column j here
     if (j + 1 < jb) {
       const int ow = (k + 1) % C, qo = (k + 1) / C;
-      for (int t = tid; t < 2 * NB; t += PT) rk[t] = remote<C>(vws, ow)[qo * VP + t];
+      const double* ro = remote<C>(vws, ow) + qo * VP;
+      for (int t = tid; t < 2 * NB; t += PT) {
+        double v;
+        if (t == j) v = vsm[k + 1];
+        else if (t == NB + j) v = w_of(remote<C>(prow, ow), remote<C>(diag, ow), ro, qo, k + 1);
+        else v = ro[t];
+        rk[t] = v;
+      }
     }
     __syncthreads();
   }
