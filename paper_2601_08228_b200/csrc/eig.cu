@@ -26,7 +26,7 @@
 //      T - lambda I), one thread per eigenvalue              -> Z
 //   5. Newton-Schulz Z <- Z (3 I - Z^T Z) / 2 until orthogonal to rounding
 //      (K3; matrices where it cannot converge fall back to V0 = I)
-//   6. V0 = Q Z: compact-WY blocks of NBT reflectors (larft + 3 K3 GEMMs each)
+//   6. V0 = Q Z: compact-WY blocks of 64 / 128 reflectors (larft + 3 K3 GEMMs each)
 //   7. Y = X V0                                      K3 GEMM
 // Deterministic: fixed thread -> data maps and reduction orders.
 #include <math.h>
@@ -42,7 +42,7 @@ namespace wt {
 namespace eig {
 
 constexpr int NB = 32;     // tridiagonalization panel width
-constexpr int NBT = 64;    // back-transformation block (reflectors per compact-WY block)
+constexpr int NBT = 128;   // back-transformation block (reflectors per compact-WY block)
 constexpr int PT = 256;    // panel kernel threads
 constexpr int NW = PT / 32;
 #ifndef WT_EIG_CH
@@ -851,32 +851,30 @@ __global__ void wy_larft(const double* __restrict__ Sall, const double* __restri
                          int n, int k0, int nb, double* __restrict__ Tall) {
   const int b = blockIdx.x;
   if (!flag[b]) return;
-  extern __shared__ double T[];  // [NBT][NBT + 1], then S [NBT][NBT + 1]
-  double* Ss = T + NBT * (NBT + 1);
+  extern __shared__ double T[];  // [NBT][NBT + 1], then column i of S [NBT]
+  double* Sc = T + NBT * (NBT + 1);
   const double* S = Sall + (int64_t)b * NBT * NBT;
   const double* tau = tauall + (int64_t)b * n + k0;
-  for (int e = threadIdx.x; e < NBT * NBT; e += blockDim.x) {
-    T[(e / NBT) * (NBT + 1) + e % NBT] = 0.0;
-    Ss[(e / NBT) * (NBT + 1) + e % NBT] = S[e];
-  }
-  __syncthreads();
+  for (int e = threadIdx.x; e < NBT * NBT; e += blockDim.x) T[(e / NBT) * (NBT + 1) + e % NBT] = 0.0;
   for (int i = 0; i < nb; ++i) {
     const double ti = tau[i];
     const int r = threadIdx.x;
+    Sc[r] = r < i ? S[r * NBT + i] : 0.0;  // column i of S = Y^T Y
+    __syncthreads();
     double s0 = 0.0, s1 = 0.0;
     if (r < i) {
       int c = r;
       for (; c + 1 < i; c += 2) {
-        s0 = fma(T[r * (NBT + 1) + c], Ss[c * (NBT + 1) + i], s0);
-        s1 = fma(T[r * (NBT + 1) + c + 1], Ss[(c + 1) * (NBT + 1) + i], s1);
+        s0 = fma(T[r * (NBT + 1) + c], Sc[c], s0);
+        s1 = fma(T[r * (NBT + 1) + c + 1], Sc[c + 1], s1);
       }
-      if (c < i) s0 = fma(T[r * (NBT + 1) + c], Ss[c * (NBT + 1) + i], s0);
+      if (c < i) s0 = fma(T[r * (NBT + 1) + c], Sc[c], s0);
     }
     __syncthreads();
     if (r < i) T[r * (NBT + 1) + i] = -ti * (s0 + s1);
     if (r == i) T[r * (NBT + 1) + i] = ti;
-    __syncthreads();
   }
+  __syncthreads();
   double* Tg = Tall + (int64_t)b * NBT * NBT;
   for (int e = threadIdx.x; e < NBT * NBT; e += blockDim.x) Tg[e] = T[(e / NBT) * (NBT + 1) + e % NBT];
 }
@@ -1064,16 +1062,18 @@ int eig_precondition(const double* Xt, double* Yt, int64_t m, int64_t n, int64_t
   mark();
   // 6. V0 = Q Z: blocks of NBT reflectors, last block first
   const int64_t nref = n - 2;  // reflectors 0 .. n-3 (tau = 0 beyond)
-  for (int64_t k0 = ((nref - 1) / NBT) * NBT; k0 >= 0; k0 -= NBT) {
-    const int64_t nb = std::min<int64_t>(NBT, nref - k0);
+  // (128-reflector blocks halve the passes over Z for n >= 512; 64 measured
+  // faster on 256^2 slices: config 3 back-transform 1.02 vs 1.43 ms)
+  const int64_t nbt = n >= 512 ? NBT : 64;
+  for (int64_t k0 = ((nref - 1) / nbt) * nbt; k0 >= 0; k0 -= nbt) {
+    const int64_t nb = std::min<int64_t>(nbt, nref - k0);
     const int64_t r0 = k0 + 1;  // first nonzero row of the block
     const double* Y = G + r0 * n + k0;  // rows r0.., columns k0.. (ld n)
     // S = Y^T Y
     if (int r = gemm_f64_lim(1, 0, nb, nb, n - r0, 1.0, Y, n, nn, Y, n, nn, 0.0, S, NBT, NBT * NBT, batch, nullptr,
                              glim, st))
       return r;
-    if (nb < NBT) WT_CUDA(cudaMemsetAsync(T, 0, sizeof(double) * (size_t)(batch * NBT * NBT), st));
-    const size_t tsm = 2 * sizeof(double) * NBT * (NBT + 1);
+    const size_t tsm = sizeof(double) * (NBT * (NBT + 1) + NBT);
     if (int r = ensure_smem(wy_larft, tsm)) return r;
     wy_larft<<<(unsigned)batch, NBT, tsm, st>>>(S, tau, flag, ni, (int)k0, (int)nb, T);
     // M1 = Y^T Z (nb x n), M2 = T M1, Z[r0:, :] -= Y M2
