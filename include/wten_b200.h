@@ -106,6 +106,18 @@ int wt_gemm_f64(int transA, int transB, int64_t M, int64_t N, int64_t K, double 
                 int64_t batch, void* stream);
 
 /*
+ * The whole w-product C = inverse_w(face_product(forward_w(A), forward_w(B)))
+ * (reference algebra.py:43-51) in one call: K1 on A (n1 x n2 x p) and B
+ * (n2 x n3 x p), one K3 over all p wavelet slices, K2 into C (n1 x n3 x p), all
+ * C-contiguous device arrays.  `workspace` holds the three packed pyramids
+ * (wt_w_product_workspace_bytes).  A call repeating the previous call's exact
+ * arguments on the same host thread replays a CUDA graph of the four launches.
+ */
+size_t wt_w_product_workspace_bytes(int64_t n1, int64_t n2, int64_t n3, int64_t p);
+int wt_w_product_f64(const double* a, const double* b, int64_t n1, int64_t n2, int64_t n3, int64_t p,
+                     int levels, double* c, void* workspace, size_t workspace_bytes, void* stream);
+
+/*
  * K4 -- batched one-sided block-Jacobi SVD (Gram/rotation tiles on DMMA).
  * Replaces _stack_svd (decomposition.py:64-67, LAPACK dgesdd).
  * For each b < batch, A[b] is an n1 x n2 row-major matrix (lda, strideA).

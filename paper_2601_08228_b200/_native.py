@@ -38,6 +38,9 @@ SIGNATURES = {
     "wt_gemm_f64":(ctypes.c_int, [ctypes.c_int, ctypes.c_int, i64, i64, i64, ctypes.c_double,
                                    c_double_p, i64, i64, c_double_p, i64, i64, ctypes.c_double,
                                    c_double_p, i64, i64, i64, ctypes.c_void_p]),
+    "wt_w_product_workspace_bytes": (ctypes.c_size_t, [i64, i64, i64, i64]),
+    "wt_w_product_f64": (ctypes.c_int, [c_double_p, c_double_p, i64, i64, i64, i64, ctypes.c_int, c_double_p,
+                                        ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]),
     "wt_svd_workspace_bytes": (ctypes.c_size_t, [i64, i64, i64]),
     "wt_svd_jacobi_f64": (ctypes.c_int, [c_double_p, i64, i64, i64, i64, i64, c_double_p,
                                          c_double_p, i64, ctypes.c_void_p, ctypes.c_double,

@@ -70,13 +70,9 @@ def _as_operand(x):
 
 def w_product_device(a: torch.Tensor, b: torch.Tensor, levels: int,
                      out: torch.Tensor | None = None) -> torch.Tensor:
-    """Device core of w_product on contiguous CUDA tensors (no validation)."""
-    n1, n2, p = a.shape
-    n3 = b.shape[1]
-    pa = E.lift_forward(a, levels)
-    pb = E.lift_forward(b, levels)
-    pc = E.gemm(pa, pb)
-    return E.lift_inverse(pc, n1, n3, p, levels, out=out)
+    """Device core of w_product on contiguous CUDA tensors (no validation): K1, K1, K3,
+    K2 in one C-ABI call (engine.w_product)."""
+    return E.w_product(a, b, levels, out=out)
 
 
 def w_product(a, b, levels):

@@ -351,6 +351,29 @@ def lift_inverse_peer(table: torch.Tensor, n1: int, n2: int, p: int, levels: int
     return out
 
 
+_WP_WS: dict = {}  # (device, stream) -> cached workspace of the one-call w-product
+
+
+def w_product(a: torch.Tensor, b: torch.Tensor, levels: int, out: torch.Tensor | None = None) -> torch.Tensor:
+    """K1, K1, K3, K2 of a w-product in ONE C-ABI call (wt_w_product_f64); a, b
+    C-contiguous CUDA f64.  The pyramid workspace is cached per device and stream
+    (repeated calls on resident tensors replay a CUDA graph of the four launches)."""
+    lib = N.require_gpu()
+    n1, n2, p = a.shape
+    n3 = b.shape[1]
+    if out is None:
+        out = torch.empty((n1, n3, p), dtype=F64, device=a.device)
+    need = int(lib.wt_w_product_workspace_bytes(n1, n2, n3, p))
+    key = (a.device.index, _stream())
+    ws = _WP_WS.get(key)
+    if ws is None or ws.numel() < need:
+        ws = torch.empty((max(need, 1),), dtype=torch.uint8, device=a.device)
+        _WP_WS[key] = ws
+    N.check(lib.wt_w_product_f64(_ptr(a), _ptr(b), n1, n2, n3, p, levels, _ptr(out), _ptr(ws), ws.numel(),
+                                 _stream()), "wt_w_product_f64")
+    return out
+
+
 # ------------------------------------------------------------------ GEMM ----
 
 def gemm(a: torch.Tensor, b: torch.Tensor, trans_a: bool = False, trans_b: bool = False,
