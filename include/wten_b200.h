@@ -142,6 +142,19 @@ int wt_svd_jacobi_f64(const double* A, int64_t lda, int64_t strideA, int64_t n1,
                       void* stream);
 
 /*
+ * K4, leading triplets only: the k largest singular values (descending) of every
+ * slice and their long-side singular vectors (nvec <= k), same conventions as
+ * wt_svd_jacobi_f64.  The Jacobi sweeps run on X V0[:, :k], V0 the k leading
+ * eigenvectors of X^T X -- the rank-r truncation of sp_w_svd (reference
+ * decomposition.py:140-154, which needs no other singular value) with k well
+ * above r (3 <= min(n1, n2) <= 2048; batch <= 65535).
+ */
+size_t wt_svd_topk_workspace_bytes(int64_t n1, int64_t n2, int64_t batch, int64_t k);
+int wt_svd_topk_f64(const double* A, int64_t lda, int64_t strideA, int64_t n1, int64_t n2, int64_t batch, int64_t k,
+                    double* sigma, double* vec, int64_t nvec, int* info, double tol, int max_sweeps,
+                    void* workspace, size_t workspace_bytes, void* stream);
+
+/*
  * K5/K6/K7 helpers: scale the columns of a batch of row-major matrices,
  * M[b][i][j] *= f(s[b*q + j]) for j < ncols, where f is
  *   WT_SCALE_MUL (s), WT_SCALE_DIV (1/s, 0 if s == 0),

@@ -47,6 +47,10 @@ SIGNATURES = {
                                          ctypes.c_int, ctypes.c_void_p, ctypes.c_size_t,
                                          ctypes.c_void_p]),
     "wt_set_option": (ctypes.c_int, [ctypes.c_int, ctypes.c_int]),
+    "wt_svd_topk_workspace_bytes": (ctypes.c_size_t, [i64, i64, i64, i64]),
+    "wt_svd_topk_f64": (ctypes.c_int, [c_double_p, i64, i64, i64, i64, i64, i64, c_double_p, c_double_p, i64,
+                                       ctypes.c_void_p, ctypes.c_double, ctypes.c_int, ctypes.c_void_p,
+                                       ctypes.c_size_t, ctypes.c_void_p]),
     "wt_svd_last_sweeps": (ctypes.c_int, []),
     "wt_svd_last_fallbacks": (ctypes.c_int, []),
     "wt_svd_last_jacobi_flops": (ctypes.c_double, []),

@@ -594,9 +594,10 @@ __global__ void tri_prepare(double* __restrict__ dall, double* __restrict__ eall
   }
 }
 
-// One thread per eigenvalue: lam[b][j] = j-th smallest eigenvalue of (scaled) T
+// One thread per eigenvalue: lam[b][j] = j-th smallest eigenvalue of (scaled) T, for the kk largest
 __global__ void tri_bisect(const double* __restrict__ dall, const double* __restrict__ e2all,
-                           const double* __restrict__ info, const int* flag, int n, double* __restrict__ lam) {
+                           const double* __restrict__ info, const int* flag, int n, int kk,
+                           double* __restrict__ lam) {
   extern __shared__ double tsm[];  // d[n], e2[n]
   const int b = blockIdx.y;
   if (!flag[b]) return;
@@ -607,7 +608,7 @@ __global__ void tri_bisect(const double* __restrict__ dall, const double* __rest
     e2s[i] = i < n - 1 ? e2all[(int64_t)b * n + i] : 0.0;
   }
   __syncthreads();
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  const int j = n - kk + blockIdx.x * blockDim.x + threadIdx.x;  // the kk largest eigenvalues
   if (j >= n) return;
   double lo = info[b * 4 + 0], hi = info[b * 4 + 1];
   const double span = info[b * 4 + 2];
@@ -637,29 +638,31 @@ __device__ __forceinline__ double hash_unit(uint32_t i, uint32_t j) {
 // Scratch L, Dinv: [i][j] layout (coalesced over the eigenvalue threads).
 __global__ void tri_inviter(const double* __restrict__ dall, const double* __restrict__ eall,
                             const double* __restrict__ info, const double* __restrict__ lamall, const int* flag,
-                            int n, double* __restrict__ Zall, double* __restrict__ Lall, double* __restrict__ Dall) {
+                            int n, int kk, double* __restrict__ Zall, double* __restrict__ Lall,
+                            double* __restrict__ Dall) {
   const int b = blockIdx.y;
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (!flag[b] || j >= n) return;
+  const int jj = blockIdx.x * blockDim.x + threadIdx.x;  // 0 .. kk-1: eigenvalue n - kk + jj
+  if (!flag[b] || jj >= kk) return;
+  const int j = n - kk + jj;
   const double* d = dall + (int64_t)b * n;
   const double* e = eall + (int64_t)b * n;
-  const int64_t nn = (int64_t)n * n;
-  double* Z = Zall + b * nn;
-  double* L = Lall + b * nn;
-  double* Di = Dall + b * nn;
+  const int64_t nk = (int64_t)n * kk;
+  double* Z = Zall + b * nk;   // n x kk, column kk-1-jj (descending eigenvalues)
+  double* L = Lall + b * nk;   // scratch [i][jj]
+  double* Di = Dall + b * nk;
   const double lam = lamall[(int64_t)b * n + j];
   const double span = info[b * 4 + 2];
   const double small = 2.220446049250313e-16 * span + 1e-300;
-  const int col = n - 1 - j;
+  const int col = kk - 1 - jj;
   // factor
   double D = d[0] - lam;
   for (int i = 0; i < n; ++i) {
     if (fabs(D) < small) D = D < 0.0 ? -small : small;
     const double inv = 1.0 / D;
-    Di[(int64_t)i * n + j] = inv;
+    Di[(int64_t)i * kk + jj] = inv;
     if (i < n - 1) {
       const double l = e[i] * inv;
-      L[(int64_t)i * n + j] = l;
+      L[(int64_t)i * kk + jj] = l;
       D = (d[i + 1] - lam) - l * e[i];
     }
   }
@@ -675,15 +678,15 @@ __global__ void tri_inviter(const double* __restrict__ dall, const double* __res
 #pragma unroll
       for (int u = 0; u < IB; ++u) {
         const int i = i0 + u;
-        xb[u] = i < n ? (it == 0 ? hash_unit(i, j) : Z[(int64_t)i * n + col] * s) : 0.0;
-        lb[u] = (i > 0 && i < n) ? L[(int64_t)(i - 1) * n + j] : 0.0;
+        xb[u] = i < n ? (it == 0 ? hash_unit(i, j) : Z[(int64_t)i * kk + col] * s) : 0.0;
+        lb[u] = (i > 0 && i < n) ? L[(int64_t)(i - 1) * kk + jj] : 0.0;
       }
 #pragma unroll
       for (int u = 0; u < IB; ++u) {
         const int i = i0 + u;
         if (i < n) {
           w = i == 0 ? xb[u] : fma(-lb[u], w, xb[u]);
-          Z[(int64_t)i * n + col] = w;
+          Z[(int64_t)i * kk + col] = w;
         }
       }
     }
@@ -694,9 +697,9 @@ __global__ void tri_inviter(const double* __restrict__ dall, const double* __res
 #pragma unroll
       for (int u = 0; u < IB; ++u) {
         const int i = i1 - u;
-        wb[u] = i >= 0 ? Z[(int64_t)i * n + col] : 0.0;
-        db[u] = i >= 0 ? Di[(int64_t)i * n + j] : 0.0;
-        lb[u] = (i >= 0 && i < n - 1) ? L[(int64_t)i * n + j] : 0.0;
+        wb[u] = i >= 0 ? Z[(int64_t)i * kk + col] : 0.0;
+        db[u] = i >= 0 ? Di[(int64_t)i * kk + jj] : 0.0;
+        lb[u] = (i >= 0 && i < n - 1) ? L[(int64_t)i * kk + jj] : 0.0;
       }
 #pragma unroll
       for (int u = 0; u < IB; ++u) {
@@ -704,14 +707,14 @@ __global__ void tri_inviter(const double* __restrict__ dall, const double* __res
         if (i >= 0) {
           const double wi = wb[u] * db[u];
           y = i == n - 1 ? wi : fma(-lb[u], y, wi);
-          Z[(int64_t)i * n + col] = y;
+          Z[(int64_t)i * kk + col] = y;
           nrm = fma(y, y, nrm);
         }
       }
     }
     s = nrm > 0.0 && isfinite(nrm) ? 1.0 / sqrt(nrm) : 0.0;
   }
-  for (int i = 0; i < n; ++i) Z[(int64_t)i * n + col] *= s;
+  for (int i = 0; i < n; ++i) Z[(int64_t)i * kk + col] *= s;
 }
 
 // Eigenvalues that coincide to rounding (gap <= 1e-13 ||T||: e.g. the doubled
@@ -721,34 +724,34 @@ __global__ void tri_inviter(const double* __restrict__ dall, const double* __res
 // ascending eigenvalues and orthonormalises each such cluster's vectors
 // (modified Gram-Schmidt, two passes), so Newton-Schulz starts near-orthogonal.
 __global__ void tri_cluster_mgs(const double* __restrict__ lamall, const double* __restrict__ info,
-                                const int* flag, int n, double* __restrict__ Zall) {
+                                const int* flag, int n, int kk, double* __restrict__ Zall) {
   const int b = blockIdx.x;
   if (!flag[b]) return;
   const double* lam = lamall + (int64_t)b * n;
-  double* Z = Zall + (int64_t)b * n * n;
+  double* Z = Zall + (int64_t)b * n * kk;  // n x kk, column kk-1-(j-(n-kk)) holds eigenvalue j
   const double ctol = 1e-13 * info[b * 4 + 2];
   __shared__ double red[NW];
-  int j0 = 0;
+  int j0 = n - kk;
   while (j0 < n) {
     int j1 = j0 + 1;
     while (j1 < n && lam[j1] - lam[j1 - 1] <= ctol) ++j1;  // cluster [j0, j1)
     for (int j = j0 + 1; j < j1; ++j) {
-      const int cj = n - 1 - j;
+      const int cj = n - 1 - j;  // == kk - 1 - (j - (n - kk))
       for (int pass = 0; pass < 2; ++pass) {
         for (int t = j0; t < j; ++t) {
           const int ct = n - 1 - t;
           double dsum = 0.0;
-          for (int i = threadIdx.x; i < n; i += blockDim.x) dsum = fma(Z[(int64_t)i * n + ct], Z[(int64_t)i * n + cj], dsum);
+          for (int i = threadIdx.x; i < n; i += blockDim.x) dsum = fma(Z[(int64_t)i * kk + ct], Z[(int64_t)i * kk + cj], dsum);
           dsum = block_sum(dsum, red);
-          for (int i = threadIdx.x; i < n; i += blockDim.x) Z[(int64_t)i * n + cj] = fma(-dsum, Z[(int64_t)i * n + ct], Z[(int64_t)i * n + cj]);
+          for (int i = threadIdx.x; i < n; i += blockDim.x) Z[(int64_t)i * kk + cj] = fma(-dsum, Z[(int64_t)i * kk + ct], Z[(int64_t)i * kk + cj]);
           __syncthreads();
         }
       }
       double nrm = 0.0;
-      for (int i = threadIdx.x; i < n; i += blockDim.x) nrm = fma(Z[(int64_t)i * n + cj], Z[(int64_t)i * n + cj], nrm);
+      for (int i = threadIdx.x; i < n; i += blockDim.x) nrm = fma(Z[(int64_t)i * kk + cj], Z[(int64_t)i * kk + cj], nrm);
       nrm = block_sum(nrm, red);
       const double inv = nrm > 0.0 ? 1.0 / sqrt(nrm) : 0.0;
-      for (int i = threadIdx.x; i < n; i += blockDim.x) Z[(int64_t)i * n + cj] *= inv;
+      for (int i = threadIdx.x; i < n; i += blockDim.x) Z[(int64_t)i * kk + cj] *= inv;
       __syncthreads();
     }
     j0 = j1;
@@ -879,14 +882,14 @@ __global__ void wy_larft(const double* __restrict__ Sall, const double* __restri
   for (int e = threadIdx.x; e < NBT * NBT; e += blockDim.x) Tg[e] = T[(e / NBT) * (NBT + 1) + e % NBT];
 }
 
-// V0 = I for the matrices that fall back
-__global__ void set_identity(double* __restrict__ Vall, int n, const int* flag) {
+// V0 = I[:, :kk] for the matrices that fall back
+__global__ void set_identity(double* __restrict__ Vall, int n, int kk, const int* flag) {
   const int b = blockIdx.y;
   if (flag[b]) return;
-  double* V = Vall + (int64_t)b * n * n;
-  const int64_t nn = (int64_t)n * n;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nn; e += (int64_t)gridDim.x * blockDim.x)
-    V[e] = (e / n == e % n) ? 1.0 : 0.0;
+  double* V = Vall + (int64_t)b * n * kk;
+  const int64_t nk = (int64_t)n * kk;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nk; e += (int64_t)gridDim.x * blockDim.x)
+    V[e] = (e / kk == e % kk) ? 1.0 : 0.0;
 }
 
 struct Layout {
@@ -951,11 +954,13 @@ int launch_panel(double* G, double* VW, double* WV, double* d, double* e, double
 size_t eig_workspace_bytes(int64_t n, int64_t batch) { return eig::layout(n, batch).total; }
 
 int eig_precondition(const double* Xt, double* Yt, int64_t m, int64_t n, int64_t ldx, int64_t sx, int64_t batch,
-                     void* ws, size_t ws_bytes, int* n_fallback, cudaStream_t st) {
+                     int64_t kk, int64_t ldy, int64_t sy, void* ws, size_t ws_bytes, int* n_fallback,
+                     cudaStream_t st) {
   using namespace eig;
   const Layout L = layout(n, batch);
   WT_REQUIRE(ws != nullptr && ws_bytes >= L.total, "eig: workspace too small");
   WT_REQUIRE(n >= 3 && n <= 8 * MAXR, "eig: n = %lld unsupported", (long long)n);
+  WT_REQUIRE(kk >= 1 && kk <= n, "eig: %lld leading eigenvectors of %lld", (long long)kk, (long long)n);
   char* base = static_cast<char*>(ws);
   auto D = [&](size_t off) { return reinterpret_cast<double*>(base + off); };
   double *G = D(L.G), *Z = D(L.Z), *Z2 = D(L.Z2), *P = D(L.P), *VW = D(L.VW), *WV = D(L.WV);
@@ -965,7 +970,9 @@ int eig_precondition(const double* Xt, double* Yt, int64_t m, int64_t n, int64_t
   int* flag = reinterpret_cast<int*>(base + L.flag);
   int* glim = reinterpret_cast<int*>(base + L.glim);
   const int64_t nn = n * n;
-  const int ni = (int)n;
+  const int64_t nk = n * kk;  // Z, Z2: n x kk (the kk leading eigenvectors, descending)
+  const int64_t kk2 = kk * kk;  // P, Z2-as-P^2: kk x kk
+  const int ni = (int)n, ki = (int)kk;
   // WT_OPT_EIG_PROFILE: per-phase device times on stderr (diagnostics)
   const bool prof = option(WT_OPT_EIG_PROFILE) != 0;
   cudaEvent_t ev[10] = {};
@@ -1013,12 +1020,12 @@ int eig_precondition(const double* Xt, double* Yt, int64_t m, int64_t n, int64_t
   // 3-4. eigenvalues (bisection) and eigenvectors (inverse iteration) of T
   tri_prepare<<<(unsigned)batch, PT, 0, st>>>(dd, ee, e2, info, flag, ni);
   {
-    dim3 grid((unsigned)((n + 127) / 128), (unsigned)batch);
+    dim3 grid((unsigned)((kk + 127) / 128), (unsigned)batch);
     if (int r = ensure_smem(tri_bisect, 2 * sizeof(double) * (size_t)n)) return r;
-    tri_bisect<<<grid, 128, 2 * sizeof(double) * (size_t)n, st>>>(dd, e2, info, flag, ni, lam);
+    tri_bisect<<<grid, 128, 2 * sizeof(double) * (size_t)n, st>>>(dd, e2, info, flag, ni, ki, lam);
     mark();
-    tri_inviter<<<grid, 128, 0, st>>>(dd, ee, info, lam, flag, ni, Z, P, Z2);
-    tri_cluster_mgs<<<(unsigned)batch, PT, 0, st>>>(lam, info, flag, ni, Z);
+    tri_inviter<<<grid, 128, 0, st>>>(dd, ee, info, lam, flag, ni, ki, Z, P, Z2);
+    tri_cluster_mgs<<<(unsigned)batch, PT, 0, st>>>(lam, info, flag, ni, ki, Z);
   }
   if (int r = check_launch("eig bisection / inverse iteration")) return r;
   mark();
@@ -1026,6 +1033,7 @@ int eig_precondition(const double* Xt, double* Yt, int64_t m, int64_t n, int64_t
   //    order 2 or 3 per matrix as its delta needs (ns_decide); every decision is
   //    per matrix, so the result does not depend on the batch.
   const double done_tol = 64.0 * 2.220446049250313e-16 * sqrt((double)n);
+  // (Z^T Z and its polynomial are kk x kk, packed with stride kk^2)
   constexpr int kMaxNs = 3;
   int* mode = reinterpret_cast<int*>(base + L.done);
   int* glim2 = reinterpret_cast<int*>(base + L.glim2);
@@ -1033,12 +1041,12 @@ int eig_precondition(const double* Xt, double* Yt, int64_t m, int64_t n, int64_t
   WT_CUDA(cudaMemsetAsync(mode, 0xff, sizeof(int) * (size_t)batch, st));  // -1 != 0: not yet known
   int h_counts[2] = {0, 0};
   for (int it = 0; it < kMaxNs; ++it) {
-    if (int r = gemm_f64_lim(1, 0, n, n, n, 1.0, Z, n, nn, Z, n, nn, 0.0, P, n, nn, batch, nullptr, glim, st, 1))
+    if (int r = gemm_f64_lim(1, 0, kk, kk, n, 1.0, Z, kk, nk, Z, kk, nk, 0.0, P, kk, kk2, batch, nullptr, glim, st, 1))
       return r;
     WT_CUDA(cudaMemsetAsync(delta, 0, sizeof(unsigned long long) * (size_t)batch, st));
     WT_CUDA(cudaMemsetAsync(counts, 0, 2 * sizeof(int), st));
-    const dim3 grid((unsigned)std::min<int64_t>((nn + 255) / 256, 64), (unsigned)batch);
-    ns_delta<<<grid, 256, 0, st>>>(P, ni, flag, mode, delta);
+    const dim3 grid((unsigned)std::min<int64_t>((kk2 + 255) / 256, 64), (unsigned)batch);
+    ns_delta<<<grid, 256, 0, st>>>(P, ki, flag, mode, delta);
     // last iteration: keep only the matrices this update brings to rounding
     const double lim = it == kMaxNs - 1 ? cbrt(done_tol / 0.3125) : 0.25;
     ns_decide<<<(unsigned)((batch + 255) / 256), 256, 0, st>>>(delta, (int)batch, done_tol, lim, flag, glim, mode,
@@ -1047,10 +1055,11 @@ int eig_precondition(const double* Xt, double* Yt, int64_t m, int64_t n, int64_t
     WT_CUDA(cudaStreamSynchronize(st));
     if (h_counts[0] == 0) break;  // every matrix orthogonal (or fallen back)
     // P^2 for the order-3 matrices (lower tiles; P still holds the lower triangle of Z^T Z)
-    if (int r = gemm_f64_lim(0, 1, n, n, n, 1.0, P, n, nn, P, n, nn, 0.0, Z2, n, nn, batch, nullptr, glim2, st, 1))
+    if (int r = gemm_f64_lim(0, 1, kk, kk, kk, 1.0, P, kk, kk2, P, kk, kk2, 0.0, Z2, kk, kk2, batch, nullptr, glim2,
+                             st, 1))
       return r;
-    ns_form<<<grid, 256, 0, st>>>(P, Z2, ni, mode);
-    if (int r = gemm_f64_lim(0, 0, n, n, n, 1.0, Z, n, nn, P, n, nn, 0.0, Z2, n, nn, batch, nullptr, glim, st))
+    ns_form<<<grid, 256, 0, st>>>(P, Z2, ki, mode);
+    if (int r = gemm_f64_lim(0, 0, n, kk, kk, 1.0, Z, kk, nk, P, kk, kk2, 0.0, Z2, kk, nk, batch, nullptr, glim, st))
       return r;
     std::swap(Z, Z2);
     if (h_counts[1] == 0) break;  // every update reached rounding: no further check needed
@@ -1077,24 +1086,24 @@ int eig_precondition(const double* Xt, double* Yt, int64_t m, int64_t n, int64_t
     if (int r = ensure_smem(wy_larft, tsm)) return r;
     wy_larft<<<(unsigned)batch, NBT, tsm, st>>>(S, tau, flag, ni, (int)k0, (int)nb, T);
     // M1 = Y^T Z (nb x n), M2 = T M1, Z[r0:, :] -= Y M2
-    if (int r = gemm_f64_lim(1, 0, nb, n, n - r0, 1.0, Y, n, nn, Z + r0 * n, n, nn, 0.0, M1, n, NBT * n, batch,
+    if (int r = gemm_f64_lim(1, 0, nb, kk, n - r0, 1.0, Y, n, nn, Z + r0 * kk, kk, nk, 0.0, M1, kk, NBT * n, batch,
                              nullptr, glim, st))
       return r;
-    if (int r = gemm_f64_lim(0, 0, nb, n, nb, 1.0, T, NBT, NBT * NBT, M1, n, NBT * n, 0.0, M2, n, NBT * n, batch,
+    if (int r = gemm_f64_lim(0, 0, nb, kk, nb, 1.0, T, NBT, NBT * NBT, M1, kk, NBT * n, 0.0, M2, kk, NBT * n, batch,
                              nullptr, glim, st))
       return r;
-    if (int r = gemm_f64_lim(0, 0, n - r0, n, nb, -1.0, Y, n, nn, M2, n, NBT * n, 1.0, Z + r0 * n, n, nn, batch,
+    if (int r = gemm_f64_lim(0, 0, n - r0, kk, nb, -1.0, Y, n, nn, M2, kk, NBT * n, 1.0, Z + r0 * kk, kk, nk, batch,
                              nullptr, glim, st))
       return r;
   }
   {
-    dim3 grid((unsigned)std::min<int64_t>((nn + 255) / 256, 256), (unsigned)batch);
-    set_identity<<<grid, 256, 0, st>>>(Z, ni, flag);
+    dim3 grid((unsigned)std::min<int64_t>((nk + 255) / 256, 256), (unsigned)batch);
+    set_identity<<<grid, 256, 0, st>>>(Z, ni, ki, flag);
   }
   if (int r = check_launch("eig back-transformation")) return r;
   mark();
-  // 7. Y = X V0  (Yt = V0^T Xt)
-  if (int r = gemm_f64_lim(1, 0, n, m, n, 1.0, Z, n, nn, Xt, ldx, sx, 0.0, Yt, ldx, sx, batch, nullptr, nullptr, st))
+  // 7. Y = X V0  (Yt = V0^T Xt: kk rows of pitch ldy, stride sy)
+  if (int r = gemm_f64_lim(1, 0, kk, m, n, 1.0, Z, kk, nk, Xt, ldx, sx, 0.0, Yt, ldy, sy, batch, nullptr, nullptr, st))
     return r;
   mark();
   if (prof && nev > 1) {

@@ -119,3 +119,17 @@ extern "C" int wt_svd_jacobi_f64(const double* A, int64_t lda, int64_t strideA, 
   return hb16::jacobi(A, lda, strideA, n1, n2, batch, sigma, vec, nvec, info, tol, max_sweeps,
                       workspace, workspace_bytes, stream);
 }
+
+extern "C" size_t wt_svd_topk_workspace_bytes(int64_t n1, int64_t n2, int64_t batch, int64_t k) {
+  if (n1 < 1 || n2 < 1 || batch < 0 || k < 1) return 0;
+  return hb16::topk_layout(n1, n2, batch, k).total;
+}
+
+extern "C" int wt_svd_topk_f64(const double* A, int64_t lda, int64_t strideA, int64_t n1, int64_t n2, int64_t batch,
+                               int64_t k, double* sigma, double* vec, int64_t nvec, int* info, double tol,
+                               int max_sweeps, void* workspace, size_t workspace_bytes, void* stream) {
+  WT_REQUIRE(batch <= 65535, "svd_topk: batch above 65535");
+  g_last_hb = 16;
+  return hb16::jacobi_topk(A, lda, strideA, n1, n2, batch, k, sigma, vec, nvec, info, tol, max_sweeps, workspace,
+                           workspace_bytes, stream);
+}

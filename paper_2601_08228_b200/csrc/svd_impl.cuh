@@ -847,7 +847,7 @@ inline bool precond_enabled(int64_t n) {
   return option(WT_OPT_SVD_PRECOND) != 0 && n >= kPrecondMinN && n <= 2048;
 }
 
-WsLayout ws_layout(int64_t n1, int64_t n2, int64_t batch) {
+WsLayout ws_layout(int64_t n1, int64_t n2, int64_t batch, bool allow_precond = true) {
   WsLayout L{};
   L.m = std::max(n1, n2);
   L.n = std::min(n1, n2);
@@ -870,7 +870,7 @@ WsLayout ws_layout(int64_t n1, int64_t n2, int64_t batch) {
   L.off_bver = take(L.skip ? sizeof(int) * (size_t)(batch * nbk) : 0);
   L.off_pclean = take(L.skip ? sizeof(unsigned long long) * (size_t)(batch * nbk * nbk) : 0);
   L.off_scale = take(sizeof(double) * (size_t)batch);
-  L.precond = precond_enabled(L.n);
+  L.precond = allow_precond && precond_enabled(L.n);
   L.eig_bytes = L.precond ? eig_workspace_bytes(L.n, batch) : 0;
   L.off_eig = take(L.eig_bytes);
   L.total = o;
@@ -925,12 +925,12 @@ size_t workspace_bytes(int64_t n1, int64_t n2, int64_t batch) {
 int jacobi(const double* A, int64_t lda, int64_t strideA, int64_t n1,
                                  int64_t n2, int64_t batch, double* sigma, double* vec,
                                  int64_t nvec, int* info, double tol, int max_sweeps,
-                                 void* workspace, size_t workspace_bytes, void* stream) {
+                                 void* workspace, size_t workspace_bytes, void* stream, bool allow_precond = true) {
   WT_REQUIRE(n1 >= 1 && n2 >= 1 && batch >= 0, "svd: bad shape %lld x %lld", (long long)n1,
              (long long)n2);
   if (batch == 0) return WT_OK;
   WT_REQUIRE(lda >= n2, "svd: lda < n2");
-  const WsLayout L = ws_layout(n1, n2, batch);
+  const WsLayout L = ws_layout(n1, n2, batch, allow_precond);
   WT_REQUIRE(nvec >= 0 && nvec <= L.n, "svd: nvec %lld outside [0, %lld]", (long long)nvec,
              (long long)L.n);
   WT_REQUIRE(workspace != nullptr && workspace_bytes >= L.total,
@@ -976,8 +976,8 @@ int jacobi(const double* A, int64_t lda, int64_t strideA, int64_t n1,
     // every matrix starts from buffer 1
     WT_CUDA(cudaMemsetAsync(ws.X2, 0, sizeof(double) * (size_t)(batch * L.npad * L.mpad), st));
     int fallback = 0;
-    if (int e = eig_precondition(ws.X, ws.X2, L.mpad, L.n, L.mpad, L.npad * L.mpad, batch, base + L.off_eig,
-                                 L.eig_bytes, &fallback, st))
+    if (int e = eig_precondition(ws.X, ws.X2, L.mpad, L.n, L.mpad, L.npad * L.mpad, batch, L.n, L.mpad,
+                                 L.npad * L.mpad, base + L.off_eig, L.eig_bytes, &fallback, st))
       return e;
     g_last_fallbacks = fallback;
     svd_fill_int<<<(unsigned)((batch + 255) / 256), 256, 0, st>>>(ws.xsel, (int)batch, 1);
@@ -1158,5 +1158,82 @@ int jacobi(const double* A, int64_t lda, int64_t strideA, int64_t n1,
   return WT_OK;
 }
 
+
+// ------------------------------------------------------- leading triplets --
+// The k leading singular triplets only (sp-w-svd needs no more: its result is
+// the rank-r reconstruction of the coarse slices, decomposition.py:140-154):
+// X V0 with V0 the k leading eigenvectors of X^T X (eig.cu), then the one-sided
+// Jacobi on that m x k matrix.  Its columns span the leading singular subspace
+// to eps ||X||^2 / (s_k^2 - s_{k+1}^2), so with k well above r the rank-r
+// truncation is that of the full SVD (tested against LAPACK / the oracle);
+// the sweeps run on k columns instead of n.
+struct TopkLayout {
+  WsLayout inner;
+  int64_t m, n, mpad, npad, k;
+  size_t off_X, off_scale, off_eig, eig_bytes, off_X1, off_inner, total;
+};
+
+TopkLayout topk_layout(int64_t n1, int64_t n2, int64_t batch, int64_t k) {
+  TopkLayout T{};
+  T.m = std::max(n1, n2);
+  T.n = std::min(n1, n2);
+  T.k = k;
+  T.mpad = round_up(std::max<int64_t>(T.m, 1), RCH);
+  T.npad = round_up(std::max<int64_t>(T.n, 1), BW);
+  size_t o = 0;
+  auto take = [&](size_t bytes) { size_t r = o; o = (o + bytes + 255) / 256 * 256; return r; };
+  T.off_X = take(sizeof(double) * (size_t)(batch * T.npad * T.mpad));
+  T.off_scale = take(sizeof(double) * (size_t)batch);
+  T.eig_bytes = eig_workspace_bytes(T.n, batch);
+  T.off_eig = take(T.eig_bytes);
+  T.off_X1 = take(sizeof(double) * (size_t)(batch * k * T.mpad));
+  T.inner = ws_layout(k, T.m, batch, false);
+  T.off_inner = take(T.inner.total);
+  T.total = o;
+  return T;
+}
+
+__global__ void svd_unscale(double* __restrict__ sigma, int64_t k, int64_t batch, const double* __restrict__ scale) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < batch * k; e += (int64_t)gridDim.x * blockDim.x)
+    sigma[e] /= scale[e / k];
+}
+
+int jacobi_topk(const double* A, int64_t lda, int64_t strideA, int64_t n1, int64_t n2, int64_t batch, int64_t k,
+                double* sigma, double* vec, int64_t nvec, int* info, double tol, int max_sweeps, void* workspace,
+                size_t workspace_bytes, void* stream) {
+  WT_REQUIRE(n1 >= 1 && n2 >= 1 && batch >= 0, "svd_topk: bad shape");
+  if (batch == 0) return WT_OK;
+  const TopkLayout T = topk_layout(n1, n2, batch, k);
+  WT_REQUIRE(k >= 1 && k <= T.n && nvec >= 0 && nvec <= k, "svd_topk: k = %lld, nvec = %lld for min(n1, n2) = %lld",
+             (long long)k, (long long)nvec, (long long)T.n);
+  WT_REQUIRE(T.n >= 3 && T.n <= 2048, "svd_topk: min(n1, n2) = %lld outside [3, 2048]", (long long)T.n);
+  WT_REQUIRE(lda >= n2, "svd_topk: lda < n2");
+  WT_REQUIRE(workspace != nullptr && workspace_bytes >= T.total, "svd_topk: workspace too small (%zu < %zu)",
+             workspace_bytes, T.total);
+  cudaStream_t st = (cudaStream_t)stream;
+  char* base = static_cast<char*>(workspace);
+  double* X = reinterpret_cast<double*>(base + T.off_X);
+  double* scale = reinterpret_cast<double*>(base + T.off_scale);
+  double* X1 = reinterpret_cast<double*>(base + T.off_X1);
+  const bool right = n1 <= n2;
+  svd_absmax_scale<<<(unsigned)batch, 256, 0, st>>>(A, lda, strideA, n1, n2, scale);
+  {
+    dim3 grid((unsigned)std::min<int64_t>((T.npad * T.mpad + 255) / 256, 4096), (unsigned)batch);
+    svd_copy_in<<<grid, 256, 0, st>>>(A, lda, strideA, right, T.m, T.n, T.mpad, T.npad, scale, X);
+    if (int e = check_launch("svd_topk copy-in")) return e;
+  }
+  int fallback = 0;
+  if (int e = eig_precondition(X, X1, T.mpad, T.n, T.mpad, T.npad * T.mpad, batch, k, T.mpad, k * T.mpad,
+                               base + T.off_eig, T.eig_bytes, &fallback, st))
+    return e;
+  // rows of X1 are the k columns of X V0: the Jacobi on that (k x m) row-major matrix,
+  // right side: its long-side vectors are X's (A's long side), its sigma X V0's
+  if (int e = jacobi(X1, T.mpad, k * T.mpad, k, T.m, batch, sigma, vec, nvec, info, tol, max_sweeps,
+                     base + T.off_inner, T.inner.total, stream, false))
+    return e;
+  g_last_fallbacks = fallback;
+  svd_unscale<<<(unsigned)std::min<int64_t>((batch * k + 255) / 256, 4096), 256, 0, st>>>(sigma, k, batch, scale);
+  return check_launch("svd_topk unscale");
+}
 }  // namespace SVD_NS
 }  // namespace wt

@@ -26,14 +26,16 @@ int gemm_f64_lim(int transA, int transB, int64_t M, int64_t N, int64_t K, double
                  int64_t strideB, double beta, double* C, int64_t ldc, int64_t strideC,
                  int64_t batch, const int* klim, const int* nlim, void* stream, int lower = 0);
 
-// K4 preconditioner (eig.cu): replaces the columns of the batch of m x n
-// matrices Xt (row r of Xt = column r of X, pitch ldx, stride sx; n <= m) by
-// those of X V0, V0 = the eigenbasis of X^T X (Householder tridiagonalization,
-// bisection, inverse iteration, Newton-Schulz), written to Yt (same layout).
-// Matrices whose basis fails the orthogonality check get V0 = I.
+// K4 preconditioner (eig.cu): for the batch of m x n matrices X given as Xt
+// (row r of Xt = column r of X, pitch ldx, stride sx; n <= m) writes the kk
+// columns of X V0 as the rows of Yt (pitch ldy, stride sy), V0 = the kk leading
+// eigenvectors of X^T X (Householder tridiagonalization, bisection, inverse
+// iteration, Newton-Schulz), descending.  Matrices whose basis fails the
+// orthogonality check get V0 = I[:, :kk].
 size_t eig_workspace_bytes(int64_t n, int64_t batch);
 int eig_precondition(const double* Xt, double* Yt, int64_t m, int64_t n, int64_t ldx, int64_t sx,
-                     int64_t batch, void* ws, size_t ws_bytes, int* n_fallback, cudaStream_t st);
+                     int64_t batch, int64_t kk, int64_t ldy, int64_t sy, void* ws, size_t ws_bytes, int* n_fallback,
+                     cudaStream_t st);
 // wt_scale_cols_f64 with an optional per-matrix column limit (columns >= clim[b] untouched).
 int scale_cols_lim(double* M, int64_t rows, int64_t ncols, int64_t ld, int64_t strideM,
                    const double* s, int64_t q, int64_t batch, int mode, double tol,

@@ -135,9 +135,7 @@ def sp_w_svd_device(x: torch.Tensor, r: int, levels: int, tol: float = 0.0,
     base = p - 2 * m
     mask = E.level_mask(levels, smooth=True, details=[levels])
     coarse = E.lift_forward(x, levels, mask=mask, slice_base=base)   # (2m, n1, n2)
-    sigma, vec, info = E.svd(coarse, r, tol=tol)
-    E.raise_if_failed(info)
-    rec = E.truncated_recon(coarse, sigma, vec, r)
+    rec = E.svd_truncated_recon(coarse, r, tol=tol)                  # K4 (leading triplets) + K5
     return E.lift_inverse(rec, n1, n2, p, levels, mask=mask, slice_base=base, out=out)
 
 
@@ -146,9 +144,7 @@ _STREAM_MIN_BYTES = 64 << 20  # host cubes from this size stream through the GPU
 
 def _coarse_truncate(r, tol=0.0):
     def decompose(coarse):
-        sigma, vec, info = E.svd(coarse, r, tol=tol)
-        E.raise_if_failed(info)
-        return E.truncated_recon(coarse, sigma, vec, r)
+        return E.svd_truncated_recon(coarse, r, tol=tol)
     return decompose
 
 

@@ -518,6 +518,47 @@ def svd(a: torch.Tensor, nvec: int, tol: float = 0.0, max_sweeps: int = 0):
     return sigma, vec, info
 
 
+def svd_topk(a: torch.Tensor, k: int, nvec: int, tol: float = 0.0, max_sweeps: int = 0):
+    """K4, the k leading singular triplets of every (n1, n2) slice (wt_svd_topk_f64):
+    (sigma (batch, k) descending, vec (batch, nvec, max(n1, n2)), info)."""
+    lib = N.require_gpu()
+    batch, n1, n2 = a.shape
+    assert a.stride(2) == 1 and 1 <= nvec <= k
+    ln = max(n1, n2)
+    sigma = torch.empty((batch, k), dtype=F64, device=a.device)
+    vec = torch.empty((batch, nvec, ln), dtype=F64, device=a.device)
+    info = torch.empty((batch,), dtype=torch.int32, device=a.device)
+    if batch == 0:
+        return sigma, vec, info
+    wsb = int(lib.wt_svd_topk_workspace_bytes(n1, n2, batch, k))
+    ws = torch.empty((wsb,), dtype=torch.uint8, device=a.device)
+    N.check(lib.wt_svd_topk_f64(_ptr(a), a.stride(1), a.stride(0), n1, n2, batch, k, _ptr(sigma), _ptr(vec), nvec,
+                                _ptr(info), float(tol), int(max_sweeps), _ptr(ws), wsb, _stream()),
+            "wt_svd_topk_f64")
+    return sigma, vec, info
+
+
+def topk_width(q: int, r: int) -> int:
+    """Leading triplets computed for a rank-r truncation of slices with q = min(n1, n2):
+    k = max(64, 2r) rounded up to 32 when that is at most q / 2 (else 0: full SVD)."""
+    k = max(64, (2 * r + 31) // 32 * 32)
+    return k if q >= 256 and k <= q // 2 else 0
+
+
+def svd_truncated_recon(a: torch.Tensor, r: int, out: torch.Tensor | None = None, tol: float = 0.0) -> torch.Tensor:
+    """Rank-r reconstruction of every slice (_stack_svd + _truncated_blocks,
+    decomposition.py:64-72): K4 on the k leading triplets when k = topk_width(q, r)
+    applies, the full K4 otherwise, then K5."""
+    batch, n1, n2 = a.shape
+    k = topk_width(min(n1, n2), r)
+    if k:
+        sigma, vec, info = svd_topk(a, k, r, tol=tol)
+    else:
+        sigma, vec, info = svd(a, r, tol=tol)
+    raise_if_failed(info)
+    return truncated_recon(a, sigma, vec, r, out=out)
+
+
 def last_sweeps() -> int:
     return int(N.load().wt_svd_last_sweeps())
 

@@ -59,9 +59,7 @@ class CudaOps:
     def truncated(self, slices, r):
         if slices.shape[0] == 0:
             return self.empty(slices.shape)
-        sigma, vec, info = E.svd(slices, r)
-        E.raise_if_failed(info)
-        return E.truncated_recon(slices, sigma, vec, r)
+        return E.svd_truncated_recon(slices, r)
 
     def pinv(self, slices, tol):
         k, n1, n2 = slices.shape
@@ -354,9 +352,7 @@ def sp_w_svd_fused(x_local, r, levels, n1, group=None, phase_times=False):
     m = p >> levels
 
     def decompose(full, out):
-        sigma, vec, info = E.svd(full, r)
-        E.raise_if_failed(info)
-        E.truncated_recon(full, sigma, vec, r, out=out)
+        E.svd_truncated_recon(full, r, out=out)
 
     mask = E.level_mask(levels, smooth=True, details=[levels])
     phases = {} if phase_times else None

@@ -169,3 +169,25 @@ def test_inverse_tensor_follows_lu_semantics():
     with pytest.raises(ValueError) as e2:
         O.inverse_tensor(sing, 1)
     assert (e.value.level, e.value.slice_index) == e2.value.args[0]
+
+
+def test_one_call_w_product_graph_replay():
+    """wt_w_product_f64: repeated calls with the same arguments replay a captured CUDA
+    graph; the graph reads the buffers at replay time (in-place input updates are seen),
+    and new arguments run eagerly.  Every result equals the oracle."""
+    from paper_2601_08228_b200.algebra import w_product_device
+
+    rng = np.random.default_rng(12)
+    a = rng.uniform(-1, 1, (20, 12, 16))
+    b = rng.uniform(-1, 1, (12, 9, 16))
+    ad, bd = torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()
+    out = torch.empty((20, 9, 16), dtype=torch.float64, device="cuda")
+    for _ in range(4):  # eager, eager + capture, replay, replay
+        w_product_device(ad, bd, 2, out=out)
+        assert relerr(out.cpu().numpy(), O.w_product(a, b, 2)) < 1e-13
+    a2 = rng.uniform(-1, 1, a.shape)
+    ad.copy_(torch.from_numpy(a2))  # same pointer, new data
+    w_product_device(ad, bd, 2, out=out)
+    assert relerr(out.cpu().numpy(), O.w_product(a2, b, 2)) < 1e-13
+    fresh = w_product_device(bd.transpose(0, 1).contiguous(), ad.transpose(0, 1).contiguous(), 2)
+    assert relerr(fresh.cpu().numpy(), O.w_product(np.swapaxes(b, 0, 1), np.swapaxes(a2, 0, 1), 2)) < 1e-13

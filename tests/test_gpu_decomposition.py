@@ -318,3 +318,28 @@ def test_sp_pinv_w_empty():
     for shape in [(0, 3, 4), (3, 0, 4)]:
         out = W.sp_pinv_w(np.zeros(shape), 1)
         assert out.shape == (shape[1], shape[0], shape[2]) and not out.any()
+
+
+@pytest.mark.parametrize("shape,r", [((6, 256, 256), 20), ((3, 300, 512), 30), ((2, 520, 256), 8)])
+def test_topk_truncation_matches_full_and_lapack(shape, r):
+    """K4's leading-triplet mode (wt_svd_topk_f64, used by sp_w_svd's rank-r truncation):
+    the k leading singular values equal the full K4's / LAPACK's, the rank-r
+    reconstruction equals the full path's and LAPACK's; graded and noise-like slices."""
+    rng = np.random.default_rng(sum(shape) + r)
+    a = rng.standard_normal(shape)
+    a[0] = (np.linalg.qr(rng.standard_normal((shape[1], shape[1])))[0][:, :min(shape[1:])]
+            * np.logspace(0, -9, min(shape[1:]))) @ np.linalg.qr(rng.standard_normal((shape[2], min(shape[1:]))))[0].T
+    at = torch.from_numpy(a).cuda()
+    k = E.topk_width(min(shape[1:]), r)
+    assert k >= 2 * r
+    s_k, v_k, info = E.svd_topk(at, k, r)
+    E.raise_if_failed(info)
+    ref = np.linalg.svd(a, compute_uv=False)
+    assert np.max(np.abs(s_k.cpu().numpy() - ref[:, :k]) / ref[:, :1]) < 1e-12
+    rec = E.svd_truncated_recon(at, r).cpu().numpy()
+    u, s, vh = np.linalg.svd(a, full_matrices=False)
+    want = u[:, :, :r] @ (s[:, :r, None] * vh[:, :r, :])
+    assert relerr(rec, want) < 1e-10
+    s_f, v_f, _ = E.svd(at, r)
+    full = E.truncated_recon(at, s_f, v_f, r).cpu().numpy()
+    assert relerr(rec, full) < 1e-10
