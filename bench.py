@@ -378,7 +378,11 @@ def headline_single(args, x_host, sampler):
     # e2e: the public API on host (numpy) arrays -- H2D of the cube and D2H of the
     # reconstruction inside every call (decomposition.sp_w_svd)
     e2e_steps = max(1, min(args.steps, 5))
-    W.sp_w_svd(x_host, r, L)
+    # warm-up as in the timed loop (the previous result alive while the next call
+    # runs): the caching host allocator then holds both pinned result blocks (a
+    # fresh 2 GiB cudaHostAlloc costs ~0.9 s once)
+    y_host = W.sp_w_svd(x_host, r, L)
+    y_host = W.sp_w_svd(x_host, r, L)
     torch.cuda.synchronize()
     t = time.perf_counter()
     for _ in range(e2e_steps):
@@ -503,9 +507,11 @@ def transform_key(args, dist, rank, ws, with_cpu):
                                                       "frac": round(af / peak, 4)},
                                        "K2_inverse": {"ms": round(i_ms, 4), "GBps": round(ai, 1),
                                                       "frac": round(ai / peak, 4)}}}}
-    # public API on host arrays (pyramid returned to the host, then inverted from it)
-    for L in CFG2_LEVELS:
-        W.inverse_w(W.forward_w(x_host, L))
+    # public API on host arrays (pyramid returned to the host, then inverted from it);
+    # two warm-up passes fill the caching host allocator's pinned blocks
+    for _ in range(2):
+        for L in CFG2_LEVELS:
+            W.inverse_w(W.forward_w(x_host, L))
     t = time.perf_counter()
     for L in CFG2_LEVELS:
         o = W.inverse_w(W.forward_w(x_host, L))
