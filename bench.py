@@ -640,6 +640,7 @@ def deblur_workload(args, steps=2, warmup=1):
     k3 = ev[0].elapsed_time(ev[1]) / 5
     peak, src = fp64_peak()
     svd_f = 2 * 128 * svd_flops(512, 512)
+    nz_f = 2 * 16 * svd_flops(512, 512)  # slice-constant operators: 16 nonzero (smooth) wavelet slices each
     gemm_f = 2 * 512 ** 3 * 128
     xr = res["x"].cpu().numpy()
     b_host = b.cpu().numpy()
@@ -663,11 +664,14 @@ def deblur_workload(args, steps=2, warmup=1):
                              "8-band means and the 9x9 sigma=2 Toeplitz operators amplify the noise up to 1e3x "
                              "per side: the recovery is poor by construction of the config"),
             "roofline_k4_pinv": {"bound": "tensor", "kernel": "K4 on both operators' 256 wavelet slices of 512^2 "
-                                 "(224 exactly zero: retired at the first sort)",
-                                 "achieved": round(svd_f / (k4 * 1e-3) / 1e12, 3), "peak": peak, "unit": "TFLOP/s",
-                                 "frac": round(svd_f / (k4 * 1e-3) / 1e12 / peak, 4), "peak_source": src,
+                                 "(224 exactly zero: retired before any work)",
+                                 "achieved": round(nz_f / (k4 * 1e-3) / 1e12, 3), "peak": peak, "unit": "TFLOP/s",
+                                 "frac": round(nz_f / (k4 * 1e-3) / 1e12 / peak, 4), "peak_source": src,
                                  "k4_ms_per_call": round(k4, 3),
-                                 "flops_model": "2 x 128 x (14 m n^2 + 8 n^3), dense as the reference executes it"},
+                                 "flops_model": "32 nonzero slices x (14 m n^2 + 8 n^3), m = n = 512",
+                                 "effective_frac_dense": round(svd_f / (k4 * 1e-3) / 1e12 / peak, 4),
+                                 "effective_note": "on the dense count the reference executes (2 x 128 slices, the "
+                                                   "zero ones included)"},
             "roofline_k3_face_gemm": {"bound": "tensor", "kernel": "K3 face GEMM (128 x 512^3 per w-product)",
                                       "achieved": round(gemm_f / (k3 * 1e-3) / 1e12, 3) if k3 else None,
                                       "peak": peak, "unit": "TFLOP/s",
