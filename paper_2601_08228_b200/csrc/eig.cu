@@ -41,7 +41,7 @@
 namespace wt {
 namespace eig {
 
-constexpr int NB = 32;     // tridiagonalization panel width
+constexpr int NB_MAX = 32;  // tridiagonalization panel width: 16 or 32 (panel_shape)
 constexpr int NBT = 128;   // back-transformation block (reflectors per compact-WY block)
 constexpr int PT = 256;    // panel kernel threads
 constexpr int NW = PT / 32;
@@ -55,10 +55,9 @@ constexpr int CH = WT_EIG_CH;  // symv column chunk (CH / 64 double2 register ac
 constexpr int NCH2 = CH / 64;
 constexpr int RB = WT_EIG_RB;  // rows per warp in flight in the symv
 static_assert(RB == 4, "the symv's row-sum reduction handles exactly 4 rows per warp");
-static_assert(CH >= 2 * NB + 1, "the y partials alias the symv's per-warp accumulators");
+static_assert(CH >= 2 * NB_MAX + 1, "the y partials alias the symv's per-warp accumulators");
 constexpr int MAXR = 256;  // own rows per CTA (the panel's V, W rows of a CTA live in shared memory)
 constexpr int PREF_R = 128;  // preferred own rows per CTA (two CTAs per SM)
-constexpr int VP = 2 * NB + 2;  // shared pitch of a [V | W] row (even: 16-byte aligned rows)
 
 __device__ __forceinline__ void cl_sync() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
@@ -99,8 +98,9 @@ __device__ __forceinline__ double block_sum(double v, double* red) {
 }
 
 struct PanelSmem {
-  static size_t bytes(int n, int C) {
+  static size_t bytes(int n, int C, int NB) {
     const int R = (n + C - 1) / C;
+    const int VP = 2 * NB + 2;
     return sizeof(double) * ((size_t)R * VP + 10 + 3 * (size_t)n + 2 + 2 * (size_t)R + (size_t)NW * CH + 4 + 2 +
                              2 * NB + 2 * NW + 7 * NB);
   }
@@ -121,11 +121,13 @@ struct PanelSmem {
 // norm partials; every CTA then forms the whole v from the owners' entries)
 // and S3 (symv partials); w of row k+1, needed by every CTA's next lazy
 // update, is evaluated redundantly by every CTA with its owner's expression.
-template <int C>
+template <int C, int NB>
 __global__ void __launch_bounds__(PT, 2) tridiag_panel(double* __restrict__ Gall, double* __restrict__ VWall,
                                                     double* __restrict__ WVall, double* __restrict__ dall,
                                                     double* __restrict__ eall, double* __restrict__ tauall,
                                                     const int* __restrict__ flag, int n, int k0) {
+  static_assert(NB == 16 || NB == 32, "panel width");
+  constexpr int VP = 2 * NB + 2;  // shared pitch of a [V | W] row (even: 16-byte aligned rows)
   extern __shared__ __align__(16) double sm[];
   const int R = (n + C - 1) / C;  // local rows (upper bound)
   double* vws = sm;                    // [R][VP]  my rows of [V | W]
@@ -323,8 +325,10 @@ __global__ void __launch_bounds__(PT, 2) tridiag_panel(double* __restrict__ Gall
           const int i = row_of(qb + r);
           const double vi = qb + r < nloc ? vsm[i] : 0.0;
           if (cb == cstart && qb + r < nloc) {  // every row >= k+1 is visited in the first chunk
+            // NB = 32: lane t sums V[i][t] v_i and W[i][t] v_i; NB = 16: lane t < 32
+            // sums column t of the contiguous [V | W] row
             yv_l = fma(vws[(qb + r) * VP + lane], vi, yv_l);
-            yw_l = fma(vws[(qb + r) * VP + NB + lane], vi, yw_l);
+            if constexpr (NB == 32) yw_l = fma(vws[(qb + r) * VP + NB + lane], vi, yw_l);
           }
           rp[r] = 0.0;
 #pragma unroll
@@ -377,8 +381,12 @@ __global__ void __launch_bounds__(PT, 2) tridiag_panel(double* __restrict__ Gall
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) pv_own += __shfl_xor_sync(0xffffffffu, pv_own, o);
-    ywacc[warp * (2 * NB + 1) + lane] = yw_l;          // yW[t] partials (t = lane)
-    ywacc[warp * (2 * NB + 1) + NB + lane] = yv_l;     // yV[t]
+    if constexpr (NB == 32) {
+      ywacc[warp * (2 * NB + 1) + lane] = yw_l;          // yW[t] partials (t = lane)
+      ywacc[warp * (2 * NB + 1) + NB + lane] = yv_l;     // yV[t]
+    } else {  // lane < NB: yV[lane], lane >= NB: yW[lane - NB]
+      ywacc[warp * (2 * NB + 1) + (lane < NB ? NB + lane : lane - NB)] = yv_l;
+    }
     if (lane == 0) ywacc[warp * (2 * NB + 1) + 2 * NB] = pv_own;
     __syncthreads();
     for (int t = tid; t <= 2 * NB; t += PT) {
@@ -905,8 +913,8 @@ Layout layout(int64_t n, int64_t batch) {
   L.Z = take(nn);
   L.Z2 = take(nn);
   L.P = take(nn);  // also the inverse-iteration L factors; Z2 holds their 1/D
-  L.VW = take(sizeof(double) * (size_t)(batch * n * 2 * NB));
-  L.WV = take(sizeof(double) * (size_t)(batch * n * 2 * NB));
+  L.VW = take(sizeof(double) * (size_t)(batch * n * 2 * NB_MAX));
+  L.WV = take(sizeof(double) * (size_t)(batch * n * 2 * NB_MAX));
   L.d = take(sizeof(double) * (size_t)(batch * n));
   L.e = take(sizeof(double) * (size_t)(batch * n));
   L.e2 = take(sizeof(double) * (size_t)(batch * n));
@@ -927,11 +935,31 @@ Layout layout(int64_t n, int64_t batch) {
   return L;
 }
 
-template <int C>
+// Cluster size C and panel width NB of the tridiagonalization for n x n Grams.
+// A function of n only (the cluster split changes the summation order, so a
+// matrix gets the same bits in any batch).  At most MAXR rows per CTA (the
+// panel's V and W rows of a CTA stay in shared memory); NB = 16 halves that
+// shared footprint so 256-row CTAs still fit two per SM.
+struct PanelShape {
+  int C, NB;
+};
+PanelShape panel_shape(int64_t n) {
+  // 129..256: one 256-row CTA per matrix, no cluster barriers (config 3: 192 x
+  // 256^2 runs as one wave of 192 CTAs; the 2-CTA clusters of width-32 panels
+  // needed two waves: K4 9.05 vs 11.24 ms, tools/panel_probe.py)
+  if (n > PREF_R && n <= MAXR) return PanelShape{1, 16};
+  // otherwise >= 128 rows per CTA at width 32 (n = 512: C = 4 17.0 ms vs C = 2,
+  // NB = 16 18.9 ms on 64 x 512^2; n = 1024: C = 8 60.8 ms vs C = 4 69.4 ms)
+  int C = 1;
+  while (C < 8 && n > (int64_t)C * PREF_R) C *= 2;
+  return PanelShape{C, 32};
+}
+
+template <int C, int NB>
 int launch_panel(double* G, double* VW, double* WV, double* d, double* e, double* tau, const int* flag, int n,
                  int k0, int64_t batch, cudaStream_t st) {
-  auto kern = tridiag_panel<C>;
-  const size_t smem = PanelSmem::bytes(n, C);
+  auto kern = tridiag_panel<C, NB>;
+  const size_t smem = PanelSmem::bytes(n, C, NB);
   if (int r = ensure_smem(kern, smem)) return r;
   cudaLaunchConfig_t cfg = {};
   cudaLaunchAttribute attr[1];
@@ -990,21 +1018,19 @@ int eig_precondition(const double* Xt, double* Yt, int64_t m, int64_t n, int64_t
     return r;
   gram_flag<<<(unsigned)batch, PT, 0, st>>>(G, ni, flag, glim);
   mark();
+  const PanelShape ps = panel_shape(n);
+  const int C = ps.C, NB = ps.NB;
   WT_CUDA(cudaMemsetAsync(VW, 0, sizeof(double) * (size_t)(batch * n * 2 * NB), st));
   WT_CUDA(cudaMemsetAsync(WV, 0, sizeof(double) * (size_t)(batch * n * 2 * NB), st));
-  // cluster size: enough CTAs per matrix to occupy the SMs, >= 64 rows per CTA
-  // (at most MAXR rows per CTA: the panel's rows of V and W stay in shared memory)
-  // (C depends on n only, so that a matrix gets the same bits in any batch)
-  int C = 1;
-  while (C < 8 && n > (int64_t)C * PREF_R) C *= 2;
   // 2. tridiagonalization, panel by panel
   for (int64_t k0 = 0; k0 < n; k0 += NB) {
     int r = WT_OK;
-    switch (C) {
-      case 8: r = launch_panel<8>(G, VW, WV, dd, ee, tau, flag, ni, (int)k0, batch, st); break;
-      case 4: r = launch_panel<4>(G, VW, WV, dd, ee, tau, flag, ni, (int)k0, batch, st); break;
-      case 2: r = launch_panel<2>(G, VW, WV, dd, ee, tau, flag, ni, (int)k0, batch, st); break;
-      default: r = launch_panel<1>(G, VW, WV, dd, ee, tau, flag, ni, (int)k0, batch, st);
+    switch (C * 100 + NB) {
+      case 832: r = launch_panel<8, 32>(G, VW, WV, dd, ee, tau, flag, ni, (int)k0, batch, st); break;
+      case 432: r = launch_panel<4, 32>(G, VW, WV, dd, ee, tau, flag, ni, (int)k0, batch, st); break;
+      case 232: r = launch_panel<2, 32>(G, VW, WV, dd, ee, tau, flag, ni, (int)k0, batch, st); break;
+      case 116: r = launch_panel<1, 16>(G, VW, WV, dd, ee, tau, flag, ni, (int)k0, batch, st); break;
+      default: r = launch_panel<1, 32>(G, VW, WV, dd, ee, tau, flag, ni, (int)k0, batch, st);
     }
     if (r) return r;
     const int64_t k1 = k0 + NB;

@@ -39,7 +39,7 @@ struct SvdWs {
   int* ticket;      // 1 counter: next visit of the current sweep (persistent sweeps)
   int* bver;        // batch * nblk: version of every column block (bumped when its data changes)
   unsigned long long* pclean;  // batch * nblk * nblk: (ver_I, ver_J) when pair (I, J) last tested clean
-  double* scale;    // batch: power-of-two input scale (svd_absmax_scale)
+  double* scale;    // batch: power-of-two input scale (absmax_scale)
 };
 
 __host__ __device__ inline int64_t round_up(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
@@ -53,27 +53,42 @@ __device__ __forceinline__ double* mat_ptr(const SvdWs& ws, int64_t b, int64_t n
 // entries the iteration forms (squares of the data) then stay far from the
 // subnormal / overflow ranges, as LAPACK's dgesdd scales out-of-range inputs.
 // The singular values are scaled back at the end (exact: powers of two).
-__global__ void svd_absmax_scale(const double* __restrict__ A, int64_t lda, int64_t sA, int64_t n1,
-                                 int64_t n2, double* __restrict__ scale) {
-  const int64_t b = blockIdx.x;
-  double mx = 0.0;
-  for (int64_t e = threadIdx.x; e < n1 * n2; e += blockDim.x) {
-    const double v = fabs(A[b * sA + (e / n2) * lda + e % n2]);
-    mx = (v > mx || isnan(v)) ? v : mx;
+// (two kernels: a grid over row blocks of every matrix max-reduces |A| into the
+// scale slot as IEEE bits -- non-negative doubles and NaN order as unsigned
+// integers -- then one thread per matrix turns the maximum into the scale)
+__global__ void svd_absmax_part(const double* __restrict__ A, int64_t lda, int64_t sA, int64_t n1, int64_t n2,
+                                unsigned long long* __restrict__ bits) {
+  const int64_t b = blockIdx.y;
+  unsigned long long mx = 0ull;
+  for (int64_t row = blockIdx.x; row < n1; row += gridDim.x) {
+    const double* a = A + b * sA + row * lda;
+    for (int64_t c = threadIdx.x; c < n2; c += blockDim.x) {
+      const unsigned long long v = (unsigned long long)__double_as_longlong(fabs(a[c]));
+      mx = v > mx ? v : mx;
+    }
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
-    const double t = __shfl_xor_sync(0xffffffffu, mx, o);
-    mx = (t > mx || isnan(t)) ? t : mx;
+    const unsigned long long t = __shfl_xor_sync(0xffffffffu, mx, o);
+    mx = t > mx ? t : mx;
   }
-  __shared__ double red[32];
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) mx = (red[w] > mx || isnan(red[w])) ? red[w] : mx;
-    mx = fmax(mx, red[0]);
-    scale[b] = (mx > 0.0 && isfinite(mx)) ? ldexp(1.0, -ilogb(mx)) : 1.0;
-  }
+  if ((threadIdx.x & 31) == 0 && mx) atomicMax(bits + b, mx);
+}
+
+__global__ void svd_absmax_final(double* __restrict__ scale, int64_t batch) {
+  const int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (b >= batch) return;
+  const double mx = __longlong_as_double((long long)reinterpret_cast<const unsigned long long*>(scale)[b]);
+  scale[b] = (mx > 0.0 && isfinite(mx)) ? ldexp(1.0, -ilogb(mx)) : 1.0;
+}
+
+int absmax_scale(const double* A, int64_t lda, int64_t sA, int64_t n1, int64_t n2, int64_t batch, double* scale,
+                 cudaStream_t st) {
+  WT_CUDA(cudaMemsetAsync(scale, 0, sizeof(double) * (size_t)batch, st));
+  dim3 grid((unsigned)std::min<int64_t>(n1, std::max<int64_t>(1, 2048 / std::max<int64_t>(batch, 1))), (unsigned)batch);
+  svd_absmax_part<<<grid, 256, 0, st>>>(A, lda, sA, n1, n2, reinterpret_cast<unsigned long long*>(scale));
+  svd_absmax_final<<<(unsigned)((batch + 255) / 256), 256, 0, st>>>(scale, batch);
+  return check_launch("svd absmax scale");
 }
 
 __global__ void svd_copy_in(const double* __restrict__ A, int64_t lda, int64_t sA, bool right,
@@ -963,7 +978,7 @@ int jacobi(const double* A, int64_t lda, int64_t strideA, int64_t n1,
 
   {
     dim3 grid((unsigned)std::min<int64_t>((L.npad * L.mpad + 255) / 256, 4096), (unsigned)batch);
-    svd_absmax_scale<<<(unsigned)batch, 256, 0, st>>>(A, lda, strideA, n1, n2, ws.scale);
+    if (int e = absmax_scale(A, lda, strideA, n1, n2, batch, ws.scale, st)) return e;
     svd_copy_in<<<grid, 256, 0, st>>>(A, lda, strideA, right, L.m, L.n, L.mpad, L.npad, ws.scale, ws.X);
     if (int e = check_launch("svd_copy_in")) return e;
   }
@@ -1216,7 +1231,7 @@ int jacobi_topk(const double* A, int64_t lda, int64_t strideA, int64_t n1, int64
   double* scale = reinterpret_cast<double*>(base + T.off_scale);
   double* X1 = reinterpret_cast<double*>(base + T.off_X1);
   const bool right = n1 <= n2;
-  svd_absmax_scale<<<(unsigned)batch, 256, 0, st>>>(A, lda, strideA, n1, n2, scale);
+  if (int e = absmax_scale(A, lda, strideA, n1, n2, batch, scale, st)) return e;
   {
     dim3 grid((unsigned)std::min<int64_t>((T.npad * T.mpad + 255) / 256, 4096), (unsigned)batch);
     svd_copy_in<<<grid, 256, 0, st>>>(A, lda, strideA, right, T.m, T.n, T.mpad, T.npad, scale, X);
