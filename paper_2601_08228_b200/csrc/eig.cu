@@ -630,6 +630,47 @@ __global__ void tri_bisect(const double* __restrict__ dall, const double* __rest
   lam[(int64_t)b * n + j] = 0.5 * (lo + hi);
 }
 
+// The same with one warp per eigenvalue (multisection), for few eigenvalues
+// (kk <= 128: the leading-triplet mode), where one thread per eigenvalue leaves
+// the GPU nearly idle: every round the 32 lanes take Sturm counts at 32
+// equispaced interior points of the bracket, which shrinks 33-fold to the
+// sub-interval where the count crosses j (~10 rounds instead of ~50 bisection
+// steps; all lanes read the same d, e2 entries: shared-memory broadcasts).
+__global__ void tri_multisect(const double* __restrict__ dall, const double* __restrict__ e2all,
+                              const double* __restrict__ info, const int* flag, int n, int kk,
+                              double* __restrict__ lam) {
+  extern __shared__ double tsm[];  // d[n], e2[n]
+  const int b = blockIdx.y;
+  if (!flag[b]) return;
+  double* ds = tsm;
+  double* e2s = tsm + n;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    ds[i] = dall[(int64_t)b * n + i];
+    e2s[i] = i < n - 1 ? e2all[(int64_t)b * n + i] : 0.0;
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const double span = info[b * 4 + 2];
+  const double tol = 4.0 * 2.220446049250313e-16 * span;
+  const double pivmin = 1e-30 * span + 1e-300;
+  for (int jj = blockIdx.x * nw + (threadIdx.x >> 5); jj < kk; jj += gridDim.x * nw) {
+    const int j = n - kk + jj;  // the kk largest eigenvalues
+    double lo = info[b * 4 + 0], hi = info[b * 4 + 1];
+    for (int it = 0; it < 24 && hi - lo > tol; ++it) {
+      const double h = (hi - lo) * (1.0 / 33.0);
+      const double x = fma((double)(lane + 1), h, lo);
+      // lanes whose point lies at or below lambda_j: a prefix (counts are monotone in x)
+      const unsigned below = __ballot_sync(0xffffffffu, sturm_count(ds, e2s, n, x, pivmin) <= j);
+      const int L = 32 - __clz(below);  // points 1..L are <= lambda_j
+      const double nlo = L > 0 ? fma((double)L, h, lo) : lo;
+      const double nhi = L < 32 ? fma((double)(L + 1), h, lo) : hi;
+      lo = nlo;
+      hi = nhi;
+    }
+    if (lane == 0) lam[(int64_t)b * n + j] = 0.5 * (lo + hi);
+  }
+}
+
 __device__ __forceinline__ double hash_unit(uint32_t i, uint32_t j) {
   uint32_t h = i * 0x9E3779B1u ^ (j + 0x7F4A7C15u) * 0x85EBCA77u;
   h ^= h >> 15;
@@ -858,36 +899,53 @@ __global__ void ns_form(double* __restrict__ Pall, const double* __restrict__ Qa
 // Compact-WY factor T (NBT x NBT upper triangular) of the block of reflectors
 // Y (columns k0 .. k0 + nb - 1 of the stored panels), from S = Y^T Y:
 // T_ii = tau_i, T[0:i, i] = -tau_i T[0:i, 0:i] S[0:i, i]   (dlarft, forward, columnwise)
+// The strict upper triangle of S is staged transposed in T's free strict lower
+// triangle (S[c][i] at T[i][c]) before the column recurrence, so the recurrence
+// reads only shared memory.
 __global__ void wy_larft(const double* __restrict__ Sall, const double* __restrict__ tauall, const int* flag,
                          int n, int k0, int nb, double* __restrict__ Tall) {
   const int b = blockIdx.x;
   if (!flag[b]) return;
-  extern __shared__ double T[];  // [NBT][NBT + 1], then column i of S [NBT]
-  double* Sc = T + NBT * (NBT + 1);
+  extern __shared__ double T[];  // [NBT][NBT + 1]
+  constexpr int LD = NBT + 1;
   const double* S = Sall + (int64_t)b * NBT * NBT;
   const double* tau = tauall + (int64_t)b * n + k0;
-  for (int e = threadIdx.x; e < NBT * NBT; e += blockDim.x) T[(e / NBT) * (NBT + 1) + e % NBT] = 0.0;
-  for (int i = 0; i < nb; ++i) {
-    const double ti = tau[i];
-    const int r = threadIdx.x;
-    Sc[r] = r < i ? S[r * NBT + i] : 0.0;  // column i of S = Y^T Y
-    __syncthreads();
-    double s0 = 0.0, s1 = 0.0;
-    if (r < i) {
-      int c = r;
-      for (; c + 1 < i; c += 2) {
-        s0 = fma(T[r * (NBT + 1) + c], Sc[c], s0);
-        s1 = fma(T[r * (NBT + 1) + c + 1], Sc[c + 1], s1);
-      }
-      if (c < i) s0 = fma(T[r * (NBT + 1) + c], Sc[c], s0);
-    }
-    __syncthreads();
-    if (r < i) T[r * (NBT + 1) + i] = -ti * (s0 + s1);
-    if (r == i) T[r * (NBT + 1) + i] = ti;
+  for (int e = threadIdx.x; e < NBT * NBT; e += blockDim.x) {
+    const int r = e / NBT, c = e % NBT;  // S[r][c], coalesced over c
+    T[c * LD + r] = (r < c && c < nb) ? S[e] : 0.0;
   }
   __syncthreads();
+  // four threads per row r (lanes 4r' .. 4r'+3 of a warp), each summing every
+  // fourth term of the row's dot product (chains a quarter as long), combined
+  // by two shuffles in a fixed order
+  const int r = threadIdx.x >> 2, part = threadIdx.x & 3;
+  for (int i = 0; i < nb; ++i) {
+    double s0 = 0.0, s1 = 0.0;
+    if (r < i) {
+      const double* Tr = T + r * LD;
+      const double* Si = T + i * LD;  // S[c][i] = T[i][c], c < i
+      int c = r + part;
+      for (; c + 4 < i; c += 8) {
+        s0 = fma(Tr[c], Si[c], s0);
+        s1 = fma(Tr[c + 4], Si[c + 4], s1);
+      }
+      if (c < i) s0 = fma(Tr[c], Si[c], s0);
+    }
+    double sum = s0 + s1;
+    sum += __shfl_xor_sync(0xffffffffu, sum, 1);
+    sum += __shfl_xor_sync(0xffffffffu, sum, 2);
+    __syncthreads();  // every thread has read column i's inputs (row r of T left of i, row i of S)
+    if (part == 0) {
+      if (r < i) T[r * LD + i] = -tau[i] * sum;
+      if (r == i) T[r * LD + i] = tau[i];
+    }
+    __syncthreads();
+  }
   double* Tg = Tall + (int64_t)b * NBT * NBT;
-  for (int e = threadIdx.x; e < NBT * NBT; e += blockDim.x) Tg[e] = T[(e / NBT) * (NBT + 1) + e % NBT];
+  for (int e = threadIdx.x; e < NBT * NBT; e += blockDim.x) {
+    const int rr = e / NBT, c = e % NBT;
+    Tg[e] = (c >= rr && c < nb) ? T[rr * LD + c] : 0.0;
+  }
 }
 
 // V0 = I[:, :kk] for the matrices that fall back
@@ -1048,7 +1106,13 @@ int eig_precondition(const double* Xt, double* Yt, int64_t m, int64_t n, int64_t
   {
     dim3 grid((unsigned)((kk + 127) / 128), (unsigned)batch);
     if (int r = ensure_smem(tri_bisect, 2 * sizeof(double) * (size_t)n)) return r;
-    tri_bisect<<<grid, 128, 2 * sizeof(double) * (size_t)n, st>>>(dd, e2, info, flag, ni, ki, lam);
+    if (kk <= 128) {  // (8 warps per CTA: 8 eigenvalues per CTA)
+      if (int r = ensure_smem(tri_multisect, 2 * sizeof(double) * (size_t)n)) return r;
+      tri_multisect<<<dim3((unsigned)((kk + 7) / 8), (unsigned)batch), 256, 2 * sizeof(double) * (size_t)n, st>>>(
+          dd, e2, info, flag, ni, ki, lam);
+    } else {
+      tri_bisect<<<grid, 128, 2 * sizeof(double) * (size_t)n, st>>>(dd, e2, info, flag, ni, ki, lam);
+    }
     mark();
     tri_inviter<<<grid, 128, 0, st>>>(dd, ee, info, lam, flag, ni, ki, Z, P, Z2);
     tri_cluster_mgs<<<(unsigned)batch, PT, 0, st>>>(lam, info, flag, ni, ki, Z);
@@ -1108,9 +1172,9 @@ int eig_precondition(const double* Xt, double* Yt, int64_t m, int64_t n, int64_t
     if (int r = gemm_f64_lim(1, 0, nb, nb, n - r0, 1.0, Y, n, nn, Y, n, nn, 0.0, S, NBT, NBT * NBT, batch, nullptr,
                              glim, st))
       return r;
-    const size_t tsm = sizeof(double) * (NBT * (NBT + 1) + NBT);
+    const size_t tsm = sizeof(double) * NBT * (NBT + 1);
     if (int r = ensure_smem(wy_larft, tsm)) return r;
-    wy_larft<<<(unsigned)batch, NBT, tsm, st>>>(S, tau, flag, ni, (int)k0, (int)nb, T);
+    wy_larft<<<(unsigned)batch, 4 * NBT, tsm, st>>>(S, tau, flag, ni, (int)k0, (int)nb, T);
     // M1 = Y^T Z (nb x n), M2 = T M1, Z[r0:, :] -= Y M2
     if (int r = gemm_f64_lim(1, 0, nb, kk, n - r0, 1.0, Y, n, nn, Z + r0 * kk, kk, nk, 0.0, M1, kk, NBT * n, batch,
                              nullptr, glim, st))
