@@ -250,11 +250,20 @@ __global__ void __launch_bounds__(PT, 2) tridiag_panel(double* __restrict__ Gall
     if (k == n - 1) break;  // the last column only has its diagonal
     // v for every row of the trailing block, from the owners' a values (no
     // barrier between: the a values stay untouched until after the next S3)
-    for (int i = tid; i < n; i += PT) {
-      double v = 0.0;
-      if (i >= k + 2) v = remote<C>(aw, i % C)[i] * scale;
-      else if (i == k + 1) v = tk != 0.0 ? 1.0 : 0.0;
-      vsm[i] = v;
+    {
+      // (all remote loads first, then the stores: the DSMEM latencies overlap)
+      constexpr int VI = (8 * MAXR + PT - 1) / PT;  // n <= 8 MAXR
+      double av_r[VI];
+#pragma unroll
+      for (int u = 0; u < VI; ++u) {
+        const int i = tid + u * PT;
+        av_r[u] = (i < n && i >= k + 2) ? remote<C>(aw, i % C)[i] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < VI; ++u) {
+        const int i = tid + u * PT;
+        if (i < n) vsm[i] = i >= k + 2 ? av_r[u] * scale : (i == k + 1 && tk != 0.0 ? 1.0 : 0.0);
+      }
     }
     __syncthreads();
     for (int q = tid; q < nloc; q += PT) vws[q * VP + j] = vsm[row_of(q)];
@@ -410,8 +419,10 @@ __global__ void __launch_bounds__(PT, 2) tridiag_panel(double* __restrict__ Gall
       ys[t] = sacc;
     }
     __syncthreads();
-    double ywv = 0.0;
-    for (int t = 0; t < j; ++t) ywv = fma(ys[t], ys[NB + t], ywv);
+    // yW . yV over the panel's first j columns: one term per lane, butterfly sum
+    double ywv = lane < j ? ys[lane] * ys[NB + lane] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) ywv += __shfl_xor_sync(0xffffffffu, ywv, o);
     const double alpha2 = -0.5 * tk * tk * (pvt - 2.0 * ywv);
     // w_i = tau (A22 v - V yW - W yV)_i + alpha2 v_i from the owner's row part,
     // diagonal and [V | W] row, and every CTA's column part (one expression,
