@@ -367,7 +367,8 @@ def headline_single(args, x_host, sampler):
                                               "(Gram, tridiagonalization, bisection, inverse iteration, Newton-Schulz, "
                                               "back-transform, X V0, Jacobi sweeps, sort)",
                 "achieved": round(ach, 3), "peak": peak, "unit": "TFLOP/s", "frac": round(ach / peak, 4),
-                "peak_source": src, "traffic": profile_value("K4_cfg4", "dram_bytes_per_call"),
+                "peak_source": src,
+                "traffic": profile_value("K4_cfg4t" if k4_name == "svd_topk" else "K4_cfg4", "dram_bytes_per_call"),
                 "flops_per_launch": flops,
                 "flops_model": "32 x (14 m n^2 + 8 n^3), m = n = 1024: the Golub-Kahan thin-SVD count of the work the "
                                "reference does for this result (SURVEY 8(d)); the leading-triplet mode executes less "

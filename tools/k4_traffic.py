@@ -21,7 +21,7 @@ for r in rows[1:]:
 
 def phase(n):
     for key, ph in (("tridiag_panel", "tridiagonalization panels"), ("gemm_f64", "K3 GEMMs (Gram, trailing, NS, back-transform, X V0)"),
-                    ("tri_bisect", "bisection"), ("tri_inviter", "inverse iteration"), ("cluster_mgs", "cluster MGS"),
+                    ("tri_bisect", "bisection"), ("tri_multisect", "bisection"), ("tri_inviter", "inverse iteration"), ("cluster_mgs", "cluster MGS"),
                     ("svd_sweep_kernel", "Jacobi sweeps"), ("ns_", "Newton-Schulz bookkeeping"), ("wy_larft", "larft")):
         if key in n:
             return ph
