@@ -125,7 +125,7 @@ template <int C, int NB>
 __global__ void __launch_bounds__(PT, 2) tridiag_panel(double* __restrict__ Gall, double* __restrict__ VWall,
                                                     double* __restrict__ WVall, double* __restrict__ dall,
                                                     double* __restrict__ eall, double* __restrict__ tauall,
-                                                    const int* __restrict__ flag, int n, int k0) {
+                                                    const int* __restrict__ flag, int n, int k0, float l2keep) {
   static_assert(NB == 16 || NB == 32, "panel width");
   constexpr int VP = 2 * NB + 2;  // shared pitch of a [V | W] row (even: 16-byte aligned rows)
   extern __shared__ __align__(16) double sm[];
@@ -151,6 +151,13 @@ __global__ void __launch_bounds__(PT, 2) tridiag_panel(double* __restrict__ Gall
   if (!flag[b]) return;  // cluster-uniform
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   double* A = Gall + (int64_t)b * n * n;
+  // L2 policy of the symv loads: the fraction l2keep of the trailing blocks' lines
+  // (by address hash) is kept (evict_last), the rest streams (evict_first), so a
+  // batch whose trailing blocks exceed L2 keeps most of them resident across the
+  // panel's columns instead of thrashing all of them
+  uint64_t l2pol = 0;
+  if constexpr (C > 1)
+    asm volatile("createpolicy.fractional.L2::evict_last.L2::evict_first.b64 %0, %1;" : "=l"(l2pol) : "f"(l2keep));
   double* VW = VWall + (int64_t)b * n * 2 * NB;
   double* WV = WVall + (int64_t)b * n * 2 * NB;
   double* d = dall + (int64_t)b * n;
@@ -252,7 +259,7 @@ __global__ void __launch_bounds__(PT, 2) tridiag_panel(double* __restrict__ Gall
     // barrier between: the a values stay untouched until after the next S3)
     {
       // (all remote loads first, then the stores: the DSMEM latencies overlap)
-      constexpr int VI = (8 * MAXR + PT - 1) / PT;  // n <= 8 MAXR
+      constexpr int VI = (C * MAXR + PT - 1) / PT;  // n <= C MAXR
       double av_r[VI];
 #pragma unroll
       for (int u = 0; u < VI; ++u) {
@@ -316,9 +323,17 @@ __global__ void __launch_bounds__(PT, 2) tridiag_panel(double* __restrict__ Gall
             av[r][t][0] = av[r][t][1] = 0.0;
             if (q < nloc && c <= cend) {
               if ((n & 1) == 0) {
-                const double2 x = *reinterpret_cast<const double2*>(Ar + c);
-                av[r][t][0] = x.x;
-                av[r][t][1] = c + 1 <= cend ? x.y : 0.0;  // (upper triangle beyond the diagonal)
+                double x0, x1;
+                if constexpr (C > 1) {  // (the single-CTA shapes serve batches that fit L2)
+                  asm("ld.global.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;"
+                      : "=d"(x0), "=d"(x1) : "l"(Ar + c), "l"(l2pol));
+                } else {
+                  const double2 x = *reinterpret_cast<const double2*>(Ar + c);
+                  x0 = x.x;
+                  x1 = x.y;
+                }
+                av[r][t][0] = x0;
+                av[r][t][1] = c + 1 <= cend ? x1 : 0.0;  // (upper triangle beyond the diagonal)
               } else {
                 av[r][t][0] = Ar[c];
                 if (c + 1 <= cend) av[r][t][1] = Ar[c + 1];
@@ -1042,7 +1057,13 @@ int launch_panel(double* G, double* VW, double* WV, double* d, double* e, double
   cfg.stream = st;
   cfg.attrs = attr;
   cfg.numAttrs = C > 1 ? 1 : 0;
-  WT_CUDA(cudaLaunchKernelEx(&cfg, kern, G, VW, WV, d, e, tau, flag, n, k0));
+  // fraction of the batch's trailing lower triangles marked evict_last: a 48 MB
+  // share of the 126 MB L2 (config 4, 32 x 1024^2: 45 MB 23.8 ms, 30 MB 23.9,
+  // 60 MB 24.1, 90 MB 24.9, no hint 25.0 ms)
+  constexpr double kL2KeepBytes = 48.0 * 1048576.0;
+  const double bytes = (double)batch * 4.0 * (double)(n - k0) * (double)(n - k0);
+  const double keep = std::min(1.0, kL2KeepBytes / std::max(bytes, 1.0));
+  WT_CUDA(cudaLaunchKernelEx(&cfg, kern, G, VW, WV, d, e, tau, flag, n, k0, (float)keep));
   return WT_OK;
 }
 
