@@ -276,7 +276,7 @@ __global__ void __launch_bounds__(PT, 2) tridiag_panel(double* __restrict__ Gall
     for (int q = tid; q < nloc; q += PT) vws[q * VP + j] = vsm[row_of(q)];
     // L2 prefetch of my rows' part of the next column's symv (A22 is constant
     // within the panel): one bulk prefetch per row, issued a column ahead
-    if (j + 1 < jb) {
+    if (C > 1 && j + 1 < jb) {  // (single-CTA shapes: batches that fit L2, measured faster without)
       const int c0 = (k + 2) & ~1;
       for (int q = q_first(k + 2) + tid; q < nloc; q += PT) {
         const int i = row_of(q);
