@@ -1073,7 +1073,7 @@ size_t eig_workspace_bytes(int64_t n, int64_t batch) { return eig::layout(n, bat
 
 int eig_precondition(const double* Xt, double* Yt, int64_t m, int64_t n, int64_t ldx, int64_t sx, int64_t batch,
                      int64_t kk, int64_t ldy, int64_t sy, void* ws, size_t ws_bytes, int* n_fallback,
-                     cudaStream_t st) {
+                     cudaStream_t st, const int* kmask) {
   using namespace eig;
   const Layout L = layout(n, batch);
   WT_REQUIRE(ws != nullptr && ws_bytes >= L.total, "eig: workspace too small");
@@ -1103,7 +1103,7 @@ int eig_precondition(const double* Xt, double* Yt, int64_t m, int64_t n, int64_t
   mark();
 
   // 1. G = X^T X (rows of Xt are the columns of X)
-  if (int r = gemm_f64_lim(0, 1, n, n, m, 1.0, Xt, ldx, sx, Xt, ldx, sx, 0.0, G, n, nn, batch, nullptr, nullptr, st,
+  if (int r = gemm_f64_lim(0, 1, n, n, m, 1.0, Xt, ldx, sx, Xt, ldx, sx, 0.0, G, n, nn, batch, kmask, nullptr, st,
                            1))  // lower tiles: the tridiagonalization reads only the lower triangle
     return r;
   gram_flag<<<(unsigned)batch, PT, 0, st>>>(G, ni, flag, glim);
@@ -1225,7 +1225,7 @@ int eig_precondition(const double* Xt, double* Yt, int64_t m, int64_t n, int64_t
   if (int r = check_launch("eig back-transformation")) return r;
   mark();
   // 7. Y = X V0  (Yt = V0^T Xt: kk rows of pitch ldy, stride sy)
-  if (int r = gemm_f64_lim(1, 0, kk, m, n, 1.0, Z, kk, nk, Xt, ldx, sx, 0.0, Yt, ldy, sy, batch, nullptr, nullptr, st))
+  if (int r = gemm_f64_lim(1, 0, kk, m, n, 1.0, Z, kk, nk, Xt, ldx, sx, 0.0, Yt, ldy, sy, batch, kmask, nullptr, st))
     return r;
   mark();
   if (prof && nev > 1) {

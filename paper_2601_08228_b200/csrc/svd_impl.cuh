@@ -75,19 +75,22 @@ __global__ void svd_absmax_part(const double* __restrict__ A, int64_t lda, int64
   if ((threadIdx.x & 31) == 0 && mx) atomicMax(bits + b, mx);
 }
 
-__global__ void svd_absmax_final(double* __restrict__ scale, int64_t batch) {
+__global__ void svd_absmax_final(double* __restrict__ scale, int* __restrict__ nz, int64_t batch) {
   const int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (b >= batch) return;
   const double mx = __longlong_as_double((long long)reinterpret_cast<const unsigned long long*>(scale)[b]);
   scale[b] = (mx > 0.0 && isfinite(mx)) ? ldexp(1.0, -ilogb(mx)) : 1.0;
+  // K limit of the preconditioner's GEMMs on this slice: 0 for an all-zero slice
+  // (its Gram and X V0 are zero: K3 writes the zero tiles without the k loop)
+  if (nz) nz[b] = mx != 0.0 ? 0x7fffffff : 0;
 }
 
 int absmax_scale(const double* A, int64_t lda, int64_t sA, int64_t n1, int64_t n2, int64_t batch, double* scale,
-                 cudaStream_t st) {
+                 cudaStream_t st, int* nz = nullptr) {
   WT_CUDA(cudaMemsetAsync(scale, 0, sizeof(double) * (size_t)batch, st));
   dim3 grid((unsigned)std::min<int64_t>(n1, std::max<int64_t>(1, 2048 / std::max<int64_t>(batch, 1))), (unsigned)batch);
   svd_absmax_part<<<grid, 256, 0, st>>>(A, lda, sA, n1, n2, reinterpret_cast<unsigned long long*>(scale));
-  svd_absmax_final<<<(unsigned)((batch + 255) / 256), 256, 0, st>>>(scale, batch);
+  svd_absmax_final<<<(unsigned)((batch + 255) / 256), 256, 0, st>>>(scale, nz, batch);
   return check_launch("svd absmax scale");
 }
 
@@ -849,7 +852,7 @@ __global__ void svd_flip(SvdWs ws, int batch) {
 struct WsLayout {
   int64_t m, n, mpad, npad;
   size_t off_X, off_X2, off_xsel, off_active, off_off, off_conv, off_pending, off_sig, off_perm, off_bdone,
-      off_bver, off_pclean, off_scale, off_eig, eig_bytes, total;
+      off_bver, off_pclean, off_scale, off_nz, off_eig, eig_bytes, total;
   bool skip;     // pair-skip bookkeeping (nblk <= kSkipMaxBlocks)
   bool precond;  // Gram-eigenbasis preconditioner (eig.cu) before the sweeps
 };
@@ -885,6 +888,7 @@ WsLayout ws_layout(int64_t n1, int64_t n2, int64_t batch, bool allow_precond = t
   L.off_bver = take(L.skip ? sizeof(int) * (size_t)(batch * nbk) : 0);
   L.off_pclean = take(L.skip ? sizeof(unsigned long long) * (size_t)(batch * nbk * nbk) : 0);
   L.off_scale = take(sizeof(double) * (size_t)batch);
+  L.off_nz = take(sizeof(int) * (size_t)batch);
   L.precond = allow_precond && precond_enabled(L.n);
   L.eig_bytes = L.precond ? eig_workspace_bytes(L.n, batch) : 0;
   L.off_eig = take(L.eig_bytes);
@@ -978,7 +982,8 @@ int jacobi(const double* A, int64_t lda, int64_t strideA, int64_t n1,
 
   {
     dim3 grid((unsigned)std::min<int64_t>((L.npad * L.mpad + 255) / 256, 4096), (unsigned)batch);
-    if (int e = absmax_scale(A, lda, strideA, n1, n2, batch, ws.scale, st)) return e;
+    if (int e = absmax_scale(A, lda, strideA, n1, n2, batch, ws.scale, st, reinterpret_cast<int*>(base + L.off_nz)))
+      return e;
     svd_copy_in<<<grid, 256, 0, st>>>(A, lda, strideA, right, L.m, L.n, L.mpad, L.npad, ws.scale, ws.X);
     if (int e = check_launch("svd_copy_in")) return e;
   }
@@ -992,7 +997,8 @@ int jacobi(const double* A, int64_t lda, int64_t strideA, int64_t n1,
     WT_CUDA(cudaMemsetAsync(ws.X2, 0, sizeof(double) * (size_t)(batch * L.npad * L.mpad), st));
     int fallback = 0;
     if (int e = eig_precondition(ws.X, ws.X2, L.mpad, L.n, L.mpad, L.npad * L.mpad, batch, L.n, L.mpad,
-                                 L.npad * L.mpad, base + L.off_eig, L.eig_bytes, &fallback, st))
+                                 L.npad * L.mpad, base + L.off_eig, L.eig_bytes, &fallback, st,
+                                 reinterpret_cast<const int*>(base + L.off_nz)))
       return e;
     g_last_fallbacks = fallback;
     svd_fill_int<<<(unsigned)((batch + 255) / 256), 256, 0, st>>>(ws.xsel, (int)batch, 1);
@@ -1185,7 +1191,7 @@ int jacobi(const double* A, int64_t lda, int64_t strideA, int64_t n1,
 struct TopkLayout {
   WsLayout inner;
   int64_t m, n, mpad, npad, k;
-  size_t off_X, off_scale, off_eig, eig_bytes, off_X1, off_inner, total;
+  size_t off_X, off_scale, off_nz, off_eig, eig_bytes, off_X1, off_inner, total;
 };
 
 TopkLayout topk_layout(int64_t n1, int64_t n2, int64_t batch, int64_t k) {
@@ -1199,6 +1205,7 @@ TopkLayout topk_layout(int64_t n1, int64_t n2, int64_t batch, int64_t k) {
   auto take = [&](size_t bytes) { size_t r = o; o = (o + bytes + 255) / 256 * 256; return r; };
   T.off_X = take(sizeof(double) * (size_t)(batch * T.npad * T.mpad));
   T.off_scale = take(sizeof(double) * (size_t)batch);
+  T.off_nz = take(sizeof(int) * (size_t)batch);
   T.eig_bytes = eig_workspace_bytes(T.n, batch);
   T.off_eig = take(T.eig_bytes);
   T.off_X1 = take(sizeof(double) * (size_t)(batch * k * T.mpad));
@@ -1231,7 +1238,8 @@ int jacobi_topk(const double* A, int64_t lda, int64_t strideA, int64_t n1, int64
   double* scale = reinterpret_cast<double*>(base + T.off_scale);
   double* X1 = reinterpret_cast<double*>(base + T.off_X1);
   const bool right = n1 <= n2;
-  if (int e = absmax_scale(A, lda, strideA, n1, n2, batch, scale, st)) return e;
+  int* nz = reinterpret_cast<int*>(base + T.off_nz);
+  if (int e = absmax_scale(A, lda, strideA, n1, n2, batch, scale, st, nz)) return e;
   {
     dim3 grid((unsigned)std::min<int64_t>((T.npad * T.mpad + 255) / 256, 4096), (unsigned)batch);
     svd_copy_in<<<grid, 256, 0, st>>>(A, lda, strideA, right, T.m, T.n, T.mpad, T.npad, scale, X);
@@ -1239,7 +1247,7 @@ int jacobi_topk(const double* A, int64_t lda, int64_t strideA, int64_t n1, int64
   }
   int fallback = 0;
   if (int e = eig_precondition(X, X1, T.mpad, T.n, T.mpad, T.npad * T.mpad, batch, k, T.mpad, k * T.mpad,
-                               base + T.off_eig, T.eig_bytes, &fallback, st))
+                               base + T.off_eig, T.eig_bytes, &fallback, st, nz))
     return e;
   // rows of X1 are the k columns of X V0: the Jacobi on that (k x m) row-major matrix,
   // right side: its long-side vectors are X's (A's long side), its sigma X V0's

@@ -10,6 +10,9 @@ import paper_2601_08228_b200 as W  # noqa: E402
 from paper_2601_08228_b200 import synth  # noqa: E402
 from paper_2601_08228_b200.algebra import w_product_device  # noqa: E402
 from paper_2601_08228_b200.decomposition import pinv_w_device_many  # noqa: E402
+from paper_2601_08228_b200 import engine as E  # noqa: E402
+
+E.options_from_env()  # WT_OPT_<NAME>=value diagnostics switches
 
 x, av, ah, eta = synth.deblur_problem()
 xd, avd, ahd = (torch.from_numpy(t).cuda() for t in (x, av, ah))
