@@ -10,8 +10,8 @@ block order ``[d1 | ... | dL | sL]`` (include/wten_b200.h).
 from __future__ import annotations
 
 import contextlib
-
 import threading
+import weakref
 
 import numpy as np
 import torch
@@ -104,12 +104,127 @@ def as_device(x, device=None) -> torch.Tensor:
     return t.to(device or "cuda").contiguous()
 
 
+# ----------------------------------------------------------- host results ----
+# Large results handed to numpy callers live in pinned memory only while that is
+# cheap: a pool of at most two pinned buffers per size (and _POOL_BYTES in all)
+# that no handed-out array still references.  A caller who keeps every result
+# would otherwise make each call page-lock a fresh multi-GB block (~0.9 s for
+# 2 GiB, more than the whole computation); beyond the pool the result goes to
+# pageable memory through the pinned download ring instead (~2x the DMA time).
+_POOL_MIN_ELEMS = 8 << 20   # 64 MB: smaller results use torch's caching host allocator
+_POOL_PER_SIZE = 2
+_POOL_BYTES = 8 << 30
+_pool: dict = {}            # numel -> [[pinned tensor, state]]; state: None free, _BUSY, weakref to the ndarray
+_BUSY = object()
+_pool_lock = threading.Lock()
+_dl_ring: list = []         # pinned download staging slots (for pageable results)
+_dl_lock = threading.Lock()
+
+
+def host_buffer(numel: int) -> torch.Tensor:
+    """1-D CPU f64 buffer for a host result (pinned when the pool has one to spare)."""
+    if numel < _POOL_MIN_ELEMS:
+        return torch.empty(numel, dtype=F64, pin_memory=True)
+    with _pool_lock:
+        lst = _pool.setdefault(numel, [])
+        for ent in lst:
+            st = ent[1]
+            if st is None or (st is not _BUSY and st() is None):
+                ent[1] = _BUSY
+                return ent[0]
+        pooled = sum(len(v) * k for k, v in _pool.items()) * 8
+        if len(lst) < _POOL_PER_SIZE and pooled + numel * 8 <= _POOL_BYTES:
+            t = torch.empty(numel, dtype=F64, pin_memory=True)
+            lst.append([t, _BUSY])
+            return t
+    return torch.empty(numel, dtype=F64)
+
+
+def hand_out(t: torch.Tensor) -> np.ndarray:
+    """The numpy array of a host_buffer() result for the caller; a pooled buffer
+    returns to the pool once that array and every view of it are gone."""
+    arr = t.numpy()
+    with _pool_lock:
+        for ent in _pool.get(t.numel(), []):
+            if ent[0].data_ptr() == t.data_ptr():
+                ent[1] = weakref.ref(arr)
+    return arr
+
+
+def release(t: torch.Tensor) -> None:
+    """Return a host_buffer() result that is not handed out (error paths)."""
+    with _pool_lock:
+        for ent in _pool.get(t.numel(), []):
+            if ent[0].data_ptr() == t.data_ptr():
+                ent[1] = None
+
+
+class Download:
+    """D2H of device pieces into a 1-D host buffer on the current stream: direct
+    DMA into pinned memory, else through the pinned download ring (each slot's
+    host copy runs when the slot is reused, overlapping the other slots' DMA)."""
+
+    def __init__(self, host: torch.Tensor):
+        self.host = host
+        self.direct = host.is_pinned()
+        self.pending = []
+        self.i = 0
+        if not self.direct:
+            _dl_lock.acquire()
+            if not _dl_ring:
+                _dl_ring.extend((torch.empty(_STAGE_ELEMS, dtype=F64, pin_memory=True), torch.cuda.Event())
+                                for _ in range(_STAGE_SLOTS + 1))
+
+    def put(self, lo: int, src: torch.Tensor) -> None:
+        src = src.reshape(-1)
+        n = src.numel()
+        if self.direct:
+            self.host[lo:lo + n].copy_(src, non_blocking=True)
+            return
+        stream = torch.cuda.current_stream()
+        for c0 in range(0, n, _STAGE_ELEMS):
+            m = min(_STAGE_ELEMS, n - c0)
+            slot = self.i % len(_dl_ring)
+            self.i += 1
+            self._drain(slot)
+            buf, ev = _dl_ring[slot]
+            buf[:m].copy_(src[c0:c0 + m], non_blocking=True)
+            ev.record(stream)
+            self.pending.append((slot, lo + c0, m))
+
+    def _drain(self, slot=None) -> None:
+        keep = []
+        for ent in self.pending:
+            s, lo, m = ent
+            if slot is None or s == slot:
+                buf, ev = _dl_ring[s]
+                ev.synchronize()
+                self.host[lo:lo + m].copy_(buf[:m])
+            else:
+                keep.append(ent)
+        self.pending = keep
+
+    def finish(self) -> None:
+        """Wait for every piece (host copies done; pinned: the caller synchronizes)."""
+        if not self.direct:
+            try:
+                self._drain()
+            finally:
+                _dl_lock.release()
+
+
 def to_host(t: torch.Tensor) -> np.ndarray:
-    """D2H into pinned host memory (full-bandwidth DMA); the returned numpy array
-    owns a reference to the pinned buffer."""
-    h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
-    h.copy_(t)
-    return h.numpy()
+    """D2H of a result into host memory (pinned when cheap: host_buffer)."""
+    t = t.contiguous()
+    h = host_buffer(t.numel())
+    dl = Download(h)
+    try:
+        dl.put(0, t)
+    finally:
+        dl.finish()
+    if dl.direct:
+        torch.cuda.current_stream().synchronize()
+    return hand_out(h).reshape(t.shape)
 
 
 # ------------------------------------------------- host-streamed transform ----
@@ -145,11 +260,15 @@ def host_lift(src, n1: int, n2: int, p: int, levels: int, forward: bool) -> torc
     nt = n1 * n2
     rows, chunks = _row_chunks(n1, n2 * p)
     blocks = [(off, cnt) for _, off, cnt in block_slices(p, levels)]
-    out = torch.empty(nt * p, dtype=F64, pin_memory=True)
+    out = host_buffer(nt * p)
     s_in, s_cmp, s_out = _pipe_streams()
     main = torch.cuda.current_stream()
     for st in (s_in, s_cmp, s_out):
         st.wait_stream(main)
+    if not forward and not src.is_pinned():  # a pageable pyramid (host_buffer fallback): stage it up whole
+        src = _upload(src, "cuda")
+        for st in (s_in, s_cmp, s_out):
+            st.wait_stream(main)
     cap = rows * n2 * p
     with _stage_lock:
         if forward and not _stage_ring:
@@ -158,6 +277,7 @@ def host_lift(src, n1: int, n2: int, p: int, levels: int, forward: bool) -> torc
         dy = [torch.empty(cap, dtype=F64, device="cuda") for _ in range(2)]
         free_in = [None, None]   # dx[b] consumed by the kernel
         free_out = [None, None]  # dy[b] drained by the D2H
+        dl = Download(out)
         for i, (r0, r1) in enumerate(chunks):
             b = i % 2
             rn = (r1 - r0) * n2
@@ -199,13 +319,13 @@ def host_lift(src, n1: int, n2: int, p: int, levels: int, forward: bool) -> torc
                 s_out.wait_event(free_in[b])
                 if forward:
                     for off, cnt in blocks:
-                        out[off * nt + r0 * n2 * cnt:off * nt + r1 * n2 * cnt].copy_(
-                            dy[b][off * rn:(off + cnt) * rn], non_blocking=True)
+                        dl.put(off * nt + r0 * n2 * cnt, dy[b][off * rn:(off + cnt) * rn])
                 else:
-                    out[r0 * n2 * p:r1 * n2 * p].copy_(dy[b][:n], non_blocking=True)
+                    dl.put(r0 * n2 * p, dy[b][:n])
                 free_out[b] = torch.cuda.Event()
                 free_out[b].record(s_out)
         s_out.synchronize()
+        dl.finish()
         main.wait_stream(s_out)
     return out
 
@@ -222,7 +342,8 @@ def host_slices_pipeline(src: np.ndarray, levels: int, mask: int, base: int, dec
     ``decompose(slices)`` returns the (p - base, out_rows, out_cols) result slices;
     K2 then loads them back chunk by chunk of result rows (wt_lift_inv_f64_peer)
     while the D2H of the previous chunk drains into the pinned result.  Returns
-    the (out_rows, out_cols, p) result as a numpy view of pinned memory.
+    the (out_rows, out_cols, p) result as a numpy array (pinned memory from
+    host_buffer's pool when one is free, else pageable).
     """
     lib = N.require_gpu()  # noqa: F841  (fail loudly without the library / a GPU)
     n1, n2, p = src.shape
@@ -276,10 +397,11 @@ def host_slices_pipeline(src: np.ndarray, levels: int, mask: int, base: int, dec
         st.wait_stream(main)
     orows, ochunks = _row_chunks(out_rows, out_cols * p)
     tab_i = tables(result, out_rows, out_cols, ochunks)
-    out = torch.empty(out_rows * out_cols * p, dtype=F64, pin_memory=True)
+    out = host_buffer(out_rows * out_cols * p)
     ocap = orows * out_cols * p
     dy = [torch.empty(ocap, dtype=F64, device=dev) for _ in range(2)]
     free_out = [None, None]
+    dl = Download(out)
     for i, (r0, r1) in enumerate(ochunks):
         b = i % 2
         n = (r1 - r0) * out_cols * p
@@ -292,13 +414,14 @@ def host_slices_pipeline(src: np.ndarray, levels: int, mask: int, base: int, dec
             done.record(s_cmp)
         with torch.cuda.stream(s_out):
             s_out.wait_event(done)
-            out[r0 * out_cols * p:r1 * out_cols * p].copy_(dy[b][:n], non_blocking=True)
+            dl.put(r0 * out_cols * p, dy[b][:n])
             free_out[b] = torch.cuda.Event()
             free_out[b].record(s_out)
     s_out.synchronize()
+    dl.finish()
     main.wait_stream(s_out)
     result.record_stream(s_cmp)
-    return out.numpy().reshape(out_rows, out_cols, p)
+    return hand_out(out).reshape(out_rows, out_cols, p)
 
 
 # --------------------------------------------------------------- lifting ----

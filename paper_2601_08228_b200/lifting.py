@@ -168,9 +168,10 @@ def forward_w(t, levels):
     if dev:
         return _pyramid_from_packed(E.lift_forward(E.as_device(t), levels), levels, n1, n2, p)
     # host mode: tube-major blocks = the reference's own per-level arrays, all
-    # views of one pinned host buffer (inverse_w re-uploads it without packing)
+    # views of one host buffer, pinned when host_buffer's pool has one to spare
+    # (inverse_w re-uploads it without packing)
     if n1 * n2 * p >= _STREAM_MIN and t.flags.c_contiguous:
-        host = E.host_lift(t, n1, n2, p, levels, forward=True).numpy()
+        host = E.hand_out(E.host_lift(t, n1, n2, p, levels, forward=True))
     else:
         host = E.to_host(E.lift_forward(E.as_device(t), levels, layout=N.LAYOUT_TUBE)).reshape(-1)
     nt = n1 * n2
@@ -222,8 +223,8 @@ def inverse_w(pyr):
     hf = getattr(pyr, "_host_flat", None)
     if hf is not None and pyr._same_views(hf[1]):
         if n1 * n2 * p >= _STREAM_MIN:          # streamed H2D | K2 | D2H in row chunks
-            return E.host_lift(torch.from_numpy(hf[0]), n1, n2, p, levels,
-                               forward=False).numpy().reshape(n1, n2, p)
+            return E.hand_out(E.host_lift(torch.from_numpy(hf[0]), n1, n2, p, levels,
+                                          forward=False)).reshape(n1, n2, p)
         flat, dev = E.as_device(hf[0]), False   # blocks are still views of the pinned buffer
     else:
         flat, dev = _pack_blocks(pyr)
