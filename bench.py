@@ -380,8 +380,8 @@ def headline_single(args, x_host, sampler):
     # reconstruction inside every call (decomposition.sp_w_svd)
     e2e_steps = max(1, min(args.steps, 5))
     # warm-up as in the timed loop (the previous result alive while the next call
-    # runs): the caching host allocator then holds both pinned result blocks (a
-    # fresh 2 GiB cudaHostAlloc costs ~0.9 s once)
+    # runs): the two calls allocate engine.host_buffer's two pooled pinned result
+    # buffers (page-locking a fresh 2 GiB block costs ~0.9 s, once)
     y_host = W.sp_w_svd(x_host, r, L)
     y_host = W.sp_w_svd(x_host, r, L)
     torch.cuda.synchronize()
