@@ -1067,6 +1067,15 @@ int launch_panel(double* G, double* VW, double* WV, double* d, double* e, double
   return WT_OK;
 }
 
+#include "eig_sbr.cuh"
+
+// Two-stage path: wide Grams whose rows below the band fit one row per thread,
+// few leading eigenvectors (the stage-2 back-transformation streams every
+// reflector once per SB_QC columns of Z).
+bool use_two_stage(int64_t n, int64_t kk) {
+  return option(WT_OPT_EIG_TWOSTAGE) != 0 && n >= 512 && n - SB_B <= SB_NT && n % 2 == 0 && kk <= 128;
+}
+
 }  // namespace eig
 
 size_t eig_workspace_bytes(int64_t n, int64_t batch) { return eig::layout(n, batch).total; }
@@ -1110,6 +1119,36 @@ int eig_precondition(const double* Xt, double* Yt, int64_t m, int64_t n, int64_t
   mark();
   const PanelShape ps = panel_shape(n);
   const int C = ps.C, NB = ps.NB;
+  const bool sbr = use_two_stage(n, kk);
+  if (sbr) {
+    // 2'. dense -> band (stage 1), band -> tridiagonal (stage 2); eig_sbr.cuh
+    constexpr int B = SB_B;
+    double* AB = Z2;                                   // [batch][n][SB_LDB]
+    double* Zp = AB + (size_t)batch * n * SB_LDB;      // [batch][n][B]   Z = A22 V of the current panel
+    double* Tp = Zp + (size_t)batch * n * B;           // [batch][B][B]
+    WT_CUDA(cudaMemsetAsync(AB, 0, sizeof(double) * (size_t)batch * n * SB_LDB, st));
+    WT_CUDA(cudaMemsetAsync(tau, 0, sizeof(double) * (size_t)batch * n, st));
+    // the panel QR reads full rows: mirror the Gram's lower triangle first
+    sym_mirror<<<dim3((unsigned)((n + 31) / 32), (unsigned)((n + 31) / 32), (unsigned)batch), dim3(32, 8), 0, st>>>(
+        G, ni, flag);
+    for (int64_t c0 = 0; c0 < n; c0 += B) {
+      sbr_panel<<<(unsigned)batch, SB_NT, 0, st>>>(G, AB, tau, Tp, flag, ni, (int)c0);
+      const int64_t r0 = c0 + B, mrem = n - r0;
+      if (mrem < 2) continue;
+      const int64_t off = r0 * n + r0;
+      if (int r = gemm_f64_lim(0, 0, mrem, B, mrem, 1.0, G + off, n, nn, G + r0 * n + c0, n, nn, 0.0, Zp + r0 * B, B,
+                               n * B, batch, nullptr, glim, st))
+        return r;
+      sbr_w<<<(unsigned)batch, SB_NT, 0, st>>>(G, Zp, Tp, VW, WV, flag, ni, (int)c0);
+      const int64_t offp = r0 * 2 * B;
+      if (int r = gemm_f64_lim(0, 1, mrem, mrem, 2 * B, -1.0, VW + offp, 2 * B, n * 2 * B, WV + offp, 2 * B, n * 2 * B,
+                               1.0, G + off, n, nn, batch, nullptr, glim, st))
+        return r;
+    }
+    const size_t csm = ChaseSmem::bytes(ni);
+    if (int r = ensure_smem(sbr_chase, csm)) return r;
+    sbr_chase<<<(unsigned)batch, SB_CW * 32, csm, st>>>(AB, G, dd, ee, flag, ni);
+  } else {
   WT_CUDA(cudaMemsetAsync(VW, 0, sizeof(double) * (size_t)(batch * n * 2 * NB), st));
   WT_CUDA(cudaMemsetAsync(WV, 0, sizeof(double) * (size_t)(batch * n * 2 * NB), st));
   // 2. tridiagonalization, panel by panel
@@ -1130,6 +1169,7 @@ int eig_precondition(const double* Xt, double* Yt, int64_t m, int64_t n, int64_t
                                 n * 2 * NB, 1.0, G + off, n, nn, batch, nullptr, glim, st, 1))
         return r2;
     }
+  }
   }
   if (int r = check_launch("eig tridiagonalization")) return r;
   mark();
@@ -1192,13 +1232,23 @@ int eig_precondition(const double* Xt, double* Yt, int64_t m, int64_t n, int64_t
   WT_CUDA(cudaMemcpyAsync(hflag.data(), flag, sizeof(int) * (size_t)batch, cudaMemcpyDeviceToHost, st));
   mark();
   // 6. V0 = Q Z: blocks of NBT reflectors, last block first
-  const int64_t nref = n - 2;  // reflectors 0 .. n-3 (tau = 0 beyond)
+  // (two-stage: Z <- Q2 Z with the stage-2 reflectors, then the stage-1 reflectors
+  // c = 0 .. n - SB_B - 2, unit entry at row c + SB_B, as the same compact-WY blocks)
+  const int64_t roff = sbr ? SB_B : 1;  // row of reflector c's unit entry: c + roff
+  if (sbr) {
+    const size_t qsm = Q2Smem::bytes(ni);
+    if (int r = ensure_smem(sbr_apply_q2, qsm)) return r;
+    sbr_apply_q2<<<dim3((unsigned)((kk + SB_QC - 1) / SB_QC), (unsigned)batch), SB_QT, qsm, st>>>(G, Z, flag, ni, ki);
+    const dim3 grid((unsigned)std::min<int64_t>((nn + 255) / 256, 1024), (unsigned)batch);
+    sbr_clean_y<<<grid, 256, 0, st>>>(G, ni, flag);
+  }
+  const int64_t nref = n - 1 - roff;  // reflectors 0 .. nref-1 (tau = 0 beyond)
   // (128-reflector blocks halve the passes over Z for n >= 512; 64 measured
   // faster on 256^2 slices: config 3 back-transform 1.02 vs 1.43 ms)
   const int64_t nbt = n >= 512 ? NBT : 64;
   for (int64_t k0 = ((nref - 1) / nbt) * nbt; k0 >= 0; k0 -= nbt) {
     const int64_t nb = std::min<int64_t>(nbt, nref - k0);
-    const int64_t r0 = k0 + 1;  // first nonzero row of the block
+    const int64_t r0 = k0 + roff;  // first nonzero row of the block
     const double* Y = G + r0 * n + k0;  // rows r0.., columns k0.. (ld n)
     // S = Y^T Y
     if (int r = gemm_f64_lim(1, 0, nb, nb, n - r0, 1.0, Y, n, nn, Y, n, nn, 0.0, S, NBT, NBT * NBT, batch, nullptr,
