@@ -1140,14 +1140,28 @@ int eig_precondition(const double* Xt, double* Yt, int64_t m, int64_t n, int64_t
                                n * B, batch, nullptr, glim, st))
         return r;
       sbr_w<<<(unsigned)batch, SB_NT, 0, st>>>(G, Zp, Tp, VW, WV, flag, ni, (int)c0);
-      const int64_t offp = r0 * 2 * B;
-      if (int r = gemm_f64_lim(0, 1, mrem, mrem, 2 * B, -1.0, VW + offp, 2 * B, n * 2 * B, WV + offp, 2 * B, n * 2 * B,
-                               1.0, G + off, n, nn, batch, nullptr, glim, st))
-        return r;
+      if (int r = ensure_smem(sbr_syr2k, SY_SMEM)) return r;
+      sbr_syr2k<<<dim3((unsigned)((mrem + SY_BN - 1) / SY_BN), (unsigned)((mrem + SY_BM - 1) / SY_BM), (unsigned)batch),
+                  SY_NT, SY_SMEM, st>>>(G, VW, WV, flag, ni, (int)r0);
     }
     const size_t csm = ChaseSmem::bytes(ni);
     if (int r = ensure_smem(sbr_chase, csm)) return r;
+    cudaEvent_t ce[2] = {};
+    if (prof) {
+      cudaEventCreate(&ce[0]);
+      cudaEventCreate(&ce[1]);
+      cudaEventRecord(ce[0], st);
+    }
     sbr_chase<<<(unsigned)batch, SB_CW * 32, csm, st>>>(AB, G, dd, ee, flag, ni);
+    if (prof) {
+      cudaEventRecord(ce[1], st);
+      cudaEventSynchronize(ce[1]);
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, ce[0], ce[1]);
+      fprintf(stderr, "[wt_eig] two-stage: band chase %.3f ms (inside tridiag)\n", ms);
+      cudaEventDestroy(ce[0]);
+      cudaEventDestroy(ce[1]);
+    }
   } else {
   WT_CUDA(cudaMemsetAsync(VW, 0, sizeof(double) * (size_t)(batch * n * 2 * NB), st));
   WT_CUDA(cudaMemsetAsync(WV, 0, sizeof(double) * (size_t)(batch * n * 2 * NB), st));

@@ -25,9 +25,13 @@
 #pragma once
 
 constexpr int SB_B = 12;             // band half-width (2 SB_B - 1 diagonals x 1024 columns fit one CTA's shared memory)
-constexpr int SB_LDB = 2 * SB_B - 1;  // band storage: AB[c * SB_LDB + d] = A[c + d][c], d = 0 .. 2 SB_B - 2
+constexpr int SB_LDB = 2 * SB_B;      // band storage: AB[c * SB_LDB + d] = A[c + d][c], d = 0 .. 2 SB_B - 1 (the last one a
+                                      // scratch slot of the chase: always zero between hops)
 constexpr int SB_NT = 1024;          // threads of the stage-1 kernels: one row below the band per thread
-constexpr int SB_CW = 16;            // chase warps per CTA
+#ifndef WT_SB_CW
+#define WT_SB_CW 16
+#endif
+constexpr int SB_CW = WT_SB_CW;            // chase warps per CTA
 constexpr int SB_QC = 16;            // columns of Z per CTA in sbr_apply_q2
 constexpr int SB_QT = 512;           // its threads
 static_assert(SB_B <= 16 && SB_B % 2 == 0, "lane maps below assume an even band width of at most 16");
@@ -80,10 +84,18 @@ __device__ __forceinline__ double warp_sum16(F f, int lane, int& idx) {
 // dlarfg on (alpha, ss = sum of squares of the tail): H x = beta e1, H = I - tau v v^T,
 // v = [1; tail * scale]
 __device__ __forceinline__ void house_gen(double alpha, double ss, double& beta, double& tau, double& scale) {
-  if (ss > 0.0) {
-    beta = -copysign(sqrt(fma(alpha, alpha, ss)), alpha);
-    tau = (beta - alpha) / beta;
-    scale = 1.0 / (alpha - beta);
+  // one rsqrt and one reciprocal on the dependent chain (the chase pays this
+  // latency once per hop).  Columns whose norm is below 1e-140 of the scaled
+  // Gram's unit magnitude are left alone (tau = 0): the neglected entries are far
+  // below rounding of the band.
+  const double nrm2 = fma(alpha, alpha, ss);
+  if (ss > 0.0 && nrm2 > 1e-280) {
+    const double nrm = nrm2 * rsqrt(nrm2);
+    beta = -copysign(nrm, alpha);
+    const double amb = alpha - beta;           // |amb| >= |beta|: no cancellation
+    const double r = 1.0 / (beta * amb);
+    tau = -amb * (r * amb);                    // (beta - alpha) / beta
+    scale = r * beta;                          // 1 / (alpha - beta)
   } else {
     beta = alpha;
     tau = 0.0;
@@ -121,6 +133,93 @@ __global__ void sbr_clean_y(double* __restrict__ Gall, int n, const int* __restr
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nn; e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r = e / n, c = e - r * n;
     if (r < c + SB_B) A[e] = 0.0;
+  }
+}
+
+// A22 -= VW WV^T (the symmetric rank-2 SB_B update A22 - V W^T - W V^T, every tile)
+// for the trailing block at r0 (m = n - r0 rows): a streaming kernel -- the 64 x 64
+// tile of A22 arrives by one bulk copy per row while the DMMA product of the two
+// 24-wide operand strips (bulk copies of contiguous rows) runs, is updated in
+// shared memory and leaves by bulk stores.  K3's general kernel spends these
+// K = 24 updates in its pipeline prologue and a synchronous C read-modify-write
+// (1.2 TB/s).  grid (ceil(m / SY_BN), ceil(m / SY_BM), batch), SY_NT threads, 3 CTAs per SM.
+constexpr int SY_BM = 64, SY_BN = 64, SY_LDC = 72, SY_K = 2 * SB_B, SY_NT = SY_BM * 2;
+constexpr size_t SY_SMEM = sizeof(double) * (SY_BM * SY_K + SY_BN * SY_K + SY_BM * SY_LDC) + 16;
+__global__ void __launch_bounds__(SY_NT, 3) sbr_syr2k(double* __restrict__ Gall, const double* __restrict__ VWall,
+                                                   const double* __restrict__ WVall, const int* __restrict__ flag,
+                                                   int n, int r0) {
+  const int b = blockIdx.z;
+  if (!flag[b]) return;
+  extern __shared__ __align__(128) double ssm[];
+  double* VWs = ssm;                       // [SY_BM][SY_K]
+  double* WVs = VWs + SY_BM * SY_K;        // [SY_BN][SY_K]
+  double* Cs = WVs + SY_BN * SY_K;         // [SY_BM][SY_LDC]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(Cs + SY_BM * SY_LDC);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int m = n - r0;
+  const int i0 = blockIdx.y * SY_BM, j0 = blockIdx.x * SY_BN;
+  const int hrows = min(SY_BM, m - i0), wcols = min(SY_BN, m - j0);
+  double* C = Gall + (int64_t)b * n * n + (int64_t)(r0 + i0) * n + (r0 + j0);
+  const double* VW = VWall + ((int64_t)b * n + r0 + i0) * SY_K;
+  const double* WV = WVall + ((int64_t)b * n + r0 + j0) * SY_K;
+  if (tid == 0) {
+    mbar_init(bar, 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (tid == 0)
+    mbar_expect_tx(bar, (uint32_t)((hrows + wcols) * SY_K * 8 + hrows * wcols * 8));
+  __syncthreads();
+  if (tid == 0) {
+    bulk_g2s(VWs, VW, (uint32_t)(hrows * SY_K * 8), bar);
+    bulk_g2s(WVs, WV, (uint32_t)(wcols * SY_K * 8), bar);
+  }
+  if (tid < hrows) bulk_g2s(Cs + tid * SY_LDC, C + (int64_t)tid * n, (uint32_t)(wcols * 8), bar);
+  mbar_wait(bar, 0);
+  const int wm0 = (warp >> 1) * 32, wn0 = (warp & 1) * 32;
+  const int g = lane >> 2, t = lane & 3;
+  double acc[4][4][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+#pragma unroll
+  for (int ks = 0; ks < SY_K; ks += 8) {
+    double2 af[4], bf[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) af[i] = *reinterpret_cast<const double2*>(VWs + (wm0 + 8 * i + g) * SY_K + ks + 2 * t);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) bf[j] = *reinterpret_cast<const double2*>(WVs + (wn0 + 8 * j + g) * SY_K + ks + 2 * t);
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[i].x, bf[j].x);
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[i].y, bf[j].y);
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int r = wm0 + 8 * i + g;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int c = wn0 + 8 * j + 2 * t;
+      if (r < hrows && c < wcols) {  // (wcols even: the pair is inside together)
+        double2* p = reinterpret_cast<double2*>(Cs + r * SY_LDC + c);
+        double2 o = *p;
+        o.x -= acc[i][j][0];
+        o.y -= acc[i][j][1];
+        *p = o;
+      }
+    }
+  }
+  fence_proxy_async_smem();
+  __syncthreads();
+  if (tid < hrows) {
+    bulk_s2g(C + (int64_t)tid * n, Cs + tid * SY_LDC, (uint32_t)(wcols * 8));
+    bulk_commit();
+    bulk_wait_all();
   }
 }
 
@@ -363,145 +462,155 @@ __global__ void __launch_bounds__(SB_NT, 1) sbr_w(const double* __restrict__ Gal
 // ---------------------------------------------------------------- stage 2 ---
 struct ChaseSmem {
   static size_t bytes(int n) {
-    return sizeof(double) * ((size_t)n * SB_LDB + 2 * SB_CW * 16) + sizeof(int) * (size_t)(n + 4);
+    return sizeof(double) * ((size_t)(n + 2 * SB_B) * SB_LDB + 2 * SB_CW * 16) + sizeof(int) * (size_t)(n + 4);
   }
 };
 
-// Band -> tridiagonal.  One CTA per matrix, band in shared memory.  Warp w runs
-// the sweeps s = w, w + SB_CW, ...: sweep s annihilates column s below its
-// subdiagonal with a reflector on rows s+1 .. s+B and chases the first column of
-// every bulge down the band (hop h works on rows r0 = s + 1 + h B ..).  Sweep s
+// Band -> tridiagonal.  One CTA per matrix, band in shared memory (2 SB_B zero
+// columns appended, so every hop works on full SB_B x SB_B blocks without bounds
+// checks: reflector components of rows beyond the matrix come out as zeros).
+// Warp w runs the sweeps s = w, w + SB_CW, ...: sweep s annihilates column s below
+// its subdiagonal with a reflector on rows s+1 .. s+B and chases the first column
+// of every bulge down the band (hop h works on rows r0 = s + 1 + h B ..).  Sweep s
 // may run hop h once sweep s - 1 has completed hop h + 1 (tools/sbr_proto.py
-// checks the rule under random interleavings).  The reflectors (tau in the unit
-// entry's place) go to the dead upper triangle of G: VQ[s][row] = G[s * n + row].
+// checks the rule under random interleavings), so the kernel's time is 2 (n - 2)
+// hop latencies whatever the number of warps: the hop is written for latency
+// (lane = (row or column, half of the block's other index): 6-term chains,
+// straight-line addressing).  The reflectors (tau in the unit entry's place) go
+// to the dead upper triangle of G: VQ[s][row] = G[s * n + row].
 __global__ void __launch_bounds__(SB_CW * 32, 1) sbr_chase(const double* __restrict__ ABall, double* __restrict__ Gall,
                                                           double* __restrict__ dall, double* __restrict__ eall,
                                                           const int* __restrict__ flag, int n) {
-  constexpr int B = SB_B, LDB = SB_LDB;
+  constexpr int B = SB_B, HB = SB_B / 2, LDB = SB_LDB, LD1 = SB_LDB - 1;
   constexpr int DONE = 0x7fffffff;
   const int b = blockIdx.x;
   if (!flag[b]) return;
   extern __shared__ __align__(16) double csm[];
-  double* AB = csm;                          // [n][LDB]
-  double* vsh = AB + (size_t)n * LDB;        // [SB_CW][16] current reflector
-  double* wsh = vsh + SB_CW * 16;            // [SB_CW][16] w / next reflector
+  double* AB = csm;                               // [n + 2B][LDB]
+  double* vsh = AB + (size_t)(n + 2 * B) * LDB;   // [SB_CW][16] current reflector
+  double* wsh = vsh + SB_CW * 16;                 // [SB_CW][16] w / next reflector
   volatile int* prog = reinterpret_cast<volatile int*>(wsh + SB_CW * 16);  // [n] hops completed by sweep s
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   {
     const double* src = ABall + (int64_t)b * n * LDB;
     for (int i = tid; i < n * LDB; i += SB_CW * 32) AB[i] = src[i];
+    for (int i = n * LDB + tid; i < (n + 2 * B) * LDB; i += SB_CW * 32) AB[i] = 0.0;
     for (int i = tid; i < n; i += SB_CW * 32) prog[i] = 0;
   }
   __syncthreads();
   double* VQ = Gall + (int64_t)b * n * n;
   double* vs = vsh + warp * 16;
   double* ws = wsh + warp * 16;
-  auto lane_sum = [&](double x) {  // over the 16-lane halves (lanes >= 16 carry zeros)
+  const int i = lane & 15, hf = lane >> 4;  // block row (or column) and half of the other index
+  const bool act = i < B;
+  const int ic = act ? i : 0;
+  const int kh = hf * HB;
+  auto half_sum = [&](double x) {  // sum over the 16 lanes of a half, valid in every lane of it
 #pragma unroll
     for (int o = 8; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
     return x;
   };
   for (int s = warp; s < n - 2; s += SB_CW) {
-    int L = min(B, n - 1 - s);
     int h = 0;
     auto wait_prev = [&](int need) {
       if (s > 0) {
-        while (prog[s - 1] < need) {
-        }
+#ifndef SBR_SLEEP
+#define SBR_SLEEP 20
+#endif
+        while (prog[s - 1] < need) __nanosleep(SBR_SLEEP);
         __threadfence_block();
       }
     };
     wait_prev(2);
-    // first reflector: column s, rows s+1 .. s+L
-    double x = (lane < L) ? AB[(size_t)s * LDB + 1 + lane] : 0.0;
-    double alpha = __shfl_sync(0xffffffffu, x, 0);
-    double ss = lane_sum((lane >= 1 && lane < L) ? x * x : 0.0);
-    ss = __shfl_sync(0xffffffffu, ss, 0);
-    double beta, tau, scale;
-    house_gen(alpha, ss, beta, tau, scale);
-    double vi = lane == 0 ? 1.0 : (lane < L ? x * scale : 0.0);
-    if (lane == 0) AB[(size_t)s * LDB + 1] = beta;
+    // first reflector: column s, rows s+1 .. s+B (zeros beyond the matrix)
+    double tau, vi;
+    {
+      const double x = (act && hf == 0) ? AB[(size_t)s * LDB + 1 + ic] : 0.0;
+      const double alpha = __shfl_sync(0xffffffffu, x, 0);
+      const double ss = __shfl_sync(0xffffffffu, half_sum(i >= 1 ? x * x : 0.0), 0);
+      double beta, scale;
+      house_gen(alpha, ss, beta, tau, scale);
+      vi = i == 0 ? 1.0 : x * scale;
+      vi = __shfl_sync(0xffffffffu, vi, i);
+      if (lane == 0) AB[(size_t)s * LDB + 1] = beta;
+    }
     int r0 = s + 1;
     while (true) {
-      // store the reflector (tau in the unit entry's place)
-      if (lane < L) VQ[(int64_t)s * n + r0 + lane] = lane == 0 ? tau : vi;
+      const int L = min(B, n - r0);
+      if (hf == 0 && i < L) VQ[(int64_t)s * n + r0 + i] = i == 0 ? tau : vi;
       if (lane < 16) vs[lane] = vi;
       __syncwarp();
-      // ---- D <- H D H on the symmetric L x L block at r0 (lower band storage)
+      // ---- D <- H D H on the symmetric block at r0: lane = (row i, columns kh .. kh + HB - 1)
       {
-        double drow[B];
+        double* lo = AB + (size_t)r0 * LDB + ic + kh * LD1;        // (i, k), k <= i:  + kk * LD1
+        double* up = AB + (size_t)(r0 + ic) * LDB - ic + kh;       // (k, i), k > i:   + kk
+        double dv[HB];
         double p = 0.0;
 #pragma unroll
-        for (int k = 0; k < B; ++k) {
-          double a = 0.0;
-          if (lane < L && k < L)
-            a = k <= lane ? AB[(size_t)(r0 + k) * LDB + (lane - k)] : AB[(size_t)(r0 + lane) * LDB + (k - lane)];
-          drow[k] = a;
-          p = fma(a, vs[k], p);
+        for (int kk = 0; kk < HB; ++kk) {
+          const double* q = (kh + kk <= ic) ? lo + kk * LD1 : up + kk;
+          dv[kk] = *q;
+          p = fma(dv[kk], vs[kh + kk], p);
         }
-        p *= tau;
-        double pv = lane_sum(lane < L ? p * vi : 0.0);
-        pv = __shfl_sync(0xffffffffu, pv, 0);
+        p += __shfl_xor_sync(0xffffffffu, p, 16);
+        p = act ? p * tau : 0.0;
+        const double pv = __shfl_sync(0xffffffffu, half_sum(hf == 0 ? p * vi : 0.0), 0);
         const double wi = fma(-0.5 * tau * pv, vi, p);
-        if (lane < 16) ws[lane] = lane < L ? wi : 0.0;
-        __syncwarp();  // every lane has read its row of D; w is visible
-        if (lane < L) {
+        if (lane < 16) ws[lane] = wi;
+        __syncwarp();  // every lane has read its part of D; w is visible
 #pragma unroll
-          for (int k = 0; k < B; ++k)
-            if (k <= lane) AB[(size_t)(r0 + k) * LDB + (lane - k)] = drow[k] - vi * ws[k] - wi * vs[k];
-        }
+        for (int kk = 0; kk < HB; ++kk)
+          if (act && kh + kk <= i) lo[kk * LD1] = dv[kk] - vi * ws[kh + kk] - wi * vs[kh + kk];
       }
-      const int R0 = r0 + L;
+      const int R0 = r0 + B;
       const int M = min(B, n - R0);
       if (L < B || M < 1) break;
-      // ---- B block: rows R0 .. R0 + M - 1, columns r0 .. r0 + B - 1 (distance B + i - k)
-      double tau2 = 0.0, v2 = 0.0;
+      // ---- B block: rows R0 + i, columns r0 + k at distance B + i - k: right-apply, new reflector
+      double tau2, v2;
       {
-        double brow[B];
+        double* bp = AB + (size_t)r0 * LDB + B + ic + kh * LD1;    // + kk * LD1
+        double bv[HB];
         double xb = 0.0;
 #pragma unroll
-        for (int k = 0; k < B; ++k) {
-          const int dist = B + lane - k;
-          double a = 0.0;
-          if (lane < M && dist <= 2 * B - 2) a = AB[(size_t)(r0 + k) * LDB + dist];
-          brow[k] = a;
-          xb = fma(a, vs[k], xb);
+        for (int kk = 0; kk < HB; ++kk) {
+          bv[kk] = bp[kk * LD1];
+          xb = fma(bv[kk], vs[kh + kk], xb);
         }
+        xb += __shfl_xor_sync(0xffffffffu, xb, 16);
         xb *= tau;
 #pragma unroll
-        for (int k = 0; k < B; ++k) brow[k] = fma(-xb, vs[k], brow[k]);  // B (I - tau v v^T)
-        if (M >= 2) {
-          const double a0 = __shfl_sync(0xffffffffu, brow[0], 0);
-          double ss2 = lane_sum((lane >= 1 && lane < M) ? brow[0] * brow[0] : 0.0);
-          ss2 = __shfl_sync(0xffffffffu, ss2, 0);
-          double beta2, scale2;
-          house_gen(a0, ss2, beta2, tau2, scale2);
-          v2 = lane == 0 ? 1.0 : (lane < M ? brow[0] * scale2 : 0.0);
-          brow[0] = lane == 0 ? beta2 : 0.0;
-        }
+        for (int kk = 0; kk < HB; ++kk) bv[kk] = fma(-xb, vs[kh + kk], bv[kk]);  // B (I - tau v v^T)
+        const double c0 = (hf == 0 && act) ? bv[0] : 0.0;  // first column of the block
+        const double a0 = __shfl_sync(0xffffffffu, c0, 0);
+        const double ss2 = __shfl_sync(0xffffffffu, half_sum(i >= 1 ? c0 * c0 : 0.0), 0);
+        double beta2, scale2;
+        house_gen(a0, ss2, beta2, tau2, scale2);
+        v2 = i == 0 ? 1.0 : c0 * scale2;
+        v2 = __shfl_sync(0xffffffffu, v2, i);
+        if (hf == 0) bv[0] = i == 0 ? beta2 : 0.0;
         __syncwarp();  // (ws reuse: every lane is past the D update)
         if (lane < 16) ws[lane] = v2;
-        if (lane < M) {
+        if (act) {
 #pragma unroll
-          for (int k = 0; k < B; ++k) {
-            const int dist = B + lane - k;
-            if (dist <= 2 * B - 2) AB[(size_t)(r0 + k) * LDB + dist] = brow[k];
-          }
+          for (int kk = 0; kk < HB; ++kk) bp[kk * LD1] = bv[kk];
         }
         __syncwarp();
-        if (M >= 2 && lane >= 1 && lane < B) {  // (I - tau2 v2 v2^T) B[:, k], k = lane
-          double* col = AB + (size_t)(r0 + lane) * LDB + (B - lane);  // rows i = 0 .. M-1 contiguous
-          double cv[B];
-          double y = 0.0;
+      }
+      // ---- (I - tau2 v2 v2^T) B[:, k]: lane = (column k = i >= 1, rows kh .. kh + HB - 1)
+      if (tau2 != 0.0) {
+        double* cp = AB + (size_t)(r0 + ic) * LDB + B - ic + kh;
+        double cv[HB];
+        double y = 0.0;
 #pragma unroll
-          for (int i = 0; i < B; ++i) {
-            cv[i] = i < M ? col[i] : 0.0;
-            y = fma(ws[i], cv[i], y);
-          }
-          y *= tau2;
+        for (int rr = 0; rr < HB; ++rr) {
+          cv[rr] = cp[rr];
+          y = fma(ws[kh + rr], cv[rr], y);
+        }
+        y += __shfl_xor_sync(0xffffffffu, y, 16);
+        y *= tau2;
+        if (act && i >= 1) {
 #pragma unroll
-          for (int i = 0; i < B; ++i)
-            if (i < M) col[i] = fma(-y, ws[i], cv[i]);
+          for (int rr = 0; rr < HB; ++rr) cp[rr] = fma(-y, ws[kh + rr], cv[rr]);
         }
       }
       __syncwarp();
@@ -510,7 +619,6 @@ __global__ void __launch_bounds__(SB_CW * 32, 1) sbr_chase(const double* __restr
       if (lane == 0) prog[s] = h;
       if (M < 2) break;
       r0 = R0;
-      L = M;
       tau = tau2;
       vi = v2;
       wait_prev(h + 2);
@@ -522,9 +630,9 @@ __global__ void __launch_bounds__(SB_CW * 32, 1) sbr_chase(const double* __restr
   __syncthreads();
   double* d = dall + (int64_t)b * n;
   double* e = eall + (int64_t)b * n;
-  for (int i = tid; i < n; i += SB_CW * 32) {
-    d[i] = AB[(size_t)i * LDB];
-    if (i < n - 1) e[i] = AB[(size_t)i * LDB + 1];
+  for (int i2 = tid; i2 < n; i2 += SB_CW * 32) {
+    d[i2] = AB[(size_t)i2 * LDB];
+    if (i2 < n - 1) e[i2] = AB[(size_t)i2 * LDB + 1];
   }
 }
 
