@@ -1082,7 +1082,7 @@ size_t eig_workspace_bytes(int64_t n, int64_t batch) { return eig::layout(n, bat
 
 int eig_precondition(const double* Xt, double* Yt, int64_t m, int64_t n, int64_t ldx, int64_t sx, int64_t batch,
                      int64_t kk, int64_t ldy, int64_t sy, void* ws, size_t ws_bytes, int* n_fallback,
-                     cudaStream_t st, const int* kmask) {
+                     cudaStream_t st, const int* kmask, int* h_flags) {
   using namespace eig;
   const Layout L = layout(n, batch);
   WT_REQUIRE(ws != nullptr && ws_bytes >= L.total, "eig: workspace too small");
@@ -1308,7 +1308,10 @@ int eig_precondition(const double* Xt, double* Yt, int64_t m, int64_t n, int64_t
   if (n_fallback) {
     WT_CUDA(cudaStreamSynchronize(st));
     int active = 0;
-    for (int64_t b = 0; b < batch; ++b) active += hflag[b] != 0;
+    for (int64_t b = 0; b < batch; ++b) {
+      active += hflag[b] != 0;
+      if (h_flags) h_flags[b] = hflag[b];
+    }
     *n_fallback = (int)batch - active;
   }
   return WT_OK;

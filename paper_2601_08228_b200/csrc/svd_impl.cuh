@@ -1246,17 +1246,48 @@ int jacobi_topk(const double* A, int64_t lda, int64_t strideA, int64_t n1, int64
     if (int e = check_launch("svd_topk copy-in")) return e;
   }
   int fallback = 0;
+  std::vector<int> hflags((size_t)batch, 1);
   if (int e = eig_precondition(X, X1, T.mpad, T.n, T.mpad, T.npad * T.mpad, batch, k, T.mpad, k * T.mpad,
-                               base + T.off_eig, T.eig_bytes, &fallback, st, nz))
+                               base + T.off_eig, T.eig_bytes, &fallback, st, nz, hflags.data()))
     return e;
   // rows of X1 are the k columns of X V0: the Jacobi on that (k x m) row-major matrix,
   // right side: its long-side vectors are X's (A's long side), its sigma X V0's
   if (int e = jacobi(X1, T.mpad, k * T.mpad, k, T.m, batch, sigma, vec, nvec, info, tol, max_sweeps,
                      base + T.off_inner, T.inner.total, stream, false))
     return e;
-  g_last_fallbacks = fallback;
   svd_unscale<<<(unsigned)std::min<int64_t>((batch * k + 255) / 256, 4096), 256, 0, st>>>(sigma, k, batch, scale);
-  return check_launch("svd_topk unscale");
+  if (int e = check_launch("svd_topk unscale")) return e;
+  if (fallback > 0) {
+    // Matrices without a usable eigenbasis (numerically rank-deficient Grams whose
+    // inverse-iteration vectors Newton-Schulz could not repair, all-zero slices):
+    // I[:, :k] does not span their leading subspace, so they take the full SVD
+    // (which starts its Jacobi from X itself) and keep its k leading values /
+    // nvec leading vectors.  Rare: scratch comes from the stream-ordered allocator.
+    const int64_t ln = T.m;
+    const size_t wsb1 = ws_layout(n1, n2, 1).total;
+    const size_t sig_b = (sizeof(double) * (size_t)T.n + 255) / 256 * 256;
+    const size_t vec_b = (sizeof(double) * (size_t)(std::max<int64_t>(nvec, 1) * ln) + 255) / 256 * 256;
+    char* tmp = nullptr;
+    WT_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&tmp), sig_b + vec_b + 256 + wsb1, st));
+    double* sig1 = reinterpret_cast<double*>(tmp);
+    double* vec1 = reinterpret_cast<double*>(tmp + sig_b);
+    int* info1 = reinterpret_cast<int*>(tmp + sig_b + vec_b);
+    int rc = WT_OK;
+    for (int64_t b = 0; b < batch && rc == WT_OK; ++b) {
+      if (hflags[(size_t)b]) continue;
+      rc = jacobi(A + b * strideA, lda, strideA, n1, n2, 1, sig1, vec1, nvec, info1, tol, max_sweeps,
+                  tmp + sig_b + vec_b + 256, wsb1, stream, true);
+      if (rc != WT_OK) break;
+      cudaMemcpyAsync(sigma + b * k, sig1, sizeof(double) * (size_t)k, cudaMemcpyDeviceToDevice, st);
+      if (nvec > 0)
+        cudaMemcpyAsync(vec + b * nvec * ln, vec1, sizeof(double) * (size_t)(nvec * ln), cudaMemcpyDeviceToDevice, st);
+      cudaMemcpyAsync(info + b, info1, sizeof(int), cudaMemcpyDeviceToDevice, st);
+    }
+    cudaFreeAsync(tmp, st);
+    if (rc != WT_OK) return rc;
+  }
+  g_last_fallbacks = fallback;
+  return check_launch("svd_topk");
 }
 }  // namespace SVD_NS
 }  // namespace wt

@@ -37,7 +37,8 @@ size_t eig_workspace_bytes(int64_t n, int64_t batch);
 // an all-zero slice (its Gram and X V0 are written as zeros without the k loop).
 int eig_precondition(const double* Xt, double* Yt, int64_t m, int64_t n, int64_t ldx, int64_t sx,
                      int64_t batch, int64_t kk, int64_t ldy, int64_t sy, void* ws, size_t ws_bytes, int* n_fallback,
-                     cudaStream_t st, const int* kmask = nullptr);
+                     cudaStream_t st, const int* kmask = nullptr, int* h_flags = nullptr);
+// (h_flags, host, nullable, needs n_fallback: per matrix 1 = preconditioned, 0 = fell back to V0 = I)
 // wt_scale_cols_f64 with an optional per-matrix column limit (columns >= clim[b] untouched).
 int scale_cols_lim(double* M, int64_t rows, int64_t ncols, int64_t ld, int64_t strideM,
                    const double* s, int64_t q, int64_t batch, int mode, double tol,
