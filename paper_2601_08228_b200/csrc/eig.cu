@@ -29,6 +29,8 @@
 //   6. V0 = Q Z: compact-WY blocks of 64 / 128 reflectors (larft + 3 K3 GEMMs each)
 //   7. Y = X V0                                      K3 GEMM
 // Deterministic: fixed thread -> data maps and reduction orders.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <math.h>
 #include <stdint.h>
 #include <string.h>
@@ -1069,6 +1071,32 @@ int launch_panel(double* G, double* VW, double* WV, double* d, double* e, double
 
 #include "eig_sbr.cuh"
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
+PFN_cuTensorMapEncodeTiled_v12000 tmap_encode_fn() {
+  static const PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    return static_cast<PFN_cuTensorMapEncodeTiled_v12000>(nullptr);
+  }();
+  return fn;
+}
+
+// G as [batch][n][n] with 64-row x 16-column boxes, 128-byte swizzle (sbr_update_mult)
+bool make_gmap(CUtensorMap* map, double* G, int64_t n, int64_t batch) {
+  auto enc = tmap_encode_fn();
+  if (!enc) return false;
+  const cuuint64_t dims[3] = {(cuuint64_t)n, (cuuint64_t)n, (cuuint64_t)batch};
+  const cuuint64_t strides[2] = {(cuuint64_t)n * sizeof(double), (cuuint64_t)n * n * sizeof(double)};
+  const cuuint32_t box[3] = {16, FU_T, 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, G, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+             CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 // Two-stage path: wide Grams whose rows below the band fit one row per thread,
 // few leading eigenvectors (the stage-2 back-transformation streams every
 // reflector once per SB_QC columns of Z).
@@ -1126,23 +1154,27 @@ int eig_precondition(const double* Xt, double* Yt, int64_t m, int64_t n, int64_t
     double* AB = Z2;                                   // [batch][n][SB_LDB]
     double* Zp = AB + (size_t)batch * n * SB_LDB;      // [batch][n][B]   Z = A22 V of the current panel
     double* Tp = Zp + (size_t)batch * n * B;           // [batch][B][B]
+    double* Vc = Tp + (size_t)batch * B * B;           // [batch][n][B]   compact copy of the current panel's V rows
+    CUtensorMap gmap;
+    WT_REQUIRE(make_gmap(&gmap, G, n, batch), "eig: cuTensorMapEncodeTiled failed");
     WT_CUDA(cudaMemsetAsync(AB, 0, sizeof(double) * (size_t)batch * n * SB_LDB, st));
     WT_CUDA(cudaMemsetAsync(tau, 0, sizeof(double) * (size_t)batch * n, st));
     // the panel QR reads full rows: mirror the Gram's lower triangle first
     sym_mirror<<<dim3((unsigned)((n + 31) / 32), (unsigned)((n + 31) / 32), (unsigned)batch), dim3(32, 8), 0, st>>>(
         G, ni, flag);
+    // Per panel: QR of the rows below the band (with the previous panel's update
+    // applied to its own columns on load), then one fused pass over the trailing
+    // block (previous update + Z = A22 V), then W -> [V | W], [W | V].
+    if (int r = ensure_smem(sbr_update_mult, FU_SMEM)) return r;
+    int pend = 0;
     for (int64_t c0 = 0; c0 < n; c0 += B) {
-      sbr_panel<<<(unsigned)batch, SB_NT, 0, st>>>(G, AB, tau, Tp, flag, ni, (int)c0);
+      sbr_panel<<<(unsigned)batch, SB_NT, 0, st>>>(G, AB, tau, Tp, flag, ni, (int)c0, VW, WV, pend, Vc);
       const int64_t r0 = c0 + B, mrem = n - r0;
       if (mrem < 2) continue;
-      const int64_t off = r0 * n + r0;
-      if (int r = gemm_f64_lim(0, 0, mrem, B, mrem, 1.0, G + off, n, nn, G + r0 * n + c0, n, nn, 0.0, Zp + r0 * B, B,
-                               n * B, batch, nullptr, glim, st))
-        return r;
+      sbr_update_mult<<<dim3((unsigned)((mrem + FU_T - 1) / FU_T), (unsigned)batch), FU_NT, FU_SMEM, st>>>(
+          gmap, VW, WV, Vc, Zp, flag, ni, (int)c0, pend);
       sbr_w<<<(unsigned)batch, SB_NT, 0, st>>>(G, Zp, Tp, VW, WV, flag, ni, (int)c0);
-      if (int r = ensure_smem(sbr_syr2k, SY_SMEM)) return r;
-      sbr_syr2k<<<dim3((unsigned)((mrem + SY_BN - 1) / SY_BN), (unsigned)((mrem + SY_BM - 1) / SY_BM), (unsigned)batch),
-                  SY_NT, SY_SMEM, st>>>(G, VW, WV, flag, ni, (int)r0);
+      pend = 1;
     }
     const size_t csm = ChaseSmem::bytes(ni);
     if (int r = ensure_smem(sbr_chase, csm)) return r;

@@ -223,6 +223,212 @@ __global__ void __launch_bounds__(SY_NT, 3) sbr_syr2k(double* __restrict__ Gall,
   }
 }
 
+// Fused trailing pass of panel j (r0 = c0 + SB_B, m = n - r0 rows): one read and one
+// write of A22 = A[r0:, r0:] do both
+//   A22 -= VW WV^T          (the previous panel's two-sided update; upd = 0 for panel 0)
+//   Z    = A22 V            (V = this panel's reflectors, rows of the compact copy Vc)
+// One CTA per 64-row strip of A22 walks the strip's 64 x 64 tiles through a FU_ST-stage
+// ring: a tile arrives as four 16-column boxes of a 3-D tensor map over G
+// (cp.async.bulk.tensor, 128-byte swizzle: the accumulator-layout accesses below are
+// bank-conflict-free; rows / columns beyond the matrix are zero-filled on load and
+// clipped on store), the WV and V rows of its columns as two bulk copies.  The
+// rank-24 product runs on the DMMA pipe; the updated 8 x 8 blocks, still in the
+// accumulator layout (row g, columns 2q, 2q+1), are exactly the A-fragment pairs of
+// the k-steps of block x V, so Z's partial needs no shared round trip.  Each warp
+// owns 32 rows x 16 tile columns; the four column-owner warps of a row group are
+// summed in a fixed order at the end (deterministic).  Ten bulk operations per tile
+// (one per row, 193 per tile, held the first version at 3.2 us per tile).
+// grid (ceil(m / 64), batch), 256 threads.
+#ifndef WT_FU_ST
+#define WT_FU_ST 4
+#endif
+#ifndef WT_FU_PD
+#define WT_FU_PD 3
+#endif
+constexpr int FU_T = 64, FU_K = 2 * SB_B, FU_NT = 256, FU_ST = WT_FU_ST, FU_PD = WT_FU_PD;  // ring stages, prefetch distance
+static_assert(FU_PD >= 1 && FU_PD < FU_ST, "prefetch distance");
+constexpr int FU_CB = FU_T * FU_T * 8;                              // tile bytes (4 boxes of 64 x 16)
+constexpr int FU_STAGE_B = FU_CB + FU_T * FU_K * 8 + FU_T * SB_B * 8;  // 51200: a multiple of 1024
+constexpr size_t FU_SMEM = (size_t)FU_ST * FU_STAGE_B + FU_T * FU_K * 8 + 8 * FU_ST + 1024;
+static_assert(FU_STAGE_B % 1024 == 0, "swizzled boxes need 1024-byte aligned stages");
+
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int x, int y, int z, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, int x, int y, int z, const void* src) {
+  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.tile.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(x), "r"(y), "r"(z), "r"(smem_u32(src))
+               : "memory");
+}
+
+__global__ void __launch_bounds__(FU_NT, 1) sbr_update_mult(const __grid_constant__ CUtensorMap gmap,
+                                                           const double* __restrict__ VWall,
+                                                           const double* __restrict__ WVall,
+                                                           const double* __restrict__ Vcall, double* __restrict__ Zall,
+                                                           const int* __restrict__ flag, int n, int c0, int upd) {
+  constexpr int B = SB_B;
+  const int b = blockIdx.y;
+  if (!flag[b]) return;
+  extern __shared__ __align__(1024) unsigned char fraw[];
+  unsigned char* fsm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(fraw) + 1023) & ~(uintptr_t)1023);
+  double* VWs = reinterpret_cast<double*>(fsm + FU_ST * FU_STAGE_B);  // [FU_T][FU_K] the strip's rows of VW
+  uint64_t* bars = reinterpret_cast<uint64_t*>(VWs + FU_T * FU_K);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int r0 = c0 + B, m = n - r0;
+  const int i0 = blockIdx.x * FU_T;
+  const int hrows = min(FU_T, m - i0);
+  const int ntiles = (m + FU_T - 1) / FU_T;
+  const double* VWb = VWall + ((int64_t)b * n + r0) * FU_K;
+  const double* WVb = WVall + ((int64_t)b * n + r0) * FU_K;
+  const double* Vcb = Vcall + ((int64_t)b * n + r0) * B;
+  // no stale NaN bit patterns in the ring: leftovers of partial tiles meet zero blocks
+  for (int e = tid; e < (FU_ST * FU_STAGE_B + FU_T * FU_K * 8) / 8; e += FU_NT) reinterpret_cast<double*>(fsm)[e] = 0.0;
+  if (tid == 0) {
+    for (int s = 0; s < FU_ST; ++s) mbar_init(bars + s, 1);
+    fence_mbar_init();
+  }
+  fence_proxy_async_smem();  // the generic-proxy zero fill precedes the bulk copies into the same bytes
+  __syncthreads();
+  // tile t -> stage t % FU_ST (thread 0 only)
+  auto issue = [&](int t) {
+    const int s = t % FU_ST, j0 = t * FU_T, wc = min(FU_T, m - j0);
+    const int nbox = (wc + 15) / 16;
+    unsigned char* st = fsm + s * FU_STAGE_B;
+    uint32_t bytes = (uint32_t)(nbox * FU_T * 16 * 8 + wc * B * 8 + (upd ? wc * FU_K * 8 : 0));
+    if (t == 0 && upd) bytes += (uint32_t)(hrows * FU_K * 8);
+    mbar_expect_tx(bars + s, bytes);
+    for (int c = 0; c < nbox; ++c) tma_load_3d(st + c * (FU_T * 16 * 8), &gmap, r0 + j0 + 16 * c, r0 + i0, b, bars + s);
+    bulk_g2s(st + FU_CB + FU_T * FU_K * 8, Vcb + (int64_t)j0 * B, (uint32_t)(wc * B * 8), bars + s);
+    if (upd) {
+      bulk_g2s(st + FU_CB, WVb + (int64_t)j0 * FU_K, (uint32_t)(wc * FU_K * 8), bars + s);
+      if (t == 0) bulk_g2s(VWs, VWb + (int64_t)i0 * FU_K, (uint32_t)(hrows * FU_K * 8), bars + s);
+    }
+  };
+  if (tid == 0) {
+    for (int t = 0; t < FU_PD && t < ntiles; ++t) issue(t);
+  }
+  const int g = lane >> 2, q = lane & 3;
+  const int um0 = (warp >> 2) * 32, own = warp & 3;  // warp tile: rows um0 .. um0+31, tile columns 16 own .. 16 own + 15
+  double zacc[4][2][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 2; ++j) zacc[i][j][0] = zacc[i][j][1] = 0.0;
+  for (int t = 0; t < ntiles; ++t) {
+    const int s = t % FU_ST, j0 = t * FU_T, wc = min(FU_T, m - j0);
+    unsigned char* st = fsm + s * FU_STAGE_B;
+    unsigned char* Cb = st + own * (FU_T * 16 * 8);  // my 16-column box: [64 rows][128 B], 16-byte units XOR (row & 7)
+    const double* WVs = reinterpret_cast<const double*>(st + FU_CB);
+    const double* Vs = reinterpret_cast<const double*>(st + FU_CB + FU_T * FU_K * 8);  // [64][B]
+    mbar_wait(bars + s, (uint32_t)((t / FU_ST) & 1));
+    double acc[4][2][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 2; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    if (upd) {
+#pragma unroll
+      for (int ks = 0; ks < FU_K; ks += 8) {
+        double2 af[4], bf[2];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) af[i] = *reinterpret_cast<const double2*>(VWs + (um0 + 8 * i + g) * FU_K + ks + 2 * q);
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+          bf[j] = *reinterpret_cast<const double2*>(WVs + (16 * own + 8 * j + g) * FU_K + ks + 2 * q);
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 2; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[i].x, bf[j].x);
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 2; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[i].y, bf[j].y);
+      }
+    }
+    // updated blocks -> acc (zero-filled beyond the matrix by the loads), and back to the tile
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int r = um0 + 8 * i + g;
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        double2* p = reinterpret_cast<double2*>(Cb + r * 128 + (((4 * j + q) ^ g) << 4));
+        double2 o = *p;
+        o.x -= acc[i][j][0];
+        o.y -= acc[i][j][1];
+        if (upd) *p = o;
+        const bool in = r < hrows && 16 * own + 8 * j + 2 * q < wc;  // (stale rows of VW / WV beyond the matrix)
+        acc[i][j][0] = in ? o.x : 0.0;
+        acc[i][j][1] = in ? o.y : 0.0;
+      }
+    }
+    // Z[my rows] += updated blocks x V[my tile columns]
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      double bx[2], by[2];
+#pragma unroll
+      for (int nf = 0; nf < 2; ++nf) {
+        const int col = 8 * nf + g;  // (V has B = 12 columns: the fragment's columns 12..15 are zeros)
+        bx[nf] = col < B ? Vs[(16 * own + 8 * j + 2 * q) * B + col] : 0.0;
+        by[nf] = col < B ? Vs[(16 * own + 8 * j + 2 * q + 1) * B + col] : 0.0;
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int nf = 0; nf < 2; ++nf) dmma884(zacc[i][nf][0], zacc[i][nf][1], acc[i][j][0], bx[nf]);
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int nf = 0; nf < 2; ++nf) dmma884(zacc[i][nf][0], zacc[i][nf][1], acc[i][j][1], by[nf]);
+    }
+    if (upd) fence_proxy_async_smem();
+    __syncthreads();  // the updated tile is complete; every warp is past tile t - 1's stage
+    if (tid == 0) {
+      if (upd) {
+        const int nbox = (wc + 15) / 16;
+        for (int c = 0; c < nbox; ++c) tma_store_3d(&gmap, r0 + j0 + 16 * c, r0 + i0, b, st + c * (FU_T * 16 * 8));
+        bulk_commit();
+      }
+      // refill: tile t + FU_PD goes to the stage of tile t + FU_PD - FU_ST, whose stores
+      // (FU_ST - FU_PD groups back) must have read their shared bytes
+      if (t + FU_PD < ntiles) {
+        if (upd) asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(FU_ST - FU_PD) : "memory");
+        issue(t + FU_PD);
+      }
+    }
+  }
+  // Z strip = sum over the four column-owner warps of a row group (fixed order), through the ring
+  if (tid == 0 && upd) bulk_wait_all();
+  __syncthreads();
+  {
+    double* zp = reinterpret_cast<double*>(fsm);  // [4][FU_T][16]
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int nf = 0; nf < 2; ++nf)
+        *reinterpret_cast<double2*>(zp + (own * FU_T + um0 + 8 * i + g) * 16 + 8 * nf + 2 * q) =
+            make_double2(zacc[i][nf][0], zacc[i][nf][1]);
+    __syncthreads();
+    for (int e = tid; e < FU_T * (B / 2); e += FU_NT) {
+      const int r = e / (B / 2), c = (e % (B / 2)) * 2;
+      if (r < hrows) {
+        double2 sum = make_double2(0.0, 0.0);
+#pragma unroll
+        for (int o = 0; o < 4; ++o) {
+          const double2 v = *reinterpret_cast<const double2*>(zp + (o * FU_T + r) * 16 + c);
+          sum.x += v.x;
+          sum.y += v.y;
+        }
+        *reinterpret_cast<double2*>(Zall + ((int64_t)b * n + r0 + i0 + r) * B + c) = sum;
+      }
+    }
+  }
+}
+
 // ---------------------------------------------------------------- stage 1 ---
 // Panel c0 (columns c0 .. c0 + SB_B - 1) of matrix b = blockIdx.x, A = G[b] full
 // symmetric n x n (the panel's rows c0.. are current).
@@ -233,9 +439,15 @@ __global__ void __launch_bounds__(SY_NT, 3) sbr_syr2k(double* __restrict__ Gall,
 //     explicitly (zeros above the unit entry, 1 on it: the Y block of the
 //     back-transformation and the B operand of Z = A22 V), tau to tau[c0 + c],
 //     the compact-WY factor T (upper triangular, SB_B x SB_B) to Tp[b].
+//   * pend = 1: the previous panel's two-sided update (A -= VW WV^T, rows >= c0) has
+//     not reached this panel's columns yet (sbr_update_mult applies it to the block
+//     right of them only): every thread applies it to its row on load.
 __global__ void __launch_bounds__(SB_NT, 1) sbr_panel(double* __restrict__ Gall, double* __restrict__ ABall,
                                                      double* __restrict__ tauall, double* __restrict__ Tpall,
-                                                     const int* __restrict__ flag, int n, int c0) {
+                                                     const int* __restrict__ flag, int n, int c0,
+                                                     const double* __restrict__ VWall,
+                                                     const double* __restrict__ WVall, int pend,
+                                                     double* __restrict__ Vcall) {
   constexpr int B = SB_B;
   const int b = blockIdx.x;
   if (!flag[b]) return;
@@ -253,24 +465,48 @@ __global__ void __launch_bounds__(SB_NT, 1) sbr_panel(double* __restrict__ Gall,
   __shared__ double Ts[B][B + 1];
   __shared__ double taus[B];
 
+  __shared__ __align__(16) double wvs[B][2 * B];  // WV rows of the panel's columns (pending update)
+  if (pend) {
+    for (int e = tid; e < bw * 2 * B; e += SB_NT)
+      wvs[e / (2 * B)][e % (2 * B)] = WVall[((int64_t)b * n + c0) * 2 * B + e];
+    __syncthreads();
+  }
+  // my row's panel entries minus the pending update  sum_t VW[row][t] WV[c0 + k][t]
+  auto load_row = [&](int grow, double* row) {
+    const double* ar = A + (int64_t)grow * n + c0;
+#pragma unroll
+    for (int k = 0; k < B; k += 2) {
+      const double2 x = *reinterpret_cast<const double2*>(ar + k);  // (n, c0 even: 16-byte aligned)
+      row[k] = x.x;
+      row[k + 1] = x.y;
+    }
+    if (pend) {
+      const double* vw = VWall + ((int64_t)b * n + grow) * 2 * B;
+#pragma unroll
+      for (int t = 0; t < 2 * B; t += 2) {
+        const double2 v2 = *reinterpret_cast<const double2*>(vw + t);
+#pragma unroll
+        for (int k = 0; k < B; ++k) {
+          const double2 w2 = *reinterpret_cast<const double2*>(&wvs[k][t]);
+          row[k] = fma(-v2.x, w2.x, fma(-v2.y, w2.y, row[k]));
+        }
+      }
+    }
+  };
   // diagonal block -> band (lower part)
   if (tid < bw) {
-    const double* ar = A + (int64_t)(c0 + tid) * n + c0;
-    for (int k = 0; k <= tid; ++k) AB[(int64_t)(c0 + k) * SB_LDB + (tid - k)] = ar[k];
+    double drow[B];
+    load_row(c0 + tid, drow);
+#pragma unroll
+    for (int k = 0; k < B; ++k)
+      if (k <= tid) AB[(int64_t)(c0 + k) * SB_LDB + (tid - k)] = drow[k];
   }
   if (m <= 0) return;
   const bool have = tid < m;
   double row[B];
-  {
-    const double* ar = A + (int64_t)(r0 + tid) * n + c0;
 #pragma unroll
-    for (int k = 0; k < B; k += 2) {
-      double2 x = make_double2(0.0, 0.0);
-      if (have) x = *reinterpret_cast<const double2*>(ar + k);  // (n, c0 even: 16-byte aligned)
-      row[k] = x.x;
-      row[k + 1] = x.y;
-    }
-  }
+  for (int k = 0; k < B; ++k) row[k] = 0.0;
+  if (have) load_row(r0 + tid, row);
   for (int c = 0; c < jb; ++c) {
     const int pb = c & 1;
     // x = my row's entry of column c (rows below the pivot row c only)
@@ -358,6 +594,7 @@ __global__ void __launch_bounds__(SB_NT, 1) sbr_panel(double* __restrict__ Gall,
       o.x = (k < jb && tid >= k) ? (tid == k ? 1.0 : row[k]) : 0.0;
       o.y = (k + 1 < jb && tid >= k + 1) ? (tid == k + 1 ? 1.0 : row[k + 1]) : 0.0;
       *reinterpret_cast<double2*>(ar + k) = o;
+      *reinterpret_cast<double2*>(Vcall + ((int64_t)b * n + r0 + tid) * B + k) = o;  // compact copy: bulk-copied tile rows
     }
   }
 }
