@@ -1155,6 +1155,7 @@ int eig_precondition(const double* Xt, double* Yt, int64_t m, int64_t n, int64_t
     double* Zp = AB + (size_t)batch * n * SB_LDB;      // [batch][n][B]   Z = A22 V of the current panel
     double* Tp = Zp + (size_t)batch * n * B;           // [batch][B][B]
     double* Vc = Tp + (size_t)batch * B * B;           // [batch][n][B]   compact copy of the current panel's V rows
+    double* Np = Vc + (size_t)batch * n * B;           // [batch][strips][B][B] per-strip shares of N = V^T Z
     CUtensorMap gmap;
     WT_REQUIRE(make_gmap(&gmap, G, n, batch), "eig: cuTensorMapEncodeTiled failed");
     WT_CUDA(cudaMemsetAsync(AB, 0, sizeof(double) * (size_t)batch * n * SB_LDB, st));
@@ -1168,12 +1169,28 @@ int eig_precondition(const double* Xt, double* Yt, int64_t m, int64_t n, int64_t
     if (int r = ensure_smem(sbr_update_mult, FU_SMEM)) return r;
     int pend = 0;
     for (int64_t c0 = 0; c0 < n; c0 += B) {
-      sbr_panel<<<(unsigned)batch, SB_NT, 0, st>>>(G, AB, tau, Tp, flag, ni, (int)c0, VW, WV, pend, Vc);
+      {
+        cudaLaunchConfig_t cfg = {};
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = SB_PC;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.gridDim = dim3((unsigned)(batch * SB_PC));
+        cfg.blockDim = dim3(SB_PT);
+        cfg.dynamicSmemBytes = 0;
+        cfg.stream = st;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        WT_CUDA(cudaLaunchKernelEx(&cfg, sbr_panel, G, AB, tau, Tp, (const int*)flag, ni, (int)c0, (const double*)VW,
+                                   (const double*)WV, pend, Vc));
+      }
       const int64_t r0 = c0 + B, mrem = n - r0;
       if (mrem < 2) continue;
       sbr_update_mult<<<dim3((unsigned)((mrem + FU_T - 1) / FU_T), (unsigned)batch), FU_NT, FU_SMEM, st>>>(
-          gmap, VW, WV, Vc, Zp, flag, ni, (int)c0, pend);
-      sbr_w<<<(unsigned)batch, SB_NT, 0, st>>>(G, Zp, Tp, VW, WV, flag, ni, (int)c0);
+          gmap, VW, WV, Vc, Zp, Np, flag, ni, (int)c0, pend);
+      sbr_w<<<(unsigned)batch, SB_NT, 0, st>>>(Vc, Zp, Tp, Np, (int)((mrem + FU_T - 1) / FU_T), VW, WV, flag, ni,
+                                               (int)c0);
       pend = 1;
     }
     const size_t csm = ChaseSmem::bytes(ni);

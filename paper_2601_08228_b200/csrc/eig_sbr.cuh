@@ -8,8 +8,8 @@
 // profiles/r02_bench_launches.csv).  Two stages read the trailing block three
 // times per SB_B columns instead:
 //   stage 1  dense -> band of half-width SB_B: per panel a Householder QR of the
-//            rows below the band (sbr_panel, one 1024-thread CTA per matrix, a
-//            row per thread in registers, one block reduction per column), Z =
+//            rows below the band (sbr_panel, a 4-CTA cluster per matrix, a row per
+//            thread in registers, one cluster reduction per column), Z =
 //            A22 V on K3, W = Z T - V (T^T V^T Z T) / 2 (sbr_w), and the
 //            two-sided update A22 -= V W^T + W V^T on K3.
 //   stage 2  band -> tridiagonal by column-wise bulge chasing (Lang 1993) with
@@ -270,6 +270,7 @@ __global__ void __launch_bounds__(FU_NT, 1) sbr_update_mult(const __grid_constan
                                                            const double* __restrict__ VWall,
                                                            const double* __restrict__ WVall,
                                                            const double* __restrict__ Vcall, double* __restrict__ Zall,
+                                                           double* __restrict__ Npall,
                                                            const int* __restrict__ flag, int n, int c0, int upd) {
   constexpr int B = SB_B;
   const int b = blockIdx.y;
@@ -413,10 +414,12 @@ __global__ void __launch_bounds__(FU_NT, 1) sbr_update_mult(const __grid_constan
         *reinterpret_cast<double2*>(zp + (own * FU_T + um0 + 8 * i + g) * 16 + 8 * nf + 2 * q) =
             make_double2(zacc[i][nf][0], zacc[i][nf][1]);
     __syncthreads();
+    double* zs = zp + 4 * FU_T * 16;   // [FU_T][B] the summed strip
+    double* vs = zs + FU_T * B;        // [FU_T][B] the strip's rows of V
     for (int e = tid; e < FU_T * (B / 2); e += FU_NT) {
       const int r = e / (B / 2), c = (e % (B / 2)) * 2;
+      double2 sum = make_double2(0.0, 0.0), vv = make_double2(0.0, 0.0);
       if (r < hrows) {
-        double2 sum = make_double2(0.0, 0.0);
 #pragma unroll
         for (int o = 0; o < 4; ++o) {
           const double2 v = *reinterpret_cast<const double2*>(zp + (o * FU_T + r) * 16 + c);
@@ -424,7 +427,24 @@ __global__ void __launch_bounds__(FU_NT, 1) sbr_update_mult(const __grid_constan
           sum.y += v.y;
         }
         *reinterpret_cast<double2*>(Zall + ((int64_t)b * n + r0 + i0 + r) * B + c) = sum;
+        vv = *reinterpret_cast<const double2*>(Vcb + (int64_t)(i0 + r) * B + c);
       }
+      *reinterpret_cast<double2*>(zs + r * B + c) = sum;
+      *reinterpret_cast<double2*>(vs + r * B + c) = vv;
+    }
+    __syncthreads();
+    // the strip's share of N = V^T Z (SB_B x SB_B; sbr_w sums the strips in order)
+    if (tid < B * B) {
+      const int k = tid / B, l = tid % B;
+      double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#pragma unroll 4
+      for (int r = 0; r < FU_T; r += 4) {
+        s0 = fma(vs[r * B + k], zs[r * B + l], s0);
+        s1 = fma(vs[(r + 1) * B + k], zs[(r + 1) * B + l], s1);
+        s2 = fma(vs[(r + 2) * B + k], zs[(r + 2) * B + l], s2);
+        s3 = fma(vs[(r + 3) * B + k], zs[(r + 3) * B + l], s3);
+      }
+      Npall[((int64_t)b * gridDim.x + blockIdx.x) * B * B + tid] = (s0 + s1) + (s2 + s3);
     }
   }
 }
@@ -442,32 +462,39 @@ __global__ void __launch_bounds__(FU_NT, 1) sbr_update_mult(const __grid_constan
 //   * pend = 1: the previous panel's two-sided update (A -= VW WV^T, rows >= c0) has
 //     not reached this panel's columns yet (sbr_update_mult applies it to the block
 //     right of them only): every thread applies it to its row on load.
-__global__ void __launch_bounds__(SB_NT, 1) sbr_panel(double* __restrict__ Gall, double* __restrict__ ABall,
+constexpr int SB_PC = 4;               // CTAs of the panel kernel's cluster (rows dealt in contiguous quarters)
+constexpr int SB_PT = SB_NT / SB_PC;   // its threads per CTA: one row below the band per thread
+constexpr int SB_PW = SB_PT / 32;
+__global__ void __launch_bounds__(SB_PT, 1) sbr_panel(double* __restrict__ Gall, double* __restrict__ ABall,
                                                      double* __restrict__ tauall, double* __restrict__ Tpall,
                                                      const int* __restrict__ flag, int n, int c0,
                                                      const double* __restrict__ VWall,
                                                      const double* __restrict__ WVall, int pend,
                                                      double* __restrict__ Vcall) {
   constexpr int B = SB_B;
-  const int b = blockIdx.x;
-  if (!flag[b]) return;
+  const int b = blockIdx.x / SB_PC;
+  if (!flag[b]) return;  // cluster-uniform
+  const int rank = cl_rank();
   double* A = Gall + (int64_t)b * n * n;
   double* AB = ABall + (int64_t)b * n * SB_LDB;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int gt = rank * SB_PT + tid;  // my row below the band: r0 + gt
   const int bw = min(B, n - c0);  // panel width
   const int r0 = c0 + B;
   const int m = max(n - r0, 0);            // rows below the band
   const int jb = max(min(B, m - 1), 0);    // reflectors of this panel
-  __shared__ double wp[2][32][16];         // per-warp partial sums (double-buffered by column parity)
-  __shared__ double gsm[2][16];            // block sums
-  __shared__ double pivrow[2][16];         // the pivot row's entries
+  __shared__ double wp[2][SB_PW][16];      // per-warp partial sums (double-buffered by column parity)
+  __shared__ double gpart[2][16];          // this CTA's share of the column sums (read by the whole cluster)
+  __shared__ double pivrow[2][16];         // the pivot row's entries (rank 0; read by the whole cluster)
   __shared__ double vdot[B][B];            // V[:, k]^T v_c, k < c
   __shared__ double Ts[B][B + 1];
   __shared__ double taus[B];
+  __shared__ double coef[2][16];  // tau * v^T P[:, k] of the current column (k > c)
+  __shared__ double hs[2][2];     // scale, beta
 
   __shared__ __align__(16) double wvs[B][2 * B];  // WV rows of the panel's columns (pending update)
   if (pend) {
-    for (int e = tid; e < bw * 2 * B; e += SB_NT)
+    for (int e = tid; e < bw * 2 * B; e += SB_PT)
       wvs[e / (2 * B)][e % (2 * B)] = WVall[((int64_t)b * n + c0) * 2 * B + e];
     __syncthreads();
   }
@@ -483,87 +510,94 @@ __global__ void __launch_bounds__(SB_NT, 1) sbr_panel(double* __restrict__ Gall,
     if (pend) {
       const double* vw = VWall + ((int64_t)b * n + grow) * 2 * B;
 #pragma unroll
-      for (int t = 0; t < 2 * B; t += 2) {
-        const double2 v2 = *reinterpret_cast<const double2*>(vw + t);
+      for (int t0 = 0; t0 < 2 * B; t0 += B) {  // two batches of independent loads (L2 latency paid twice, not 12 times)
+        double2 v2[B / 2];
 #pragma unroll
-        for (int k = 0; k < B; ++k) {
-          const double2 w2 = *reinterpret_cast<const double2*>(&wvs[k][t]);
-          row[k] = fma(-v2.x, w2.x, fma(-v2.y, w2.y, row[k]));
+        for (int u = 0; u < B / 2; ++u) v2[u] = *reinterpret_cast<const double2*>(vw + t0 + 2 * u);
+#pragma unroll
+        for (int u = 0; u < B / 2; ++u) {
+#pragma unroll
+          for (int k = 0; k < B; ++k) {
+            const double2 w2 = *reinterpret_cast<const double2*>(&wvs[k][t0 + 2 * u]);
+            row[k] = fma(-v2[u].x, w2.x, fma(-v2[u].y, w2.y, row[k]));
+          }
         }
       }
     }
   };
-  // diagonal block -> band (lower part)
-  if (tid < bw) {
+  // diagonal block -> band (lower part); the last CTA has the fewest QR rows to load
+  if (rank == SB_PC - 1 && tid < bw) {
     double drow[B];
     load_row(c0 + tid, drow);
 #pragma unroll
     for (int k = 0; k < B; ++k)
       if (k <= tid) AB[(int64_t)(c0 + k) * SB_LDB + (tid - k)] = drow[k];
   }
-  if (m <= 0) return;
-  const bool have = tid < m;
+  if (m <= 0) return;  // cluster-uniform
+  const bool have = gt < m;
   double row[B];
 #pragma unroll
   for (int k = 0; k < B; ++k) row[k] = 0.0;
-  if (have) load_row(r0 + tid, row);
-  for (int c = 0; c < jb; ++c) {
-    const int pb = c & 1;
-    // x = my row's entry of column c (rows below the pivot row c only)
-    double x = 0.0;
+  if (have) load_row(r0 + gt, row);
 #pragma unroll
-    for (int k = 0; k < B; ++k)
-      if (k == c) x = row[k];
-    const double xt = (have && tid > c) ? x : 0.0;
-    int idx;
-    const double sum = warp_sum16([&](int i) { return i < B ? xt * row[i < B ? i : 0] : 0.0; }, lane, idx);
-    if ((lane & 1) == 0) wp[pb][warp][idx] = sum;
-    if (tid == c) {
+  for (int c = 0; c < B; ++c) {  // (unrolled: static register indices)
+    if (c < jb) {
+      const int pb = c & 1;
+      // x = my row's entry of column c (rows below the pivot row c only)
+      const double x = row[c];
+      const double xt = (have && gt > c) ? x : 0.0;
+      int idx;
+      const double sum = warp_sum16([&](int i) { return i < B ? xt * row[i < B ? i : 0] : 0.0; }, lane, idx);
+      if ((lane & 1) == 0) wp[pb][warp][idx] = sum;
+      if (gt == c) {  // (rank 0)
 #pragma unroll
-      for (int k = 0; k < B; ++k) pivrow[pb][k] = row[k];
-    }
-    __syncthreads();
-    if (tid < 16) {
-      double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-#pragma unroll
-      for (int w = 0; w < 32; w += 4) {
-        s0 += wp[pb][w][tid];
-        s1 += wp[pb][w + 1][tid];
-        s2 += wp[pb][w + 2][tid];
-        s3 += wp[pb][w + 3][tid];
+        for (int k = 0; k < B; ++k) pivrow[pb][k] = row[k];
       }
-      gsm[pb][tid] = (s0 + s1) + (s2 + s3);
-    }
-    __syncthreads();
-    double alpha = 0.0, ss = 0.0;
+      __syncthreads();
+      if (tid < 16) {
+        double s0 = 0.0, s1 = 0.0;
 #pragma unroll
-    for (int k = 0; k < B; ++k)
-      if (k == c) {
-        alpha = pivrow[pb][k];
-        ss = gsm[pb][k];
-      }
-    double beta, tau, scale;
-    house_gen(alpha, ss, beta, tau, scale);
-    if (tid == 0) {
-      taus[c] = tau;
-      for (int k = 0; k < c; ++k) vdot[k][c] = fma(scale, gsm[pb][k], pivrow[pb][k]);
-    }
-    if (have && tid >= c) {
-      const double vi = tid == c ? 1.0 : x * scale;
-#pragma unroll
-      for (int k = 0; k < B; ++k) {
-        if (k > c) {
-          const double s = fma(scale, gsm[pb][k], pivrow[pb][k]);  // v^T P[:, k]
-          row[k] = fma(-tau * s, vi, row[k]);
-        } else if (k == c) {
-          row[k] = tid == c ? beta : vi;
+        for (int w = 0; w < SB_PW; w += 2) {
+          s0 += wp[pb][w][tid];
+          s1 += wp[pb][w + 1][tid];
         }
+        gpart[pb][tid] = s0 + s1;
+      }
+      cl_sync();  // every CTA's share and the pivot row are visible
+      if (warp == 0) {  // cluster sums, reflector and update coefficients (every CTA, identically)
+        double gk = 0.0, pk = 0.0;
+        if (lane < 16) {
+#pragma unroll
+          for (int r = 0; r < SB_PC; ++r) gk += cl_map(&gpart[pb][lane], r)[0];
+          pk = cl_map(&pivrow[pb][lane], 0)[0];
+        }
+        const double ss = __shfl_sync(0xffffffffu, gk, c);
+        const double alpha = __shfl_sync(0xffffffffu, pk, c);
+        double beta, tau, scale;
+        house_gen(alpha, ss, beta, tau, scale);
+        if (lane < B) {
+          const double sk = fma(scale, gk, pk);  // v^T P[:, k] (k > c), V[:, k]^T v (k < c)
+          coef[pb][lane] = tau * sk;
+          if (lane < c) vdot[lane][c] = sk;
+        }
+        if (lane == 0) {
+          hs[pb][0] = scale;
+          hs[pb][1] = beta;
+          taus[c] = tau;
+        }
+      }
+      __syncthreads();
+      if (have && gt >= c) {
+        const double vi = gt == c ? 1.0 : x * hs[pb][0];
+#pragma unroll
+        for (int k = c + 1; k < B; ++k) row[k] = fma(-coef[pb][k], vi, row[k]);
+        row[c] = gt == c ? hs[pb][1] : vi;
       }
     }
   }
   __syncthreads();
   // compact-WY factor: T_cc = tau_c, T[0:c, c] = -tau_c T[0:c, 0:c] vdot[0:c, c]
-  if (warp == 0) {
+  if (rank == 0 && warp == 0) {
     for (int k = lane; k < B * (B + 1); k += 32) (&Ts[0][0])[k] = 0.0;
     __syncwarp();
     for (int c = 0; c < jb; ++c) {
@@ -579,83 +613,68 @@ __global__ void __launch_bounds__(SB_NT, 1) sbr_panel(double* __restrict__ Gall,
     for (int k = lane; k < B * B; k += 32) Tp[k] = Ts[k / B][k % B];
     if (lane < B) tauall[(int64_t)b * n + c0 + lane] = lane < jb ? taus[lane] : 0.0;
   }
-  // R -> band: row i = tid, column k >= i: distance B + i - k
-  if (have && tid < B) {
+  // R -> band: row i = gt, column k >= i: distance B + i - k
+  if (have && gt < B) {
 #pragma unroll
     for (int k = 0; k < B; ++k)
-      if (k >= tid) AB[(int64_t)(c0 + k) * SB_LDB + (B + tid - k)] = row[k];
+      if (k >= gt) AB[(int64_t)(c0 + k) * SB_LDB + (B + gt - k)] = row[k];
   }
   // explicit reflectors over the panel columns (columns >= jb: zeros)
   if (have) {
-    double* ar = A + (int64_t)(r0 + tid) * n + c0;
+    double* ar = A + (int64_t)(r0 + gt) * n + c0;
 #pragma unroll
     for (int k = 0; k < B; k += 2) {
       double2 o;
-      o.x = (k < jb && tid >= k) ? (tid == k ? 1.0 : row[k]) : 0.0;
-      o.y = (k + 1 < jb && tid >= k + 1) ? (tid == k + 1 ? 1.0 : row[k + 1]) : 0.0;
+      o.x = (k < jb && gt >= k) ? (gt == k ? 1.0 : row[k]) : 0.0;
+      o.y = (k + 1 < jb && gt >= k + 1) ? (gt == k + 1 ? 1.0 : row[k + 1]) : 0.0;
       *reinterpret_cast<double2*>(ar + k) = o;
-      *reinterpret_cast<double2*>(Vcall + ((int64_t)b * n + r0 + tid) * B + k) = o;  // compact copy: bulk-copied tile rows
+      *reinterpret_cast<double2*>(Vcall + ((int64_t)b * n + r0 + gt) * B + k) = o;  // compact copy: bulk-copied tile rows
     }
   }
+  cl_sync();  // no CTA exits while the others may still read its shared memory
 }
 
 // W = Z T - V (T^T (V^T Z) T) / 2 for the panel at c0 (rows r0 = c0 + SB_B ..), Z = A22 V
-// (m x SB_B, pitch SB_B) from K3; writes the rows of VW = [V | W] and WV = [W | V]
-// (pitch 2 SB_B, row index = global row) for the rank-2 SB_B update on K3.
-__global__ void __launch_bounds__(SB_NT, 1) sbr_w(const double* __restrict__ Gall, const double* __restrict__ Zall,
-                                                 const double* __restrict__ Tpall, double* __restrict__ VWall,
-                                                 double* __restrict__ WVall, const int* __restrict__ flag, int n,
-                                                 int c0) {
+// (m x SB_B, pitch SB_B) and the per-strip shares of N = V^T Z from sbr_update_mult;
+// writes the rows of VW = [V | W] and WV = [W | V] (pitch 2 SB_B, row index = global
+// row) for the next panel's pending update and trailing pass.  One thread per row.
+__global__ void __launch_bounds__(SB_NT, 1) sbr_w(const double* __restrict__ Vcall, const double* __restrict__ Zall,
+                                                 const double* __restrict__ Tpall, const double* __restrict__ Npall,
+                                                 int nstrips, double* __restrict__ VWall, double* __restrict__ WVall,
+                                                 const int* __restrict__ flag, int n, int c0) {
   constexpr int B = SB_B;
   const int b = blockIdx.x;
   if (!flag[b]) return;
-  const double* A = Gall + (int64_t)b * n * n;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tid = threadIdx.x;
   const int r0 = c0 + B;
   const int m = n - r0;
   const bool have = tid < m;
-  constexpr int HB = B / 2;
-  __shared__ double wp[32][HB][16];  // per-warp partials of N = V^T Z (half of V's columns at a time)
-  __shared__ double Ns[B][B], Ts[B][B], NT[B][B], Ss[B][B];
-  for (int k = tid; k < B * B; k += SB_NT) (&Ts[0][0])[k] = Tpall[(int64_t)b * B * B + k];
-  // (V is re-read from the panel columns where needed: z, v and w rows together
-  // do not fit 64 registers)
-  const double* vr = A + (int64_t)(r0 + (have ? tid : 0)) * n + c0;
-  double z[B];
+  __shared__ __align__(16) double Ns[B][B], Ts[B][B], NT[B][B], Ss[B][B];
+  if (tid < B * B) {
+    Ts[tid / B][tid % B] = Tpall[(int64_t)b * B * B + tid];
+    double s = 0.0;
+    for (int q = 0; q < nstrips; ++q) s += Npall[((int64_t)b * nstrips + q) * B * B + tid];
+    Ns[tid / B][tid % B] = s;
+  }
+  // my rows of Z and V (both contiguous SB_B-wide rows)
+  double z[B], v[B];
   {
     const double* zr = Zall + ((int64_t)b * n + r0 + tid) * B;
+    const double* vr = Vcall + ((int64_t)b * n + r0 + tid) * B;
 #pragma unroll
     for (int k = 0; k < B; k += 2) {
-      double2 x = make_double2(0.0, 0.0);
-      if (have) x = *reinterpret_cast<const double2*>(zr + k);
+      double2 x = make_double2(0.0, 0.0), y = make_double2(0.0, 0.0);
+      if (have) {
+        x = *reinterpret_cast<const double2*>(zr + k);
+        y = *reinterpret_cast<const double2*>(vr + k);
+      }
       z[k] = x.x;
       z[k + 1] = x.y;
+      v[k] = y.x;
+      v[k + 1] = y.y;
     }
   }
-#pragma unroll 1
-  for (int half = 0; half < 2; ++half) {
-#pragma unroll
-    for (int kh = 0; kh < HB; ++kh) {
-      int idx;
-      const double vk = have ? vr[half * HB + kh] : 0.0;
-      const double sum = warp_sum16([&](int i) { return i < B ? vk * z[i < B ? i : 0] : 0.0; }, lane, idx);
-      if ((lane & 1) == 0) wp[warp][kh][idx] = sum;
-    }
-    __syncthreads();
-    if (tid < HB * B) {
-      const int kh = tid / B, l = tid % B;
-      double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-#pragma unroll
-      for (int w = 0; w < 32; w += 4) {
-        s0 += wp[w][kh][l];
-        s1 += wp[w + 1][kh][l];
-        s2 += wp[w + 2][kh][l];
-        s3 += wp[w + 3][kh][l];
-      }
-      Ns[half * HB + kh][l] = (s0 + s1) + (s2 + s3);
-    }
-    __syncthreads();
-  }
+  __syncthreads();
   if (tid < B * B) {  // NT = N T
     const int k = tid / B, l = tid % B;
     double s = 0.0;
@@ -675,23 +694,30 @@ __global__ void __launch_bounds__(SB_NT, 1) sbr_w(const double* __restrict__ Gal
   if (have) {
     double* vw = VWall + ((int64_t)b * n + r0 + tid) * 2 * B;
     double* wv = WVall + ((int64_t)b * n + r0 + tid) * 2 * B;
-#pragma unroll 1
-    for (int l0 = 0; l0 < B; l0 += 2) {
-      double w0 = 0.0, w1 = 0.0, u0 = 0.0, u1 = 0.0;
+    // W row in three groups of four columns (z, v and a full w row exceed 64 registers)
+#pragma unroll
+    for (int l0 = 0; l0 < B; l0 += 4) {
+      double w[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
       for (int k = 0; k < B; ++k) {
-        const double vk = vr[k];
-        w0 = fma(z[k], Ts[k][l0], w0);
-        w1 = fma(z[k], Ts[k][l0 + 1], w1);
-        u0 = fma(vk, Ss[k][l0], u0);
-        u1 = fma(vk, Ss[k][l0 + 1], u1);
+        const double2 t01 = *reinterpret_cast<const double2*>(&Ts[k][l0]);
+        const double2 t23 = *reinterpret_cast<const double2*>(&Ts[k][l0 + 2]);
+        const double2 s01 = *reinterpret_cast<const double2*>(&Ss[k][l0]);
+        const double2 s23 = *reinterpret_cast<const double2*>(&Ss[k][l0 + 2]);
+        w[0] = fma(z[k], t01.x, fma(-v[k], s01.x, w[0]));
+        w[1] = fma(z[k], t01.y, fma(-v[k], s01.y, w[1]));
+        w[2] = fma(z[k], t23.x, fma(-v[k], s23.x, w[2]));
+        w[3] = fma(z[k], t23.y, fma(-v[k], s23.y, w[3]));
       }
-      const double2 ww = make_double2(w0 - u0, w1 - u1);
-      const double2 vv = *reinterpret_cast<const double2*>(vr + l0);
-      *reinterpret_cast<double2*>(vw + l0) = vv;
-      *reinterpret_cast<double2*>(vw + B + l0) = ww;
-      *reinterpret_cast<double2*>(wv + l0) = ww;
-      *reinterpret_cast<double2*>(wv + B + l0) = vv;
+#pragma unroll
+      for (int u = 0; u < 4; u += 2) {
+        const double2 ww = make_double2(w[u], w[u + 1]);
+        const double2 vv = make_double2(v[l0 + u], v[l0 + u + 1]);
+        *reinterpret_cast<double2*>(vw + l0 + u) = vv;
+        *reinterpret_cast<double2*>(vw + B + l0 + u) = ww;
+        *reinterpret_cast<double2*>(wv + l0 + u) = ww;
+        *reinterpret_cast<double2*>(wv + B + l0 + u) = vv;
+      }
     }
   }
 }
