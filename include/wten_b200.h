@@ -269,7 +269,8 @@ int wt_slice_reduce_f64(const double* x, const double* y, int64_t n, int64_t nsl
 #define WT_OPT_SVD_TRACE 6        /* 1: K4 per-sweep convergence trace on stderr */
 #define WT_OPT_EIG_PROFILE 7      /* 1: preconditioner phase times on stderr */
 #define WT_OPT_EIG_TWOSTAGE 8     /* 1: two-stage tridiagonalization for wide Grams in leading-triplet mode (default) */
-#define WT_OPT_COUNT 9
+#define WT_OPT_GEMM_TMA 9         /* 1: K3 large tiles fed by tensor-map TMA boxes (default); 0: cp.async ring */
+#define WT_OPT_COUNT 10
 int wt_set_option(int option, int value);
 
 /* Sweeps used by the last wt_svd_jacobi_f64 call on the calling thread, and

@@ -245,11 +245,14 @@ __global__ void __launch_bounds__(SY_NT, 3) sbr_syr2k(double* __restrict__ Gall,
 #ifndef WT_FU_PD
 #define WT_FU_PD 3
 #endif
+#ifndef WT_FU_OCC
+#define WT_FU_OCC 1
+#endif
 constexpr int FU_T = 64, FU_K = 2 * SB_B, FU_NT = 256, FU_ST = WT_FU_ST, FU_PD = WT_FU_PD;  // ring stages, prefetch distance
 static_assert(FU_PD >= 1 && FU_PD < FU_ST, "prefetch distance");
 constexpr int FU_CB = FU_T * FU_T * 8;                              // tile bytes (4 boxes of 64 x 16)
 constexpr int FU_STAGE_B = FU_CB + FU_T * FU_K * 8 + FU_T * SB_B * 8;  // 51200: a multiple of 1024
-constexpr size_t FU_SMEM = (size_t)FU_ST * FU_STAGE_B + FU_T * FU_K * 8 + 8 * FU_ST + 1024;
+constexpr size_t FU_SMEM = (size_t)FU_ST * FU_STAGE_B + FU_T * FU_K * 8 + 8 * FU_ST;  // (FU_ST = 2, two CTAs per SM: 13.9 vs 13.3 ms)
 static_assert(FU_STAGE_B % 1024 == 0, "swizzled boxes need 1024-byte aligned stages");
 
 __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int x, int y, int z, uint64_t* bar) {
@@ -266,7 +269,7 @@ __device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, int x, int 
                : "memory");
 }
 
-__global__ void __launch_bounds__(FU_NT, 1) sbr_update_mult(const __grid_constant__ CUtensorMap gmap,
+__global__ void __launch_bounds__(FU_NT, WT_FU_OCC) sbr_update_mult(const __grid_constant__ CUtensorMap gmap,
                                                            const double* __restrict__ VWall,
                                                            const double* __restrict__ WVall,
                                                            const double* __restrict__ Vcall, double* __restrict__ Zall,
@@ -275,8 +278,8 @@ __global__ void __launch_bounds__(FU_NT, 1) sbr_update_mult(const __grid_constan
   constexpr int B = SB_B;
   const int b = blockIdx.y;
   if (!flag[b]) return;
-  extern __shared__ __align__(1024) unsigned char fraw[];
-  unsigned char* fsm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(fraw) + 1023) & ~(uintptr_t)1023);
+  extern __shared__ __align__(1024) unsigned char fsm[];
+  if ((smem_u32(fsm) & 1023u) != 0) __trap();  // swizzled boxes need 1024-byte aligned stages (no static shared memory here)
   double* VWs = reinterpret_cast<double*>(fsm + FU_ST * FU_STAGE_B);  // [FU_T][FU_K] the strip's rows of VW
   uint64_t* bars = reinterpret_cast<uint64_t*>(VWs + FU_T * FU_K);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -905,7 +908,7 @@ __global__ void __launch_bounds__(SB_CW * 32, 1) sbr_chase(const double* __restr
 // row half).  The next sweep's reflector row is staged in shared memory while the
 // current one is applied.
 struct Q2Smem {
-  static size_t bytes(int n) { return sizeof(double) * ((size_t)n * (SB_QC + 1) + 2 * (size_t)(n + 2)); }
+  static size_t bytes(int n) { return sizeof(double) * ((size_t)n * (SB_QC + 1) + 3 * (size_t)(n + 2)); }
 };
 __global__ void __launch_bounds__(SB_QT, 1) sbr_apply_q2(const double* __restrict__ Gall, double* __restrict__ Zall,
                                                         const int* __restrict__ flag, int n, int kk) {
@@ -914,7 +917,7 @@ __global__ void __launch_bounds__(SB_QT, 1) sbr_apply_q2(const double* __restric
   if (!flag[b]) return;
   extern __shared__ __align__(16) double qsm[];
   double* Zs = qsm;                       // [n][LDZ]
-  double* vbuf = Zs + (size_t)n * LDZ;    // [2][n + 2]
+  double* vbuf = Zs + (size_t)n * LDZ;    // [3][n + 2]
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int NWQ = SB_QT / 32;
   const int col0 = blockIdx.x * SB_QC;
@@ -927,15 +930,22 @@ __global__ void __launch_bounds__(SB_QT, 1) sbr_apply_q2(const double* __restric
   }
   const int slast = n - 3;
   if (slast < 0) return;
-  for (int i = slast + 1 + tid; i < n; i += SB_QT) vbuf[(slast & 1) * (n + 2) + i] = VQ[(int64_t)slast * n + i];
+  // the reflector rows of the next two sweeps travel by cp.async while the current one is applied
+  auto fetch = [&](int sw) {
+    if (sw >= 0) {
+      double* nb = vbuf + (sw % 3) * (n + 2);
+      for (int i = sw + 1 + tid; i < n; i += SB_QT) cp_async_zfill<8>(nb + i, VQ + (int64_t)sw * n + i, true);
+    }
+    cp_async_commit();
+  };
+  fetch(slast);
+  fetch(slast - 1);
+  cp_async_wait<1>();
   __syncthreads();
   const int cc = lane & 15, rh = lane >> 4;
   for (int s = slast; s >= 0; --s) {
-    const double* vb = vbuf + (s & 1) * (n + 2);
-    if (s > 0) {  // stage the next sweep's reflectors
-      double* nb = vbuf + ((s - 1) & 1) * (n + 2);
-      for (int i = s + tid; i < n; i += SB_QT) nb[i] = VQ[(int64_t)(s - 1) * n + i];
-    }
+    const double* vb = vbuf + (s % 3) * (n + 2);
+    fetch(s - 2);
     for (int r0 = s + 1 + warp * B; r0 < n; r0 += NWQ * B) {
       const int L = min(B, n - r0);
       if (L < 2) break;
@@ -957,6 +967,7 @@ __global__ void __launch_bounds__(SB_QT, 1) sbr_apply_q2(const double* __restric
         if (r < L) Zs[(r0 + r) * LDZ + cc] = fma(-y, vv[i], zz[i]);
       }
     }
+    cp_async_wait<1>();  // sweep s - 1's row has landed (only the newest group may be pending)
     __syncthreads();
   }
   for (int e = tid; e < n * SB_QC; e += SB_QT) {

@@ -13,6 +13,9 @@
 // (BM/WM) x (BN/WN) held as DMMA accumulators.
 //
 // Row-major semantics: C[b] = alpha * op(A[b]) * op(B[b]) + beta * C[b].
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include <algorithm>
 
 #include "wt_common.cuh"
@@ -212,6 +215,208 @@ __global__ void __launch_bounds__(WM* WN * 32, (WM * WN == 8 && BN == 64) ? 2 : 
   }
 }
 
+
+// ------------------------------------------------------------- TMA variant ---
+// The same CTA / warp tiling fed by tensor-map boxes (cp.async.bulk.tensor, SASS
+// UTMALDG) through a full / empty mbarrier ring instead of the cp.async ring and
+// its CTA barrier per k tile: one elected thread issues the boxes of a stage, the
+// four warps release a stage with one mbarrier arrive each.  Operands are 3-D
+// tensors (inner extent, outer extent, batch) with the 128-byte swizzle:
+//   k-contiguous operand ([m][k] / [n][k]):  one box {16 k, BM} per stage; a
+//     fragment pair (k, k+1) is one LDS.128 at 16-byte unit ((k/2) ^ (row & 7));
+//   m/n-contiguous operand ([k][m] / [k][n]): BM/16 boxes {16 m, 16 k}; a fragment
+//     pair is two LDS.64 (rows k, k+1 of the box).
+// Rows / columns / k beyond the matrices are zero-filled by the TMA unit, so edge
+// tiles and K tails need no predicates.  Used for the large-tile case without
+// per-matrix limits; everything else stays on the cp.async kernel.
+constexpr int TSTAGES = 4;
+struct TmaArgs {
+  CUtensorMap a, b;
+};
+
+__device__ __forceinline__ void tma_box_3d(void* dst, const CUtensorMap* map, int x, int y, int z, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+template <int BM, int BN, int WM, int WN, bool TA, bool TB>
+__global__ void __launch_bounds__(WM* WN * 32, 2) gemm_f64_tma_kernel(GemmArgs g, const __grid_constant__ TmaArgs tm) {
+  constexpr int NT = WM * WN * 32, NWARP = WM * WN;
+  constexpr int WTM = BM / WM, WTN = BN / WN;
+  constexpr int FM = WTM / 8, FN = WTN / 8;
+  constexpr int A_BYTES = BM * BK * 8, B_BYTES = BN * BK * 8, STAGE_BYTES = A_BYTES + B_BYTES;
+  static_assert(BK == 16 && A_BYTES % 1024 == 0 && B_BYTES % 1024 == 0, "swizzled boxes: 16 doubles per row");
+  extern __shared__ __align__(1024) unsigned char tsm[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(tsm + TSTAGES * STAGE_BYTES);
+  uint64_t* empty = full + TSTAGES;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm0 = (warp / WN) * WTM, wn0 = (warp % WN) * WTN;
+  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+  if (g.lower && n0 >= m0 + BM) return;
+  const int b = blockIdx.z;
+  const int nk = (int)((g.K + BK - 1) / BK);
+  if ((smem_u32(tsm) & 1023u) != 0) __trap();
+  if (tid == 0) {
+    for (int s = 0; s < TSTAGES; ++s) {
+      mbar_init(full + s, 1);
+      mbar_init(empty + s, NWARP);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  auto issue = [&](int kt) {  // thread 0
+    const int s = kt % TSTAGES, k0 = kt * BK;
+    unsigned char* As = tsm + s * STAGE_BYTES;
+    unsigned char* Bs = As + A_BYTES;
+    mbar_expect_tx(full + s, STAGE_BYTES);
+    if (!TA) tma_box_3d(As, &tm.a, k0, m0, b, full + s);
+    else
+      for (int c = 0; c < BM / 16; ++c) tma_box_3d(As + c * 2048, &tm.a, m0 + 16 * c, k0, b, full + s);
+    if (TB) tma_box_3d(Bs, &tm.b, k0, n0, b, full + s);
+    else
+      for (int c = 0; c < BN / 16; ++c) tma_box_3d(Bs + c * 2048, &tm.b, n0 + 16 * c, k0, b, full + s);
+  };
+  if (tid == 0)
+    for (int kt = 0; kt < TSTAGES - 1 && kt < nk; ++kt) issue(kt);
+
+  double acc[FM][FN][2];
+#pragma unroll
+  for (int i = 0; i < FM; ++i)
+#pragma unroll
+    for (int j = 0; j < FN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  const int g8 = lane >> 2, q = lane & 3;
+  for (int kt = 0; kt < nk; ++kt) {
+    const int s = kt % TSTAGES;
+    // refill the stage released one iteration ago (its consumers are mostly through)
+    if (tid == 0) {
+      const int nxt = kt + TSTAGES - 1;
+      if (nxt < nk) {
+        if (nxt >= TSTAGES) mbar_wait(empty + nxt % TSTAGES, (uint32_t)(((nxt / TSTAGES) - 1) & 1));
+        issue(nxt);
+      }
+    }
+    __syncwarp();
+    mbar_wait(full + s, (uint32_t)((kt / TSTAGES) & 1));
+    const unsigned char* As = tsm + s * STAGE_BYTES;
+    const unsigned char* Bs = As + A_BYTES;
+#pragma unroll
+    for (int ks = 0; ks < BK; ks += 8) {
+      double2 af[FM], bf[FN];
+      const int kk = ks + 2 * q;
+#pragma unroll
+      for (int i = 0; i < FM; ++i) {
+        const int mm = wm0 + i * 8 + g8;
+        if (!TA) {
+          af[i] = *reinterpret_cast<const double2*>(As + mm * 128 + (((kk >> 1) ^ (mm & 7)) << 4));
+        } else {  // box (mm / 16): rows k, 16-byte unit ((mm % 16) / 2) ^ (k & 7)
+          const unsigned char* bx = As + (mm >> 4) * 2048 + (mm & 1) * 8;
+          const int u = (mm & 15) >> 1;
+          af[i].x = *reinterpret_cast<const double*>(bx + kk * 128 + ((u ^ (kk & 7)) << 4));
+          af[i].y = *reinterpret_cast<const double*>(bx + (kk + 1) * 128 + ((u ^ ((kk + 1) & 7)) << 4));
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < FN; ++j) {
+        const int nn = wn0 + j * 8 + g8;
+        if (TB) {
+          bf[j] = *reinterpret_cast<const double2*>(Bs + nn * 128 + (((kk >> 1) ^ (nn & 7)) << 4));
+        } else {
+          const unsigned char* bx = Bs + (nn >> 4) * 2048 + (nn & 1) * 8;
+          const int u = (nn & 15) >> 1;
+          bf[j].x = *reinterpret_cast<const double*>(bx + kk * 128 + ((u ^ (kk & 7)) << 4));
+          bf[j].y = *reinterpret_cast<const double*>(bx + (kk + 1) * 128 + ((u ^ ((kk + 1) & 7)) << 4));
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < FM; ++i)
+#pragma unroll
+        for (int j = 0; j < FN; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[i].x, bf[j].x);
+#pragma unroll
+      for (int i = 0; i < FM; ++i)
+#pragma unroll
+        for (int j = 0; j < FN; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[i].y, bf[j].y);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(empty + s);
+  }
+  double* __restrict__ C = g.C + (int64_t)b * g.sC;
+#pragma unroll
+  for (int i = 0; i < FM; ++i) {
+    const int64_t gm = m0 + wm0 + i * 8 + g8;
+    if (gm >= g.M) continue;
+#pragma unroll
+    for (int j = 0; j < FN; ++j) {
+      const int64_t gn = n0 + wn0 + j * 8 + 2 * q;
+      double* cp = C + gm * g.ldc + gn;
+      double v0 = g.alpha * acc[i][j][0], v1 = g.alpha * acc[i][j][1];
+      if (gn + 1 < g.N && ((reinterpret_cast<uintptr_t>(cp) & 15) == 0)) {
+        if (g.beta != 0.0) {
+          const double2 o = *reinterpret_cast<const double2*>(cp);
+          v0 = fma(g.beta, o.x, v0);
+          v1 = fma(g.beta, o.y, v1);
+        }
+        *reinterpret_cast<double2*>(cp) = make_double2(v0, v1);
+      } else {
+        if (gn < g.N) cp[0] = g.beta != 0.0 ? fma(g.beta, cp[0], v0) : v0;
+        if (gn + 1 < g.N) cp[1] = g.beta != 0.0 ? fma(g.beta, cp[1], v1) : v1;
+      }
+    }
+  }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 gemm_encode_fn() {
+  static const PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    return static_cast<PFN_cuTensorMapEncodeTiled_v12000>(nullptr);
+  }();
+  return fn;
+}
+
+// operand stored as [outer][inner] rows of pitch ld (elements), matrices sX apart
+bool operand_map(CUtensorMap* map, const double* P, int64_t inner, int64_t outer, int64_t ld, int64_t sX, int64_t batch,
+                 int box_inner, int box_outer) {
+  auto enc = gemm_encode_fn();
+  if (!enc) return false;
+  if ((reinterpret_cast<uintptr_t>(P) & 15) || (ld & 1) || (batch > 1 && (sX & 1))) return false;
+  const cuuint64_t dims[3] = {(cuuint64_t)inner, (cuuint64_t)outer, (cuuint64_t)batch};
+  const cuuint64_t strides[2] = {(cuuint64_t)ld * sizeof(double), (cuuint64_t)(batch > 1 ? sX : ld * outer) * sizeof(double)};
+  const cuuint32_t box[3] = {(cuuint32_t)box_inner, (cuuint32_t)box_outer, 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(P), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// returns WT_OK when launched, -1 when the TMA variant does not apply (caller falls back)
+template <bool TA, bool TB>
+int launch_tma(const GemmArgs& g, cudaStream_t st) {
+  constexpr int BM = 128, BN = 64;
+  if (g.klim || g.nlim || g.batch > 65535 || option(WT_OPT_GEMM_TMA) == 0) return -1;
+  TmaArgs tm;
+  const bool okA = TA ? operand_map(&tm.a, g.A, g.M, g.K, g.lda, g.sA, g.batch, 16, 16)
+                      : operand_map(&tm.a, g.A, g.K, g.M, g.lda, g.sA, g.batch, 16, BM);
+  const bool okB = TB ? operand_map(&tm.b, g.B, g.K, g.N, g.ldb, g.sB, g.batch, 16, BN)
+                      : operand_map(&tm.b, g.B, g.N, g.K, g.ldb, g.sB, g.batch, 16, 16);
+  if (!okA || !okB) return -1;
+  auto kern = gemm_f64_tma_kernel<BM, BN, 2, 2, TA, TB>;
+  constexpr size_t smem = (size_t)TSTAGES * (BM + BN) * BK * 8 + 2 * TSTAGES * 8;
+  if (int e = ensure_smem(kern, smem)) return e;
+  dim3 grid((unsigned)((g.N + BN - 1) / BN), (unsigned)((g.M + BM - 1) / BM), (unsigned)g.batch);
+  if (grid.y > 65535) return -1;
+  kern<<<grid, 128, smem, st>>>(g, tm);
+  return check_launch("wt_gemm_f64 (tma)");
+}
+
 __global__ void gemm_scale_kernel(double* C, int64_t M, int64_t N, int64_t ldc, int64_t sC,
                                   double beta) {
   double* Cb = C + (int64_t)blockIdx.y * sC;
@@ -247,6 +452,10 @@ int dispatch_tile(const GemmArgs& g, cudaStream_t st) {
   // a few tiles: 256^3 x 192 26.6 -> 28.1 TF/s; -4% at 512^3 and up)
   if (g.M >= 128 && g.N >= 64 && big_tiles >= num_sms()) {
     if (g.M <= 256 && g.N <= 256) return launch_cfg<128, 64, 4, 2, TA, TB, VEC>(g, st);
+    if (VEC == 2 && g.K >= 64) {  // tensor-map fed variant where it applies
+      const int r = launch_tma<TA, TB>(g, st);
+      if (r >= 0) return r;
+    }
     return launch_cfg<128, 64, 2, 2, TA, TB, VEC>(g, st);
   }
 #elif WT_GEMM_BIG == 4

@@ -32,6 +32,7 @@ static std::atomic<int> g_options[WT_OPT_COUNT] = {
     {0},  // WT_OPT_SVD_TRACE: per-sweep convergence trace on stderr
     {0},  // WT_OPT_EIG_PROFILE: preconditioner phase times on stderr
     {1},  // WT_OPT_EIG_TWOSTAGE: two-stage tridiagonalization (eig_sbr.cuh) where eligible
+    {1},  // WT_OPT_GEMM_TMA: K3 large tiles through the tensor-map variant
 };
 
 int option(int which) { return (which >= 0 && which < WT_OPT_COUNT) ? g_options[which].load() : 0; }

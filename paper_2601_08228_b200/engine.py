@@ -584,7 +584,7 @@ def lu_zero_pivot(a: torch.Tensor) -> torch.Tensor:
 
 # Test / diagnostic switches of the library (wt_set_option; include/wten_b200.h).
 OPTIONS = {"svd_split": 0, "svd_ctas_per_sm": 1, "svd_pair_skip": 2, "svd_persist": 3, "svd_precond": 4,
-           "svd_profile": 5, "svd_trace": 6, "eig_profile": 7, "eig_twostage": 8}
+           "svd_profile": 5, "svd_trace": 6, "eig_profile": 7, "eig_twostage": 8, "gemm_tma": 9}
 
 
 def set_option(name: str, value: int) -> int:

@@ -4,11 +4,13 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 from paper_2601_08228_b200 import engine as E
 
+E.options_from_env()  # WT_OPT_GEMM_TMA=0: the cp.async ring instead of the tensor-map variant
+
 for (b, m, n, k) in [(128, 512, 512, 512), (32, 1024, 1024, 1024), (192, 256, 256, 256), (32, 64, 40, 48)]:
     A = torch.randn(b, m, k, dtype=torch.float64, device="cuda")
     B = torch.randn(b, k, n, dtype=torch.float64, device="cuda")
     C = torch.empty(b, m, n, dtype=torch.float64, device="cuda")
-    for ta, tb in [(False, False), (False, True), (True, False)]:
+    for ta, tb in [(False, False), (False, True), (True, False), (True, True)]:
         a = A.transpose(1, 2).contiguous() if ta else A
         bb = B.transpose(1, 2).contiguous() if tb else B
         for _ in range(3):

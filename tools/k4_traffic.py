@@ -20,7 +20,10 @@ for r in rows[1:]:
 
 
 def phase(n):
-    for key, ph in (("tridiag_panel", "tridiagonalization panels"), ("gemm_f64", "K3 GEMMs (Gram, trailing, NS, back-transform, X V0)"),
+    for key, ph in (("sbr_update_mult", "two-stage: trailing pass (update + Z = A22 V)"), ("sbr_panel", "two-stage: panel QR"),
+                    ("sbr_w", "two-stage: W"), ("sbr_chase", "two-stage: band chase"),
+                    ("sbr_apply_q2", "two-stage: stage-2 back-transformation"),
+                    ("tridiag_panel", "tridiagonalization panels"), ("gemm_f64", "K3 GEMMs (Gram, trailing, NS, back-transform, X V0)"),
                     ("tri_bisect", "bisection"), ("tri_multisect", "bisection"), ("tri_inviter", "inverse iteration"), ("cluster_mgs", "cluster MGS"),
                     ("svd_sweep_kernel", "Jacobi sweeps"), ("ns_", "Newton-Schulz bookkeeping"), ("wy_larft", "larft")):
         if key in n:
