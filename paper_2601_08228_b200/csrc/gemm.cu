@@ -398,7 +398,7 @@ bool operand_map(CUtensorMap* map, const double* P, int64_t inner, int64_t outer
 }
 
 // returns WT_OK when launched, -1 when the TMA variant does not apply (caller falls back)
-template <bool TA, bool TB>
+template <bool TA, bool TB, int WM, int WN>
 int launch_tma(const GemmArgs& g, cudaStream_t st) {
   constexpr int BM = 128, BN = 64;
   if (g.klim || g.nlim || g.batch > 65535 || option(WT_OPT_GEMM_TMA) == 0) return -1;
@@ -408,12 +408,12 @@ int launch_tma(const GemmArgs& g, cudaStream_t st) {
   const bool okB = TB ? operand_map(&tm.b, g.B, g.K, g.N, g.ldb, g.sB, g.batch, 16, BN)
                       : operand_map(&tm.b, g.B, g.N, g.K, g.ldb, g.sB, g.batch, 16, 16);
   if (!okA || !okB) return -1;
-  auto kern = gemm_f64_tma_kernel<BM, BN, 2, 2, TA, TB>;
+  auto kern = gemm_f64_tma_kernel<BM, BN, WM, WN, TA, TB>;
   constexpr size_t smem = (size_t)TSTAGES * (BM + BN) * BK * 8 + 2 * TSTAGES * 8;
   if (int e = ensure_smem(kern, smem)) return e;
   dim3 grid((unsigned)((g.N + BN - 1) / BN), (unsigned)((g.M + BM - 1) / BM), (unsigned)g.batch);
   if (grid.y > 65535) return -1;
-  kern<<<grid, 128, smem, st>>>(g, tm);
+  kern<<<grid, WM * WN * 32, smem, st>>>(g, tm);
   return check_launch("wt_gemm_f64 (tma)");
 }
 
@@ -451,11 +451,12 @@ int dispatch_tile(const GemmArgs& g, cudaStream_t st) {
   // matrices 8 warps of 32 x 32 (more warps per SM where each matrix is only
   // a few tiles: 256^3 x 192 26.6 -> 28.1 TF/s; -4% at 512^3 and up)
   if (g.M >= 128 && g.N >= 64 && big_tiles >= num_sms()) {
-    if (g.M <= 256 && g.N <= 256) return launch_cfg<128, 64, 4, 2, TA, TB, VEC>(g, st);
+    const bool small = g.M <= 256 && g.N <= 256;  // (8 warps of 32 x 32 there, see above)
     if (VEC == 2 && g.K >= 64) {  // tensor-map fed variant where it applies
-      const int r = launch_tma<TA, TB>(g, st);
+      const int r = small ? launch_tma<TA, TB, 4, 2>(g, st) : launch_tma<TA, TB, 2, 2>(g, st);
       if (r >= 0) return r;
     }
+    if (small) return launch_cfg<128, 64, 4, 2, TA, TB, VEC>(g, st);
     return launch_cfg<128, 64, 2, 2, TA, TB, VEC>(g, st);
   }
 #elif WT_GEMM_BIG == 4
