@@ -48,6 +48,35 @@ def test_gemm_all_orientations(ta, tb, mnk):
     assert relerr(cd.cpu().numpy(), want) < 1e-14
 
 
+@pytest.mark.parametrize("ta", [False, True])
+@pytest.mark.parametrize("tb", [False, True])
+@pytest.mark.parametrize("shape", [(200, 130, 70, 66), (160, 256, 192, 100), (3, 1030, 1034, 72), (1, 2048, 2048, 64)])
+def test_gemm_tensor_map_variant(ta, tb, shape):
+    """K3's tensor-map (TMA) variant: ragged even sizes (zero-filled edge boxes and K tails), strided
+    row pitches, batch 1, both warp tilings -- against numpy and against the cp.async kernel."""
+    batch, M, Nn, K = shape
+    rng = np.random.default_rng(M + 3 * Nn + 5 * K + ta + 2 * tb)
+    pad = 6  # row pitch larger than the extent: operands are views of wider buffers
+    abuf = rng.standard_normal((batch, K, M + pad) if ta else (batch, M, K + pad))
+    bbuf = rng.standard_normal((batch, Nn, K + pad) if tb else (batch, K, Nn + pad))
+    at = torch.from_numpy(abuf).cuda()[:, :, :(M if ta else K)]
+    bt = torch.from_numpy(bbuf).cuda()[:, :, :(K if tb else Nn)]
+    a = abuf[:, :, :(M if ta else K)]
+    b = bbuf[:, :, :(K if tb else Nn)]
+    c0 = rng.standard_normal((batch, M, Nn))
+    opa = np.swapaxes(a, 1, 2) if ta else a
+    opb = np.swapaxes(b, 1, 2) if tb else b
+    want = 1.5 * (opa @ opb) + 0.25 * c0
+    got = {}
+    for tma in (1, 0):
+        with E.option("gemm_tma", tma):
+            cd = torch.from_numpy(c0).cuda()
+            E.gemm(at, bt, ta, tb, alpha=1.5, beta=0.25, out=cd)
+            got[tma] = cd.cpu().numpy()
+    assert relerr(got[1], want) < 1e-14
+    assert relerr(got[1], got[0]) < 1e-15
+
+
 def test_gemm_config5_size():
     rng = np.random.default_rng(9)
     a = rng.standard_normal((128, 512, 512))
