@@ -1148,14 +1148,19 @@ int eig_precondition(const double* Xt, double* Yt, int64_t m, int64_t n, int64_t
   const PanelShape ps = panel_shape(n);
   const int C = ps.C, NB = ps.NB;
   const bool sbr = use_two_stage(n, kk);
+  const double* sbr_tp = nullptr;  // the panels' compact-WY factors (two-stage), for the back-transformation
   if (sbr) {
     // 2'. dense -> band (stage 1), band -> tridiagonal (stage 2); eig_sbr.cuh
     constexpr int B = SB_B;
     double* AB = Z2;                                   // [batch][n][SB_LDB]
     double* Zp = AB + (size_t)batch * n * SB_LDB;      // [batch][n][B]   Z = A22 V of the current panel
-    double* Tp = Zp + (size_t)batch * n * B;           // [batch][B][B]
-    double* Vc = Tp + (size_t)batch * B * B;           // [batch][n][B]   compact copy of the current panel's V rows
+    // [batch][panels][B][B] the panels' compact-WY factors: kept until the back-transformation, in the
+    // tail of the VW buffer (sized for the one-stage panels' 64-wide rows; 24 are used here)
+    double* Tp = VW + (size_t)batch * n * 2 * B;
+    static_assert(2 * NB_MAX - 2 * SB_B >= SB_B + 1, "room for the panel factors behind [V | W]");
+    double* Vc = Zp + (size_t)batch * n * B;           // [batch][n][B] compact copy of the current panel's V rows
     double* Np = Vc + (size_t)batch * n * B;           // [batch][strips][B][B] per-strip shares of N = V^T Z
+    sbr_tp = Tp;
     CUtensorMap gmap;
     WT_REQUIRE(make_gmap(&gmap, G, n, batch), "eig: cuTensorMapEncodeTiled failed");
     WT_CUDA(cudaMemsetAsync(AB, 0, sizeof(double) * (size_t)batch * n * SB_LDB, st));
@@ -1308,7 +1313,7 @@ int eig_precondition(const double* Xt, double* Yt, int64_t m, int64_t n, int64_t
   const int64_t nref = n - 1 - roff;  // reflectors 0 .. nref-1 (tau = 0 beyond)
   // (128-reflector blocks halve the passes over Z for n >= 512; 64 measured
   // faster on 256^2 slices: config 3 back-transform 1.02 vs 1.43 ms)
-  const int64_t nbt = n >= 512 ? NBT : 64;
+  const int64_t nbt = sbr ? SB_TB : (n >= 512 ? NBT : 64);  // (two-stage: whole panels per block)
   for (int64_t k0 = ((nref - 1) / nbt) * nbt; k0 >= 0; k0 -= nbt) {
     const int64_t nb = std::min<int64_t>(nbt, nref - k0);
     const int64_t r0 = k0 + roff;  // first nonzero row of the block
@@ -1319,7 +1324,13 @@ int eig_precondition(const double* Xt, double* Yt, int64_t m, int64_t n, int64_t
       return r;
     const size_t tsm = sizeof(double) * NBT * (NBT + 1);
     if (int r = ensure_smem(wy_larft, tsm)) return r;
-    wy_larft<<<(unsigned)batch, 4 * NBT, tsm, st>>>(S, tau, flag, ni, (int)k0, (int)nb, T);
+    if (sbr) {  // the panels' factors merged block by block
+      if (int r = ensure_smem(sbr_larft_merge, tsm)) return r;
+      const double* Tpanels = sbr_tp;
+      sbr_larft_merge<<<(unsigned)batch, 512, tsm, st>>>(S, Tpanels, flag, ni, (int)k0, (int)nb, T);
+    } else {
+      wy_larft<<<(unsigned)batch, 4 * NBT, tsm, st>>>(S, tau, flag, ni, (int)k0, (int)nb, T);
+    }
     // M1 = Y^T Z (nb x n), M2 = T M1, Z[r0:, :] -= Y M2
     if (int r = gemm_f64_lim(1, 0, nb, kk, n - r0, 1.0, Y, n, nn, Z + r0 * kk, kk, nk, 0.0, M1, kk, NBT * n, batch,
                              nullptr, glim, st))

@@ -34,6 +34,7 @@ constexpr int SB_NT = 1024;          // threads of the stage-1 kernels: one row 
 constexpr int SB_CW = WT_SB_CW;            // chase warps per CTA
 constexpr int SB_QC = 16;            // columns of Z per CTA in sbr_apply_q2
 constexpr int SB_QT = 512;           // its threads
+constexpr int SB_QD = 6;             // reflector-row buffers: rows travel SB_QD - 1 sweeps ahead
 static_assert(SB_B <= 16 && SB_B % 2 == 0, "lane maps below assume an even band width of at most 16");
 
 // Sum of 16 per-lane values over the 32 lanes of a warp in 16 shuffles: after the
@@ -612,7 +613,7 @@ __global__ void __launch_bounds__(SB_PT, 1) sbr_panel(double* __restrict__ Gall,
       if (lane == c) Ts[c][c] = taus[c];
       __syncwarp();
     }
-    double* Tp = Tpall + (int64_t)b * B * B;
+    double* Tp = Tpall + ((int64_t)b * ((n + B - 1) / B) + c0 / B) * B * B;  // [matrix][panel][B][B]
     for (int k = lane; k < B * B; k += 32) Tp[k] = Ts[k / B][k % B];
     if (lane < B) tauall[(int64_t)b * n + c0 + lane] = lane < jb ? taus[lane] : 0.0;
   }
@@ -654,7 +655,7 @@ __global__ void __launch_bounds__(SB_NT, 1) sbr_w(const double* __restrict__ Vca
   const bool have = tid < m;
   __shared__ __align__(16) double Ns[B][B], Ts[B][B], NT[B][B], Ss[B][B];
   if (tid < B * B) {
-    Ts[tid / B][tid % B] = Tpall[(int64_t)b * B * B + tid];
+    Ts[tid / B][tid % B] = Tpall[((int64_t)b * ((n + B - 1) / B) + c0 / B) * B * B + tid];
     double s = 0.0;
     for (int q = 0; q < nstrips; ++q) s += Npall[((int64_t)b * nstrips + q) * B * B + tid];
     Ns[tid / B][tid % B] = s;
@@ -722,6 +723,60 @@ __global__ void __launch_bounds__(SB_NT, 1) sbr_w(const double* __restrict__ Vca
         *reinterpret_cast<double2*>(wv + B + l0 + u) = vv;
       }
     }
+  }
+}
+
+// Compact-WY factor of a back-transformation block of up to SB_TB = 10 SB_B stage-1
+// reflectors (whole panels, k0 a multiple of SB_TB) from the panels' own factors T_j
+// and S = Y^T Y of the block (K3):  T[0:c, c:c+B] = -T[0:c, 0:c] S[0:c, c:c+B] T_j,
+// nine merges of dense blocks instead of dlarft's 120 dependent columns (wy_larft:
+// ~1 us per column).  One CTA per matrix; T in shared memory, written as NBT x NBT.
+constexpr int SB_TB = 10 * SB_B;
+__global__ void __launch_bounds__(512, 1) sbr_larft_merge(const double* __restrict__ Sall, const double* __restrict__ Tpall,
+                                                         const int* __restrict__ flag, int n, int k0, int nb,
+                                                         double* __restrict__ Tall) {
+  constexpr int B = SB_B, LD = NBT + 1;
+  const int b = blockIdx.x;
+  if (!flag[b]) return;
+  extern __shared__ double T[];       // [NBT][LD]
+  __shared__ double X[SB_TB][B + 1];  // S[0:c, c:c+B] T_j
+  __shared__ double Tj[B][B + 1];
+  const double* S = Sall + (int64_t)b * NBT * NBT;
+  const double* Tp = Tpall + ((int64_t)b * ((n + B - 1) / B) + k0 / B) * B * B;
+  const int tid = threadIdx.x;
+  for (int e = tid; e < NBT * LD; e += 512) T[e] = 0.0;
+  __syncthreads();
+  const int np = (nb + B - 1) / B;
+  for (int j = 0; j < np; ++j) {
+    const int c = j * B;
+    if (tid < B * B) Tj[tid / B][tid % B] = Tp[(int64_t)j * B * B + tid];
+    __syncthreads();
+    if (tid < B * B && c + tid / B < NBT && c + tid % B < NBT) T[(c + tid / B) * LD + c + tid % B] = Tj[tid / B][tid % B];
+    for (int e = tid; e < c * B; e += 512) {  // X = S[0:c, c:c+B] T_j
+      const int r = e / B, l = e % B;
+      double acc = 0.0;
+#pragma unroll
+      for (int k = 0; k < B; ++k) acc = fma(c + k < nb ? S[(int64_t)r * NBT + c + k] : 0.0, Tj[k][l], acc);
+      X[r][l] = acc;
+    }
+    __syncthreads();
+    for (int e = tid; e < c * B; e += 512) {  // T[0:c, c:c+B] = -T[0:c, 0:c] X (T upper triangular)
+      const int r = e / B, l = e % B;
+      double a0 = 0.0, a1 = 0.0;
+      int k = r;
+      for (; k + 1 < c; k += 2) {
+        a0 = fma(T[r * LD + k], X[k][l], a0);
+        a1 = fma(T[r * LD + k + 1], X[k + 1][l], a1);
+      }
+      if (k < c) a0 = fma(T[r * LD + k], X[k][l], a0);
+      T[r * LD + c + l] = -(a0 + a1);
+    }
+    __syncthreads();
+  }
+  double* Tg = Tall + (int64_t)b * NBT * NBT;
+  for (int e = tid; e < NBT * NBT; e += 512) {
+    const int rr = e / NBT, cc = e % NBT;
+    Tg[e] = (cc >= rr && cc < nb) ? T[rr * LD + cc] : 0.0;
   }
 }
 
@@ -908,7 +963,7 @@ __global__ void __launch_bounds__(SB_CW * 32, 1) sbr_chase(const double* __restr
 // row half).  The next sweep's reflector row is staged in shared memory while the
 // current one is applied.
 struct Q2Smem {
-  static size_t bytes(int n) { return sizeof(double) * ((size_t)n * (SB_QC + 1) + 3 * (size_t)(n + 2)); }
+  static size_t bytes(int n) { return sizeof(double) * ((size_t)n * (SB_QC + 1) + SB_QD * (size_t)(n + 2)); }
 };
 __global__ void __launch_bounds__(SB_QT, 1) sbr_apply_q2(const double* __restrict__ Gall, double* __restrict__ Zall,
                                                         const int* __restrict__ flag, int n, int kk) {
@@ -917,7 +972,7 @@ __global__ void __launch_bounds__(SB_QT, 1) sbr_apply_q2(const double* __restric
   if (!flag[b]) return;
   extern __shared__ __align__(16) double qsm[];
   double* Zs = qsm;                       // [n][LDZ]
-  double* vbuf = Zs + (size_t)n * LDZ;    // [3][n + 2]
+  double* vbuf = Zs + (size_t)n * LDZ;    // [SB_QD][n + 2]
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int NWQ = SB_QT / 32;
   const int col0 = blockIdx.x * SB_QC;
@@ -930,22 +985,21 @@ __global__ void __launch_bounds__(SB_QT, 1) sbr_apply_q2(const double* __restric
   }
   const int slast = n - 3;
   if (slast < 0) return;
-  // the reflector rows of the next two sweeps travel by cp.async while the current one is applied
+  // the reflector rows of the next SB_QD - 1 sweeps travel by cp.async while the current one is applied
   auto fetch = [&](int sw) {
     if (sw >= 0) {
-      double* nb = vbuf + (sw % 3) * (n + 2);
+      double* nb = vbuf + (sw % SB_QD) * (n + 2);
       for (int i = sw + 1 + tid; i < n; i += SB_QT) cp_async_zfill<8>(nb + i, VQ + (int64_t)sw * n + i, true);
     }
     cp_async_commit();
   };
-  fetch(slast);
-  fetch(slast - 1);
-  cp_async_wait<1>();
+  for (int d = 0; d < SB_QD - 1; ++d) fetch(slast - d);
+  cp_async_wait<SB_QD - 2>();
   __syncthreads();
   const int cc = lane & 15, rh = lane >> 4;
   for (int s = slast; s >= 0; --s) {
-    const double* vb = vbuf + (s % 3) * (n + 2);
-    fetch(s - 2);
+    const double* vb = vbuf + (s % SB_QD) * (n + 2);
+    fetch(s - (SB_QD - 1));
     for (int r0 = s + 1 + warp * B; r0 < n; r0 += NWQ * B) {
       const int L = min(B, n - r0);
       if (L < 2) break;
@@ -967,7 +1021,7 @@ __global__ void __launch_bounds__(SB_QT, 1) sbr_apply_q2(const double* __restric
         if (r < L) Zs[(r0 + r) * LDZ + cc] = fma(-y, vv[i], zz[i]);
       }
     }
-    cp_async_wait<1>();  // sweep s - 1's row has landed (only the newest group may be pending)
+    cp_async_wait<SB_QD - 2>();  // sweep s - 1's row has landed (only the newest SB_QD - 2 groups may be pending)
     __syncthreads();
   }
   for (int e = tid; e < n * SB_QC; e += SB_QT) {
