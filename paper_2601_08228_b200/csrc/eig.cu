@@ -1168,9 +1168,9 @@ int eig_precondition(const double* Xt, double* Yt, int64_t m, int64_t n, int64_t
     // the panel QR reads full rows: mirror the Gram's lower triangle first
     sym_mirror<<<dim3((unsigned)((n + 31) / 32), (unsigned)((n + 31) / 32), (unsigned)batch), dim3(32, 8), 0, st>>>(
         G, ni, flag);
-    // Per panel: QR of the rows below the band (with the previous panel's update
-    // applied to its own columns on load), then one fused pass over the trailing
-    // block (previous update + Z = A22 V), then W -> [V | W], [W | V].
+    // Per panel two launches: sbr_panel (W of the previous panel from its Z, the
+    // previous update applied to this panel's columns, QR of the rows below the
+    // band) and one fused pass over the trailing block (previous update + Z = A22 V).
     if (int r = ensure_smem(sbr_update_mult, FU_SMEM)) return r;
     int pend = 0;
     for (int64_t c0 = 0; c0 < n; c0 += B) {
@@ -1187,16 +1187,15 @@ int eig_precondition(const double* Xt, double* Yt, int64_t m, int64_t n, int64_t
         cfg.stream = st;
         cfg.attrs = attr;
         cfg.numAttrs = 1;
-        WT_CUDA(cudaLaunchKernelEx(&cfg, sbr_panel, G, AB, tau, Tp, (const int*)flag, ni, (int)c0, (const double*)VW,
-                                   (const double*)WV, pend, Vc));
+        const int nstrips_prev = (int)((n - c0 + FU_T - 1) / FU_T);  // strips of the previous trailing pass
+        WT_CUDA(cudaLaunchKernelEx(&cfg, sbr_panel, G, AB, tau, Tp, (const int*)flag, ni, (int)c0, VW, WV, pend, Vc,
+                                   (const double*)Zp, (const double*)Np, nstrips_prev));
       }
       const int64_t r0 = c0 + B, mrem = n - r0;
       if (mrem < 2) continue;
       sbr_update_mult<<<dim3((unsigned)((mrem + FU_T - 1) / FU_T), (unsigned)batch), FU_NT, FU_SMEM, st>>>(
           gmap, VW, WV, Vc, Zp, Np, flag, ni, (int)c0, pend);
-      sbr_w<<<(unsigned)batch, SB_NT, 0, st>>>(Vc, Zp, Tp, Np, (int)((mrem + FU_T - 1) / FU_T), VW, WV, flag, ni,
-                                               (int)c0);
-      pend = 1;
+      pend = 1;  // W of this panel is formed by the next panel kernel (from Z, N and T)
     }
     const size_t csm = ChaseSmem::bytes(ni);
     if (int r = ensure_smem(sbr_chase, csm)) return r;

@@ -5,13 +5,15 @@
 // Why: the one-stage reduction (tridiag_panel) runs one symv over the trailing
 // block per column -- 46 GB of loads and ~2 us of barriers per column on the 32
 // coarse 1024^2 slices of config 4 (22.7 of the 31 ms K4 call, ncu
-// profiles/r02_bench_launches.csv).  Two stages read the trailing block three
-// times per SB_B columns instead:
+// round-2 launch lists).  Two stages read and write the trailing block once per
+// SB_B columns instead:
 //   stage 1  dense -> band of half-width SB_B: per panel a Householder QR of the
 //            rows below the band (sbr_panel, a 4-CTA cluster per matrix, a row per
-//            thread in registers, one cluster reduction per column), Z =
-//            A22 V on K3, W = Z T - V (T^T V^T Z T) / 2 (sbr_w), and the
-//            two-sided update A22 -= V W^T + W V^T on K3.
+//            thread in registers, one cluster reduction per column; it first forms
+//            the previous panel's W = Z T - V (T^T V^T Z T) / 2 and applies that
+//            panel's update to its own columns), and one fused pass over the
+//            trailing block (sbr_update_mult: the previous panel's two-sided update
+//            A22 -= V W^T + W V^T and Z = A22 V for this panel).
 //   stage 2  band -> tridiagonal by column-wise bulge chasing (Lang 1993) with
 //            the band (2 SB_B - 1 diagonals) in shared memory, one CTA per matrix,
 //            one warp per sweep, sweeps pipelined two hops apart through
@@ -134,93 +136,6 @@ __global__ void sbr_clean_y(double* __restrict__ Gall, int n, const int* __restr
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nn; e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r = e / n, c = e - r * n;
     if (r < c + SB_B) A[e] = 0.0;
-  }
-}
-
-// A22 -= VW WV^T (the symmetric rank-2 SB_B update A22 - V W^T - W V^T, every tile)
-// for the trailing block at r0 (m = n - r0 rows): a streaming kernel -- the 64 x 64
-// tile of A22 arrives by one bulk copy per row while the DMMA product of the two
-// 24-wide operand strips (bulk copies of contiguous rows) runs, is updated in
-// shared memory and leaves by bulk stores.  K3's general kernel spends these
-// K = 24 updates in its pipeline prologue and a synchronous C read-modify-write
-// (1.2 TB/s).  grid (ceil(m / SY_BN), ceil(m / SY_BM), batch), SY_NT threads, 3 CTAs per SM.
-constexpr int SY_BM = 64, SY_BN = 64, SY_LDC = 72, SY_K = 2 * SB_B, SY_NT = SY_BM * 2;
-constexpr size_t SY_SMEM = sizeof(double) * (SY_BM * SY_K + SY_BN * SY_K + SY_BM * SY_LDC) + 16;
-__global__ void __launch_bounds__(SY_NT, 3) sbr_syr2k(double* __restrict__ Gall, const double* __restrict__ VWall,
-                                                   const double* __restrict__ WVall, const int* __restrict__ flag,
-                                                   int n, int r0) {
-  const int b = blockIdx.z;
-  if (!flag[b]) return;
-  extern __shared__ __align__(128) double ssm[];
-  double* VWs = ssm;                       // [SY_BM][SY_K]
-  double* WVs = VWs + SY_BM * SY_K;        // [SY_BN][SY_K]
-  double* Cs = WVs + SY_BN * SY_K;         // [SY_BM][SY_LDC]
-  uint64_t* bar = reinterpret_cast<uint64_t*>(Cs + SY_BM * SY_LDC);
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int m = n - r0;
-  const int i0 = blockIdx.y * SY_BM, j0 = blockIdx.x * SY_BN;
-  const int hrows = min(SY_BM, m - i0), wcols = min(SY_BN, m - j0);
-  double* C = Gall + (int64_t)b * n * n + (int64_t)(r0 + i0) * n + (r0 + j0);
-  const double* VW = VWall + ((int64_t)b * n + r0 + i0) * SY_K;
-  const double* WV = WVall + ((int64_t)b * n + r0 + j0) * SY_K;
-  if (tid == 0) {
-    mbar_init(bar, 1);
-    fence_mbar_init();
-  }
-  __syncthreads();
-  if (tid == 0)
-    mbar_expect_tx(bar, (uint32_t)((hrows + wcols) * SY_K * 8 + hrows * wcols * 8));
-  __syncthreads();
-  if (tid == 0) {
-    bulk_g2s(VWs, VW, (uint32_t)(hrows * SY_K * 8), bar);
-    bulk_g2s(WVs, WV, (uint32_t)(wcols * SY_K * 8), bar);
-  }
-  if (tid < hrows) bulk_g2s(Cs + tid * SY_LDC, C + (int64_t)tid * n, (uint32_t)(wcols * 8), bar);
-  mbar_wait(bar, 0);
-  const int wm0 = (warp >> 1) * 32, wn0 = (warp & 1) * 32;
-  const int g = lane >> 2, t = lane & 3;
-  double acc[4][4][2];
-#pragma unroll
-  for (int i = 0; i < 4; ++i)
-#pragma unroll
-    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-#pragma unroll
-  for (int ks = 0; ks < SY_K; ks += 8) {
-    double2 af[4], bf[4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) af[i] = *reinterpret_cast<const double2*>(VWs + (wm0 + 8 * i + g) * SY_K + ks + 2 * t);
-#pragma unroll
-    for (int j = 0; j < 4; ++j) bf[j] = *reinterpret_cast<const double2*>(WVs + (wn0 + 8 * j + g) * SY_K + ks + 2 * t);
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-      for (int j = 0; j < 4; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[i].x, bf[j].x);
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-      for (int j = 0; j < 4; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[i].y, bf[j].y);
-  }
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int r = wm0 + 8 * i + g;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int c = wn0 + 8 * j + 2 * t;
-      if (r < hrows && c < wcols) {  // (wcols even: the pair is inside together)
-        double2* p = reinterpret_cast<double2*>(Cs + r * SY_LDC + c);
-        double2 o = *p;
-        o.x -= acc[i][j][0];
-        o.y -= acc[i][j][1];
-        *p = o;
-      }
-    }
-  }
-  fence_proxy_async_smem();
-  __syncthreads();
-  if (tid < hrows) {
-    bulk_s2g(C + (int64_t)tid * n, Cs + tid * SY_LDC, (uint32_t)(wcols * 8));
-    bulk_commit();
-    bulk_wait_all();
   }
 }
 
@@ -437,7 +352,7 @@ __global__ void __launch_bounds__(FU_NT, WT_FU_OCC) sbr_update_mult(const __grid
       *reinterpret_cast<double2*>(vs + r * B + c) = vv;
     }
     __syncthreads();
-    // the strip's share of N = V^T Z (SB_B x SB_B; sbr_w sums the strips in order)
+    // the strip's share of N = V^T Z (SB_B x SB_B; the next panel kernel sums the strips in order)
     if (tid < B * B) {
       const int k = tid / B, l = tid % B;
       double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
@@ -472,9 +387,9 @@ constexpr int SB_PW = SB_PT / 32;
 __global__ void __launch_bounds__(SB_PT, 1) sbr_panel(double* __restrict__ Gall, double* __restrict__ ABall,
                                                      double* __restrict__ tauall, double* __restrict__ Tpall,
                                                      const int* __restrict__ flag, int n, int c0,
-                                                     const double* __restrict__ VWall,
-                                                     const double* __restrict__ WVall, int pend,
-                                                     double* __restrict__ Vcall) {
+                                                     double* __restrict__ VWall, double* __restrict__ WVall, int pend,
+                                                     double* __restrict__ Vcall, const double* __restrict__ Zall,
+                                                     const double* __restrict__ Npall, int nstrips) {
   constexpr int B = SB_B;
   const int b = blockIdx.x / SB_PC;
   if (!flag[b]) return;  // cluster-uniform
@@ -496,14 +411,94 @@ __global__ void __launch_bounds__(SB_PT, 1) sbr_panel(double* __restrict__ Gall,
   __shared__ double coef[2][16];  // tau * v^T P[:, k] of the current column (k > c)
   __shared__ double hs[2][2];     // scale, beta
 
-  __shared__ __align__(16) double wvs[B][2 * B];  // WV rows of the panel's columns (pending update)
+  __shared__ __align__(16) double wvs[B][2 * B];  // [W | V] rows of the panel's columns (pending update)
+  __shared__ __align__(16) double Ns[B][B], Tq[B][B], NT[B][B], Ss[B][B];
+  // ---- previous panel (columns c0 - B ..): W = Z T - V (T^T N T) / 2 from the trailing pass's Z and the
+  //      per-strip shares of N = V^T Z; its rows are the rows r0p = c0 .. of this panel.  Every CTA forms S.
   if (pend) {
-    for (int e = tid; e < bw * 2 * B; e += SB_PT)
-      wvs[e / (2 * B)][e % (2 * B)] = WVall[((int64_t)b * n + c0) * 2 * B + e];
+    if (tid < B * B) {
+      Tq[tid / B][tid % B] = Tpall[((int64_t)b * ((n + B - 1) / B) + c0 / B - 1) * B * B + tid];
+      double sN = 0.0;
+      for (int q = 0; q < nstrips; ++q) sN += Npall[((int64_t)b * nstrips + q) * B * B + tid];
+      Ns[tid / B][tid % B] = sN;
+    }
+    __syncthreads();
+    if (tid < B * B) {  // NT = N T
+      const int k = tid / B, l = tid % B;
+      double a = 0.0;
+#pragma unroll
+      for (int j = 0; j < B; ++j) a = fma(Ns[k][j], Tq[j][l], a);
+      NT[k][l] = a;
+    }
+    __syncthreads();
+    if (tid < B * B) {  // S = T^T (N T), halved
+      const int k = tid / B, l = tid % B;
+      double a = 0.0;
+#pragma unroll
+      for (int j = 0; j < B; ++j) a = fma(Tq[j][k], NT[j][l], a);
+      Ss[k][l] = 0.5 * a;
+    }
     __syncthreads();
   }
-  // my row's panel entries minus the pending update  sum_t VW[row][t] WV[c0 + k][t]
-  auto load_row = [&](int grow, double* row) {
+  // [V | W] of the previous panel for global row grow (>= c0): vw[0:B] = V row, vw[B:2B] = W row
+  auto prev_vw = [&](int grow, double* vw) {
+    const double* zr = Zall + ((int64_t)b * n + grow) * B;
+    const double* vr = Vcall + ((int64_t)b * n + grow) * B;
+    double z[B];
+#pragma unroll
+    for (int k = 0; k < B; k += 2) {
+      const double2 x = *reinterpret_cast<const double2*>(zr + k), y = *reinterpret_cast<const double2*>(vr + k);
+      z[k] = x.x;
+      z[k + 1] = x.y;
+      vw[k] = y.x;
+      vw[k + 1] = y.y;
+    }
+#pragma unroll
+    for (int l0 = 0; l0 < B; l0 += 4) {
+      double w[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+      for (int k = 0; k < B; ++k) {
+        const double2 t01 = *reinterpret_cast<const double2*>(&Tq[k][l0]);
+        const double2 t23 = *reinterpret_cast<const double2*>(&Tq[k][l0 + 2]);
+        const double2 s01 = *reinterpret_cast<const double2*>(&Ss[k][l0]);
+        const double2 s23 = *reinterpret_cast<const double2*>(&Ss[k][l0 + 2]);
+        w[0] = fma(z[k], t01.x, fma(-vw[k], s01.x, w[0]));
+        w[1] = fma(z[k], t01.y, fma(-vw[k], s01.y, w[1]));
+        w[2] = fma(z[k], t23.x, fma(-vw[k], s23.x, w[2]));
+        w[3] = fma(z[k], t23.y, fma(-vw[k], s23.y, w[3]));
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) vw[B + l0 + u] = w[u];
+    }
+  };
+  auto store_vw = [&](int grow, const double* vw) {  // rows of [V | W] and [W | V] for the trailing pass
+    double* pv = VWall + ((int64_t)b * n + grow) * 2 * B;
+    double* pw = WVall + ((int64_t)b * n + grow) * 2 * B;
+#pragma unroll
+    for (int k = 0; k < B; k += 2) {
+      const double2 vv = make_double2(vw[k], vw[k + 1]), ww = make_double2(vw[B + k], vw[B + k + 1]);
+      *reinterpret_cast<double2*>(pv + k) = vv;
+      *reinterpret_cast<double2*>(pv + B + k) = ww;
+      *reinterpret_cast<double2*>(pw + k) = ww;
+      *reinterpret_cast<double2*>(pw + B + k) = vv;
+    }
+  };
+  if (pend) {
+    // the [W | V] rows of this panel's columns (global rows c0 .. c0 + bw - 1): every CTA needs them
+    if (tid < bw) {
+      double vw[2 * B];
+      prev_vw(c0 + tid, vw);
+#pragma unroll
+      for (int k = 0; k < B; ++k) {
+        wvs[tid][k] = vw[B + k];
+        wvs[tid][B + k] = vw[k];
+      }
+      if (rank == SB_PC - 1) store_vw(c0 + tid, vw);
+    }
+    __syncthreads();
+  }
+  // my row's panel entries minus the pending update  sum_t [V | W][row][t] [W | V][c0 + k][t]
+  auto load_row = [&](int grow, double* row, bool store) {
     const double* ar = A + (int64_t)grow * n + c0;
 #pragma unroll
     for (int k = 0; k < B; k += 2) {
@@ -512,19 +507,15 @@ __global__ void __launch_bounds__(SB_PT, 1) sbr_panel(double* __restrict__ Gall,
       row[k + 1] = x.y;
     }
     if (pend) {
-      const double* vw = VWall + ((int64_t)b * n + grow) * 2 * B;
+      double vw[2 * B];
+      prev_vw(grow, vw);
+      if (store) store_vw(grow, vw);
 #pragma unroll
-      for (int t0 = 0; t0 < 2 * B; t0 += B) {  // two batches of independent loads (L2 latency paid twice, not 12 times)
-        double2 v2[B / 2];
+      for (int t = 0; t < 2 * B; t += 2) {
 #pragma unroll
-        for (int u = 0; u < B / 2; ++u) v2[u] = *reinterpret_cast<const double2*>(vw + t0 + 2 * u);
-#pragma unroll
-        for (int u = 0; u < B / 2; ++u) {
-#pragma unroll
-          for (int k = 0; k < B; ++k) {
-            const double2 w2 = *reinterpret_cast<const double2*>(&wvs[k][t0 + 2 * u]);
-            row[k] = fma(-v2[u].x, w2.x, fma(-v2[u].y, w2.y, row[k]));
-          }
+        for (int k = 0; k < B; ++k) {
+          const double2 w2 = *reinterpret_cast<const double2*>(&wvs[k][t]);
+          row[k] = fma(-vw[t], w2.x, fma(-vw[t + 1], w2.y, row[k]));
         }
       }
     }
@@ -532,7 +523,7 @@ __global__ void __launch_bounds__(SB_PT, 1) sbr_panel(double* __restrict__ Gall,
   // diagonal block -> band (lower part); the last CTA has the fewest QR rows to load
   if (rank == SB_PC - 1 && tid < bw) {
     double drow[B];
-    load_row(c0 + tid, drow);
+    load_row(c0 + tid, drow, false);
 #pragma unroll
     for (int k = 0; k < B; ++k)
       if (k <= tid) AB[(int64_t)(c0 + k) * SB_LDB + (tid - k)] = drow[k];
@@ -542,7 +533,7 @@ __global__ void __launch_bounds__(SB_PT, 1) sbr_panel(double* __restrict__ Gall,
   double row[B];
 #pragma unroll
   for (int k = 0; k < B; ++k) row[k] = 0.0;
-  if (have) load_row(r0 + gt, row);
+  if (have) load_row(r0 + gt, row, true);
 #pragma unroll
   for (int c = 0; c < B; ++c) {  // (unrolled: static register indices)
     if (c < jb) {
@@ -636,94 +627,6 @@ __global__ void __launch_bounds__(SB_PT, 1) sbr_panel(double* __restrict__ Gall,
     }
   }
   cl_sync();  // no CTA exits while the others may still read its shared memory
-}
-
-// W = Z T - V (T^T (V^T Z) T) / 2 for the panel at c0 (rows r0 = c0 + SB_B ..), Z = A22 V
-// (m x SB_B, pitch SB_B) and the per-strip shares of N = V^T Z from sbr_update_mult;
-// writes the rows of VW = [V | W] and WV = [W | V] (pitch 2 SB_B, row index = global
-// row) for the next panel's pending update and trailing pass.  One thread per row.
-__global__ void __launch_bounds__(SB_NT, 1) sbr_w(const double* __restrict__ Vcall, const double* __restrict__ Zall,
-                                                 const double* __restrict__ Tpall, const double* __restrict__ Npall,
-                                                 int nstrips, double* __restrict__ VWall, double* __restrict__ WVall,
-                                                 const int* __restrict__ flag, int n, int c0) {
-  constexpr int B = SB_B;
-  const int b = blockIdx.x;
-  if (!flag[b]) return;
-  const int tid = threadIdx.x;
-  const int r0 = c0 + B;
-  const int m = n - r0;
-  const bool have = tid < m;
-  __shared__ __align__(16) double Ns[B][B], Ts[B][B], NT[B][B], Ss[B][B];
-  if (tid < B * B) {
-    Ts[tid / B][tid % B] = Tpall[((int64_t)b * ((n + B - 1) / B) + c0 / B) * B * B + tid];
-    double s = 0.0;
-    for (int q = 0; q < nstrips; ++q) s += Npall[((int64_t)b * nstrips + q) * B * B + tid];
-    Ns[tid / B][tid % B] = s;
-  }
-  // my rows of Z and V (both contiguous SB_B-wide rows)
-  double z[B], v[B];
-  {
-    const double* zr = Zall + ((int64_t)b * n + r0 + tid) * B;
-    const double* vr = Vcall + ((int64_t)b * n + r0 + tid) * B;
-#pragma unroll
-    for (int k = 0; k < B; k += 2) {
-      double2 x = make_double2(0.0, 0.0), y = make_double2(0.0, 0.0);
-      if (have) {
-        x = *reinterpret_cast<const double2*>(zr + k);
-        y = *reinterpret_cast<const double2*>(vr + k);
-      }
-      z[k] = x.x;
-      z[k + 1] = x.y;
-      v[k] = y.x;
-      v[k + 1] = y.y;
-    }
-  }
-  __syncthreads();
-  if (tid < B * B) {  // NT = N T
-    const int k = tid / B, l = tid % B;
-    double s = 0.0;
-#pragma unroll
-    for (int j = 0; j < B; ++j) s = fma(Ns[k][j], Ts[j][l], s);
-    NT[k][l] = s;
-  }
-  __syncthreads();
-  if (tid < B * B) {  // S = T^T (N T), halved
-    const int k = tid / B, l = tid % B;
-    double s = 0.0;
-#pragma unroll
-    for (int j = 0; j < B; ++j) s = fma(Ts[j][k], NT[j][l], s);
-    Ss[k][l] = 0.5 * s;
-  }
-  __syncthreads();
-  if (have) {
-    double* vw = VWall + ((int64_t)b * n + r0 + tid) * 2 * B;
-    double* wv = WVall + ((int64_t)b * n + r0 + tid) * 2 * B;
-    // W row in three groups of four columns (z, v and a full w row exceed 64 registers)
-#pragma unroll
-    for (int l0 = 0; l0 < B; l0 += 4) {
-      double w[4] = {0.0, 0.0, 0.0, 0.0};
-#pragma unroll
-      for (int k = 0; k < B; ++k) {
-        const double2 t01 = *reinterpret_cast<const double2*>(&Ts[k][l0]);
-        const double2 t23 = *reinterpret_cast<const double2*>(&Ts[k][l0 + 2]);
-        const double2 s01 = *reinterpret_cast<const double2*>(&Ss[k][l0]);
-        const double2 s23 = *reinterpret_cast<const double2*>(&Ss[k][l0 + 2]);
-        w[0] = fma(z[k], t01.x, fma(-v[k], s01.x, w[0]));
-        w[1] = fma(z[k], t01.y, fma(-v[k], s01.y, w[1]));
-        w[2] = fma(z[k], t23.x, fma(-v[k], s23.x, w[2]));
-        w[3] = fma(z[k], t23.y, fma(-v[k], s23.y, w[3]));
-      }
-#pragma unroll
-      for (int u = 0; u < 4; u += 2) {
-        const double2 ww = make_double2(w[u], w[u + 1]);
-        const double2 vv = make_double2(v[l0 + u], v[l0 + u + 1]);
-        *reinterpret_cast<double2*>(vw + l0 + u) = vv;
-        *reinterpret_cast<double2*>(vw + B + l0 + u) = ww;
-        *reinterpret_cast<double2*>(wv + l0 + u) = ww;
-        *reinterpret_cast<double2*>(wv + B + l0 + u) = vv;
-      }
-    }
-  }
 }
 
 // Compact-WY factor of a back-transformation block of up to SB_TB = 10 SB_B stage-1
