@@ -394,7 +394,7 @@ def headline_single(args, x_host, sampler):
                 "flops_model": "32 x (14 m n^2 + 8 n^3), m = n = 1024: the Golub-Kahan thin-SVD count of the work the "
                                "reference does for this result (SURVEY 8(d)); the leading-triplet mode executes less "
                                "(DESIGN.md 4.3), so frac is an effective rate on the reference's count",
-                "executed": executed_k4_rate(n1, n2, p >> L, k4_ms, peak) if k4_name == "svd_topk" else None,
+                "executed": executed_k4_rate(n1, n2, 2 * (p >> L), k4_ms, peak) if k4_name == "svd_topk" else None,
                 "k4_ms_per_call": round(k4_ms, 3), "share_of_step": round(k4_ms / per_call, 4),
                 "executed_jacobi_tflops": round(info["jflops"] / (k4_ms * 1e-3) / 1e12, 3),
                 "jacobi_sweeps": info["sweeps"]}

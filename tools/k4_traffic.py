@@ -25,7 +25,7 @@ def phase(n):
                     ("sbr_apply_q2", "two-stage: stage-2 back-transformation"),
                     ("tridiag_panel", "tridiagonalization panels"), ("gemm_f64", "K3 GEMMs (Gram, trailing, NS, back-transform, X V0)"),
                     ("tri_bisect", "bisection"), ("tri_multisect", "bisection"), ("tri_inviter", "inverse iteration"), ("cluster_mgs", "cluster MGS"),
-                    ("svd_sweep_kernel", "Jacobi sweeps"), ("ns_", "Newton-Schulz bookkeeping"), ("wy_larft", "larft")):
+                    ("svd_sweep_kernel", "Jacobi sweeps"), ("ns_", "Newton-Schulz bookkeeping"), ("wy_larft", "larft"), ("sbr_larft_merge", "larft")):
         if key in n:
             return ph
     return "other (copy-in, sort, permute, flags)"
