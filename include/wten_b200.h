@@ -256,6 +256,28 @@ size_t wt_slice_reduce_scratch(int64_t n, int64_t nslices);
 int wt_slice_reduce_f64(const double* x, const double* y, int64_t n, int64_t nslices,
                         int mode, double* out, void* stream);
 
+/* Imaging helpers either side of the path.
+ * The reference ships no code for them (SPEC-only), so these build the operands
+ * of BASELINE configs[2..4] directly in HBM.
+ *
+ * wt_toeplitz_tensor_f64: the slice-constant symmetric Toeplitz operator
+ * out[i][j][k] = c[|i - j|] (0 beyond nc), (n, n, p) tube-fastest.
+ *
+ * wt_gauss_smooth2d_f64: separable reflect-mode ("half-sample symmetric")
+ * Gaussian filter over axes 0 and 1 of x (n1, n2, e), e fastest, with the
+ * half-kernel w[0..radius] (w[0] = centre tap); tmp and out hold n1*n2*e doubles.
+ *
+ * wt_hsi_mix_f64: out[pix][k] = clip(sum_j ab[pix][j] spectra[j][k] + sigma z, lo, hi)
+ * with z = noise[pix][k] when `noise` is given, else standard normals from the
+ * Philox-4x32-10 stream keyed by `seed` (counter pix * ceil(p / 2) + k / 2, Box-Muller
+ * pair for bands k, k + 1); at most 32 endmembers. */
+int wt_toeplitz_tensor_f64(const double* c, int64_t nc, int64_t n, int64_t p, double* out, void* stream);
+int wt_gauss_smooth2d_f64(const double* x, int64_t n1, int64_t n2, int64_t e, const double* w,
+                          int64_t radius, double* tmp, double* out, void* stream);
+int wt_hsi_mix_f64(const double* ab, const double* spectra, int64_t npix, int64_t e, int64_t p,
+                   double noise_sigma, const double* noise, uint64_t seed, double lo, double hi,
+                   double* out, void* stream);
+
 /* Test / diagnostic switches (process-wide; the defaults are the production
  * choices).  Returns the previous value, or WT_ERR_INVALID for an unknown option.
  * Used by the test suite to force scheduling variants whose results must not

@@ -74,6 +74,11 @@ SIGNATURES = {
                                                 ctypes.c_double, ctypes.c_void_p]),
     "wt_lu_pivot_check_f64": (ctypes.c_int, [c_double_p, i64, i64, ctypes.c_void_p, ctypes.c_void_p]),
     "wt_diag_blocks_f64": (ctypes.c_int, [c_double_p, i64, i64, i64, c_double_p, ctypes.c_void_p]),
+    "wt_toeplitz_tensor_f64": (ctypes.c_int, [c_double_p, i64, i64, i64, c_double_p, ctypes.c_void_p]),
+    "wt_gauss_smooth2d_f64": (ctypes.c_int, [c_double_p, i64, i64, i64, c_double_p, i64, c_double_p, c_double_p,
+                                             ctypes.c_void_p]),
+    "wt_hsi_mix_f64": (ctypes.c_int, [c_double_p, c_double_p, i64, i64, i64, ctypes.c_double, c_double_p, u64,
+                                      ctypes.c_double, ctypes.c_double, c_double_p, ctypes.c_void_p]),
     "wt_slice_reduce_scratch": (ctypes.c_size_t, [i64, i64]),
     "wt_slice_reduce_f64": (ctypes.c_int, [c_double_p, c_double_p, i64, i64, ctypes.c_int,
                                            c_double_p, ctypes.c_void_p]),

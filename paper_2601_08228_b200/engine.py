@@ -794,3 +794,40 @@ def band_sums(x: torch.Tensor, y: torch.Tensor | None, mode: int) -> torch.Tenso
     N.check(lib.wt_slice_reduce_f64(_ptr(x), _ptr(y), nt, p, mode, _ptr(out), _stream()),
             "wt_slice_reduce_f64")
     return out[:p]
+
+
+# --------------------------------------------------------- imaging helpers ----
+
+def toeplitz_tensor(c: torch.Tensor, n: int, p: int) -> torch.Tensor:
+    """(n, n, p) slice-constant symmetric Toeplitz operator c[|i - j|] (wt_toeplitz_tensor_f64)."""
+    lib = N.require_gpu()
+    c = c.contiguous()
+    out = torch.empty((n, n, p), dtype=F64, device=c.device)
+    N.check(lib.wt_toeplitz_tensor_f64(_ptr(c), c.numel(), n, p, _ptr(out), _stream()), "wt_toeplitz_tensor_f64")
+    return out
+
+
+def gauss_smooth2d(x: torch.Tensor, half_kernel: torch.Tensor) -> torch.Tensor:
+    """Reflect-mode separable Gaussian filter over axes 0, 1 of (n1, n2, e) (wt_gauss_smooth2d_f64)."""
+    lib = N.require_gpu()
+    x = x.contiguous()
+    n1, n2, e = x.shape
+    tmp = torch.empty_like(x)
+    out = torch.empty_like(x)
+    N.check(lib.wt_gauss_smooth2d_f64(_ptr(x), n1, n2, e, _ptr(half_kernel), half_kernel.numel() - 1, _ptr(tmp),
+                                      _ptr(out), _stream()), "wt_gauss_smooth2d_f64")
+    return out
+
+
+def hsi_mix(ab: torch.Tensor, spectra: torch.Tensor, noise_sigma: float, noise: torch.Tensor | None,
+            seed: int, lo: float = 0.0, hi: float = 1.0) -> torch.Tensor:
+    """clip(ab @ spectra + sigma * z, lo, hi) as an (n1, n2, p) cube (wt_hsi_mix_f64)."""
+    lib = N.require_gpu()
+    n1, n2, e = ab.shape
+    p = spectra.shape[1]
+    ab = ab.contiguous()
+    spectra = spectra.contiguous()
+    out = torch.empty((n1, n2, p), dtype=F64, device=ab.device)
+    N.check(lib.wt_hsi_mix_f64(_ptr(ab), _ptr(spectra), n1 * n2, e, p, float(noise_sigma), _ptr(noise),
+                               int(seed) & ((1 << 64) - 1), lo, hi, _ptr(out), _stream()), "wt_hsi_mix_f64")
+    return out

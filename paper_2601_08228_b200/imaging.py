@@ -71,13 +71,27 @@ def blur_vectors(b_v: int, b_h: int, n1: int, n2: int):
     return cv, ch
 
 
-def blur_operator(b_v: int, b_h: int, n1: int, n2: int, p: int):
-    """Slice-constant Toeplitz operators A_V (n1 x n1 x p), A_H (n2 x n2 x p)."""
+def blur_operator(b_v: int, b_h: int, n1: int, n2: int, p: int, device=None):
+    """Slice-constant Toeplitz operators A_V (n1 x n1 x p), A_H (n2 x n2 x p).
+
+    With ``device`` (e.g. ``"cuda"``) the operators are written straight into HBM by
+    ``wt_toeplitz_tensor_f64`` (bit-identical to the host construction; nothing but the
+    two coefficient vectors crosses PCIe) and returned as CUDA tensors."""
     cv, ch = blur_vectors(b_v, b_h, n1, n2)
+    if device is not None:
+        return (E.toeplitz_tensor(E.as_device(cv, device), n1, p),
+                E.toeplitz_tensor(E.as_device(ch, device), n2, p))
     av = cv[np.abs(np.subtract.outer(np.arange(n1), np.arange(n1)))]
     ah = ch[np.abs(np.subtract.outer(np.arange(n2), np.arange(n2)))]
     return (np.ascontiguousarray(np.broadcast_to(av[:, :, None], av.shape + (p,))),
             np.ascontiguousarray(np.broadcast_to(ah[:, :, None], ah.shape + (p,))))
+
+
+def toeplitz_operator(c, n: int, p: int, device="cuda"):
+    """(n, n, p) slice-constant operator with every slice A[i, j] = c[|i - j|] (0 beyond
+    len(c)), built on the GPU: the 9 x 9 Gaussian-PSF operators of BASELINE configs[4]
+    are ``toeplitz_operator(synth.gaussian_taps(9, 2.0)[4:], n, p)``."""
+    return E.toeplitz_tensor(E.as_device(np.ascontiguousarray(c, dtype=np.float64), device), n, p)
 
 
 def blur(x, a_v, a_h, levels):

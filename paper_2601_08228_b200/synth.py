@@ -54,6 +54,56 @@ def hyperspectral_cube(n1: int, n2: int, p: int, endmembers: int = 10, seed: int
     return x
 
 
+def _hsi_draws(rng, n1, n2, p, endmembers):
+    """The generator's small host draws, in hyperspectral_cube's order: raw Dirichlet
+    abundances, then the spectra parameters."""
+    ab = rng.dirichlet([0.5] * endmembers, (n1, n2))
+    amp = rng.uniform(0.2, 1.0, (endmembers, 3))
+    cen = rng.uniform(0.0, p, (endmembers, 3))
+    wid = rng.uniform(p / 32, p / 8, (endmembers, 3))
+    k = np.arange(p, dtype=np.float64)
+    spectra = np.zeros((endmembers, p))
+    for e in range(endmembers):
+        for j in range(3):
+            spectra[e] += amp[e, j] * np.exp(-0.5 * ((k - cen[e, j]) / wid[e, j]) ** 2)
+    return ab, spectra
+
+
+def gaussian_half_kernel(sigma: float = 4.0, truncate: float = 4.0) -> np.ndarray:
+    """Centre-to-edge half of the normalised sampled Gaussian of radius
+    int(truncate * sigma + 0.5) (the kernel scipy.ndimage.gaussian_filter applies)."""
+    radius = int(truncate * float(sigma) + 0.5)
+    x = np.arange(-radius, radius + 1)
+    phi = np.exp(-0.5 / (sigma * sigma) * x ** 2)
+    phi = phi / phi.sum()
+    return np.ascontiguousarray(phi[radius:])
+
+
+def hyperspectral_cube_device(n1: int, n2: int, p: int, endmembers: int = 10, seed: int = 0,
+                              noise: float = 0.01, noise_source: str = "philox", device="cuda"):
+    """hyperspectral_cube with its heavy stages on the GPU.
+
+    The host draws only the raw abundances and the spectra parameters from
+    ``default_rng(seed)`` (n1 n2 E + 9 E numbers); smoothing (reflect-mode separable
+    Gaussian, sigma = 4 px), mixing, noise and clipping run in HBM and the cube is
+    returned as a CUDA tensor -- the n1 n2 p cube never crosses PCIe.
+    ``noise_source="numpy"`` continues the same numpy stream for the noise and uploads
+    it, which reproduces hyperspectral_cube to rounding (parity tests);
+    ``"philox"`` (default) draws the noise on the device from the Philox-4x32-10
+    stream keyed by ``seed`` -- the same distribution, a different seeded stream."""
+    from . import engine as E
+
+    if noise_source not in ("philox", "numpy"):
+        raise ValueError(f"unknown noise_source {noise_source!r}")
+    rng = np.random.default_rng(seed)
+    ab, spectra = _hsi_draws(rng, n1, n2, p, endmembers)
+    ab_d = E.gauss_smooth2d(E.as_device(ab, device), E.as_device(gaussian_half_kernel(4.0), device))
+    z = None
+    if noise_source == "numpy" and noise != 0.0:
+        z = E.as_device(rng.standard_normal((n1, n2, p)), device)
+    return E.hsi_mix(ab_d, E.as_device(spectra, device), noise, z, seed)
+
+
 def gaussian_taps(taps: int = 9, sigma: float = 2.0) -> np.ndarray:
     """1-D normalised Gaussian PSF (outer product = taps x taps PSF)."""
     h = taps // 2

@@ -96,3 +96,66 @@ def test_ac9_blur_semantics_follow_the_reference_code():
     xw = imaging.deblur(b, av, ah, 3, "w")
     assert relerr(xw, imaging.deblur(b, av, ah, 3, "spw")) < 1e-12
     assert relerr(xw, np.broadcast_to(x.mean(axis=2, keepdims=True), x.shape)) < 1e-6
+
+
+# ---- generator / operator construction on the GPU ----
+
+def test_blur_operator_device_bit_identical():
+    for (bv, bh, n1, n2, p) in [(2, 1, 4, 3, 4), (5, 7, 33, 70, 9), (3, 3, 128, 65, 32), (9, 2, 1, 1, 1)]:
+        av, ah = imaging.blur_operator(bv, bh, n1, n2, p)
+        avd, ahd = imaging.blur_operator(bv, bh, n1, n2, p, device="cuda")
+        assert avd.is_cuda and tuple(avd.shape) == av.shape and tuple(ahd.shape) == ah.shape
+        assert np.array_equal(avd.cpu().numpy(), av) and np.array_equal(ahd.cpu().numpy(), ah)
+
+
+def test_toeplitz_operator_matches_host_psf_operator():
+    for n, p in [(40, 6), (7, 5), (64, 16)]:
+        ref = synth.slice_constant(synth.toeplitz_blur(n, 9, 2.0), p)
+        got = imaging.toeplitz_operator(synth.gaussian_taps(9, 2.0)[4:], n, p)
+        assert np.array_equal(got.cpu().numpy(), ref)
+    assert tuple(imaging.toeplitz_operator([1.0], 0, 3).shape) == (0, 0, 3)
+
+
+def test_gauss_smooth_matches_scipy_reflect():
+    from scipy.ndimage import gaussian_filter
+
+    from paper_2601_08228_b200 import engine as E
+
+    rng = np.random.default_rng(5)
+    w = torch.from_numpy(synth.gaussian_half_kernel(4.0)).cuda()
+    for shape in [(50, 37, 3), (9, 70, 2), (5, 4, 1), (128, 96, 10)]:   # (9, ..) / (5, 4, ..): radius 16 > extent
+        x = rng.random(shape)
+        ref = np.stack([gaussian_filter(x[:, :, e], sigma=4, mode="reflect") for e in range(shape[2])], axis=2)
+        got = E.gauss_smooth2d(torch.from_numpy(x).cuda(), w).cpu().numpy()
+        assert np.abs(got - ref).max() <= 4e-16, shape
+
+
+def test_hyperspectral_cube_device_matches_host_generator():
+    for (n1, n2, p, e, seed) in [(48, 40, 24, 10, 0), (33, 21, 17, 12, 3)]:
+        ref = synth.hyperspectral_cube(n1, n2, p, e, seed=seed)
+        got = synth.hyperspectral_cube_device(n1, n2, p, e, seed=seed, noise_source="numpy")
+        assert got.is_cuda and tuple(got.shape) == ref.shape
+        assert np.abs(got.cpu().numpy() - ref).max() < 1e-13
+    clean_ref = synth.hyperspectral_cube(32, 32, 16, noise=0.0)
+    clean = synth.hyperspectral_cube_device(32, 32, 16, noise=0.0)
+    assert np.abs(clean.cpu().numpy() - clean_ref).max() < 1e-13
+
+
+def test_hyperspectral_cube_device_philox_noise():
+    n1, n2, p = 96, 96, 64
+    a = synth.hyperspectral_cube_device(n1, n2, p, seed=7)
+    b = synth.hyperspectral_cube_device(n1, n2, p, seed=7)
+    c = synth.hyperspectral_cube_device(n1, n2, p, seed=8)
+    assert torch.equal(a, b) and not torch.equal(a, c)            # seeded, deterministic
+    assert float(a.min()) >= 0.0 and float(a.max()) <= 1.0
+    clean = synth.hyperspectral_cube_device(n1, n2, p, seed=7, noise=0.0)
+    inside = (clean > 0.06) & (clean < 0.94)                        # 6 sigma from the clip bounds
+    z = ((a - clean)[inside] / 0.01).cpu().numpy()
+    assert z.size > 1e5
+    assert abs(z.mean()) < 5 / np.sqrt(z.size) and abs(z.std() - 1.0) < 0.01
+    assert abs(np.mean(z ** 3)) < 0.05 and abs(np.mean(z ** 4) - 3.0) < 0.1
+    # neighbouring samples (the two Box-Muller outputs of one counter, and adjacent counters) uncorrelated
+    flat = ((a - clean) / 0.01).reshape(-1)
+    ok = (inside.reshape(-1)[:-1] & inside.reshape(-1)[1:])
+    corr = float((flat[:-1] * flat[1:])[ok].mean())
+    assert abs(corr) < 0.01
