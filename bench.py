@@ -404,16 +404,30 @@ def headline_single(args, x_host, sampler):
     # warm-up as in the timed loop (the previous result alive while the next call
     # runs): the two calls allocate engine.host_buffer's two pooled pinned result
     # buffers (page-locking a fresh 2 GiB block costs ~0.9 s, once)
-    y_host = W.sp_w_svd(x_host, r, L)
-    y_host = W.sp_w_svd(x_host, r, L)
-    torch.cuda.synchronize()
-    t = time.perf_counter()
-    for _ in range(e2e_steps):
-        y_host = W.sp_w_svd(x_host, r, L)
-    e2e_s = (time.perf_counter() - t) / e2e_steps
+    # The input cube lives in page-locked host memory (W.pinned_empty), as the contract's e2e leg
+    # prescribes: the call DMAs its row chunks in place.  The same call on an ordinary (pageable)
+    # numpy array goes through the pinned staging ring and is reported beside it.
+    x_pin = W.pinned_empty(x_host.shape)
+    x_pin[...] = x_host
+
+    def e2e_leg(xin):
+        y = W.sp_w_svd(xin, r, L)
+        y = W.sp_w_svd(xin, r, L)
+        torch.cuda.synchronize()
+        t = time.perf_counter()
+        for _ in range(e2e_steps):
+            y = W.sp_w_svd(xin, r, L)
+        return (time.perf_counter() - t) / e2e_steps, y
+
+    e2e_pageable_s, y_host = e2e_leg(x_host)
+    del y_host  # (its pinned result buffer goes back to the pool of two before the next leg)
+    e2e_s, y_host = e2e_leg(x_pin)
     e2e = {"value": round(N / e2e_s, 1), "unit": UNIT, "h2d_bytes_per_step": 8 * N, "d2h_bytes_per_step": 8 * N,
            "ms_per_call": round(e2e_s * 1e3, 2), "steps": e2e_steps,
-           "api": "sp_w_svd(numpy cube, 30, 4) -> numpy reconstruction (pinned staging, H2D and D2H inside)"}
+           "ms_per_call_pageable_input": round(e2e_pageable_s * 1e3, 2),
+           "api": "sp_w_svd(numpy cube in page-locked memory, 30, 4) -> numpy reconstruction (H2D of the 2 GiB cube "
+                  "and D2H of the 2 GiB result inside every call; ms_per_call_pageable_input: the same call on a "
+                  "pageable numpy cube, staged through the pinned ring)"}
     # (after the e2e leg: the profiler's CUPTI session slows later host-side calls)
     n_launch, names = count_launches(lambda: sp_w_svd_device(x, r, L, out=out))
     return {"ms": ms, "value": N * args.steps / (ms * 1e-3), "roofline": roofline, "e2e": e2e,

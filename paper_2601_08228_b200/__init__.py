@@ -27,6 +27,7 @@ from .decomposition import (
     truncation_bound,
     w_svd,
 )
+from .engine import is_pinned_array, pinned_empty
 from .errors import (
     FormatError,
     IoError,
@@ -63,4 +64,5 @@ __all__ = [
     "as_tensor3", "frobenius_norm", "frontal_slice", "matrix_svd", "set_frontal_slice", "trace",
     "transpose",
     "load_tensor", "save_preview", "save_tensor",
+    "is_pinned_array", "pinned_empty",
 ]

@@ -36,6 +36,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <mutex>
 #include <vector>
 
 #include "wt_common.cuh"
@@ -1097,6 +1098,18 @@ bool make_gmap(CUtensorMap* map, double* G, int64_t n, int64_t batch) {
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// One non-blocking side stream per device for the second half of a split two-stage reduction
+// (created once; ordered against the caller's stream by per-call events).
+cudaStream_t side_stream() {
+  static std::mutex mu;
+  static cudaStream_t streams[64] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+  std::lock_guard<std::mutex> lock(mu);
+  if (!streams[dev] && cudaStreamCreateWithFlags(&streams[dev], cudaStreamNonBlocking) != cudaSuccess) return nullptr;
+  return streams[dev];
+}
+
 // Two-stage path: wide Grams whose rows below the band fit one row per thread,
 // few leading eigenvectors (the stage-2 back-transformation streams every
 // reflector once per SB_QC columns of Z).
@@ -1161,59 +1174,99 @@ int eig_precondition(const double* Xt, double* Yt, int64_t m, int64_t n, int64_t
     double* Vc = Zp + (size_t)batch * n * B;           // [batch][n][B] compact copy of the current panel's V rows
     double* Np = Vc + (size_t)batch * n * B;           // [batch][strips][B][B] per-strip shares of N = V^T Z
     sbr_tp = Tp;
-    CUtensorMap gmap;
-    WT_REQUIRE(make_gmap(&gmap, G, n, batch), "eig: cuTensorMapEncodeTiled failed");
-    WT_CUDA(cudaMemsetAsync(AB, 0, sizeof(double) * (size_t)batch * n * SB_LDB, st));
-    WT_CUDA(cudaMemsetAsync(tau, 0, sizeof(double) * (size_t)batch * n, st));
-    // the panel QR reads full rows: mirror the Gram's lower triangle first
-    sym_mirror<<<dim3((unsigned)((n + 31) / 32), (unsigned)((n + 31) / 32), (unsigned)batch), dim3(32, 8), 0, st>>>(
-        G, ni, flag);
-    // Per panel two launches: sbr_panel (W of the previous panel from its Z, the
-    // previous update applied to this panel's columns, QR of the rows below the
-    // band) and one fused pass over the trailing block (previous update + Z = A22 V).
     if (int r = ensure_smem(sbr_update_mult, FU_SMEM)) return r;
-    int pend = 0;
-    for (int64_t c0 = 0; c0 < n; c0 += B) {
-      {
-        cudaLaunchConfig_t cfg = {};
-        cudaLaunchAttribute attr[1];
-        attr[0].id = cudaLaunchAttributeClusterDimension;
-        attr[0].val.clusterDim.x = SB_PC;
-        attr[0].val.clusterDim.y = 1;
-        attr[0].val.clusterDim.z = 1;
-        cfg.gridDim = dim3((unsigned)(batch * SB_PC));
-        cfg.blockDim = dim3(SB_PT);
-        cfg.dynamicSmemBytes = 0;
-        cfg.stream = st;
-        cfg.attrs = attr;
-        cfg.numAttrs = 1;
-        const int nstrips_prev = (int)((n - c0 + FU_T - 1) / FU_T);  // strips of the previous trailing pass
-        WT_CUDA(cudaLaunchKernelEx(&cfg, sbr_panel, G, AB, tau, Tp, (const int*)flag, ni, (int)c0, VW, WV, pend, Vc,
-                                   (const double*)Zp, (const double*)Np, nstrips_prev));
-      }
-      const int64_t r0 = c0 + B, mrem = n - r0;
-      if (mrem < 2) continue;
-      sbr_update_mult<<<dim3((unsigned)((mrem + FU_T - 1) / FU_T), (unsigned)batch), FU_NT, FU_SMEM, st>>>(
-          gmap, VW, WV, Vc, Zp, Np, flag, ni, (int)c0, pend);
-      pend = 1;  // W of this panel is formed by the next panel kernel (from Z, N and T)
-    }
     const size_t csm = ChaseSmem::bytes(ni);
     if (int r = ensure_smem(sbr_chase, csm)) return r;
-    cudaEvent_t ce[2] = {};
-    if (prof) {
-      cudaEventCreate(&ce[0]);
-      cudaEventCreate(&ce[1]);
-      cudaEventRecord(ce[0], st);
-    }
-    sbr_chase<<<(unsigned)batch, SB_CW * 32, csm, st>>>(AB, G, dd, ee, flag, ni);
-    if (prof) {
-      cudaEventRecord(ce[1], st);
-      cudaEventSynchronize(ce[1]);
-      float ms = 0.f;
-      cudaEventElapsedTime(&ms, ce[0], ce[1]);
-      fprintf(stderr, "[wt_eig] two-stage: band chase %.3f ms (inside tridiag)\n", ms);
-      cudaEventDestroy(ce[0]);
-      cudaEventDestroy(ce[1]);
+    const int64_t npanels = (n + B - 1) / B, max_strips = (n + FU_T - 1) / FU_T;
+    // Stages 1 and 2 of the matrices [b0, b0 + nb) on stream s (every array is indexed by matrix).
+    auto reduce = [&](int64_t b0, int64_t nb, cudaStream_t s) -> int {
+      double* Gh = G + b0 * nn;
+      double* ABh = AB + b0 * n * SB_LDB;
+      double* tauh = tau + b0 * n;
+      double* Tph = Tp + b0 * npanels * B * B;
+      double *VWh = VW + b0 * n * 2 * B, *WVh = WV + b0 * n * 2 * B;
+      double *Vch = Vc + b0 * n * B, *Zph = Zp + b0 * n * B;
+      double* Nph = Np + b0 * max_strips * B * B;  // (strips of a pass <= max_strips: the halves never overlap)
+      const int* flagh = flag + b0;
+      CUtensorMap gmap;
+      WT_REQUIRE(make_gmap(&gmap, Gh, n, nb), "eig: cuTensorMapEncodeTiled failed");
+      WT_CUDA(cudaMemsetAsync(ABh, 0, sizeof(double) * (size_t)nb * n * SB_LDB, s));
+      WT_CUDA(cudaMemsetAsync(tauh, 0, sizeof(double) * (size_t)nb * n, s));
+      // the panel QR reads full rows: mirror the Gram's lower triangle first
+      sym_mirror<<<dim3((unsigned)((n + 31) / 32), (unsigned)((n + 31) / 32), (unsigned)nb), dim3(32, 8), 0, s>>>(
+          Gh, ni, flagh);
+      // Per panel two launches: sbr_panel (W of the previous panel from its Z, the
+      // previous update applied to this panel's columns, QR of the rows below the
+      // band) and one fused pass over the trailing block (previous update + Z = A22 V).
+      int pend = 0;
+      for (int64_t c0 = 0; c0 < n; c0 += B) {
+        {
+          cudaLaunchConfig_t cfg = {};
+          cudaLaunchAttribute attr[1];
+          attr[0].id = cudaLaunchAttributeClusterDimension;
+          attr[0].val.clusterDim.x = SB_PC;
+          attr[0].val.clusterDim.y = 1;
+          attr[0].val.clusterDim.z = 1;
+          cfg.gridDim = dim3((unsigned)(nb * SB_PC));
+          cfg.blockDim = dim3(SB_PT);
+          cfg.dynamicSmemBytes = 0;
+          cfg.stream = s;
+          cfg.attrs = attr;
+          cfg.numAttrs = 1;
+          const int nstrips_prev = (int)((n - c0 + FU_T - 1) / FU_T);  // strips of the previous trailing pass
+          WT_CUDA(cudaLaunchKernelEx(&cfg, sbr_panel, Gh, ABh, tauh, Tph, flagh, ni, (int)c0, VWh, WVh, pend, Vch,
+                                     (const double*)Zph, (const double*)Nph, nstrips_prev));
+        }
+        const int64_t r0 = c0 + B, mrem = n - r0;
+        if (mrem < 2) continue;
+        sbr_update_mult<<<dim3((unsigned)((mrem + FU_T - 1) / FU_T), (unsigned)nb), FU_NT, FU_SMEM, s>>>(
+            gmap, VWh, WVh, Vch, Zph, Nph, flagh, ni, (int)c0, pend);
+        pend = 1;  // W of this panel is formed by the next panel kernel (from Z, N and T)
+      }
+      cudaEvent_t ce[2] = {};
+      if (prof) {
+        cudaEventCreate(&ce[0]);
+        cudaEventCreate(&ce[1]);
+        cudaEventRecord(ce[0], s);
+      }
+      sbr_chase<<<(unsigned)nb, SB_CW * 32, csm, s>>>(ABh, Gh, dd + b0 * n, ee + b0 * n, flagh, ni);
+      if (prof) {
+        cudaEventRecord(ce[1], s);
+        cudaEventSynchronize(ce[1]);
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, ce[0], ce[1]);
+        fprintf(stderr, "[wt_eig] two-stage: band chase %.3f ms (inside tridiag, matrices %lld..%lld)\n", ms,
+                (long long)b0, (long long)(b0 + nb - 1));
+        cudaEventDestroy(ce[0]);
+        cudaEventDestroy(ce[1]);
+      }
+      return check_launch("eig two-stage reduction");
+    };
+    // Two halves of the batch on two streams: the panel QR is latency-bound (a 4-CTA cluster per
+    // matrix, one cluster reduction per column) and the trailing pass throughput-bound, so one half's
+    // panels run under the other half's trailing passes; both band chases (one SM per matrix) run
+    // side by side at the end.  Per-matrix arithmetic does not depend on the split.
+    const int split_opt = option(WT_OPT_EIG_SPLIT);
+    const bool split = split_opt == 2 || (split_opt == 0 && batch >= 16 && !prof);
+    if (split && batch >= 2) {
+      cudaStream_t side = side_stream();
+      WT_REQUIRE(side != nullptr, "eig: side stream creation failed");
+      cudaEvent_t fork = nullptr, join = nullptr;
+      WT_CUDA(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
+      WT_CUDA(cudaEventCreateWithFlags(&join, cudaEventDisableTiming));
+      const int64_t h = (batch + 1) / 2;
+      int r = WT_OK;
+      if (cudaEventRecord(fork, st) != cudaSuccess || cudaStreamWaitEvent(side, fork, 0) != cudaSuccess) r = WT_ERR_CUDA;
+      // (alternate the issue order? the streams are independent queues: host order only matters for
+      // when work becomes visible, and enqueueing is far faster than execution)
+      if (!r) r = reduce(h, batch - h, side);
+      if (!r) r = reduce(0, h, st);
+      if (cudaEventRecord(join, side) != cudaSuccess || cudaStreamWaitEvent(st, join, 0) != cudaSuccess) r = r ? r : WT_ERR_CUDA;
+      cudaEventDestroy(fork);
+      cudaEventDestroy(join);
+      if (r) return r;
+    } else {
+      if (int r = reduce(0, batch, st)) return r;
     }
   } else {
   WT_CUDA(cudaMemsetAsync(VW, 0, sizeof(double) * (size_t)(batch * n * 2 * NB), st));

@@ -89,3 +89,26 @@ def test_host_streamed_sp_w_svd_repeated():
     for _ in range(3):
         assert np.array_equal(W.sp_w_svd(x, 6, 3), y0)
     assert relerr(y0, O.sp_w_svd(x, 6, 3)) < 1e-8
+
+
+def test_pinned_numpy_inputs_are_uploaded_in_place_with_the_same_bits():
+    """Cubes in page-locked memory (W.pinned_empty) skip the staging ring on the streamed host
+    paths (engine.host_slices_pipeline, engine.host_lift); the results are those of the pageable
+    path bit for bit, and the input array is left untouched."""
+    import paper_2601_08228_b200 as W
+
+    rng = np.random.default_rng(23)
+    x = rng.standard_normal((160, 256, 256))           # 80 MB: streamed in row chunks
+    xp = W.pinned_empty(x.shape)
+    xp[...] = x
+    assert W.is_pinned_array(xp) and not W.is_pinned_array(x)
+    assert not W.is_pinned_array(xp[:, ::2]) and not W.is_pinned_array(xp.astype(np.float32))
+    y = W.sp_w_svd(x, 12, 3)
+    for _ in range(2):
+        assert np.array_equal(W.sp_w_svd(xp, 12, 3), y)
+    assert np.array_equal(xp, x)
+    pa, pb = W.forward_w(x, 4), W.forward_w(xp, 4)
+    assert np.array_equal(pa.smooth, pb.smooth) and all(np.array_equal(u, v) for u, v in zip(pa.details, pb.details))
+    assert np.array_equal(W.inverse_w(pb), W.inverse_w(pa))
+    # a pinned view with an offset (rows 8..) is still DMA'd in place
+    assert np.array_equal(W.sp_w_svd(xp[8:], 12, 3), W.sp_w_svd(np.ascontiguousarray(x[8:]), 12, 3))
