@@ -1114,7 +1114,10 @@ cudaStream_t side_stream() {
 // few leading eigenvectors (the stage-2 back-transformation streams every
 // reflector once per SB_QC columns of Z).
 bool use_two_stage(int64_t n, int64_t kk) {
-  return option(WT_OPT_EIG_TWOSTAGE) != 0 && n >= 512 && n - SB_B <= SB_NT && n % 2 == 0 && kk <= 128;
+  // (full mode, kk = n: the stage-2 back-transformation grows with kk; measured on 32 matrices:
+  // 512^2 13.3 -> 12.0 ms, 1024^2 49.3 -> 51.9 ms.  A function of n and kk only: same bits in any batch.)
+  const int opt = option(WT_OPT_EIG_TWOSTAGE);
+  return opt != 0 && n >= 512 && n - SB_B <= SB_NT && n % 2 == 0 && (kk <= 128 || n <= 640 || opt == 2);
 }
 
 }  // namespace eig

@@ -883,7 +883,7 @@ __global__ void __launch_bounds__(SB_CW * 32, 1) sbr_chase(const double* __restr
 struct Q2Smem {
   static size_t bytes(int n) { return sizeof(double) * ((size_t)n * (SB_QC + 1) + SB_QD * (size_t)(n + 2)); }
 };
-__global__ void __launch_bounds__(SB_QT, 1) sbr_apply_q2(const double* __restrict__ Gall, double* __restrict__ Zall,
+__global__ void __launch_bounds__(SB_QT, 2) sbr_apply_q2(const double* __restrict__ Gall, double* __restrict__ Zall,
                                                         const int* __restrict__ flag, int n, int kk) {
   constexpr int B = SB_B, HB = SB_B / 2, LDZ = SB_QC + 1;
   const int b = blockIdx.y;
