@@ -24,6 +24,7 @@ from .decomposition import (
     pinv_w_via_factors,
     sp_pinv_w,
     sp_w_svd,
+    sp_w_svd_many,
     truncation_bound,
     w_svd,
 )
@@ -55,7 +56,7 @@ __all__ = [
     "baselines",
     "NativeError", "NativeUnavailable",
     "face_product", "identity_tensor", "inverse_tensor", "orthogonal_tensor", "slicewise_matmul", "w_product",
-    "SvdFactors", "TruncationBound", "pinv_w", "pinv_w_via_factors", "sp_pinv_w", "sp_w_svd",
+    "SvdFactors", "TruncationBound", "pinv_w", "pinv_w_via_factors", "sp_pinv_w", "sp_w_svd", "sp_w_svd_many",
     "truncation_bound", "w_svd",
     "FormatError", "IoError", "LevelError", "OrthogonalityError", "RankError", "ShapeError",
     "SingularSliceError",

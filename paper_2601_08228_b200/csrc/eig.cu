@@ -1117,7 +1117,7 @@ bool use_two_stage(int64_t n, int64_t kk) {
   // (full mode, kk = n: the stage-2 back-transformation grows with kk; measured on 32 matrices:
   // 512^2 13.3 -> 12.0 ms, 1024^2 49.3 -> 51.9 ms.  A function of n and kk only: same bits in any batch.)
   const int opt = option(WT_OPT_EIG_TWOSTAGE);
-  return opt != 0 && n >= 512 && n - SB_B <= SB_NT && n % 2 == 0 && (kk <= 128 || n <= 640 || opt == 2);
+  return opt != 0 && (n >= 512 || (opt == 2 && n >= 128)) && n - SB_B <= SB_NT && n % 2 == 0 && (kk <= 128 || n <= 640 || opt == 2);
 }
 
 }  // namespace eig
@@ -1324,7 +1324,20 @@ int eig_precondition(const double* Xt, double* Yt, int64_t m, int64_t n, int64_t
   int* glim2 = reinterpret_cast<int*>(base + L.glim2);
   int* counts = reinterpret_cast<int*>(base + L.cnt);
   WT_CUDA(cudaMemsetAsync(mode, 0xff, sizeof(int) * (size_t)batch, st));  // -1 != 0: not yet known
-  int h_counts[2] = {0, 0};
+  // (page-locked readback scratch, one per host thread: a pageable destination costs the stream
+  // ~100 us of staging per read; [0..1] Newton-Schulz counts, [2..] the per-matrix flags)
+  static thread_local int* h_pin = nullptr;
+  static thread_local size_t h_pin_n = 0;
+  if (h_pin_n < (size_t)batch + 2) {
+    if (h_pin) cudaFreeHost(h_pin);
+    h_pin = nullptr;
+    h_pin_n = 0;
+    const size_t want = std::max<size_t>((size_t)batch + 2, 4096);
+    WT_CUDA(cudaMallocHost(&h_pin, sizeof(int) * want));
+    h_pin_n = want;
+  }
+  int* h_counts = h_pin;
+  h_counts[0] = h_counts[1] = 0;
   for (int it = 0; it < kMaxNs; ++it) {
     if (int r = gemm_f64_lim(1, 0, kk, kk, n, 1.0, Z, kk, nk, Z, kk, nk, 0.0, P, kk, kk2, batch, nullptr, glim, st, 1))
       return r;
@@ -1351,8 +1364,8 @@ int eig_precondition(const double* Xt, double* Yt, int64_t m, int64_t n, int64_t
     // (the next P of the matrices already at rounding: mode 0 is kept via ns_delta's skip)
   }
   // (after kMaxNs iterations every matrix left is done or fell back: see lim)
-  std::vector<int> hflag((size_t)batch);
-  WT_CUDA(cudaMemcpyAsync(hflag.data(), flag, sizeof(int) * (size_t)batch, cudaMemcpyDeviceToHost, st));
+  int* hflag = h_pin + 2;
+  WT_CUDA(cudaMemcpyAsync(hflag, flag, sizeof(int) * (size_t)batch, cudaMemcpyDeviceToHost, st));
   mark();
   // 6. V0 = Q Z: blocks of NBT reflectors, last block first
   // (two-stage: Z <- Q2 Z with the stage-2 reflectors, then the stage-1 reflectors

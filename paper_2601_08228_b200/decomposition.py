@@ -166,6 +166,48 @@ def sp_w_svd(a, r, levels):
     return _out(sp_w_svd_device(E.as_device(a), r, levels), dev)
 
 
+def sp_w_svd_many(cubes, r, levels, depth: int = 2):
+    """``sp_w_svd(c, r, levels)`` for every cube of an iterable, ``depth`` calls in flight.
+
+    A single call on a host cube is PCIe-bound and strictly sequential (upload, K4, download:
+    nothing can be downloaded before the whole cube has arrived).  Over a stream of cubes the
+    upload of cube i+1 runs under the K4 and the download of cube i: each call runs on its own
+    host thread and CUDA streams, so the two DMA directions and the SMs work at once.  Results
+    are yielded in order and are those of the single calls bit for bit (no reference
+    counterpart: the reference is one synchronous call per cube, decomposition.py:140-154)."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    if depth < 1:
+        raise ValueError("depth must be at least 1")
+    N_dev = torch.cuda.current_device() if torch.cuda.is_available() else 0
+
+    def work(c):
+        torch.cuda.set_device(N_dev)
+        with torch.cuda.stream(_worker_stream()):
+            return sp_w_svd(c, r, levels)
+
+    with ThreadPoolExecutor(max_workers=depth, thread_name_prefix="wten-pipe") as pool:
+        pending = []
+        for c in cubes:  # at most `depth` results in flight or waiting (each holds a pinned result buffer)
+            if len(pending) >= depth:
+                yield pending.pop(0).result()
+            pending.append(pool.submit(work, c))
+        for f in pending:
+            yield f.result()
+
+
+_WORKER_STREAMS: dict = {}
+
+
+def _worker_stream():
+    import threading
+
+    key = (torch.cuda.current_device(), threading.get_ident())
+    if key not in _WORKER_STREAMS:
+        _WORKER_STREAMS[key] = torch.cuda.Stream()
+    return _WORKER_STREAMS[key]
+
+
 # ------------------------------------------------------------------ pinv ----
 
 def pinv_w_device(x: torch.Tensor, levels: int, tol: float = 1e-12,

@@ -131,7 +131,7 @@ def pinned_empty(shape) -> np.ndarray:
 # 2 GiB, more than the whole computation); beyond the pool the result goes to
 # pageable memory through the pinned download ring instead (~2x the DMA time).
 _POOL_MIN_ELEMS = 8 << 20   # 64 MB: smaller results use torch's caching host allocator
-_POOL_PER_SIZE = 2
+_POOL_PER_SIZE = 4          # (a depth-3 pipeline of calls plus the result the caller still holds)
 _POOL_BYTES = 8 << 30
 _pool: dict = {}            # numel -> [[pinned tensor, state]]; state: None free, _BUSY, weakref to the ndarray
 _BUSY = object()
@@ -254,9 +254,10 @@ _CHUNK_BYTES = 32 << 20
 
 def _pipe_streams():
     dev = torch.cuda.current_device()
-    if dev not in _PIPE_STREAMS:
-        _PIPE_STREAMS[dev] = tuple(torch.cuda.Stream() for _ in range(3))
-    return _PIPE_STREAMS[dev]
+    key = (dev, threading.get_ident())  # per host thread: concurrent calls must not queue behind each other
+    if key not in _PIPE_STREAMS:
+        _PIPE_STREAMS[key] = tuple(torch.cuda.Stream() for _ in range(3))
+    return _PIPE_STREAMS[key]
 
 
 def _row_chunks(n1: int, row_elems: int):

@@ -220,7 +220,7 @@ def test_host_input_conventions_and_streamed_path():
 
 
 def test_host_results_pool_and_pageable_fallback():
-    """Large numpy results come from a pool of at most two pinned buffers per size that no
+    """Large numpy results come from a pool of a few (engine._POOL_PER_SIZE) pinned buffers per size that no
     caller still references; a caller keeping every result gets pageable results (staged
     through the pinned download ring) instead of a fresh page-locked block per call, with
     identical values -- for the streamed transform, its inverse and the sp_w_svd pipeline."""
@@ -228,9 +228,12 @@ def test_host_results_pool_and_pageable_fallback():
     x = rng.standard_normal((256, 256, 128))            # 8.4 M elements = 64 MiB results
     s_ref, d_ref = O.lift_forward(x, 3)
     x_back = O.lift_inverse(s_ref, d_ref)
-    kept = [W.forward_w(x, 3) for _ in range(4)]        # all alive: pool (2) exhausted
+    from paper_2601_08228_b200 import engine as E
+
+    P = E._POOL_PER_SIZE
+    kept = [W.forward_w(x, 3) for _ in range(P + 2)]    # all alive: the pool is exhausted
     pinned = [torch.from_numpy(k.smooth).is_pinned() for k in kept]
-    assert pinned[:2] == [True, True] and pinned[2:] == [False, False]
+    assert pinned[:P] == [True] * P and pinned[P:] == [False, False]
     for pyr in kept:
         assert np.array_equal(pyr.smooth, s_ref) and all(np.array_equal(a, b) for a, b in zip(pyr.details, d_ref))
         assert np.array_equal(W.inverse_w(pyr), x_back)  # pinned and pageable pyramids both stream back
@@ -240,8 +243,8 @@ def test_host_results_pool_and_pageable_fallback():
     again = W.forward_w(x, 3)                           # a freed pooled buffer is reused
     assert torch.from_numpy(again.smooth).is_pinned()
     assert np.array_equal(again.smooth, s_ref)
-    ys = [W.sp_w_svd(x, 20, 3) for _ in range(3)]      # streamed sp_w_svd, results kept
-    assert not torch.from_numpy(ys[2]).is_pinned()
+    ys = [W.sp_w_svd(x, 20, 3) for _ in range(P + 1)]  # streamed sp_w_svd, results kept
+    assert not torch.from_numpy(ys[P]).is_pinned()
     ref = O.sp_w_svd(x, 20, 3)
     for y in ys:
         assert np.array_equal(y, ys[0])

@@ -112,3 +112,28 @@ def test_pinned_numpy_inputs_are_uploaded_in_place_with_the_same_bits():
     assert np.array_equal(W.inverse_w(pb), W.inverse_w(pa))
     # a pinned view with an offset (rows 8..) is still DMA'd in place
     assert np.array_equal(W.sp_w_svd(xp[8:], 12, 3), W.sp_w_svd(np.ascontiguousarray(x[8:]), 12, 3))
+
+
+def test_sp_w_svd_many_pipeline_equals_single_calls():
+    """Two calls in flight on their own host threads and streams (upload of the next cube under the
+    K4 / download of the current one): the results, in order, are the single calls' bit for bit."""
+    import paper_2601_08228_b200 as W
+
+    rng = np.random.default_rng(29)
+    cubes = [rng.standard_normal((160, 256, 256)) for _ in range(3)]    # 80 MB each: streamed
+    pinned = W.pinned_empty(cubes[0].shape)
+    pinned[...] = cubes[0]
+    seq = [pinned, cubes[1], cubes[2], pinned, cubes[1]]
+    want = [W.sp_w_svd(c, 10, 3) for c in cubes]
+    order = [0, 1, 2, 0, 1]
+    for depth in (1, 2, 3):
+        got = list(W.sp_w_svd_many(iter(seq), 10, 3, depth=depth))
+        assert len(got) == len(seq)
+        for g, k in zip(got, order):
+            assert np.array_equal(g, want[k])
+    small = [rng.standard_normal((8, 6, 8)) for _ in range(4)]          # device path (below the streaming size)
+    for g, c in zip(W.sp_w_svd_many(small, 2, 1), small):
+        assert np.array_equal(g, W.sp_w_svd(c, 2, 1))
+    assert list(W.sp_w_svd_many([], 2, 1)) == []
+    with pytest.raises(ValueError):
+        list(W.sp_w_svd_many(small, 2, 1, depth=0))
