@@ -152,6 +152,17 @@ def host_buffer(numel: int) -> torch.Tensor:
                 ent[1] = _BUSY
                 return ent[0]
         pooled = sum(len(v) * k for k, v in _pool.items()) * 8
+        if len(lst) < _POOL_PER_SIZE and pooled + numel * 8 > _POOL_BYTES:
+            # over the cap: give up unreferenced buffers of other sizes (a workload of another shape
+            # came before; its buffers go back to torch's caching host allocator)
+            for k in list(_pool):
+                if k == numel:
+                    continue
+                keep = [e for e in _pool[k] if not (e[1] is None or (e[1] is not _BUSY and e[1]() is None))]
+                pooled -= (len(_pool[k]) - len(keep)) * k * 8
+                _pool[k] = keep
+                if pooled + numel * 8 <= _POOL_BYTES:
+                    break
         if len(lst) < _POOL_PER_SIZE and pooled + numel * 8 <= _POOL_BYTES:
             t = torch.empty(numel, dtype=F64, pin_memory=True)
             lst.append([t, _BUSY])

@@ -249,3 +249,28 @@ def test_host_results_pool_and_pageable_fallback():
     for y in ys:
         assert np.array_equal(y, ys[0])
         assert np.linalg.norm(y - ref) / np.linalg.norm(ref) < 1e-10
+
+
+def test_host_results_pool_evicts_other_sizes_at_the_cap(monkeypatch):
+    """At the pool's byte cap, unreferenced pinned buffers of other result sizes are given up
+    instead of sending the new size's results to pageable memory."""
+    import gc
+
+    rng = np.random.default_rng(6)
+    xa = rng.standard_normal((256, 256, 128))            # 64 MiB results
+    xb = rng.standard_normal((256, 288, 128))            # 72 MiB results
+    with E._pool_lock:
+        E._pool.clear()
+    monkeypatch.setattr(E, "_POOL_BYTES", 150 << 20)     # room for two buffers
+    a1, a2 = W.forward_w(xa, 2), W.forward_w(xa, 2)
+    assert torch.from_numpy(a1.smooth).is_pinned() and torch.from_numpy(a2.smooth).is_pinned()
+    b_held = W.forward_w(xb, 2)                          # cap reached, both A buffers referenced: pageable
+    assert not torch.from_numpy(b_held.smooth).is_pinned()
+    del a1, a2, b_held
+    gc.collect()
+    b1 = W.forward_w(xb, 2)                              # the free A buffers make room
+    assert torch.from_numpy(b1.smooth).is_pinned()
+    s_ref, d_ref = O.lift_forward(xb, 2)
+    assert np.array_equal(b1.smooth, s_ref) and all(np.array_equal(u, v) for u, v in zip(b1.details, d_ref))
+    with E._pool_lock:
+        E._pool.clear()
