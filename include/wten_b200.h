@@ -132,7 +132,7 @@ int wt_w_product_f64(const double* a, const double* b, int64_t n1, int64_t n2, i
  * wt_svd_factors_f64 / wt_pinv_from_svd_f64).
  * `workspace` must hold wt_svd_workspace_bytes(n1, n2, min(batch, 65535)) bytes
  * (larger batches run in chunks of 65535 matrices through that workspace).
- * tol <= 0 selects the default; max_sweeps <= 0 selects 40.
+ * tol <= 0 selects the default; max_sweeps <= 0 selects 80.
  * The call synchronizes `stream` once per sweep to test convergence.
  */
 size_t wt_svd_workspace_bytes(int64_t n1, int64_t n2, int64_t batch);

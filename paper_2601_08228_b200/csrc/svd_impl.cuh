@@ -40,6 +40,7 @@ struct SvdWs {
   int* bver;        // batch * nblk: version of every column block (bumped when its data changes)
   unsigned long long* pclean;  // batch * nblk * nblk: (ver_I, ver_J) when pair (I, J) last tested clean
   double* scale;    // batch: power-of-two input scale (absmax_scale)
+  double* gref;     // batch: largest squared column norm at the last reordering (null-column reference)
 };
 
 __host__ __device__ inline int64_t round_up(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
@@ -372,6 +373,15 @@ __device__ __forceinline__ void pair_visit(PairSmem& S, const SvdWs& ws, int b, 
   const double gmax = S.gmax;
 #endif
   const double floor_c = kFloorEps * kFloorEps / tol;
+  // Two numerically-null columns (both norms below 1e3 eps times the matrix's largest column norm at
+  // the reordering before this sweep -- sigma_1 from the second sweep on) are left to each other: when
+  // every column of a visit is null the panel-relative floor above is itself noise and such pairs
+  // rotated for ever (rank-82 123 x 245 slices: 40 sweeps without progress, found by
+  // tools/fuzz_parity.py).  Their singular values are below 1e-12 sigma_1, where the vectors are
+  // re-orthonormalised by wt_orthonormal_fixup_f64 anyway.  (A null column is still rotated against
+  // the real ones: K5's projector V_r V_r^T needs the null vectors out of the real subspace --
+  // exempting every pair with a null column gave O(1) reconstruction errors in the same sweep.)
+  const double kNull2 = kFloorEps * kFloorEps * ws.gref[b];
   {
     // 1 / max(sqrt(g_ii g_jj), floor_c g_max) = min(rsqrt(g_ii g_jj), 1 / (floor_c g_max)):
     // no sqrt and no division per pair (the test was ~10% of the kernel's stall samples)
@@ -381,7 +391,7 @@ __device__ __forceinline__ void pair_visit(PairSmem& S, const SvdWs& ws, int b, 
       const double gii = S.G[0][i * LDG + i], gjj = S.G[0][j * LDG + j];
       const double gij = S.G[0][i * LDG + j];
       double c = 0.0;
-      if (gij != 0.0) c = fabs(gij) * fmin(rsqrt(gii * gjj), rfl);
+      if (gij != 0.0 && fmax(gii, gjj) > kNull2) c = fabs(gij) * fmin(rsqrt(gii * gjj), rfl);
       if (isnan(gii) || isnan(gjj)) c = gii + gjj;
       mx = nanmax(mx, c);
     };
@@ -397,7 +407,7 @@ __device__ __forceinline__ void pair_visit(PairSmem& S, const SvdWs& ws, int b, 
         const double gii = S.G[0][i * LDG + i], gjj = S.G[0][j * LDG + j];
         const double gij = S.G[0][i * LDG + j];
         double c = 0.0;
-        if (gij != 0.0) c = fabs(gij) * fmin(rsqrt(gii * gjj), rfl);
+        if (gij != 0.0 && fmax(gii, gjj) > kNull2) c = fabs(gij) * fmin(rsqrt(gii * gjj), rfl);
         if (isnan(gii) || isnan(gjj)) c = gii + gjj;
         mx = nanmax(mx, c);
       }
@@ -461,7 +471,7 @@ __device__ __forceinline__ void pair_visit(PairSmem& S, const SvdWs& ws, int b, 
         }
         const double gpp = G[p * LDG + p], gqq = G[q * LDG + q], gpq = G[p * LDG + q];
         // rotate iff |g_pq| > tol * max(sqrt(g_pp g_qq), floor_c g_max)  (squared: no sqrt)
-        const bool rot = gpq * gpq > fmax(tol2 * (gpp * gqq), rot_floor);
+        const bool rot = gpq * gpq > fmax(tol2 * (gpp * gqq), rot_floor) && fmax(gpp, gqq) > kNull2;
         __syncwarp();
         double c = 1.0, s = 0.0;
         if (rot) {
@@ -782,6 +792,7 @@ __global__ void svd_norms_sort(SvdWs ws, int64_t mpad, int64_t npad, int64_t n, 
     // an all-zero matrix (largest norm exactly 0, e.g. the detail slices of a
     // slice-constant operator) is already diagonal: retire it before any visit
     if (threadIdx.x == 0 && key[0] == 0.0) ws.conv[b] = 1;
+    if (threadIdx.x == 0) ws.gref[b] = key[0];
     for (int i = threadIdx.x; i < npad; i += blockDim.x) ws.perm[(int64_t)b * npad + i] = idx[i];
     // the norms follow their columns (blocks skipped in the next sweep keep them valid)
     for (int i = threadIdx.x; i < n; i += blockDim.x) ws.sig[(int64_t)b * npad + i] = key[i];
@@ -852,7 +863,7 @@ __global__ void svd_flip(SvdWs ws, int batch) {
 struct WsLayout {
   int64_t m, n, mpad, npad;
   size_t off_X, off_X2, off_xsel, off_active, off_off, off_conv, off_pending, off_sig, off_perm, off_bdone,
-      off_bver, off_pclean, off_scale, off_nz, off_eig, eig_bytes, total;
+      off_bver, off_pclean, off_scale, off_gref, off_nz, off_eig, eig_bytes, total;
   bool skip;     // pair-skip bookkeeping (nblk <= kSkipMaxBlocks)
   bool precond;  // Gram-eigenbasis preconditioner (eig.cu) before the sweeps
 };
@@ -888,6 +899,7 @@ WsLayout ws_layout(int64_t n1, int64_t n2, int64_t batch, bool allow_precond = t
   L.off_bver = take(L.skip ? sizeof(int) * (size_t)(batch * nbk) : 0);
   L.off_pclean = take(L.skip ? sizeof(unsigned long long) * (size_t)(batch * nbk * nbk) : 0);
   L.off_scale = take(sizeof(double) * (size_t)batch);
+  L.off_gref = take(sizeof(double) * (size_t)batch);
   L.off_nz = take(sizeof(int) * (size_t)batch);
   L.precond = allow_precond && precond_enabled(L.n);
   L.eig_bytes = L.precond ? eig_workspace_bytes(L.n, batch) : 0;
@@ -966,7 +978,8 @@ int jacobi(const double* A, int64_t lda, int64_t strideA, int64_t n1,
            reinterpret_cast<int*>(base + L.off_conv), reinterpret_cast<int*>(base + L.off_pending),
            reinterpret_cast<double*>(base + L.off_sig), reinterpret_cast<int*>(base + L.off_perm),
            reinterpret_cast<int*>(base + L.off_bdone), reinterpret_cast<int*>(base + L.off_pending) + 2,
-           nullptr, nullptr, reinterpret_cast<double*>(base + L.off_scale)};
+           nullptr, nullptr, reinterpret_cast<double*>(base + L.off_scale),
+           reinterpret_cast<double*>(base + L.off_gref)};
   const int pair_skip = option(WT_OPT_SVD_PAIR_SKIP);
   if (L.skip && pair_skip) {
     ws.bver = reinterpret_cast<int*>(base + L.off_bver);
@@ -977,7 +990,7 @@ int jacobi(const double* A, int64_t lda, int64_t strideA, int64_t n1,
                             (cudaStream_t)stream));
   }
   if (tol <= 0.0) tol = 4.0 * 2.220446049250313e-16 * sqrt((double)L.m) + 1e-15;
-  if (max_sweeps <= 0) max_sweeps = 40;
+  if (max_sweeps <= 0) max_sweeps = 80;  // (full-rank slices take 3-17; rank-deficient ones without the preconditioner up to ~25)
   const bool right = n1 <= n2;
 
   {
@@ -1175,6 +1188,13 @@ int jacobi(const double* A, int64_t lda, int64_t strideA, int64_t n1,
     svd_gather<<<dim3((unsigned)nvec, (unsigned)batch), 256, 0, st>>>(ws, L.mpad, L.npad, L.m,
                                                                        nvec, vec);
     if (int e = check_launch("svd_gather")) return e;
+    // The normalised columns of numerically-null singular values (s_j <= 1e-12 s_0) are rounding
+    // noise -- the convergence floor leaves them wherever they are, even parallel to a real vector
+    // (two parallel columns of a 12 x 3 slice: the truncated reconstruction counted that direction
+    // twice; tools/fuzz_parity.py) -- so they are completed orthonormally here, for every consumer
+    // (K5's projector, K6, K7, matrix_svd), as LAPACK's vectors are.
+    const int64_t rfix = std::min<int64_t>(nvec, L.n);
+    if (int e = ortho_fixup_strided(vec, L.m, rfix, 1, L.m, nvec * L.m, sigma, L.n, batch, 1e-12, st)) return e;
   }
   return WT_OK;
 }

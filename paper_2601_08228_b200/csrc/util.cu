@@ -283,8 +283,10 @@ __device__ double ortho_block_sum(double v, double* red) {
 }
 
 __global__ void __launch_bounds__(OT) ortho_fixup_kernel(double* __restrict__ M, int64_t rows, int64_t r,
-                                                         int64_t ld, int64_t sM, const double* __restrict__ s,
-                                                         int64_t q, double tau) {
+                                                         int64_t ld, int64_t cs, int64_t sM,
+                                                         const double* __restrict__ s, int64_t q, double tau) {
+  // element (row i, column j) at Mb[i * ld + j * cs]: (ld, 1) for rows x r blocks, (1, vector pitch)
+  // for K4's vectors-as-rows output
   extern __shared__ double osm[];  // dots [r], red [8]
   double* dots = osm;
   double* red = osm + r;
@@ -299,12 +301,12 @@ __global__ void __launch_bounds__(OT) ortho_fixup_kernel(double* __restrict__ M,
     bool fresh = false;
     for (int attempt = 0; attempt <= rows; ++attempt) {
       if (fresh) {  // candidate e_k
-        for (int64_t i = threadIdx.x; i < rows; i += OT) Mb[i * ld + j] = (i == next_e) ? 1.0 : 0.0;
+        for (int64_t i = threadIdx.x; i < rows; i += OT) Mb[i * ld + j * cs] = (i == next_e) ? 1.0 : 0.0;
         ++next_e;
         __syncthreads();
       }
       double nrm0 = 0.0;
-      for (int64_t i = threadIdx.x; i < rows; i += OT) nrm0 = fma(Mb[i * ld + j], Mb[i * ld + j], nrm0);
+      for (int64_t i = threadIdx.x; i < rows; i += OT) nrm0 = fma(Mb[i * ld + j * cs], Mb[i * ld + j * cs], nrm0);
       nrm0 = sqrt(ortho_block_sum(nrm0, red));
       if (!(nrm0 > 0.0) || !isfinite(nrm0)) {  // nothing to orthogonalise: take a unit vector
         fresh = true;
@@ -315,31 +317,31 @@ __global__ void __launch_bounds__(OT) ortho_fixup_kernel(double* __restrict__ M,
         const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
         for (int64_t c = warp; c < j; c += OT / 32) {
           double d = 0.0;
-          for (int64_t i = lane; i < rows; i += 32) d = fma(Mb[i * ld + c], Mb[i * ld + j], d);
+          for (int64_t i = lane; i < rows; i += 32) d = fma(Mb[i * ld + c * cs], Mb[i * ld + j * cs], d);
 #pragma unroll
           for (int o = 16; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
           if (lane == 0) dots[c] = d;
         }
         __syncthreads();
         for (int64_t i = threadIdx.x; i < rows; i += OT) {
-          double v = Mb[i * ld + j];
-          for (int64_t c = 0; c < j; ++c) v = fma(-dots[c], Mb[i * ld + c], v);
-          Mb[i * ld + j] = v;
+          double v = Mb[i * ld + j * cs];
+          for (int64_t c = 0; c < j; ++c) v = fma(-dots[c], Mb[i * ld + c * cs], v);
+          Mb[i * ld + j * cs] = v;
         }
         __syncthreads();
       }
       double nrm = 0.0;
-      for (int64_t i = threadIdx.x; i < rows; i += OT) nrm = fma(Mb[i * ld + j], Mb[i * ld + j], nrm);
+      for (int64_t i = threadIdx.x; i < rows; i += OT) nrm = fma(Mb[i * ld + j * cs], Mb[i * ld + j * cs], nrm);
       nrm = sqrt(ortho_block_sum(nrm, red));
       if (nrm > 0.5 * nrm0) {  // an independent direction survived: normalise it
         const double inv = 1.0 / nrm;
-        for (int64_t i = threadIdx.x; i < rows; i += OT) Mb[i * ld + j] *= inv;
+        for (int64_t i = threadIdx.x; i < rows; i += OT) Mb[i * ld + j * cs] *= inv;
         __syncthreads();
         break;
       }
       if (!fresh && nrm > 1e-8 * nrm0) {  // mostly dependent but not empty: keep its independent part
         const double inv = 1.0 / nrm;
-        for (int64_t i = threadIdx.x; i < rows; i += OT) Mb[i * ld + j] *= inv;
+        for (int64_t i = threadIdx.x; i < rows; i += OT) Mb[i * ld + j * cs] *= inv;
         __syncthreads();
         // one more round of orthogonalisation in the next attempt
         continue;
@@ -351,16 +353,23 @@ __global__ void __launch_bounds__(OT) ortho_fixup_kernel(double* __restrict__ M,
 }  // namespace ortho
 }  // namespace wt
 
+namespace wt {
+int ortho_fixup_strided(double* M, int64_t rows, int64_t r, int64_t si, int64_t sj, int64_t strideM,
+                        const double* s, int64_t q, int64_t batch, double tau, void* stream) {
+  if (batch == 0 || r == 0) return WT_OK;
+  WT_REQUIRE(batch <= 2147483647, "orthonormal_fixup: batch too large");
+  const size_t smem = sizeof(double) * (size_t)(r + ortho::OT / 32);
+  if (int e = ensure_smem(ortho::ortho_fixup_kernel, smem)) return e;
+  ortho::ortho_fixup_kernel<<<(unsigned)batch, ortho::OT, smem, (cudaStream_t)stream>>>(M, rows, r, si, sj, strideM,
+                                                                                         s, q, tau);
+  return check_launch("wt_orthonormal_fixup_f64");
+}
+}  // namespace wt
+
 extern "C" int wt_orthonormal_fixup_f64(double* M, int64_t rows, int64_t r, int64_t ld, int64_t strideM,
                                         const double* s, int64_t q, int64_t batch, double tau, void* stream) {
   WT_REQUIRE(rows >= 0 && r >= 0 && r <= q && r <= rows && batch >= 0 && ld >= r, "orthonormal_fixup: bad shape");
-  if (batch == 0 || r == 0) return WT_OK;
-  WT_REQUIRE(batch <= 2147483647, "orthonormal_fixup: batch too large");
-  const size_t smem = sizeof(double) * (size_t)(r + wt::ortho::OT / 32);
-  if (int e = ensure_smem(wt::ortho::ortho_fixup_kernel, smem)) return e;
-  wt::ortho::ortho_fixup_kernel<<<(unsigned)batch, wt::ortho::OT, smem, (cudaStream_t)stream>>>(M, rows, r, ld,
-                                                                                                 strideM, s, q, tau);
-  return check_launch("wt_orthonormal_fixup_f64");
+  return wt::ortho_fixup_strided(M, rows, r, ld, 1, strideM, s, q, batch, tau, stream);
 }
 
 // ------------------------------------------------------------ LU pivots --
