@@ -1,7 +1,7 @@
 """Randomised parity sweep of the public API against the CPU oracle (test infrastructure: the
 oracle is the checker).  Shapes, levels, ranks, spectra and host / device modes are drawn at random;
 bars as in the tests (transform bit-exact, products 1e-10, reconstructions / pseudo-inverses 1e-8).
-usage: python tools/fuzz_parity.py [cases] [seed]"""
+usage: python tools/fuzz_parity.py [cases] [seed] [big]   (big: 130..700-wide slices, 2..8 bands)"""
 import os
 import sys
 import warnings
@@ -15,6 +15,7 @@ from oracle import wten_oracle as O  # noqa: E402
 
 cases = int(sys.argv[1]) if len(sys.argv) > 1 else 200
 seed = int(sys.argv[2]) if len(sys.argv) > 2 else 0
+BIG = len(sys.argv) > 3 and sys.argv[3] == "big"
 rng = np.random.default_rng(seed)
 warnings.simplefilter("ignore")
 from paper_2601_08228_b200 import engine as _E  # noqa: E402
@@ -58,6 +59,9 @@ for c in range(cases):
     if rng.random() < 0.1:
         n1, n2 = int(rng.integers(100, 300)), int(rng.integers(100, 300))
     p = int(rng.choice(PS))
+    if BIG:  # preconditioned / two-stage K4 paths: wide slices, few bands
+        n1, n2 = (int(v) for v in rng.choice([130, 200, 256, 300, 384, 512, 520, 600, 640, 700], 2))
+        p = int(rng.choice([2, 4, 6, 8]))
     L = int(rng.integers(1, O.max_levels(p) + 1))
     kind = str(rng.choice(KINDS))
     dev = bool(rng.random() < 0.5)
@@ -87,6 +91,21 @@ for c in range(cases):
         if kind in ("normal", "lowrank", "const", "zero"):  # cut-off ties are ill-posed on graded / sparse spectra
             pw = O.pinv_w(a, L, tol)
             errs["pinv_w"] = rel(host(W.pinv_w(wrap(a), L, tol)), pw) / 1e-8 if kind != "lowrank" else 0.0
+        errs["transpose"] = 0.0 if np.array_equal(host(W.transpose(wrap(a))), O.transpose(a)) else 1.0
+        errs["truncation_bound"] = abs(W.truncation_bound(f, r).bound - O.truncation_bound(want["sigma_table"], r)) / (
+            1e-8 * max(np.linalg.norm(a.ravel()), 1e-300))
+        if kind in ("normal", "const", "zero"):
+            errs["sp_pinv_w"] = rel(host(W.sp_pinv_w(wrap(a), L, tol)), O.sp_pinv_w(a, L, tol)) / 1e-8
+        if kind == "normal" and min(n1, n2) <= 64:
+            errs["pinv_w_via_factors"] = rel(host(W.pinv_w_via_factors(wrap(a), L, 1e-12)), O.pinv_w(a, L, 1e-12)) / 1e-8
+            sq = cube((n2, n2, p), "normal") + 4.0 * np.sqrt(n2) * np.eye(n2)[:, :, None]
+            errs["inverse_tensor"] = rel(host(W.inverse_tensor(wrap(sq), L)), O.inverse_tensor(sq, L)) / 1e-8
+            pa, pb = W.forward_w(wrap(a), L), W.forward_w(wrap(b), L)
+            sa, da = O.lift_forward(a, L)
+            sb_, db_ = O.lift_forward(b, L)
+            fp = W.face_product(pa, pb)
+            errs["face_product"] = max([rel(host(fp.smooth), O.face_matmul(sa, sb_))]
+                                       + [rel(host(u), O.face_matmul(x, y)) for u, x, y in zip(fp.details, da, db_)]) / 1e-10
         bad = {k: v for k, v in errs.items() if not v <= 1.0}
         for k, v in errs.items():
             worst[k] = max(worst.get(k, 0.0), v)
