@@ -426,8 +426,10 @@ def headline_single(args, x_host, sampler):
     # uploaded and its result downloaded, the two PCIe directions and K4 of neighbouring calls overlap
     del y_host
     n_pipe = 4 * e2e_steps
-    for _ in W.sp_w_svd_many((x_pin for _ in range(6)), r, L):  # (warm-up: the third pooled pinned result buffer)
-        pass
+    # warm-up: every result kept, so the pool page-locks all of its result buffers now (a 2 GiB
+    # cudaHostAlloc costs ~0.9 s; in the timed stream below it landed in some runs and not in others)
+    keep = list(W.sp_w_svd_many((x_pin for _ in range(5)), r, L))
+    del keep
     torch.cuda.synchronize()
     t = time.perf_counter()
     for y_host in W.sp_w_svd_many((x_pin for _ in range(n_pipe)), r, L):
@@ -570,14 +572,17 @@ def transform_key(args, dist, rank, ws, with_cpu):
     for _ in range(2):  # (as the timed loop: the previous result alive while the next call runs, so
         for L in CFG2_LEVELS:  # the pool's third pinned result buffer is page-locked here, not there)
             o = W.inverse_w(W.forward_w(x_pin, L))
-    t = time.perf_counter()
-    for L in CFG2_LEVELS:
-        o = W.inverse_w(W.forward_w(x_pin, L))
-    dt = time.perf_counter() - t
+    dts = []
+    for _ in range(3):  # median of three passes (a pass that page-locks a new pooled buffer costs +0.2 s)
+        t = time.perf_counter()
+        for L in CFG2_LEVELS:
+            o = W.inverse_w(W.forward_w(x_pin, L))
+        dts.append(time.perf_counter() - t)
+    dt = sorted(dts)[1]
     assert float(np.linalg.norm((o - x_host).ravel()) / np.linalg.norm(x_host.ravel())) < 1e-12
     out["e2e"] = {"value": round(bytes_step / dt / 1e9, 2), "unit": "GB/s",
                   "api": "inverse_w(forward_w(numpy cube in page-locked memory, L)) for L = 1, 2, 4, 8 "
-                         "(pyramid returned to host)",
+                         "(pyramid returned to host); median of 3 passes",
                   "h2d_bytes_per_step": len(CFG2_LEVELS) * 16 * N, "d2h_bytes_per_step": len(CFG2_LEVELS) * 16 * N}
     if with_cpu:
         from oracle import parallel as P

@@ -1192,9 +1192,11 @@ int jacobi(const double* A, int64_t lda, int64_t strideA, int64_t n1,
     // noise -- the convergence floor leaves them wherever they are, even parallel to a real vector
     // (two parallel columns of a 12 x 3 slice: the truncated reconstruction counted that direction
     // twice; tools/fuzz_parity.py) -- so they are completed orthonormally here, for every consumer
-    // (K5's projector, K6, K7, matrix_svd), as LAPACK's vectors are.
+    // (K5's projector, K6, K7, matrix_svd), as LAPACK's vectors are.  All-zero matrices are skipped
+    // (config 5's 224 zero detail slices would each cost a 512-vector Gram-Schmidt: 188 ms; K6 and
+    // matrix_svd, which hand vectors out, complete those themselves).
     const int64_t rfix = std::min<int64_t>(nvec, L.n);
-    if (int e = ortho_fixup_strided(vec, L.m, rfix, 1, L.m, nvec * L.m, sigma, L.n, batch, 1e-12, st)) return e;
+    if (int e = ortho_fixup_strided(vec, L.m, rfix, 1, L.m, nvec * L.m, sigma, L.n, batch, 1e-12, st, 1)) return e;
   }
   return WT_OK;
 }

@@ -284,7 +284,8 @@ __device__ double ortho_block_sum(double v, double* red) {
 
 __global__ void __launch_bounds__(OT) ortho_fixup_kernel(double* __restrict__ M, int64_t rows, int64_t r,
                                                          int64_t ld, int64_t cs, int64_t sM,
-                                                         const double* __restrict__ s, int64_t q, double tau) {
+                                                         const double* __restrict__ s, int64_t q, double tau,
+                                                         int skip_zero) {
   // element (row i, column j) at Mb[i * ld + j * cs]: (ld, 1) for rows x r blocks, (1, vector pitch)
   // for K4's vectors-as-rows output
   extern __shared__ double osm[];  // dots [r], red [8]
@@ -294,6 +295,7 @@ __global__ void __launch_bounds__(OT) ortho_fixup_kernel(double* __restrict__ M,
   double* Mb = M + b * sM;
   const double* sb = s + b * q;
   const double smax = sb[0];
+  if (skip_zero && !(smax > 0.0)) return;  // an all-zero matrix: nothing refers to its vectors (K4's own pass)
   int64_t next_e = 0;  // next unit-vector candidate
   for (int64_t j = 0; j < r; ++j) {
     const double sj = sb[j];
@@ -355,13 +357,13 @@ __global__ void __launch_bounds__(OT) ortho_fixup_kernel(double* __restrict__ M,
 
 namespace wt {
 int ortho_fixup_strided(double* M, int64_t rows, int64_t r, int64_t si, int64_t sj, int64_t strideM,
-                        const double* s, int64_t q, int64_t batch, double tau, void* stream) {
+                        const double* s, int64_t q, int64_t batch, double tau, void* stream, int skip_zero) {
   if (batch == 0 || r == 0) return WT_OK;
   WT_REQUIRE(batch <= 2147483647, "orthonormal_fixup: batch too large");
   const size_t smem = sizeof(double) * (size_t)(r + ortho::OT / 32);
   if (int e = ensure_smem(ortho::ortho_fixup_kernel, smem)) return e;
   ortho::ortho_fixup_kernel<<<(unsigned)batch, ortho::OT, smem, (cudaStream_t)stream>>>(M, rows, r, si, sj, strideM,
-                                                                                         s, q, tau);
+                                                                                         s, q, tau, skip_zero);
   return check_launch("wt_orthonormal_fixup_f64");
 }
 }  // namespace wt
@@ -369,7 +371,7 @@ int ortho_fixup_strided(double* M, int64_t rows, int64_t r, int64_t si, int64_t 
 extern "C" int wt_orthonormal_fixup_f64(double* M, int64_t rows, int64_t r, int64_t ld, int64_t strideM,
                                         const double* s, int64_t q, int64_t batch, double tau, void* stream) {
   WT_REQUIRE(rows >= 0 && r >= 0 && r <= q && r <= rows && batch >= 0 && ld >= r, "orthonormal_fixup: bad shape");
-  return wt::ortho_fixup_strided(M, rows, r, ld, 1, strideM, s, q, batch, tau, stream);
+  return wt::ortho_fixup_strided(M, rows, r, ld, 1, strideM, s, q, batch, tau, stream, 0);
 }
 
 // ------------------------------------------------------------ LU pivots --

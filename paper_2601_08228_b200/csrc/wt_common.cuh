@@ -46,7 +46,8 @@ int scale_cols_lim(double* M, int64_t rows, int64_t ncols, int64_t ld, int64_t s
 
 // wt_orthonormal_fixup_f64 with general strides: element (row i, vector j) at M[i * si + j * sj].
 int ortho_fixup_strided(double* M, int64_t rows, int64_t r, int64_t si, int64_t sj, int64_t strideM,
-                        const double* s, int64_t q, int64_t batch, double tau, void* stream);
+                        const double* s, int64_t q, int64_t batch, double tau, void* stream, int skip_zero);
+// (skip_zero: matrices whose largest singular value is 0 are left untouched)
 
 #define WT_REQUIRE(cond, ...)        \
   do {                               \

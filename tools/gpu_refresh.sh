@@ -23,4 +23,6 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:trid
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:svd_sweep_kernel --launch-skip 2 -c 1 -o $O/k4_sweep_cfg3 -f python tools/eig_one.py 3 > $O/ncu_k4_3.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:gemm_f64_kernel -c 1 -o $O/gemm -f python tools/gemm_one.py > $O/ncu_gemm.log 2>&1
 timeout 900 ncu --set full --clock-control none -k regex:"fwd_|inv_" -c 8 -o $O/lift -f python tools/lift_one.py 1 2 4 8 > $O/ncu_lift.log 2>&1
+timeout 600 ncu --metrics $M --clock-control none -c 200 --csv --log-file $O/imaging_launches.csv python tools/imaging_probe.py > $O/ncu_imaging.log 2>&1
+timeout 900 python tools/fuzz_parity.py 200 7 > $O/fuzz.log 2>&1
 for f in $O/*.ncu-rep; do ncu -i $f --page raw --csv > ${f%.ncu-rep}_raw.csv 2>/dev/null; done

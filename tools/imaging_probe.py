@@ -1,9 +1,12 @@
 """Time the GPU imaging helpers at BASELINE sizes (write bandwidth vs the HBM peak)."""
+import os
+import sys
 import time
 
 import numpy as np
 import torch
 
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2601_08228_b200 import engine as E, imaging, synth
 
 
