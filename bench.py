@@ -600,7 +600,7 @@ def transform_key(args, dist, rank, ws, with_cpu):
 
 # ----------------------------------------------------------- workloads ----
 
-def wsvd_workload(args, steps=3, warmup=1):
+def wsvd_workload(args, steps=5, warmup=3):
     """Config 3: w_svd rank 20 of the 256x256x192 cube, L = 3."""
     import torch
 
@@ -665,7 +665,7 @@ def api_e2e(fn, reps):
     return (time.perf_counter() - t) / reps * 1e3
 
 
-def deblur_workload(args, steps=2, warmup=1):
+def deblur_workload(args, steps=3, warmup=3):
     """Config 5: w-pinv deblurring recovery (2 pinv_w + 2 w_product), 512x512x128, L = 3."""
     import torch
 
