@@ -292,7 +292,7 @@ int wt_hsi_mix_f64(const double* ab, const double* spectra, int64_t npix, int64_
 #define WT_OPT_EIG_PROFILE 7      /* 1: preconditioner phase times on stderr */
 #define WT_OPT_EIG_TWOSTAGE 8     /* 1: two-stage tridiagonalization for wide Grams in leading-triplet mode (default) */
 #define WT_OPT_GEMM_TMA 9         /* 1: K3 large tiles fed by tensor-map TMA boxes (default); 0: cp.async ring */
-#define WT_OPT_EIG_SPLIT 10       /* 0: host rule; 1: never, 2: always run the two-stage reduction as two half-batches on two streams */
+#define WT_OPT_EIG_SPLIT 10       /* 0: host rule; 1: never; 2, 3, 4: always run the two-stage reduction as that many groups of matrices on their own streams */
 #define WT_OPT_COUNT 11
 int wt_set_option(int option, int value);
 

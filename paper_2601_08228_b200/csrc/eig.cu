@@ -1098,16 +1098,18 @@ bool make_gmap(CUtensorMap* map, double* G, int64_t n, int64_t batch) {
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-// One non-blocking side stream per device for the second half of a split two-stage reduction
+// Non-blocking side streams per device for the other groups of a split two-stage reduction
 // (created once; ordered against the caller's stream by per-call events).
-cudaStream_t side_stream() {
+constexpr int kSideStreams = 3;
+cudaStream_t side_stream(int i = 0) {
   static std::mutex mu;
-  static cudaStream_t streams[64] = {};
+  static cudaStream_t streams[64][kSideStreams] = {};
   int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64 || i < 0 || i >= kSideStreams) return nullptr;
   std::lock_guard<std::mutex> lock(mu);
-  if (!streams[dev] && cudaStreamCreateWithFlags(&streams[dev], cudaStreamNonBlocking) != cudaSuccess) return nullptr;
-  return streams[dev];
+  if (!streams[dev][i] && cudaStreamCreateWithFlags(&streams[dev][i], cudaStreamNonBlocking) != cudaSuccess)
+    return nullptr;
+  return streams[dev][i];
 }
 
 // Two-stage path: wide Grams whose rows below the band fit one row per thread,
@@ -1250,23 +1252,36 @@ int eig_precondition(const double* Xt, double* Yt, int64_t m, int64_t n, int64_t
     // panels run under the other half's trailing passes; both band chases (one SM per matrix) run
     // side by side at the end.  Per-matrix arithmetic does not depend on the split.
     const int split_opt = option(WT_OPT_EIG_SPLIT);
-    const bool split = split_opt == 2 || (split_opt == 0 && batch >= 16 && !prof);
-    if (split && batch >= 2) {
-      cudaStream_t side = side_stream();
-      WT_REQUIRE(side != nullptr, "eig: side stream creation failed");
-      cudaEvent_t fork = nullptr, join = nullptr;
+    const bool split = split_opt >= 2 || (split_opt == 0 && batch >= 16 && !prof);
+    // groups: 2 by default; WT_OPT_EIG_SPLIT = 2 / 3 / 4 forces that many (diagnostics)
+    const int groups = (int)std::min<int64_t>(batch, split_opt >= 2 ? std::min(split_opt, kSideStreams + 1) : 2);
+    if (split && groups >= 2) {
+      cudaEvent_t fork = nullptr, join[kSideStreams] = {};
       WT_CUDA(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
-      WT_CUDA(cudaEventCreateWithFlags(&join, cudaEventDisableTiming));
-      const int64_t h = (batch + 1) / 2;
       int r = WT_OK;
-      if (cudaEventRecord(fork, st) != cudaSuccess || cudaStreamWaitEvent(side, fork, 0) != cudaSuccess) r = WT_ERR_CUDA;
-      // (alternate the issue order? the streams are independent queues: host order only matters for
-      // when work becomes visible, and enqueueing is far faster than execution)
-      if (!r) r = reduce(h, batch - h, side);
-      if (!r) r = reduce(0, h, st);
-      if (cudaEventRecord(join, side) != cudaSuccess || cudaStreamWaitEvent(st, join, 0) != cudaSuccess) r = r ? r : WT_ERR_CUDA;
+      if (cudaEventRecord(fork, st) != cudaSuccess) r = WT_ERR_CUDA;
+      // group g: matrices [g h, min(batch, (g + 1) h)); group 0 on the caller's stream, issued last
+      const int64_t h = (batch + groups - 1) / groups;
+      for (int g = groups - 1; g >= 0 && !r; --g) {
+        const int64_t b0 = g * h, nb = std::min<int64_t>(h, batch - b0);
+        if (nb <= 0) continue;
+        if (g == 0) {
+          r = reduce(0, nb, st);
+          continue;
+        }
+        cudaStream_t side = side_stream(g - 1);
+        if (side == nullptr || cudaStreamWaitEvent(side, fork, 0) != cudaSuccess) r = WT_ERR_CUDA;
+        if (!r) r = reduce(b0, nb, side);
+        if (!r && (cudaEventCreateWithFlags(&join[g - 1], cudaEventDisableTiming) != cudaSuccess ||
+                   cudaEventRecord(join[g - 1], side) != cudaSuccess))
+          r = WT_ERR_CUDA;
+      }
+      for (int g = 0; g < kSideStreams; ++g) {
+        if (!join[g]) continue;
+        if (cudaStreamWaitEvent(st, join[g], 0) != cudaSuccess) r = r ? r : WT_ERR_CUDA;
+        cudaEventDestroy(join[g]);
+      }
       cudaEventDestroy(fork);
-      cudaEventDestroy(join);
       if (r) return r;
     } else {
       if (int r = reduce(0, batch, st)) return r;

@@ -33,7 +33,7 @@ static std::atomic<int> g_options[WT_OPT_COUNT] = {
     {0},  // WT_OPT_EIG_PROFILE: preconditioner phase times on stderr
     {1},  // WT_OPT_EIG_TWOSTAGE: two-stage tridiagonalization (eig_sbr.cuh) where eligible
     {1},  // WT_OPT_GEMM_TMA: K3 large tiles through the tensor-map variant
-    {0},  // WT_OPT_EIG_SPLIT: 0 = host rule, 1 = never, 2 = always split the two-stage reduction over two streams
+    {0},  // WT_OPT_EIG_SPLIT: 0 = host rule, 1 = never, 2 / 3 / 4 = always split the two-stage reduction into that many groups on their own streams
 };
 
 int option(int which) { return (which >= 0 && which < WT_OPT_COUNT) ? g_options[which].load() : 0; }

@@ -1,5 +1,5 @@
-"""Two-stage reduction as two half-batches on two streams (WT_OPT_EIG_SPLIT): bit-identity and
-leading-triplet call time, split vs unsplit.  usage: python tools/split_probe.py"""
+"""Two-stage reduction as 2 / 3 / 4 groups of matrices on their own streams (WT_OPT_EIG_SPLIT):
+bit-identity and leading-triplet call time, split vs unsplit.  usage: python tools/split_probe.py"""
 import os
 import sys
 import time
@@ -30,8 +30,10 @@ for shape in [(32, 1024, 1024), (16, 1024, 1024), (8, 1024, 1024), (4, 1024, 102
     with E.option("eig_split", 1):
         ref = E.svd_truncated_recon(at, 30)
         t1 = timed(lambda: E.svd_truncated_recon(at, 30))
-    with E.option("eig_split", 2):
-        got = E.svd_truncated_recon(at, 30)
-        same = torch.equal(got, ref) and all(torch.equal(E.svd_truncated_recon(at, 30), ref) for _ in range(3))
-        t2 = timed(lambda: E.svd_truncated_recon(at, 30))
-    print(f"{shape}: unsplit {t1:.2f} ms, split {t2:.2f} ms, same bits {same}", flush=True)
+    res = []
+    for g in (2, 3, 4):
+        with E.option("eig_split", g):
+            got = E.svd_truncated_recon(at, 30)
+            same = torch.equal(got, ref) and all(torch.equal(E.svd_truncated_recon(at, 30), ref) for _ in range(3))
+            res.append(f"{g} groups {timed(lambda: E.svd_truncated_recon(at, 30)):.2f} ms (same bits {same})")
+    print(f"{shape}: unsplit {t1:.2f} ms, " + ", ".join(res), flush=True)
