@@ -422,7 +422,7 @@ def headline_single(args, x_host, sampler):
     e2e_pageable_s, y_host = e2e_leg(x_host)
     del y_host  # (its pinned result buffer goes back to the pool of two before the next leg)
     e2e_s, y_host = e2e_leg(x_pin)
-    # the same calls as a stream of cubes, two in flight (W.sp_w_svd_many): every cube is still
+    # the same calls as a stream of cubes, three in flight (W.sp_w_svd_many): every cube is still
     # uploaded and its result downloaded, the two PCIe directions and K4 of neighbouring calls overlap
     del y_host
     n_pipe = 4 * e2e_steps
@@ -439,7 +439,7 @@ def headline_single(args, x_host, sampler):
            "ms_per_call": round(e2e_s * 1e3, 2), "steps": e2e_steps,
            "ms_per_call_pageable_input": round(e2e_pageable_s * 1e3, 2),
            "pipelined": {"value": round(N / pipe_s, 1), "unit": UNIT, "ms_per_cube": round(pipe_s * 1e3, 2),
-                         "cubes": n_pipe, "api": "sp_w_svd_many(stream of page-locked numpy cubes, 30, 4): two "
+                         "cubes": n_pipe, "api": "sp_w_svd_many(stream of page-locked numpy cubes, 30, 4): three "
                          "calls in flight, every cube uploaded and every result downloaded"},
            "api": "sp_w_svd(numpy cube in page-locked memory, 30, 4) -> numpy reconstruction (H2D of the 2 GiB cube "
                   "and D2H of the 2 GiB result inside every call; ms_per_call_pageable_input: the same call on a "

@@ -224,6 +224,14 @@ int wt_tube_delta_f64(const double* x, int64_t ntubes, int64_t p, double* out, v
 int wt_tube_transpose_f64(const double* x, int64_t n1, int64_t n2, int64_t p, double* y,
                           void* stream);
 
+/* n int32 values from device memory into PAGE-LOCKED host memory, then a
+ * synchronisation of `stream`: a one-warp kernel stores straight into the mapped
+ * host block instead of a copy-engine copy, so a status readback (K4's info
+ * vector: the reference's LinAlgError check, decomposition.py:66) does not queue
+ * behind bulk transfers other streams have in flight.  host_pinned must come
+ * from cudaMallocHost / cudaHostAlloc / a pinned torch tensor. */
+int wt_readback_i32(const int* src, int* host_pinned, int64_t n, void* stream);
+
 /* Orthonormal completion of singular-vector columns: M[b] is rows x r (pitch ld,
  * stride strideM), its columns in the order of s[b*q + 0 ..] (descending).  Every
  * column j with s_j <= tau * s_0 (or s_j == 0 / non-finite) is re-orthonormalised

@@ -70,6 +70,7 @@ SIGNATURES = {
                                                    c_double_p, ctypes.c_void_p, ctypes.c_void_p]),
     "wt_tube_delta_f64": (ctypes.c_int, [c_double_p, i64, i64, c_double_p, ctypes.c_void_p]),
     "wt_tube_transpose_f64": (ctypes.c_int, [c_double_p, i64, i64, i64, c_double_p, ctypes.c_void_p]),
+    "wt_readback_i32": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, i64, ctypes.c_void_p]),
     "wt_orthonormal_fixup_f64": (ctypes.c_int, [c_double_p, i64, i64, i64, i64, c_double_p, i64, i64,
                                                 ctypes.c_double, ctypes.c_void_p]),
     "wt_lu_pivot_check_f64": (ctypes.c_int, [c_double_p, i64, i64, ctypes.c_void_p, ctypes.c_void_p]),

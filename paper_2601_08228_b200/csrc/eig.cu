@@ -1364,7 +1364,7 @@ int eig_precondition(const double* Xt, double* Yt, int64_t m, int64_t n, int64_t
     const double lim = it == kMaxNs - 1 ? cbrt(done_tol / 0.3125) : 0.25;
     ns_decide<<<(unsigned)((batch + 255) / 256), 256, 0, st>>>(delta, (int)batch, done_tol, lim, flag, glim, mode,
                                                              glim2, counts);
-    WT_CUDA(cudaMemcpyAsync(h_counts, counts, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
+    WT_CUDA(readback_ints(h_counts, counts, 2, st));  // (not a copy-engine copy: wt_common.cuh)
     WT_CUDA(cudaStreamSynchronize(st));
     if (h_counts[0] == 0) break;  // every matrix orthogonal (or fallen back)
     // P^2 for the order-3 matrices (lower tiles; P still holds the lower triangle of Z^T Z)
@@ -1380,7 +1380,7 @@ int eig_precondition(const double* Xt, double* Yt, int64_t m, int64_t n, int64_t
   }
   // (after kMaxNs iterations every matrix left is done or fell back: see lim)
   int* hflag = h_pin + 2;
-  WT_CUDA(cudaMemcpyAsync(hflag, flag, sizeof(int) * (size_t)batch, cudaMemcpyDeviceToHost, st));
+  WT_CUDA(readback_ints(hflag, flag, (int)batch, st));
   mark();
   // 6. V0 = Q Z: blocks of NBT reflectors, last block first
   // (two-stage: Z <- Q2 Z with the stage-2 reflectors, then the stage-1 reflectors

@@ -1051,7 +1051,8 @@ int jacobi(const double* A, int64_t lda, int64_t strideA, int64_t n1,
     ws.prof = d_prof;
   }
   static thread_local int* h_pending = nullptr;  // per host thread: concurrent calls on other streams
-  if (!h_pending) WT_CUDA(cudaMallocHost(&h_pending, sizeof(int)));
+  if (!h_pending) WT_CUDA(cudaMallocHost(&h_pending, 2 * sizeof(int)));  // [pending, rotated visits]
+  h_pending[0] = h_pending[1] = 0;
   const int nb = (int)(L.npad / HB);
   // One inner Jacobi sweep per pair visit: measured on the config-3/4 slices it
   // needs the same number of outer sweeps as full diagonalisation (13 / 18) at
@@ -1156,16 +1157,14 @@ int jacobi(const double* A, int64_t lda, int64_t strideA, int64_t n1,
     }
     WT_CUDA(cudaMemsetAsync(ws.pending, 0, sizeof(int), st));
     svd_end_sweep<<<(unsigned)((batch + 255) / 256), 256, 0, st>>>(ws, (int)batch, tol);
-    WT_CUDA(cudaMemcpyAsync(h_pending, ws.pending, sizeof(int), cudaMemcpyDeviceToHost, st));
+    WT_CUDA(readback_ints(h_pending, ws.pending, 2, st));  // (not a copy-engine copy: wt_common.cuh)
     WT_CUDA(cudaStreamSynchronize(st));
     g_last_sweeps = sweep + 1;
     if (*h_pending == 0) { hit_max = false; break; }
     n_active = *h_pending;  // svd_end_sweep compacted the survivors into ws.active
   }
   {
-    int rotated = 0;  // stream is idle here (synchronised at the end of the last sweep)
-    WT_CUDA(cudaMemcpy(&rotated, ws.pending + 1, sizeof(int), cudaMemcpyDeviceToHost));
-    g_last_rotations = rotated;
+    g_last_rotations = h_pending[1];  // read back with the last sweep's pending count
     g_last_panel_rows = L.mpad;
   }
   if (profile) {

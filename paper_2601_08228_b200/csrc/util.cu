@@ -471,3 +471,12 @@ extern "C" int wt_diag_blocks_f64(const double* s, int64_t q, int64_t r, int64_t
   wt::ortho::diag_blocks_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(s, q, r, batch, S);
   return check_launch("wt_diag_blocks_f64");
 }
+
+extern "C" int wt_readback_i32(const int* src, int* host_pinned, int64_t n, void* stream) {
+  WT_REQUIRE(n >= 0 && n <= (int64_t)1 << 30, "readback: bad count %lld", (long long)n);
+  if (n == 0) return WT_OK;
+  WT_REQUIRE(src && host_pinned, "readback: null pointer");
+  WT_CUDA(wt::readback_ints(host_pinned, src, (int)n, (cudaStream_t)stream));
+  WT_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
+  return WT_OK;
+}

