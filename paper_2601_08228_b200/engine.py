@@ -750,7 +750,7 @@ def raise_if_failed(info: torch.Tensor):
             buf = torch.empty(max(n, 1024), dtype=torch.int32, pin_memory=True)
             _readback_tls.buf = buf
         with torch.cuda.device(info.device):
-            N.check(N.require_gpu().wt_readback_i32(_ptr(info), buf.data_ptr(), n, _stream()))
+            N.check(N.require_gpu().wt_readback_i32(_ptr(info), buf.data_ptr(), n, _stream()), "wt_readback_i32")
         failed = bool((buf[:n] != 0).any())
     else:
         failed = bool((info.cpu() != 0).any())

@@ -137,3 +137,31 @@ def test_sp_w_svd_many_pipeline_equals_single_calls():
     assert list(W.sp_w_svd_many([], 2, 1)) == []
     with pytest.raises(ValueError):
         list(W.sp_w_svd_many(small, 2, 1, depth=0))
+
+
+def test_status_readback_bypasses_the_copy_engine_and_matches():
+    """wt_readback_i32 (K4's info vector into page-locked memory by a kernel, not a copy-engine
+    copy): values, counts on both sides of the block size, and the LinAlgError mapping of
+    raise_if_failed (decomposition.py:66) while another stream keeps the D2H engine busy."""
+    from paper_2601_08228_b200 import _native as N
+
+    lib = N.require_gpu()
+    for n in (1, 2, 31, 32, 255, 256, 257, 5000):
+        src = torch.arange(n, dtype=torch.int32, device="cuda") * 3 - 7
+        dst = torch.full((n + 3,), -99, dtype=torch.int32).pin_memory()
+        N.check(lib.wt_readback_i32(src.data_ptr(), dst.data_ptr(), n, torch.cuda.current_stream().cuda_stream), "readback")
+        assert torch.equal(dst[:n], src.cpu()) and bool((dst[n:] == -99).all())
+    N.check(lib.wt_readback_i32(0, 0, 0, torch.cuda.current_stream().cuda_stream), "readback")
+    big_d = torch.empty(64 << 20, dtype=torch.float64, device="cuda")
+    big_h = torch.empty(64 << 20, dtype=torch.float64).pin_memory()
+    side = torch.cuda.Stream()
+    with torch.cuda.stream(side):
+        for _ in range(4):
+            big_h.copy_(big_d, non_blocking=True)
+    ok = torch.zeros(40, dtype=torch.int32, device="cuda")
+    E.raise_if_failed(ok)
+    bad = ok.clone()
+    bad[17] = 2
+    with pytest.raises(np.linalg.LinAlgError, match="SVD did not converge"):
+        E.raise_if_failed(bad)
+    side.synchronize()
