@@ -1008,8 +1008,8 @@ Layout layout(int64_t n, int64_t batch) {
   L.tau = take(sizeof(double) * (size_t)(batch * n));
   L.lam = take(sizeof(double) * (size_t)(batch * n));
   L.info = take(sizeof(double) * (size_t)(batch * 4));
-  L.S = take(sizeof(double) * (size_t)(batch * NBT * NBT));
-  L.T = take(sizeof(double) * (size_t)(batch * NBT * NBT));
+  L.S = take(sizeof(double) * (size_t)(2 * batch * NBT * NBT));  // two of each: the two-stage back-transformation
+  L.T = take(sizeof(double) * (size_t)(2 * batch * NBT * NBT));  // forms block i+1's factor under block i's GEMMs
   L.M1 = take(sizeof(double) * (size_t)(batch * NBT * n));
   L.M2 = take(sizeof(double) * (size_t)(batch * NBT * n));
   L.delta = take(sizeof(unsigned long long) * (size_t)batch);
@@ -1397,34 +1397,84 @@ int eig_precondition(const double* Xt, double* Yt, int64_t m, int64_t n, int64_t
   // (128-reflector blocks halve the passes over Z for n >= 512; 64 measured
   // faster on 256^2 slices: config 3 back-transform 1.02 vs 1.43 ms)
   const int64_t nbt = sbr ? SB_TB : (n >= 512 ? NBT : 64);  // (two-stage: whole panels per block)
-  for (int64_t k0 = ((nref - 1) / nbt) * nbt; k0 >= 0; k0 -= nbt) {
+  const size_t tsm = sizeof(double) * NBT * (NBT + 1);
+  if (int r = ensure_smem(wy_larft, tsm)) return r;
+  if (sbr) {
+    if (int r = ensure_smem(sbr_larft_merge, tsm)) return r;
+  }
+  // Two-stage path: the blocks' factors (S = Y^T Y, merged T) do not depend on Z, and the chain of
+  // small launches is latency-bound, so they are formed on a side stream one block ahead of the
+  // three Z-dependent GEMMs (two S / T buffers, events both ways).  Same kernels and arguments as
+  // the in-order chain: same bits.
+  const bool ahead = sbr && option(WT_OPT_EIG_SPLIT) != 1 && !prof;
+  cudaStream_t fs = ahead ? side_stream(kSideStreams - 1) : st;
+  WT_REQUIRE(!ahead || fs != nullptr, "eig: side stream creation failed");
+  constexpr int kMaxBlk = 64;
+  cudaEvent_t ready[kMaxBlk] = {}, freed[kMaxBlk] = {};
+  const int64_t k_first = ((nref - 1) / nbt) * nbt;
+  const int nblk = (int)(k_first / nbt) + 1;
+  WT_REQUIRE(!ahead || nblk <= kMaxBlk, "eig: %d back-transformation blocks", nblk);
+  const int64_t stS = batch * NBT * NBT;  // one S / T buffer
+  int rc = WT_OK;
+  auto factor = [&](int i, cudaStream_t s2) -> int {  // S and T of block i (k0 = k_first - i nbt) into buffer i % 2
+    const int64_t k0 = k_first - (int64_t)i * nbt, nb = std::min<int64_t>(nbt, nref - k0), r0 = k0 + roff;
+    const double* Y = G + r0 * n + k0;  // rows r0.., columns k0.. (ld n)
+    double *Si = S + (ahead ? (i & 1) * stS : 0), *Ti = T + (ahead ? (i & 1) * stS : 0);
+    if (int r = gemm_f64_lim(1, 0, nb, nb, n - r0, 1.0, Y, n, nn, Y, n, nn, 0.0, Si, NBT, NBT * NBT, batch, nullptr,
+                             glim, s2))
+      return r;
+    if (sbr) {  // the panels' factors merged block by block
+      sbr_larft_merge<<<(unsigned)batch, 512, tsm, s2>>>(Si, sbr_tp, flag, ni, (int)k0, (int)nb, Ti);
+    } else {
+      wy_larft<<<(unsigned)batch, 4 * NBT, tsm, s2>>>(Si, tau, flag, ni, (int)k0, (int)nb, Ti);
+    }
+    return WT_OK;
+  };
+  if (ahead) {
+    cudaEvent_t fork = nullptr;
+    if (cudaEventCreateWithFlags(&fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventRecord(fork, st) != cudaSuccess || cudaStreamWaitEvent(fs, fork, 0) != cudaSuccess)
+      rc = WT_ERR_CUDA;
+    if (fork) cudaEventDestroy(fork);
+    for (int i = 0; i < nblk && !rc; ++i)
+      if (cudaEventCreateWithFlags(&ready[i], cudaEventDisableTiming) != cudaSuccess ||
+          cudaEventCreateWithFlags(&freed[i], cudaEventDisableTiming) != cudaSuccess)
+        rc = WT_ERR_CUDA;
+    for (int i = 0; i < 2 && i < nblk && !rc; ++i) {  // the first two factors
+      rc = factor(i, fs);
+      if (!rc && cudaEventRecord(ready[i], fs) != cudaSuccess) rc = WT_ERR_CUDA;
+    }
+  }
+  for (int i = 0; i < nblk && !rc; ++i) {
+    const int64_t k0 = k_first - (int64_t)i * nbt;
     const int64_t nb = std::min<int64_t>(nbt, nref - k0);
     const int64_t r0 = k0 + roff;  // first nonzero row of the block
-    const double* Y = G + r0 * n + k0;  // rows r0.., columns k0.. (ld n)
-    // S = Y^T Y
-    if (int r = gemm_f64_lim(1, 0, nb, nb, n - r0, 1.0, Y, n, nn, Y, n, nn, 0.0, S, NBT, NBT * NBT, batch, nullptr,
-                             glim, st))
-      return r;
-    const size_t tsm = sizeof(double) * NBT * (NBT + 1);
-    if (int r = ensure_smem(wy_larft, tsm)) return r;
-    if (sbr) {  // the panels' factors merged block by block
-      if (int r = ensure_smem(sbr_larft_merge, tsm)) return r;
-      const double* Tpanels = sbr_tp;
-      sbr_larft_merge<<<(unsigned)batch, 512, tsm, st>>>(S, Tpanels, flag, ni, (int)k0, (int)nb, T);
-    } else {
-      wy_larft<<<(unsigned)batch, 4 * NBT, tsm, st>>>(S, tau, flag, ni, (int)k0, (int)nb, T);
-    }
+    const double* Y = G + r0 * n + k0;
+    const double* Ti = T + (ahead ? (i & 1) * stS : 0);
+    if (!ahead) rc = factor(i, st);
     // M1 = Y^T Z (nb x n), M2 = T M1, Z[r0:, :] -= Y M2
-    if (int r = gemm_f64_lim(1, 0, nb, kk, n - r0, 1.0, Y, n, nn, Z + r0 * kk, kk, nk, 0.0, M1, kk, NBT * n, batch,
-                             nullptr, glim, st))
-      return r;
-    if (int r = gemm_f64_lim(0, 0, nb, kk, nb, 1.0, T, NBT, NBT * NBT, M1, kk, NBT * n, 0.0, M2, kk, NBT * n, batch,
-                             nullptr, glim, st))
-      return r;
-    if (int r = gemm_f64_lim(0, 0, n - r0, kk, nb, -1.0, Y, n, nn, M2, kk, NBT * n, 1.0, Z + r0 * kk, kk, nk, batch,
-                             nullptr, glim, st))
-      return r;
+    if (!rc)
+      rc = gemm_f64_lim(1, 0, nb, kk, n - r0, 1.0, Y, n, nn, Z + r0 * kk, kk, nk, 0.0, M1, kk, NBT * n, batch, nullptr,
+                        glim, st);
+    if (!rc && ahead && cudaStreamWaitEvent(st, ready[i], 0) != cudaSuccess) rc = WT_ERR_CUDA;
+    if (!rc)
+      rc = gemm_f64_lim(0, 0, nb, kk, nb, 1.0, Ti, NBT, NBT * NBT, M1, kk, NBT * n, 0.0, M2, kk, NBT * n, batch, nullptr,
+                        glim, st);
+    if (!rc && ahead && i + 2 < nblk) {  // buffer i % 2 is free: block i + 2's factor goes there
+      if (cudaEventRecord(freed[i], st) != cudaSuccess || cudaStreamWaitEvent(fs, freed[i], 0) != cudaSuccess)
+        rc = WT_ERR_CUDA;
+      if (!rc) rc = factor(i + 2, fs);
+      if (!rc && cudaEventRecord(ready[i + 2], fs) != cudaSuccess) rc = WT_ERR_CUDA;
+    }
+    if (!rc)
+      rc = gemm_f64_lim(0, 0, n - r0, kk, nb, -1.0, Y, n, nn, M2, kk, NBT * n, 1.0, Z + r0 * kk, kk, nk, batch, nullptr,
+                        glim, st);
   }
+  for (int i = 0; i < kMaxBlk; ++i) {
+    if (ready[i]) cudaEventDestroy(ready[i]);
+    if (freed[i]) cudaEventDestroy(freed[i]);
+  }
+  if (rc) return rc;
   {
     dim3 grid((unsigned)std::min<int64_t>((nk + 255) / 256, 256), (unsigned)batch);
     set_identity<<<grid, 256, 0, st>>>(Z, ni, ki, flag);
