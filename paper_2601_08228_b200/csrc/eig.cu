@@ -1402,11 +1402,11 @@ int eig_precondition(const double* Xt, double* Yt, int64_t m, int64_t n, int64_t
   if (sbr) {
     if (int r = ensure_smem(sbr_larft_merge, tsm)) return r;
   }
-  // Two-stage path: the blocks' factors (S = Y^T Y, merged T) do not depend on Z, and the chain of
+  // The blocks' factors (S = Y^T Y and the larft / merged T) do not depend on Z, and the chain of
   // small launches is latency-bound, so they are formed on a side stream one block ahead of the
   // three Z-dependent GEMMs (two S / T buffers, events both ways).  Same kernels and arguments as
-  // the in-order chain: same bits.
-  const bool ahead = sbr && option(WT_OPT_EIG_SPLIT) != 1 && !prof;
+  // the in-order chain: same bits.  (WT_OPT_EIG_SPLIT = 1 keeps everything on the caller's stream.)
+  const bool ahead = option(WT_OPT_EIG_SPLIT) != 1 && !prof && nref > nbt;
   cudaStream_t fs = ahead ? side_stream(kSideStreams - 1) : st;
   WT_REQUIRE(!ahead || fs != nullptr, "eig: side stream creation failed");
   constexpr int kMaxBlk = 64;
