@@ -364,6 +364,9 @@ def host_lift(src, n1: int, n2: int, p: int, levels: int, forward: bool) -> torc
     return out
 
 
+_download_lock = threading.Lock()
+
+
 def host_slices_pipeline(src: np.ndarray, levels: int, mask: int, base: int, decompose,
                          out_rows: int, out_cols: int) -> np.ndarray:
     """Host cube in, host cube out, with the PCIe traffic overlapped with K1 / K2.
@@ -389,15 +392,19 @@ def host_slices_pipeline(src: np.ndarray, levels: int, mask: int, base: int, dec
     for st in (s_in, s_cmp, s_out):
         st.wait_stream(main)
 
-    def tables(buf, rows_total, cols, chunks):
-        base_ptr = buf.data_ptr()
-        t = np.empty((len(chunks), K), dtype=np.int64)
-        for c, (r0, _) in enumerate(chunks):
-            t[c] = base_ptr + (np.arange(K, dtype=np.int64) * rows_total + r0) * cols * 8
-        return torch.from_numpy(t).to(dev)
+    def tables(buf, rows_total, cols, rows_per_chunk, chunks):
+        # (len(chunks), K) row-block addresses, computed ON the device (chunk c starts at row
+        # c * rows_per_chunk): a pageable H2D copy of the table would queue on the upload copy
+        # engine behind the bulk chunks of other calls in flight (sp_w_svd_many) -- up to a whole
+        # cube, ~39 ms -- and stall this call's K2 / download.  The consumer stream waits for it.
+        ks = torch.arange(K, dtype=torch.int64, device=dev)[None, :] * rows_total
+        r0s = torch.arange(len(chunks), dtype=torch.int64, device=dev)[:, None] * rows_per_chunk
+        t = (ks + r0s) * (cols * 8) + buf.data_ptr()
+        s_cmp.wait_stream(torch.cuda.current_stream())
+        return t
 
     rows, chunks = _row_chunks(n1, n2 * p)
-    tab_f = tables(slices, n1, n2, chunks)
+    tab_f = tables(slices, n1, n2, rows, chunks)
     direct = is_pinned_array(src)
     cap = rows * n2 * p
     with _stage_lock:
@@ -428,34 +435,40 @@ def host_slices_pipeline(src: np.ndarray, levels: int, mask: int, base: int, dec
                 lift_forward_peer(dx[b][:n].view(r1 - r0, n2, p), levels, tab_f[i], mask, base)
                 free_in[b] = torch.cuda.Event()
                 free_in[b].record(s_cmp)
+        # The lock is kept until this cube has ARRIVED: concurrent calls (sp_w_svd_many) then upload
+        # one after the other at the full PCIe rate instead of chunk by chunk side by side, so the
+        # next call's upload runs under this call's K4 and download (two interleaved uploads end
+        # together, and so do their K4s and downloads: ~61 instead of ~41 ms per config-4 cube).
+        loaded.synchronize()
     main.wait_stream(s_cmp)
     result = decompose(slices)                                  # (K, out_rows, out_cols)
     for st in (s_cmp, s_out):
         st.wait_stream(main)
     orows, ochunks = _row_chunks(out_rows, out_cols * p)
-    tab_i = tables(result, out_rows, out_cols, ochunks)
+    tab_i = tables(result, out_rows, out_cols, orows, ochunks)
     out = host_buffer(out_rows * out_cols * p)
     ocap = orows * out_cols * p
     dy = [torch.empty(ocap, dtype=F64, device=dev) for _ in range(2)]
     free_out = [None, None]
     dl = Download(out)
-    for i, (r0, r1) in enumerate(ochunks):
-        b = i % 2
-        n = (r1 - r0) * out_cols * p
-        with torch.cuda.stream(s_cmp):
-            if free_out[b] is not None:
-                s_cmp.wait_event(free_out[b])
-            lift_inverse_peer(tab_i[i], r1 - r0, out_cols, p, levels, mask, base,
-                              out=dy[b][:n].view(r1 - r0, out_cols, p))
-            done = torch.cuda.Event()
-            done.record(s_cmp)
-        with torch.cuda.stream(s_out):
-            s_out.wait_event(done)
-            dl.put(r0 * out_cols * p, dy[b][:n])
-            free_out[b] = torch.cuda.Event()
-            free_out[b].record(s_out)
-    s_out.synchronize()
-    dl.finish()
+    with _download_lock:  # (one result at a time on the D2H engine, for the same reason)
+        for i, (r0, r1) in enumerate(ochunks):
+            b = i % 2
+            n = (r1 - r0) * out_cols * p
+            with torch.cuda.stream(s_cmp):
+                if free_out[b] is not None:
+                    s_cmp.wait_event(free_out[b])
+                lift_inverse_peer(tab_i[i], r1 - r0, out_cols, p, levels, mask, base,
+                                  out=dy[b][:n].view(r1 - r0, out_cols, p))
+                done = torch.cuda.Event()
+                done.record(s_cmp)
+            with torch.cuda.stream(s_out):
+                s_out.wait_event(done)
+                dl.put(r0 * out_cols * p, dy[b][:n])
+                free_out[b] = torch.cuda.Event()
+                free_out[b].record(s_out)
+        s_out.synchronize()
+        dl.finish()
     main.wait_stream(s_out)
     result.record_stream(s_cmp)
     return hand_out(out).reshape(out_rows, out_cols, p)
