@@ -173,8 +173,8 @@ def sp_w_svd_many(cubes, r, levels, depth: int = 3):
     nothing can be downloaded before the whole cube has arrived).  Over a stream of cubes the
     upload of cube i+1 runs under the K4 and the download of cube i: each call runs on its own
     host thread and CUDA streams, so the two DMA directions and the SMs work at once (three
-    in flight keep both copy engines busy: ~41 ms per config-4 cube against 39 ms for 2 GiB one
-    way, 50 ms with two, 95 ms for single calls).  Results
+    in flight keep both copy engines busy: ~47 ms per config-4 cube in steady state against 39 ms
+    for 2 GiB one way, 95 ms for single calls).  Results
     are yielded in order and are those of the single calls bit for bit (no reference
     counterpart: the reference is one synchronous call per cube, decomposition.py:140-154)."""
     from concurrent.futures import ThreadPoolExecutor
